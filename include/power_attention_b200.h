@@ -1,0 +1,115 @@
+/*
+ * power_attention_b200.h -- C ABI of the B200-native chunked power attention.
+ *
+ * Plain pointers, sizes and a cudaStream_t; no torch types.  Every pointer is
+ * device memory unless stated otherwise.  All entry points are stream-ordered
+ * and asynchronous (no host synchronisation), reentrant, and return 0 on
+ * success or a PA_ERR_* code (message via pa_last_error(), thread-local).
+ *
+ * Tensor layout is the reference's [b, t, h, x] (row-major, contiguous):
+ *   q, k : [b, t, h, d]     v, y : [b, t, h, e]     log_g, rowsum : [b, t, h]
+ * ("e" is the value width, the reference's "v").
+ *
+ * Reference interfaces replaced (file:line under /root/reference/pkg/src/power_attention):
+ *   pa_update_state   <- _core.update_state   _core.pyx:18-43  (dispatch kernels.py:55-83)
+ *   pa_query_state    <- _core.query_state    _core.pyx:46-64  (dispatch kernels.py:86-110)
+ *   pa_discumsum      <- discumsum            chunked.py:156-176
+ *   pa_power_full_fwd <- chunked_power_attention chunked.py:287-413 (attention form when chunk >= t,
+ *                        attention.py:273-309), with log-gates g = exp(log_g)
+ *   pa_power_full_bwd <- vjp_chunked          gradients.py:361-483 (dlog_g = g * dgates)
+ *   pa_feature_dim / pa_feature_table <- expansion_dim / monomial_table expansions.py:87-99, 171-198
+ */
+#ifndef POWER_ATTENTION_B200_H
+#define POWER_ATTENTION_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* pa_stream_t; /* == cudaStream_t */
+
+enum pa_dtype { PA_F32 = 0, PA_BF16 = 1, PA_F16 = 2, PA_F64 = 3 };
+
+enum pa_status {
+  PA_OK = 0,
+  PA_ERR_INVALID_SPEC = 1,   /* -> errors.InvalidSpec          (errors.py:8)  */
+  PA_ERR_SHAPE = 2,          /* -> errors.ShapeMismatch        (errors.py:16) */
+  PA_ERR_CUDA = 3,           /* CUDA launch / runtime failure                  */
+  PA_ERR_UNSUPPORTED = 4,    /* shape/dtype outside what the kernels cover    */
+  PA_ERR_WORKSPACE = 5,      /* workspace smaller than pa_*_workspace_bytes   */
+  PA_ERR_ODD_NORMALIZE = 6   /* -> errors.OddPowerWithNormalize (errors.py:24) */
+};
+
+/* One power_full problem (reference AttentionConfig attention.py:106-171 +
+ * ChunkPlan chunked.py:66-86). */
+typedef struct pa_problem {
+  int32_t b, t, h, d, e; /* batch, tokens, heads, q/k width, value width      */
+  int32_t p;             /* degree of the SPOW_p expansion (1..4)             */
+  int32_t chunk;         /* chunk size c; c >= t selects the attention form   */
+  float scale;           /* sigma; <= 0 means 1/sqrt(d) (attention.py:149)    */
+  int32_t normalize;     /* 1: divide by the score sum (even p only)          */
+  int32_t dtype;         /* pa_dtype of q, k, v, y, dy, dq, dk, dv            */
+  int32_t gated;         /* 1: log_g is read; 0: ungated (log_g ignored)      */
+} pa_problem;
+
+/* D = C(d+p-1, p); -1 on overflow. */
+int64_t pa_feature_dim(int32_t p, int32_t d);
+/* Host buffers: idx [D*p] int32 (NDMI, lexicographic), w [D] double. */
+int pa_feature_table(int32_t p, int32_t d, int32_t* idx, double* w);
+
+/* Bytes of forward workspace.  The forward leaves in it everything the
+ * backward needs; keep it alive between the two calls. */
+size_t pa_fwd_workspace_bytes(const pa_problem* pr);
+size_t pa_bwd_workspace_bytes(const pa_problem* pr);
+
+/* y [b,t,h,e] (dtype), rowsum [b,t,h] fp32 (may be NULL). */
+int pa_power_full_fwd(const pa_problem* pr, const void* q, const void* k, const void* v,
+                      const float* log_g, void* y, float* rowsum, void* ws, size_t ws_bytes,
+                      pa_stream_t stream);
+
+/* Gradients for a cotangent dy on y.  y and rowsum are the forward outputs
+ * (rowsum required when normalize=1).  dlog_g [b,t,h] fp32 (NULL if ungated). */
+int pa_power_full_bwd(const pa_problem* pr, const void* q, const void* k, const void* v,
+                      const float* log_g, const void* y, const float* rowsum, const void* dy,
+                      void* dq, void* dk, void* dv, float* dlog_g, const void* fwd_ws,
+                      void* bwd_ws, size_t bwd_ws_bytes, pa_stream_t stream);
+
+/* Device-side status of the last forward: number of non-positive score sums
+ * seen while normalizing (the reference raises ZeroDenominator,
+ * chunked.py:392-395).  Reads 4 bytes from ws; synchronises the stream. */
+int pa_fwd_zero_denominators(const pa_problem* pr, const void* ws, pa_stream_t stream,
+                             int32_t* count);
+
+/* Reference _core.update_state: state[s] (+)= sum_j w[s,j] phi(k[s,j]) (x) v[s,j],
+ * key_sum[s] (+)= sum_j w[s,j] phi(k[s,j]).  k [n,c,d], v [n,c,e], w [n,c] or
+ * NULL (all ones), state [n,D,e], key_sum [n,D]; all of `dtype` (F32 or F64).
+ * accumulate=0 overwrites, 1 adds (the reference accumulates into zeroed
+ * outputs). */
+int pa_update_state(int32_t n, int32_t c, int32_t d, int32_t e, int32_t p, int32_t dtype,
+                    const void* k, const void* v, const void* w, void* state, void* key_sum,
+                    int32_t accumulate, pa_stream_t stream);
+
+/* Reference _core.query_state: y[s,m] (+)= phi(q[s,m]) . state[s],
+ * denom[s,m] (+)= phi(q[s,m]) . key_sum[s]; q pre-scaled [n,c,d]. */
+int pa_query_state(int32_t n, int32_t c, int32_t d, int32_t e, int32_t p, int32_t dtype,
+                   const void* q, const void* state, const void* key_sum, void* y, void* denom,
+                   int32_t accumulate, pa_stream_t stream);
+
+/* Reference discumsum: out[0] = values[0]; out[k] = lams[k-1, l] * out[k-1, l, m]
+ * + values[k, l, m] with a separate multiply and add (bit-exact with the
+ * sequential loop).  values/out [n, L, M]; lams [n-1, L]; out may alias values. */
+int pa_discumsum(int32_t n, int64_t L, int64_t M, int32_t dtype, const void* values,
+                 const void* lams, void* out, pa_stream_t stream);
+
+const char* pa_last_error(void);
+/* Number of CUDA kernels this library launched since load (for the bench's
+ * gpu_launches claim). */
+int64_t pa_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

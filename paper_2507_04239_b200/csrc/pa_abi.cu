@@ -1,0 +1,329 @@
+// C ABI (include/power_attention_b200.h): validation, workspace carving and
+// the stage order of the forward / backward pipelines.
+#include <math.h>
+
+#include <algorithm>
+#include <atomic>
+#include <string>
+
+#include "../../include/power_attention_b200.h"
+#include "pa_common.cuh"
+#include "pa_simt.cuh"
+#include "pa_tc.cuh"
+
+namespace pa {
+
+static thread_local std::string g_err;
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_err = msg; }
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+int cuda_check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string(what) + ": " + cudaGetErrorString(e));
+    return PA_ERR_CUDA;
+  }
+  return PA_OK;
+}
+
+static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Carves consecutive 256-byte aligned regions out of one workspace buffer.
+struct Carver {
+  char* base;
+  size_t off = 0;
+  explicit Carver(void* b) : base((char*)b) {}
+  template <typename T>
+  T* take(size_t count) {
+    T* p = base ? (T*)(base + off) : nullptr;
+    off += align_up(count * sizeof(T));
+    return p;
+  }
+};
+
+static int make_geo(const pa_problem* pr, Geo* g) {
+  if (!pr) {
+    set_error("null problem");
+    return PA_ERR_INVALID_SPEC;
+  }
+  if (pr->b < 1 || pr->t < 1 || pr->h < 1 || pr->d < 1 || pr->e < 1) {
+    set_error("need b, t, h, d, e >= 1");
+    return PA_ERR_SHAPE;
+  }
+  if (pr->p < 1 || pr->p > 4) {
+    set_error("power degree p must be in [1, 4] on the CUDA path");
+    return PA_ERR_UNSUPPORTED;
+  }
+  if (pr->d > 128 || pr->e > 128) {
+    set_error("d and e must be <= 128 on the CUDA path");
+    return PA_ERR_UNSUPPORTED;
+  }
+  if (pr->chunk < 1) {
+    set_error("chunk_size must be >= 1");
+    return PA_ERR_INVALID_SPEC;
+  }
+  if (pr->normalize && (pr->p % 2)) {
+    set_error("normalization needs positive scores: p must be even");
+    return PA_ERR_ODD_NORMALIZE;
+  }
+  if (pr->dtype < 0 || pr->dtype > 2) {
+    set_error("power_full dtype must be f32, bf16 or f16");
+    return PA_ERR_UNSUPPORTED;
+  }
+  g->b = pr->b;
+  g->t = pr->t;
+  g->h = pr->h;
+  g->d = pr->d;
+  g->e = pr->e;
+  g->E1 = pr->e + 1;
+  g->p = pr->p;
+  g->c = std::min(pr->chunk, pr->t);
+  g->n = (pr->t + g->c - 1) / g->c;
+  int64_t D = host_binom(pr->d + pr->p - 1, pr->p);
+  if (D > (int64_t)1 << 30) {
+    set_error("expanded dimension too large");
+    return PA_ERR_UNSUPPORTED;
+  }
+  g->D = (int)D;
+  g->ns = pr->b * pr->h;
+  g->scale = pr->scale > 0.f ? pr->scale : 1.0f / sqrtf((float)pr->d);
+  g->normalize = pr->normalize ? 1 : 0;
+  g->gated = pr->gated ? 1 : 0;
+  g->bth = 1;
+  return PA_OK;
+}
+
+static SimtWs carve_simt_fwd(const Geo& g, void* ws, size_t* bytes) {
+  Carver c(ws);
+  SimtWs w;
+  w.zflag = c.take<int>(1);
+  w.ell = c.take<float>((size_t)g.ns * g.t);
+  w.lamlog = c.take<float>((size_t)g.ns * g.n);
+  w.idx = c.take<int>((size_t)g.D * g.p);
+  w.wt = c.take<float>(g.D);
+  w.A = c.take<float>((size_t)g.ns * g.n * g.D * g.E1);
+  w.yat = c.take<float>((size_t)g.ns * g.t * g.E1);
+  *bytes = c.off;
+  return w;
+}
+
+static SimtBwdWs carve_simt_bwd(const Geo& g, void* ws, size_t* bytes) {
+  Carver c(ws);
+  SimtBwdWs b;
+  b.dz = c.take<float>((size_t)g.ns * g.t * g.E1);
+  b.dA = c.take<float>((size_t)g.ns * g.n * g.D * g.E1);
+  b.dq32 = c.take<float>((size_t)g.ns * g.t * g.d);
+  b.dk32 = c.take<float>((size_t)g.ns * g.t * g.d);
+  b.dv32 = c.take<float>((size_t)g.ns * g.t * g.e);
+  b.dell = c.take<float>((size_t)g.ns * g.t);
+  b.dellend = c.take<float>((size_t)g.ns * g.n);
+  b.dlam = c.take<float>((size_t)g.ns * g.n);
+  *bytes = c.off;
+  return b;
+}
+
+}  // namespace pa
+
+using namespace pa;
+
+extern "C" {
+
+int64_t pa_feature_dim(int32_t p, int32_t d) {
+  if (p < 1 || d < 1) return -1;
+  return host_binom((int64_t)d + p - 1, p);
+}
+
+int pa_feature_table(int32_t p, int32_t d, int32_t* idx, double* w) {
+  if (p < 1 || p > 4 || d < 1 || !idx || !w) {
+    set_error("feature table needs 1 <= p <= 4, d >= 1 and output buffers");
+    return PA_ERR_INVALID_SPEC;
+  }
+  host_feature_table(p, d, idx, w);
+  return PA_OK;
+}
+
+size_t pa_fwd_workspace_bytes(const pa_problem* pr) {
+  Geo g;
+  if (make_geo(pr, &g)) return 0;
+  if (tc_supported(g, pr->dtype)) return tc_fwd_workspace_bytes(g);
+  size_t n;
+  carve_simt_fwd(g, nullptr, &n);
+  return n;
+}
+
+size_t pa_bwd_workspace_bytes(const pa_problem* pr) {
+  Geo g;
+  if (make_geo(pr, &g)) return 0;
+  if (tc_supported(g, pr->dtype)) return tc_bwd_workspace_bytes(g);
+  size_t n;
+  carve_simt_bwd(g, nullptr, &n);
+  return n;
+}
+
+int pa_power_full_fwd(const pa_problem* pr, const void* q, const void* k, const void* v,
+                      const float* log_g, void* y, float* rowsum, void* ws, size_t ws_bytes,
+                      pa_stream_t stream) {
+  Geo g;
+  if (int rc = make_geo(pr, &g)) return rc;
+  if (!q || !k || !v || !y || !ws || (g.gated && !log_g)) {
+    set_error("null tensor pointer");
+    return PA_ERR_INVALID_SPEC;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (tc_supported(g, pr->dtype)) {
+    if (ws_bytes < tc_fwd_workspace_bytes(g)) {
+      set_error("forward workspace too small");
+      return PA_ERR_WORKSPACE;
+    }
+    return tc_forward(g, q, k, v, log_g, y, rowsum, ws, st);
+  }
+  size_t need;
+  SimtWs w = carve_simt_fwd(g, ws, &need);
+  if (ws_bytes < need) {
+    set_error("forward workspace too small");
+    return PA_ERR_WORKSPACE;
+  }
+  cudaMemsetAsync(w.zflag, 0, sizeof(int), st);
+  if (int rc = simt_build_table(g.p, g.d, g.D, w.idx, w.wt, st)) return rc;
+  return simt_forward(g, pr->dtype, q, k, v, log_g, y, rowsum, w, st);
+}
+
+int pa_power_full_bwd(const pa_problem* pr, const void* q, const void* k, const void* v,
+                      const float* log_g, const void* y, const float* rowsum, const void* dy,
+                      void* dq, void* dk, void* dv, float* dlog_g, const void* fwd_ws, void* bwd_ws,
+                      size_t bwd_ws_bytes, pa_stream_t stream) {
+  Geo g;
+  if (int rc = make_geo(pr, &g)) return rc;
+  if (!q || !k || !v || !y || !dy || !dq || !dk || !dv || !fwd_ws || !bwd_ws ||
+      (g.normalize && !rowsum)) {
+    set_error("null tensor pointer");
+    return PA_ERR_INVALID_SPEC;
+  }
+  if (!g.gated) dlog_g = nullptr;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (tc_supported(g, pr->dtype)) {
+    if (bwd_ws_bytes < tc_bwd_workspace_bytes(g)) {
+      set_error("backward workspace too small");
+      return PA_ERR_WORKSPACE;
+    }
+    return tc_backward(g, q, k, v, log_g, y, rowsum, dy, dq, dk, dv, dlog_g, fwd_ws, bwd_ws, st);
+  }
+  size_t n1, n2;
+  SimtWs w = carve_simt_fwd(g, (void*)fwd_ws, &n1);
+  SimtBwdWs b = carve_simt_bwd(g, bwd_ws, &n2);
+  if (bwd_ws_bytes < n2) {
+    set_error("backward workspace too small");
+    return PA_ERR_WORKSPACE;
+  }
+  return simt_backward(g, pr->dtype, q, k, v, y, rowsum, dy, dq, dk, dv, dlog_g, w, b, st);
+}
+
+int pa_fwd_zero_denominators(const pa_problem* pr, const void* ws, pa_stream_t stream,
+                             int32_t* count) {
+  Geo g;
+  if (int rc = make_geo(pr, &g)) return rc;
+  // both workspace layouts keep the flag in the first 4 bytes
+  cudaError_t e = cudaMemcpyAsync(count, ws, sizeof(int32_t), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    set_error(cudaGetErrorString(e));
+    return PA_ERR_CUDA;
+  }
+  return PA_OK;
+}
+
+static int check_op(int n, int c, int d, int e, int p, int dtype) {
+  if (n < 1 || c < 1 || d < 1 || e < 1) {
+    set_error("need n, c, d, e >= 1");
+    return PA_ERR_SHAPE;
+  }
+  if (p < 1 || p > 4) {
+    set_error("power degree p must be in [1, 4] on the CUDA path");
+    return PA_ERR_UNSUPPORTED;
+  }
+  if (dtype != PA_F32 && dtype != PA_F64) {
+    set_error("per-operator kernels take f32 or f64");
+    return PA_ERR_UNSUPPORTED;
+  }
+  return PA_OK;
+}
+
+// The per-operator entry points keep a tiny cached table per (p, d) on the
+// device: they are reference-compatibility shims, not the hot path.
+static int op_table(int p, int d, int** idx, float** wt, cudaStream_t st) {
+  struct Ent {
+    int p, d, dev;
+    int* idx;
+    float* wt;
+  };
+  static Ent cache[16];
+  static int used = 0;
+  static std::atomic_flag lock = ATOMIC_FLAG_INIT;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  while (lock.test_and_set()) {
+  }
+  for (int i = 0; i < used; ++i)
+    if (cache[i].p == p && cache[i].d == d && cache[i].dev == dev) {
+      *idx = cache[i].idx;
+      *wt = cache[i].wt;
+      lock.clear();
+      return PA_OK;
+    }
+  int D = (int)host_binom(d + p - 1, p);
+  int* di = nullptr;
+  float* dw = nullptr;
+  if (cudaMalloc(&di, sizeof(int) * D * p) != cudaSuccess || cudaMalloc(&dw, sizeof(float) * D) != cudaSuccess) {
+    lock.clear();
+    set_error("cudaMalloc for the feature table failed");
+    return PA_ERR_CUDA;
+  }
+  int rc = simt_build_table(p, d, D, di, dw, st);
+  if (rc == PA_OK && used < 16) cache[used++] = Ent{p, d, dev, di, dw};
+  lock.clear();
+  *idx = di;
+  *wt = dw;
+  return rc;
+}
+
+int pa_update_state(int32_t n, int32_t c, int32_t d, int32_t e, int32_t p, int32_t dtype,
+                    const void* k, const void* v, const void* w, void* state, void* key_sum,
+                    int32_t accumulate, pa_stream_t stream) {
+  if (int rc = check_op(n, c, d, e, p, dtype)) return rc;
+  int* idx;
+  float* wt;
+  if (int rc = op_table(p, d, &idx, &wt, (cudaStream_t)stream)) return rc;
+  int D = (int)host_binom(d + p - 1, p);
+  return pub_update(n, c, d, e, p, D, dtype, k, v, w, idx, wt, state, key_sum, accumulate, (cudaStream_t)stream);
+}
+
+int pa_query_state(int32_t n, int32_t c, int32_t d, int32_t e, int32_t p, int32_t dtype,
+                   const void* q, const void* state, const void* key_sum, void* y, void* denom,
+                   int32_t accumulate, pa_stream_t stream) {
+  if (int rc = check_op(n, c, d, e, p, dtype)) return rc;
+  int* idx;
+  float* wt;
+  if (int rc = op_table(p, d, &idx, &wt, (cudaStream_t)stream)) return rc;
+  int D = (int)host_binom(d + p - 1, p);
+  return pub_query(n, c, d, e, p, D, dtype, q, state, key_sum, idx, y, denom, accumulate, (cudaStream_t)stream);
+}
+
+int pa_discumsum(int32_t n, int64_t L, int64_t M, int32_t dtype, const void* values,
+                 const void* lams, void* out, pa_stream_t stream) {
+  if (n < 1 || L < 1 || M < 1) {
+    set_error("need n, L, M >= 1");
+    return PA_ERR_SHAPE;
+  }
+  if (dtype != PA_F32 && dtype != PA_F64) {
+    set_error("discumsum takes f32 or f64");
+    return PA_ERR_UNSUPPORTED;
+  }
+  return pub_discumsum(n, L, M, dtype, values, lams, out, (cudaStream_t)stream);
+}
+
+const char* pa_last_error(void) { return g_err.c_str(); }
+int64_t pa_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"

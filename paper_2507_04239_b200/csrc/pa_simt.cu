@@ -1,0 +1,999 @@
+// FP32 (CUDA-core) kernels for every stage of chunked power attention, forward
+// and backward, for any SPOW degree p <= 4 and d, e <= 128.
+//
+// These are the full-precision path ("fp32 mode", north star: 1e-4 against
+// the oracle) and the path for shapes the bf16 tensor-core kernels do not
+// specialise.  Each kernel states the reference computation it restates.
+//
+// Internal layouts (all fp32, stream-major):
+//   ell   [ns, t]          inclusive in-chunk cumsum of log g (chunked.py:98-100 in log space)
+//   lamlog[ns, n]          log of the chunk total decay lambda_k (chunked.py:279)
+//   yat   [ns, t, E1]      intra-chunk output, column e = score sum zeta
+//   A     [ns, n, D, E1]   chunk states S_k, then (in place) discumsum A_k; column e = key_sum
+#include <algorithm>
+
+#include "pa_common.cuh"
+#include "pa_simt.cuh"
+
+namespace pa {
+
+// --------------------------------------------------------------------------
+// NDMI table (expansions.py:106-123 order, weights 149-163)
+// --------------------------------------------------------------------------
+__host__ __device__ inline int64_t binom(int64_t n, int64_t k) {
+  if (k < 0 || n < k) return 0;
+  if (k > n - k) k = n - k;
+  int64_t r = 1;
+  for (int64_t i = 1; i <= k; ++i) r = r * (n - k + i) / i;
+  return r;
+}
+
+__host__ __device__ inline void ndmi_unrank(int64_t r, int p, int d, int* out, float* w) {
+  int lo = 0;
+  for (int z = 0; z < p; ++z) {
+    int rem = p - z - 1;
+    for (int a = lo; a < d; ++a) {
+      int64_t cnt = binom(d - a + rem - 1, rem);  // tuples of length rem from [a, d)
+      if (r < cnt) {
+        out[z] = a;
+        lo = a;
+        break;
+      }
+      r -= cnt;
+    }
+  }
+  // sqrt(p! / prod hist!) via run lengths
+  double fact = 1, den = 1;
+  int run = 1;
+  for (int z = 1; z <= p; ++z) fact *= z;
+  for (int z = 1; z < p; ++z) {
+    run = (out[z] == out[z - 1]) ? run + 1 : 1;
+    den *= run;
+  }
+  *w = (float)sqrt(fact / den);
+}
+
+__global__ void k_build_table(int p, int d, int D, int* idx, float* wt) {
+  int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= D) return;
+  int o[4] = {0, 0, 0, 0};
+  float w;
+  ndmi_unrank(f, p, d, o, &w);
+  for (int z = 0; z < p; ++z) idx[f * p + z] = o[z];
+  wt[f] = w;
+}
+
+void host_feature_table(int p, int d, int* idx, double* w) {
+  int64_t D = binom(d + p - 1, p);
+  for (int64_t f = 0; f < D; ++f) {
+    int o[4] = {0, 0, 0, 0};
+    float wf;
+    ndmi_unrank(f, p, d, o, &wf);
+    double fact = 1, den = 1;
+    int run = 1;
+    for (int z = 1; z <= p; ++z) fact *= z;
+    for (int z = 1; z < p; ++z) {
+      run = (o[z] == o[z - 1]) ? run + 1 : 1;
+      den *= run;
+    }
+    for (int z = 0; z < p; ++z) idx[f * p + z] = o[z];
+    w[f] = sqrt(fact / den);
+  }
+}
+
+// phi_f(x) with x in shared memory (row pointer), weight included.
+__device__ __forceinline__ float phi_at(const float* xrow, const int* id, float w, int p) {
+  float r = w * xrow[id[0]];
+  for (int z = 1; z < p; ++z) r *= xrow[id[z]];
+  return r;
+}
+
+// --------------------------------------------------------------------------
+// gate prep: ell = inclusive in-chunk cumsum of log g; lamlog = ell at chunk end
+// --------------------------------------------------------------------------
+__global__ void k_gate_prep(Geo g, const float* __restrict__ log_g, float* ell, float* lamlog) {
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= g.ns * g.n) return;
+  int s = idx / g.n, k = idx - s * g.n;
+  int s0 = k * g.c, s1 = min(s0 + g.c, g.t);
+  float acc = 0.f;
+  for (int m = s0; m < s1; ++m) {
+    float lg = g.gated ? fmaxf(log_g[rowid(g, s, m)], -80.f) : 0.f;
+    acc += lg;
+    ell[(size_t)s * g.t + m] = acc;
+  }
+  lamlog[idx] = acc;
+}
+
+// --------------------------------------------------------------------------
+// intra-chunk forward (attention.py:273-309 / 253-270, normalize=False):
+// yat[i] = sum_{j<=i, same chunk} exp(ell_i - ell_j) (sigma q_i.k_j)^p [v_j, 1]
+// --------------------------------------------------------------------------
+template <typename T, int DM>
+__global__ void __launch_bounds__(64) k_intra_fwd(Geo g, const T* __restrict__ q,
+                                                  const T* __restrict__ k, const T* __restrict__ v,
+                                                  const float* __restrict__ ell, float* yat) {
+  extern __shared__ float sm_dyn[];
+  float* sm_ptr = sm_dyn;
+  float (*Ks)[DM + 1] = reinterpret_cast<float (*)[DM + 1]>(sm_ptr);
+  sm_ptr += (64) * (DM + 1);
+  float (*Vs)[DM + 1] = reinterpret_cast<float (*)[DM + 1]>(sm_ptr);
+  sm_ptr += (64) * (DM + 1);
+  __shared__ float Ls[64];
+  const int tpc = (g.c + 63) / 64;
+  const int kch = blockIdx.x / tpc, tile = blockIdx.x - kch * tpc, s = blockIdx.y;
+  const int s0 = kch * g.c, s1 = min(s0 + g.c, g.t);
+  const int q0 = s0 + tile * 64;
+  if (q0 >= s1) return;
+  const int i = q0 + threadIdx.x;
+  const bool act = i < s1;
+  float qr[DM], o[DM + 1];
+#pragma unroll
+  for (int a = 0; a < DM; ++a) qr[a] = (act && a < g.d) ? g.scale * to_f(q[rowid(g, s, i) * g.d + a]) : 0.f;
+#pragma unroll
+  for (int u = 0; u <= DM; ++u) o[u] = 0.f;
+  const float li = act ? ell[(size_t)s * g.t + i] : 0.f;
+  const int jend = min(q0 + 64, s1);
+  for (int j0 = s0; j0 < jend; j0 += 64) {
+    __syncthreads();
+    {
+      int j = j0 + threadIdx.x;
+      bool ok = j < jend;
+      for (int a = 0; a < DM; ++a) Ks[threadIdx.x][a] = (ok && a < g.d) ? to_f(k[rowid(g, s, j) * g.d + a]) : 0.f;
+      for (int u = 0; u < DM; ++u) Vs[threadIdx.x][u] = (ok && u < g.e) ? to_f(v[rowid(g, s, j) * g.e + u]) : 0.f;
+      Ls[threadIdx.x] = ok ? ell[(size_t)s * g.t + j] : 0.f;
+    }
+    __syncthreads();
+    const int jn = min(64, jend - j0);
+    for (int jj = 0; jj < jn; ++jj) {
+      if (act && j0 + jj <= i) {
+        float sd = 0.f;
+#pragma unroll
+        for (int a = 0; a < DM; ++a) sd += qr[a] * Ks[jj][a];
+        const float P = expf(li - Ls[jj]) * ipow(sd, g.p);
+#pragma unroll
+        for (int u = 0; u < DM; ++u) o[u] += P * Vs[jj][u];
+        o[DM] += P;
+      }
+    }
+  }
+  if (!act) return;
+  float* out = yat + ((size_t)s * g.t + i) * g.E1;
+#pragma unroll
+  for (int u = 0; u < DM; ++u)
+    if (u < g.e) out[u] = o[u];
+  out[g.e] = o[DM];
+}
+
+// --------------------------------------------------------------------------
+// state accumulation (update_state kernels.py:55-83 / _core.pyx:18-43, and
+// the dA half of the query-state VJP gradients.py:429-430):
+//   out[s, kin-koff, f, u] = sum_{j in chunk kin} wt_j phi_f(xs * x_j) vec_j[u]
+// wt mode 0: 1; 1: exp(lamlog_k - ell_j) (suffix decay W_j); 2: exp(ell_j) (prefix gp_j)
+// vec: u < ev from vec rows (type TV, leading dim ldv); u == ev -> 1 if ones
+// --------------------------------------------------------------------------
+template <typename TX, typename TV, int DM>
+__global__ void __launch_bounds__(256) k_state_accum(Geo g, const TX* __restrict__ x, float xs,
+                                                     int wmode, const float* __restrict__ ell,
+                                                     const float* __restrict__ lamlog,
+                                                     const TV* __restrict__ vec, int vec_bth, int ldv,
+                                                     int ev, int ones, const int* __restrict__ idx,
+                                                     const float* __restrict__ wt, int kfirst,
+                                                     int koff, float* out) {
+  constexpr int UM = (DM + 1 + 7) / 8;
+  __shared__ float Xs[32][DM + 1];
+  __shared__ float Us[32][DM + 2];
+  const int fl = threadIdx.x & 31, ug = threadIdx.x >> 5;
+  const int f = blockIdx.x * 32 + fl;
+  const int kin = kfirst + blockIdx.y, s = blockIdx.z;
+  const int s0 = kin * g.c, s1 = min(s0 + g.c, g.t);
+  const int ncol = ev + (ones ? 1 : 0);
+  int id[4] = {0, 0, 0, 0};
+  float w = 0.f;
+  if (f < g.D) {
+    for (int z = 0; z < g.p; ++z) id[z] = idx[f * g.p + z];
+    w = wt[f];
+  }
+  const float lend = (wmode == 1) ? lamlog[s * g.n + kin] : 0.f;
+  float acc[UM];
+#pragma unroll
+  for (int i = 0; i < UM; ++i) acc[i] = 0.f;
+  Geo gv = g;
+  gv.bth = vec_bth;
+  for (int j0 = s0; j0 < s1; j0 += 32) {
+    __syncthreads();
+    for (int el = threadIdx.x; el < 32 * (DM + 1); el += 256) {
+      int r = el / (DM + 1), a = el - r * (DM + 1);
+      int j = j0 + r;
+      bool ok = j < s1;
+      float wj = 1.f;
+      if (ok && wmode) {
+        float lj = ell[(size_t)s * g.t + j];
+        wj = (wmode == 1) ? expf(lend - lj) : expf(lj);
+      }
+      Xs[r][a] = (ok && a < g.d) ? xs * to_f(x[rowid(g, s, j) * g.d + a]) : 0.f;
+      float uv = 0.f;
+      if (ok && a < ev) uv = to_f(vec[rowid(gv, s, j) * ldv + a]);
+      else if (ok && a == ev && ones) uv = 1.f;
+      Us[r][a] = uv * wj;
+    }
+    __syncthreads();
+    const int jn = min(32, s1 - j0);
+    if (f < g.D) {
+      for (int jj = 0; jj < jn; ++jj) {
+        const float ph = phi_at(Xs[jj], id, w, g.p);
+#pragma unroll
+        for (int i = 0; i < UM; ++i) {
+          int u = ug + 8 * i;
+          if (u < ncol) acc[i] += ph * Us[jj][u];
+        }
+      }
+    }
+  }
+  if (f >= g.D) return;
+  float* o = out + (((size_t)s * g.n + (kin - koff)) * g.D + f) * g.E1;
+#pragma unroll
+  for (int i = 0; i < UM; ++i) {
+    int u = ug + 8 * i;
+    if (u < ncol) o[u] = acc[i];
+  }
+}
+
+// --------------------------------------------------------------------------
+// discumsum over chunk states (chunked.py:156-176, call 356-367), in place:
+//   A[s,k] = lambda_k * A[s,k-1] + A[s,k]   (separate mul and add)
+// --------------------------------------------------------------------------
+__global__ void k_discumsum_states(Geo g, const float* __restrict__ lamlog, float* A) {
+  const size_t per = (size_t)g.D * g.E1;
+  const int s = blockIdx.y;
+  for (size_t m = blockIdx.x * (size_t)blockDim.x + threadIdx.x; m < per; m += (size_t)gridDim.x * blockDim.x) {
+    float* p = A + (size_t)s * g.n * per + m;
+    float prev = p[0];
+    for (int k = 1; k < g.n; ++k) {
+      const float lam = g.gated ? expf(lamlog[s * g.n + k]) : 1.f;
+      prev = __fadd_rn(__fmul_rn(lam, prev), p[(size_t)k * per]);
+      p[(size_t)k * per] = prev;
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// query-state + combine + normalize (kernels.py:86-110, chunked.py:372-395):
+//   y_i = yat_i + gp_i phi(sigma q_i)^T A_{k-1};  optional y /= rowsum
+// --------------------------------------------------------------------------
+template <typename T, int DM>
+__global__ void __launch_bounds__(64) k_query_combine(Geo g, const T* __restrict__ q,
+                                                      const float* __restrict__ A,
+                                                      const int* __restrict__ idx,
+                                                      const float* __restrict__ wt,
+                                                      const float* __restrict__ ell,
+                                                      const float* __restrict__ yat, T* y,
+                                                      float* rowsum, int* zflag) {
+  extern __shared__ float sm_dyn[];
+  float* sm_ptr = sm_dyn;
+  float (*Qs)[DM + 1] = reinterpret_cast<float (*)[DM + 1]>(sm_ptr);
+  sm_ptr += (64) * (DM + 1);
+  float (*As)[DM + 2] = reinterpret_cast<float (*)[DM + 2]>(sm_ptr);
+  sm_ptr += (32) * (DM + 2);
+  __shared__ int Is[32][4];
+  __shared__ float Ws[32];
+  const int tpc = (g.c + 63) / 64;
+  const int kch = blockIdx.x / tpc, tile = blockIdx.x - kch * tpc, s = blockIdx.y;
+  const int s0 = kch * g.c, s1 = min(s0 + g.c, g.t);
+  const int q0 = s0 + tile * 64;
+  if (q0 >= s1) return;
+  const int i = q0 + threadIdx.x;
+  const bool act = i < s1;
+  for (int a = 0; a < DM; ++a) Qs[threadIdx.x][a] = (act && a < g.d) ? g.scale * to_f(q[rowid(g, s, i) * g.d + a]) : 0.f;
+  float acc[DM + 1];
+#pragma unroll
+  for (int u = 0; u <= DM; ++u) acc[u] = 0.f;
+  if (kch >= 1) {
+    const float* Ak = A + ((size_t)s * g.n + (kch - 1)) * g.D * g.E1;
+    for (int f0 = 0; f0 < g.D; f0 += 32) {
+      __syncthreads();
+      for (int el = threadIdx.x; el < 32 * g.E1; el += 64) {
+        int r = el / g.E1, u = el - r * g.E1;
+        As[r][u] = (f0 + r < g.D) ? Ak[(size_t)(f0 + r) * g.E1 + u] : 0.f;
+      }
+      if (threadIdx.x < 32) {
+        int f = f0 + threadIdx.x;
+        for (int z = 0; z < 4; ++z) Is[threadIdx.x][z] = (f < g.D && z < g.p) ? idx[f * g.p + z] : 0;
+        Ws[threadIdx.x] = f < g.D ? wt[f] : 0.f;
+      }
+      __syncthreads();
+      const int fn = min(32, g.D - f0);
+      for (int fl = 0; fl < fn; ++fl) {
+        const float ph = phi_at(Qs[threadIdx.x], Is[fl], Ws[fl], g.p);
+#pragma unroll
+        for (int u = 0; u < DM; ++u) acc[u] += ph * As[fl][u];
+        acc[DM] += ph * As[fl][g.e];
+      }
+    }
+  }
+  if (!act) return;
+  const float gp = g.gated ? expf(ell[(size_t)s * g.t + i]) : 1.f;
+  const float* ya = yat + ((size_t)s * g.t + i) * g.E1;
+  const float R = ya[g.e] + gp * acc[DM];
+  const size_t r = rowid(g, s, i);
+  if (rowsum) rowsum[r] = R;
+  float inv = 1.f;
+  if (g.normalize) {
+    if (!(R > 0.f)) atomicAdd(zflag, 1);
+    inv = 1.f / R;
+  }
+#pragma unroll
+  for (int u = 0; u < DM; ++u)
+    if (u < g.e) y[r * g.e + u] = from_f<T>((ya[u] + gp * acc[u]) * inv);
+}
+
+// --------------------------------------------------------------------------
+// backward prep: dz = [dnum, dden] (gradients.py:381-386)
+// --------------------------------------------------------------------------
+template <typename T>
+__global__ void k_bwd_prep(Geo g, const T* __restrict__ dy, const T* __restrict__ y,
+                           const float* __restrict__ rowsum, float* dz) {
+  const size_t n = (size_t)g.ns * g.t;
+  for (size_t it = blockIdx.x * (size_t)blockDim.x + threadIdx.x; it < n; it += (size_t)gridDim.x * blockDim.x) {
+    const int s = (int)(it / g.t), m = (int)(it - (size_t)s * g.t);
+    const size_t r = rowid(g, s, m);
+    float* o = dz + it * g.E1;
+    if (g.normalize) {
+      const float R = rowsum[r];
+      float dot = 0.f;
+      for (int u = 0; u < g.e; ++u) {
+        const float dyu = to_f(dy[r * g.e + u]);
+        dot += dyu * to_f(y[r * g.e + u]);
+        o[u] = dyu / R;
+      }
+      o[g.e] = -dot / R;
+    } else {
+      for (int u = 0; u < g.e; ++u) o[u] = to_f(dy[r * g.e + u]);
+      o[g.e] = 0.f;
+    }
+  }
+}
+
+// accumulate d phi_f into dx (expand_vjp, gradients.py:46-76) -- shared row
+__device__ __forceinline__ void phi_vjp_add(const float* xrow, float* dxrow, const int* id, float gw,
+                                            int p) {
+  if (p == 1) {
+    dxrow[id[0]] += gw;
+    return;
+  }
+  for (int z = 0; z < p; ++z) {
+    float pr = gw;
+    for (int z2 = 0; z2 < p; ++z2)
+      if (z2 != z) pr *= xrow[id[z2]];
+    dxrow[id[z]] += pr;
+  }
+}
+
+// --------------------------------------------------------------------------
+// query-state backward, token side (gradients.py:406-431):
+//   t_f = A_{k-1}[f,:] . dz_i ; dq_i += sigma * expand_vjp(sigma q_i, gp_i t)
+//   dell_i += gp_i * sum_f phi_f(sigma q_i) t_f      (gate prefix, 260-264)
+// --------------------------------------------------------------------------
+template <typename T, int DM>
+__global__ void __launch_bounds__(64) k_query_bwd(Geo g, const T* __restrict__ q,
+                                                  const float* __restrict__ A,
+                                                  const int* __restrict__ idx,
+                                                  const float* __restrict__ wt,
+                                                  const float* __restrict__ ell,
+                                                  const float* __restrict__ dz, float* dq32,
+                                                  float* dell) {
+  extern __shared__ float sm_dyn[];
+  float* sm_ptr = sm_dyn;
+  float (*Qs)[DM + 1] = reinterpret_cast<float (*)[DM + 1]>(sm_ptr);
+  sm_ptr += (64) * (DM + 1);
+  float (*Dq)[DM + 1] = reinterpret_cast<float (*)[DM + 1]>(sm_ptr);
+  sm_ptr += (64) * (DM + 1);
+  float (*As)[DM + 2] = reinterpret_cast<float (*)[DM + 2]>(sm_ptr);
+  sm_ptr += (32) * (DM + 2);
+  __shared__ int Is[32][4];
+  __shared__ float Ws[32];
+  const int tpc = (g.c + 63) / 64;
+  const int kch = 1 + blockIdx.x / tpc, tile = blockIdx.x % tpc, s = blockIdx.y;
+  const int s0 = kch * g.c, s1 = min(s0 + g.c, g.t);
+  const int q0 = s0 + tile * 64;
+  if (q0 >= s1) return;
+  const int i = q0 + threadIdx.x;
+  const bool act = i < s1;
+  for (int a = 0; a <= DM; ++a) {
+    Qs[threadIdx.x][a] = (act && a < g.d) ? g.scale * to_f(q[rowid(g, s, i) * g.d + a]) : 0.f;
+    Dq[threadIdx.x][a] = 0.f;
+  }
+  float dzr[DM + 1];
+#pragma unroll
+  for (int u = 0; u <= DM; ++u) dzr[u] = 0.f;
+  if (act) {
+    const float* dzi = dz + ((size_t)s * g.t + i) * g.E1;
+#pragma unroll
+    for (int u = 0; u < DM; ++u)
+      if (u < g.e) dzr[u] = dzi[u];
+    dzr[DM] = dzi[g.e];
+  }
+  const float gp = (act && g.gated) ? expf(ell[(size_t)s * g.t + i]) : 1.f;
+  float dl = 0.f;
+  const float* Ak = A + ((size_t)s * g.n + (kch - 1)) * g.D * g.E1;
+  for (int f0 = 0; f0 < g.D; f0 += 32) {
+    __syncthreads();
+    for (int el = threadIdx.x; el < 32 * g.E1; el += 64) {
+      int r = el / g.E1, u = el - r * g.E1;
+      As[r][u] = (f0 + r < g.D) ? Ak[(size_t)(f0 + r) * g.E1 + u] : 0.f;
+    }
+    if (threadIdx.x < 32) {
+      int f = f0 + threadIdx.x;
+      for (int z = 0; z < 4; ++z) Is[threadIdx.x][z] = (f < g.D && z < g.p) ? idx[f * g.p + z] : 0;
+      Ws[threadIdx.x] = f < g.D ? wt[f] : 0.f;
+    }
+    __syncthreads();
+    const int fn = min(32, g.D - f0);
+    for (int fl = 0; fl < fn; ++fl) {
+      float tf = 0.f;
+#pragma unroll
+      for (int u = 0; u < DM; ++u) tf += As[fl][u] * dzr[u];
+      tf += As[fl][g.e] * dzr[DM];
+      const float ph = phi_at(Qs[threadIdx.x], Is[fl], Ws[fl], g.p);
+      dl += ph * tf;
+      phi_vjp_add(Qs[threadIdx.x], Dq[threadIdx.x], Is[fl], Ws[fl] * gp * tf, g.p);
+    }
+  }
+  if (!act) return;
+  float* o = dq32 + ((size_t)s * g.t + i) * g.d;
+  for (int a = 0; a < g.d; ++a) o[a] += g.scale * Dq[threadIdx.x][a];
+  dell[(size_t)s * g.t + i] += gp * dl;
+}
+
+// --------------------------------------------------------------------------
+// discumsum backward in place (gradients.py:267-288) + d lambda reduction:
+//   dS_k = dA_k + lambda_{k+1} dS_{k+1};  dlam_{k+1} += <A_k, dS_{k+1}>
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_discumsum_bwd(Geo g, const float* __restrict__ lamlog,
+                                                       const float* __restrict__ A, float* dA,
+                                                       float* dlam) {
+  __shared__ float red[32];
+  const size_t per = (size_t)g.D * g.E1;
+  const int s = blockIdx.y;
+  const size_t m = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  const bool ok = m < per;
+  const float* Ap = A + (size_t)s * g.n * per + m;
+  float* dp = dA + (size_t)s * g.n * per + m;
+  float acc = ok ? dp[(size_t)(g.n - 1) * per] : 0.f;
+  for (int k = g.n - 2; k >= 0; --k) {
+    const float part = ok ? Ap[(size_t)k * per] * acc : 0.f;
+    const float tot = block_sum(part, red);
+    if (threadIdx.x == 0) atomicAdd(dlam + s * g.n + k + 1, tot);
+    const float lam = g.gated ? expf(lamlog[s * g.n + k + 1]) : 1.f;
+    if (ok) {
+      acc = dp[(size_t)k * per] + lam * acc;
+      dp[(size_t)k * per] = acc;
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// update-state backward, token side (gradients.py:191-213, 245-257):
+//   t_f = dS_k[f,:] . [v_j,1];  dk_j += expand_vjp(k_j, W_j t);  dv_j += W_j phi(k_j)^T dS_k
+//   dW_j = phi(k_j).t  ->  dell_j -= W_j dW_j,  dell_end(k) += W_j dW_j
+// --------------------------------------------------------------------------
+template <typename T, int DM>
+__global__ void __launch_bounds__(64) k_update_bwd(Geo g, const T* __restrict__ k,
+                                                   const T* __restrict__ v,
+                                                   const float* __restrict__ dS,
+                                                   const int* __restrict__ idx,
+                                                   const float* __restrict__ wt,
+                                                   const float* __restrict__ ell,
+                                                   const float* __restrict__ lamlog, float* dk32,
+                                                   float* dv32, float* dell, float* dellend) {
+  extern __shared__ float sm_dyn[];
+  float* sm_ptr = sm_dyn;
+  float (*Ks)[DM + 1] = reinterpret_cast<float (*)[DM + 1]>(sm_ptr);
+  sm_ptr += (64) * (DM + 1);
+  float (*Dk)[DM + 1] = reinterpret_cast<float (*)[DM + 1]>(sm_ptr);
+  sm_ptr += (64) * (DM + 1);
+  float (*Ss)[DM + 2] = reinterpret_cast<float (*)[DM + 2]>(sm_ptr);
+  sm_ptr += (32) * (DM + 2);
+  __shared__ int Is[32][4];
+  __shared__ float Ws[32];
+  __shared__ float red[32];
+  const int tpc = (g.c + 63) / 64;
+  const int kch = blockIdx.x / tpc, tile = blockIdx.x % tpc, s = blockIdx.y;
+  const int s0 = kch * g.c, s1 = min(s0 + g.c, g.t);
+  const int q0 = s0 + tile * 64;
+  if (q0 >= s1) return;
+  const int j = q0 + threadIdx.x;
+  const bool act = j < s1;
+  for (int a = 0; a <= DM; ++a) {
+    Ks[threadIdx.x][a] = (act && a < g.d) ? to_f(k[rowid(g, s, j) * g.d + a]) : 0.f;
+    Dk[threadIdx.x][a] = 0.f;
+  }
+  float vr[DM + 1], dvr[DM];
+#pragma unroll
+  for (int u = 0; u < DM; ++u) {
+    vr[u] = (act && u < g.e) ? to_f(v[rowid(g, s, j) * g.e + u]) : 0.f;
+    dvr[u] = 0.f;
+  }
+  vr[DM] = 1.f;
+  const float W = (act && g.gated) ? expf(lamlog[s * g.n + kch] - ell[(size_t)s * g.t + j]) : 1.f;
+  float dW = 0.f;
+  const float* Sk = dS + ((size_t)s * g.n + kch) * g.D * g.E1;
+  for (int f0 = 0; f0 < g.D; f0 += 32) {
+    __syncthreads();
+    for (int el = threadIdx.x; el < 32 * g.E1; el += 64) {
+      int r = el / g.E1, u = el - r * g.E1;
+      Ss[r][u] = (f0 + r < g.D) ? Sk[(size_t)(f0 + r) * g.E1 + u] : 0.f;
+    }
+    if (threadIdx.x < 32) {
+      int f = f0 + threadIdx.x;
+      for (int z = 0; z < 4; ++z) Is[threadIdx.x][z] = (f < g.D && z < g.p) ? idx[f * g.p + z] : 0;
+      Ws[threadIdx.x] = f < g.D ? wt[f] : 0.f;
+    }
+    __syncthreads();
+    const int fn = min(32, g.D - f0);
+    for (int fl = 0; fl < fn; ++fl) {
+      float tf = Ss[fl][g.e];
+#pragma unroll
+      for (int u = 0; u < DM; ++u) tf += Ss[fl][u] * vr[u];
+      const float ph = phi_at(Ks[threadIdx.x], Is[fl], Ws[fl], g.p);
+      dW += ph * tf;
+      phi_vjp_add(Ks[threadIdx.x], Dk[threadIdx.x], Is[fl], Ws[fl] * W * tf, g.p);
+      const float wp = W * ph;
+#pragma unroll
+      for (int u = 0; u < DM; ++u) dvr[u] += wp * Ss[fl][u];
+    }
+  }
+  const float contrib = act ? W * dW : 0.f;
+  const float tot = block_sum(contrib, red);
+  if (threadIdx.x == 0 && g.gated) atomicAdd(dellend + s * g.n + kch, tot);
+  if (!act) return;
+  float* ok_ = dk32 + ((size_t)s * g.t + j) * g.d;
+  for (int a = 0; a < g.d; ++a) ok_[a] += Dk[threadIdx.x][a];
+  float* ov = dv32 + ((size_t)s * g.t + j) * g.e;
+#pragma unroll
+  for (int u = 0; u < DM; ++u)
+    if (u < g.e) ov[u] += dvr[u];
+  dell[(size_t)s * g.t + j] -= contrib;
+}
+
+// --------------------------------------------------------------------------
+// intra-chunk backward (gradients.py:98-176): query side
+//   dP_ij = dnum_i . v_j + dden_i;  ds = dP E p s^(p-1);  dq_i += sigma sum_j ds k_j
+//   dell_i += sum_j dP_ij P_ij   (pairwise-decay rule 79-95 in log space)
+// --------------------------------------------------------------------------
+template <typename T, int DM>
+__global__ void __launch_bounds__(64) k_intra_bwd_q(Geo g, const T* __restrict__ q,
+                                                    const T* __restrict__ k,
+                                                    const T* __restrict__ v,
+                                                    const float* __restrict__ ell,
+                                                    const float* __restrict__ dz, float* dq32,
+                                                    float* dell) {
+  extern __shared__ float sm_dyn[];
+  float* sm_ptr = sm_dyn;
+  float (*Ks)[DM + 1] = reinterpret_cast<float (*)[DM + 1]>(sm_ptr);
+  sm_ptr += (64) * (DM + 1);
+  float (*Vs)[DM + 1] = reinterpret_cast<float (*)[DM + 1]>(sm_ptr);
+  sm_ptr += (64) * (DM + 1);
+  __shared__ float Ls[64];
+  float (*Qr)[DM + 1] = reinterpret_cast<float (*)[DM + 1]>(sm_ptr);
+  sm_ptr += (64) * (DM + 1);
+  float (*Zr)[DM + 2] = reinterpret_cast<float (*)[DM + 2]>(sm_ptr);
+  sm_ptr += (64) * (DM + 2);
+  const int tpc = (g.c + 63) / 64;
+  const int kch = blockIdx.x / tpc, tile = blockIdx.x - kch * tpc, s = blockIdx.y;
+  const int s0 = kch * g.c, s1 = min(s0 + g.c, g.t);
+  const int q0 = s0 + tile * 64;
+  if (q0 >= s1) return;
+  const int i = q0 + threadIdx.x;
+  const bool act = i < s1;
+  for (int a = 0; a < DM; ++a) Qr[threadIdx.x][a] = (act && a < g.d) ? g.scale * to_f(q[rowid(g, s, i) * g.d + a]) : 0.f;
+  for (int u = 0; u <= DM; ++u) {
+    float val = 0.f;
+    if (act && u < g.e) val = dz[((size_t)s * g.t + i) * g.E1 + u];
+    if (act && u == DM) val = dz[((size_t)s * g.t + i) * g.E1 + g.e];
+    Zr[threadIdx.x][u] = val;
+  }
+  float dqa[DM];
+#pragma unroll
+  for (int a = 0; a < DM; ++a) dqa[a] = 0.f;
+  float rowD = 0.f;
+  const float li = act ? ell[(size_t)s * g.t + i] : 0.f;
+  const int jend = min(q0 + 64, s1);
+  for (int j0 = s0; j0 < jend; j0 += 64) {
+    __syncthreads();
+    {
+      int j = j0 + threadIdx.x;
+      bool ok = j < jend;
+      for (int a = 0; a < DM; ++a) Ks[threadIdx.x][a] = (ok && a < g.d) ? to_f(k[rowid(g, s, j) * g.d + a]) : 0.f;
+      for (int u = 0; u < DM; ++u) Vs[threadIdx.x][u] = (ok && u < g.e) ? to_f(v[rowid(g, s, j) * g.e + u]) : 0.f;
+      Ls[threadIdx.x] = ok ? ell[(size_t)s * g.t + j] : 0.f;
+    }
+    __syncthreads();
+    const int jn = min(64, jend - j0);
+    for (int jj = 0; jj < jn; ++jj) {
+      if (act && j0 + jj <= i) {
+        float sd = 0.f;
+        for (int a = 0; a < DM; ++a) sd += Qr[threadIdx.x][a] * Ks[jj][a];
+        float dP = Zr[threadIdx.x][DM];
+        for (int u = 0; u < DM; ++u) dP += Zr[threadIdx.x][u] * Vs[jj][u];
+        const float E = expf(li - Ls[jj]);
+        const float sp1 = ipow(sd, g.p - 1);
+        rowD += dP * E * sp1 * sd;
+        const float ds = dP * E * g.p * sp1;
+#pragma unroll
+        for (int a = 0; a < DM; ++a) dqa[a] += ds * Ks[jj][a];
+      }
+    }
+  }
+  if (!act) return;
+  float* o = dq32 + ((size_t)s * g.t + i) * g.d;
+  for (int a = 0; a < DM; ++a)
+    if (a < g.d) o[a] += g.scale * dqa[a];
+  dell[(size_t)s * g.t + i] += rowD;
+}
+
+// key side: dv_j += sum_i P_ij dnum_i; dk_j += sum_i ds_ij (sigma q_i); dell_j -= sum_i dP_ij P_ij
+template <typename T, int DM>
+__global__ void __launch_bounds__(64) k_intra_bwd_kv(Geo g, const T* __restrict__ q,
+                                                     const T* __restrict__ k,
+                                                     const T* __restrict__ v,
+                                                     const float* __restrict__ ell,
+                                                     const float* __restrict__ dz, float* dk32,
+                                                     float* dv32, float* dell) {
+  extern __shared__ float sm_dyn[];
+  float* sm_ptr = sm_dyn;
+  float (*Qs)[DM + 1] = reinterpret_cast<float (*)[DM + 1]>(sm_ptr);
+  sm_ptr += (64) * (DM + 1);
+  float (*Zs)[DM + 2] = reinterpret_cast<float (*)[DM + 2]>(sm_ptr);
+  sm_ptr += (64) * (DM + 2);
+  __shared__ float Ls[64];
+  float (*Kr)[DM + 1] = reinterpret_cast<float (*)[DM + 1]>(sm_ptr);
+  sm_ptr += (64) * (DM + 1);
+  float (*Vr)[DM + 1] = reinterpret_cast<float (*)[DM + 1]>(sm_ptr);
+  sm_ptr += (64) * (DM + 1);
+  const int tpc = (g.c + 63) / 64;
+  const int kch = blockIdx.x / tpc, tile = blockIdx.x - kch * tpc, s = blockIdx.y;
+  const int s0 = kch * g.c, s1 = min(s0 + g.c, g.t);
+  const int k0 = s0 + tile * 64;
+  if (k0 >= s1) return;
+  const int j = k0 + threadIdx.x;
+  const bool act = j < s1;
+  for (int a = 0; a < DM; ++a) {
+    Kr[threadIdx.x][a] = (act && a < g.d) ? to_f(k[rowid(g, s, j) * g.d + a]) : 0.f;
+    Vr[threadIdx.x][a] = (act && a < g.e) ? to_f(v[rowid(g, s, j) * g.e + a]) : 0.f;
+  }
+  float dka[DM], dva[DM];
+#pragma unroll
+  for (int a = 0; a < DM; ++a) dka[a] = dva[a] = 0.f;
+  float colD = 0.f;
+  const float lj = act ? ell[(size_t)s * g.t + j] : 0.f;
+  for (int i0 = k0; i0 < s1; i0 += 64) {
+    __syncthreads();
+    {
+      int i = i0 + threadIdx.x;
+      bool ok = i < s1;
+      for (int a = 0; a < DM; ++a) Qs[threadIdx.x][a] = (ok && a < g.d) ? g.scale * to_f(q[rowid(g, s, i) * g.d + a]) : 0.f;
+      for (int u = 0; u <= DM; ++u) {
+        float val = 0.f;
+        if (ok && u < g.e) val = dz[((size_t)s * g.t + i) * g.E1 + u];
+        if (ok && u == DM) val = dz[((size_t)s * g.t + i) * g.E1 + g.e];
+        Zs[threadIdx.x][u] = val;
+      }
+      Ls[threadIdx.x] = ok ? ell[(size_t)s * g.t + i] : 0.f;
+    }
+    __syncthreads();
+    const int in = min(64, s1 - i0);
+    for (int ii = 0; ii < in; ++ii) {
+      if (act && i0 + ii >= j) {
+        float sd = 0.f;
+        for (int a = 0; a < DM; ++a) sd += Qs[ii][a] * Kr[threadIdx.x][a];
+        float dP = Zs[ii][DM];
+        for (int u = 0; u < DM; ++u) dP += Zs[ii][u] * Vr[threadIdx.x][u];
+        const float E = expf(Ls[ii] - lj);
+        const float sp1 = ipow(sd, g.p - 1);
+        const float P = E * sp1 * sd;
+        colD += dP * P;
+        const float ds = dP * E * g.p * sp1;
+#pragma unroll
+        for (int a = 0; a < DM; ++a) {
+          dka[a] += ds * Qs[ii][a];
+          dva[a] += P * Zs[ii][a];
+        }
+      }
+    }
+  }
+  if (!act) return;
+  float* ok_ = dk32 + ((size_t)s * g.t + j) * g.d;
+  float* ov = dv32 + ((size_t)s * g.t + j) * g.e;
+  for (int a = 0; a < DM; ++a) {
+    if (a < g.d) ok_[a] += dka[a];
+    if (a < g.e) ov[a] += dva[a];
+  }
+  dell[(size_t)s * g.t + j] -= colD;
+}
+
+// --------------------------------------------------------------------------
+// gate finish: dlog g_u = sum_{m >= u in chunk} dell_m, with the chunk-end
+// cotangents (suffix decay + lambda) folded into the last token.
+// --------------------------------------------------------------------------
+__global__ void k_gate_finish(Geo g, const float* __restrict__ lamlog, const float* __restrict__ dell,
+                              const float* __restrict__ dellend, const float* __restrict__ dlam,
+                              float* dlogg) {
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= g.ns * g.n) return;
+  int s = idx / g.n, kch = idx - s * g.n;
+  int s0 = kch * g.c, s1 = min(s0 + g.c, g.t);
+  float acc = dellend[idx] + (kch >= 1 ? dlam[idx] * expf(lamlog[idx]) : 0.f);
+  for (int m = s1 - 1; m >= s0; --m) {
+    acc += dell[(size_t)s * g.t + m];
+    dlogg[rowid(g, s, m)] = acc;
+  }
+}
+
+template <typename T>
+__global__ void k_finalize(Geo g, const float* __restrict__ src, int w, T* dst) {
+  const size_t n = (size_t)g.ns * g.t * w;
+  for (size_t it = blockIdx.x * (size_t)blockDim.x + threadIdx.x; it < n; it += (size_t)gridDim.x * blockDim.x) {
+    const size_t tok = it / w;
+    const int col = (int)(it - tok * w);
+    const int s = (int)(tok / g.t), m = (int)(tok - (size_t)s * g.t);
+    dst[rowid(g, s, m) * w + col] = from_f<T>(src[it]);
+  }
+}
+
+// --------------------------------------------------------------------------
+// public per-operator kernels (reference kernels.py / _core.pyx), f32 or f64
+// --------------------------------------------------------------------------
+template <typename A>
+__global__ void k_pub_update(int n, int c, int d, int e, int p, int D, const A* __restrict__ k,
+                             const A* __restrict__ v, const A* __restrict__ w,
+                             const int* __restrict__ idx, const float* __restrict__ wt, A* state,
+                             A* key_sum, int accumulate) {
+  const size_t tot = (size_t)n * D * (e + 1);
+  for (size_t it = blockIdx.x * (size_t)blockDim.x + threadIdx.x; it < tot; it += (size_t)gridDim.x * blockDim.x) {
+    const int u = (int)(it % (e + 1));
+    const size_t sf = it / (e + 1);
+    const int f = (int)(sf % D), s = (int)(sf / D);
+    int id[4] = {0, 0, 0, 0};
+    for (int z = 0; z < p; ++z) id[z] = idx[f * p + z];
+    // exact double weight (table is float): recompute from the run lengths
+    double fact = 1, den = 1;
+    int run = 1;
+    for (int z = 1; z <= p; ++z) fact *= z;
+    for (int z = 1; z < p; ++z) {
+      run = (id[z] == id[z - 1]) ? run + 1 : 1;
+      den *= run;
+    }
+    const A wf = (A)sqrt(fact / den);
+    A acc = 0;
+    for (int j = 0; j < c; ++j) {
+      const A* kr = k + ((size_t)s * c + j) * d;
+      A ph = wf * kr[id[0]];
+      for (int z = 1; z < p; ++z) ph *= kr[id[z]];
+      if (w) ph *= w[(size_t)s * c + j];
+      acc += (u < e) ? ph * v[((size_t)s * c + j) * e + u] : ph;
+    }
+    A* o = (u < e) ? state + ((size_t)s * D + f) * e + u : key_sum + (size_t)s * D + f;
+    *o = accumulate ? *o + acc : acc;
+  }
+}
+
+template <typename A>
+__global__ void k_pub_query(int n, int c, int d, int e, int p, int D, const A* __restrict__ q,
+                            const A* __restrict__ state, const A* __restrict__ key_sum,
+                            const int* __restrict__ idx, A* y, A* denom, int accumulate) {
+  const size_t tot = (size_t)n * c * (e + 1);
+  for (size_t it = blockIdx.x * (size_t)blockDim.x + threadIdx.x; it < tot; it += (size_t)gridDim.x * blockDim.x) {
+    const int u = (int)(it % (e + 1));
+    const size_t sm = it / (e + 1);
+    const int m = (int)(sm % c), s = (int)(sm / c);
+    const A* qr = q + ((size_t)s * c + m) * d;
+    A acc = 0;
+    for (int f = 0; f < D; ++f) {
+      int id[4] = {0, 0, 0, 0};
+      for (int z = 0; z < p; ++z) id[z] = idx[f * p + z];
+      double fact = 1, den = 1;
+      int run = 1;
+      for (int z = 1; z <= p; ++z) fact *= z;
+      for (int z = 1; z < p; ++z) {
+        run = (id[z] == id[z - 1]) ? run + 1 : 1;
+        den *= run;
+      }
+      A ph = (A)sqrt(fact / den) * qr[id[0]];
+      for (int z = 1; z < p; ++z) ph *= qr[id[z]];
+      acc += ph * ((u < e) ? state[((size_t)s * D + f) * e + u] : key_sum[(size_t)s * D + f]);
+    }
+    A* o = (u < e) ? y + ((size_t)s * c + m) * e + u : denom + (size_t)s * c + m;
+    *o = accumulate ? *o + acc : acc;
+  }
+}
+
+template <typename A>
+__global__ void k_pub_discumsum(int n, int64_t L, int64_t M, const A* __restrict__ values,
+                                const A* __restrict__ lams, A* out) {
+  const size_t tot = (size_t)L * M;
+  for (size_t it = blockIdx.x * (size_t)blockDim.x + threadIdx.x; it < tot; it += (size_t)gridDim.x * blockDim.x) {
+    const size_t l = it / M;
+    A prev = values[it];
+    out[it] = prev;
+    for (int k = 1; k < n; ++k) {
+      const A lam = lams[(size_t)(k - 1) * L + l];
+      A prod;
+      if constexpr (sizeof(A) == 8) {
+        prod = __dmul_rn(lam, prev);
+        prev = __dadd_rn(prod, values[(size_t)k * tot + it]);
+      } else {
+        prod = __fmul_rn(lam, prev);
+        prev = __fadd_rn(prod, values[(size_t)k * tot + it]);
+      }
+      out[(size_t)k * tot + it] = prev;
+    }
+  }
+}
+
+// ==========================================================================
+// host launchers
+// ==========================================================================
+
+// dynamic shared memory per block for the kernels above (floats -> bytes)
+template <int DM> constexpr size_t smb_intra_fwd() { return 4 * (2 * 64 * (DM + 1)); }
+template <int DM> constexpr size_t smb_query_combine() { return 4 * (64 * (DM + 1) + 32 * (DM + 2)); }
+template <int DM> constexpr size_t smb_query_bwd() { return 4 * (2 * 64 * (DM + 1) + 32 * (DM + 2)); }
+template <int DM> constexpr size_t smb_update_bwd() { return smb_query_bwd<DM>(); }
+template <int DM> constexpr size_t smb_intra_bwd() { return 4 * (3 * 64 * (DM + 1) + 64 * (DM + 2)); }
+
+template <typename K>
+static size_t dyn_smem(K kern, size_t bytes) {
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  return bytes;
+}
+
+static inline unsigned nblk(size_t n, int bs) { return (unsigned)std::min<size_t>((n + bs - 1) / bs, 148 * 32); }
+
+int simt_build_table(int p, int d, int D, int* idx, float* wt, cudaStream_t st) {
+  k_build_table<<<(D + 127) / 128, 128, 0, st>>>(p, d, D, idx, wt);
+  count_launch();
+  return cuda_check("build_table");
+}
+
+template <typename T, int DM>
+static int simt_forward_t(const Geo& g, const T* q, const T* k, const T* v, const float* log_g, T* y,
+                          float* rowsum, const SimtWs& w, cudaStream_t st) {
+  const int tpc = (g.c + 63) / 64;
+  k_gate_prep<<<(g.ns * g.n + 127) / 128, 128, 0, st>>>(g, log_g, w.ell, w.lamlog);
+  k_intra_fwd<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_intra_fwd<T, DM>, smb_intra_fwd<DM>()), st>>>(g, q, k, v, w.ell, w.yat);
+  k_state_accum<T, T, DM><<<dim3((g.D + 31) / 32, g.n, g.ns), 256, 0, st>>>(
+      g, k, 1.f, g.gated ? 1 : 0, w.ell, w.lamlog, v, 1, g.e, g.e, 1, w.idx, w.wt, 0, 0, w.A);
+  if (g.n > 1) k_discumsum_states<<<dim3((unsigned)std::min<size_t>(((size_t)g.D * g.E1 + 255) / 256, 512), g.ns), 256, 0, st>>>(g, w.lamlog, w.A);
+  k_query_combine<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_query_combine<T, DM>, smb_query_combine<DM>()), st>>>(g, q, w.A, w.idx, w.wt, w.ell, w.yat, y, rowsum, w.zflag);
+  count_launch(g.n > 1 ? 5 : 4);
+  return cuda_check("simt forward");
+}
+
+template <typename T, int DM>
+static int simt_backward_t(const Geo& g, const T* q, const T* k, const T* v, const T* y,
+                           const float* rowsum, const T* dy, T* dq, T* dk, T* dv, float* dlogg,
+                           const SimtWs& w, const SimtBwdWs& b, cudaStream_t st) {
+  const int tpc = (g.c + 63) / 64;
+  const size_t per = (size_t)g.D * g.E1;
+  cudaMemsetAsync(b.dA, 0, sizeof(float) * g.ns * g.n * per, st);
+  cudaMemsetAsync(b.dq32, 0, sizeof(float) * g.ns * g.t * g.d, st);
+  cudaMemsetAsync(b.dk32, 0, sizeof(float) * g.ns * g.t * g.d, st);
+  cudaMemsetAsync(b.dv32, 0, sizeof(float) * g.ns * g.t * g.e, st);
+  cudaMemsetAsync(b.dell, 0, sizeof(float) * g.ns * g.t, st);
+  cudaMemsetAsync(b.dellend, 0, sizeof(float) * g.ns * g.n, st);
+  cudaMemsetAsync(b.dlam, 0, sizeof(float) * g.ns * g.n, st);
+  int launches = 0;
+  k_bwd_prep<T><<<nblk((size_t)g.ns * g.t, 256), 256, 0, st>>>(g, dy, y, rowsum, b.dz);
+  ++launches;
+  if (g.n > 1) {
+    k_query_bwd<T, DM><<<dim3((g.n - 1) * tpc, g.ns), 64, dyn_smem(k_query_bwd<T, DM>, smb_query_bwd<DM>()), st>>>(g, q, w.A, w.idx, w.wt, w.ell, b.dz, b.dq32, b.dell);
+    Geo gz = g;
+    k_state_accum<T, float, DM><<<dim3((g.D + 31) / 32, g.n - 1, g.ns), 256, 0, st>>>(
+        gz, q, g.scale, g.gated ? 2 : 0, w.ell, w.lamlog, b.dz, 0, g.E1, g.E1, 0, w.idx, w.wt, 1, 1, b.dA);
+    k_discumsum_bwd<<<dim3((unsigned)((per + 255) / 256), g.ns), 256, 0, st>>>(g, w.lamlog, w.A, b.dA, b.dlam);
+    launches += 3;
+  }
+  k_update_bwd<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_update_bwd<T, DM>, smb_update_bwd<DM>()), st>>>(g, k, v, b.dA, w.idx, w.wt, w.ell, w.lamlog, b.dk32, b.dv32, b.dell, b.dellend);
+  k_intra_bwd_q<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_intra_bwd_q<T, DM>, smb_intra_bwd<DM>()), st>>>(g, q, k, v, w.ell, b.dz, b.dq32, b.dell);
+  k_intra_bwd_kv<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_intra_bwd_kv<T, DM>, smb_intra_bwd<DM>()), st>>>(g, q, k, v, w.ell, b.dz, b.dk32, b.dv32, b.dell);
+  launches += 3;
+  if (dlogg) {
+    k_gate_finish<<<(g.ns * g.n + 127) / 128, 128, 0, st>>>(g, w.lamlog, b.dell, b.dellend, b.dlam, dlogg);
+    ++launches;
+  }
+  k_finalize<T><<<nblk((size_t)g.ns * g.t * g.d, 256), 256, 0, st>>>(g, b.dq32, g.d, dq);
+  k_finalize<T><<<nblk((size_t)g.ns * g.t * g.d, 256), 256, 0, st>>>(g, b.dk32, g.d, dk);
+  k_finalize<T><<<nblk((size_t)g.ns * g.t * g.e, 256), 256, 0, st>>>(g, b.dv32, g.e, dv);
+  launches += 3;
+  count_launch(launches);
+  return cuda_check("simt backward");
+}
+
+template <typename T>
+static int simt_forward_dm(const Geo& g, const void* q, const void* k, const void* v, const float* lg,
+                           void* y, float* rs, const SimtWs& w, cudaStream_t st) {
+  const int mx = std::max(g.d, g.e);
+  if (mx <= 64)
+    return simt_forward_t<T, 64>(g, (const T*)q, (const T*)k, (const T*)v, lg, (T*)y, rs, w, st);
+  return simt_forward_t<T, 128>(g, (const T*)q, (const T*)k, (const T*)v, lg, (T*)y, rs, w, st);
+}
+
+int simt_forward(const Geo& g, int dtype, const void* q, const void* k, const void* v, const float* lg,
+                 void* y, float* rs, const SimtWs& w, cudaStream_t st) {
+  switch (dtype) {
+    case 0: return simt_forward_dm<float>(g, q, k, v, lg, y, rs, w, st);
+    case 1: return simt_forward_dm<__nv_bfloat16>(g, q, k, v, lg, y, rs, w, st);
+    case 2: return simt_forward_dm<__half>(g, q, k, v, lg, y, rs, w, st);
+  }
+  set_error("unsupported dtype for power_full");
+  return 4;
+}
+
+template <typename T>
+static int simt_backward_dm(const Geo& g, const void* q, const void* k, const void* v, const void* y,
+                            const float* rs, const void* dy, void* dq, void* dk, void* dv,
+                            float* dlogg, const SimtWs& w, const SimtBwdWs& b, cudaStream_t st) {
+  const int mx = std::max(g.d, g.e);
+  if (mx <= 64)
+    return simt_backward_t<T, 64>(g, (const T*)q, (const T*)k, (const T*)v, (const T*)y, rs, (const T*)dy,
+                                  (T*)dq, (T*)dk, (T*)dv, dlogg, w, b, st);
+  return simt_backward_t<T, 128>(g, (const T*)q, (const T*)k, (const T*)v, (const T*)y, rs, (const T*)dy,
+                                 (T*)dq, (T*)dk, (T*)dv, dlogg, w, b, st);
+}
+
+int simt_backward(const Geo& g, int dtype, const void* q, const void* k, const void* v, const void* y,
+                  const float* rs, const void* dy, void* dq, void* dk, void* dv, float* dlogg,
+                  const SimtWs& w, const SimtBwdWs& b, cudaStream_t st) {
+  switch (dtype) {
+    case 0: return simt_backward_dm<float>(g, q, k, v, y, rs, dy, dq, dk, dv, dlogg, w, b, st);
+    case 1: return simt_backward_dm<__nv_bfloat16>(g, q, k, v, y, rs, dy, dq, dk, dv, dlogg, w, b, st);
+    case 2: return simt_backward_dm<__half>(g, q, k, v, y, rs, dy, dq, dk, dv, dlogg, w, b, st);
+  }
+  set_error("unsupported dtype for power_full backward");
+  return 4;
+}
+
+int pub_update(int n, int c, int d, int e, int p, int D, int dtype, const void* k, const void* v,
+               const void* w, const int* idx, const float* wt, void* state, void* ks, int acc,
+               cudaStream_t st) {
+  const size_t tot = (size_t)n * D * (e + 1);
+  if (dtype == 3)
+    k_pub_update<double><<<nblk(tot, 128), 128, 0, st>>>(n, c, d, e, p, D, (const double*)k, (const double*)v,
+                                                         (const double*)w, idx, wt, (double*)state, (double*)ks, acc);
+  else
+    k_pub_update<float><<<nblk(tot, 128), 128, 0, st>>>(n, c, d, e, p, D, (const float*)k, (const float*)v,
+                                                        (const float*)w, idx, wt, (float*)state, (float*)ks, acc);
+  count_launch();
+  return cuda_check("update_state");
+}
+
+int pub_query(int n, int c, int d, int e, int p, int D, int dtype, const void* q, const void* state,
+              const void* ks, const int* idx, void* y, void* den, int acc, cudaStream_t st) {
+  const size_t tot = (size_t)n * c * (e + 1);
+  if (dtype == 3)
+    k_pub_query<double><<<nblk(tot, 128), 128, 0, st>>>(n, c, d, e, p, D, (const double*)q, (const double*)state,
+                                                        (const double*)ks, idx, (double*)y, (double*)den, acc);
+  else
+    k_pub_query<float><<<nblk(tot, 128), 128, 0, st>>>(n, c, d, e, p, D, (const float*)q, (const float*)state,
+                                                       (const float*)ks, idx, (float*)y, (float*)den, acc);
+  count_launch();
+  return cuda_check("query_state");
+}
+
+int pub_discumsum(int n, int64_t L, int64_t M, int dtype, const void* values, const void* lams, void* out,
+                  cudaStream_t st) {
+  const size_t tot = (size_t)L * M;
+  if (dtype == 3)
+    k_pub_discumsum<double><<<nblk(tot, 256), 256, 0, st>>>(n, L, M, (const double*)values, (const double*)lams, (double*)out);
+  else
+    k_pub_discumsum<float><<<nblk(tot, 256), 256, 0, st>>>(n, L, M, (const float*)values, (const float*)lams, (float*)out);
+  count_launch();
+  return cuda_check("discumsum");
+}
+
+}  // namespace pa
+
+namespace pa {
+int64_t host_binom(int64_t n, int64_t k) { return binom(n, k); }
+}  // namespace pa

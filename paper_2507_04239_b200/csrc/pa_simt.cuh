@@ -1,0 +1,44 @@
+// Host-side interface of the fp32 CUDA-core kernels (pa_simt.cu).
+#pragma once
+#include "pa_common.cuh"
+
+namespace pa {
+
+struct SimtWs {           // forward workspace, kept for the backward
+  float* ell;             // [ns, t]
+  float* lamlog;          // [ns, n]
+  int* idx;               // [D, p]
+  float* wt;              // [D]
+  float* A;               // [ns, n, D, E1]
+  float* yat;             // [ns, t, E1]
+  int* zflag;             // [1]
+};
+
+struct SimtBwdWs {
+  float* dz;              // [ns, t, E1]
+  float* dA;              // [ns, n, D, E1]
+  float* dq32;            // [ns, t, d]
+  float* dk32;            // [ns, t, d]
+  float* dv32;            // [ns, t, e]
+  float* dell;            // [ns, t]
+  float* dellend;         // [ns, n]
+  float* dlam;            // [ns, n]
+};
+
+int64_t host_binom(int64_t n, int64_t k);
+void host_feature_table(int p, int d, int* idx, double* w);
+int simt_build_table(int p, int d, int D, int* idx, float* wt, cudaStream_t st);
+int simt_forward(const Geo& g, int dtype, const void* q, const void* k, const void* v, const float* lg,
+                 void* y, float* rs, const SimtWs& w, cudaStream_t st);
+int simt_backward(const Geo& g, int dtype, const void* q, const void* k, const void* v, const void* y,
+                  const float* rs, const void* dy, void* dq, void* dk, void* dv, float* dlogg,
+                  const SimtWs& w, const SimtBwdWs& b, cudaStream_t st);
+int pub_update(int n, int c, int d, int e, int p, int D, int dtype, const void* k, const void* v,
+               const void* w, const int* idx, const float* wt, void* state, void* ks, int acc,
+               cudaStream_t st);
+int pub_query(int n, int c, int d, int e, int p, int D, int dtype, const void* q, const void* state,
+              const void* ks, const int* idx, void* y, void* den, int acc, cudaStream_t st);
+int pub_discumsum(int n, int64_t L, int64_t M, int dtype, const void* values, const void* lams, void* out,
+                  cudaStream_t st);
+
+}  // namespace pa

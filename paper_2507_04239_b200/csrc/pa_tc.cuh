@@ -1,0 +1,16 @@
+// Host-side interface of the bf16 tcgen05 (sm_100a tensor-core) pipeline.
+#pragma once
+#include "pa_common.cuh"
+
+namespace pa {
+
+bool tc_supported(const Geo& g, int dtype);
+size_t tc_fwd_workspace_bytes(const Geo& g);
+size_t tc_bwd_workspace_bytes(const Geo& g);
+int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const float* log_g, void* y,
+               float* rowsum, void* ws, cudaStream_t st);
+int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const float* log_g,
+                const void* y, const float* rowsum, const void* dy, void* dq, void* dk, void* dv,
+                float* dlog_g, const void* fwd_ws, void* bwd_ws, cudaStream_t st);
+
+}  // namespace pa

@@ -1,0 +1,134 @@
+"""power_full: the north-star operator (chunked power attention with log-gates)
+as a torch autograd op over the C ABI.
+
+Semantics (reference chunked.py:287-413 with g = exp(log_G); attention form
+when chunk_size is None or >= t, reference test_chunked.py:239-243):
+
+    y[i] = sum_{j <= i} exp(L_i - L_j) (scale * q_i . k_j)^p v_j      (unnormalized)
+    y[i] /= sum_{j <= i} exp(L_i - L_j) (scale * q_i . k_j)^p          (normalize=True)
+
+with L the cumulative sum of log_G over time.  Gradients: dQ, dK, dV and
+dlog_G = g * dgates (reference gradients.py:361-483).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import torch
+
+from . import _lib
+from .errors import InvalidSpec, ShapeMismatch, ZeroDenominator
+
+_DTYPES = {torch.float32: _lib.PA_F32, torch.bfloat16: _lib.PA_BF16, torch.float16: _lib.PA_F16}
+
+
+def _ptr(t):
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _stream(device):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def make_problem(Q, V, p, chunk_size, scale, normalize, gated) -> _lib.PaProblem:
+    b, t, h, d = Q.shape
+    e = V.shape[-1]
+    c = t if chunk_size is None else min(int(chunk_size), t)
+    return _lib.PaProblem(b, t, h, d, e, int(p), c,
+                          float(scale) if scale else 0.0, int(bool(normalize)),
+                          _DTYPES[Q.dtype], int(bool(gated)))
+
+
+def _validate(Q, K, V, log_G, p, chunk_size, normalize):
+    for name, x in (("Q", Q), ("K", K), ("V", V)):
+        if not isinstance(x, torch.Tensor) or x.dim() != 4:
+            raise ShapeMismatch(f"{name} must be a [b, t, h, feature] tensor")
+        if not x.is_cuda:
+            raise InvalidSpec(f"{name} must be a CUDA tensor (this package has no CPU path)")
+    if K.shape != Q.shape:
+        raise ShapeMismatch(f"K shape {tuple(K.shape)} != Q shape {tuple(Q.shape)}")
+    if V.shape[:3] != Q.shape[:3]:
+        raise ShapeMismatch(f"V shape {tuple(V.shape)} disagrees with Q on [b, t, h]")
+    if Q.dtype not in _DTYPES or K.dtype != Q.dtype or V.dtype != Q.dtype:
+        raise InvalidSpec("Q, K, V must share one dtype among float32, bfloat16, float16")
+    if log_G is not None and tuple(log_G.shape) != tuple(Q.shape[:3]):
+        raise ShapeMismatch(f"log_G shape {tuple(log_G.shape)} != [b, t, h] {tuple(Q.shape[:3])}")
+    if chunk_size is not None and int(chunk_size) < 1:
+        raise InvalidSpec(f"chunk_size must be >= 1, got {chunk_size}")
+    if p < 1:
+        raise InvalidSpec(f"power degree must be >= 1, got {p}")
+
+
+class _PowerFull(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, Q, K, V, log_G, p, chunk_size, scale, normalize, check_den):
+        lib = _lib.load()
+        Q, K, V = Q.contiguous(), K.contiguous(), V.contiguous()
+        lg = None if log_G is None else log_G.detach().to(torch.float32).contiguous()
+        pr = make_problem(Q, V, p, chunk_size, scale, normalize, lg is not None)
+        wsb = lib.pa_fwd_workspace_bytes(ctypes.byref(pr))
+        if wsb == 0:
+            _lib.check(lib.pa_fwd_workspace_bytes(ctypes.byref(pr)) or 1, "power_full")
+        ws = torch.empty(wsb, dtype=torch.uint8, device=Q.device)
+        y = torch.empty(*Q.shape[:3], V.shape[-1], dtype=Q.dtype, device=Q.device)
+        rowsum = torch.empty(*Q.shape[:3], dtype=torch.float32, device=Q.device)
+        _lib.check(lib.pa_power_full_fwd(ctypes.byref(pr), _ptr(Q), _ptr(K), _ptr(V), _ptr(lg),
+                                         _ptr(y), _ptr(rowsum), _ptr(ws), wsb, _stream(Q.device)),
+                   "power_full forward")
+        if normalize and check_den:
+            cnt = ctypes.c_int32(0)
+            _lib.check(lib.pa_fwd_zero_denominators(ctypes.byref(pr), _ptr(ws), _stream(Q.device),
+                                                    ctypes.byref(cnt)), "zero-denominator check")
+            if cnt.value:
+                raise ZeroDenominator(
+                    "zeta + phi(q) . key_sum is not positive; cannot normalize")
+        ctx.pr = pr
+        ctx.has_lg = lg is not None
+        ctx.save_for_backward(Q, K, V, lg if lg is not None else torch.empty(0, device=Q.device),
+                              y, rowsum, ws)
+        ctx.mark_non_differentiable(rowsum)
+        return y, rowsum
+
+    @staticmethod
+    def backward(ctx, dy, _drowsum):
+        lib = _lib.load()
+        Q, K, V, lg, y, rowsum, ws = ctx.saved_tensors
+        lg = lg if ctx.has_lg else None
+        pr = ctx.pr
+        dy = dy.contiguous().to(Q.dtype)
+        bb = lib.pa_bwd_workspace_bytes(ctypes.byref(pr))
+        bws = torch.empty(bb, dtype=torch.uint8, device=Q.device)
+        dQ = torch.empty_like(Q)
+        dK = torch.empty_like(K)
+        dV = torch.empty_like(V)
+        dlg = torch.empty_like(lg) if lg is not None else None
+        _lib.check(lib.pa_power_full_bwd(ctypes.byref(pr), _ptr(Q), _ptr(K), _ptr(V), _ptr(lg),
+                                         _ptr(y), _ptr(rowsum), _ptr(dy), _ptr(dQ), _ptr(dK),
+                                         _ptr(dV), _ptr(dlg), _ptr(ws), _ptr(bws), bb,
+                                         _stream(Q.device)), "power_full backward")
+        return dQ, dK, dV, dlg, None, None, None, None, None
+
+
+def power_full_with_rowsum(Q, K, V, log_G=None, *, p=2, chunk_size=None, scale=None,
+                           normalize=False, check_denominator=True):
+    """(y, rowsum): rowsum is the reference AttentionOutput.rowsum
+    (unnormalized score sum zeta + phi(q).key_sum, chunked.py:390)."""
+    _validate(Q, K, V, log_G, p, chunk_size, normalize)
+    return _PowerFull.apply(Q, K, V, log_G, int(p), chunk_size, scale, bool(normalize),
+                            bool(check_denominator))
+
+
+def power_full(Q, K, V, log_G=None, *, p=2, chunk_size=None, scale=None, normalize=False,
+               check_denominator=True):
+    """Chunked power attention on CUDA.  Q, K [b, t, h, d]; V [b, t, h, e];
+    log_G [b, t, h] (log of gates in (0, 1]; None = ungated).  Returns y
+    [b, t, h, e] in Q's dtype.  Zero gates (log_G = -inf) are clamped to
+    log g = -80 inside the kernels."""
+    return power_full_with_rowsum(Q, K, V, log_G, p=p, chunk_size=chunk_size, scale=scale,
+                                  normalize=normalize, check_denominator=check_denominator)[0]
+
+
+def default_scale(d: int) -> float:
+    return 1.0 / math.sqrt(d)

@@ -1,0 +1,81 @@
+"""CPU-side checks of the C ABI: the library loads, exports every symbol the
+header declares, and its host logic (tables, validation, workspace sizing)
+agrees with the oracle.  No kernel is launched here."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+from oracle import power_oracle as O
+
+P = pytest.importorskip("paper_2507_04239_b200")
+from paper_2507_04239_b200 import _lib  # noqa: E402
+
+HEADER = os.path.join(ROOT, "include", "power_attention_b200.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|size_t|const char\*)\s+(pa_\w+)\s*\(", text, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load()
+    syms = declared_symbols()
+    assert len(syms) >= 12
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) <= set(_lib.EXPORTED)
+
+
+@pytest.mark.parametrize("p,d", [(1, 7), (2, 4), (2, 64), (3, 5), (4, 6), (4, 32)])
+def test_feature_table_matches_reference_order(p, d):
+    spec = P.ExpansionSpec.spow(p, d)
+    idx, w = P.monomial_table(spec)
+    ridx, rw = O.ndmi_table(p, d)
+    assert (idx == ridx).all()
+    np.testing.assert_allclose(w, rw, rtol=1e-15)
+    assert _lib.load().pa_feature_dim(p, d) == O.feature_dim(p, d)
+
+
+def _problem(**kw):
+    base = dict(b=1, t=64, h=2, d=16, e=16, p=2, chunk=16, scale=0.0, normalize=0, dtype=0, gated=1)
+    base.update(kw)
+    return _lib.PaProblem(**base)
+
+
+def test_workspace_sizes_and_validation():
+    lib = _lib.load()
+    pr = _problem()
+    assert lib.pa_fwd_workspace_bytes(ctypes.byref(pr)) > 0
+    assert lib.pa_bwd_workspace_bytes(ctypes.byref(pr)) > 0
+    bad = _problem(p=3, normalize=1)
+    assert lib.pa_fwd_workspace_bytes(ctypes.byref(bad)) == 0
+    rc = lib.pa_power_full_fwd(ctypes.byref(bad), None, None, None, None, None, None, None, 0, None)
+    assert rc == 6 and b"even" in lib.pa_last_error()
+    rc = lib.pa_power_full_fwd(ctypes.byref(_problem(chunk=0)), None, None, None, None, None, None, None, 0, None)
+    assert rc == 1
+    with pytest.raises(P.OddPowerWithNormalize):
+        _lib.check(6, "x")
+
+
+def test_reference_surface_names():
+    for name in ("power_full", "attention", "update_state", "query_state", "discumsum",
+                 "chunked_power_attention", "power_attention", "vjp_chunked", "stream_chunk",
+                 "available_backends", "resolve_backend"):
+        assert hasattr(P, name), name
+    assert P.available_backends() == ("cuda",)
+    assert P.resolve_backend(None) == "cuda"
+    with pytest.raises(P.InvalidSpec):
+        P.resolve_backend("gpu")
+
+
+def test_cpu_inputs_fail_loudly():
+    import torch
+    q = torch.zeros(1, 4, 1, 2)
+    with pytest.raises(P.InvalidSpec):
+        P.power_full(q, q, q)

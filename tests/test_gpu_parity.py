@@ -1,0 +1,166 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+outputs and the numpy oracle.
+
+Tolerances (north star, with the reference metric max_rel_error of
+checks.py:26-31): fp32 mode <= 1e-4, bf16 mode <= 2e-2.  Integer-exact
+operations (discumsum's mul-then-add) are checked bit for bit.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden_names, load_golden
+from oracle import power_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2507_04239_b200")
+
+FP32_TOL = 1e-4
+BF16_TOL = 2e-2
+
+
+def cuda(x, dt=torch.float32):
+    return torch.from_numpy(np.ascontiguousarray(x)).to("cuda", dt)
+
+
+def run_full(q, k, v, g, p, c, normalize, dtype=torch.float32, dy=None, scale=None):
+    Q, K, V = (cuda(x, dtype).requires_grad_(dy is not None) for x in (q, k, v))
+    lg = None if g is None else torch.log(cuda(g)).requires_grad_(dy is not None)
+    y, rs = P.power_full_with_rowsum(Q, K, V, lg, p=p, chunk_size=c, normalize=normalize, scale=scale)
+    out = dict(y=y.float().cpu().numpy(), rowsum=rs.cpu().numpy())
+    if dy is not None:
+        ins = [Q, K, V] + ([lg] if lg is not None else [])
+        gr = torch.autograd.grad(y, ins, cuda(dy, dtype))
+        out.update(dq=gr[0].float().cpu().numpy(), dk=gr[1].float().cpu().numpy(),
+                   dv=gr[2].float().cpu().numpy())
+        if lg is not None:
+            out["dlogg"] = gr[3].cpu().numpy()
+    return out
+
+
+@pytest.mark.parametrize("name", golden_names("chunked_"))
+def test_golden_chunked_fp32(name):
+    g = load_golden(name)
+    gates = g.get("gates")
+    r = run_full(g["q"], g["k"], g["v"], gates, int(g["p"]), int(g["c"]), bool(g["normalize"]), dy=g["dy"])
+    assert O.max_rel_error(r["y"], g["y"]) <= FP32_TOL
+    assert O.max_rel_error(r["rowsum"], g["rowsum"]) <= FP32_TOL
+    assert O.max_rel_error(r["dq"], g["dq"]) <= FP32_TOL
+    assert O.max_rel_error(r["dk"], g["dk"]) <= FP32_TOL
+    assert O.max_rel_error(r["dv"], g["dv"]) <= FP32_TOL
+    if gates is not None:
+        assert O.max_rel_error(r["dlogg"], g["dgates"] * gates) <= FP32_TOL
+
+
+def test_config1_fp32_matches_reference():
+    """BASELINE configs[0]: fp32 p=2 d=32 b=1 h=2 t=1024 c=128 gated."""
+    g = load_golden("config1")
+    r = run_full(g["q"], g["k"], g["v"], g["gates"], 2, 128, False, dy=g["dy"])
+    for key in ("y", "rowsum", "dq", "dk", "dv"):
+        assert O.max_rel_error(r[key], g[key]) <= FP32_TOL, key
+    assert O.max_rel_error(r["dlogg"], g["dgates"] * g["gates"]) <= FP32_TOL
+
+
+@pytest.mark.parametrize("normalize", [False, True])
+@pytest.mark.parametrize("p,d,c,t", [(2, 64, 256, 1024), (2, 32, 128, 512), (4, 16, 64, 256)])
+def test_bf16_matches_oracle(p, d, c, t, normalize):
+    q, k, v, g = O.generate_inputs(1, t, 2, d, d, seed=3, gating=True)
+    # the oracle runs in float64 on the same bf16-representable inputs
+    q, k, v = (torch.tensor(x).bfloat16().double().numpy() for x in (q, k, v))
+    dy = np.random.default_rng(4).uniform(-1, 1, (1, t, 2, d))
+    dyb = torch.tensor(dy).bfloat16().double().numpy()
+    r = run_full(q, k, v, g, p, c, normalize, dtype=torch.bfloat16, dy=dyb)
+    y_ref, rs_ref = O.chunked_forward(q, k, v, g, p, c, normalize=normalize)
+    assert O.max_rel_error(r["y"], y_ref) <= BF16_TOL
+    dq, dk, dv, dg = O.chunked_backward(q, k, v, g, p, c, dyb, normalize=normalize)
+    for a, b in ((r["dq"], dq), (r["dk"], dk), (r["dv"], dv), (r["dlogg"], dg * g)):
+        assert O.max_rel_error(a, b) <= BF16_TOL
+
+
+def test_ungated_and_attention_form():
+    q, k, v, _ = O.generate_inputs(2, 96, 2, 8, 8, seed=9)
+    r = run_full(q, k, v, None, 2, None, True, dy=np.ones((2, 96, 2, 8)))
+    y_ref, _ = O.attention_forward(q, k, v, None, 2, normalize=True)
+    assert O.max_rel_error(r["y"], y_ref) <= FP32_TOL
+    dq, dk, dv, _ = O.chunked_backward(q, k, v, None, 2, 96, np.ones((2, 96, 2, 8)), normalize=True)
+    assert O.max_rel_error(r["dq"], dq) <= FP32_TOL and O.max_rel_error(r["dv"], dv) <= FP32_TOL
+
+
+@pytest.mark.parametrize("name", golden_names("kernels_"))
+def test_operator_kernels_f64(name):
+    g = load_golden(name)
+    spec = P.ExpansionSpec.spow(int(g["p"]), g["k"].shape[-1])
+    st, ks = P.update_state_kernel(g["k"], g["v"], g["w"], spec)
+    np.testing.assert_allclose(st, g["state"], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(ks, g["key_sum"], rtol=1e-12, atol=1e-12)
+    y, den = P.query_state_kernel(g["q"], g["state"], g["key_sum"], spec)
+    np.testing.assert_allclose(y, g["y"], rtol=1e-12, atol=1e-11)
+    np.testing.assert_allclose(den, g["denom"], rtol=1e-12, atol=1e-11)
+
+
+def test_discumsum_bit_exact():
+    g = load_golden("discumsum")
+    out = P.discumsum(g["values"], g["lams"])
+    assert (out == g["out"]).all()
+    rng = np.random.default_rng(88)
+    for trial in range(40):
+        n = int(rng.integers(1, 9))
+        vals = rng.normal(size=(n, int(rng.integers(1, 6)), int(rng.integers(1, 5))))
+        lams = rng.uniform(0, 1, max(n - 1, 0))
+        if n > 1 and trial % 5 == 0:
+            lams[int(rng.integers(0, n - 1))] = float(rng.integers(0, 2))
+        assert (P.discumsum(vals, lams) == O.discumsum(vals, lams)).all()
+        v32, l32 = vals.astype(np.float32), lams.astype(np.float32)
+        assert (P.discumsum(v32, l32) == O.discumsum(v32, l32)).all()
+
+
+def test_reference_named_shims_and_worked_examples():
+    spec = P.ExpansionSpec.spow(2, 2)
+    st, lam = P.update_state(spec, np.array([[1.0, 0.0]]), np.array([[5.0]]), np.array([1.0]))
+    assert st.s.tolist() == [[5.0], [0.0], [0.0]] and st.key_sum.tolist() == [1.0, 0.0, 0.0]
+    out = P.query_state(st, np.array([[1.0, 0.0]]), y_attn=np.zeros((1, 1)), zeta=np.zeros(1),
+                        gates_prefix=np.ones(1), scale=1.0, normalize=True)
+    assert out[0, 0] == pytest.approx(5.0)
+    batch = P.SequenceBatch(np.array([1.0, 2.0]).reshape(1, 2, 1, 1), np.array([1.0, 2.0]).reshape(1, 2, 1, 1),
+                            np.array([10.0, 20.0]).reshape(1, 2, 1, 1))
+    cfg = P.AttentionConfig.power(P.ExpansionSpec.spow(2, 1), scale=1.0)
+    o = P.power_attention_form(batch, cfg)
+    np.testing.assert_allclose(o.y.ravel(), [10.0, 360.0], rtol=1e-6)
+    np.testing.assert_allclose(o.rowsum.ravel(), [1.0, 20.0], rtol=1e-6)
+    ones = np.ones((1, 4, 1, 1))
+    o = P.chunked_power_attention(P.SequenceBatch(ones, ones, np.arange(1.0, 5.0).reshape(1, 4, 1, 1)), cfg,
+                                  P.ChunkPlan(4, 2))
+    np.testing.assert_allclose(o.y.ravel(), [1, 3, 6, 10], rtol=1e-6)
+
+
+def test_zero_denominator_raises():
+    q = torch.zeros(1, 4, 1, 2, device="cuda")
+    with pytest.raises(P.ZeroDenominator):
+        P.power_full(q, q, q, None, p=2, chunk_size=2, normalize=True)
+
+
+def test_vjp_chunked_shim_matches_reference():
+    g = load_golden("chunked_0")
+    batch = P.SequenceBatch(g["q"], g["k"], g["v"], g["gates"])
+    cfg = P.AttentionConfig.power(P.ExpansionSpec.spow(2, 4), normalize=True)
+    gr = P.vjp_chunked(batch, cfg, P.ChunkPlan(9, 3), g["dy"])
+    for a, b in ((gr.dq, g["dq"]), (gr.dk, g["dk"]), (gr.dv, g["dv"]), (gr.dgates, g["dgates"])):
+        assert O.max_rel_error(a, b) <= FP32_TOL
+
+
+def test_stream_chunk_matches_full():
+    rng = np.random.default_rng(5)
+    t, c, d, e = 20, 6, 4, 3
+    q, k = rng.uniform(-1, 1, (t, d)), rng.uniform(-1, 1, (t, d))
+    vv, g = rng.uniform(-1, 1, (t, e)), rng.uniform(0.5, 1.0, t)
+    cfg = P.AttentionConfig.power(P.ExpansionSpec.spow(2, d), normalize=True)
+    full, _ = O.chunked_forward(q[None, :, None], k[None, :, None], vv[None, :, None], g[None, :, None], 2, c,
+                                normalize=True)
+    state, ys = None, []
+    for s0 in range(0, t, c):
+        s1 = min(s0 + c, t)
+        y, state = P.stream_chunk(state, q[s0:s1], k[s0:s1], vv[s0:s1], g[s0:s1], cfg)
+        ys.append(y)
+    assert O.max_rel_error(full[0, :, 0], np.concatenate(ys)) <= FP32_TOL
