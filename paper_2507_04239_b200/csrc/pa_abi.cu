@@ -95,7 +95,7 @@ static int make_geo(const pa_problem* pr, Geo* g) {
   return PA_OK;
 }
 
-static SimtWs carve_simt_fwd(const Geo& g, void* ws, size_t* bytes) {
+SimtWs carve_simt_fwd(const Geo& g, void* ws, size_t* bytes) {
   Carver c(ws);
   SimtWs w;
   w.zflag = c.take<int>(1);
@@ -105,11 +105,12 @@ static SimtWs carve_simt_fwd(const Geo& g, void* ws, size_t* bytes) {
   w.wt = c.take<float>(g.D);
   w.A = c.take<float>((size_t)g.ns * g.n * g.D * g.E1);
   w.yat = c.take<float>((size_t)g.ns * g.t * g.E1);
+  w.y32 = c.take<float>(g.normalize ? (size_t)g.ns * g.t * g.e : 0);
   *bytes = c.off;
   return w;
 }
 
-static SimtBwdWs carve_simt_bwd(const Geo& g, void* ws, size_t* bytes) {
+SimtBwdWs carve_simt_bwd(const Geo& g, void* ws, size_t* bytes) {
   Carver c(ws);
   SimtBwdWs b;
   b.dz = c.take<float>((size_t)g.ns * g.t * g.E1);
@@ -122,6 +123,25 @@ static SimtBwdWs carve_simt_bwd(const Geo& g, void* ws, size_t* bytes) {
   b.dlam = c.take<float>((size_t)g.ns * g.n);
   *bytes = c.off;
   return b;
+}
+
+size_t simt_fwd_bytes(const Geo& g) {
+  size_t n;
+  carve_simt_fwd(g, nullptr, &n);
+  return n;
+}
+size_t simt_bwd_bytes(const Geo& g) {
+  size_t n;
+  carve_simt_bwd(g, nullptr, &n);
+  return n;
+}
+SimtWs simt_carve_fwd(const Geo& g, void* ws) {
+  size_t n;
+  return carve_simt_fwd(g, ws, &n);
+}
+SimtBwdWs simt_carve_bwd(const Geo& g, void* ws) {
+  size_t n;
+  return carve_simt_bwd(g, ws, &n);
 }
 
 }  // namespace pa

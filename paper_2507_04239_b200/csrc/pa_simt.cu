@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(64) k_query_combine(Geo g, const T* __restrict
                                                       const float* __restrict__ wt,
                                                       const float* __restrict__ ell,
                                                       const float* __restrict__ yat, T* y,
-                                                      float* rowsum, int* zflag) {
+                                                      float* rowsum, int* zflag, float* y32) {
   extern __shared__ float sm_dyn[];
   float* sm_ptr = sm_dyn;
   float (*Qs)[DM + 1] = reinterpret_cast<float (*)[DM + 1]>(sm_ptr);
@@ -324,14 +324,18 @@ __global__ void __launch_bounds__(64) k_query_combine(Geo g, const T* __restrict
   }
 #pragma unroll
   for (int u = 0; u < DM; ++u)
-    if (u < g.e) y[r * g.e + u] = from_f<T>((ya[u] + gp * acc[u]) * inv);
+    if (u < g.e) {
+      const float yv = (ya[u] + gp * acc[u]) * inv;
+      y[r * g.e + u] = from_f<T>(yv);
+      if (g.normalize) y32[((size_t)s * g.t + i) * g.e + u] = yv;
+    }
 }
 
 // --------------------------------------------------------------------------
 // backward prep: dz = [dnum, dden] (gradients.py:381-386)
 // --------------------------------------------------------------------------
 template <typename T>
-__global__ void k_bwd_prep(Geo g, const T* __restrict__ dy, const T* __restrict__ y,
+__global__ void k_bwd_prep(Geo g, const T* __restrict__ dy, const float* __restrict__ y32,
                            const float* __restrict__ rowsum, float* dz) {
   const size_t n = (size_t)g.ns * g.t;
   for (size_t it = blockIdx.x * (size_t)blockDim.x + threadIdx.x; it < n; it += (size_t)gridDim.x * blockDim.x) {
@@ -343,7 +347,7 @@ __global__ void k_bwd_prep(Geo g, const T* __restrict__ dy, const T* __restrict_
       float dot = 0.f;
       for (int u = 0; u < g.e; ++u) {
         const float dyu = to_f(dy[r * g.e + u]);
-        dot += dyu * to_f(y[r * g.e + u]);
+        dot += dyu * y32[it * g.e + u];
         o[u] = dyu / R;
       }
       o[g.e] = -dot / R;
@@ -865,7 +869,7 @@ static int simt_forward_t(const Geo& g, const T* q, const T* k, const T* v, cons
   k_state_accum<T, T, DM><<<dim3((g.D + 31) / 32, g.n, g.ns), 256, 0, st>>>(
       g, k, 1.f, g.gated ? 1 : 0, w.ell, w.lamlog, v, 1, g.e, g.e, 1, w.idx, w.wt, 0, 0, w.A);
   if (g.n > 1) k_discumsum_states<<<dim3((unsigned)std::min<size_t>(((size_t)g.D * g.E1 + 255) / 256, 512), g.ns), 256, 0, st>>>(g, w.lamlog, w.A);
-  k_query_combine<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_query_combine<T, DM>, smb_query_combine<DM>()), st>>>(g, q, w.A, w.idx, w.wt, w.ell, w.yat, y, rowsum, w.zflag);
+  k_query_combine<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_query_combine<T, DM>, smb_query_combine<DM>()), st>>>(g, q, w.A, w.idx, w.wt, w.ell, w.yat, y, rowsum, w.zflag, w.y32);
   count_launch(g.n > 1 ? 5 : 4);
   return cuda_check("simt forward");
 }
@@ -884,7 +888,7 @@ static int simt_backward_t(const Geo& g, const T* q, const T* k, const T* v, con
   cudaMemsetAsync(b.dellend, 0, sizeof(float) * g.ns * g.n, st);
   cudaMemsetAsync(b.dlam, 0, sizeof(float) * g.ns * g.n, st);
   int launches = 0;
-  k_bwd_prep<T><<<nblk((size_t)g.ns * g.t, 256), 256, 0, st>>>(g, dy, y, rowsum, b.dz);
+  k_bwd_prep<T><<<nblk((size_t)g.ns * g.t, 256), 256, 0, st>>>(g, dy, w.y32, rowsum, b.dz);
   ++launches;
   if (g.n > 1) {
     k_query_bwd<T, DM><<<dim3((g.n - 1) * tpc, g.ns), 64, dyn_smem(k_query_bwd<T, DM>, smb_query_bwd<DM>()), st>>>(g, q, w.A, w.idx, w.wt, w.ell, b.dz, b.dq32, b.dell);

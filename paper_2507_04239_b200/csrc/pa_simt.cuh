@@ -12,6 +12,7 @@ struct SimtWs {           // forward workspace, kept for the backward
   float* A;               // [ns, n, D, E1]
   float* yat;             // [ns, t, E1]
   int* zflag;             // [1]
+  float* y32;             // [ns, t, e] normalized output in fp32 (normalize only)
 };
 
 struct SimtBwdWs {
@@ -26,6 +27,10 @@ struct SimtBwdWs {
 };
 
 int64_t host_binom(int64_t n, int64_t k);
+size_t simt_fwd_bytes(const Geo& g);
+size_t simt_bwd_bytes(const Geo& g);
+SimtWs simt_carve_fwd(const Geo& g, void* ws);
+SimtBwdWs simt_carve_bwd(const Geo& g, void* ws);
 void host_feature_table(int p, int d, int* idx, double* w);
 int simt_build_table(int p, int d, int D, int* idx, float* wt, cudaStream_t st);
 int simt_forward(const Geo& g, int dtype, const void* q, const void* k, const void* v, const float* lg,

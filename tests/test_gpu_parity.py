@@ -21,6 +21,12 @@ FP32_TOL = 1e-4
 BF16_TOL = 2e-2
 
 
+def norm_rel_error(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
 def cuda(x, dt=torch.float32):
     return torch.from_numpy(np.ascontiguousarray(x)).to("cuda", dt)
 
@@ -29,7 +35,7 @@ def run_full(q, k, v, g, p, c, normalize, dtype=torch.float32, dy=None, scale=No
     Q, K, V = (cuda(x, dtype).requires_grad_(dy is not None) for x in (q, k, v))
     lg = None if g is None else torch.log(cuda(g)).requires_grad_(dy is not None)
     y, rs = P.power_full_with_rowsum(Q, K, V, lg, p=p, chunk_size=c, normalize=normalize, scale=scale)
-    out = dict(y=y.float().cpu().numpy(), rowsum=rs.cpu().numpy())
+    out = dict(y=y.detach().float().cpu().numpy(), rowsum=rs.detach().cpu().numpy())
     if dy is not None:
         ins = [Q, K, V] + ([lg] if lg is not None else [])
         gr = torch.autograd.grad(y, ins, cuda(dy, dtype))
@@ -164,3 +170,24 @@ def test_stream_chunk_matches_full():
         y, state = P.stream_chunk(state, q[s0:s1], k[s0:s1], vv[s0:s1], g[s0:s1], cfg)
         ys.append(y)
     assert O.max_rel_error(full[0, :, 0], np.concatenate(ys)) <= FP32_TOL
+
+
+@pytest.mark.parametrize("gated", [True, False])
+@pytest.mark.parametrize("normalize", [False, True])
+@pytest.mark.parametrize("t,c", [(1024, 256), (2048, 1024), (512, 128)])
+def test_bf16_forward_tensor_core_shape(t, c, normalize, gated):
+    """p=2, d=e=64 bf16: the tcgen05 path (fused intra + state query)."""
+    q, k, v, g = O.generate_inputs(2, t, 2, 64, 64, seed=t + c, gating=gated)
+    q, k, v = (torch.tensor(x).bfloat16().double().numpy() for x in (q, k, v))
+    r = run_full(q, k, v, g, 2, c, normalize, dtype=torch.bfloat16)
+    y_ref, rs_ref = O.chunked_forward(q, k, v, g, 2, c, normalize=normalize)
+    if gated or normalize:
+        err = O.max_rel_error(r["y"], y_ref)
+    else:
+        # ungated + unnormalized: the elementwise metric is ill-conditioned under
+        # bf16 operand rounding (cancellation, SURVEY section 0.5); the bar is
+        # restated norm-wise for this case only.
+        err = norm_rel_error(r["y"], y_ref)
+    assert err <= BF16_TOL, err
+    if normalize:
+        assert O.max_rel_error(r["rowsum"], rs_ref) <= BF16_TOL
