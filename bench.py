@@ -1,0 +1,362 @@
+"""Benchmark: chunked power attention fwd+bwd, BASELINE.json configs[1]
+(p=2, d=e=64, b=4, h=16, t=65536, c=1024, gated, bf16) on B200.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+One step = power_full forward + backward over the whole synthetic batch
+(inputs resident in HBM, each 512 MiB >> the 126 MB L2, so no L2 flush is
+needed).  Multi-GPU: one process per GPU (torchrun), each rank runs the full
+per-GPU workload on its own (batch, head) streams with no data-path collective
+(weak scaling: streams are independent).  Timing: CUDA events on
+the launching stream, barrier + synchronize on both sides, max over ranks.
+
+--impl reference times the reference's own CPU algorithm (the numpy oracle
+port, oracle/power_oracle.py, which is pinned to the reference by
+tests/golden) on the host cores: one process per core, each running a bounded
+slice of one (batch, head) stream; tokens/s is extrapolated linearly in t
+(the chunked form is linear in t, reference test_acceptance.py:345-354).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "power-attn fwd+bwd tokens/sec at p=2,d=64,64k ctx; % of BF16 tensor peak"
+CFG = dict(b=4, h=16, t=65536, d=64, e=64, p=2, chunk=1024, gated=True, normalize=False)
+WORKLOAD = "configs[1]: power_full fwd+bwd bf16 p=2 d=64 b=4 h=16 t=65536 chunk=1024 gated"
+
+
+# --------------------------------------------------------------------------
+# algorithmic FLOPs (SURVEY section 8d / BASELINE.md: 2 FLOP per MAC, contractions only)
+# --------------------------------------------------------------------------
+def flops(cfg, ns=None):
+    b, h, t, d, e, p, c = (cfg[k] for k in ("b", "h", "t", "d", "e", "p", "chunk"))
+    ns = b * h if ns is None else ns
+    D = math.comb(d + p - 1, p)
+    n = t // c
+    ecols = e + (1 if cfg["normalize"] else 0)
+    intra = n * c * (c + 1) // 2 * (d + e)
+    update = t * D * ecols
+    query = (t - c) * D * ecols
+    fwd = 2 * ns * (intra + update + query)
+    return dict(fwd=fwd, bwd=2 * fwd, total=3 * fwd, intra=2 * ns * intra, update=2 * ns * update,
+                query=2 * ns * query)
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return pk.get("bf16_tflops", 1590.0), pk.get("bf16_tflops_sustained", 1400.0), pk.get("hbm_gbs", 6650.0), "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+# --------------------------------------------------------------------------
+# clocks sampler (B200_PROFILING.md clocks line)
+# --------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons, power = [], None, set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+                power.append(float(f[3]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_max": max(power) if power else None}
+
+
+# --------------------------------------------------------------------------
+# CPU reference arm / baseline (oracle port of the reference algorithm)
+# --------------------------------------------------------------------------
+def _cpu_worker(args):
+    t_slice, c, seed = args
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+
+    from oracle import power_oracle as O
+
+    with threadpool_limits(1):
+        q, k, v, g = O.generate_inputs(1, t_slice, 1, 64, 64, seed=seed, dtype=np.float32, gating=True)
+        dy = np.ones_like(v)
+        t0 = time.perf_counter()
+        O.chunked_forward(q, k, v, g, 2, c)
+        O.chunked_backward(q, k, v, g, 2, c, dy)
+        return time.perf_counter() - t0
+
+
+def cpu_sample(cores: int, t_slice: int = 4096):
+    """One bounded sample: `cores` processes, each fwd+bwd over one stream
+    slice of t_slice tokens (c=1024, d=64).  Returns (tokens/s of the full
+    b*t metric, seconds, description)."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(cores) as pool:
+        pool.map(_cpu_worker, [(t_slice, CFG["chunk"], i) for i in range(cores)])
+    wall = time.perf_counter() - t0
+    stream_tok_s = cores * t_slice / wall
+    tok_s = stream_tok_s / CFG["h"]  # metric counts b*t tokens; each token spans h streams
+    desc = (f"{cores} processes x 1 stream x {t_slice} tokens (c=1024, d=64, gated) fwd+bwd, numpy oracle "
+            f"(port of reference chunked.py/gradients.py), 1 BLAS thread each; tokens/s = stream-tokens/s / h, "
+            f"linear in t")
+    return tok_s, wall, desc
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_sample(cores, 1024)
+    vals = []
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        v, wall, desc = cpu_sample(cores)
+        vals.append(v)
+    elapsed = time.perf_counter() - t_all
+    val = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * elapsed / max(args.steps, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (Philox, reference inputs.py distributions)",
+        "config": {"workload": WORKLOAD + " (bounded CPU sample, extrapolated)", **CFG},
+        "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": desc},
+        "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------
+# GPU arm
+# --------------------------------------------------------------------------
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_04239_b200 import _lib, power_full
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    b, h, t, d, e, c = (CFG[k] for k in ("b", "h", "t", "d", "e", "chunk"))
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    Q = (torch.rand(b, t, h, d, device=dev, generator=g) * 2 - 1).bfloat16().requires_grad_()
+    K = (torch.rand(b, t, h, d, device=dev, generator=g) * 2 - 1).bfloat16().requires_grad_()
+    V = (torch.rand(b, t, h, e, device=dev, generator=g) * 2 - 1).bfloat16().requires_grad_()
+    LG = torch.log(torch.rand(b, t, h, device=dev, generator=g) * 0.1 + 0.9).requires_grad_()
+    dY = (torch.rand(b, t, h, e, device=dev, generator=g) * 2 - 1).bfloat16()
+
+    def step():
+        y = power_full(Q, K, V, LG, p=CFG["p"], chunk_size=c, normalize=CFG["normalize"])
+        return torch.autograd.grad(y, [Q, K, V, LG], dY)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    _lib.profile_reset()
+    _lib.profile_enable(True)
+    n0 = _lib.launch_count()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    barrier()
+    launches = _lib.launch_count() - n0
+    _lib.profile_enable(False)
+    stages = _lib.profile_read()
+    ck = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    tokens = b * t * world
+    value = tokens / (ms / 1000.0)
+
+    # ---- e2e: reference-facing call with HOST buffers (copies timed) ------
+    e2e = None
+    if not args.no_e2e:
+        hQ, hK, hV = (x.detach().cpu().pin_memory() for x in (Q, K, V))
+        hL = LG.detach().cpu().pin_memory()
+        hdY = dY.cpu().pin_memory()
+        outs = [torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in (Q, K, V, LG)]
+        h2d = sum(x.numel() * x.element_size() for x in (hQ, hK, hV, hL, hdY))
+        d2h = sum(x.numel() * x.element_size() for x in outs)
+
+        def e2e_step():
+            dq, dk, dv, dl, ddy = (x.to(dev, non_blocking=True) for x in (hQ, hK, hV, hL, hdY))
+            for x in (dq, dk, dv, dl):
+                x.requires_grad_()
+            y = power_full(dq, dk, dv, dl, p=CFG["p"], chunk_size=c, normalize=CFG["normalize"])
+            gr = torch.autograd.grad(y, [dq, dk, dv, dl], ddy)
+            for o, gx in zip(outs, gr):
+                o.copy_(gx, non_blocking=True)
+
+        e2e_step()
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(max(1, args.steps // 2)):
+            e2e_step()
+        f1.record()
+        barrier()
+        ems = f0.elapsed_time(f1) / max(1, args.steps // 2)
+        if world > 1:
+            tt = torch.tensor([ems], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt.item())
+        e2e = {"value": tokens / (ems / 1000.0), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": ems}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_sus, hbm, peak_kind = load_peaks()
+    fl = flops(CFG)
+    tflops = fl["total"] / (ms / 1000.0) / 1e12
+    # dominant kernel (largest share of step time) and its roofline
+    stage_ms = {k: v[0] / args.steps for k, v in stages.items()}
+    stage_n = {k: v[1] / args.steps for k, v in stages.items()}
+    roof = None
+    if stage_ms:
+        dom = max(stage_ms, key=stage_ms.get)
+        per = stage_flops(dom, fl)
+        if per is not None:
+            launch_ms = stage_ms[dom] / max(stage_n[dom], 1)
+            achieved = per / max(stage_n[dom], 1) / (launch_ms / 1000.0) / 1e12
+            roof = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peak_sus, "unit": "TFLOP/s",
+                    "frac": achieved / peak_sus, "traffic": traffic_for(dom),
+                    "peak_kind": f"{peak_kind} sustained bf16 (cuBLAS, MEASURED_PEAKS.json)",
+                    "share_of_step": stage_ms[dom] / ms}
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform q,k,v in [-1,1], gates in [0.9,1])",
+        "config": {"workload": WORKLOAD, **CFG, "parallelism": f"streams (b*h) per rank, {world} rank(s)",
+                   "l2": "inputs 512 MiB each >> 126 MB L2; no flush"},
+        "tflops_algorithmic": tflops, "frac_of_peak": tflops / peak, "frac_of_sustained_peak": tflops / peak_sus,
+        "gpu_launches": launches, "stages_ms": stage_ms, "clocks": ck, "e2e": e2e, "roofline": roof,
+    }
+    if world == 1 and not args.no_cpu:
+        try:
+            cores = os.cpu_count() or 1
+            v, wall, desc = cpu_sample(cores)
+            line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": desc,
+                                    "sample_seconds": wall}
+        except Exception as exc:  # the CPU leg must not sink the GPU number
+            line["cpu_baseline"] = {"value": None, "error": repr(exc)}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def stage_flops(stage: str, fl: dict):
+    """Algorithmic FLOPs of one stage per step (the kernel's share of SURVEY 8d)."""
+    return {
+        "fwd_update_state": fl["update"],
+        "fwd_attn_query": fl["intra"] + fl["query"],
+        "bwd_attn_query": 2 * (fl["intra"] + fl["query"]),
+        "bwd_update_state": 2 * fl["update"],
+        "bwd_query_state": 2 * fl["query"],
+        "bwd_intra": 2 * fl["intra"],
+        "bwd_fp32": fl["bwd"],
+    }.get(stage)
+
+
+def traffic_for(stage: str):
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(stage)
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -104,6 +104,14 @@ int pa_query_state(int32_t n, int32_t c, int32_t d, int32_t e, int32_t p, int32_
 int pa_discumsum(int32_t n, int64_t L, int64_t M, int32_t dtype, const void* values,
                  const void* lams, void* out, pa_stream_t stream);
 
+/* Per-stage device timing: CUDA events recorded on the launching stream
+ * around every kernel of the pipelines while enabled.  pa_profile_read fills
+ * up to cap entries (names: cap x 32 bytes) with accumulated milliseconds and
+ * launch counts per stage and returns the number of entries (synchronises). */
+int pa_profile_enable(int32_t on);
+void pa_profile_reset(void);
+int pa_profile_read(char* names, double* ms, int64_t* launches, int32_t cap);
+
 const char* pa_last_error(void);
 /* Number of CUDA kernels this library launched since load (for the bench's
  * gpu_launches claim). */

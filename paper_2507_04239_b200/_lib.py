@@ -67,6 +67,9 @@ _SIGS = {
     "pa_query_state": (ctypes.c_int, [_I32, _I32, _I32, _I32, _I32, _I32, _VP, _VP, _VP, _VP,
                                        _VP, _I32, _VP]),
     "pa_discumsum": (ctypes.c_int, [_I32, _I64, _I64, _I32, _VP, _VP, _VP, _VP]),
+    "pa_profile_enable": (ctypes.c_int, [_I32]),
+    "pa_profile_reset": (None, []),
+    "pa_profile_read": (ctypes.c_int, [_VP, _VP, _VP, _I32]),
     "pa_last_error": (ctypes.c_char_p, []),
     "pa_launch_count": (_I64, []),
 }
@@ -102,3 +105,29 @@ def check(rc: int, what: str) -> None:
 
 def launch_count() -> int:
     return int(load().pa_launch_count())
+
+
+def profile_enable(on: bool) -> None:
+    load().pa_profile_enable(1 if on else 0)
+
+
+def profile_reset() -> None:
+    load().pa_profile_reset()
+
+
+def profile_read() -> dict:
+    """{stage: (milliseconds, launches)} accumulated since the last reset."""
+    import numpy as np
+
+    cap = 64
+    names = ctypes.create_string_buffer(32 * cap)
+    ms = np.zeros(cap, dtype=np.float64)
+    cnt = np.zeros(cap, dtype=np.int64)
+    n = load().pa_profile_read(names, ms.ctypes.data_as(ctypes.c_void_p),
+                               cnt.ctypes.data_as(ctypes.c_void_p), cap)
+    raw = names.raw
+    out = {}
+    for i in range(n):
+        nm = raw[32 * i: 32 * i + 32].split(b"\0", 1)[0].decode()
+        out[nm] = (float(ms[i]), int(cnt[i]))
+    return out

@@ -2,9 +2,14 @@
 // the stage order of the forward / backward pipelines.
 #include <math.h>
 
+#include <string.h>
+
 #include <algorithm>
 #include <atomic>
+#include <map>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/power_attention_b200.h"
 #include "pa_common.cuh"
@@ -26,6 +31,45 @@ int cuda_check(const char* what) {
     return PA_ERR_CUDA;
   }
   return PA_OK;
+}
+
+// ---------------------------------------------------------------- profiling
+struct ProfRec {
+  const char* name;
+  cudaEvent_t a, b;
+};
+static std::mutex g_pm;
+static std::vector<ProfRec> g_prof;
+static std::atomic<bool> g_prof_on{false};
+static std::map<std::string, std::pair<double, int64_t>> g_prof_acc;
+
+StageTimer::StageTimer(const char* n, cudaStream_t s) : name(n), st(s), a(nullptr) {
+  if (!g_prof_on.load()) return;
+  cudaEventCreate(&a);
+  cudaEventRecord(a, st);
+}
+StageTimer::~StageTimer() {
+  if (!a) return;
+  cudaEvent_t b;
+  cudaEventCreate(&b);
+  cudaEventRecord(b, st);
+  std::lock_guard<std::mutex> lk(g_pm);
+  g_prof.push_back({name, a, b});
+}
+
+static void prof_drain() {
+  std::lock_guard<std::mutex> lk(g_pm);
+  for (auto& r : g_prof) {
+    float ms = 0.f;
+    cudaEventSynchronize(r.b);
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    auto& e = g_prof_acc[r.name];
+    e.first += ms;
+    e.second += 1;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_prof.clear();
 }
 
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
@@ -341,6 +385,33 @@ int pa_discumsum(int32_t n, int64_t L, int64_t M, int32_t dtype, const void* val
     return PA_ERR_UNSUPPORTED;
   }
   return pub_discumsum(n, L, M, dtype, values, lams, out, (cudaStream_t)stream);
+}
+
+int pa_profile_enable(int32_t on) {
+  if (!on) prof_drain();
+  g_prof_on.store(on != 0);
+  return PA_OK;
+}
+
+void pa_profile_reset(void) {
+  prof_drain();
+  std::lock_guard<std::mutex> lk(g_pm);
+  g_prof_acc.clear();
+}
+
+int pa_profile_read(char* names, double* ms, int64_t* launches, int32_t cap) {
+  prof_drain();
+  std::lock_guard<std::mutex> lk(g_pm);
+  int i = 0;
+  for (auto& kv : g_prof_acc) {
+    if (i >= cap) break;
+    strncpy(names + 32 * i, kv.first.c_str(), 31);
+    names[32 * i + 31] = 0;
+    ms[i] = kv.second.first;
+    launches[i] = kv.second.second;
+    ++i;
+  }
+  return i;
 }
 
 const char* pa_last_error(void) { return g_err.c_str(); }

@@ -62,6 +62,17 @@ __device__ __forceinline__ float block_sum(float v, float* red /*[32]*/) {
   return warp_sum(r);
 }
 
+// Per-stage device timing (CUDA events on the launching stream), enabled by
+// pa_profile_enable(1).  Scope object: records start on construction, end on
+// destruction.
+struct StageTimer {
+  StageTimer(const char* name, cudaStream_t st);
+  ~StageTimer();
+  const char* name;
+  cudaStream_t st;
+  cudaEvent_t a;
+};
+
 // error plumbing shared by the host side
 void set_error(const std::string& msg);
 int cuda_check(const char* what);

@@ -63,7 +63,7 @@ def _validate(Q, K, V, log_G, p, chunk_size, normalize):
 
 class _PowerFull(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, Q, K, V, log_G, p, chunk_size, scale, normalize, check_den):
+    def forward(ctx, Q, K, V, log_G, p, chunk_size, scale, normalize, check_den, want_rowsum):
         lib = _lib.load()
         Q, K, V = Q.contiguous(), K.contiguous(), V.contiguous()
         lg = None if log_G is None else log_G.detach().to(torch.float32).contiguous()
@@ -73,9 +73,12 @@ class _PowerFull(torch.autograd.Function):
             _lib.check(lib.pa_fwd_workspace_bytes(ctypes.byref(pr)) or 1, "power_full")
         ws = torch.empty(wsb, dtype=torch.uint8, device=Q.device)
         y = torch.empty(*Q.shape[:3], V.shape[-1], dtype=Q.dtype, device=Q.device)
-        rowsum = torch.empty(*Q.shape[:3], dtype=torch.float32, device=Q.device)
+        # the score sum costs extra MMAs; only produce it when it is consumed
+        need_rs = bool(normalize or want_rowsum)
+        rowsum = torch.empty(*Q.shape[:3] if need_rs else (0,), dtype=torch.float32, device=Q.device)
         _lib.check(lib.pa_power_full_fwd(ctypes.byref(pr), _ptr(Q), _ptr(K), _ptr(V), _ptr(lg),
-                                         _ptr(y), _ptr(rowsum), _ptr(ws), wsb, _stream(Q.device)),
+                                         _ptr(y), _ptr(rowsum if need_rs else None), _ptr(ws), wsb,
+                                         _stream(Q.device)),
                    "power_full forward")
         if normalize and check_den:
             cnt = ctypes.c_int32(0)
@@ -105,19 +108,20 @@ class _PowerFull(torch.autograd.Function):
         dV = torch.empty_like(V)
         dlg = torch.empty_like(lg) if lg is not None else None
         _lib.check(lib.pa_power_full_bwd(ctypes.byref(pr), _ptr(Q), _ptr(K), _ptr(V), _ptr(lg),
-                                         _ptr(y), _ptr(rowsum), _ptr(dy), _ptr(dQ), _ptr(dK),
+                                         _ptr(y), _ptr(rowsum if rowsum.numel() else None), _ptr(dy),
+                                         _ptr(dQ), _ptr(dK),
                                          _ptr(dV), _ptr(dlg), _ptr(ws), _ptr(bws), bb,
                                          _stream(Q.device)), "power_full backward")
-        return dQ, dK, dV, dlg, None, None, None, None, None
+        return dQ, dK, dV, dlg, None, None, None, None, None, None
 
 
 def power_full_with_rowsum(Q, K, V, log_G=None, *, p=2, chunk_size=None, scale=None,
-                           normalize=False, check_denominator=True):
+                           normalize=False, check_denominator=True, _want_rowsum=True):
     """(y, rowsum): rowsum is the reference AttentionOutput.rowsum
     (unnormalized score sum zeta + phi(q).key_sum, chunked.py:390)."""
     _validate(Q, K, V, log_G, p, chunk_size, normalize)
     return _PowerFull.apply(Q, K, V, log_G, int(p), chunk_size, scale, bool(normalize),
-                            bool(check_denominator))
+                            bool(check_denominator), bool(_want_rowsum))
 
 
 def power_full(Q, K, V, log_G=None, *, p=2, chunk_size=None, scale=None, normalize=False,
@@ -127,7 +131,8 @@ def power_full(Q, K, V, log_G=None, *, p=2, chunk_size=None, scale=None, normali
     [b, t, h, e] in Q's dtype.  Zero gates (log_G = -inf) are clamped to
     log g = -80 inside the kernels."""
     return power_full_with_rowsum(Q, K, V, log_G, p=p, chunk_size=chunk_size, scale=scale,
-                                  normalize=normalize, check_denominator=check_denominator)[0]
+                                  normalize=normalize, check_denominator=check_denominator,
+                                  _want_rowsum=False)[0]
 
 
 def default_scale(d: int) -> float:
