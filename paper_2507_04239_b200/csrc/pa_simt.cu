@@ -1000,4 +1000,31 @@ int pub_discumsum(int n, int64_t L, int64_t M, int dtype, const void* values, co
 
 namespace pa {
 int64_t host_binom(int64_t n, int64_t k) { return binom(n, k); }
+
+// pieces reused by the bf16 tensor-core backward (pa_tc.cu)
+int simt_intra_bwd(const Geo& g, const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
+                   const float* ell, const float* dz, float* dq32, float* dk32, float* dv32, float* dell,
+                   cudaStream_t st) {
+  using T = __nv_bfloat16;
+  const int tpc = (g.c + 63) / 64;
+  k_intra_bwd_q<T, 64><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_intra_bwd_q<T, 64>, smb_intra_bwd<64>()), st>>>(
+      g, q, k, v, ell, dz, dq32, dell);
+  k_intra_bwd_kv<T, 64><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_intra_bwd_kv<T, 64>, smb_intra_bwd<64>()), st>>>(
+      g, q, k, v, ell, dz, dk32, dv32, dell);
+  count_launch(2);
+  return cuda_check("intra backward");
+}
+
+int simt_gate_finish(const Geo& g, const float* lamlog, const float* dell, const float* dellend,
+                     const float* dlam, float* dlogg, cudaStream_t st) {
+  k_gate_finish<<<(g.ns * g.n + 127) / 128, 128, 0, st>>>(g, lamlog, dell, dellend, dlam, dlogg);
+  count_launch();
+  return cuda_check("gate finish");
+}
+
+int simt_finalize_bf16(const Geo& g, const float* src, int w, void* dst, cudaStream_t st) {
+  k_finalize<__nv_bfloat16><<<nblk((size_t)g.ns * g.t * w, 256), 256, 0, st>>>(g, src, w, (__nv_bfloat16*)dst);
+  count_launch();
+  return cuda_check("finalize");
+}
 }  // namespace pa

@@ -38,6 +38,12 @@ int simt_forward(const Geo& g, int dtype, const void* q, const void* k, const vo
 int simt_backward(const Geo& g, int dtype, const void* q, const void* k, const void* v, const void* y,
                   const float* rs, const void* dy, void* dq, void* dk, void* dv, float* dlogg,
                   const SimtWs& w, const SimtBwdWs& b, cudaStream_t st);
+int simt_intra_bwd(const Geo& g, const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
+                   const float* ell, const float* dz, float* dq32, float* dk32, float* dv32, float* dell,
+                   cudaStream_t st);
+int simt_gate_finish(const Geo& g, const float* lamlog, const float* dell, const float* dellend,
+                     const float* dlam, float* dlogg, cudaStream_t st);
+int simt_finalize_bf16(const Geo& g, const float* src, int w, void* dst, cudaStream_t st);
 int pub_update(int n, int c, int d, int e, int p, int D, int dtype, const void* k, const void* v,
                const void* w, const int* idx, const float* wt, void* state, void* ks, int acc,
                cudaStream_t st);

@@ -2,18 +2,20 @@
 //
 // Forward (per stream s, chunk k; reference chunked.py:287-413):
 //   prep_gates : ell = in-chunk cumsum of log g, lamlog = ell at chunk end
-//   prep_kt    : K~^T [dim][token] with k~_j = k_j * exp((ell_end - ell_j)/2),
+//   prep_xt    : K~^T [dim][token] with k~_j = k_j * exp((ell_end - ell_j)/2),
 //                so phi'(k~_j) = W_j phi'(k_j) (suffix decay, chunked.py:89-95)
-//   upd        : S'_k = phi'(K~)^T [V | 1] -- tcgen05, A = phi'(K~)^T generated
+//   featmajor  : S'_k = phi'(K~)^T [V | 1] -- tcgen05, A = phi'(K~)^T generated
 //                into TMEM from K~^T in smem (update_state, kernels.py:55-83)
-//   scan       : A'_k = lambda_k A'_{k-1} + omega * S'_k in fp32 (discumsum,
-//                chunked.py:156-176), stored bf16 in the compact [u][f] tiles
+//   scan       : A'_k = lambda_k A'_{k-1} + omega S'_k in fp32 (discumsum,
+//                chunked.py:156-176), stored bf16 [slot][u]
 //   out        : y = intra-chunk power attention (S = Q K^T, P = decay * s^2,
 //                O += P V on tcgen05) + phi'(q~) A'_{k-1} with phi'(q~)
 //                generated from registers into TMEM (query_state + combine,
 //                chunked.py:372-395); one TMEM accumulator for both.
+// Backward (gradients.py:361-483) mirrors it: featmajor<true> (dA' =
+// phi'(Q~)^T [dnum|dden]), reverse scan, token-major dphi GEMMs with the
+// expand-VJP fused into their epilogue, and the intra-chunk VJP.
 #include <cuda.h>
-
 #include <stdio.h>
 
 #include <algorithm>
@@ -264,53 +266,43 @@ __global__ void __launch_bounds__(256, 1) k_tc_featmajor(const __grid_constant__
 }
 
 // ==========================================================================
-// scan (discumsum over chunk states) + reorder to compact [u][f] bf16 tiles
-//   A'_k = lambda_k A'_{k-1} + omega_f S'_k      (chunked.py:156-176, 356-367)
-// grid (33 feature blocks, stream); 256 threads
+// state layout helpers: [slot][64] bf16 rows (SW128) + [slot][16] bf16 (SW32)
 // ==========================================================================
-__device__ __forceinline__ int hard_slot(int a, int b) {
-  const int blk = c_blk.idx[a >> 2][b >> 3];
-  return blk * 32 + (a & 3) * 8 + (b & 7);
+__device__ __forceinline__ uint32_t sw128_elem(int row, int col) {  // bf16 element offset in bytes
+  return (uint32_t)row * 128u + ((((uint32_t)col >> 3) ^ ((uint32_t)row & 7u)) << 4) + ((uint32_t)col & 7u) * 2u;
 }
-
-__device__ __forceinline__ uint32_t st_off(int u, int f) {  // byte offset inside a [80][64] bf16 tile
-  return (uint32_t)u * 128u + ((((uint32_t)f >> 3) ^ ((uint32_t)u & 7u)) << 4) + ((uint32_t)f & 7u) * 2u;
+__device__ __forceinline__ uint32_t sw32_elem(int row, int col) {
+  return (uint32_t)row * 32u + ((((uint32_t)col >> 3) ^ (((uint32_t)row >> 2) & 1u)) << 4) + ((uint32_t)col & 7u) * 2u;
 }
+__device__ __forceinline__ float slot_omega(int f) {
+  const int a = 4 * c_blk.al[f >> 5] + ((f >> 3) & 3), b = 8 * c_blk.be[f >> 5] + (f & 7);
+  return a == b ? 1.f : (a < b ? 2.f : 0.f);
+}
+constexpr size_t ST_MAIN = (size_t)FH * 64;   // bf16 elements per (stream, chunk) state, value part
+constexpr size_t ST_DEN = (size_t)FH * 16;    // bf16 elements, score-sum part
 
+// ==========================================================================
+// forward scan (discumsum over chunk states, chunked.py:156-176 / 356-367):
+//   A'_k = lambda_k A'_{k-1} + omega * S'_k   (fp32 running sum, bf16 stores)
+// thread per (slot, column); grid (ceil(FH*ucols/256), stream)
+// ==========================================================================
 __global__ void __launch_bounds__(256) k_tc_scan_fwd(Geo g, int ucols, const float* __restrict__ lamlog,
-                                                     const float* __restrict__ sp, __nv_bfloat16* stout) {
-  __shared__ float tile[64][UW + 1];
-  __shared__ int rows[64];
-  __shared__ float om[64];
-  const int fb = blockIdx.x, s = blockIdx.y, tid = threadIdx.x;
-  if (tid < 64) {
-    int a, b;
-    compact_ab(fb * 64 + tid, a, b);
-    rows[tid] = (a <= b) ? hard_slot(a, b) : -1;
-    om[tid] = (a == b) ? 1.f : (a < b ? 2.f : 0.f);
-  }
-  __syncthreads();
-  const int fl = tid & 63, u0 = tid >> 6;
-  constexpr int PER = UW / 4;  // 20 columns per thread
-  float acc[PER];
-#pragma unroll
-  for (int i = 0; i < PER; ++i) acc[i] = 0.f;
+                                                     const float* __restrict__ sp, __nv_bfloat16* st_main,
+                                                     __nv_bfloat16* st_den) {
+  const int s = blockIdx.y;
+  const int e = blockIdx.x * 256 + threadIdx.x;
+  if (e >= FH * ucols) return;
+  const int f = e / ucols, u = e - f * ucols;
+  const float om = slot_omega(f);
+  float acc = 0.f;
   for (int k = 0; k < g.n; ++k) {
-    __syncthreads();
-    const float* src = sp + (size_t)(s * g.n + k) * FH * UW;
-    for (int i = tid; i < 64 * UW; i += 256) {
-      const int r = i / UW, u = i - r * UW;
-      tile[r][u] = (rows[r] >= 0 && u < ucols) ? src[(size_t)rows[r] * UW + u] : 0.f;
-    }
-    __syncthreads();
-    const float lam = (k == 0 || !g.gated) ? (k == 0 ? 0.f : 1.f) : __expf(lamlog[s * g.n + k]);
-    uint8_t* dst = (uint8_t*)(stout + ((size_t)(s * g.n + k) * NFB + fb) * (UW * 64));
-#pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int u = u0 + 4 * i;
-      acc[i] = lam * acc[i] + om[fl] * tile[fl][u];
-      *(__nv_bfloat16*)(dst + st_off(u, fl)) = __float2bfloat16_rn(acc[i]);
-    }
+    const float lam = k == 0 ? 0.f : (g.gated ? __expf(lamlog[s * g.n + k]) : 1.f);
+    acc = lam * acc + om * sp[((size_t)(s * g.n + k) * FH + f) * UW + u];
+    const __nv_bfloat16 v = __float2bfloat16_rn(acc);
+    if (u < 64)
+      *(__nv_bfloat16*)((uint8_t*)(st_main + (size_t)(s * g.n + k) * ST_MAIN) + sw128_elem(f, u)) = v;
+    else
+      *(__nv_bfloat16*)((uint8_t*)(st_den + (size_t)(s * g.n + k) * ST_DEN) + sw32_elem(f, u - 64)) = v;
   }
 }
 
@@ -326,33 +318,24 @@ namespace outk {
 constexpr int QB = 128 * 128;           // Q tile bytes (128 tok x 64 dims bf16)
 constexpr int KB = 128 * 128;           // K tile
 constexpr int VB = 128 * 128;           // V tile
-constexpr int STB = UW * 128;           // state block (80 u x 64 f bf16)
+constexpr int STB = 64 * 128;           // state K-block: 64 slots x 64 values
+constexpr int STD = 64 * 32;            // state K-block score-sum part
 constexpr int KV_ST = 3;
 constexpr int ST_ST = 8;
-constexpr int NA = 4;                   // TMEM A buffers (64 features each)
-constexpr int SMEM = 1024 + QB + KV_ST * (KB + VB) + ST_ST * STB + 2048 + 4096 + 1024 + 512;
+constexpr int NA = 4;                   // TMEM A buffers (64 slots each)
+constexpr int SMEM = 1024 + QB + KV_ST * (KB + VB) + ST_ST * (STB + STD) + 2048 + 4096 + 1024 + 512;
 }  // namespace outk
 
-template <int C>
-__device__ __forceinline__ uint32_t bcast_a(const uint32_t* qp) {
-  constexpr int a = col_a(C);
-  return __byte_perm(qp[a >> 1], 0, (a & 1) ? 0x3232 : 0x1010);
-}
-template <int FB, int... I>
-__device__ __forceinline__ void gen_block(const uint32_t* qp, uint32_t* o, std::integer_sequence<int, I...>) {
-  ((o[I] = hmul2_bf16(bcast_a<FB * 32 + I>(qp), qp[col_beta(FB * 32 + I)])), ...);
-}
-
-// compute warps: phi'(x) for the 33 compact feature blocks of one token row,
-// each written to a TMEM A buffer and handed to the MMA warp via a_full.
-template <int FB>
-__device__ __forceinline__ void gen_all_blocks(const uint32_t (&qp)[32], uint32_t a_base, uint32_t lane_off,
-                                               uint64_t* a_full, uint64_t* a_empty, int l) {
-  constexpr int NA = outk::NA;
-  constexpr int bb = FB % NA;
-  if (FB >= NA) mbar_wait(&a_empty[bb], ((FB / NA) + 1) & 1);
+// compute warps: phi'(x) for the 36 K blocks of one token row, each written to
+// a TMEM A buffer and handed to the MMA warp.
+template <int KB, int NA>
+__device__ __forceinline__ void gen_all_kblocks(const uint32_t (&xp)[32], uint32_t a_base, uint32_t lane_off,
+                                                uint64_t* a_full, uint64_t* a_empty, int l) {
+  constexpr int bb = KB % NA;
+  if (KB >= NA) mbar_wait(&a_empty[bb], ((KB / NA) + 1) & 1);
   uint32_t o[32];
-  gen_block<FB>(qp, o, std::make_integer_sequence<int, 32>{});
+  gen_fblock<2 * KB>(xp, o);
+  gen_fblock<2 * KB + 1>(xp, o + 16);
   const uint32_t ast = a_base + (uint32_t)(bb * 32) + lane_off;
   tmem_st16(ast, o);
   tmem_st16(ast + 16, o + 16);
@@ -360,7 +343,21 @@ __device__ __forceinline__ void gen_all_blocks(const uint32_t (&qp)[32], uint32_
   tc_fence_before();
   __syncwarp();
   if (l == 0) mbar_arrive(&a_full[bb]);
-  if constexpr (FB + 1 < NFB) gen_all_blocks<FB + 1>(qp, a_base, lane_off, a_full, a_empty, l);
+  if constexpr (KB + 1 < NKB) gen_all_kblocks<KB + 1, NA>(xp, a_base, lane_off, a_full, a_empty, l);
+}
+
+__device__ __forceinline__ void load_scaled_row(const __nv_bfloat16* src, float f, uint32_t (&xp)[32]) {
+  const uint4* row = (const uint4*)src;
+#pragma unroll
+  for (int c8 = 0; c8 < 8; ++c8) {
+    uint4 v4 = row[c8];
+    const uint32_t* pv = (const uint32_t*)&v4;
+#pragma unroll
+    for (int e2 = 0; e2 < 4; ++e2) {
+      float2 f2 = __bfloat1622float2(*(const __nv_bfloat162*)&pv[e2]);
+      xp[c8 * 4 + e2] = pack_bf16(f2.x * f, f2.y * f);
+    }
+  }
 }
 
 __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUtensorMap tm_q,
@@ -368,17 +365,18 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
                                                    const __grid_constant__ CUtensorMap tm_v, Geo g,
                                                    const __nv_bfloat16* __restrict__ qraw,
                                                    const float* __restrict__ ell,
-                                                   const __nv_bfloat16* __restrict__ st_all, int with_den,
-                                                   __nv_bfloat16* y, float* rowsum, float* y32, int* zflag,
-                                                   unsigned long long* dbg) {
+                                                   const __nv_bfloat16* __restrict__ st_main,
+                                                   const __nv_bfloat16* __restrict__ st_den, int with_den,
+                                                   __nv_bfloat16* y, float* rowsum, float* y32, int* zflag) {
   using namespace outk;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keep the shared address space
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* q_s = smem;
   uint8_t* k_s = q_s + QB;
   uint8_t* v_s = k_s + KV_ST * KB;
   uint8_t* st_s = v_s + KV_ST * VB;
-  uint8_t* ones = st_s + ST_ST * STB;
+  uint8_t* sd_s = st_s + ST_ST * STB;
+  uint8_t* ones = sd_s + ST_ST * STD;
   float* ell_s = (float*)(ones + 2048);       // [1024]
   float* cj = ell_s + 1024;                   // [2][128]
   uint64_t* bars = (uint64_t*)(cj + 256);
@@ -434,15 +432,6 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
   const uint32_t tm = tmem_base;
   const uint32_t a_base = tm + 128u;
   auto sbuf = [&](int b) { return tm + 256u + (uint32_t)(b * 128); };
-  const size_t cta = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-  auto stamp = [&](int i) {
-    if (dbg) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      dbg[cta * 64 + i] = t;
-    }
-  };
-  if (tid == 0) stamp(0);
 
   if (w == 0) {
     // ---------------- loads ----------------
@@ -455,7 +444,6 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
       auto kv = [&](int J) {
         const int st = J % KV_ST;
         if (J >= KV_ST) mbar_wait(&kv_empty[st], ((J / KV_ST) + 1) & 1);
-        if (J < 8) stamp(8 + J);
         mbar_expect_tx(&kv_full[st], KB + VB);
         tma_load_4d(k_s + st * KB, &tm_k, &kv_full[st], 0, hi, c0 + J * 128, bi);
         tma_load_4d(v_s + st * VB, &tm_v, &kv_full[st], 0, hi, c0 + J * 128, bi);
@@ -463,13 +451,14 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
       const int early = min(I + 1, KV_ST);
       for (int J = 0; J < early; ++J) kv(J);
       if (has_state) {
-        const __nv_bfloat16* src = st_all + ((size_t)(s * g.n + (k - 1)) * NFB) * (UW * 64);
-        const uint32_t bytes = den ? STB : 64 * 128;
-        for (int fb = 0; fb < NFB; ++fb) {
-          const int sb = fb % ST_ST;
-          if (fb >= ST_ST) mbar_wait(&st_empty[sb], ((fb / ST_ST) + 1) & 1);
-          mbar_expect_tx(&st_full[sb], bytes);
-          bulk_load(st_s + sb * STB, src + (size_t)fb * (UW * 64), bytes, &st_full[sb]);
+        const __nv_bfloat16* srcm = st_main + (size_t)(s * g.n + (k - 1)) * ST_MAIN;
+        const __nv_bfloat16* srcd = st_den + (size_t)(s * g.n + (k - 1)) * ST_DEN;
+        for (int kb = 0; kb < NKB; ++kb) {
+          const int sb = kb % ST_ST;
+          if (kb >= ST_ST) mbar_wait(&st_empty[sb], ((kb / ST_ST) + 1) & 1);
+          mbar_expect_tx(&st_full[sb], STB + (den ? STD : 0));
+          bulk_load(st_s + sb * STB, srcm + (size_t)kb * 64 * 64, STB, &st_full[sb]);
+          if (den) bulk_load(sd_s + sb * STD, srcd + (size_t)kb * 64 * 16, STD, &st_full[sb]);
         }
       }
       for (int J = early; J <= I; ++J) kv(J);
@@ -477,29 +466,28 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
   } else if (w == 1) {
     // ---------------- MMA issuer ----------------
     if (l == 0) {
-      const uint32_t id64k = idesc_bf16(128, 64, false, false);
-      const uint32_t id16k = idesc_bf16(128, 16, false, false);
       const uint32_t id64mn = idesc_bf16(128, 64, false, true);
+      const uint32_t id16mn = idesc_bf16(128, 16, false, true);
+      const uint32_t id16k = idesc_bf16(128, 16, false, false);
       const uint32_t id128 = idesc_bf16(128, 128, false, false);
       if (has_state) {
-        for (int fb = 0; fb < NFB; ++fb) {
-          const int bb = fb % NA, sb = fb % ST_ST;
-          mbar_wait(&a_full[bb], (fb / NA) & 1);
-          mbar_wait(&st_full[sb], (fb / ST_ST) & 1);
+        for (int kb = 0; kb < NKB; ++kb) {
+          const int bb = kb % NA, sb = kb % ST_ST;
+          mbar_wait(&a_full[bb], (kb / NA) & 1);
+          mbar_wait(&st_full[sb], (kb / ST_ST) & 1);
           tc_fence_after();
-          const uint32_t sbase = smem_u32(st_s + sb * STB);
+          const uint32_t sm = smem_u32(st_s + sb * STB), sdn = smem_u32(sd_s + sb * STD);
           const uint32_t ab = a_base + (uint32_t)(bb * 32);
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            const uint32_t f = (fb > 0 || kk > 0) ? 1u : 0u;
-            mma_ts(tm, ab + kk * 8, smem_desc(sbase + kk * 32, 16, 1024, 2), id64k, f);
-            if (den) mma_ts(tm + 64, ab + kk * 8, smem_desc(sbase + 8192 + kk * 32, 16, 1024, 2), id16k, f);
+            const uint32_t f = (kb > 0 || kk > 0) ? 1u : 0u;
+            mma_ts(tm, ab + kk * 8, smem_desc(sm + kk * 2048, 8192, 1024, 2), id64mn, f);
+            if (den) mma_ts(tm + 64, ab + kk * 8, smem_desc(sdn + kk * 512, 2048, 256, 6), id16mn, f);
           }
           tc_commit(&a_empty[bb]);
           tc_commit(&st_empty[sb]);
         }
       }
-      stamp(1);
       mbar_wait(q_full, 0);
       auto issue_s = [&](int J) {
         const int st = J % KV_ST, sb = J & 1;
@@ -511,14 +499,12 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
           mma_ss(sbuf(sb), smem_desc(smem_u32(q_s) + kk * 32, 16, 1024, 2),
                  smem_desc(smem_u32(k_s + st * KB) + kk * 32, 16, 1024, 2), id128, kk > 0 ? 1u : 0u);
         tc_commit(&s_full[sb]);
-        if (J < 8) stamp(16 + J);
       };
       issue_s(0);
       for (int J = 0; J <= I; ++J) {
         if (J + 1 <= I) issue_s(J + 1);
         const int sb = J & 1, st = J % KV_ST;
         mbar_wait(&p_full[sb], (J >> 1) & 1);
-        if (J < 8) stamp(24 + J);
         tc_fence_after();
         const uint32_t vb = smem_u32(v_s + st * VB);
 #pragma unroll
@@ -532,7 +518,6 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
         tc_commit(&kv_empty[st]);
       }
       tc_commit(fin);
-      stamp(2);
     }
   } else if (w >= 4) {
     // ---------------- compute warps ----------------
@@ -543,21 +528,9 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
     const float sig2 = g.scale * g.scale;
     if (has_state) {
       uint32_t qp[32];
-      const float f = g.scale * __expf(0.5f * li);
-      const uint4* qrow = (const uint4*)(qraw + rowid(g, s, tok) * HD);
-#pragma unroll
-      for (int c8 = 0; c8 < 8; ++c8) {
-        uint4 v4 = qrow[c8];
-        const uint32_t* pv = (const uint32_t*)&v4;
-#pragma unroll
-        for (int e2 = 0; e2 < 4; ++e2) {
-          float2 f2 = __bfloat1622float2(*(const __nv_bfloat162*)&pv[e2]);
-          qp[c8 * 4 + e2] = pack_bf16(f2.x * f, f2.y * f);
-        }
-      }
-      gen_all_blocks<0>(qp, a_base, lane_off, a_full, a_empty, l);
+      load_scaled_row(qraw + rowid(g, s, tok) * HD, g.scale * __expf(0.5f * li), qp);
+      gen_all_kblocks<0, NA>(qp, a_base, lane_off, a_full, a_empty, l);
     }
-    if (tid == 128) stamp(3);
     for (int J = 0; J <= I; ++J) {
       const int sb = J & 1;
       const bool diag = (J == I);
@@ -565,7 +538,6 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
       cj[sb * 128 + row] = diag ? ell_s[J * 128 + row] : __expf(lref - ell_s[J * 128 + row]);
       asm volatile("bar.sync 1, 128;" ::: "memory");
       mbar_wait(&s_full[sb], (J >> 1) & 1);
-      if (tid == 128 && J < 8) stamp(32 + J);
       tc_fence_after();
       const float ri = __expf(li - lref) * sig2;
       const float* cjs = cj + sb * 128;
@@ -616,9 +588,8 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
       tc_fence_before();
       __syncwarp();
       if (l == 0) mbar_arrive(&p_full[sb]);
-      if (tid == 128 && J < 8) stamp(40 + J);
     }
-    // ---------------- epilogue ----------------
+    // ---------------- epilogue -------------------------------------------
     mbar_wait(fin, 0);
     tc_fence_after();
     uint32_t o[64];
@@ -657,10 +628,633 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
                               __uint_as_float(o[c4 * 4 + 2]) * inv, __uint_as_float(o[c4 * 4 + 3]) * inv);
     }
   }
-  if (tid == 128) stamp(6);
   tc_fence_before();
   __syncthreads();
   if (w == 2) tmem_dealloc<512>(tm);
+}
+
+// ==========================================================================
+// BACKWARD
+// ==========================================================================
+// prep: normalization cotangents (gradients.py:381-386) in the layouts the
+// tensor-core kernels read: dN [ns*t][64] bf16 (dnum), dD [ns*t][16] bf16
+// (col 0 = dden), and dden [ns*t] fp32 for the intra-chunk kernels.
+__global__ void __launch_bounds__(256) k_tc_bwd_prep(Geo g, const __nv_bfloat16* __restrict__ dy,
+                                                     const float* __restrict__ y32,
+                                                     const float* __restrict__ rowsum, __nv_bfloat16* dN,
+                                                     __nv_bfloat16* dD, float* dden_out) {
+  const size_t it = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (it >= (size_t)g.ns * g.t) return;
+  const int s = (int)(it / g.t), m = (int)(it - (size_t)s * g.t);
+  const size_t r = rowid(g, s, m);
+  float R = 1.f, dot = 0.f;
+  if (g.normalize) R = rowsum[r];
+  const float inv = 1.f / R;
+  const uint4* src = (const uint4*)(dy + r * HD);
+  uint4* dst = (uint4*)(dN + it * HD);
+#pragma unroll
+  for (int c8 = 0; c8 < 8; ++c8) {
+    uint4 v4 = src[c8];
+    uint32_t* pv = (uint32_t*)&v4;
+#pragma unroll
+    for (int e2 = 0; e2 < 4; ++e2) {
+      float2 f2 = __bfloat1622float2(*(const __nv_bfloat162*)&pv[e2]);
+      const int u = c8 * 8 + e2 * 2;
+      if (g.normalize) dot += f2.x * y32[it * HD + u] + f2.y * y32[it * HD + u + 1];
+      f2.x *= inv;
+      f2.y *= inv;
+      pv[e2] = pack_bf16(f2.x, f2.y);
+    }
+    dst[c8] = v4;
+  }
+  const float dden = g.normalize ? -dot * inv : 0.f;
+  dden_out[it] = dden;
+  if (dD) {
+    uint4* dd = (uint4*)(dD + it * 16);
+    dd[0] = make_uint4(pack_bf16(dden, 0.f), 0u, 0u, 0u);
+    dd[1] = make_uint4(0u, 0u, 0u, 0u);
+  }
+}
+
+// backward scan (discumsum VJP, gradients.py:267-288) over chunk states:
+//   G_k = dA'_k + lambda_{k+1} G_{k+1};  dlambda_k = <A'_{k-1}, G_k>;  dS~_k = omega G_k
+// dA'_k comes from the feature-major GEMM (fp32, slot k holds dA'_k for k <= n-2).
+// thread per (slot, column); grid (ceil(FH*ucols/256), stream)
+__global__ void __launch_bounds__(256) k_tc_scan_bwd(Geo g, int ucols, const float* __restrict__ lamlog,
+                                                     const float* __restrict__ dA,
+                                                     const __nv_bfloat16* __restrict__ st_main,
+                                                     const __nv_bfloat16* __restrict__ st_den,
+                                                     __nv_bfloat16* ds_main, __nv_bfloat16* ds_den, float* dlam) {
+  __shared__ float red[32];
+  const int s = blockIdx.y;
+  const int e = blockIdx.x * 256 + threadIdx.x;
+  const bool ok = e < FH * ucols;
+  const int f = ok ? e / ucols : 0, u = ok ? e - f * ucols : 0;
+  const float om = ok ? slot_omega(f) : 0.f;
+  float G = 0.f;
+  for (int k = g.n - 1; k >= 0; --k) {
+    const float lam_next = (k + 1 < g.n) ? (g.gated ? __expf(lamlog[s * g.n + k + 1]) : 1.f) : 0.f;
+    const float dAk = (ok && k + 1 < g.n) ? dA[((size_t)(s * g.n + k) * FH + f) * UW + u] : 0.f;
+    G = dAk + lam_next * G;
+    if (ok) {
+      const __nv_bfloat16 v = __float2bfloat16_rn(om * G);
+      if (u < 64)
+        *(__nv_bfloat16*)((uint8_t*)(ds_main + (size_t)(s * g.n + k) * ST_MAIN) + sw128_elem(f, u)) = v;
+      else
+        *(__nv_bfloat16*)((uint8_t*)(ds_den + (size_t)(s * g.n + k) * ST_DEN) + sw32_elem(f, u - 64)) = v;
+    }
+    if (k >= 1) {
+      float a = 0.f;
+      if (ok) {
+        const __nv_bfloat16* src =
+            u < 64 ? (const __nv_bfloat16*)((const uint8_t*)(st_main + (size_t)(s * g.n + k - 1) * ST_MAIN) +
+                                            sw128_elem(f, u))
+                   : (const __nv_bfloat16*)((const uint8_t*)(st_den + (size_t)(s * g.n + k - 1) * ST_DEN) +
+                                            sw32_elem(f, u - 64));
+        a = __bfloat162float(*src) * G;
+      }
+      const float tot = block_sum(a, red);
+      if (threadIdx.x == 0 && g.gated) atomicAdd(dlam + s * g.n + k, tot);
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// token-major dphi GEMM + fused expand_vjp (gradients.py:46-76):
+//   query  (gradients.py:406-431): dphi'(q~) = [dnum|dden] A'^T_{k-1}
+//          -> dq += sigma e^{ell/2} dq~,  dell += dq~.q~ / 2
+//   update (gradients.py:191-213): dphi'(k~) = [v|1] dS~_k^T
+//          -> dk += e^{(lend-ell)/2} dk~, dell -= dk~.k~/2, dell_end += dk~.k~/2;
+//          then dv = phi'(k~) dS~_k (second GEMM, A generated into TMEM)
+// Warp roles as above.  TMEM: dphi buffers [0,256), dU [256,320), A [384,512).
+// grid (token tile of 128, chunk, stream)
+// --------------------------------------------------------------------------
+namespace dp {
+constexpr int AB = 128 * 128;    // A main tile (128 tok x 64)
+constexpr int A16 = 128 * 32;    // A score-sum tile (128 tok x 16)
+constexpr int BM = 128 * 128;    // B stage: 128 slots x 64
+constexpr int BD = 128 * 32;     // B stage score-sum part
+constexpr int NST = 4;
+constexpr int NA = 4;
+constexpr int NT = FH / 128;     // 18 dphi tiles
+constexpr int SMEM = 1024 + AB + A16 + NST * (BM + BD) + 256;
+}  // namespace dp
+
+template <int NTI>
+__device__ __forceinline__ void dphi_tiles(const float (&x)[64], float (&dx)[64], uint32_t dbase, uint32_t lane_off,
+                                           uint64_t* d_full, uint64_t* d_empty, int l) {
+  constexpr int db = NTI & 1;
+  mbar_wait(&d_full[db], (NTI >> 1) & 1);
+  tc_fence_after();
+#pragma unroll
+  for (int ch = 0; ch < 4; ++ch) {
+    uint32_t r[32];
+    tmem_ld32(dbase + (uint32_t)(db * 128) + lane_off + ch * 32, r);
+    tc_wait_ld();
+    if (ch == 0) evjp_fblock<NTI * 4 + 0>(x, dx, r);
+    if (ch == 1) evjp_fblock<NTI * 4 + 1>(x, dx, r);
+    if (ch == 2) evjp_fblock<NTI * 4 + 2>(x, dx, r);
+    if (ch == 3) evjp_fblock<NTI * 4 + 3>(x, dx, r);
+  }
+  tc_fence_before();
+  __syncwarp();
+  if (l == 0) mbar_arrive(&d_empty[db]);
+  if constexpr (NTI + 1 < dp::NT) dphi_tiles<NTI + 1>(x, dx, dbase, lane_off, d_full, d_empty, l);
+}
+
+template <bool kUpd>
+__global__ void __launch_bounds__(256, 1) k_tc_dphi(const __grid_constant__ CUtensorMap tm_a,
+                                                    const __grid_constant__ CUtensorMap tm_a16, Geo g,
+                                                    const __nv_bfloat16* __restrict__ xraw,
+                                                    const float* __restrict__ ell,
+                                                    const float* __restrict__ lamlog,
+                                                    const __nv_bfloat16* __restrict__ b_main,
+                                                    const __nv_bfloat16* __restrict__ b_den, int with_den,
+                                                    float* dx32, float* dv32, float* dell, float* dellend) {
+  using namespace dp;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* a_s = smem;
+  uint8_t* a16_s = a_s + AB;
+  uint8_t* bm_s = a16_s + A16;
+  uint8_t* bd_s = bm_s + NST * BM;
+  uint64_t* bars = (uint64_t*)(bd_s + NST * BD);
+  uint64_t* a_ready = bars;              // 1 (TMA tx + 4 compute-warp arrivals)
+  uint64_t* b_full = a_ready + 1;        // NST
+  uint64_t* b_empty = b_full + NST;      // NST
+  uint64_t* d_full = b_empty + NST;      // 2
+  uint64_t* d_empty = d_full + 2;        // 2
+  uint64_t* g_full = d_empty + 2;        // NA
+  uint64_t* g_empty = g_full + NA;       // NA
+  uint64_t* fin = g_empty + NA;          // 1
+  __shared__ uint32_t tmem_base;
+  __shared__ float red_s[4];
+
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  const int I = blockIdx.x, k = blockIdx.y + (kUpd ? 0 : 1), s = blockIdx.z;
+  const int bi = s / g.h, hi = s % g.h;
+  const int tok0 = k * g.c + I * 128;
+  const bool den = with_den != 0;
+  const int bslot = kUpd ? k : k - 1;    // state index the B operand comes from
+  const __nv_bfloat16* bm = b_main + (size_t)(s * g.n + bslot) * ST_MAIN;
+  const __nv_bfloat16* bd = b_den + (size_t)(s * g.n + bslot) * ST_DEN;
+
+  if (w == 2) tmem_alloc<512>(&tmem_base);
+  if (tid == 0) {
+    mbar_init(a_ready, 5);
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&b_full[i], 1);
+      mbar_init(&b_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&d_full[i], 1);
+      mbar_init(&d_empty[i], 4);
+    }
+    for (int i = 0; i < NA; ++i) {
+      mbar_init(&g_full[i], 4);
+      mbar_init(&g_empty[i], 1);
+    }
+    mbar_init(fin, 1);
+    fence_barrier_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tmem_base;
+
+  if (w == 0) {
+    if (l == 0) {
+      tma_prefetch(&tm_a);
+      mbar_expect_tx(a_ready, AB + ((!kUpd && den) ? A16 : 0));
+      if (kUpd) {
+        tma_load_4d(a_s, &tm_a, a_ready, 0, hi, tok0, bi);
+      } else {
+        tma_load_2d(a_s, &tm_a, a_ready, 0, s * g.t + tok0);
+        if (den) tma_load_2d(a16_s, &tm_a16, a_ready, 0, s * g.t + tok0);
+      }
+      int j = 0;
+      auto stage = [&](const __nv_bfloat16* m, uint32_t mb, const __nv_bfloat16* d, uint32_t dbytes) {
+        const int st = j % NST;
+        if (j >= NST) mbar_wait(&b_empty[st], ((j / NST) + 1) & 1);
+        mbar_expect_tx(&b_full[st], mb + dbytes);
+        bulk_load(bm_s + st * BM, m, mb, &b_full[st]);
+        if (dbytes) bulk_load(bd_s + st * BD, d, dbytes, &b_full[st]);
+        ++j;
+      };
+      for (int nt = 0; nt < NT; ++nt) stage(bm + (size_t)nt * 128 * 64, BM, bd + (size_t)nt * 128 * 16, den ? BD : 0);
+      if (kUpd)
+        for (int kb = 0; kb < NKB; ++kb) stage(bm + (size_t)kb * 64 * 64, 64 * 128, nullptr, 0);
+    }
+  } else if (w == 1) {
+    if (l == 0) {
+      const uint32_t id128 = idesc_bf16(128, 128, false, false);
+      const uint32_t id64mn = idesc_bf16(128, 64, false, true);
+      mbar_wait(a_ready, 0);
+      tc_fence_after();
+      const uint32_t am = smem_u32(a_s), a16 = smem_u32(a16_s);
+      int j = 0;
+      for (int nt = 0; nt < NT; ++nt, ++j) {
+        const int st = j % NST, db = nt & 1;
+        mbar_wait(&b_full[st], (j / NST) & 1);
+        if (nt >= 2) mbar_wait(&d_empty[db], ((nt >> 1) + 1) & 1);
+        tc_fence_after();
+        const uint32_t bmm = smem_u32(bm_s + st * BM), bdd = smem_u32(bd_s + st * BD);
+        const uint32_t dt = tm + (uint32_t)(db * 128);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          mma_ss(dt, smem_desc(am + kk * 32, 16, 1024, 2), smem_desc(bmm + kk * 32, 16, 1024, 2), id128,
+                 kk > 0 ? 1u : 0u);
+        if (den) mma_ss(dt, smem_desc(a16, 16, 256, 6), smem_desc(bdd, 16, 256, 6), id128, 1u);
+        tc_commit(&d_full[db]);
+        tc_commit(&b_empty[st]);
+      }
+      if (kUpd) {
+        for (int kb = 0; kb < NKB; ++kb, ++j) {
+          const int st = j % NST, bb = kb % NA;
+          mbar_wait(&g_full[bb], (kb / NA) & 1);
+          mbar_wait(&b_full[st], (j / NST) & 1);
+          tc_fence_after();
+          const uint32_t bmm = smem_u32(bm_s + st * BM);
+          const uint32_t ab = tm + 384u + (uint32_t)(bb * 32);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_ts(tm + 256u, ab + kk * 8, smem_desc(bmm + kk * 2048, 8192, 1024, 2), id64mn,
+                   (kb > 0 || kk > 0) ? 1u : 0u);
+          tc_commit(&g_empty[bb]);
+          tc_commit(&b_empty[st]);
+        }
+      }
+      tc_commit(fin);
+    }
+  } else if (w >= 4) {
+    const int q = w & 3, row = q * 32 + l;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const int tok = tok0 + row;
+    const float lt = ell[(size_t)s * g.t + tok];
+    // this token's scaled row: q~ = sigma e^{ell/2} q  or  k~ = e^{(lend-ell)/2} k (bf16-rounded as in the forward)
+    const float fsc = kUpd ? (g.gated ? __expf(0.5f * (lamlog[s * g.n + k] - lt)) : 1.f)
+                           : g.scale * __expf(0.5f * lt);
+    uint32_t xp[32];
+    load_scaled_row(xraw + rowid(g, s, tok) * HD, fsc, xp);
+    if (kUpd && den) {
+      // A score-sum tile for the update side: [v | 1]: row = token, column 0 = 1 (SW32 layout)
+      uint32_t* rowp = (uint32_t*)(a16_s + (size_t)row * 32);
+      for (int i = 0; i < 8; ++i) rowp[i] = 0u;
+      *(__nv_bfloat16*)(a16_s + sw32_elem(row, 0)) = __float2bfloat16_rn(1.f);
+      fence_async_smem();
+    }
+    __syncwarp();
+    if (l == 0) mbar_arrive(a_ready);
+    float x[64], dx[64];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const float2 f2 = __bfloat1622float2(*(const __nv_bfloat162*)&xp[i]);
+      x[2 * i] = f2.x;
+      x[2 * i + 1] = f2.y;
+      dx[2 * i] = 0.f;
+      dx[2 * i + 1] = 0.f;
+    }
+    dphi_tiles<0>(x, dx, tm, lane_off, d_full, d_empty, l);
+    float c = 0.f;
+#pragma unroll
+    for (int a = 0; a < 64; ++a) c = fmaf(dx[a], x[a], c);
+    c *= 0.5f;
+    float* o = dx32 + ((size_t)s * g.t + tok) * HD;
+    if (!kUpd) {
+      const float sc = g.scale * __expf(0.5f * lt);
+#pragma unroll
+      for (int a = 0; a < 64; a += 4) {
+        float4 v = *(float4*)(o + a);
+        v.x += dx[a] * sc;
+        v.y += dx[a + 1] * sc;
+        v.z += dx[a + 2] * sc;
+        v.w += dx[a + 3] * sc;
+        *(float4*)(o + a) = v;
+      }
+      if (g.gated) dell[(size_t)s * g.t + tok] += c;
+    } else {
+#pragma unroll
+      for (int a = 0; a < 64; a += 4) {
+        float4 v = *(float4*)(o + a);
+        v.x += dx[a] * fsc;
+        v.y += dx[a + 1] * fsc;
+        v.z += dx[a + 2] * fsc;
+        v.w += dx[a + 3] * fsc;
+        *(float4*)(o + a) = v;
+      }
+      // suffix-decay cotangent: -c on ell_tok and +c on ell_end; summed over the
+      // chunk this is an exclusive prefix sum (no cancellation), done in gate_finish
+      if (g.gated) dellend[(size_t)s * g.t + tok] = c;
+      // second GEMM: dU = phi'(k~) dS~  (A generated, 36 K blocks)
+      gen_all_kblocks<0, NA>(xp, tm + 384u, lane_off, g_full, g_empty, l);
+      mbar_wait(fin, 0);
+      tc_fence_after();
+      uint32_t r[64];
+      tmem_ld32(tm + 256u + lane_off, r);
+      tmem_ld32(tm + 256u + lane_off + 32, r + 32);
+      tc_wait_ld();
+      float* ov = dv32 + ((size_t)s * g.t + tok) * HD;
+#pragma unroll
+      for (int a = 0; a < 64; a += 4) {
+        float4 v = *(float4*)(ov + a);
+        v.x += __uint_as_float(r[a]);
+        v.y += __uint_as_float(r[a + 1]);
+        v.z += __uint_as_float(r[a + 2]);
+        v.w += __uint_as_float(r[a + 3]);
+        *(float4*)(ov + a) = v;
+      }
+    }
+    (void)red_s;
+  }
+  if (!kUpd && w >= 4) {
+    // query side has no second GEMM; fin still closes the MMA stream
+    mbar_wait(fin, 0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (w == 2) tmem_dealloc<512>(tm);
+}
+
+// --------------------------------------------------------------------------
+// intra-chunk backward on tcgen05 (gradients.py:98-176 power branch, with the
+// pairwise-decay rule 79-95 in log space):
+//   P = E sig^2 s^2,  dP' = dnum.v + dden,  dS = dP' E 2 sig^2 s   (s = q.k raw)
+//   key side  : dV_J += P^T dnum_I, dK_J += dS^T Q_I, dell_j -= sum_i dP' P
+//   query side: dQ_I += dS K_J,                       dell_i += sum_j dP' P
+// E_ij = exp(ell_i - ell_j): exact per element on the diagonal block,
+// factored r_i c_j (both <= 1) off it.
+// --------------------------------------------------------------------------
+namespace ib {
+constexpr int T128 = 128 * 128;   // one 128-token x 64 bf16 tile
+constexpr int NST = 2;            // streamed-tile stages
+constexpr int SMEM = 1024 + 2 * T128 + NST * 2 * T128 + 4096 + 2048 + 512;
+}  // namespace ib
+
+// kKV = true: one CTA per key block J, loops query blocks I = J..nq-1.
+// kKV = false: one CTA per query block I, loops key blocks J = 0..I.
+template <bool kKV>
+__global__ void __launch_bounds__(256, 1) k_tc_intra_bwd(const __grid_constant__ CUtensorMap tm_q,
+                                                         const __grid_constant__ CUtensorMap tm_k,
+                                                         const __grid_constant__ CUtensorMap tm_v,
+                                                         const __grid_constant__ CUtensorMap tm_dn, Geo g,
+                                                         const float* __restrict__ ell,
+                                                         const float* __restrict__ dden, float* out_a,
+                                                         float* out_b, float* dell) {
+  using namespace ib;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  // fixed tiles: kKV: K_J, V_J   | q-side: Q_I, dN_I
+  uint8_t* f0 = smem;
+  uint8_t* f1 = f0 + T128;
+  // streamed tiles per stage: kKV: Q_I, dN_I | q-side: K_J, V_J
+  uint8_t* s0 = f1 + T128;
+  float* ell_s = (float*)(s0 + NST * 2 * T128);   // [1024]
+  float* sc = ell_s + 1024;                        // [2][128] per-column decay factor
+  float* sd = sc + 256;                            // [2][128] per-column dden (kKV)
+  uint64_t* bars = (uint64_t*)(sd + 256);
+  uint64_t* f_full = bars;            // 1
+  uint64_t* t_full = f_full + 1;      // NST
+  uint64_t* t_empty = t_full + NST;   // NST
+  uint64_t* s_full = t_empty + NST;   // 1  (S and dP of the current block)
+  uint64_t* pd_full = s_full + 1;     // 1  (P/dS written, S/dP consumed)
+  uint64_t* pd_free = pd_full + 1;    // 1  (gradient MMAs of the block done)
+  uint64_t* fin = pd_free + 1;        // 1
+  __shared__ uint32_t tmem_base;
+
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  const int B0 = blockIdx.x, k = blockIdx.y, s = blockIdx.z;
+  const int bi = s / g.h, hi = s % g.h;
+  const int c0 = k * g.c, nq = g.c / 128;
+  const int first = kKV ? B0 : 0, last = kKV ? nq - 1 : B0;
+  const int nblk = last - first + 1;
+
+  if (w == 2) tmem_alloc<512>(&tmem_base);
+  if (tid == 0) {
+    mbar_init(f_full, 1);
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&t_full[i], 1);
+      mbar_init(&t_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(pd_full, 4);
+    mbar_init(pd_free, 1);
+    mbar_init(fin, 1);
+    fence_barrier_init();
+  }
+  for (int i = tid; i < g.c; i += 256) ell_s[i] = ell[(size_t)s * g.t + c0 + i];
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tmem_base;
+  // TMEM: S [0,128) dP [128,256) P [256,320) dS [320,384) acc_a [384,448) acc_b [448,512)
+  const uint32_t tS = tm, tDP = tm + 128, tP = tm + 256, tDS = tm + 320, tA = tm + 384, tB = tm + 448;
+
+  if (w == 0) {
+    if (l == 0) {
+      tma_prefetch(&tm_q);
+      tma_prefetch(&tm_k);
+      tma_prefetch(&tm_v);
+      tma_prefetch(&tm_dn);
+      mbar_expect_tx(f_full, 2 * T128);
+      if (kKV) {
+        tma_load_4d(f0, &tm_k, f_full, 0, hi, c0 + B0 * 128, bi);
+        tma_load_4d(f1, &tm_v, f_full, 0, hi, c0 + B0 * 128, bi);
+      } else {
+        tma_load_4d(f0, &tm_q, f_full, 0, hi, c0 + B0 * 128, bi);
+        tma_load_2d(f1, &tm_dn, f_full, 0, s * g.t + c0 + B0 * 128);
+      }
+      for (int it = 0; it < nblk; ++it) {
+        const int X = first + it, st = it % NST;
+        if (it >= NST) mbar_wait(&t_empty[st], ((it / NST) + 1) & 1);
+        mbar_expect_tx(&t_full[st], 2 * T128);
+        uint8_t* d0 = s0 + st * 2 * T128;
+        if (kKV) {
+          tma_load_4d(d0, &tm_q, &t_full[st], 0, hi, c0 + X * 128, bi);
+          tma_load_2d(d0 + T128, &tm_dn, &t_full[st], 0, s * g.t + c0 + X * 128);
+        } else {
+          tma_load_4d(d0, &tm_k, &t_full[st], 0, hi, c0 + X * 128, bi);
+          tma_load_4d(d0 + T128, &tm_v, &t_full[st], 0, hi, c0 + X * 128, bi);
+        }
+      }
+    }
+  } else if (w == 1) {
+    if (l == 0) {
+      const uint32_t id128 = idesc_bf16(128, 128, false, false);
+      const uint32_t id64mn = idesc_bf16(128, 64, false, true);
+      mbar_wait(f_full, 0);
+      const uint32_t F0 = smem_u32(f0), F1 = smem_u32(f1);
+      for (int it = 0; it < nblk; ++it) {
+        const int st = it % NST;
+        mbar_wait(&t_full[st], (it / NST) & 1);
+        if (it >= 1) mbar_wait(pd_full, (it - 1) & 1);   // S/dP of the previous block consumed
+        tc_fence_after();
+        const uint32_t T0 = smem_u32(s0 + st * 2 * T128), T1 = T0 + T128;
+        // S (or S^T) and dP (or dP^T): kKV rows = keys: A = K_J / V_J, B = Q_I / dN_I
+        //                               q-side rows = queries: A = Q_I / dN_I, B = K_J / V_J
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          mma_ss(tS, smem_desc(F0 + kk * 32, 16, 1024, 2), smem_desc(T0 + kk * 32, 16, 1024, 2), id128, kk > 0);
+          mma_ss(tDP, smem_desc(F1 + kk * 32, 16, 1024, 2), smem_desc(T1 + kk * 32, 16, 1024, 2), id128, kk > 0);
+        }
+        tc_commit(s_full);
+        // gradient MMAs of this block once P / dS are in TMEM
+        mbar_wait(pd_full, it & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t f = (it > 0 || kk > 0) ? 1u : 0u;
+          if (kKV) {
+            mma_ts(tB, tP + kk * 8, smem_desc(T1 + kk * 2048, 8192, 1024, 2), id64mn, f);   // dV += P^T dN
+            mma_ts(tA, tDS + kk * 8, smem_desc(T0 + kk * 2048, 8192, 1024, 2), id64mn, f);  // dK += dS^T Q
+          } else {
+            mma_ts(tA, tDS + kk * 8, smem_desc(T0 + kk * 2048, 8192, 1024, 2), id64mn, f);  // dQ += dS K
+          }
+        }
+        tc_commit(pd_free);
+        tc_commit(&t_empty[st]);
+      }
+      tc_commit(fin);
+    }
+  } else if (w >= 4) {
+    const int q = w & 3, row = q * 32 + l;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const float sig2 = g.scale * g.scale;
+    const float l_own = ell_s[B0 * 128 + row];
+    const float dden_own = kKV ? 0.f : dden[(size_t)s * g.t + c0 + B0 * 128 + row];
+    float red = 0.f;  // kKV: col sum of dP'P (-> -dell_j); q-side: row sum (-> +dell_i)
+    for (int it = 0; it < nblk; ++it) {
+      const int X = first + it, sb = it & 1;
+      const bool diag = (X == B0);
+      // per-column factors of block X (columns = the streamed tokens)
+      const int J = kKV ? B0 : X;                      // key block of this (I, J) pair
+      const float lref = ell_s[J * 128 + 127];
+      const float lcol = ell_s[X * 128 + row];
+      if (kKV) {
+        sc[sb * 128 + row] = diag ? lcol : __expf(lcol - lref);        // r_i for query column i
+        sd[sb * 128 + row] = dden[(size_t)s * g.t + c0 + X * 128 + row];
+      } else {
+        sc[sb * 128 + row] = diag ? lcol : __expf(lref - lcol);        // c_j for key column j
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      // own-row factor
+      const float fo = kKV ? __expf(lref - l_own) : __expf(l_own - lref);  // c_j (keys) or r_i (queries)
+      mbar_wait(s_full, it & 1);
+      if (it >= 1) mbar_wait(pd_free, (it - 1) & 1);   // P/dS regions free again
+      tc_fence_after();
+      const float* scs = sc + sb * 128;
+      const float* sds = sd + sb * 128;
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        uint32_t rs[32], rd[32], pp[16], pdsv[16];
+        tmem_ld32(tS + lane_off + ch * 32, rs);
+        tmem_ld32(tDP + lane_off + ch * 32, rd);
+        tc_wait_ld();
+#pragma unroll
+        for (int e2 = 0; e2 < 16; ++e2) {
+          float pv[2], dv[2];
+#pragma unroll
+          for (int z = 0; z < 2; ++z) {
+            const int col = ch * 32 + e2 * 2 + z;
+            const float sv = __uint_as_float(rs[e2 * 2 + z]);
+            const float dd = kKV ? sds[col] : dden_own;
+            const float dpv = __uint_as_float(rd[e2 * 2 + z]) + dd;
+            float E;
+            if (diag) {
+              // kKV: row = key j, col = query i (valid i >= j); q-side: row = query i, col = key j (j <= i)
+              const bool valid = kKV ? (col >= row) : (col <= row);
+              const float li = kKV ? scs[col] : l_own, lj = kKV ? l_own : scs[col];
+              E = valid ? __expf(fminf(li - lj, 0.f)) : 0.f;
+            } else {
+              E = fo * scs[col];
+            }
+            const float P = E * sig2 * sv * sv;
+            red = fmaf(dpv, P, red);
+            pv[z] = P;
+            dv[z] = dpv * E * 2.f * sig2 * sv;
+          }
+          pp[e2] = pack_bf16(pv[0], pv[1]);
+          pdsv[e2] = pack_bf16(dv[0], dv[1]);
+        }
+        if (kKV) tmem_st16(tP + lane_off + ch * 16, pp);
+        tmem_st16(tDS + lane_off + ch * 16, pdsv);
+      }
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (l == 0) mbar_arrive(pd_full);
+    }
+    // epilogue: accumulate gradients (fp32, stream-major) and the gate cotangent
+    mbar_wait(fin, 0);
+    tc_fence_after();
+    const size_t tokr = (size_t)s * g.t + c0 + B0 * 128 + row;
+    uint32_t r[64];
+    tmem_ld32(tA + lane_off, r);
+    tmem_ld32(tA + lane_off + 32, r + 32);
+    tc_wait_ld();
+    float* oa = out_a + tokr * HD;
+#pragma unroll
+    for (int a = 0; a < 64; a += 4) {
+      float4 v4 = *(float4*)(oa + a);
+      v4.x += __uint_as_float(r[a]);
+      v4.y += __uint_as_float(r[a + 1]);
+      v4.z += __uint_as_float(r[a + 2]);
+      v4.w += __uint_as_float(r[a + 3]);
+      *(float4*)(oa + a) = v4;
+    }
+    if (kKV) {
+      tmem_ld32(tB + lane_off, r);
+      tmem_ld32(tB + lane_off + 32, r + 32);
+      tc_wait_ld();
+      float* ob = out_b + tokr * HD;
+#pragma unroll
+      for (int a = 0; a < 64; a += 4) {
+        float4 v4 = *(float4*)(ob + a);
+        v4.x += __uint_as_float(r[a]);
+        v4.y += __uint_as_float(r[a + 1]);
+        v4.z += __uint_as_float(r[a + 2]);
+        v4.w += __uint_as_float(r[a + 3]);
+        *(float4*)(ob + a) = v4;
+      }
+    }
+    if (g.gated) dell[tokr] += kKV ? -red : red;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (w == 2) tmem_dealloc<512>(tm);
+}
+
+// gate finish (gradients.py:79-95, 245-264 in log space), one warp per chunk:
+//   dlog g_u = sum_{m >= u} dell_m + dlam_k lam_k + sum_{m < u} cu_m
+__global__ void __launch_bounds__(128) k_tc_gate_finish(Geo g, const float* __restrict__ lamlog,
+                                                        const float* __restrict__ dell, const float* __restrict__ cu,
+                                                        const float* __restrict__ dlam, float* dlogg) {
+  const int wid = blockIdx.x * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (wid >= g.ns * g.n) return;
+  const int s = wid / g.n, k = wid - s * g.n;
+  const int s0 = k * g.c, s1 = s0 + g.c;
+  const float base = k >= 1 ? dlam[wid] * __expf(lamlog[wid]) : 0.f;
+  // pass 1: prefix of cu (exclusive) and suffix of dell (inclusive) in 32-token steps
+  float tot_dell = 0.f;
+  for (int m0 = s0; m0 < s1; m0 += 32) tot_dell += warp_sum(dell[(size_t)s * g.t + m0 + lane]);
+  float carry_c = 0.f, carry_d = 0.f;  // sum of cu before this step, sum of dell before this step
+  for (int m0 = s0; m0 < s1; m0 += 32) {
+    const size_t i = (size_t)s * g.t + m0 + lane;
+    float xc = cu[i], xd = dell[i];
+    float ic = xc, id = xd;  // inclusive scans
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const float yc = __shfl_up_sync(0xffffffffu, ic, o), yd = __shfl_up_sync(0xffffffffu, id, o);
+      if (lane >= o) {
+        ic += yc;
+        id += yd;
+      }
+    }
+    const float excl_c = carry_c + ic - xc;        // sum_{m < u} cu_m
+    const float suff_d = tot_dell - (carry_d + id - xd);  // sum_{m >= u} dell_m
+    dlogg[rowid(g, s, m0 + lane)] = suff_d + base + excl_c;
+    carry_c += __shfl_sync(0xffffffffu, ic, 31);
+    carry_d += __shfl_sync(0xffffffffu, id, 31);
+  }
 }
 
 // ==========================================================================
@@ -670,32 +1264,70 @@ struct TcFwdWs {
   int* zflag;
   float* ell;
   float* lamlog;
-  __nv_bfloat16* kt;
-  float* sp;
-  __nv_bfloat16* st;
+  __nv_bfloat16* kt;     // K~^T  [ns*n*64][c]  (reused for Q~^T in the backward)
+  float* sp;             // S'_k fp32 [ns][n][FH][80] (reused for dA' in the backward)
+  __nv_bfloat16* stm;    // A'_k [ns][n][FH][64]
+  __nv_bfloat16* std_;   // A'_k score-sum part [ns][n][FH][16]
   float* y32;
+};
+
+struct TcBwdWs {
+  __nv_bfloat16* dN;
+  __nv_bfloat16* dD;
+  float* dden;
+  __nv_bfloat16* dsm;
+  __nv_bfloat16* dsd;
+  float* dq32;
+  float* dk32;
+  float* dv32;
+  float* dell;
+  float* cu;
+  float* dlam;
 };
 
 static size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
 
-static TcFwdWs carve_fwd(const Geo& g, void* base, size_t* bytes) {
-  char* p = (char*)base;
+struct Take {
+  char* p;
   size_t off = 0;
-  auto take = [&](size_t n) {
+  void* operator()(size_t n) {
     void* r = p ? p + off : nullptr;
     off += a256(n);
     return r;
-  };
+  }
+};
+
+static TcFwdWs carve_fwd(const Geo& g, void* base, size_t* bytes) {
+  Take take{(char*)base};
   TcFwdWs w;
   w.zflag = (int*)take(4);
   w.ell = (float*)take(sizeof(float) * g.ns * g.t);
   w.lamlog = (float*)take(sizeof(float) * g.ns * g.n);
   w.kt = (__nv_bfloat16*)take(2ull * g.ns * g.t * HD);
   w.sp = (float*)take(4ull * g.ns * g.n * FH * UW);
-  w.st = (__nv_bfloat16*)take(2ull * g.ns * g.n * NFB * UW * 64);
+  w.stm = (__nv_bfloat16*)take(2ull * g.ns * g.n * ST_MAIN);
+  w.std_ = (__nv_bfloat16*)take(2ull * g.ns * g.n * ST_DEN);
   w.y32 = (float*)take(g.normalize ? 4ull * g.ns * g.t * HD : 0);
-  *bytes = off;
+  *bytes = take.off;
   return w;
+}
+
+static TcBwdWs carve_bwd(const Geo& g, void* base, size_t* bytes) {
+  Take take{(char*)base};
+  TcBwdWs b;
+  b.dN = (__nv_bfloat16*)take(2ull * g.ns * g.t * HD);
+  b.dD = (__nv_bfloat16*)take(2ull * g.ns * g.t * 16);
+  b.dden = (float*)take(4ull * g.ns * g.t);
+  b.dsm = (__nv_bfloat16*)take(2ull * g.ns * g.n * ST_MAIN);
+  b.dsd = (__nv_bfloat16*)take(2ull * g.ns * g.n * ST_DEN);
+  b.dq32 = (float*)take(4ull * g.ns * g.t * HD);
+  b.dk32 = (float*)take(4ull * g.ns * g.t * HD);
+  b.dv32 = (float*)take(4ull * g.ns * g.t * HD);
+  b.dell = (float*)take(4ull * g.ns * g.t);
+  b.cu = (float*)take(4ull * g.ns * g.t);
+  b.dlam = (float*)take(4ull * g.ns * g.n);
+  *bytes = take.off;
+  return b;
 }
 
 bool tc_supported(const Geo& g, int dtype) {
@@ -710,6 +1342,11 @@ bool tc_supported(const Geo& g, int dtype) {
 size_t tc_fwd_workspace_bytes(const Geo& g) {
   size_t n;
   carve_fwd(g, nullptr, &n);
+  return n;
+}
+size_t tc_bwd_workspace_bytes(const Geo& g) {
+  size_t n;
+  carve_bwd(g, nullptr, &n);
   return n;
 }
 
@@ -730,84 +1367,27 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
-static bool make_map_4d(CUtensorMap* m, const void* ptr, const Geo& g, int box_tokens) {
-  // [b][t][h][64] bf16: dims inner -> outer {64, h, t, b}
+static bool encode(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
+                   const cuuint32_t* box, CUtensorMapSwizzle sw) {
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  EncodeTiledFn fn = encode_fn();
+  return fn && fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// [b][t][h][64] bf16, box of `box_tokens` tokens of one (b, h) stream
+static bool map_bth(CUtensorMap* m, const void* ptr, const Geo& g, int box_tokens) {
   cuuint64_t dims[4] = {(cuuint64_t)HD, (cuuint64_t)g.h, (cuuint64_t)g.t, (cuuint64_t)g.b};
   cuuint64_t strides[3] = {(cuuint64_t)HD * 2, (cuuint64_t)g.h * HD * 2, (cuuint64_t)g.t * g.h * HD * 2};
   cuuint32_t box[4] = {64, 1, (cuuint32_t)box_tokens, 1};
-  cuuint32_t es[4] = {1, 1, 1, 1};
-  return encode_fn() && encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box,
-                                es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  return encode(m, ptr, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
-
-static bool make_map_xt(CUtensorMap* m, const void* ptr, const Geo& g) {
-  // [ns*n*64 rows][c tokens] bf16, box 64 tokens x 64 rows
-  cuuint64_t dims[2] = {(cuuint64_t)g.c, (cuuint64_t)g.ns * g.n * HD};
-  cuuint64_t strides[1] = {(cuuint64_t)g.c * 2};
-  cuuint32_t box[2] = {64, 64};
-  cuuint32_t es[2] = {1, 1};
-  return encode_fn() && encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
-                                es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-// PA_DEBUG_TIMING=1: per-CTA globaltimer stamps of k_tc_out (investigation aid)
-static unsigned long long* g_dbg = nullptr;
-static size_t g_dbg_n = 0;
-static unsigned long long* dbg_buf(const Geo& g) {
-  static const bool on = [] {
-    const char* e = getenv("PA_DEBUG_TIMING");
-    return e && e[0] == '1';
-  }();
-  if (!on) return nullptr;
-  size_t n = (size_t)(g.c / 128) * g.n * g.ns * 64;
-  if (n > g_dbg_n) {
-    if (g_dbg) cudaFree(g_dbg);
-    cudaMalloc(&g_dbg, n * 8);
-    g_dbg_n = n;
-  }
-  cudaMemset(g_dbg, 0, n * 8);
-  return g_dbg;
-}
-static void dbg_report(const Geo& g, cudaStream_t st) {
-  if (!g_dbg) return;
-  cudaStreamSynchronize(st);
-  size_t ncta = (size_t)(g.c / 128) * g.n * g.ns;
-  std::vector<unsigned long long> h(ncta * 64);
-  cudaMemcpy(h.data(), g_dbg, h.size() * 8, cudaMemcpyDeviceToHost);
-  double acc[8] = {0};
-  unsigned long long tmin = ~0ull, tmax = 0;
-  for (size_t c = 0; c < ncta; ++c) {
-    unsigned long long* r = &h[c * 64];
-    tmin = std::min(tmin, r[0]);
-    tmax = std::max(tmax, r[6]);
-    for (int i = 1; i <= 6; ++i) acc[i] += (double)(r[i] - r[0]);
-  }
-  fprintf(stderr, "[k_tc_out] ctas %zu span %.3f ms; mean since start (us): mmaA_done %.2f fin_issued %.2f genA_done %.2f loopB_done %.2f fin_seen %.2f end %.2f\n",
-          ncta, (tmax - tmin) * 1e-6, acc[1] / ncta * 1e-3, acc[2] / ncta * 1e-3, acc[3] / ncta * 1e-3,
-          acc[4] / ncta * 1e-3, acc[5] / ncta * 1e-3, acc[6] / ncta * 1e-3);
-  // per query-tile index I averages
-  for (int I = 0; I < g.c / 128; ++I) {
-    double a = 0, b = 0;
-    size_t cnt = 0;
-    for (size_t c = I; c < ncta; c += g.c / 128) {
-      a += (double)(h[c * 64 + 6] - h[c * 64 + 0]);
-      b += (double)(h[c * 64 + 3] - h[c * 64 + 0]);
-      ++cnt;
-    }
-    fprintf(stderr, "   I=%d mean total %.2f us, genA %.2f us\n", I, a / cnt * 1e-3, b / cnt * 1e-3);
-  }
-  // detailed phase-B timeline of the I=7 CTAs (first stream/chunk with k>=1)
-  for (size_t c = 7 + (size_t)(g.c / 128); c < ncta && c < 7 + 3 * (size_t)(g.c / 128); c += g.c / 128) {
-    unsigned long long* r = &h[c * 64];
-    fprintf(stderr, "   cta %zu (us from start): mmaA_done %.2f\n", c, (r[1] - r[0]) * 1e-3);
-    for (int J = 0; J < 8; ++J)
-      fprintf(stderr, "     J=%d kv_issue %.2f S_issued %.2f s_full_seen %.2f p_arrive %.2f p_seen %.2f\n", J,
-              ((long long)(r[8 + J] - r[0])) * 1e-3, ((long long)(r[16 + J] - r[0])) * 1e-3,
-              ((long long)(r[32 + J] - r[0])) * 1e-3, ((long long)(r[40 + J] - r[0])) * 1e-3,
-              ((long long)(r[24 + J] - r[0])) * 1e-3);
-  }
+// row-major [rows][cols] bf16 with a box of bc x br
+static bool map_2d(CUtensorMap* m, const void* ptr, size_t rows, int cols, int bc, int br, CUtensorMapSwizzle sw) {
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)bc, (cuuint32_t)br};
+  return encode(m, ptr, 2, dims, strides, box, sw);
 }
 
 int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const float* log_g, void* y, float* rowsum,
@@ -816,8 +1396,8 @@ int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const 
   TcFwdWs w = carve_fwd(g, ws, &need);
   const int with_den = (g.normalize || rowsum) ? 1 : 0;
   CUtensorMap m_q, m_k, m_v, m_v64, m_kt;
-  if (!make_map_4d(&m_q, q, g, 128) || !make_map_4d(&m_k, k, g, 128) || !make_map_4d(&m_v, v, g, 128) ||
-      !make_map_4d(&m_v64, v, g, 64) || !make_map_xt(&m_kt, w.kt, g)) {
+  if (!map_bth(&m_q, q, g, 128) || !map_bth(&m_k, k, g, 128) || !map_bth(&m_v, v, g, 128) ||
+      !map_bth(&m_v64, v, g, 64) || !map_2d(&m_kt, w.kt, (size_t)g.ns * g.n * HD, g.c, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B)) {
     set_error("cuTensorMapEncodeTiled failed");
     return 3;
   }
@@ -835,46 +1415,107 @@ int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const 
   }
   {
     StageTimer tmr("fwd_discumsum", st);
-    k_tc_scan_fwd<<<dim3(NFB, g.ns), 256, 0, st>>>(g, with_den ? UW : 64, w.lamlog, w.sp, w.st);
+    const int uc = with_den ? UW : 64;
+    k_tc_scan_fwd<<<dim3((FH * uc + 255) / 256, g.ns), 256, 0, st>>>(g, uc, w.lamlog, w.sp, w.stm, w.std_);
   }
   {
     StageTimer tmr("fwd_attn_query", st);
     cudaFuncSetAttribute(k_tc_out, cudaFuncAttributeMaxDynamicSharedMemorySize, outk::SMEM);
     k_tc_out<<<dim3(g.c / 128, g.n, g.ns), 256, outk::SMEM, st>>>(m_q, m_k, m_v, g, (const __nv_bfloat16*)q, w.ell,
-                                                                  w.st, with_den, (__nv_bfloat16*)y, rowsum, w.y32,
-                                                                  w.zflag, dbg_buf(g));
+                                                                  w.stm, w.std_, with_den, (__nv_bfloat16*)y, rowsum,
+                                                                  w.y32, w.zflag);
   }
-  dbg_report(g, st);
   count_launch(5);
   return cuda_check("tc forward");
 }
 
-// backward (interim): recompute the forward with the fp32 CUDA-core kernels
-// into the backward workspace and run their backward.  The tensor-core
-// backward replaces this.
-size_t tc_bwd_workspace_bytes(const Geo& g) {
-  return simt_fwd_bytes(g) + simt_bwd_bytes(g) + a256(4ull * g.ns * g.t) + a256(2ull * g.ns * g.t * g.e);
-}
-
 int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const float* log_g, const void* y,
-                const float* rowsum, const void* dy, void* dq, void* dk, void* dv, float* dlog_g, const void*,
+                const float* rowsum, const void* dy, void* dq, void* dk, void* dv, float* dlog_g, const void* fwd_ws,
                 void* bwd_ws, cudaStream_t st) {
-  const size_t f = simt_fwd_bytes(g), fb = simt_bwd_bytes(g);
-  SimtWs w = simt_carve_fwd(g, bwd_ws);
-  SimtBwdWs b = simt_carve_bwd(g, (char*)bwd_ws + f);
-  float* r32 = (float*)((char*)bwd_ws + f + fb);
-  void* yscr = (char*)r32 + a256(4ull * g.ns * g.t);
-  cudaMemsetAsync(w.zflag, 0, 4, st);
-  if (int rc = simt_build_table(g.p, g.d, g.D, w.idx, w.wt, st)) return rc;
-  // y / rowsum recomputed into scratch (the caller's copies stay untouched)
-  {
-    StageTimer tmr("bwd_recompute_fp32", st);
-    if (int rc = simt_forward(g, 1, q, k, v, log_g, yscr, r32, w, st)) return rc;
-  }
+  (void)log_g;
   (void)y;
-  (void)rowsum;
-  StageTimer tmr("bwd_fp32", st);
-  return simt_backward(g, 1, q, k, v, yscr, r32, dy, dq, dk, dv, dlog_g, w, b, st);
+  size_t n1, n2;
+  TcFwdWs w = carve_fwd(g, const_cast<void*>(fwd_ws), &n1);  // sp / kt are dead after the forward: reused
+  TcBwdWs b = carve_bwd(g, bwd_ws, &n2);
+  const int den = g.normalize ? 1 : 0;   // the backward needs the score sum only when normalizing
+  const int uc = den ? UW : 64;
+  CUtensorMap m_qt, m_dn, m_dd, m_v128, m_dummy;
+  if (!map_2d(&m_qt, w.kt, (size_t)g.ns * g.n * HD, g.c, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !map_2d(&m_dn, b.dN, (size_t)g.ns * g.t, HD, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !map_2d(&m_dd, b.dD, (size_t)g.ns * g.t, 16, 16, 64, CU_TENSOR_MAP_SWIZZLE_32B) ||
+      !map_bth(&m_v128, v, g, 128)) {
+    set_error("cuTensorMapEncodeTiled failed");
+    return 3;
+  }
+  CUtensorMap m_dn128, m_dd128;
+  if (!map_2d(&m_dn128, b.dN, (size_t)g.ns * g.t, HD, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !map_2d(&m_dd128, b.dD, (size_t)g.ns * g.t, 16, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B)) {
+    set_error("cuTensorMapEncodeTiled failed");
+    return 3;
+  }
+  m_dummy = m_dn;
+  {
+    StageTimer tmr("bwd_prep", st);
+    cudaMemsetAsync(b.dq32, 0, 4ull * g.ns * g.t * HD, st);
+    cudaMemsetAsync(b.dk32, 0, 4ull * g.ns * g.t * HD, st);
+    cudaMemsetAsync(b.dv32, 0, 4ull * g.ns * g.t * HD, st);
+    cudaMemsetAsync(b.dell, 0, 4ull * g.ns * g.t, st);
+    cudaMemsetAsync(b.cu, 0, 4ull * g.ns * g.t, st);
+    cudaMemsetAsync(b.dlam, 0, 4ull * g.ns * g.n, st);
+    k_tc_bwd_prep<<<(unsigned)(((size_t)g.ns * g.t + 255) / 256), 256, 0, st>>>(
+        g, (const __nv_bfloat16*)dy, w.y32, rowsum, b.dN, den ? b.dD : nullptr, b.dden);
+    k_tc_prep_xt<<<dim3(g.c / 64, g.n, g.ns), 256, 0, st>>>(g, (const __nv_bfloat16*)q, w.ell, w.lamlog, 1, w.kt);
+  }
+  if (g.n > 1) {
+    StageTimer tmr("bwd_query_state_dA", st);
+    cudaFuncSetAttribute(k_tc_featmajor<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fm::SMEM);
+    k_tc_featmajor<true><<<dim3((NTH + 3) / 4, g.n - 1, g.ns), 256, fm::SMEM, st>>>(m_qt, m_dn, m_dd, g, den, w.sp);
+  }
+  {
+    StageTimer tmr("bwd_discumsum", st);
+    k_tc_scan_bwd<<<dim3((FH * uc + 255) / 256, g.ns), 256, 0, st>>>(g, uc, w.lamlog, w.sp, w.stm, w.std_, b.dsm,
+                                                                      b.dsd, b.dlam);
+  }
+  {
+    StageTimer tmr("bwd_intra", st);
+    CUtensorMap m_q128, m_k128;
+    if (!map_bth(&m_q128, q, g, 128) || !map_bth(&m_k128, k, g, 128)) {
+      set_error("cuTensorMapEncodeTiled failed");
+      return 3;
+    }
+    cudaFuncSetAttribute(k_tc_intra_bwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ib::SMEM);
+    cudaFuncSetAttribute(k_tc_intra_bwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ib::SMEM);
+    k_tc_intra_bwd<true><<<dim3(g.c / 128, g.n, g.ns), 256, ib::SMEM, st>>>(m_q128, m_k128, m_v128, m_dn128, g,
+                                                                            w.ell, b.dden, b.dk32, b.dv32, b.dell);
+    k_tc_intra_bwd<false><<<dim3(g.c / 128, g.n, g.ns), 256, ib::SMEM, st>>>(m_q128, m_k128, m_v128, m_dn128, g,
+                                                                             w.ell, b.dden, b.dq32, nullptr, b.dell);
+  }
+  if (g.n > 1) {
+    StageTimer tmr("bwd_query_state_dq", st);
+    cudaFuncSetAttribute(k_tc_dphi<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dp::SMEM);
+    k_tc_dphi<false><<<dim3(g.c / 128, g.n - 1, g.ns), 256, dp::SMEM, st>>>(
+        m_dn128, m_dd128, g, (const __nv_bfloat16*)q, w.ell, w.lamlog, w.stm, w.std_, den, b.dq32, nullptr, b.dell,
+        nullptr);
+  }
+  {
+    StageTimer tmr("bwd_update_state", st);
+    cudaFuncSetAttribute(k_tc_dphi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dp::SMEM);
+    k_tc_dphi<true><<<dim3(g.c / 128, g.n, g.ns), 256, dp::SMEM, st>>>(
+        m_v128, m_dummy, g, (const __nv_bfloat16*)k, w.ell, w.lamlog, b.dsm, b.dsd, den, b.dk32, b.dv32, b.dell,
+        b.cu);
+  }
+  {
+    StageTimer tmr("bwd_finish", st);
+    if (dlog_g) {
+      k_tc_gate_finish<<<(g.ns * g.n + 3) / 4, 128, 0, st>>>(g, w.lamlog, b.dell, b.cu, b.dlam, dlog_g);
+      count_launch();
+    }
+    if (int rc = simt_finalize_bf16(g, b.dq32, HD, dq, st)) return rc;
+    if (int rc = simt_finalize_bf16(g, b.dk32, HD, dk, st)) return rc;
+    if (int rc = simt_finalize_bf16(g, b.dv32, HD, dv, st)) return rc;
+  }
+  count_launch(8);
+  return cuda_check("tc backward");
 }
 
 }  // namespace pa

@@ -1,58 +1,37 @@
 // Shared layouts and compile-time feature tables for the bf16 tcgen05
 // pipeline (SPOW p = 2, d = e = 64).
 //
-// Two orders of the 2080 SPOW features (a <= b) are used:
-//  * compact order (2112 slots, 33 blocks of 64): for a = 0..63, for
-//    beta = a/2..31 the pair of features (a, 2 beta), (a, 2 beta + 1).  One
-//    bf16x2 TMEM column holds one pair, so phi'(x) for a token held in
-//    registers is one HMUL2 per column.  The slot (a, a-1) for odd a is a
-//    duplicate; its state row is zero (weight 0).
-//  * block order (2304 slots, 72 blocks of 4 a x 8 b, 18 tiles of 128): the
-//    M-rows of the "feature-major" GEMMs (update_state, dA of query_state),
-//    chosen so each warp's 32 lanes read 4 + 8 distinct K^T rows.  Slots with
-//    a > b are duplicates and are dropped when converting to compact order.
-// The state weight omega = w^2 (1 on the diagonal, 2 off it) is folded into
-// the stored states, so phi' is the bare monomial product.
+// Feature order ("block order", 2304 slots): the 2080 SPOW features (a <= b,
+// reference expansions.py:106-123) tiled by 72 blocks of 4 a x 8 b values,
+// blocks listed by beta (b/8) then alpha (a/4).  Slot = 32*block + 8*(a%4) +
+// b%8.  Slots with a > b (inside diagonal blocks) are duplicates whose state
+// rows are kept at zero (weight 0).  Every GEMM uses this order:
+//  * feature-major GEMMs (update_state, dA) put 128 slots on the M lanes,
+//    each warp owning one 4x8 block (4 + 8 distinct K^T rows per warp);
+//  * token-major GEMMs generate phi'(x) for a token held in registers: one
+//    bf16x2 TMEM column = features (a, b), (a, b+1) = one HMUL2.
+// States are stored feature-major, [slot][u] with u = 64 value columns in
+// 128-byte SW128 rows, plus (when the score sum is needed) [slot][16] SW32
+// rows whose column 0 is the key_sum.  The SPOW weight omega = w^2 (1 on the
+// diagonal, 2 off it, reference expansions.py:149-163) is folded into stored
+// states, so phi' is the bare monomial product.
 #pragma once
 
 #include <stdint.h>
 
 #include <utility>
 
+#include "pa_sm100.cuh"
+
 namespace pa {
 namespace tc {
 
 constexpr int HD = 64;        // d = e for this specialisation
-constexpr int NCOL = 1056;    // compact bf16x2 columns
-constexpr int DC = 2112;      // compact feature slots
-constexpr int NFB = 33;       // 64-feature blocks (compact)
-constexpr int NBLK = 72;      // 4x8 blocks (block order)
-constexpr int FH = 2304;      // block-order slots
-constexpr int NTH = 18;       // 128-row tiles in block order
-constexpr int UW = 80;        // state columns: 64 values + 16 (col 64 = key_sum)
-
-constexpr int col_a(int c) {
-  int a = 0;
-  while (c >= 32 - a / 2) {
-    c -= 32 - a / 2;
-    ++a;
-  }
-  return a;
-}
-constexpr int col_beta(int c) {
-  int a = 0;
-  while (c >= 32 - a / 2) {
-    c -= 32 - a / 2;
-    ++a;
-  }
-  return a / 2 + c;
-}
-// first compact column of row a
-constexpr int col_start(int a) {
-  int c = 0;
-  for (int i = 0; i < a; ++i) c += 32 - i / 2;
-  return c;
-}
+constexpr int NBLK = 72;      // 4x8 blocks
+constexpr int FH = 2304;      // feature slots
+constexpr int NTH = 18;       // 128-slot tiles
+constexpr int NKB = 36;       // 64-slot K blocks (2 feature blocks each)
+constexpr int UW = 80;        // fp32 state columns: 64 values + 16 (col 64 = key_sum)
 
 struct BlkTab {
   uint8_t al[NBLK];
@@ -73,16 +52,55 @@ constexpr BlkTab make_blk_tab() {
     }
   return t;
 }
+constexpr BlkTab kBlk = make_blk_tab();
 
-// compact slot -> (a, b); b = -1 never (dummies report b = a - 1)
-__host__ __device__ inline void compact_ab(int f, int& a, int& b) {
-  int c = f >> 1;
-  a = 0;
-  while (c >= 32 - a / 2) {
-    c -= 32 - a / 2;
-    ++a;
+// slot -> (a, b) and omega
+__host__ __device__ constexpr int slot_a(int f, const BlkTab& t) { return 4 * t.al[f >> 5] + ((f >> 3) & 3); }
+__host__ __device__ constexpr int slot_b(int f, const BlkTab& t) { return 8 * t.be[f >> 5] + (f & 7); }
+
+// ---------------------------------------------------------------- generation
+// phi'(x) columns of feature block B (16 bf16x2 columns): column i*4 + jp holds
+// features (4 al + i, 8 be + 2 jp) and (4 al + i, 8 be + 2 jp + 1).
+template <int A>
+__device__ __forceinline__ uint32_t bcast_x(const uint32_t* xp) {
+  return __byte_perm(xp[A >> 1], 0, (A & 1) ? 0x3232 : 0x1010);
+}
+template <int B>
+__device__ __forceinline__ void gen_fblock(const uint32_t* xp, uint32_t* o) {
+  constexpr int al = kBlk.al[B], be = kBlk.be[B];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint32_t bc;
+    if (i == 0) bc = bcast_x<4 * al + 0>(xp);
+    if (i == 1) bc = bcast_x<4 * al + 1>(xp);
+    if (i == 2) bc = bcast_x<4 * al + 2>(xp);
+    if (i == 3) bc = bcast_x<4 * al + 3>(xp);
+#pragma unroll
+    for (int jp = 0; jp < 4; ++jp) o[i * 4 + jp] = sm100::hmul2_bf16(bc, xp[4 * be + jp]);
   }
-  b = 2 * (a / 2 + c) + (f & 1);
+}
+
+// ---------------------------------------------------------------- expand VJP
+// d<g, phi'(x)>/dx for the 32 features of block B given their cotangents g
+// (fp32, slot order): dx[b] += g x[a]; dx[a] += g x[b].  Diagonal features
+// get both terms (2 g x[a]); duplicate slots carry g = 0.
+template <int B>
+__device__ __forceinline__ void evjp_fblock(const float (&x)[64], float (&dx)[64], const uint32_t* g) {
+  constexpr int al = kBlk.al[B], be = kBlk.be[B];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float xa = x[4 * al + i];
+    float t0 = 0.f, t1 = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+      const float g0 = __uint_as_float(g[i * 8 + j]), g1 = __uint_as_float(g[i * 8 + j + 1]);
+      dx[8 * be + j] = fmaf(g0, xa, dx[8 * be + j]);
+      dx[8 * be + j + 1] = fmaf(g1, xa, dx[8 * be + j + 1]);
+      t0 = fmaf(g0, x[8 * be + j], t0);
+      t1 = fmaf(g1, x[8 * be + j + 1], t1);
+    }
+    dx[4 * al + i] += t0 + t1;
+  }
 }
 
 }  // namespace tc
