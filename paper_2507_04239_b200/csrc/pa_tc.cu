@@ -61,11 +61,11 @@ __global__ void __launch_bounds__(128) k_tc_prep_gates(Geo g, const float* __res
 }
 
 // X~^T [((s*n + k)*64 + dim)][tok] = x_j * exp(mode) for 64-token blocks;
-// mode 0: exp((lend - ell_j)/2) (keys, suffix decay); 1: scale*exp(ell_j/2) (queries, prefix)
+// mode 0: exp((lend - ell_j)/2) (keys, suffix decay); 1: scale*exp(ell_j/2) (queries, prefix); 2: 1 (exact copy)
 __global__ void __launch_bounds__(256) k_tc_prep_xt(Geo g, const __nv_bfloat16* __restrict__ x,
                                                     const float* __restrict__ ell,
                                                     const float* __restrict__ lamlog, int mode,
-                                                    __nv_bfloat16* xt) {
+                                                    __half* xt) {
   __shared__ float tile[64][65];
   const int tb = blockIdx.x, k = blockIdx.y, s = blockIdx.z;
   const int j0 = k * g.c + tb * 64;
@@ -74,14 +74,62 @@ __global__ void __launch_bounds__(256) k_tc_prep_xt(Geo g, const __nv_bfloat16* 
     const int r = i >> 6, dcol = i & 63;
     const int j = j0 + r;
     const float lj = ell[(size_t)s * g.t + j];
-    const float f = mode == 0 ? __expf(0.5f * (lamlog[s * g.n + k] - lj)) : g.scale * __expf(0.5f * lj);
-    tile[r][dcol] = __bfloat162float(x[rowid(g, s, j) * HD + dcol]) * (g.gated || mode ? f : 1.f);
+    const float f = mode == 2 ? 1.f
+                    : mode == 0 ? __expf(0.5f * (lamlog[s * g.n + k] - lj))
+                                : g.scale * __expf(0.5f * lj);
+    tile[r][dcol] = __bfloat162float(x[rowid(g, s, j) * HD + dcol]) * f;
   }
   __syncthreads();
-  __nv_bfloat16* dst = xt + ((size_t)(s * g.n + k) * HD) * g.c + tb * 64;
+  __half* dst = xt + ((size_t)(s * g.n + k) * HD) * g.c + tb * 64;
   for (int i = threadIdx.x; i < 64 * 64; i += 256) {
     const int dim = i >> 6, r = i & 63;
-    dst[(size_t)dim * g.c + r] = __float2bfloat16_rn(tile[r][dim]);
+    dst[(size_t)dim * g.c + r] = __float2half_rn(tile[r][dim]);
+  }
+}
+
+// Per-token scaled operand rows for the feature-major GEMMs, so that phi' can
+// be generated from the exact bf16 inputs (one rounding per feature) while the
+// per-token decay/scale rides on the other operand:
+//   mode 0 (forward):  rows = W_m v_m,        aux = (W_m, 0...)      W_m = exp(lend - ell_m)
+//   mode 1 (backward): rows = c_m dnum_m,     aux = (c_m dden_m, 0...)  c_m = sigma^2 exp(ell_m)
+// rows [ns*t][64] bf16, aux [ns*t][16] bf16 (may be null).
+__global__ void __launch_bounds__(256) k_tc_prep_rows(Geo g, int mode, const __nv_bfloat16* __restrict__ src,
+                                                      const float* __restrict__ ell,
+                                                      const float* __restrict__ lamlog,
+                                                      const float* __restrict__ dden, __half* rows,
+                                                      __half* aux) {
+  const size_t it = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (it >= (size_t)g.ns * g.t) return;
+  const int s = (int)(it / g.t), m = (int)(it - (size_t)s * g.t);
+  const float lm = ell[it];
+  float f, a;
+  const __nv_bfloat16* row;
+  if (mode == 0 || mode == 2) {
+    f = (mode == 0 && g.gated) ? __expf(lamlog[s * g.n + m / g.c] - lm) : 1.f;
+    a = f;
+    row = src + rowid(g, s, m) * HD;
+  } else {
+    f = g.scale * g.scale * __expf(lm);
+    a = dden ? f * dden[it] : 0.f;
+    row = src + it * HD;
+  }
+  const uint4* in = (const uint4*)row;
+  uint4* out = (uint4*)(rows + it * HD);
+#pragma unroll
+  for (int c8 = 0; c8 < 8; ++c8) {
+    uint4 v4 = in[c8];
+    uint32_t* pv = (uint32_t*)&v4;
+#pragma unroll
+    for (int e2 = 0; e2 < 4; ++e2) {
+      const float2 f2 = __bfloat1622float2(*(const __nv_bfloat162*)&pv[e2]);
+      pv[e2] = pack_f16(f2.x * f, f2.y * f);
+    }
+    out[c8] = v4;
+  }
+  if (aux) {
+    uint4* ao = (uint4*)(aux + it * 16);
+    ao[0] = make_uint4(pack_f16(a, 0.f), 0u, 0u, 0u);
+    ao[1] = make_uint4(0u, 0u, 0u, 0u);
   }
 }
 
@@ -146,8 +194,6 @@ __global__ void __launch_bounds__(256, 1) k_tc_featmajor(const __grid_constant__
     mbar_init(fin, 1);
     fence_barrier_init();
   }
-  if (!kBwd)  // K-major 16-row block whose row 0 is all ones: the key_sum column
-    for (int i = tid; i < 2048 / 4; i += 256) ((uint32_t*)ones)[i] = (i < 32) ? 0x3F803F80u : 0u;
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
@@ -160,26 +206,21 @@ __global__ void __launch_bounds__(256, 1) k_tc_featmajor(const __grid_constant__
       tma_prefetch(&tm_xt);
       tma_prefetch(&tm_b);
       const int row0 = (s * g.n + kin) * HD;
-      const int bi = s / g.h, hi = s % g.h;
       for (int j = 0; j < nstage; ++j) {
         const int st = j % ST;
         if (j >= ST) mbar_wait(&empty[st], ((j / ST) + 1) & 1);
-        const uint32_t bytes = XT_B + B_B + ((kBwd && den) ? B16_B : 0);
+        const uint32_t bytes = XT_B + B_B + (den ? B16_B : 0);
         mbar_expect_tx(&full[st], bytes);
         tma_load_2d(xt_s + st * XT_B, &tm_xt, &full[st], j * TOK, row0);
-        if (kBwd) {
-          tma_load_2d(b_s + st * B_B, &tm_b, &full[st], 0, s * g.t + kin * g.c + j * TOK);
-          if (den) tma_load_2d(b16_s + st * B16_B, &tm_b16, &full[st], 0, s * g.t + kin * g.c + j * TOK);
-        } else {
-          tma_load_4d(b_s + st * B_B, &tm_b, &full[st], 0, hi, kin * g.c + j * TOK, bi);
-        }
+        tma_load_2d(b_s + st * B_B, &tm_b, &full[st], 0, s * g.t + kin * g.c + j * TOK);
+        if (den) tma_load_2d(b16_s + st * B16_B, &tm_b16, &full[st], 0, s * g.t + kin * g.c + j * TOK);
       }
     }
   } else if (w == 1) {
     // ---------------- MMA issuer ----------------
     if (l == 0) {
-      const uint32_t id64 = idesc_bf16(128, 64, false, true);
-      const uint32_t id16 = idesc_bf16(128, 16, false, !kBwd ? false : true);
+      const uint32_t id64 = idesc_f16(128, 64, false, true);
+      const uint32_t id16 = idesc_f16(128, 16, false, true);
       for (int i = 0; i < nsub; ++i) {
         const int j = i >> 1, h = i & 1, st = j % ST, buf = i % NB;
         mbar_wait(&full[st], (j / ST) & 1);
@@ -196,8 +237,7 @@ __global__ void __launch_bounds__(256, 1) k_tc_featmajor(const __grid_constant__
             const int trow = h * 32 + kk * 16;  // token row inside the 64-token stage
             mma_ts(acc, ab + kk * 8, smem_desc(bsm + trow * 128, 8192, 1024, 2), id64, f);
             if (den) {
-              const uint64_t dd = kBwd ? smem_desc(b16 + trow * 32, 512, 256, 6)
-                                       : smem_desc(smem_u32(ones) + ((h * 2 + kk) & 3) * 32, 16, 1024, 2);
+              const uint64_t dd = smem_desc(b16 + trow * 32, 512, 256, 6);
               mma_ts(acc + 64, ab + kk * 8, dd, id16, f);
             }
           }
@@ -234,7 +274,7 @@ __global__ void __launch_bounds__(256, 1) k_tc_featmajor(const __grid_constant__
             *(uint4*)&vb[c4 * 4] = *(const uint4*)(xs + sw128_off(rb[t], ch));
           }
 #pragma unroll
-          for (int c = 0; c < 16; ++c) o[c] = hmul2_bf16(va[c], vb[c]);
+          for (int c = 0; c < 16; ++c) o[c] = hmul2_f16(va[c], vb[c]);
           tmem_st16(tm + 320u + (uint32_t)((buf * 4 + t) * 16) + lane_off, o);
         }
       }
@@ -287,8 +327,8 @@ constexpr size_t ST_DEN = (size_t)FH * 16;    // bf16 elements, score-sum part
 // thread per (slot, column); grid (ceil(FH*ucols/256), stream)
 // ==========================================================================
 __global__ void __launch_bounds__(256) k_tc_scan_fwd(Geo g, int ucols, const float* __restrict__ lamlog,
-                                                     const float* __restrict__ sp, __nv_bfloat16* st_main,
-                                                     __nv_bfloat16* st_den) {
+                                                     const float* __restrict__ sp, __half* st_main,
+                                                     __half* st_den) {
   const int s = blockIdx.y;
   const int e = blockIdx.x * 256 + threadIdx.x;
   if (e >= FH * ucols) return;
@@ -298,11 +338,11 @@ __global__ void __launch_bounds__(256) k_tc_scan_fwd(Geo g, int ucols, const flo
   for (int k = 0; k < g.n; ++k) {
     const float lam = k == 0 ? 0.f : (g.gated ? __expf(lamlog[s * g.n + k]) : 1.f);
     acc = lam * acc + om * sp[((size_t)(s * g.n + k) * FH + f) * UW + u];
-    const __nv_bfloat16 v = __float2bfloat16_rn(acc);
+    const __half v = __float2half_rn(acc * pow2_neg_bits(k));
     if (u < 64)
-      *(__nv_bfloat16*)((uint8_t*)(st_main + (size_t)(s * g.n + k) * ST_MAIN) + sw128_elem(f, u)) = v;
+      *(__half*)((uint8_t*)(st_main + (size_t)(s * g.n + k) * ST_MAIN) + sw128_elem(f, u)) = v;
     else
-      *(__nv_bfloat16*)((uint8_t*)(st_den + (size_t)(s * g.n + k) * ST_DEN) + sw32_elem(f, u - 64)) = v;
+      *(__half*)((uint8_t*)(st_den + (size_t)(s * g.n + k) * ST_DEN) + sw32_elem(f, u - 64)) = v;
   }
 }
 
@@ -346,6 +386,21 @@ __device__ __forceinline__ void gen_all_kblocks(const uint32_t (&xp)[32], uint32
   if constexpr (KB + 1 < NKB) gen_all_kblocks<KB + 1, NA>(xp, a_base, lane_off, a_full, a_empty, l);
 }
 
+// a bf16 row of 64 as fp16 pairs (exact for |x| < 65504)
+__device__ __forceinline__ void load_row_f16(const __nv_bfloat16* src, uint32_t (&xp)[32]) {
+  const uint4* row = (const uint4*)src;
+#pragma unroll
+  for (int c8 = 0; c8 < 8; ++c8) {
+    uint4 v4 = row[c8];
+    const uint32_t* pv = (const uint32_t*)&v4;
+#pragma unroll
+    for (int e2 = 0; e2 < 4; ++e2) {
+      float2 f2 = __bfloat1622float2(*(const __nv_bfloat162*)&pv[e2]);
+      xp[c8 * 4 + e2] = pack_f16(f2.x, f2.y);
+    }
+  }
+}
+
 __device__ __forceinline__ void load_scaled_row(const __nv_bfloat16* src, float f, uint32_t (&xp)[32]) {
   const uint4* row = (const uint4*)src;
 #pragma unroll
@@ -365,8 +420,8 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
                                                    const __grid_constant__ CUtensorMap tm_v, Geo g,
                                                    const __nv_bfloat16* __restrict__ qraw,
                                                    const float* __restrict__ ell,
-                                                   const __nv_bfloat16* __restrict__ st_main,
-                                                   const __nv_bfloat16* __restrict__ st_den, int with_den,
+                                                   const __half* __restrict__ st_main,
+                                                   const __half* __restrict__ st_den, int with_den,
                                                    __nv_bfloat16* y, float* rowsum, float* y32, int* zflag) {
   using namespace outk;
   extern __shared__ uint8_t smem_raw[];
@@ -391,6 +446,8 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
   uint64_t* p_full = s_full + 2;              // 2
   uint64_t* pv_done = p_full + 2;             // 2
   uint64_t* fin = pv_done + 2;                // 1
+  uint64_t* a_done = fin + 1;                 // 1  (all state-query MMAs complete)
+  uint64_t* o_ready = a_done + 1;             // 1  (state rows rescaled by the compute warps)
   __shared__ uint32_t tmem_base;
 
   const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
@@ -421,6 +478,8 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
       mbar_init(&pv_done[i], 1);
     }
     mbar_init(fin, 1);
+    mbar_init(a_done, 1);
+    mbar_init(o_ready, 4);
     fence_barrier_init();
   }
   for (int i = tid; i < 2048 / 4; i += 256) ((uint32_t*)ones)[i] = (i < 32) ? 0x3F803F80u : 0u;
@@ -451,8 +510,8 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
       const int early = min(I + 1, KV_ST);
       for (int J = 0; J < early; ++J) kv(J);
       if (has_state) {
-        const __nv_bfloat16* srcm = st_main + (size_t)(s * g.n + (k - 1)) * ST_MAIN;
-        const __nv_bfloat16* srcd = st_den + (size_t)(s * g.n + (k - 1)) * ST_DEN;
+        const __half* srcm = st_main + (size_t)(s * g.n + (k - 1)) * ST_MAIN;
+        const __half* srcd = st_den + (size_t)(s * g.n + (k - 1)) * ST_DEN;
         for (int kb = 0; kb < NKB; ++kb) {
           const int sb = kb % ST_ST;
           if (kb >= ST_ST) mbar_wait(&st_empty[sb], ((kb / ST_ST) + 1) & 1);
@@ -466,8 +525,9 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
   } else if (w == 1) {
     // ---------------- MMA issuer ----------------
     if (l == 0) {
-      const uint32_t id64mn = idesc_bf16(128, 64, false, true);
-      const uint32_t id16mn = idesc_bf16(128, 16, false, true);
+      const uint32_t id64mn = idesc_bf16(128, 64, false, true);     // P V (bf16)
+      const uint32_t id64mn_h = idesc_f16(128, 64, false, true);    // phi'(q) A' (fp16)
+      const uint32_t id16mn_h = idesc_f16(128, 16, false, true);
       const uint32_t id16k = idesc_bf16(128, 16, false, false);
       const uint32_t id128 = idesc_bf16(128, 128, false, false);
       if (has_state) {
@@ -481,12 +541,13 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             const uint32_t f = (kb > 0 || kk > 0) ? 1u : 0u;
-            mma_ts(tm, ab + kk * 8, smem_desc(sm + kk * 2048, 8192, 1024, 2), id64mn, f);
-            if (den) mma_ts(tm + 64, ab + kk * 8, smem_desc(sdn + kk * 512, 2048, 256, 6), id16mn, f);
+            mma_ts(tm, ab + kk * 8, smem_desc(sm + kk * 2048, 8192, 1024, 2), id64mn_h, f);
+            if (den) mma_ts(tm + 64, ab + kk * 8, smem_desc(sdn + kk * 512, 2048, 256, 6), id16mn_h, f);
           }
           tc_commit(&a_empty[bb]);
           tc_commit(&st_empty[sb]);
         }
+        tc_commit(a_done);
       }
       mbar_wait(q_full, 0);
       auto issue_s = [&](int J) {
@@ -501,6 +562,7 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
         tc_commit(&s_full[sb]);
       };
       issue_s(0);
+      if (has_state) mbar_wait(o_ready, 0);   // O holds the rescaled state query before P V accumulates
       for (int J = 0; J <= I; ++J) {
         if (J + 1 <= I) issue_s(J + 1);
         const int sb = J & 1, st = J % KV_ST;
@@ -527,9 +589,35 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
     const float li = ell_s[I * 128 + row];
     const float sig2 = g.scale * g.scale;
     if (has_state) {
+      // phi'(q) from the exact bf16 q (one rounding per feature); the query
+      // scale sigma^2 * gp_m (chunked.py:379-385) is applied to the fp32 row
       uint32_t qp[32];
-      load_scaled_row(qraw + rowid(g, s, tok) * HD, g.scale * __expf(0.5f * li), qp);
+      load_row_f16(qraw + rowid(g, s, tok) * HD, qp);
       gen_all_kblocks<0, NA>(qp, a_base, lane_off, a_full, a_empty, l);
+      mbar_wait(a_done, 0);
+      tc_fence_after();
+      const float cm = sig2 * __expf(li) / pow2_neg_bits(k - 1);   // undo the stored-state scale
+      uint32_t r[32];
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        tmem_ld32(tm + lane_off + h2 * 32, r);
+        tc_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * cm);
+        tmem_st16(tm + lane_off + h2 * 32, r);
+        tmem_st16(tm + lane_off + h2 * 32 + 16, r + 16);
+      }
+      if (den) {
+        tmem_ld16(tm + lane_off + 64, r);
+        tc_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * cm);
+        tmem_st16(tm + lane_off + 64, r);
+      }
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (l == 0) mbar_arrive(o_ready);
     }
     for (int J = 0; J <= I; ++J) {
       const int sb = J & 1;
@@ -642,7 +730,7 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
 __global__ void __launch_bounds__(256) k_tc_bwd_prep(Geo g, const __nv_bfloat16* __restrict__ dy,
                                                      const float* __restrict__ y32,
                                                      const float* __restrict__ rowsum, __nv_bfloat16* dN,
-                                                     __nv_bfloat16* dD, float* dden_out) {
+                                                     __half* dN16, __half* dD, float* dden_out) {
   const size_t it = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (it >= (size_t)g.ns * g.t) return;
   const int s = (int)(it / g.t), m = (int)(it - (size_t)s * g.t);
@@ -652,11 +740,14 @@ __global__ void __launch_bounds__(256) k_tc_bwd_prep(Geo g, const __nv_bfloat16*
   const float inv = 1.f / R;
   const uint4* src = (const uint4*)(dy + r * HD);
   uint4* dst = (uint4*)(dN + it * HD);
+  uint4* dst16 = (uint4*)(dN16 + it * HD);
 #pragma unroll
   for (int c8 = 0; c8 < 8; ++c8) {
     uint4 v4 = src[c8];
     uint32_t* pv = (uint32_t*)&v4;
 #pragma unroll
+    uint4 h4;
+    uint32_t* ph = (uint32_t*)&h4;
     for (int e2 = 0; e2 < 4; ++e2) {
       float2 f2 = __bfloat1622float2(*(const __nv_bfloat162*)&pv[e2]);
       const int u = c8 * 8 + e2 * 2;
@@ -664,14 +755,16 @@ __global__ void __launch_bounds__(256) k_tc_bwd_prep(Geo g, const __nv_bfloat16*
       f2.x *= inv;
       f2.y *= inv;
       pv[e2] = pack_bf16(f2.x, f2.y);
+      ph[e2] = pack_f16(f2.x, f2.y);
     }
     dst[c8] = v4;
+    dst16[c8] = h4;
   }
   const float dden = g.normalize ? -dot * inv : 0.f;
   dden_out[it] = dden;
   if (dD) {
     uint4* dd = (uint4*)(dD + it * 16);
-    dd[0] = make_uint4(pack_bf16(dden, 0.f), 0u, 0u, 0u);
+    dd[0] = make_uint4(pack_f16(dden, 0.f), 0u, 0u, 0u);
     dd[1] = make_uint4(0u, 0u, 0u, 0u);
   }
 }
@@ -682,9 +775,9 @@ __global__ void __launch_bounds__(256) k_tc_bwd_prep(Geo g, const __nv_bfloat16*
 // thread per (slot, column); grid (ceil(FH*ucols/256), stream)
 __global__ void __launch_bounds__(256) k_tc_scan_bwd(Geo g, int ucols, const float* __restrict__ lamlog,
                                                      const float* __restrict__ dA,
-                                                     const __nv_bfloat16* __restrict__ st_main,
-                                                     const __nv_bfloat16* __restrict__ st_den,
-                                                     __nv_bfloat16* ds_main, __nv_bfloat16* ds_den, float* dlam) {
+                                                     const __half* __restrict__ st_main,
+                                                     const __half* __restrict__ st_den,
+                                                     __half* ds_main, __half* ds_den, float* dlam) {
   __shared__ float red[32];
   const int s = blockIdx.y;
   const int e = blockIdx.x * 256 + threadIdx.x;
@@ -697,21 +790,20 @@ __global__ void __launch_bounds__(256) k_tc_scan_bwd(Geo g, int ucols, const flo
     const float dAk = (ok && k + 1 < g.n) ? dA[((size_t)(s * g.n + k) * FH + f) * UW + u] : 0.f;
     G = dAk + lam_next * G;
     if (ok) {
-      const __nv_bfloat16 v = __float2bfloat16_rn(om * G);
+      const __half v = __float2half_rn(om * G * pow2_neg_bits(g.n - 1 - k));
       if (u < 64)
-        *(__nv_bfloat16*)((uint8_t*)(ds_main + (size_t)(s * g.n + k) * ST_MAIN) + sw128_elem(f, u)) = v;
+        *(__half*)((uint8_t*)(ds_main + (size_t)(s * g.n + k) * ST_MAIN) + sw128_elem(f, u)) = v;
       else
-        *(__nv_bfloat16*)((uint8_t*)(ds_den + (size_t)(s * g.n + k) * ST_DEN) + sw32_elem(f, u - 64)) = v;
+        *(__half*)((uint8_t*)(ds_den + (size_t)(s * g.n + k) * ST_DEN) + sw32_elem(f, u - 64)) = v;
     }
     if (k >= 1) {
       float a = 0.f;
       if (ok) {
-        const __nv_bfloat16* src =
-            u < 64 ? (const __nv_bfloat16*)((const uint8_t*)(st_main + (size_t)(s * g.n + k - 1) * ST_MAIN) +
-                                            sw128_elem(f, u))
-                   : (const __nv_bfloat16*)((const uint8_t*)(st_den + (size_t)(s * g.n + k - 1) * ST_DEN) +
-                                            sw32_elem(f, u - 64));
-        a = __bfloat162float(*src) * G;
+        const __half* src =
+            u < 64 ? (const __half*)((const uint8_t*)(st_main + (size_t)(s * g.n + k - 1) * ST_MAIN) + sw128_elem(f, u))
+                   : (const __half*)((const uint8_t*)(st_den + (size_t)(s * g.n + k - 1) * ST_DEN) +
+                                     sw32_elem(f, u - 64));
+        a = __half2float(*src) / pow2_neg_bits(k - 1) * G;
       }
       const float tot = block_sum(a, red);
       if (threadIdx.x == 0 && g.gated) atomicAdd(dlam + s * g.n + k, tot);
@@ -768,8 +860,8 @@ __global__ void __launch_bounds__(256, 1) k_tc_dphi(const __grid_constant__ CUte
                                                     const __nv_bfloat16* __restrict__ xraw,
                                                     const float* __restrict__ ell,
                                                     const float* __restrict__ lamlog,
-                                                    const __nv_bfloat16* __restrict__ b_main,
-                                                    const __nv_bfloat16* __restrict__ b_den, int with_den,
+                                                    const __half* __restrict__ b_main,
+                                                    const __half* __restrict__ b_den, int with_den,
                                                     float* dx32, float* dv32, float* dell, float* dellend) {
   using namespace dp;
   extern __shared__ uint8_t smem_raw[];
@@ -796,8 +888,10 @@ __global__ void __launch_bounds__(256, 1) k_tc_dphi(const __grid_constant__ CUte
   const int tok0 = k * g.c + I * 128;
   const bool den = with_den != 0;
   const int bslot = kUpd ? k : k - 1;    // state index the B operand comes from
-  const __nv_bfloat16* bm = b_main + (size_t)(s * g.n + bslot) * ST_MAIN;
-  const __nv_bfloat16* bd = b_den + (size_t)(s * g.n + bslot) * ST_DEN;
+  const __half* bm = b_main + (size_t)(s * g.n + bslot) * ST_MAIN;
+  const __half* bd = b_den + (size_t)(s * g.n + bslot) * ST_DEN;
+  // undo the stored-state scale (A'_{k-1} for the query side, G_k for the update side)
+  const float sscale = 1.f / (kUpd ? pow2_neg_bits(g.n - 1 - k) : pow2_neg_bits(k - 1));
 
   if (w == 2) tmem_alloc<512>(&tmem_base);
   if (tid == 0) {
@@ -826,14 +920,10 @@ __global__ void __launch_bounds__(256, 1) k_tc_dphi(const __grid_constant__ CUte
     if (l == 0) {
       tma_prefetch(&tm_a);
       mbar_expect_tx(a_ready, AB + ((!kUpd && den) ? A16 : 0));
-      if (kUpd) {
-        tma_load_4d(a_s, &tm_a, a_ready, 0, hi, tok0, bi);
-      } else {
-        tma_load_2d(a_s, &tm_a, a_ready, 0, s * g.t + tok0);
-        if (den) tma_load_2d(a16_s, &tm_a16, a_ready, 0, s * g.t + tok0);
-      }
+      tma_load_2d(a_s, &tm_a, a_ready, 0, s * g.t + tok0);
+      if (!kUpd && den) tma_load_2d(a16_s, &tm_a16, a_ready, 0, s * g.t + tok0);
       int j = 0;
-      auto stage = [&](const __nv_bfloat16* m, uint32_t mb, const __nv_bfloat16* d, uint32_t dbytes) {
+      auto stage = [&](const __half* m, uint32_t mb, const __half* d, uint32_t dbytes) {
         const int st = j % NST;
         if (j >= NST) mbar_wait(&b_empty[st], ((j / NST) + 1) & 1);
         mbar_expect_tx(&b_full[st], mb + dbytes);
@@ -847,8 +937,8 @@ __global__ void __launch_bounds__(256, 1) k_tc_dphi(const __grid_constant__ CUte
     }
   } else if (w == 1) {
     if (l == 0) {
-      const uint32_t id128 = idesc_bf16(128, 128, false, false);
-      const uint32_t id64mn = idesc_bf16(128, 64, false, true);
+      const uint32_t id128 = idesc_f16(128, 128, false, false);
+      const uint32_t id64mn = idesc_f16(128, 64, false, true);
       mbar_wait(a_ready, 0);
       tc_fence_after();
       const uint32_t am = smem_u32(a_s), a16 = smem_u32(a16_s);
@@ -891,16 +981,19 @@ __global__ void __launch_bounds__(256, 1) k_tc_dphi(const __grid_constant__ CUte
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const int tok = tok0 + row;
     const float lt = ell[(size_t)s * g.t + tok];
-    // this token's scaled row: q~ = sigma e^{ell/2} q  or  k~ = e^{(lend-ell)/2} k (bf16-rounded as in the forward)
-    const float fsc = kUpd ? (g.gated ? __expf(0.5f * (lamlog[s * g.n + k] - lt)) : 1.f)
-                           : g.scale * __expf(0.5f * lt);
+    // phi' is generated from the exact bf16 row; the per-token factor
+    //   query : c_m = sigma^2 gp_m (y_state = c_m phi'(q) A')
+    //   update: W_j = exp(lend - ell_j) (S' = sum_j W_j phi'(k_j) u_j^T)
+    // multiplies the fp32 results instead of a rounded operand.
+    const float fct =
+        sscale * (kUpd ? (g.gated ? __expf(lamlog[s * g.n + k] - lt) : 1.f) : g.scale * g.scale * __expf(lt));
     uint32_t xp[32];
-    load_scaled_row(xraw + rowid(g, s, tok) * HD, fsc, xp);
+    load_row_f16(xraw + rowid(g, s, tok) * HD, xp);
     if (kUpd && den) {
       // A score-sum tile for the update side: [v | 1]: row = token, column 0 = 1 (SW32 layout)
       uint32_t* rowp = (uint32_t*)(a16_s + (size_t)row * 32);
       for (int i = 0; i < 8; ++i) rowp[i] = 0u;
-      *(__nv_bfloat16*)(a16_s + sw32_elem(row, 0)) = __float2bfloat16_rn(1.f);
+      *(__half*)(a16_s + sw32_elem(row, 0)) = __float2half_rn(1.f);
       fence_async_smem();
     }
     __syncwarp();
@@ -908,7 +1001,7 @@ __global__ void __launch_bounds__(256, 1) k_tc_dphi(const __grid_constant__ CUte
     float x[64], dx[64];
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
-      const float2 f2 = __bfloat1622float2(*(const __nv_bfloat162*)&xp[i]);
+      const float2 f2 = __half22float2(*(const __half2*)&xp[i]);
       x[2 * i] = f2.x;
       x[2 * i + 1] = f2.y;
       dx[2 * i] = 0.f;
@@ -918,34 +1011,24 @@ __global__ void __launch_bounds__(256, 1) k_tc_dphi(const __grid_constant__ CUte
     float c = 0.f;
 #pragma unroll
     for (int a = 0; a < 64; ++a) c = fmaf(dx[a], x[a], c);
-    c *= 0.5f;
+    c *= 0.5f * fct;   // = d<.,.>/d(log factor): degree-2 homogeneity of phi'
     float* o = dx32 + ((size_t)s * g.t + tok) * HD;
+#pragma unroll
+    for (int a = 0; a < 64; a += 4) {
+      float4 v = *(float4*)(o + a);
+      v.x += dx[a] * fct;
+      v.y += dx[a + 1] * fct;
+      v.z += dx[a + 2] * fct;
+      v.w += dx[a + 3] * fct;
+      *(float4*)(o + a) = v;
+    }
     if (!kUpd) {
-      const float sc = g.scale * __expf(0.5f * lt);
-#pragma unroll
-      for (int a = 0; a < 64; a += 4) {
-        float4 v = *(float4*)(o + a);
-        v.x += dx[a] * sc;
-        v.y += dx[a + 1] * sc;
-        v.z += dx[a + 2] * sc;
-        v.w += dx[a + 3] * sc;
-        *(float4*)(o + a) = v;
-      }
-      if (g.gated) dell[(size_t)s * g.t + tok] += c;
+      if (g.gated) dell[(size_t)s * g.t + tok] += c;   // gp_m = exp(ell_m)
     } else {
-#pragma unroll
-      for (int a = 0; a < 64; a += 4) {
-        float4 v = *(float4*)(o + a);
-        v.x += dx[a] * fsc;
-        v.y += dx[a + 1] * fsc;
-        v.z += dx[a + 2] * fsc;
-        v.w += dx[a + 3] * fsc;
-        *(float4*)(o + a) = v;
-      }
       // suffix-decay cotangent: -c on ell_tok and +c on ell_end; summed over the
       // chunk this is an exclusive prefix sum (no cancellation), done in gate_finish
       if (g.gated) dellend[(size_t)s * g.t + tok] = c;
-      // second GEMM: dU = phi'(k~) dS~  (A generated, 36 K blocks)
+      // second GEMM: dU = W_j phi'(k_j) dS~  (A generated, 36 K blocks)
       gen_all_kblocks<0, NA>(xp, tm + 384u, lane_off, g_full, g_empty, l);
       mbar_wait(fin, 0);
       tc_fence_after();
@@ -957,10 +1040,10 @@ __global__ void __launch_bounds__(256, 1) k_tc_dphi(const __grid_constant__ CUte
 #pragma unroll
       for (int a = 0; a < 64; a += 4) {
         float4 v = *(float4*)(ov + a);
-        v.x += __uint_as_float(r[a]);
-        v.y += __uint_as_float(r[a + 1]);
-        v.z += __uint_as_float(r[a + 2]);
-        v.w += __uint_as_float(r[a + 3]);
+        v.x += __uint_as_float(r[a]) * fct;
+        v.y += __uint_as_float(r[a + 1]) * fct;
+        v.z += __uint_as_float(r[a + 2]) * fct;
+        v.w += __uint_as_float(r[a + 3]) * fct;
         *(float4*)(ov + a) = v;
       }
     }
@@ -1264,19 +1347,23 @@ struct TcFwdWs {
   int* zflag;
   float* ell;
   float* lamlog;
-  __nv_bfloat16* kt;     // K~^T  [ns*n*64][c]  (reused for Q~^T in the backward)
+  __half* kt;            // K^T   [ns*n*64][c]  exact fp16 transposed copy (reused for Q^T in the backward)
+  __half* vr;            // W_m v_m rows [ns*t][64] (reused for c_m dnum_m in the backward)
+  __half* wa;            // (W_m, 0..) rows [ns*t][16] (reused for (c_m dden_m, 0..))
   float* sp;             // S'_k fp32 [ns][n][FH][80] (reused for dA' in the backward)
-  __nv_bfloat16* stm;    // A'_k [ns][n][FH][64]
-  __nv_bfloat16* std_;   // A'_k score-sum part [ns][n][FH][16]
+  __half* stm;           // A'_k 2^-nbits(k) [ns][n][FH][64]
+  __half* std_;          // score-sum part [ns][n][FH][16]
   float* y32;
 };
 
 struct TcBwdWs {
-  __nv_bfloat16* dN;
-  __nv_bfloat16* dD;
+  __nv_bfloat16* dN;     // dnum (bf16, intra-chunk GEMMs)
+  __half* dN16;          // dnum (fp16, state GEMMs)
+  __half* dD;            // (dden, 0..) fp16
+  __half* v16;           // v rows fp16 [ns*t][64]
   float* dden;
-  __nv_bfloat16* dsm;
-  __nv_bfloat16* dsd;
+  __half* dsm;
+  __half* dsd;
   float* dq32;
   float* dk32;
   float* dv32;
@@ -1303,10 +1390,12 @@ static TcFwdWs carve_fwd(const Geo& g, void* base, size_t* bytes) {
   w.zflag = (int*)take(4);
   w.ell = (float*)take(sizeof(float) * g.ns * g.t);
   w.lamlog = (float*)take(sizeof(float) * g.ns * g.n);
-  w.kt = (__nv_bfloat16*)take(2ull * g.ns * g.t * HD);
+  w.kt = (__half*)take(2ull * g.ns * g.t * HD);
+  w.vr = (__half*)take(2ull * g.ns * g.t * HD);
+  w.wa = (__half*)take(2ull * g.ns * g.t * 16);
   w.sp = (float*)take(4ull * g.ns * g.n * FH * UW);
-  w.stm = (__nv_bfloat16*)take(2ull * g.ns * g.n * ST_MAIN);
-  w.std_ = (__nv_bfloat16*)take(2ull * g.ns * g.n * ST_DEN);
+  w.stm = (__half*)take(2ull * g.ns * g.n * ST_MAIN);
+  w.std_ = (__half*)take(2ull * g.ns * g.n * ST_DEN);
   w.y32 = (float*)take(g.normalize ? 4ull * g.ns * g.t * HD : 0);
   *bytes = take.off;
   return w;
@@ -1316,10 +1405,12 @@ static TcBwdWs carve_bwd(const Geo& g, void* base, size_t* bytes) {
   Take take{(char*)base};
   TcBwdWs b;
   b.dN = (__nv_bfloat16*)take(2ull * g.ns * g.t * HD);
-  b.dD = (__nv_bfloat16*)take(2ull * g.ns * g.t * 16);
+  b.dN16 = (__half*)take(2ull * g.ns * g.t * HD);
+  b.dD = (__half*)take(2ull * g.ns * g.t * 16);
+  b.v16 = (__half*)take(2ull * g.ns * g.t * HD);
   b.dden = (float*)take(4ull * g.ns * g.t);
-  b.dsm = (__nv_bfloat16*)take(2ull * g.ns * g.n * ST_MAIN);
-  b.dsd = (__nv_bfloat16*)take(2ull * g.ns * g.n * ST_DEN);
+  b.dsm = (__half*)take(2ull * g.ns * g.n * ST_MAIN);
+  b.dsd = (__half*)take(2ull * g.ns * g.n * ST_DEN);
   b.dq32 = (float*)take(4ull * g.ns * g.t * HD);
   b.dk32 = (float*)take(4ull * g.ns * g.t * HD);
   b.dv32 = (float*)take(4ull * g.ns * g.t * HD);
@@ -1395,9 +1486,11 @@ int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const 
   size_t need;
   TcFwdWs w = carve_fwd(g, ws, &need);
   const int with_den = (g.normalize || rowsum) ? 1 : 0;
-  CUtensorMap m_q, m_k, m_v, m_v64, m_kt;
+  CUtensorMap m_q, m_k, m_v, m_vr, m_wa, m_kt;
   if (!map_bth(&m_q, q, g, 128) || !map_bth(&m_k, k, g, 128) || !map_bth(&m_v, v, g, 128) ||
-      !map_bth(&m_v64, v, g, 64) || !map_2d(&m_kt, w.kt, (size_t)g.ns * g.n * HD, g.c, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B)) {
+      !map_2d(&m_vr, w.vr, (size_t)g.ns * g.t, HD, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !map_2d(&m_wa, w.wa, (size_t)g.ns * g.t, 16, 16, 64, CU_TENSOR_MAP_SWIZZLE_32B) ||
+      !map_2d(&m_kt, w.kt, (size_t)g.ns * g.n * HD, g.c, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B)) {
     set_error("cuTensorMapEncodeTiled failed");
     return 3;
   }
@@ -1405,12 +1498,14 @@ int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const 
   {
     StageTimer tmr("fwd_prep", st);
     k_tc_prep_gates<<<(g.ns * g.n + 3) / 4, 128, 0, st>>>(g, log_g, w.ell, w.lamlog);
-    k_tc_prep_xt<<<dim3(g.c / 64, g.n, g.ns), 256, 0, st>>>(g, (const __nv_bfloat16*)k, w.ell, w.lamlog, 0, w.kt);
+    k_tc_prep_xt<<<dim3(g.c / 64, g.n, g.ns), 256, 0, st>>>(g, (const __nv_bfloat16*)k, w.ell, w.lamlog, 2, w.kt);
+    k_tc_prep_rows<<<(unsigned)(((size_t)g.ns * g.t + 255) / 256), 256, 0, st>>>(
+        g, 0, (const __nv_bfloat16*)v, w.ell, w.lamlog, nullptr, w.vr, with_den ? w.wa : nullptr);
   }
   {
     StageTimer tmr("fwd_update_state", st);
     cudaFuncSetAttribute(k_tc_featmajor<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fm::SMEM);
-    k_tc_featmajor<false><<<dim3((NTH + 3) / 4, g.n, g.ns), 256, fm::SMEM, st>>>(m_kt, m_v64, m_v64, g, with_den,
+    k_tc_featmajor<false><<<dim3((NTH + 3) / 4, g.n, g.ns), 256, fm::SMEM, st>>>(m_kt, m_vr, m_wa, g, with_den,
                                                                                  w.sp);
   }
   {
@@ -1441,14 +1536,16 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
   const int uc = den ? UW : 64;
   CUtensorMap m_qt, m_dn, m_dd, m_v128, m_dummy;
   if (!map_2d(&m_qt, w.kt, (size_t)g.ns * g.n * HD, g.c, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !map_2d(&m_dn, b.dN, (size_t)g.ns * g.t, HD, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !map_2d(&m_dd, b.dD, (size_t)g.ns * g.t, 16, 16, 64, CU_TENSOR_MAP_SWIZZLE_32B) ||
+      !map_2d(&m_dn, w.vr, (size_t)g.ns * g.t, HD, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !map_2d(&m_dd, w.wa, (size_t)g.ns * g.t, 16, 16, 64, CU_TENSOR_MAP_SWIZZLE_32B) ||
       !map_bth(&m_v128, v, g, 128)) {
     set_error("cuTensorMapEncodeTiled failed");
     return 3;
   }
-  CUtensorMap m_dn128, m_dd128;
+  CUtensorMap m_dn128, m_dd128, m_dn16, m_v16;
   if (!map_2d(&m_dn128, b.dN, (size_t)g.ns * g.t, HD, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !map_2d(&m_dn16, b.dN16, (size_t)g.ns * g.t, HD, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !map_2d(&m_v16, b.v16, (size_t)g.ns * g.t, HD, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !map_2d(&m_dd128, b.dD, (size_t)g.ns * g.t, 16, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B)) {
     set_error("cuTensorMapEncodeTiled failed");
     return 3;
@@ -1463,8 +1560,12 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
     cudaMemsetAsync(b.cu, 0, 4ull * g.ns * g.t, st);
     cudaMemsetAsync(b.dlam, 0, 4ull * g.ns * g.n, st);
     k_tc_bwd_prep<<<(unsigned)(((size_t)g.ns * g.t + 255) / 256), 256, 0, st>>>(
-        g, (const __nv_bfloat16*)dy, w.y32, rowsum, b.dN, den ? b.dD : nullptr, b.dden);
-    k_tc_prep_xt<<<dim3(g.c / 64, g.n, g.ns), 256, 0, st>>>(g, (const __nv_bfloat16*)q, w.ell, w.lamlog, 1, w.kt);
+        g, (const __nv_bfloat16*)dy, w.y32, rowsum, b.dN, b.dN16, den ? b.dD : nullptr, b.dden);
+    k_tc_prep_rows<<<(unsigned)(((size_t)g.ns * g.t + 255) / 256), 256, 0, st>>>(
+        g, 2, (const __nv_bfloat16*)v, w.ell, w.lamlog, nullptr, b.v16, nullptr);
+    k_tc_prep_xt<<<dim3(g.c / 64, g.n, g.ns), 256, 0, st>>>(g, (const __nv_bfloat16*)q, w.ell, w.lamlog, 2, w.kt);
+    k_tc_prep_rows<<<(unsigned)(((size_t)g.ns * g.t + 255) / 256), 256, 0, st>>>(
+        g, 1, b.dN, w.ell, w.lamlog, den ? b.dden : nullptr, w.vr, den ? w.wa : nullptr);
   }
   if (g.n > 1) {
     StageTimer tmr("bwd_query_state_dA", st);
@@ -1494,14 +1595,14 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
     StageTimer tmr("bwd_query_state_dq", st);
     cudaFuncSetAttribute(k_tc_dphi<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dp::SMEM);
     k_tc_dphi<false><<<dim3(g.c / 128, g.n - 1, g.ns), 256, dp::SMEM, st>>>(
-        m_dn128, m_dd128, g, (const __nv_bfloat16*)q, w.ell, w.lamlog, w.stm, w.std_, den, b.dq32, nullptr, b.dell,
+        m_dn16, m_dd128, g, (const __nv_bfloat16*)q, w.ell, w.lamlog, w.stm, w.std_, den, b.dq32, nullptr, b.dell,
         nullptr);
   }
   {
     StageTimer tmr("bwd_update_state", st);
     cudaFuncSetAttribute(k_tc_dphi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dp::SMEM);
     k_tc_dphi<true><<<dim3(g.c / 128, g.n, g.ns), 256, dp::SMEM, st>>>(
-        m_v128, m_dummy, g, (const __nv_bfloat16*)k, w.ell, w.lamlog, b.dsm, b.dsd, den, b.dk32, b.dv32, b.dell,
+        m_v16, m_dummy, g, (const __nv_bfloat16*)k, w.ell, w.lamlog, b.dsm, b.dsd, den, b.dk32, b.dv32, b.dell,
         b.cu);
   }
   {

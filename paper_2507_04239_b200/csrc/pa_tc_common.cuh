@@ -58,8 +58,22 @@ constexpr BlkTab kBlk = make_blk_tab();
 __host__ __device__ constexpr int slot_a(int f, const BlkTab& t) { return 4 * t.al[f >> 5] + ((f >> 3) & 3); }
 __host__ __device__ constexpr int slot_b(int f, const BlkTab& t) { return 8 * t.be[f >> 5] + (f & 7); }
 
+// State-path precision: phi', stored states and the operands of every state
+// GEMM are fp16 (10-bit mantissa; same tensor-core rate as bf16).  Stored
+// states carry a per-chunk power-of-two scale so long ungated sums stay in
+// range: A'_k is stored as A'_k * 2^-nbits(k), the backward state cotangent
+// G_k as G_k * 2^-nbits(n-1-k).
+__host__ __device__ inline float pow2_neg_bits(int k) {  // 2^-(number of bits of k)
+  int e = 0;
+  while (k) {
+    ++e;
+    k >>= 1;
+  }
+  return 1.f / (float)(1 << e);
+}
+
 // ---------------------------------------------------------------- generation
-// phi'(x) columns of feature block B (16 bf16x2 columns): column i*4 + jp holds
+// phi'(x) columns of feature block B (16 fp16x2 columns): column i*4 + jp holds
 // features (4 al + i, 8 be + 2 jp) and (4 al + i, 8 be + 2 jp + 1).
 template <int A>
 __device__ __forceinline__ uint32_t bcast_x(const uint32_t* xp) {
@@ -76,7 +90,7 @@ __device__ __forceinline__ void gen_fblock(const uint32_t* xp, uint32_t* o) {
     if (i == 2) bc = bcast_x<4 * al + 2>(xp);
     if (i == 3) bc = bcast_x<4 * al + 3>(xp);
 #pragma unroll
-    for (int jp = 0; jp < 4; ++jp) o[i * 4 + jp] = sm100::hmul2_bf16(bc, xp[4 * be + jp]);
+    for (int jp = 0; jp < 4; ++jp) o[i * 4 + jp] = sm100::hmul2_f16(bc, xp[4 * be + jp]);
   }
 }
 
