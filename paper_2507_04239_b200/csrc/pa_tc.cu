@@ -323,26 +323,47 @@ constexpr size_t ST_DEN = (size_t)FH * 16;    // bf16 elements, score-sum part
 
 // ==========================================================================
 // forward scan (discumsum over chunk states, chunked.py:156-176 / 356-367):
-//   A'_k = lambda_k A'_{k-1} + omega * S'_k   (fp32 running sum, bf16 stores)
-// thread per (slot, column); grid (ceil(FH*ucols/256), stream)
+//   A'_k = lambda_k A'_{k-1} + omega * S'_k   (fp32 running sum, fp16 stores)
+// HBM-bound: each thread owns 4 consecutive columns of one slot (float4 loads,
+// 8-byte fp16 stores) and prefetches SCAN_PF chunks ahead so that every thread
+// keeps several independent loads in flight.  grid (ceil(FH*ucols/4/256), stream)
 // ==========================================================================
+constexpr int SCAN_PF = 8;
+
+__device__ __forceinline__ uint8_t* state_elem_ptr(__half* st_main, __half* st_den, size_t sk, int f, int u) {
+  return u < 64 ? (uint8_t*)(st_main + sk * ST_MAIN) + sw128_elem(f, u)
+                : (uint8_t*)(st_den + sk * ST_DEN) + sw32_elem(f, u - 64);
+}
+
 __global__ void __launch_bounds__(256) k_tc_scan_fwd(Geo g, int ucols, const float* __restrict__ lamlog,
                                                      const float* __restrict__ sp, __half* st_main,
                                                      __half* st_den) {
   const int s = blockIdx.y;
-  const int e = blockIdx.x * 256 + threadIdx.x;
+  const int e = (blockIdx.x * 256 + threadIdx.x) * 4;
   if (e >= FH * ucols) return;
   const int f = e / ucols, u = e - f * ucols;
   const float om = slot_omega(f);
-  float acc = 0.f;
-  for (int k = 0; k < g.n; ++k) {
-    const float lam = k == 0 ? 0.f : (g.gated ? __expf(lamlog[s * g.n + k]) : 1.f);
-    acc = lam * acc + om * sp[((size_t)(s * g.n + k) * FH + f) * UW + u];
-    const __half v = __float2half_rn(acc * pow2_neg_bits(k));
-    if (u < 64)
-      *(__half*)((uint8_t*)(st_main + (size_t)(s * g.n + k) * ST_MAIN) + sw128_elem(f, u)) = v;
-    else
-      *(__half*)((uint8_t*)(st_den + (size_t)(s * g.n + k) * ST_DEN) + sw32_elem(f, u - 64)) = v;
+  const float* src = sp + ((size_t)s * g.n * FH + f) * UW + u;
+  const size_t kstride = (size_t)FH * UW;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int k0 = 0; k0 < g.n; k0 += SCAN_PF) {
+    float4 x[SCAN_PF];
+#pragma unroll
+    for (int i = 0; i < SCAN_PF; ++i)
+      if (k0 + i < g.n) x[i] = __ldcs((const float4*)(src + (size_t)(k0 + i) * kstride));
+#pragma unroll
+    for (int i = 0; i < SCAN_PF; ++i) {
+      const int k = k0 + i;
+      if (k >= g.n) break;
+      const float lam = k == 0 ? 0.f : (g.gated ? __expf(lamlog[s * g.n + k]) : 1.f);
+      acc.x = fmaf(lam, acc.x, om * x[i].x);
+      acc.y = fmaf(lam, acc.y, om * x[i].y);
+      acc.z = fmaf(lam, acc.z, om * x[i].z);
+      acc.w = fmaf(lam, acc.w, om * x[i].w);
+      const float sc = pow2_neg_bits(k);
+      *(uint2*)state_elem_ptr(st_main, st_den, (size_t)s * g.n + k, f, u) =
+          make_uint2(pack_f16(acc.x * sc, acc.y * sc), pack_f16(acc.z * sc, acc.w * sc));
+    }
   }
 }
 
@@ -772,42 +793,67 @@ __global__ void __launch_bounds__(256) k_tc_bwd_prep(Geo g, const __nv_bfloat16*
 // backward scan (discumsum VJP, gradients.py:267-288) over chunk states:
 //   G_k = dA'_k + lambda_{k+1} G_{k+1};  dlambda_k = <A'_{k-1}, G_k>;  dS~_k = omega G_k
 // dA'_k comes from the feature-major GEMM (fp32, slot k holds dA'_k for k <= n-2).
-// thread per (slot, column); grid (ceil(FH*ucols/256), stream)
+// 4 columns per thread with SCAN_PF-deep prefetch; the dlambda reduction is
+// per-warp into shared memory, then one non-atomic partial per (block, chunk):
+// dlam_part[(s*n + k) * gridDim.x + block], summed by k_tc_gate_finish.
+// grid (ceil(FH*ucols/4/256), stream)
 __global__ void __launch_bounds__(256) k_tc_scan_bwd(Geo g, int ucols, const float* __restrict__ lamlog,
                                                      const float* __restrict__ dA,
                                                      const __half* __restrict__ st_main,
                                                      const __half* __restrict__ st_den,
-                                                     __half* ds_main, __half* ds_den, float* dlam) {
-  __shared__ float red[32];
-  const int s = blockIdx.y;
-  const int e = blockIdx.x * 256 + threadIdx.x;
+                                                     __half* ds_main, __half* ds_den, float* dlam_part) {
+  extern __shared__ float red[];  // [n][8]
+  const int s = blockIdx.y, wq = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int e = (blockIdx.x * 256 + threadIdx.x) * 4;
   const bool ok = e < FH * ucols;
   const int f = ok ? e / ucols : 0, u = ok ? e - f * ucols : 0;
   const float om = ok ? slot_omega(f) : 0.f;
-  float G = 0.f;
-  for (int k = g.n - 1; k >= 0; --k) {
-    const float lam_next = (k + 1 < g.n) ? (g.gated ? __expf(lamlog[s * g.n + k + 1]) : 1.f) : 0.f;
-    const float dAk = (ok && k + 1 < g.n) ? dA[((size_t)(s * g.n + k) * FH + f) * UW + u] : 0.f;
-    G = dAk + lam_next * G;
-    if (ok) {
-      const __half v = __float2half_rn(om * G * pow2_neg_bits(g.n - 1 - k));
-      if (u < 64)
-        *(__half*)((uint8_t*)(ds_main + (size_t)(s * g.n + k) * ST_MAIN) + sw128_elem(f, u)) = v;
-      else
-        *(__half*)((uint8_t*)(ds_den + (size_t)(s * g.n + k) * ST_DEN) + sw32_elem(f, u - 64)) = v;
-    }
-    if (k >= 1) {
-      float a = 0.f;
-      if (ok) {
-        const __half* src =
-            u < 64 ? (const __half*)((const uint8_t*)(st_main + (size_t)(s * g.n + k - 1) * ST_MAIN) + sw128_elem(f, u))
-                   : (const __half*)((const uint8_t*)(st_den + (size_t)(s * g.n + k - 1) * ST_DEN) +
-                                     sw32_elem(f, u - 64));
-        a = __half2float(*src) / pow2_neg_bits(k - 1) * G;
+  const float* src = dA + ((size_t)s * g.n * FH + f) * UW + u;
+  const size_t kstride = (size_t)FH * UW;
+  float4 G = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int k1 = g.n - 1; k1 >= 0; k1 -= SCAN_PF) {
+    float4 x[SCAN_PF];
+    uint2 a[SCAN_PF];
+#pragma unroll
+    for (int i = 0; i < SCAN_PF; ++i) {
+      const int k = k1 - i;
+      x[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      a[i] = make_uint2(0u, 0u);
+      if (ok && k >= 0) {
+        if (k + 1 < g.n) x[i] = __ldcs((const float4*)(src + (size_t)k * kstride));
+        if (k >= 1)
+          a[i] = *(const uint2*)state_elem_ptr(const_cast<__half*>(st_main), const_cast<__half*>(st_den),
+                                               (size_t)s * g.n + k - 1, f, u);
       }
-      const float tot = block_sum(a, red);
-      if (threadIdx.x == 0 && g.gated) atomicAdd(dlam + s * g.n + k, tot);
     }
+#pragma unroll
+    for (int i = 0; i < SCAN_PF; ++i) {
+      const int k = k1 - i;
+      if (k < 0) break;
+      const float lam_next = (k + 1 < g.n) ? (g.gated ? __expf(lamlog[s * g.n + k + 1]) : 1.f) : 0.f;
+      G.x = fmaf(lam_next, G.x, x[i].x);
+      G.y = fmaf(lam_next, G.y, x[i].y);
+      G.z = fmaf(lam_next, G.z, x[i].z);
+      G.w = fmaf(lam_next, G.w, x[i].w);
+      if (ok) {
+        const float sc = om * pow2_neg_bits(g.n - 1 - k);
+        *(uint2*)state_elem_ptr(ds_main, ds_den, (size_t)s * g.n + k, f, u) =
+            make_uint2(pack_f16(G.x * sc, G.y * sc), pack_f16(G.z * sc, G.w * sc));
+      }
+      if (k >= 1) {
+        const float2 a01 = __half22float2(*(const __half2*)&a[i].x), a23 = __half22float2(*(const __half2*)&a[i].y);
+        float t = a01.x * G.x + a01.y * G.y + a23.x * G.z + a23.y * G.w;
+        t = warp_sum(t);
+        if (lane == 0) red[k * 8 + wq] = t / pow2_neg_bits(k - 1);
+      }
+    }
+  }
+  __syncthreads();
+  for (int k = 1 + threadIdx.x; k < g.n; k += 256) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += red[k * 8 + i];
+    dlam_part[((size_t)s * g.n + k) * gridDim.x + blockIdx.x] = t;
   }
 }
 
@@ -862,7 +908,9 @@ __global__ void __launch_bounds__(256, 1) k_tc_dphi(const __grid_constant__ CUte
                                                     const float* __restrict__ lamlog,
                                                     const __half* __restrict__ b_main,
                                                     const __half* __restrict__ b_den, int with_den,
-                                                    float* dx32, float* dv32, float* dell, float* dellend) {
+                                                    const float* __restrict__ dx32, const float* __restrict__ dv32,
+                                                    float* dell, float* dellend, __nv_bfloat16* dxo,
+                                                    __nv_bfloat16* dvo) {
   using namespace dp;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -883,10 +931,19 @@ __global__ void __launch_bounds__(256, 1) k_tc_dphi(const __grid_constant__ CUte
   __shared__ float red_s[4];
 
   const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
-  const int I = blockIdx.x, k = blockIdx.y + (kUpd ? 0 : 1), s = blockIdx.z;
-  const int bi = s / g.h, hi = s % g.h;
+  const int I = blockIdx.x, k = blockIdx.y, s = blockIdx.z;
   const int tok0 = k * g.c + I * 128;
   const bool den = with_den != 0;
+  if (!kUpd && k == 0) {
+    // chunk 0 has no state query: its dq is the intra-chunk part alone
+    for (int i = tid; i < 128 * 16; i += 256) {
+      const int r = i >> 4, c4 = (i & 15) * 4;
+      const float4 v = *(const float4*)(dx32 + ((size_t)s * g.t + tok0 + r) * HD + c4);
+      uint2 o2 = make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
+      *(uint2*)(dxo + rowid(g, s, tok0 + r) * HD + c4) = o2;
+    }
+    return;
+  }
   const int bslot = kUpd ? k : k - 1;    // state index the B operand comes from
   const __half* bm = b_main + (size_t)(s * g.n + bslot) * ST_MAIN;
   const __half* bd = b_den + (size_t)(s * g.n + bslot) * ST_DEN;
@@ -1012,15 +1069,18 @@ __global__ void __launch_bounds__(256, 1) k_tc_dphi(const __grid_constant__ CUte
 #pragma unroll
     for (int a = 0; a < 64; ++a) c = fmaf(dx[a], x[a], c);
     c *= 0.5f * fct;   // = d<.,.>/d(log factor): degree-2 homogeneity of phi'
-    float* o = dx32 + ((size_t)s * g.t + tok) * HD;
+    {
+      // final gradient row = intra-chunk part (fp32) + this state part, stored once in bf16
+      const float* o = dx32 + ((size_t)s * g.t + tok) * HD;
+      uint4* dst = (uint4*)(dxo + rowid(g, s, tok) * HD);
 #pragma unroll
-    for (int a = 0; a < 64; a += 4) {
-      float4 v = *(float4*)(o + a);
-      v.x += dx[a] * fct;
-      v.y += dx[a + 1] * fct;
-      v.z += dx[a + 2] * fct;
-      v.w += dx[a + 3] * fct;
-      *(float4*)(o + a) = v;
+      for (int a = 0; a < 64; a += 8) {
+        const float4 v0 = *(const float4*)(o + a), v1 = *(const float4*)(o + a + 4);
+        dst[a / 8] = make_uint4(pack_bf16(fmaf(dx[a], fct, v0.x), fmaf(dx[a + 1], fct, v0.y)),
+                                pack_bf16(fmaf(dx[a + 2], fct, v0.z), fmaf(dx[a + 3], fct, v0.w)),
+                                pack_bf16(fmaf(dx[a + 4], fct, v1.x), fmaf(dx[a + 5], fct, v1.y)),
+                                pack_bf16(fmaf(dx[a + 6], fct, v1.z), fmaf(dx[a + 7], fct, v1.w)));
+      }
     }
     if (!kUpd) {
       if (g.gated) dell[(size_t)s * g.t + tok] += c;   // gp_m = exp(ell_m)
@@ -1036,15 +1096,16 @@ __global__ void __launch_bounds__(256, 1) k_tc_dphi(const __grid_constant__ CUte
       tmem_ld32(tm + 256u + lane_off, r);
       tmem_ld32(tm + 256u + lane_off + 32, r + 32);
       tc_wait_ld();
-      float* ov = dv32 + ((size_t)s * g.t + tok) * HD;
+      const float* ov = dv32 + ((size_t)s * g.t + tok) * HD;
+      uint4* dst = (uint4*)(dvo + rowid(g, s, tok) * HD);
 #pragma unroll
-      for (int a = 0; a < 64; a += 4) {
-        float4 v = *(float4*)(ov + a);
-        v.x += __uint_as_float(r[a]) * fct;
-        v.y += __uint_as_float(r[a + 1]) * fct;
-        v.z += __uint_as_float(r[a + 2]) * fct;
-        v.w += __uint_as_float(r[a + 3]) * fct;
-        *(float4*)(ov + a) = v;
+      for (int a = 0; a < 64; a += 8) {
+        const float4 v0 = *(const float4*)(ov + a), v1 = *(const float4*)(ov + a + 4);
+        float f[8];
+#pragma unroll
+        for (int z = 0; z < 8; ++z) f[z] = __uint_as_float(r[a + z]) * fct;
+        dst[a / 8] = make_uint4(pack_bf16(f[0] + v0.x, f[1] + v0.y), pack_bf16(f[2] + v0.z, f[3] + v0.w),
+                                pack_bf16(f[4] + v1.x, f[5] + v1.y), pack_bf16(f[6] + v1.z, f[7] + v1.w));
       }
     }
     (void)red_s;
@@ -1276,28 +1337,18 @@ __global__ void __launch_bounds__(256, 1) k_tc_intra_bwd(const __grid_constant__
     tc_wait_ld();
     float* oa = out_a + tokr * HD;
 #pragma unroll
-    for (int a = 0; a < 64; a += 4) {
-      float4 v4 = *(float4*)(oa + a);
-      v4.x += __uint_as_float(r[a]);
-      v4.y += __uint_as_float(r[a + 1]);
-      v4.z += __uint_as_float(r[a + 2]);
-      v4.w += __uint_as_float(r[a + 3]);
-      *(float4*)(oa + a) = v4;
-    }
+    for (int a = 0; a < 64; a += 4)
+      *(float4*)(oa + a) = make_float4(__uint_as_float(r[a]), __uint_as_float(r[a + 1]), __uint_as_float(r[a + 2]),
+                                       __uint_as_float(r[a + 3]));
     if (kKV) {
       tmem_ld32(tB + lane_off, r);
       tmem_ld32(tB + lane_off + 32, r + 32);
       tc_wait_ld();
       float* ob = out_b + tokr * HD;
 #pragma unroll
-      for (int a = 0; a < 64; a += 4) {
-        float4 v4 = *(float4*)(ob + a);
-        v4.x += __uint_as_float(r[a]);
-        v4.y += __uint_as_float(r[a + 1]);
-        v4.z += __uint_as_float(r[a + 2]);
-        v4.w += __uint_as_float(r[a + 3]);
-        *(float4*)(ob + a) = v4;
-      }
+      for (int a = 0; a < 64; a += 4)
+        *(float4*)(ob + a) = make_float4(__uint_as_float(r[a]), __uint_as_float(r[a + 1]), __uint_as_float(r[a + 2]),
+                                         __uint_as_float(r[a + 3]));
     }
     if (g.gated) dell[tokr] += kKV ? -red : red;
   }
@@ -1310,12 +1361,16 @@ __global__ void __launch_bounds__(256, 1) k_tc_intra_bwd(const __grid_constant__
 //   dlog g_u = sum_{m >= u} dell_m + dlam_k lam_k + sum_{m < u} cu_m
 __global__ void __launch_bounds__(128) k_tc_gate_finish(Geo g, const float* __restrict__ lamlog,
                                                         const float* __restrict__ dell, const float* __restrict__ cu,
-                                                        const float* __restrict__ dlam, float* dlogg) {
+                                                        const float* __restrict__ dlam_part, int nparts,
+                                                        float* dlogg) {
   const int wid = blockIdx.x * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (wid >= g.ns * g.n) return;
   const int s = wid / g.n, k = wid - s * g.n;
   const int s0 = k * g.c, s1 = s0 + g.c;
-  const float base = k >= 1 ? dlam[wid] * __expf(lamlog[wid]) : 0.f;
+  float dl = 0.f;
+  for (int i = lane; i < nparts; i += 32) dl += dlam_part[(size_t)wid * nparts + i];
+  dl = warp_sum(dl);
+  const float base = k >= 1 ? dl * __expf(lamlog[wid]) : 0.f;
   // pass 1: prefix of cu (exclusive) and suffix of dell (inclusive) in 32-token steps
   float tot_dell = 0.f;
   for (int m0 = s0; m0 < s1; m0 += 32) tot_dell += warp_sum(dell[(size_t)s * g.t + m0 + lane]);
@@ -1372,6 +1427,7 @@ struct TcBwdWs {
   float* dlam;
 };
 
+static int scan_blocks(int ucols) { return (FH * ucols / 4 + 255) / 256; }
 static size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Take {
@@ -1416,7 +1472,7 @@ static TcBwdWs carve_bwd(const Geo& g, void* base, size_t* bytes) {
   b.dv32 = (float*)take(4ull * g.ns * g.t * HD);
   b.dell = (float*)take(4ull * g.ns * g.t);
   b.cu = (float*)take(4ull * g.ns * g.t);
-  b.dlam = (float*)take(4ull * g.ns * g.n);
+  b.dlam = (float*)take(4ull * g.ns * g.n * scan_blocks(UW));   // per-block dlambda partials
   *bytes = take.off;
   return b;
 }
@@ -1462,9 +1518,21 @@ static bool encode(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t* 
                    const cuuint32_t* box, CUtensorMapSwizzle sw) {
   cuuint32_t es[5] = {1, 1, 1, 1, 1};
   EncodeTiledFn fn = encode_fn();
-  return fn && fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled: driver entry point unavailable");
+    return false;
+  }
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[256];
+    snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (CUresult %d): ptr %p rank %d dims0 %llu dims1 %llu box %u x %u",
+             (int)r, ptr, rank, (unsigned long long)dims[0], (unsigned long long)dims[1], box[0], box[1]);
+    set_error(buf);
+    return false;
+  }
+  return true;
 }
 // [b][t][h][64] bf16, box of `box_tokens` tokens of one (b, h) stream
 static bool map_bth(CUtensorMap* m, const void* ptr, const Geo& g, int box_tokens) {
@@ -1481,17 +1549,26 @@ static bool map_2d(CUtensorMap* m, const void* ptr, size_t rows, int cols, int b
   return encode(m, ptr, 2, dims, strides, box, sw);
 }
 
+// The driver-API tensor-map encoder needs the device's primary context to be
+// current on the calling thread; torch's autograd worker threads may not have
+// bound it yet (CUresult 201).  Bind the context that owns the operand.
+static void bind_context_of(const void* ptr) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, ptr) == cudaSuccess && at.device >= 0) cudaSetDevice(at.device);
+  cudaGetLastError();
+}
+
 int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const float* log_g, void* y, float* rowsum,
                void* ws, cudaStream_t st) {
   size_t need;
   TcFwdWs w = carve_fwd(g, ws, &need);
+  bind_context_of(q);
   const int with_den = (g.normalize || rowsum) ? 1 : 0;
   CUtensorMap m_q, m_k, m_v, m_vr, m_wa, m_kt;
   if (!map_bth(&m_q, q, g, 128) || !map_bth(&m_k, k, g, 128) || !map_bth(&m_v, v, g, 128) ||
       !map_2d(&m_vr, w.vr, (size_t)g.ns * g.t, HD, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !map_2d(&m_wa, w.wa, (size_t)g.ns * g.t, 16, 16, 64, CU_TENSOR_MAP_SWIZZLE_32B) ||
       !map_2d(&m_kt, w.kt, (size_t)g.ns * g.n * HD, g.c, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B)) {
-    set_error("cuTensorMapEncodeTiled failed");
     return 3;
   }
   cudaMemsetAsync(w.zflag, 0, 4, st);
@@ -1511,7 +1588,7 @@ int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const 
   {
     StageTimer tmr("fwd_discumsum", st);
     const int uc = with_den ? UW : 64;
-    k_tc_scan_fwd<<<dim3((FH * uc + 255) / 256, g.ns), 256, 0, st>>>(g, uc, w.lamlog, w.sp, w.stm, w.std_);
+    k_tc_scan_fwd<<<dim3((FH * uc / 4 + 255) / 256, g.ns), 256, 0, st>>>(g, uc, w.lamlog, w.sp, w.stm, w.std_);
   }
   {
     StageTimer tmr("fwd_attn_query", st);
@@ -1532,6 +1609,7 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
   size_t n1, n2;
   TcFwdWs w = carve_fwd(g, const_cast<void*>(fwd_ws), &n1);  // sp / kt are dead after the forward: reused
   TcBwdWs b = carve_bwd(g, bwd_ws, &n2);
+  bind_context_of(q);
   const int den = g.normalize ? 1 : 0;   // the backward needs the score sum only when normalizing
   const int uc = den ? UW : 64;
   CUtensorMap m_qt, m_dn, m_dd, m_v128, m_dummy;
@@ -1539,7 +1617,6 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
       !map_2d(&m_dn, w.vr, (size_t)g.ns * g.t, HD, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !map_2d(&m_dd, w.wa, (size_t)g.ns * g.t, 16, 16, 64, CU_TENSOR_MAP_SWIZZLE_32B) ||
       !map_bth(&m_v128, v, g, 128)) {
-    set_error("cuTensorMapEncodeTiled failed");
     return 3;
   }
   CUtensorMap m_dn128, m_dd128, m_dn16, m_v16;
@@ -1547,18 +1624,14 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
       !map_2d(&m_dn16, b.dN16, (size_t)g.ns * g.t, HD, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !map_2d(&m_v16, b.v16, (size_t)g.ns * g.t, HD, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !map_2d(&m_dd128, b.dD, (size_t)g.ns * g.t, 16, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B)) {
-    set_error("cuTensorMapEncodeTiled failed");
     return 3;
   }
   m_dummy = m_dn;
   {
     StageTimer tmr("bwd_prep", st);
-    cudaMemsetAsync(b.dq32, 0, 4ull * g.ns * g.t * HD, st);
-    cudaMemsetAsync(b.dk32, 0, 4ull * g.ns * g.t * HD, st);
-    cudaMemsetAsync(b.dv32, 0, 4ull * g.ns * g.t * HD, st);
     cudaMemsetAsync(b.dell, 0, 4ull * g.ns * g.t, st);
     cudaMemsetAsync(b.cu, 0, 4ull * g.ns * g.t, st);
-    cudaMemsetAsync(b.dlam, 0, 4ull * g.ns * g.n, st);
+    cudaMemsetAsync(b.dlam, 0, 4ull * g.ns * g.n * scan_blocks(uc), st);
     k_tc_bwd_prep<<<(unsigned)(((size_t)g.ns * g.t + 255) / 256), 256, 0, st>>>(
         g, (const __nv_bfloat16*)dy, w.y32, rowsum, b.dN, b.dN16, den ? b.dD : nullptr, b.dden);
     k_tc_prep_rows<<<(unsigned)(((size_t)g.ns * g.t + 255) / 256), 256, 0, st>>>(
@@ -1574,14 +1647,16 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
   }
   {
     StageTimer tmr("bwd_discumsum", st);
-    k_tc_scan_bwd<<<dim3((FH * uc + 255) / 256, g.ns), 256, 0, st>>>(g, uc, w.lamlog, w.sp, w.stm, w.std_, b.dsm,
-                                                                      b.dsd, b.dlam);
+    const int red_bytes = 8 * 4 * g.n;
+    if (red_bytes > 48 * 1024)
+      cudaFuncSetAttribute(k_tc_scan_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, red_bytes);
+    k_tc_scan_bwd<<<dim3(scan_blocks(uc), g.ns), 256, red_bytes, st>>>(g, uc, w.lamlog, w.sp, w.stm, w.std_,
+                                                                          b.dsm, b.dsd, b.dlam);
   }
   {
     StageTimer tmr("bwd_intra", st);
     CUtensorMap m_q128, m_k128;
     if (!map_bth(&m_q128, q, g, 128) || !map_bth(&m_k128, k, g, 128)) {
-      set_error("cuTensorMapEncodeTiled failed");
       return 3;
     }
     cudaFuncSetAttribute(k_tc_intra_bwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ib::SMEM);
@@ -1591,29 +1666,27 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
     k_tc_intra_bwd<false><<<dim3(g.c / 128, g.n, g.ns), 256, ib::SMEM, st>>>(m_q128, m_k128, m_v128, m_dn128, g,
                                                                              w.ell, b.dden, b.dq32, nullptr, b.dell);
   }
-  if (g.n > 1) {
+  {
     StageTimer tmr("bwd_query_state_dq", st);
     cudaFuncSetAttribute(k_tc_dphi<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dp::SMEM);
-    k_tc_dphi<false><<<dim3(g.c / 128, g.n - 1, g.ns), 256, dp::SMEM, st>>>(
+    k_tc_dphi<false><<<dim3(g.c / 128, g.n, g.ns), 256, dp::SMEM, st>>>(
         m_dn16, m_dd128, g, (const __nv_bfloat16*)q, w.ell, w.lamlog, w.stm, w.std_, den, b.dq32, nullptr, b.dell,
-        nullptr);
+        nullptr, (__nv_bfloat16*)dq, nullptr);
   }
   {
     StageTimer tmr("bwd_update_state", st);
     cudaFuncSetAttribute(k_tc_dphi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dp::SMEM);
     k_tc_dphi<true><<<dim3(g.c / 128, g.n, g.ns), 256, dp::SMEM, st>>>(
         m_v16, m_dummy, g, (const __nv_bfloat16*)k, w.ell, w.lamlog, b.dsm, b.dsd, den, b.dk32, b.dv32, b.dell,
-        b.cu);
+        b.cu, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv);
   }
   {
     StageTimer tmr("bwd_finish", st);
     if (dlog_g) {
-      k_tc_gate_finish<<<(g.ns * g.n + 3) / 4, 128, 0, st>>>(g, w.lamlog, b.dell, b.cu, b.dlam, dlog_g);
+      k_tc_gate_finish<<<(g.ns * g.n + 3) / 4, 128, 0, st>>>(g, w.lamlog, b.dell, b.cu, b.dlam, scan_blocks(uc),
+                                                             dlog_g);
       count_launch();
     }
-    if (int rc = simt_finalize_bf16(g, b.dq32, HD, dq, st)) return rc;
-    if (int rc = simt_finalize_bf16(g, b.dk32, HD, dk, st)) return rc;
-    if (int rc = simt_finalize_bf16(g, b.dv32, HD, dv, st)) return rc;
   }
   count_launch(8);
   return cuda_check("tc backward");
