@@ -139,8 +139,10 @@ __global__ void __launch_bounds__(256) k_tc_prep_rows(Geo g, int mode, const __n
 // X~^T tiles, B = per-token rows (MN-major) + a 16-column score-sum block.
 //   forward  (update_state, kernels.py:55-83):  X~ = K~, B = [V | 1]     -> S'_k
 //   backward (query_state VJP, gradients.py:429-430): X~ = Q~, B = [dnum | dden] -> dA'_{k-1}
-// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM owner,
-// w4..w7 generate A (lane quadrant = warp % 4) and run the epilogue.
+// Warp roles (384 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM owner,
+// w4..w11 generate A and run the epilogue: lane quadrant = warp % 4, tile
+// pair = (warp - 4) / 4, so two generation warps share each SM sub-partition
+// and every warp issues all its shared-memory loads before its multiplies.
 // grid (group of 4 tiles, chunk, stream)
 // ==========================================================================
 namespace fm {
@@ -152,13 +154,15 @@ constexpr int B_B = 64 * 128;         // 64 tokens x 64 values bf16
 constexpr int B16_B = 64 * 32;        // 64 tokens x 16 bf16 (SW32)
 constexpr int SMEM_USED = 1024 + ST * (XT_B + B_B + B16_B) + 2048 + 512;
 constexpr int SMEM = SMEM_USED > 120 * 1024 ? SMEM_USED : 120 * 1024;  // 1 CTA (512 TMEM cols) per SM
+constexpr int THREADS = 384;
+constexpr int GEN_WARPS = 8;
 }  // namespace fm
 
-template <bool kBwd>
-__global__ void __launch_bounds__(256, 1) k_tc_featmajor(const __grid_constant__ CUtensorMap tm_xt,
+template <bool kBwd, int kDen>
+__global__ void __launch_bounds__(fm::THREADS, 1) k_tc_featmajor(const __grid_constant__ CUtensorMap tm_xt,
                                                          const __grid_constant__ CUtensorMap tm_b,
                                                          const __grid_constant__ CUtensorMap tm_b16, Geo g,
-                                                         int with_den, float* out) {
+                                                         float* out) {
   using namespace fm;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keep the shared address space
@@ -179,7 +183,7 @@ __global__ void __launch_bounds__(256, 1) k_tc_featmajor(const __grid_constant__
   const int slot = kBwd ? kin - 1 : kin;
   const int t0 = grp * 4, nt = min(4, NTH - t0);
   const int nsub = g.c / 32, nstage = g.c / TOK;
-  const bool den = with_den != 0;
+  constexpr bool den = kDen != 0;   // compile-time: a predicated-off tcgen05.mma still costs an issue slot
 
   if (w == 2) tmem_alloc<512>(&tmem_base);
   if (tid == 0) {
@@ -188,7 +192,7 @@ __global__ void __launch_bounds__(256, 1) k_tc_featmajor(const __grid_constant__
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < NB; ++i) {
-      mbar_init(&afull[i], 4);
+      mbar_init(&afull[i], GEN_WARPS);
       mbar_init(&aempty[i], 1);
     }
     mbar_init(fin, 1);
@@ -249,13 +253,16 @@ __global__ void __launch_bounds__(256, 1) k_tc_featmajor(const __grid_constant__
     }
   } else if (w >= 4) {
     // ---------------- A generation (phi'(X~)^T into TMEM) ----------------
-    const int q = w & 3;
-    int ra[4], rb[4];
+    const int q = w & 3, tp = (w - 4) >> 2;   // lane quadrant, tile pair
+    int ra[2], rb[2];
+    bool act[2];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int blk = (t < nt) ? (t0 + t) * 4 + q : 0;
-      ra[t] = 4 * c_blk.al[blk] + (l >> 3);
-      rb[t] = 8 * c_blk.be[blk] + (l & 7);
+    for (int u = 0; u < 2; ++u) {
+      const int t = tp * 2 + u;
+      act[u] = t < nt;
+      const int blk = act[u] ? (t0 + t) * 4 + q : 0;
+      ra[u] = 4 * c_blk.al[blk] + (l >> 3);
+      rb[u] = 8 * c_blk.be[blk] + (l & 7);
     }
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     for (int i = 0; i < nsub; ++i) {
@@ -263,19 +270,22 @@ __global__ void __launch_bounds__(256, 1) k_tc_featmajor(const __grid_constant__
       mbar_wait(&full[st], (j / ST) & 1);
       if (i >= NB) mbar_wait(&aempty[buf], ((i / NB) + 1) & 1);
       const uint8_t* xs = xt_s + st * XT_B;
+      uint32_t va[2][16], vb[2][16];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        if (t < nt) {
-          uint32_t va[16], vb[16], o[16];
+      for (int u = 0; u < 2; ++u)
 #pragma unroll
-          for (int c4 = 0; c4 < 4; ++c4) {
-            const int ch = h * 4 + c4;
-            *(uint4*)&va[c4 * 4] = *(const uint4*)(xs + sw128_off(ra[t], ch));
-            *(uint4*)&vb[c4 * 4] = *(const uint4*)(xs + sw128_off(rb[t], ch));
-          }
+        for (int c4 = 0; c4 < 4; ++c4) {
+          const int ch = h * 4 + c4;
+          *(uint4*)&va[u][c4 * 4] = *(const uint4*)(xs + sw128_off(ra[u], ch));
+          *(uint4*)&vb[u][c4 * 4] = *(const uint4*)(xs + sw128_off(rb[u], ch));
+        }
 #pragma unroll
-          for (int c = 0; c < 16; ++c) o[c] = hmul2_f16(va[c], vb[c]);
-          tmem_st16(tm + 320u + (uint32_t)((buf * 4 + t) * 16) + lane_off, o);
+      for (int u = 0; u < 2; ++u) {
+        if (act[u]) {
+          uint32_t o[16];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) o[c] = hmul2_f16(va[u][c], vb[u][c]);
+          tmem_st16(tm + 320u + (uint32_t)((buf * 4 + tp * 2 + u) * 16) + lane_off, o);
         }
       }
       tc_wait_st();
@@ -287,7 +297,10 @@ __global__ void __launch_bounds__(256, 1) k_tc_featmajor(const __grid_constant__
     mbar_wait(fin, 0);
     tc_fence_after();
     const int ncols = den ? UW : 64;
-    for (int t = 0; t < nt; ++t) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int t = tp * 2 + u;
+      if (!act[u]) continue;
       float* dst = out + (((size_t)(s * g.n + slot) * FH) + (size_t)(t0 + t) * 128 + q * 32 + l) * UW;
       for (int c0 = 0; c0 < ncols; c0 += 16) {
         uint32_t r[16];
@@ -436,13 +449,14 @@ __device__ __forceinline__ void load_scaled_row(const __nv_bfloat16* src, float 
   }
 }
 
+template <int kDen>
 __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUtensorMap tm_q,
                                                    const __grid_constant__ CUtensorMap tm_k,
                                                    const __grid_constant__ CUtensorMap tm_v, Geo g,
                                                    const __nv_bfloat16* __restrict__ qraw,
                                                    const float* __restrict__ ell,
                                                    const __half* __restrict__ st_main,
-                                                   const __half* __restrict__ st_den, int with_den,
+                                                   const __half* __restrict__ st_den,
                                                    __nv_bfloat16* y, float* rowsum, float* y32, int* zflag) {
   using namespace outk;
   extern __shared__ uint8_t smem_raw[];
@@ -475,7 +489,7 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
   const int I = blockIdx.x, k = blockIdx.y, s = blockIdx.z;
   const int bi = s / g.h, hi = s % g.h;
   const int c0 = k * g.c;
-  const bool den = with_den != 0;
+  constexpr bool den = kDen != 0;
   const bool has_state = k >= 1;
 
   if (w == 2) tmem_alloc<512>(&tmem_base);
@@ -900,14 +914,14 @@ __device__ __forceinline__ void dphi_tiles(const float (&x)[64], float (&dx)[64]
   if constexpr (NTI + 1 < dp::NT) dphi_tiles<NTI + 1>(x, dx, dbase, lane_off, d_full, d_empty, l);
 }
 
-template <bool kUpd>
+template <bool kUpd, int kDen>
 __global__ void __launch_bounds__(256, 1) k_tc_dphi(const __grid_constant__ CUtensorMap tm_a,
                                                     const __grid_constant__ CUtensorMap tm_a16, Geo g,
                                                     const __nv_bfloat16* __restrict__ xraw,
                                                     const float* __restrict__ ell,
                                                     const float* __restrict__ lamlog,
                                                     const __half* __restrict__ b_main,
-                                                    const __half* __restrict__ b_den, int with_den,
+                                                    const __half* __restrict__ b_den,
                                                     const float* __restrict__ dx32, const float* __restrict__ dv32,
                                                     float* dell, float* dellend, __nv_bfloat16* dxo,
                                                     __nv_bfloat16* dvo) {
@@ -933,7 +947,7 @@ __global__ void __launch_bounds__(256, 1) k_tc_dphi(const __grid_constant__ CUte
   const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
   const int I = blockIdx.x, k = blockIdx.y, s = blockIdx.z;
   const int tok0 = k * g.c + I * 128;
-  const bool den = with_den != 0;
+  constexpr bool den = kDen != 0;
   if (!kUpd && k == 0) {
     // chunk 0 has no state query: its dq is the intra-chunk part alone
     for (int i = tid; i < 128 * 16; i += 256) {
@@ -1581,9 +1595,9 @@ int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const 
   }
   {
     StageTimer tmr("fwd_update_state", st);
-    cudaFuncSetAttribute(k_tc_featmajor<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fm::SMEM);
-    k_tc_featmajor<false><<<dim3((NTH + 3) / 4, g.n, g.ns), 256, fm::SMEM, st>>>(m_kt, m_vr, m_wa, g, with_den,
-                                                                                 w.sp);
+    auto fn = with_den ? k_tc_featmajor<false, 1> : k_tc_featmajor<false, 0>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, fm::SMEM);
+    fn<<<dim3((NTH + 3) / 4, g.n, g.ns), fm::THREADS, fm::SMEM, st>>>(m_kt, m_vr, m_wa, g, w.sp);
   }
   {
     StageTimer tmr("fwd_discumsum", st);
@@ -1592,10 +1606,10 @@ int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const 
   }
   {
     StageTimer tmr("fwd_attn_query", st);
-    cudaFuncSetAttribute(k_tc_out, cudaFuncAttributeMaxDynamicSharedMemorySize, outk::SMEM);
-    k_tc_out<<<dim3(g.c / 128, g.n, g.ns), 256, outk::SMEM, st>>>(m_q, m_k, m_v, g, (const __nv_bfloat16*)q, w.ell,
-                                                                  w.stm, w.std_, with_den, (__nv_bfloat16*)y, rowsum,
-                                                                  w.y32, w.zflag);
+    auto fn = with_den ? k_tc_out<1> : k_tc_out<0>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, outk::SMEM);
+    fn<<<dim3(g.c / 128, g.n, g.ns), 256, outk::SMEM, st>>>(m_q, m_k, m_v, g, (const __nv_bfloat16*)q, w.ell, w.stm,
+                                                            w.std_, (__nv_bfloat16*)y, rowsum, w.y32, w.zflag);
   }
   count_launch(5);
   return cuda_check("tc forward");
@@ -1642,8 +1656,9 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
   }
   if (g.n > 1) {
     StageTimer tmr("bwd_query_state_dA", st);
-    cudaFuncSetAttribute(k_tc_featmajor<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fm::SMEM);
-    k_tc_featmajor<true><<<dim3((NTH + 3) / 4, g.n - 1, g.ns), 256, fm::SMEM, st>>>(m_qt, m_dn, m_dd, g, den, w.sp);
+    auto fn = den ? k_tc_featmajor<true, 1> : k_tc_featmajor<true, 0>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, fm::SMEM);
+    fn<<<dim3((NTH + 3) / 4, g.n - 1, g.ns), fm::THREADS, fm::SMEM, st>>>(m_qt, m_dn, m_dd, g, w.sp);
   }
   {
     StageTimer tmr("bwd_discumsum", st);
@@ -1668,16 +1683,18 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
   }
   {
     StageTimer tmr("bwd_query_state_dq", st);
-    cudaFuncSetAttribute(k_tc_dphi<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dp::SMEM);
-    k_tc_dphi<false><<<dim3(g.c / 128, g.n, g.ns), 256, dp::SMEM, st>>>(
-        m_dn16, m_dd128, g, (const __nv_bfloat16*)q, w.ell, w.lamlog, w.stm, w.std_, den, b.dq32, nullptr, b.dell,
+    auto fn = den ? k_tc_dphi<false, 1> : k_tc_dphi<false, 0>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dp::SMEM);
+    fn<<<dim3(g.c / 128, g.n, g.ns), 256, dp::SMEM, st>>>(
+        m_dn16, m_dd128, g, (const __nv_bfloat16*)q, w.ell, w.lamlog, w.stm, w.std_, b.dq32, nullptr, b.dell,
         nullptr, (__nv_bfloat16*)dq, nullptr);
   }
   {
     StageTimer tmr("bwd_update_state", st);
-    cudaFuncSetAttribute(k_tc_dphi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dp::SMEM);
-    k_tc_dphi<true><<<dim3(g.c / 128, g.n, g.ns), 256, dp::SMEM, st>>>(
-        m_v16, m_dummy, g, (const __nv_bfloat16*)k, w.ell, w.lamlog, b.dsm, b.dsd, den, b.dk32, b.dv32, b.dell,
+    auto fn = den ? k_tc_dphi<true, 1> : k_tc_dphi<true, 0>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dp::SMEM);
+    fn<<<dim3(g.c / 128, g.n, g.ns), 256, dp::SMEM, st>>>(
+        m_v16, m_dummy, g, (const __nv_bfloat16*)k, w.ell, w.lamlog, b.dsm, b.dsd, b.dk32, b.dv32, b.dell,
         b.cu, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv);
   }
   {

@@ -11,15 +11,16 @@
 
 using namespace pa::sm100;
 
-__global__ void __launch_bounds__(128, 1) rate(int ts, int bmn, int N, int R, unsigned long long* out) {
+__global__ void __launch_bounds__(128, 1) rate(int var, int ts, int bmn, int N, int R, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, bar2;
   __shared__ uint32_t tbase;
   const int tid = threadIdx.x;
   if (tid < 32) tmem_alloc<512>(&tbase);
   if (tid == 0) {
     mbar_init(&bar, 1);
+    mbar_init(&bar2, 1);
     fence_barrier_init();
   }
   for (int i = tid; i < 96 * 1024 / 4; i += 128) ((uint32_t*)smem)[i] = 0x3c003c00u;
@@ -28,7 +29,8 @@ __global__ void __launch_bounds__(128, 1) rate(int ts, int bmn, int N, int R, un
   __syncthreads();
   tc_fence_after();
   const uint32_t tm = tbase;
-  if (tid == 0) {
+  if (var == 0 && tid == 0) {
+    // one thread runs the loop (divergent branch)
     const uint32_t id = idesc_f16(128, N, false, bmn != 0);
     const uint32_t a = smem_u32(smem), b = smem_u32(smem + 32768);
     long long t0 = clock64();
@@ -44,10 +46,172 @@ __global__ void __launch_bounds__(128, 1) rate(int ts, int bmn, int N, int R, un
     mbar_wait(&bar, 0);
     long long t1 = clock64();
     out[blockIdx.x] = (unsigned long long)(t1 - t0);
+  } else if (var == 1 && tid < 32) {
+    // whole warp runs the loop (uniform datapath), one elected lane issues
+    const uint32_t id = idesc_f16(128, N, false, bmn != 0);
+    const uint32_t a = smem_u32(smem), b = smem_u32(smem + 32768);
+    long long t0 = clock64();
+    for (int i = 0; i < R; i += 4) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        uint64_t bd = bmn ? smem_desc(b + kk * 2048, 8192, 1024, 2) : smem_desc(b + kk * 32, 16, 1024, 2);
+        if (elect_one()) {
+          if (ts)
+            mma_ts(tm, tm + 256u + (uint32_t)(kk * 8), bd, id, 1u);
+          else
+            mma_ss(tm, smem_desc(a + kk * 32, 16, 1024, 2), bd, id, 1u);
+        }
+        __syncwarp();
+      }
+    }
+    if (elect_one()) tc_commit(&bar);
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    if (tid == 0) out[blockIdx.x] = (unsigned long long)(t1 - t0);
+  } else if (var == 2 && tid == 0) {
+    // one thread, descriptors precomputed, unrolled by 4
+    const uint32_t id = idesc_f16(128, N, false, bmn != 0);
+    const uint32_t a = smem_u32(smem), b = smem_u32(smem + 32768);
+    uint64_t bd[4], ad[4];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      bd[kk] = bmn ? smem_desc(b + kk * 2048, 8192, 1024, 2) : smem_desc(b + kk * 32, 16, 1024, 2);
+      ad[kk] = smem_desc(a + kk * 32, 16, 1024, 2);
+    }
+    long long t0 = clock64();
+    for (int i = 0; i < R; i += 4) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        if (ts)
+          mma_ts(tm, tm + 256u + (uint32_t)(kk * 8), bd[kk], id, 1u);
+        else
+          mma_ss(tm, ad[kk], bd[kk], id, 1u);
+      }
+    }
+    tc_commit(&bar);
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    out[blockIdx.x] = (unsigned long long)(t1 - t0);
+  }
+  else if (var >= 3 && tid == 0) {
+    // one thread, precomputed descriptors, rotating over nacc accumulators
+    const int nacc = var == 3 ? 2 : 4;
+    const uint32_t id = idesc_f16(128, N, false, bmn != 0);
+    const uint32_t a = smem_u32(smem), b = smem_u32(smem + 32768);
+    uint64_t bd[4], ad[4];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      bd[kk] = bmn ? smem_desc(b + kk * 2048, 8192, 1024, 2) : smem_desc(b + kk * 32, 16, 1024, 2);
+      ad[kk] = smem_desc(a + kk * 32, 16, 1024, 2);
+    }
+    long long t0 = clock64();
+    for (int i = 0; i < R; i += 4) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint32_t acc = tm + (uint32_t)((kk % nacc) * N);
+        if (ts)
+          mma_ts(acc, tm + 256u + (uint32_t)(kk * 8), bd[kk], id, 1u);
+        else
+          mma_ss(acc, ad[kk], bd[kk], id, 1u);
+      }
+    }
+    tc_commit(&bar);
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    out[blockIdx.x] = (unsigned long long)(t1 - t0);
+  }
+  else if (var == 5 && (tid == 0 || tid == 32)) {
+    // two issuing warps, separate accumulators
+    const uint32_t id = idesc_f16(128, N, false, bmn != 0);
+    const uint32_t b = smem_u32(smem + 32768);
+    uint64_t bd[4];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+      bd[kk] = bmn ? smem_desc(b + kk * 2048, 8192, 1024, 2) : smem_desc(b + kk * 32, 16, 1024, 2);
+    const uint32_t acc = tm + (tid ? 128u : 0u);
+    long long t0 = clock64();
+    for (int i = 0; i < R / 2; i += 4) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) mma_ts(acc, tm + 256u + (uint32_t)(kk * 8), bd[kk], id, 1u);
+    }
+    tc_commit(tid ? &bar2 : &bar);
+    mbar_wait(tid ? &bar2 : &bar, 0);
+    long long t1 = clock64();
+    if (tid == 0) out[blockIdx.x] = (unsigned long long)(t1 - t0);
+  }
+  else if (var >= 6 && tid == 0) {
+    // 6: accumulate = 0 ; 7: M = 64 ; 8: kind::f8f6f4 (e4m3, K = 32) ; 9: N=256 baseline
+    const int M = var == 7 ? 64 : 128;
+    uint32_t id = idesc_f16(M, N, false, bmn != 0);
+    if (var == 8) id = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);  // A,B e4m3 (0)
+    const uint32_t b = smem_u32(smem + 32768);
+    uint64_t bd[4];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+      bd[kk] = smem_desc(b + kk * 32, 16, 1024, 2);
+    const int acol = bmn;
+    const uint32_t accf = var == 6 ? 0u : 1u;
+    long long t0 = clock64();
+    for (int i = 0; i < R; i += 4) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        if (var == 8)
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tm),
+              "r"(tm + 256u + (uint32_t)(kk * 8)), "l"(bd[kk]), "r"(id), "r"(accf));
+        else
+          mma_ts(tm, tm + (uint32_t)acol + (uint32_t)(kk * 8), bd[kk], id, accf);
+      }
+    }
+    tc_commit(&bar);
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    out[blockIdx.x] = (unsigned long long)(t1 - t0);
   }
   tc_fence_before();
   __syncthreads();
   if (tid < 32) tmem_dealloc<512>(tm);
+}
+
+template <int COLS>
+__global__ void __launch_bounds__(128, 1) rate2(int N, int R, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x;
+  if (tid < 32) tmem_alloc<COLS>(&tbase);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  for (int i = tid; i < 40 * 1024 / 4; i += 128) ((uint32_t*)smem)[i] = 0x3c003c00u;
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tbase;
+  if (tid == 0) {
+    const uint32_t id = idesc_f16(128, N, false, false);
+    const uint32_t b = smem_u32(smem + 16384);
+    uint64_t bd[4];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) bd[kk] = smem_desc(b + kk * 32, 16, 1024, 2);
+    long long t0 = clock64();
+    for (int i = 0; i < R; i += 4) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) mma_ts(tm, tm + 192u + (uint32_t)(kk * 8), bd[kk], id, 1u);
+    }
+    tc_commit(&bar);
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    out[blockIdx.x] = (unsigned long long)(t1 - t0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (tid < 32) tmem_dealloc<COLS>(tm);
 }
 
 int main() {
@@ -55,11 +219,34 @@ int main() {
   cudaMalloc(&d, 148 * 8);
   cudaFuncSetAttribute(rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   const int R = 8192;
-  for (int ts = 0; ts < 2; ++ts)
-    for (int bmn = 0; bmn < 2; ++bmn)
-      for (int N : {16, 64, 128, 256}) {
-        rate<<<148, 128, 100 * 1024>>>(ts, bmn, N, R, d);
-        rate<<<148, 128, 100 * 1024>>>(ts, bmn, N, R, d);
+  {
+    unsigned long long* d2;
+    cudaMalloc(&d2, 296 * 8);
+    cudaFuncSetAttribute(rate2<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
+    cudaFuncSetAttribute(rate2<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
+    for (int cols : {256, 512})
+      for (int sm : {48, 100})
+        for (int N : {64, 128}) {
+          auto fn = cols == 256 ? rate2<256> : rate2<512>;
+          fn<<<148, 128, sm * 1024>>>(N, 8192, d2);
+          fn<<<148, 128, sm * 1024>>>(N, 8192, d2);
+          cudaError_t e = cudaDeviceSynchronize();
+          unsigned long long h[296];
+          cudaMemcpy(h, d2, sizeof h, cudaMemcpyDeviceToHost);
+          double avg = 0;
+          for (int i = 0; i < 148; ++i) avg += h[i];
+          avg /= 148;
+          printf("rate2 cols %d smem %dKB N=%d: %.2f cyc per MMA (%s)\n", cols, sm, N, avg / 8192,
+                 e ? cudaGetErrorString(e) : "ok");
+        }
+  }
+  for (int var = 6; var < 6; ++var)
+  for (int ts = 1; ts < 2; ++ts)
+    for (int bmn : {128, 192, 256, 320, 384, 448})
+      for (int N : {32, 64, 128}) {
+        
+        rate<<<148, 128, 100 * 1024>>>(var, ts, bmn, N, R, d);
+        rate<<<148, 128, 100 * 1024>>>(var, ts, bmn, N, R, d);
         cudaError_t e = cudaDeviceSynchronize();
         unsigned long long h[148];
         cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
@@ -67,8 +254,8 @@ int main() {
         for (int i = 0; i < 148; ++i) avg += h[i];
         avg /= 148;
         const double cyc = avg / R;
-        printf("%s B %s N=%3d : %6.2f cyc/MMA  ideal %5.1f  -> %5.1f%% of 8192 FLOP/clk  %s\n", ts ? "TS" : "SS",
-               bmn ? "MN" : "K ", N, cyc, N / 2.0, 100.0 * (N / 2.0) / cyc, e ? cudaGetErrorString(e) : "");
+        printf("var%d %s Acol %d N=%3d : %6.2f cyc/MMA  ideal %5.1f  -> %5.1f%% of 8192 FLOP/clk  %s\n", var, ts ? "TS" : "SS",
+               bmn, N, cyc, N / 2.0, 100.0 * (N / 2.0) / cyc, e ? cudaGetErrorString(e) : "");
       }
   return 0;
 }
