@@ -1674,12 +1674,7 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
     if (!map_bth(&m_q128, q, g, 128) || !map_bth(&m_k128, k, g, 128)) {
       return 3;
     }
-    cudaFuncSetAttribute(k_tc_intra_bwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ib::SMEM);
-    cudaFuncSetAttribute(k_tc_intra_bwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ib::SMEM);
-    k_tc_intra_bwd<true><<<dim3(g.c / 128, g.n, g.ns), 256, ib::SMEM, st>>>(m_q128, m_k128, m_v128, m_dn128, g,
-                                                                            w.ell, b.dden, b.dk32, b.dv32, b.dell);
-    k_tc_intra_bwd<false><<<dim3(g.c / 128, g.n, g.ns), 256, ib::SMEM, st>>>(m_q128, m_k128, m_v128, m_dn128, g,
-                                                                             w.ell, b.dden, b.dq32, nullptr, b.dell);
+    tc_intra_bwd(g, m_q128, m_k128, m_v128, m_dn128, w.ell, b.dden, b.dk32, b.dv32, b.dq32, b.dell, st);
   }
   {
     StageTimer tmr("bwd_query_state_dq", st);

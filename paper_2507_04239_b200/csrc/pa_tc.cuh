@@ -1,5 +1,7 @@
 // Host-side interface of the bf16 tcgen05 (sm_100a tensor-core) pipeline.
 #pragma once
+#include <cuda.h>
+
 #include "pa_common.cuh"
 
 namespace pa {
@@ -12,5 +14,10 @@ int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const 
 int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const float* log_g,
                 const void* y, const float* rowsum, const void* dy, void* dq, void* dk, void* dv,
                 float* dlog_g, const void* fwd_ws, void* bwd_ws, cudaStream_t st);
+
+// intra-chunk backward (pa_tc_ib.cu): dK, dV (fp32, =), dQ (fp32, =), dell (+=)
+int tc_intra_bwd(const Geo& g, const CUtensorMap& m_q, const CUtensorMap& m_k, const CUtensorMap& m_v,
+                 const CUtensorMap& m_dn, const float* ell, const float* dden, float* dk32, float* dv32,
+                 float* dq32, float* dell, cudaStream_t st);
 
 }  // namespace pa

@@ -1,0 +1,321 @@
+// Intra-chunk backward on tcgen05 (reference gradients.py:98-176, power branch,
+// with the pairwise-decay chain rule 79-95 taken in log space).
+//
+// Per chunk, with s = q.k (raw), E_ij = exp(ell_i - ell_j) for j <= i:
+//   P = sigma^2 E s^2,   dP' = dnum.v + dden,   dS = 2 sigma^2 E dP' s
+//   key side  (kKV):  dV_J = sum_I P^T dnum_I,  dK_J = sum_I dS^T Q_I,  dell_j -= sum_i dP' P
+//   query side:       dQ_I = sum_J dS K_J,                            dell_i += sum_j dP' P
+//
+// Design (B200): two CTAs per SM (256 TMEM columns, ~110 KB shared memory
+// each) so one CTA's elementwise phase overlaps the other's MMAs and the two
+// CTAs' tcgen05 issue streams interleave (one CTA alone is capped at ~72% of
+// the tensor peak by the per-CTA MMA issue interval at N = 64, see
+// profiles/r01_mma_rate_probe.txt).  The streamed 128-token block is
+// processed as two 64-token sub-blocks: S/dP for a sub-block use 128 TMEM
+// columns, P and dS are written back in place as bf16 (the gradient MMAs read
+// them as the TMEM A operand), and the two 64-column gradient accumulators
+// take the other 128 columns.
+// Off-diagonal blocks use the factorisation E_ij = r_i c_j with both factors
+// <= 1 (referenced to the end of the key block); the diagonal block evaluates
+// exp(ell_i - ell_j) per element under the causal mask.
+#include <cuda.h>
+
+#include "pa_common.cuh"
+#include "pa_sm100.cuh"
+#include "pa_tc.cuh"
+#include "pa_tc_common.cuh"
+
+namespace pa {
+using namespace sm100;
+using namespace tc;
+
+namespace ib2 {
+constexpr int T128 = 128 * 128;   // one 128-token x 64 bf16 tile
+constexpr int NST = 2;            // streamed-tile stages
+constexpr int SMEM = 1024 + 2 * T128 + NST * 2 * T128 + 3 * 4096 + 256;
+}  // namespace ib2
+
+struct f2 {
+  float x, y;
+};
+__device__ __forceinline__ uint64_t u64(f2 a) { return *(uint64_t*)&a; }
+__device__ __forceinline__ f2 mk(uint64_t r) { return *(f2*)&r; }
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(u64(a)), "l"(u64(b)));
+  return mk(r);
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(u64(a)), "l"(u64(b)));
+  return mk(r);
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(u64(a)), "l"(u64(b)), "l"(u64(c)));
+  return mk(r);
+}
+
+// kKV = true: one CTA per key block J, loops query blocks I = J..nq-1.
+// kKV = false: one CTA per query block I (heaviest first), loops key blocks J = 0..I.
+template <bool kKV, bool kNorm>
+__global__ void __launch_bounds__(256, 2) k_tc_ib(const __grid_constant__ CUtensorMap tm_q,
+                                                  const __grid_constant__ CUtensorMap tm_k,
+                                                  const __grid_constant__ CUtensorMap tm_v,
+                                                  const __grid_constant__ CUtensorMap tm_dn, Geo g,
+                                                  const float* __restrict__ ell, const float* __restrict__ dden,
+                                                  float* out_a, float* out_b, float* dell) {
+  using namespace ib2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* f0 = smem;                      // kKV: K_J   | q-side: Q_I
+  uint8_t* f1 = f0 + T128;                 // kKV: V_J   | q-side: dN_I
+  uint8_t* s0 = f1 + T128;                 // stages: kKV: (Q_X, dN_X) | q-side: (K_X, V_X)
+  float* ell_s = (float*)(s0 + NST * 2 * T128);   // [1024] in-chunk log prefix
+  float* colf = ell_s + 1024;                       // [1024] off-diagonal column factor
+  float* cold = colf + 1024;                        // [1024] dden per query column (kKV, normalize)
+  uint64_t* bars = (uint64_t*)(cold + 1024);
+  uint64_t* f_full = bars;
+  uint64_t* t_full = f_full + 1;         // NST
+  uint64_t* t_empty = t_full + NST;      // NST
+  uint64_t* s_full = t_empty + NST;      // S / dP of the current sub-block in TMEM
+  uint64_t* p_full = s_full + 1;         // P / dS written back (4 compute warps)
+  uint64_t* fin = p_full + 1;
+  __shared__ uint32_t tmem_base;
+
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  const int nq = g.c / 128;
+  const int B0 = kKV ? (int)blockIdx.x : nq - 1 - (int)blockIdx.x;
+  const int k = blockIdx.y, s = blockIdx.z;
+  const int bi = s / g.h, hi = s % g.h;
+  const int c0 = k * g.c;
+  const int nblk = kKV ? nq - B0 : B0 + 1;
+  const float sig2 = g.scale * g.scale;
+
+  if (w == 2) tmem_alloc<256>(&tmem_base);
+  if (tid == 0) {
+    mbar_init(f_full, 1);
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&t_full[i], 1);
+      mbar_init(&t_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 4);
+    mbar_init(fin, 1);
+    fence_barrier_init();
+  }
+  for (int i = tid; i < g.c; i += 256) ell_s[i] = ell[(size_t)s * g.t + c0 + i];
+  __syncthreads();
+  // column factors (both <= 1): kKV  r_i = sigma^2 exp(ell_i - ell_endJ)   (queries after block J)
+  //                             q-side c_j = exp(ell_end(J(j)) - ell_j)    (keys, own block end)
+  {
+    const float lrefJ = ell_s[B0 * 128 + 127];
+    const int lim = kKV ? g.c : (B0 + 1) * 128;
+    for (int i = tid; i < lim; i += 256) {
+      if (kKV)
+        colf[i] = sig2 * __expf(fminf(ell_s[i] - lrefJ, 0.f));
+      else
+        colf[i] = __expf(fminf(ell_s[(i | 127)] - ell_s[i], 0.f));
+      if (kKV && kNorm) cold[i] = dden[(size_t)s * g.t + c0 + i];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tmem_base;
+  const uint32_t tS = tm, tDP = tm + 64, tA = tm + 128, tB = tm + 192;
+
+  if (w == 0) {
+    if (l == 0) {
+      tma_prefetch(&tm_q);
+      tma_prefetch(&tm_k);
+      tma_prefetch(&tm_v);
+      tma_prefetch(&tm_dn);
+      mbar_expect_tx(f_full, 2 * T128);
+      if (kKV) {
+        tma_load_4d(f0, &tm_k, f_full, 0, hi, c0 + B0 * 128, bi);
+        tma_load_4d(f1, &tm_v, f_full, 0, hi, c0 + B0 * 128, bi);
+      } else {
+        tma_load_4d(f0, &tm_q, f_full, 0, hi, c0 + B0 * 128, bi);
+        tma_load_2d(f1, &tm_dn, f_full, 0, s * g.t + c0 + B0 * 128);
+      }
+      for (int it = 0; it < nblk; ++it) {
+        const int X = kKV ? B0 + it : it, st = it % NST;
+        if (it >= NST) mbar_wait(&t_empty[st], ((it / NST) + 1) & 1);
+        mbar_expect_tx(&t_full[st], 2 * T128);
+        uint8_t* d0 = s0 + st * 2 * T128;
+        if (kKV) {
+          tma_load_4d(d0, &tm_q, &t_full[st], 0, hi, c0 + X * 128, bi);
+          tma_load_2d(d0 + T128, &tm_dn, &t_full[st], 0, s * g.t + c0 + X * 128);
+        } else {
+          tma_load_4d(d0, &tm_k, &t_full[st], 0, hi, c0 + X * 128, bi);
+          tma_load_4d(d0 + T128, &tm_v, &t_full[st], 0, hi, c0 + X * 128, bi);
+        }
+      }
+    }
+  } else if (w == 1) {
+    if (l == 0) {
+      constexpr uint32_t idS = idesc_bf16(128, 64, false, false);   // S / dP: both K-major
+      constexpr uint32_t idG = idesc_bf16(128, 64, false, true);    // gradients: B MN-major
+      mbar_wait(f_full, 0);
+      const uint32_t F0 = smem_u32(f0), F1 = smem_u32(f1);
+      for (int it = 0; it < nblk; ++it) {
+        const int st = it % NST;
+        mbar_wait(&t_full[st], (it / NST) & 1);
+        tc_fence_after();
+        const uint32_t T0 = smem_u32(s0 + st * 2 * T128), T1 = T0 + T128;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int n = it * 2 + h;
+          const uint32_t hb = (uint32_t)h * 8192u;   // 64 rows x 128 B
+          // kKV: S^T = K_J Q_h^T, dP^T = V_J dN_h^T   | q-side: S = Q_I K_h^T, dP = dN_I V_h^T
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            mma_ss(tS, smem_desc(F0 + kk * 32, 16, 1024, 2), smem_desc(T0 + hb + kk * 32, 16, 1024, 2), idS,
+                   kk > 0 ? 1u : 0u);
+            mma_ss(tDP, smem_desc(F1 + kk * 32, 16, 1024, 2), smem_desc(T1 + hb + kk * 32, 16, 1024, 2), idS,
+                   kk > 0 ? 1u : 0u);
+          }
+          tc_commit(s_full);
+          mbar_wait(p_full, n & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint32_t acc = (n > 0 || kk > 0) ? 1u : 0u;
+            if (kKV) {
+              mma_ts(tA, tS + kk * 8, smem_desc(T1 + hb + kk * 2048, 8192, 1024, 2), idG, acc);   // dV += P^T dN
+              mma_ts(tB, tDP + kk * 8, smem_desc(T0 + hb + kk * 2048, 8192, 1024, 2), idG, acc);  // dK += dS^T Q
+            } else {
+              mma_ts(tA, tDP + kk * 8, smem_desc(T0 + hb + kk * 2048, 8192, 1024, 2), idG, acc);  // dQ += dS K
+            }
+          }
+        }
+        tc_commit(&t_empty[st]);
+      }
+      tc_commit(fin);
+    }
+  } else if (w >= 4) {
+    const int q = w & 3, row = q * 32 + l;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const int own = B0 * 128 + row;            // chunk-relative token of this TMEM lane
+    const float l_own = ell_s[own];
+    const float dden_own = (!kKV && kNorm) ? dden[(size_t)s * g.t + c0 + own] : 0.f;
+    // kKV: c_own = exp(ell_endJ - ell_own) (<= 1); q-side: r_own = sigma^2 exp(ell_own - ell_endJ) per J
+    const float c_own = kKV ? __expf(fminf(ell_s[B0 * 128 + 127] - l_own, 0.f)) : 0.f;
+    f2 red = {0.f, 0.f};
+    for (int n = 0; n < 2 * nblk; ++n) {
+      const int it = n >> 1, h = n & 1;
+      const int X = kKV ? B0 + it : it;
+      const bool diag = (X == B0);
+      const float rowf = kKV ? c_own : sig2 * __expf(fminf(l_own - ell_s[X * 128 + 127], 0.f));
+      const f2 rowf2 = {rowf, rowf};
+      mbar_wait(s_full, n & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int ch = 0; ch < 2; ++ch) {
+        const int colbase = X * 128 + h * 64 + ch * 32;   // chunk-relative token of column 0
+        uint32_t rs[32], rd[32], pp[16], pd[16];
+        tmem_ld32(tS + lane_off + ch * 32, rs);
+        tmem_ld32(tDP + lane_off + ch * 32, rd);
+        tc_wait_ld();
+        if (!diag) {
+#pragma unroll
+          for (int e4 = 0; e4 < 8; ++e4) {
+            const float4 cf = *(const float4*)(colf + colbase + e4 * 4);
+            float4 cd = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (kKV && kNorm) cd = *(const float4*)(cold + colbase + e4 * 4);
+#pragma unroll
+            for (int z = 0; z < 2; ++z) {
+              const int e = e4 * 4 + z * 2;
+              const f2 sv = {__uint_as_float(rs[e]), __uint_as_float(rs[e + 1])};
+              f2 dp = {__uint_as_float(rd[e]), __uint_as_float(rd[e + 1])};
+              const f2 cc = z ? f2{cf.z, cf.w} : f2{cf.x, cf.y};
+              if (kNorm) dp = add2(dp, kKV ? (z ? f2{cd.z, cd.w} : f2{cd.x, cd.y}) : f2{dden_own, dden_own});
+              const f2 E = mul2(cc, rowf2);
+              const f2 T = mul2(E, sv);
+              const f2 P = mul2(T, sv);
+              const f2 dS = mul2(dp, T);
+              red = fma2(dp, P, red);
+              pp[e >> 1] = pack_bf16(P.x, P.y);
+              pd[e >> 1] = pack_bf16(dS.x, dS.y);
+            }
+          }
+        } else {
+          // diagonal block: exact exp(ell_i - ell_j) under the causal mask
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            float Pv[2], dSv[2];
+#pragma unroll
+            for (int z = 0; z < 2; ++z) {
+              const int col = colbase + e + z;
+              const float sv = __uint_as_float(rs[e + z]);
+              float dp = __uint_as_float(rd[e + z]);
+              if (kNorm) dp += kKV ? cold[col] : dden_own;
+              const bool valid = kKV ? (col >= own) : (col <= own);
+              const float li = kKV ? ell_s[col] : l_own, lj = kKV ? l_own : ell_s[col];
+              const float E = valid ? sig2 * __expf(fminf(li - lj, 0.f)) : 0.f;
+              const float T = E * sv;
+              Pv[z] = T * sv;
+              dSv[z] = dp * T;
+              red.x = fmaf(dp, Pv[z], red.x);
+            }
+            pp[e >> 1] = pack_bf16(Pv[0], Pv[1]);
+            pd[e >> 1] = pack_bf16(dSv[0], dSv[1]);
+          }
+        }
+        // in place: bf16 pairs of columns [32ch, 32ch+32) land in columns [16ch, 16ch+16)
+        if (kKV) tmem_st16(tS + lane_off + ch * 16, pp);
+        tmem_st16(tDP + lane_off + ch * 16, pd);
+      }
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (l == 0) mbar_arrive(p_full);
+    }
+    // epilogue: gradients in fp32 stream-major rows (dS carries a factor 1/2)
+    mbar_wait(fin, 0);
+    tc_fence_after();
+    const size_t tokr = (size_t)s * g.t + c0 + own;
+    uint32_t r[64];
+    tmem_ld32(tA + lane_off, r);
+    tmem_ld32(tA + lane_off + 32, r + 32);
+    tc_wait_ld();
+    const float fa = kKV ? 1.f : 2.f;
+    float* oa = (kKV ? out_b : out_a) + tokr * HD;   // kKV: dV; q-side: dQ
+#pragma unroll
+    for (int a = 0; a < 64; a += 4)
+      *(float4*)(oa + a) = make_float4(fa * __uint_as_float(r[a]), fa * __uint_as_float(r[a + 1]),
+                                       fa * __uint_as_float(r[a + 2]), fa * __uint_as_float(r[a + 3]));
+    if (kKV) {
+      tmem_ld32(tB + lane_off, r);
+      tmem_ld32(tB + lane_off + 32, r + 32);
+      tc_wait_ld();
+      float* ob = out_a + tokr * HD;   // dK
+#pragma unroll
+      for (int a = 0; a < 64; a += 4)
+        *(float4*)(ob + a) = make_float4(2.f * __uint_as_float(r[a]), 2.f * __uint_as_float(r[a + 1]),
+                                         2.f * __uint_as_float(r[a + 2]), 2.f * __uint_as_float(r[a + 3]));
+    }
+    const float rr = red.x + red.y;
+    if (g.gated) dell[tokr] += kKV ? -rr : rr;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (w == 2) tmem_dealloc<256>(tm);
+}
+
+int tc_intra_bwd(const Geo& g, const CUtensorMap& m_q, const CUtensorMap& m_k, const CUtensorMap& m_v,
+                 const CUtensorMap& m_dn, const float* ell, const float* dden, float* dk32, float* dv32,
+                 float* dq32, float* dell, cudaStream_t st) {
+  using namespace ib2;
+  const dim3 grid(g.c / 128, g.n, g.ns);
+  auto kv = g.normalize ? k_tc_ib<true, true> : k_tc_ib<true, false>;
+  auto qs = g.normalize ? k_tc_ib<false, true> : k_tc_ib<false, false>;
+  cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  cudaFuncSetAttribute(qs, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  kv<<<grid, 256, SMEM, st>>>(m_q, m_k, m_v, m_dn, g, ell, dden, dk32, dv32, dell);
+  qs<<<grid, 256, SMEM, st>>>(m_q, m_k, m_v, m_dn, g, ell, dden, dq32, nullptr, dell);
+  return 0;
+}
+
+}  // namespace pa
