@@ -14,7 +14,7 @@ import threading
 from .errors import InvalidSpec, KernelError, OddPowerWithNormalize, ShapeMismatch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpa_b200.so")
+LIB_PATH = os.environ.get("PA_B200_LIB") or os.path.join(HERE, "libpa_b200.so")
 
 PA_F32, PA_BF16, PA_F16, PA_F64 = 0, 1, 2, 3
 

@@ -6,8 +6,8 @@
 //   key side  (kKV):  dV_J = sum_I P^T dnum_I,  dK_J = sum_I dS^T Q_I,  dell_j -= sum_i dP' P
 //   query side:       dQ_I = sum_J dS K_J,                            dell_i += sum_j dP' P
 //
-// Design (B200): two CTAs per SM (256 TMEM columns, ~110 KB shared memory
-// each) so one CTA's elementwise phase overlaps the other's MMAs and the two
+// Design (B200): two CTAs per SM (256 TMEM columns, ~110 KB shared memory,
+// 384 threads each) so one CTA's elementwise phase overlaps the other's MMAs and the two
 // CTAs' tcgen05 issue streams interleave (one CTA alone is capped at ~72% of
 // the tensor peak by the per-CTA MMA issue interval at N = 64, see
 // profiles/r01_mma_rate_probe.txt).  The streamed 128-token block is
@@ -29,9 +29,26 @@ namespace pa {
 using namespace sm100;
 using namespace tc;
 
+#ifdef PA_TRACE
+// debug build only (tools/trace_ib.py): clock64 stamps of one CTA's pipeline
+__device__ long long g_trace[1024];
+extern "C" int pa_debug_trace(long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(long long) * n);
+}
+#define PA_TR(i) \
+  if (tr) g_trace[(i)] = clock64()
+#else
+#define PA_TR(i)
+#endif
+
 namespace ib2 {
 constexpr int T128 = 128 * 128;   // one 128-token x 64 bf16 tile
 constexpr int NST = 2;            // streamed-tile stages
+// Warp roles: w0..w7 compute, w8 TMEM owner, w9 TMA, w10 MMA.  The issuing
+// warps get the highest warp ids: the scheduler prefers high ids, so spinning
+// compute warps cannot starve the MMA / TMA issue.
+constexpr int THREADS = 352;
+constexpr int W_TMEM = 8, W_TMA = 9, W_MMA = 10;
 constexpr int SMEM = 1024 + 2 * T128 + NST * 2 * T128 + 3 * 4096 + 256;
 }  // namespace ib2
 
@@ -56,10 +73,19 @@ __device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
   return mk(r);
 }
 
+__device__ __forceinline__ float exp2_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+// TMEM column of the bf16 P / dS K-chunk kk (16 tokens): compute-warp group kk/2,
+// piece kk%2 (see the in-place write in the compute warps)
+__device__ __forceinline__ uint32_t pcol(int kk) { return (uint32_t)((kk >> 1) * 32 + (kk & 1) * 8); }
+
 // kKV = true: one CTA per key block J, loops query blocks I = J..nq-1.
 // kKV = false: one CTA per query block I (heaviest first), loops key blocks J = 0..I.
 template <bool kKV, bool kNorm>
-__global__ void __launch_bounds__(256, 2) k_tc_ib(const __grid_constant__ CUtensorMap tm_q,
+__global__ void __launch_bounds__(ib2::THREADS, 2) k_tc_ib(const __grid_constant__ CUtensorMap tm_q,
                                                   const __grid_constant__ CUtensorMap tm_k,
                                                   const __grid_constant__ CUtensorMap tm_v,
                                                   const __grid_constant__ CUtensorMap tm_dn, Geo g,
@@ -91,8 +117,11 @@ __global__ void __launch_bounds__(256, 2) k_tc_ib(const __grid_constant__ CUtens
   const int c0 = k * g.c;
   const int nblk = kKV ? nq - B0 : B0 + 1;
   const float sig2 = g.scale * g.scale;
+#ifdef PA_TRACE
+  const bool tr0 = kKV && blockIdx.x == 0 && blockIdx.y == 5 && blockIdx.z == 3;
+#endif
 
-  if (w == 2) tmem_alloc<256>(&tmem_base);
+  if (w == W_TMEM) tmem_alloc<256>(&tmem_base);
   if (tid == 0) {
     mbar_init(f_full, 1);
     for (int i = 0; i < NST; ++i) {
@@ -100,22 +129,23 @@ __global__ void __launch_bounds__(256, 2) k_tc_ib(const __grid_constant__ CUtens
       mbar_init(&t_empty[i], 1);
     }
     mbar_init(s_full, 1);
-    mbar_init(p_full, 4);
+    mbar_init(p_full, 8);
     mbar_init(fin, 1);
     fence_barrier_init();
   }
-  for (int i = tid; i < g.c; i += 256) ell_s[i] = ell[(size_t)s * g.t + c0 + i];
+  constexpr float LOG2E = 1.4426950408889634f;
+  for (int i = tid; i < g.c; i += THREADS) ell_s[i] = LOG2E * ell[(size_t)s * g.t + c0 + i];
   __syncthreads();
   // column factors (both <= 1): kKV  r_i = sigma^2 exp(ell_i - ell_endJ)   (queries after block J)
   //                             q-side c_j = exp(ell_end(J(j)) - ell_j)    (keys, own block end)
   {
     const float lrefJ = ell_s[B0 * 128 + 127];
     const int lim = kKV ? g.c : (B0 + 1) * 128;
-    for (int i = tid; i < lim; i += 256) {
+    for (int i = tid; i < lim; i += THREADS) {
       if (kKV)
-        colf[i] = sig2 * __expf(fminf(ell_s[i] - lrefJ, 0.f));
+        colf[i] = sig2 * exp2_approx(fminf(ell_s[i] - lrefJ, 0.f));
       else
-        colf[i] = __expf(fminf(ell_s[(i | 127)] - ell_s[i], 0.f));
+        colf[i] = exp2_approx(fminf(ell_s[(i | 127)] - ell_s[i], 0.f));
       if (kKV && kNorm) cold[i] = dden[(size_t)s * g.t + c0 + i];
     }
   }
@@ -125,7 +155,7 @@ __global__ void __launch_bounds__(256, 2) k_tc_ib(const __grid_constant__ CUtens
   const uint32_t tm = tmem_base;
   const uint32_t tS = tm, tDP = tm + 64, tA = tm + 128, tB = tm + 192;
 
-  if (w == 0) {
+  if (w == W_TMA) {
     if (l == 0) {
       tma_prefetch(&tm_q);
       tma_prefetch(&tm_k);
@@ -153,7 +183,7 @@ __global__ void __launch_bounds__(256, 2) k_tc_ib(const __grid_constant__ CUtens
         }
       }
     }
-  } else if (w == 1) {
+  } else if (w == W_MMA) {
     if (l == 0) {
       constexpr uint32_t idS = idesc_bf16(128, 64, false, false);   // S / dP: both K-major
       constexpr uint32_t idG = idesc_bf16(128, 64, false, true);    // gradients: B MN-major
@@ -167,6 +197,10 @@ __global__ void __launch_bounds__(256, 2) k_tc_ib(const __grid_constant__ CUtens
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int n = it * 2 + h;
+#ifdef PA_TRACE
+          const bool tr = tr0 && n < 64;
+#endif
+          PA_TR(n * 8 + 0);
           const uint32_t hb = (uint32_t)h * 8192u;   // 64 rows x 128 B
           // kKV: S^T = K_J Q_h^T, dP^T = V_J dN_h^T   | q-side: S = Q_I K_h^T, dP = dN_I V_h^T
 #pragma unroll
@@ -177,50 +211,63 @@ __global__ void __launch_bounds__(256, 2) k_tc_ib(const __grid_constant__ CUtens
                    kk > 0 ? 1u : 0u);
           }
           tc_commit(s_full);
+          PA_TR(n * 8 + 1);
           mbar_wait(p_full, n & 1);
+          PA_TR(n * 8 + 2);
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             const uint32_t acc = (n > 0 || kk > 0) ? 1u : 0u;
             if (kKV) {
-              mma_ts(tA, tS + kk * 8, smem_desc(T1 + hb + kk * 2048, 8192, 1024, 2), idG, acc);   // dV += P^T dN
-              mma_ts(tB, tDP + kk * 8, smem_desc(T0 + hb + kk * 2048, 8192, 1024, 2), idG, acc);  // dK += dS^T Q
+              mma_ts(tA, tS + pcol(kk), smem_desc(T1 + hb + kk * 2048, 8192, 1024, 2), idG, acc);   // dV += P^T dN
+              mma_ts(tB, tDP + pcol(kk), smem_desc(T0 + hb + kk * 2048, 8192, 1024, 2), idG, acc);  // dK += dS^T Q
             } else {
-              mma_ts(tA, tDP + kk * 8, smem_desc(T0 + hb + kk * 2048, 8192, 1024, 2), idG, acc);  // dQ += dS K
+              mma_ts(tA, tDP + pcol(kk), smem_desc(T0 + hb + kk * 2048, 8192, 1024, 2), idG, acc);  // dQ += dS K
             }
           }
+          PA_TR(n * 8 + 3);
         }
         tc_commit(&t_empty[st]);
       }
       tc_commit(fin);
     }
-  } else if (w >= 4) {
-    const int q = w & 3, row = q * 32 + l;
+  } else if (w < 8) {
+    // 8 compute warps: lane quadrant q = w % 4, column half grp = w / 4 of
+    // each 64-column sub-block, processed as two 16-column pieces.
+    const int q = w & 3, grp = w >> 2, row = q * 32 + l;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const int own = B0 * 128 + row;            // chunk-relative token of this TMEM lane
-    const float l_own = ell_s[own];
+    const float l_own = ell_s[own];            // log2 units
     const float dden_own = (!kKV && kNorm) ? dden[(size_t)s * g.t + c0 + own] : 0.f;
-    // kKV: c_own = exp(ell_endJ - ell_own) (<= 1); q-side: r_own = sigma^2 exp(ell_own - ell_endJ) per J
-    const float c_own = kKV ? __expf(fminf(ell_s[B0 * 128 + 127] - l_own, 0.f)) : 0.f;
+    // kKV: c_own = 2^(ell_endJ - ell_own) (<= 1); q-side: r_own = sigma^2 2^(ell_own - ell_endJ) per J
+    const float c_own = kKV ? exp2_approx(fminf(ell_s[B0 * 128 + 127] - l_own, 0.f)) : 0.f;
     f2 red = {0.f, 0.f};
     for (int n = 0; n < 2 * nblk; ++n) {
       const int it = n >> 1, h = n & 1;
       const int X = kKV ? B0 + it : it;
       const bool diag = (X == B0);
-      const float rowf = kKV ? c_own : sig2 * __expf(fminf(l_own - ell_s[X * 128 + 127], 0.f));
+      const float rowf = kKV ? c_own : sig2 * exp2_approx(fminf(l_own - ell_s[X * 128 + 127], 0.f));
       const f2 rowf2 = {rowf, rowf};
+#ifdef PA_TRACE
+      const bool tr = tr0 && n < 64 && w == 0 && l == 0;
+#endif
+      PA_TR(n * 8 + 4);
       mbar_wait(s_full, n & 1);
+      PA_TR(n * 8 + 5);
       tc_fence_after();
 #pragma unroll
-      for (int ch = 0; ch < 2; ++ch) {
-        const int colbase = X * 128 + h * 64 + ch * 32;   // chunk-relative token of column 0
-        uint32_t rs[32], rd[32], pp[16], pd[16];
-        tmem_ld32(tS + lane_off + ch * 32, rs);
-        tmem_ld32(tDP + lane_off + ch * 32, rd);
+      for (int hh = 0; hh < 2; ++hh) {
+        const int cofs = grp * 32 + hh * 16;              // column offset inside the sub-block
+        const int colbase = X * 128 + h * 64 + cofs;      // chunk-relative token of the first column
+        uint32_t rs[16], rd[16], pp[8], pd[8];
+        tmem_ld16(tS + lane_off + cofs, rs);
+        tmem_ld16(tDP + lane_off + cofs, rd);
         tc_wait_ld();
+        // the causal mask of the diagonal block: kKV needs col >= own, q-side col <= own
+        const bool all_masked = diag && (kKV ? (colbase + 15 < own) : (colbase > own));
         if (!diag) {
 #pragma unroll
-          for (int e4 = 0; e4 < 8; ++e4) {
+          for (int e4 = 0; e4 < 4; ++e4) {
             const float4 cf = *(const float4*)(colf + colbase + e4 * 4);
             float4 cd = make_float4(0.f, 0.f, 0.f, 0.f);
             if (kKV && kNorm) cd = *(const float4*)(cold + colbase + e4 * 4);
@@ -231,8 +278,7 @@ __global__ void __launch_bounds__(256, 2) k_tc_ib(const __grid_constant__ CUtens
               f2 dp = {__uint_as_float(rd[e]), __uint_as_float(rd[e + 1])};
               const f2 cc = z ? f2{cf.z, cf.w} : f2{cf.x, cf.y};
               if (kNorm) dp = add2(dp, kKV ? (z ? f2{cd.z, cd.w} : f2{cd.x, cd.y}) : f2{dden_own, dden_own});
-              const f2 E = mul2(cc, rowf2);
-              const f2 T = mul2(E, sv);
+              const f2 T = mul2(mul2(cc, rowf2), sv);
               const f2 P = mul2(T, sv);
               const f2 dS = mul2(dp, T);
               red = fma2(dp, P, red);
@@ -240,68 +286,78 @@ __global__ void __launch_bounds__(256, 2) k_tc_ib(const __grid_constant__ CUtens
               pd[e >> 1] = pack_bf16(dS.x, dS.y);
             }
           }
+        } else if (all_masked) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) pp[e] = pd[e] = 0u;
         } else {
-          // diagonal block: exact exp(ell_i - ell_j) under the causal mask
+          // diagonal block: exact 2^(ell_i - ell_j) under the causal mask
 #pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            float Pv[2], dSv[2];
+          for (int e4 = 0; e4 < 4; ++e4) {
+            const float4 lc = *(const float4*)(ell_s + colbase + e4 * 4);
+            float4 cd = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (kKV && kNorm) cd = *(const float4*)(cold + colbase + e4 * 4);
+            const float lcv[4] = {lc.x, lc.y, lc.z, lc.w};
+            const float cdv[4] = {cd.x, cd.y, cd.z, cd.w};
+            float Pv[4], dSv[4];
 #pragma unroll
-            for (int z = 0; z < 2; ++z) {
-              const int col = colbase + e + z;
-              const float sv = __uint_as_float(rs[e + z]);
-              float dp = __uint_as_float(rd[e + z]);
-              if (kNorm) dp += kKV ? cold[col] : dden_own;
+            for (int z = 0; z < 4; ++z) {
+              const int e = e4 * 4 + z, col = colbase + e;
+              const float sv = __uint_as_float(rs[e]);
+              float dp = __uint_as_float(rd[e]);
+              if (kNorm) dp += kKV ? cdv[z] : dden_own;
               const bool valid = kKV ? (col >= own) : (col <= own);
-              const float li = kKV ? ell_s[col] : l_own, lj = kKV ? l_own : ell_s[col];
-              const float E = valid ? sig2 * __expf(fminf(li - lj, 0.f)) : 0.f;
+              const float d = kKV ? lcv[z] - l_own : l_own - lcv[z];
+              const float E = valid ? sig2 * exp2_approx(fminf(d, 0.f)) : 0.f;
               const float T = E * sv;
               Pv[z] = T * sv;
               dSv[z] = dp * T;
               red.x = fmaf(dp, Pv[z], red.x);
             }
-            pp[e >> 1] = pack_bf16(Pv[0], Pv[1]);
-            pd[e >> 1] = pack_bf16(dSv[0], dSv[1]);
+            pp[e4 * 2] = pack_bf16(Pv[0], Pv[1]);
+            pp[e4 * 2 + 1] = pack_bf16(Pv[2], Pv[3]);
+            pd[e4 * 2] = pack_bf16(dSv[0], dSv[1]);
+            pd[e4 * 2 + 1] = pack_bf16(dSv[2], dSv[3]);
           }
         }
-        // in place: bf16 pairs of columns [32ch, 32ch+32) land in columns [16ch, 16ch+16)
-        if (kKV) tmem_st16(tS + lane_off + ch * 16, pp);
-        tmem_st16(tDP + lane_off + ch * 16, pd);
+        // in place: bf16 pairs of columns [cofs, cofs+16) land in u32 columns
+        // [32 grp + 8 hh, +8) -- inside this warp's own, already-read range
+        if (kKV) tmem_st8(tS + lane_off + grp * 32 + hh * 8, pp);
+        tmem_st8(tDP + lane_off + grp * 32 + hh * 8, pd);
       }
       tc_wait_st();
+      PA_TR(n * 8 + 6);
       tc_fence_before();
       __syncwarp();
       if (l == 0) mbar_arrive(p_full);
     }
-    // epilogue: gradients in fp32 stream-major rows (dS carries a factor 1/2)
+    // epilogue: this warp's 32 gradient columns in fp32 stream-major rows
     mbar_wait(fin, 0);
     tc_fence_after();
     const size_t tokr = (size_t)s * g.t + c0 + own;
-    uint32_t r[64];
-    tmem_ld32(tA + lane_off, r);
-    tmem_ld32(tA + lane_off + 32, r + 32);
+    uint32_t r[32];
+    tmem_ld32(tA + lane_off + grp * 32, r);
     tc_wait_ld();
-    const float fa = kKV ? 1.f : 2.f;
-    float* oa = (kKV ? out_b : out_a) + tokr * HD;   // kKV: dV; q-side: dQ
+    const float fa = kKV ? 1.f : 2.f;   // dS carries a factor 1/2
+    float* oa = (kKV ? out_b : out_a) + tokr * HD + grp * 32;   // kKV: dV; q-side: dQ
 #pragma unroll
-    for (int a = 0; a < 64; a += 4)
+    for (int a = 0; a < 32; a += 4)
       *(float4*)(oa + a) = make_float4(fa * __uint_as_float(r[a]), fa * __uint_as_float(r[a + 1]),
                                        fa * __uint_as_float(r[a + 2]), fa * __uint_as_float(r[a + 3]));
     if (kKV) {
-      tmem_ld32(tB + lane_off, r);
-      tmem_ld32(tB + lane_off + 32, r + 32);
+      tmem_ld32(tB + lane_off + grp * 32, r);
       tc_wait_ld();
-      float* ob = out_a + tokr * HD;   // dK
+      float* ob = out_a + tokr * HD + grp * 32;   // dK
 #pragma unroll
-      for (int a = 0; a < 64; a += 4)
+      for (int a = 0; a < 32; a += 4)
         *(float4*)(ob + a) = make_float4(2.f * __uint_as_float(r[a]), 2.f * __uint_as_float(r[a + 1]),
                                          2.f * __uint_as_float(r[a + 2]), 2.f * __uint_as_float(r[a + 3]));
     }
     const float rr = red.x + red.y;
-    if (g.gated) dell[tokr] += kKV ? -rr : rr;
+    if (g.gated) atomicAdd(dell + tokr, kKV ? -rr : rr);
   }
   tc_fence_before();
   __syncthreads();
-  if (w == 2) tmem_dealloc<256>(tm);
+  if (w == W_TMEM) tmem_dealloc<256>(tm);
 }
 
 int tc_intra_bwd(const Geo& g, const CUtensorMap& m_q, const CUtensorMap& m_k, const CUtensorMap& m_v,
@@ -313,8 +369,8 @@ int tc_intra_bwd(const Geo& g, const CUtensorMap& m_q, const CUtensorMap& m_k, c
   auto qs = g.normalize ? k_tc_ib<false, true> : k_tc_ib<false, false>;
   cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
   cudaFuncSetAttribute(qs, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-  kv<<<grid, 256, SMEM, st>>>(m_q, m_k, m_v, m_dn, g, ell, dden, dk32, dv32, dell);
-  qs<<<grid, 256, SMEM, st>>>(m_q, m_k, m_v, m_dn, g, ell, dden, dq32, nullptr, dell);
+  kv<<<grid, THREADS, SMEM, st>>>(m_q, m_k, m_v, m_dn, g, ell, dden, dk32, dv32, dell);
+  qs<<<grid, THREADS, SMEM, st>>>(m_q, m_k, m_v, m_dn, g, ell, dden, dq32, nullptr, dell);
   return 0;
 }
 
