@@ -34,6 +34,18 @@ using namespace tc;
 
 __constant__ BlkTab c_blk = make_blk_tab();
 
+#ifdef PA_TRACE
+// debug build only (tools/trace_dphi.py): clock64 stamps of one dphi CTA
+__device__ long long g_trace2[512];
+extern "C" int pa_debug_trace2(long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_trace2, sizeof(long long) * n);
+}
+#define PA_TR2(c, i) \
+  if (c) g_trace2[(i)] = clock64()
+#else
+#define PA_TR2(c, i)
+#endif
+
 // ==========================================================================
 // prep kernels
 // ==========================================================================
@@ -894,9 +906,11 @@ constexpr int SMEM = 1024 + AB + A16 + NST * (BM + BD) + 256;
 
 template <int NTI>
 __device__ __forceinline__ void dphi_tiles(const float (&x)[64], float (&dx)[64], uint32_t dbase, uint32_t lane_off,
-                                           uint64_t* d_full, uint64_t* d_empty, int l) {
+                                           uint64_t* d_full, uint64_t* d_empty, int l, bool tr) {
   constexpr int db = NTI & 1;
+  PA_TR2(tr, 100 + NTI * 4 + 0);
   mbar_wait(&d_full[db], (NTI >> 1) & 1);
+  PA_TR2(tr, 100 + NTI * 4 + 1);
   tc_fence_after();
 #pragma unroll
   for (int ch = 0; ch < 4; ++ch) {
@@ -908,10 +922,11 @@ __device__ __forceinline__ void dphi_tiles(const float (&x)[64], float (&dx)[64]
     if (ch == 2) evjp_fblock<NTI * 4 + 2>(x, dx, r);
     if (ch == 3) evjp_fblock<NTI * 4 + 3>(x, dx, r);
   }
+  PA_TR2(tr, 100 + NTI * 4 + 2);
   tc_fence_before();
   __syncwarp();
   if (l == 0) mbar_arrive(&d_empty[db]);
-  if constexpr (NTI + 1 < dp::NT) dphi_tiles<NTI + 1>(x, dx, dbase, lane_off, d_full, d_empty, l);
+  if constexpr (NTI + 1 < dp::NT) dphi_tiles<NTI + 1>(x, dx, dbase, lane_off, d_full, d_empty, l, tr);
 }
 
 template <bool kUpd, int kDen>
@@ -1014,10 +1029,16 @@ __global__ void __launch_bounds__(256, 1) k_tc_dphi(const __grid_constant__ CUte
       tc_fence_after();
       const uint32_t am = smem_u32(a_s), a16 = smem_u32(a16_s);
       int j = 0;
+#ifdef PA_TRACE
+      const bool trm = kUpd && blockIdx.x == 0 && blockIdx.y == 5 && blockIdx.z == 3;
+#endif
+      PA_TR2(trm, 99);
       for (int nt = 0; nt < NT; ++nt, ++j) {
         const int st = j % NST, db = nt & 1;
         mbar_wait(&b_full[st], (j / NST) & 1);
+        PA_TR2(trm, nt * 4 + 0);
         if (nt >= 2) mbar_wait(&d_empty[db], ((nt >> 1) + 1) & 1);
+        PA_TR2(trm, nt * 4 + 1);
         tc_fence_after();
         const uint32_t bmm = smem_u32(bm_s + st * BM), bdd = smem_u32(bd_s + st * BD);
         const uint32_t dt = tm + (uint32_t)(db * 128);
@@ -1028,6 +1049,7 @@ __global__ void __launch_bounds__(256, 1) k_tc_dphi(const __grid_constant__ CUte
         if (den) mma_ss(dt, smem_desc(a16, 16, 256, 6), smem_desc(bdd, 16, 256, 6), id128, 1u);
         tc_commit(&d_full[db]);
         tc_commit(&b_empty[st]);
+        PA_TR2(trm, nt * 4 + 2);
       }
       if (kUpd) {
         for (int kb = 0; kb < NKB; ++kb, ++j) {
@@ -1043,6 +1065,7 @@ __global__ void __launch_bounds__(256, 1) k_tc_dphi(const __grid_constant__ CUte
                    (kb > 0 || kk > 0) ? 1u : 0u);
           tc_commit(&g_empty[bb]);
           tc_commit(&b_empty[st]);
+          PA_TR2(trm, 210 + kb);
         }
       }
       tc_commit(fin);
@@ -1078,7 +1101,12 @@ __global__ void __launch_bounds__(256, 1) k_tc_dphi(const __grid_constant__ CUte
       dx[2 * i] = 0.f;
       dx[2 * i + 1] = 0.f;
     }
-    dphi_tiles<0>(x, dx, tm, lane_off, d_full, d_empty, l);
+#ifdef PA_TRACE
+    const bool trc = kUpd && blockIdx.x == 0 && blockIdx.y == 5 && blockIdx.z == 3 && w == 4 && l == 0;
+#else
+    const bool trc = false;
+#endif
+    dphi_tiles<0>(x, dx, tm, lane_off, d_full, d_empty, l, trc);
     float c = 0.f;
 #pragma unroll
     for (int a = 0; a < 64; ++a) c = fmaf(dx[a], x[a], c);
@@ -1103,8 +1131,11 @@ __global__ void __launch_bounds__(256, 1) k_tc_dphi(const __grid_constant__ CUte
       // chunk this is an exclusive prefix sum (no cancellation), done in gate_finish
       if (g.gated) dellend[(size_t)s * g.t + tok] = c;
       // second GEMM: dU = W_j phi'(k_j) dS~  (A generated, 36 K blocks)
+      PA_TR2(trc, 200);
       gen_all_kblocks<0, NA>(xp, tm + 384u, lane_off, g_full, g_empty, l);
+      PA_TR2(trc, 201);
       mbar_wait(fin, 0);
+      PA_TR2(trc, 202);
       tc_fence_after();
       uint32_t r[64];
       tmem_ld32(tm + 256u + lane_off, r);
@@ -1678,19 +1709,12 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
   }
   {
     StageTimer tmr("bwd_query_state_dq", st);
-    auto fn = den ? k_tc_dphi<false, 1> : k_tc_dphi<false, 0>;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dp::SMEM);
-    fn<<<dim3(g.c / 128, g.n, g.ns), 256, dp::SMEM, st>>>(
-        m_dn16, m_dd128, g, (const __nv_bfloat16*)q, w.ell, w.lamlog, w.stm, w.std_, b.dq32, nullptr, b.dell,
-        nullptr, (__nv_bfloat16*)dq, nullptr);
+    tc_dphi(g, false, m_dn16, m_dd128, q, w.ell, w.lamlog, w.stm, w.std_, b.dq32, nullptr, b.dell, nullptr, dq,
+            nullptr, st);
   }
   {
     StageTimer tmr("bwd_update_state", st);
-    auto fn = den ? k_tc_dphi<true, 1> : k_tc_dphi<true, 0>;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dp::SMEM);
-    fn<<<dim3(g.c / 128, g.n, g.ns), 256, dp::SMEM, st>>>(
-        m_v16, m_dummy, g, (const __nv_bfloat16*)k, w.ell, w.lamlog, b.dsm, b.dsd, b.dk32, b.dv32, b.dell,
-        b.cu, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv);
+    tc_dphi(g, true, m_v16, m_dummy, k, w.ell, w.lamlog, b.dsm, b.dsd, b.dk32, b.dv32, b.dell, b.cu, dk, dv, st);
   }
   {
     StageTimer tmr("bwd_finish", st);

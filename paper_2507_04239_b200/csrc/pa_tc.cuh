@@ -20,4 +20,10 @@ int tc_intra_bwd(const Geo& g, const CUtensorMap& m_q, const CUtensorMap& m_k, c
                  const CUtensorMap& m_dn, const float* ell, const float* dden, float* dk32, float* dv32,
                  float* dq32, float* dell, cudaStream_t st);
 
+// token-major state VJP + fused expand-VJP (pa_tc_dphi.cu): final bf16 dq (query side)
+// or dk, dv (update side)
+int tc_dphi(const Geo& g, bool upd, const CUtensorMap& m_a, const CUtensorMap& m_a16, const void* xraw,
+            const float* ell, const float* lamlog, const __half* b_main, const __half* b_den, const float* dx32,
+            const float* dv32, float* dell, float* dellend, void* dxo, void* dvo, cudaStream_t st);
+
 }  // namespace pa

@@ -1,0 +1,378 @@
+// Token-major state VJP with the expand-VJP fused into the epilogue
+// (reference gradients.py:46-76 expand_vjp, 191-213 update-state VJP,
+// 406-431 query-state VJP), bf16/fp16 tcgen05 path, p = 2, d = e = 64.
+//
+//   query  (kUpd = false): dphi'(q~) = [dnum | dden] A'^T_{k-1}
+//          -> dq = intra part + sigma^2 gp_m J^T dphi',  dell_m += <dq~, q~>/2
+//   update (kUpd = true):  dphi'(k~) = [v | 1] dS~_k^T
+//          -> dk = intra part + W_j J^T dphi',  cu_j = <dk~, k~>/2
+//          and dv = intra part + W_j phi'(k_j) dS~_k (second GEMM)
+//
+// B200 design.  One CTA per 128-token tile.  The state (2304 feature slots x
+// 64 columns, fp16) is streamed once, in 128-slot tiles: each tile feeds the
+// dphi GEMM (M = 128 tokens, N = 128 slots, K = 64) and, on the update side,
+// the dv GEMM (M = 128 tokens, N = 64, K = these 128 slots) from the same
+// shared-memory stage (K-major for one, MN-major for the other), so the
+// state is read from L2 once per CTA instead of twice.
+// The expand-VJP loops over the 4x8 feature blocks with runtime block
+// indices: each thread's x (its token row, fp32 and fp16) and dx live in
+// shared memory (thread-private columns, conflict-free float4 rows) and the
+// per-block working set (4 + 8 values of x, 8 dx accumulators of the current
+// b-block) in registers.  The fully unrolled per-block code of the earlier
+// kernel was ~140 KB of SASS and stalled on instruction fetch.
+#include <cuda.h>
+
+#include "pa_common.cuh"
+#include "pa_sm100.cuh"
+#include "pa_tc.cuh"
+#include "pa_tc_common.cuh"
+
+namespace pa {
+using namespace sm100;
+using namespace tc;
+
+static __constant__ BlkTab c_blk_d = make_blk_tab();
+
+namespace dp2 {
+constexpr int AB = 128 * 128;    // A tile: 128 tokens x 64 fp16
+constexpr int A16 = 128 * 32;    // score-sum A tile: 128 tokens x 16 (SW32)
+constexpr int BM = 128 * 128;    // state stage: 128 slots x 64 fp16
+constexpr int BD = 128 * 32;     // state stage score-sum part
+constexpr int NST = 4;
+constexpr int NT = FH / 128;     // 18 slot tiles
+constexpr int XS = 16 * 128 * 16;   // fp32 x or dx: [16 float4][128 threads]
+constexpr int XH = 8 * 128 * 16;    // fp16 x: [8 uint4][128 threads]
+constexpr int SMEM = 1024 + AB + A16 + NST * (BM + BD) + 2 * XS + XH + 256;
+constexpr int THREADS = 224;     // w0..w3 compute, w4 TMEM, w5 TMA, w6 MMA
+constexpr int W_TMEM = 4, W_TMA = 5, W_MMA = 6;
+}  // namespace dp2
+
+struct ff2 {
+  float x, y;
+};
+__device__ __forceinline__ ff2 ffma2(ff2 a, ff2 b, ff2 c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "l"(*(uint64_t*)&a), "l"(*(uint64_t*)&b), "l"(*(uint64_t*)&c));
+  return *(ff2*)&r;
+}
+
+template <bool kUpd, int kDen>
+__global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
+    const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_a16, Geo g,
+    const __nv_bfloat16* __restrict__ xraw, const float* __restrict__ ell, const float* __restrict__ lamlog,
+    const __half* __restrict__ b_main, const __half* __restrict__ b_den, const float* __restrict__ dx32,
+    const float* __restrict__ dv32, float* dell, float* dellend, __nv_bfloat16* dxo, __nv_bfloat16* dvo) {
+  using namespace dp2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* a_s = smem;
+  uint8_t* a16_s = a_s + AB;
+  uint8_t* bm_s = a16_s + A16;
+  uint8_t* bd_s = bm_s + NST * BM;
+  float4* x_s = (float4*)(bd_s + NST * BD);
+  float4* dx_s = x_s + 16 * 128;
+  uint4* xh_s = (uint4*)(dx_s + 16 * 128);
+  uint64_t* bars = (uint64_t*)(xh_s + 8 * 128);
+  uint64_t* a_ready = bars;          // TMA tx + 4 compute-warp arrivals
+  uint64_t* b_full = a_ready + 1;    // NST
+  uint64_t* b_empty = b_full + NST;  // NST
+  uint64_t* d_full = b_empty + NST;  // 2
+  uint64_t* d_empty = d_full + 2;    // 2
+  uint64_t* g_full = d_empty + 2;    // 2
+  uint64_t* g_empty = g_full + 2;    // 2
+  uint64_t* fin = g_empty + 2;
+  __shared__ uint32_t tmem_base;
+
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  const int I = blockIdx.x, k = blockIdx.y, s = blockIdx.z;
+  const int tok0 = k * g.c + I * 128;
+  constexpr bool den = kDen != 0;
+  if (!kUpd && k == 0) {
+    // chunk 0 has no state query: its dq is the intra-chunk part alone
+    for (int i = tid; i < 128 * 16; i += THREADS) {
+      const int r = i >> 4, c4 = (i & 15) * 4;
+      const float4 v = *(const float4*)(dx32 + ((size_t)s * g.t + tok0 + r) * HD + c4);
+      *(uint2*)(dxo + rowid(g, s, tok0 + r) * HD + c4) = make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
+    }
+    return;
+  }
+  const int bslot = kUpd ? k : k - 1;   // state the B operand comes from
+  const __half* bm = b_main + (size_t)(s * g.n + bslot) * ((size_t)FH * 64);
+  const __half* bd = b_den + (size_t)(s * g.n + bslot) * ((size_t)FH * 16);
+  // undo the stored-state scale (A'_{k-1} for the query side, G_k for the update side)
+  const float sscale = 1.f / (kUpd ? pow2_neg_bits(g.n - 1 - k) : pow2_neg_bits(k - 1));
+
+  if (w == W_TMEM) tmem_alloc<512>(&tmem_base);
+  if (tid == 0) {
+    mbar_init(a_ready, 5);
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&b_full[i], 1);
+      mbar_init(&b_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&d_full[i], 1);
+      mbar_init(&d_empty[i], 4);
+      mbar_init(&g_full[i], 4);
+      mbar_init(&g_empty[i], 1);
+    }
+    mbar_init(fin, 1);
+    fence_barrier_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tmem_base;
+  // TMEM: dphi buffers [0, 256), dv accumulator [256, 320), generated phi'(k) buffers [384, 512)
+
+  if (w == W_TMA) {
+    if (l == 0) {
+      tma_prefetch(&tm_a);
+      mbar_expect_tx(a_ready, AB + ((!kUpd && den) ? A16 : 0));
+      tma_load_2d(a_s, &tm_a, a_ready, 0, s * g.t + tok0);
+      if (!kUpd && den) tma_load_2d(a16_s, &tm_a16, a_ready, 0, s * g.t + tok0);
+      for (int nt = 0; nt < NT; ++nt) {
+        const int st = nt % NST;
+        if (nt >= NST) mbar_wait(&b_empty[st], ((nt / NST) + 1) & 1);
+        mbar_expect_tx(&b_full[st], BM + (den ? BD : 0));
+        bulk_load(bm_s + st * BM, bm + (size_t)nt * 128 * 64, BM, &b_full[st]);
+        if (den) bulk_load(bd_s + st * BD, bd + (size_t)nt * 128 * 16, BD, &b_full[st]);
+      }
+    }
+  } else if (w == W_MMA) {
+    if (l == 0) {
+      constexpr uint32_t id128 = idesc_f16(128, 128, false, false);
+      constexpr uint32_t id64mn = idesc_f16(128, 64, false, true);
+      mbar_wait(a_ready, 0);
+      tc_fence_after();
+      const uint32_t am = smem_u32(a_s), a16 = smem_u32(a16_s);
+      for (int nt = 0; nt < NT; ++nt) {
+        const int st = nt % NST, db = nt & 1;
+        mbar_wait(&b_full[st], (nt / NST) & 1);
+        if (nt >= 2) mbar_wait(&d_empty[db], ((nt >> 1) + 1) & 1);
+        tc_fence_after();
+        const uint32_t bmm = smem_u32(bm_s + st * BM), bdd = smem_u32(bd_s + st * BD);
+        const uint32_t dt = tm + (uint32_t)(db * 128);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          mma_ss(dt, smem_desc(am + kk * 32, 16, 1024, 2), smem_desc(bmm + kk * 32, 16, 1024, 2), id128,
+                 kk > 0 ? 1u : 0u);
+        if (den) mma_ss(dt, smem_desc(a16, 16, 256, 6), smem_desc(bdd, 16, 256, 6), id128, 1u);
+        tc_commit(&d_full[db]);
+        if (kUpd) {
+          // dv += phi'(k) [128 tok x 128 slots] * dS~ tile [128 slots x 64] (same stage, MN-major)
+          mbar_wait(&g_full[db], (nt >> 1) & 1);
+          tc_fence_after();
+          const uint32_t ab = tm + 384u + (uint32_t)(db * 64);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            mma_ts(tm + 256u, ab + kk * 8, smem_desc(bmm + kk * 2048, 8192, 1024, 2), id64mn,
+                   (nt > 0 || kk > 0) ? 1u : 0u);
+          tc_commit(&g_empty[db]);
+        }
+        tc_commit(&b_empty[st]);
+      }
+      tc_commit(fin);
+    }
+  } else if (w < 4) {
+    const int q = w, row = q * 32 + l;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const int tok = tok0 + row;
+    const float lt = ell[(size_t)s * g.t + tok];
+    // phi' is generated from the exact bf16 row; the per-token factor
+    //   query : c_m = sigma^2 gp_m        (y_state = c_m phi'(q) A')
+    //   update: W_j = exp(lend - ell_j)   (S' = sum_j W_j phi'(k_j) u_j^T)
+    // multiplies the fp32 results instead of a rounded operand.
+    const float fct =
+        sscale * (kUpd ? (g.gated ? __expf(lamlog[s * g.n + k] - lt) : 1.f) : g.scale * g.scale * __expf(lt));
+    {
+      // stage this token's row: fp32 x and zero dx (thread-private float4 columns), fp16 x
+      const uint4* src = (const uint4*)(xraw + rowid(g, s, tok) * HD);
+#pragma unroll
+      for (int c8 = 0; c8 < 8; ++c8) {
+        const uint4 v4 = src[c8];
+        const uint32_t* pv = (const uint32_t*)&v4;
+        float f[8];
+#pragma unroll
+        for (int e2 = 0; e2 < 4; ++e2) {
+          const float2 f2 = __bfloat1622float2(*(const __nv_bfloat162*)&pv[e2]);
+          f[2 * e2] = f2.x;
+          f[2 * e2 + 1] = f2.y;
+        }
+        x_s[(2 * c8) * 128 + row] = make_float4(f[0], f[1], f[2], f[3]);
+        x_s[(2 * c8 + 1) * 128 + row] = make_float4(f[4], f[5], f[6], f[7]);
+        dx_s[(2 * c8) * 128 + row] = make_float4(0.f, 0.f, 0.f, 0.f);
+        dx_s[(2 * c8 + 1) * 128 + row] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (kUpd)
+          xh_s[c8 * 128 + row] =
+              make_uint4(pack_f16(f[0], f[1]), pack_f16(f[2], f[3]), pack_f16(f[4], f[5]), pack_f16(f[6], f[7]));
+      }
+    }
+    if (kUpd && den) {
+      // score-sum A tile for the update side, [v | 1]: row = token, column 0 = 1 (SW32 layout)
+      uint32_t* rowp = (uint32_t*)(a16_s + (size_t)row * 32);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) rowp[i] = 0u;
+      *(__half*)(a16_s + ((uint32_t)row * 32u + ((0u ^ (((uint32_t)row >> 2) & 1u)) << 4))) = __float2half_rn(1.f);
+      fence_async_smem();
+    }
+    __syncwarp();
+    if (l == 0) mbar_arrive(a_ready);
+
+    // generate phi'(k~) for the 128 slots of tile nt into TMEM buffer nt % 2
+    auto gen = [&](int nt) {
+      const int db = nt & 1;
+      if (nt >= 2) mbar_wait(&g_empty[db], ((nt >> 1) + 1) & 1);
+      const uint32_t gb = tm + 384u + (uint32_t)(db * 64) + lane_off;
+#pragma unroll
+      for (int cb = 0; cb < 4; ++cb) {
+        const int blk = nt * 4 + cb, al = c_blk_d.al[blk], be = c_blk_d.be[blk];
+        const uint2 xa = *(const uint2*)((const uint32_t*)&xh_s[(al >> 1) * 128 + row] + (al & 1) * 2);
+        const uint4 xb = xh_s[be * 128 + row];
+        const uint32_t xbv[4] = {xb.x, xb.y, xb.z, xb.w};
+        const uint32_t bc[4] = {__byte_perm(xa.x, 0, 0x1010), __byte_perm(xa.x, 0, 0x3232),
+                                __byte_perm(xa.y, 0, 0x1010), __byte_perm(xa.y, 0, 0x3232)};
+        uint32_t o[16];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int jp = 0; jp < 4; ++jp) o[i * 4 + jp] = hmul2_f16(bc[i], xbv[jp]);
+        tmem_st16(gb + (uint32_t)(cb * 16), o);
+      }
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (l == 0) mbar_arrive(&g_full[db]);
+    };
+
+    if (kUpd) gen(0);
+    ff2 dxb[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};   // dx of the current b-block (8 dims)
+    int cur_be = 0;
+    float4 xb0 = x_s[0 * 128 + row], xb1 = x_s[1 * 128 + row];
+    auto flush_b = [&](int be) {
+      float4 d0 = dx_s[(2 * be) * 128 + row], d1 = dx_s[(2 * be + 1) * 128 + row];
+      d0.x += dxb[0].x;
+      d0.y += dxb[0].y;
+      d0.z += dxb[1].x;
+      d0.w += dxb[1].y;
+      d1.x += dxb[2].x;
+      d1.y += dxb[2].y;
+      d1.z += dxb[3].x;
+      d1.w += dxb[3].y;
+      dx_s[(2 * be) * 128 + row] = d0;
+      dx_s[(2 * be + 1) * 128 + row] = d1;
+    };
+    for (int nt = 0; nt < NT; ++nt) {
+      if (kUpd && nt + 1 < NT) gen(nt + 1);
+      const int db = nt & 1;
+      mbar_wait(&d_full[db], (nt >> 1) & 1);
+      tc_fence_after();
+      const uint32_t dt = tm + (uint32_t)(db * 128) + lane_off;
+#pragma unroll 1
+      for (int cb = 0; cb < 4; ++cb) {
+        const int blk = nt * 4 + cb, al = c_blk_d.al[blk], be = c_blk_d.be[blk];
+        uint32_t gr[32];
+        tmem_ld32(dt + (uint32_t)(cb * 32), gr);
+        if (be != cur_be) {
+          flush_b(cur_be);
+          cur_be = be;
+          dxb[0] = dxb[1] = dxb[2] = dxb[3] = ff2{0.f, 0.f};
+          xb0 = x_s[(2 * be) * 128 + row];
+          xb1 = x_s[(2 * be + 1) * 128 + row];
+        }
+        const float4 xa = x_s[al * 128 + row];
+        tc_wait_ld();
+        const float xav[4] = {xa.x, xa.y, xa.z, xa.w};
+        const ff2 xbp[4] = {{xb0.x, xb0.y}, {xb0.z, xb0.w}, {xb1.x, xb1.y}, {xb1.z, xb1.w}};
+        float dxa[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const ff2 xai = {xav[i], xav[i]};
+          ff2 t = {0.f, 0.f};
+#pragma unroll
+          for (int jp = 0; jp < 4; ++jp) {
+            const ff2 gg = {__uint_as_float(gr[i * 8 + 2 * jp]), __uint_as_float(gr[i * 8 + 2 * jp + 1])};
+            dxb[jp] = ffma2(gg, xai, dxb[jp]);   // dx[b] += g x[a]
+            t = ffma2(gg, xbp[jp], t);           // dx[a] += g x[b]
+          }
+          dxa[i] = t.x + t.y;
+        }
+        float4 da = dx_s[al * 128 + row];
+        da.x += dxa[0];
+        da.y += dxa[1];
+        da.z += dxa[2];
+        da.w += dxa[3];
+        dx_s[al * 128 + row] = da;
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (l == 0) mbar_arrive(&d_empty[db]);
+    }
+    flush_b(cur_be);
+
+    // epilogue: final gradient rows (intra-chunk part + state part), stored once in bf16
+    float c = 0.f;
+    {
+      const float* o = dx32 + ((size_t)s * g.t + tok) * HD;
+      uint4* dst = (uint4*)(dxo + rowid(g, s, tok) * HD);
+#pragma unroll
+      for (int a8 = 0; a8 < 8; ++a8) {
+        const float4 d0 = dx_s[(2 * a8) * 128 + row], d1 = dx_s[(2 * a8 + 1) * 128 + row];
+        const float4 x0 = x_s[(2 * a8) * 128 + row], x1 = x_s[(2 * a8 + 1) * 128 + row];
+        c += d0.x * x0.x + d0.y * x0.y + d0.z * x0.z + d0.w * x0.w + d1.x * x1.x + d1.y * x1.y + d1.z * x1.z +
+             d1.w * x1.w;
+        const float4 v0 = *(const float4*)(o + a8 * 8), v1 = *(const float4*)(o + a8 * 8 + 4);
+        dst[a8] = make_uint4(pack_bf16(fmaf(d0.x, fct, v0.x), fmaf(d0.y, fct, v0.y)),
+                             pack_bf16(fmaf(d0.z, fct, v0.z), fmaf(d0.w, fct, v0.w)),
+                             pack_bf16(fmaf(d1.x, fct, v1.x), fmaf(d1.y, fct, v1.y)),
+                             pack_bf16(fmaf(d1.z, fct, v1.z), fmaf(d1.w, fct, v1.w)));
+      }
+    }
+    c *= 0.5f * fct;   // = d<.,.>/d(log factor): degree-2 homogeneity of phi'
+    if (!kUpd) {
+      if (g.gated) dell[(size_t)s * g.t + tok] += c;   // gp_m = exp(ell_m)
+    } else {
+      // suffix-decay cotangent: -c on ell_tok and +c on ell_end; summed over the
+      // chunk this is an exclusive prefix sum (no cancellation), done in gate_finish
+      if (g.gated) dellend[(size_t)s * g.t + tok] = c;
+      mbar_wait(fin, 0);
+      tc_fence_after();
+      uint32_t r[64];
+      tmem_ld32(tm + 256u + lane_off, r);
+      tmem_ld32(tm + 256u + lane_off + 32, r + 32);
+      tc_wait_ld();
+      const float* ov = dv32 + ((size_t)s * g.t + tok) * HD;
+      uint4* dst = (uint4*)(dvo + rowid(g, s, tok) * HD);
+#pragma unroll
+      for (int a = 0; a < 64; a += 8) {
+        const float4 v0 = *(const float4*)(ov + a), v1 = *(const float4*)(ov + a + 4);
+        float f[8];
+#pragma unroll
+        for (int z = 0; z < 8; ++z) f[z] = __uint_as_float(r[a + z]) * fct;
+        dst[a / 8] = make_uint4(pack_bf16(f[0] + v0.x, f[1] + v0.y), pack_bf16(f[2] + v0.z, f[3] + v0.w),
+                                pack_bf16(f[4] + v1.x, f[5] + v1.y), pack_bf16(f[6] + v1.z, f[7] + v1.w));
+      }
+    }
+  }
+  if (!kUpd && w < 4) mbar_wait(fin, 0);   // the MMA stream must drain before TMEM is released
+  tc_fence_before();
+  __syncthreads();
+  if (w == W_TMEM) tmem_dealloc<512>(tm);
+}
+
+int tc_dphi(const Geo& g, bool upd, const CUtensorMap& m_a, const CUtensorMap& m_a16, const void* xraw,
+            const float* ell, const float* lamlog, const __half* b_main, const __half* b_den, const float* dx32,
+            const float* dv32, float* dell, float* dellend, void* dxo, void* dvo, cudaStream_t st) {
+  using namespace dp2;
+  const int den = g.normalize ? 1 : 0;
+  auto fn = upd ? (den ? k_tc_dphi2<true, 1> : k_tc_dphi2<true, 0>)
+                : (den ? k_tc_dphi2<false, 1> : k_tc_dphi2<false, 0>);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  fn<<<dim3(g.c / 128, g.n, g.ns), THREADS, SMEM, st>>>(m_a, m_a16, g, (const __nv_bfloat16*)xraw, ell, lamlog,
+                                                         b_main, b_den, dx32, dv32, dell, dellend,
+                                                         (__nv_bfloat16*)dxo, (__nv_bfloat16*)dvo);
+  return 0;
+}
+
+}  // namespace pa
