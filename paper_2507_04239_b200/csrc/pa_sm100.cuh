@@ -52,7 +52,10 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 // Bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU.
+// A completed phase still costs one try_wait round trip (~160 cycles measured on
+// B200, tools/sync_rate.cu); the retry loop (with its yield) only runs on a miss.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return;
   uint32_t spins = 0;
   while (!mbar_try_wait(bar, parity)) {
     if (++spins > 20000000u) __trap();

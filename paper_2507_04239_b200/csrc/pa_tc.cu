@@ -1709,12 +1709,12 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
   }
   {
     StageTimer tmr("bwd_query_state_dq", st);
-    tc_dphi(g, false, m_dn16, m_dd128, q, w.ell, w.lamlog, w.stm, w.std_, b.dq32, nullptr, b.dell, nullptr, dq,
+    tc_dphi(g, false, b.dN16, b.dD, q, w.ell, w.lamlog, w.stm, w.std_, b.dq32, nullptr, b.dell, nullptr, dq,
             nullptr, st);
   }
   {
     StageTimer tmr("bwd_update_state", st);
-    tc_dphi(g, true, m_v16, m_dummy, k, w.ell, w.lamlog, b.dsm, b.dsd, b.dk32, b.dv32, b.dell, b.cu, dk, dv, st);
+    tc_dphi(g, true, b.v16, nullptr, k, w.ell, w.lamlog, b.dsm, b.dsd, b.dk32, b.dv32, b.dell, b.cu, dk, dv, st);
   }
   {
     StageTimer tmr("bwd_finish", st);

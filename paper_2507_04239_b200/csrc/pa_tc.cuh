@@ -22,7 +22,7 @@ int tc_intra_bwd(const Geo& g, const CUtensorMap& m_q, const CUtensorMap& m_k, c
 
 // token-major state VJP + fused expand-VJP (pa_tc_dphi.cu): final bf16 dq (query side)
 // or dk, dv (update side)
-int tc_dphi(const Geo& g, bool upd, const CUtensorMap& m_a, const CUtensorMap& m_a16, const void* xraw,
+int tc_dphi(const Geo& g, bool upd, const __half* a_rows, const __half* a16_rows, const void* xraw,
             const float* ell, const float* lamlog, const __half* b_main, const __half* b_den, const float* dx32,
             const float* dv32, float* dell, float* dellend, void* dxo, void* dvo, cudaStream_t st);
 

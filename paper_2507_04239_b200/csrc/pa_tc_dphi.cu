@@ -33,18 +33,37 @@ using namespace tc;
 
 static __constant__ BlkTab c_blk_d = make_blk_tab();
 
+#ifdef PA_TRACE
+// debug build only (tools/trace_dphi.py): clock64 stamps of one CTA
+__device__ long long g_trace3[512];
+extern "C" int pa_debug_trace3(long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_trace3, sizeof(long long) * n);
+}
+#define PA_TR3(c, i) \
+  if (c) g_trace3[(i)] = clock64()
+#else
+#define PA_TR3(c, i)
+#endif
+
 namespace dp2 {
-constexpr int AB = 128 * 128;    // A tile: 128 tokens x 64 fp16
-constexpr int A16 = 128 * 32;    // score-sum A tile: 128 tokens x 16 (SW32)
 constexpr int BM = 128 * 128;    // state stage: 128 slots x 64 fp16
 constexpr int BD = 128 * 32;     // state stage score-sum part
 constexpr int NST = 4;
 constexpr int NT = FH / 128;     // 18 slot tiles
 constexpr int XS = 16 * 128 * 16;   // fp32 x or dx: [16 float4][128 threads]
 constexpr int XH = 8 * 128 * 16;    // fp16 x: [8 uint4][128 threads]
-constexpr int SMEM = 1024 + AB + A16 + NST * (BM + BD) + 2 * XS + XH + 256;
-constexpr int THREADS = 224;     // w0..w3 compute, w4 TMEM, w5 TMA, w6 MMA
-constexpr int W_TMEM = 4, W_TMA = 5, W_MMA = 6;
+constexpr int SMEM = 1024 + NST * (BM + BD) + 3 * XS + XH + 256;
+// w0..w7 compute (two groups of four: group g owns the slot tiles nt = g mod 2,
+// i.e. TMEM buffer g, and its own dx copy), w8 TMEM, w9 TMA, w10/w11 MMA
+// (issuer m owns the tiles nt = m mod 2: each barrier wait costs ~160 cycles
+// even when the phase is complete, so two issuers overlap their wait and
+// commit latencies).  The issuing warps take the highest ids (the scheduler
+// prefers high warp ids).
+constexpr int THREADS = 384;
+// TMEM columns: dphi buffers [0, 256), dv accumulator [256, 320), A [320, 352),
+// score-sum A [352, 360), generated phi'(k) buffers [384, 512)
+constexpr uint32_t TA = 320, TA16 = 352;
+constexpr int W_TMEM = 8, W_TMA = 9, W_MMA = 10;   // MMA issuers: w10, w11
 }  // namespace dp2
 
 struct ff2 {
@@ -60,22 +79,20 @@ __device__ __forceinline__ ff2 ffma2(ff2 a, ff2 b, ff2 c) {
 
 template <bool kUpd, int kDen>
 __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
-    const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_a16, Geo g,
+    const __half* __restrict__ a_rows, const __half* __restrict__ a16_rows, Geo g,
     const __nv_bfloat16* __restrict__ xraw, const float* __restrict__ ell, const float* __restrict__ lamlog,
     const __half* __restrict__ b_main, const __half* __restrict__ b_den, const float* __restrict__ dx32,
     const float* __restrict__ dv32, float* dell, float* dellend, __nv_bfloat16* dxo, __nv_bfloat16* dvo) {
   using namespace dp2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* a_s = smem;
-  uint8_t* a16_s = a_s + AB;
-  uint8_t* bm_s = a16_s + A16;
+  uint8_t* bm_s = smem;
   uint8_t* bd_s = bm_s + NST * BM;
   float4* x_s = (float4*)(bd_s + NST * BD);
-  float4* dx_s = x_s + 16 * 128;
-  uint4* xh_s = (uint4*)(dx_s + 16 * 128);
+  float4* dx_all = x_s + 16 * 128;          // [2 groups][16][128]
+  uint4* xh_s = (uint4*)(dx_all + 2 * 16 * 128);
   uint64_t* bars = (uint64_t*)(xh_s + 8 * 128);
-  uint64_t* a_ready = bars;          // TMA tx + 4 compute-warp arrivals
+  uint64_t* a_ready = bars;          // A operand in TMEM: 4 compute-warp arrivals
   uint64_t* b_full = a_ready + 1;    // NST
   uint64_t* b_empty = b_full + NST;  // NST
   uint64_t* d_full = b_empty + NST;  // 2
@@ -106,7 +123,7 @@ __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
 
   if (w == W_TMEM) tmem_alloc<512>(&tmem_base);
   if (tid == 0) {
-    mbar_init(a_ready, 5);
+    mbar_init(a_ready, 4);
     for (int i = 0; i < NST; ++i) {
       mbar_init(&b_full[i], 1);
       mbar_init(&b_empty[i], 1);
@@ -117,7 +134,7 @@ __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
       mbar_init(&g_full[i], 4);
       mbar_init(&g_empty[i], 1);
     }
-    mbar_init(fin, 1);
+    mbar_init(fin, 2);
     fence_barrier_init();
   }
   tc_fence_before();
@@ -128,10 +145,6 @@ __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
 
   if (w == W_TMA) {
     if (l == 0) {
-      tma_prefetch(&tm_a);
-      mbar_expect_tx(a_ready, AB + ((!kUpd && den) ? A16 : 0));
-      tma_load_2d(a_s, &tm_a, a_ready, 0, s * g.t + tok0);
-      if (!kUpd && den) tma_load_2d(a16_s, &tm_a16, a_ready, 0, s * g.t + tok0);
       for (int nt = 0; nt < NT; ++nt) {
         const int st = nt % NST;
         if (nt >= NST) mbar_wait(&b_empty[st], ((nt / NST) + 1) & 1);
@@ -140,54 +153,68 @@ __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
         if (den) bulk_load(bd_s + st * BD, bd + (size_t)nt * 128 * 16, BD, &b_full[st]);
       }
     }
-  } else if (w == W_MMA) {
+  } else if (w >= W_MMA) {
     if (l == 0) {
+      const int mw = w - W_MMA;
       constexpr uint32_t id128 = idesc_f16(128, 128, false, false);
       constexpr uint32_t id64mn = idesc_f16(128, 64, false, true);
       mbar_wait(a_ready, 0);
       tc_fence_after();
-      const uint32_t am = smem_u32(a_s), a16 = smem_u32(a16_s);
-      for (int nt = 0; nt < NT; ++nt) {
+      // descriptors are built once; per-MMA work is a 64-bit add of (byte offset >> 4)
+      const uint64_t bk0 = smem_desc(smem_u32(bm_s), 16, 1024, 2);      // K-major view of a state stage
+      const uint64_t bn0 = smem_desc(smem_u32(bm_s), 8192, 1024, 2);    // MN-major view of the same stage
+      const uint64_t bd0 = smem_desc(smem_u32(bd_s), 16, 256, 6);
+#ifdef PA_TRACE
+      const bool trm = kUpd && blockIdx.x == 0 && blockIdx.y == 5 && blockIdx.z == 3 && mw == 0;
+#endif
+      PA_TR3(trm, 99);
+      for (int nt = mw; nt < NT; nt += 2) {
         const int st = nt % NST, db = nt & 1;
         mbar_wait(&b_full[st], (nt / NST) & 1);
+        PA_TR3(trm, nt * 4 + 0);
         if (nt >= 2) mbar_wait(&d_empty[db], ((nt >> 1) + 1) & 1);
+        PA_TR3(trm, nt * 4 + 1);
         tc_fence_after();
-        const uint32_t bmm = smem_u32(bm_s + st * BM), bdd = smem_u32(bd_s + st * BD);
+        const uint64_t so = (uint64_t)((st * BM) >> 4);
         const uint32_t dt = tm + (uint32_t)(db * 128);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          mma_ss(dt, smem_desc(am + kk * 32, 16, 1024, 2), smem_desc(bmm + kk * 32, 16, 1024, 2), id128,
-                 kk > 0 ? 1u : 0u);
-        if (den) mma_ss(dt, smem_desc(a16, 16, 256, 6), smem_desc(bdd, 16, 256, 6), id128, 1u);
+          mma_ts(dt, tm + TA + (uint32_t)(kk * 8), bk0 + so + (uint64_t)(kk * 2), id128, kk > 0 ? 1u : 0u);
+        if (den) mma_ts(dt, tm + TA16, bd0 + (uint64_t)((st * BD) >> 4), id128, 1u);
         tc_commit(&d_full[db]);
+        PA_TR3(trm, 400 + nt);
         if (kUpd) {
           // dv += phi'(k) [128 tok x 128 slots] * dS~ tile [128 slots x 64] (same stage, MN-major)
           mbar_wait(&g_full[db], (nt >> 1) & 1);
+          PA_TR3(trm, nt * 4 + 2);
           tc_fence_after();
           const uint32_t ab = tm + 384u + (uint32_t)(db * 64);
+          // both issuers accumulate into the zero-initialised dv columns
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            mma_ts(tm + 256u, ab + kk * 8, smem_desc(bmm + kk * 2048, 8192, 1024, 2), id64mn,
-                   (nt > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < 8; ++kk) mma_ts(tm + 256u, ab + kk * 8, bn0 + so + (uint64_t)(kk * 128), id64mn, 1u);
           tc_commit(&g_empty[db]);
         }
         tc_commit(&b_empty[st]);
+        PA_TR3(trm, nt * 4 + 3);
       }
       tc_commit(fin);
     }
-  } else if (w < 4) {
-    const int q = w, row = q * 32 + l;
+  } else if (w < 8) {
+    const int q = w & 3, grp = w >> 2, row = q * 32 + l;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const int tok = tok0 + row;
     const float lt = ell[(size_t)s * g.t + tok];
+    float4* dx_s = dx_all + grp * (16 * 128);
     // phi' is generated from the exact bf16 row; the per-token factor
     //   query : c_m = sigma^2 gp_m        (y_state = c_m phi'(q) A')
     //   update: W_j = exp(lend - ell_j)   (S' = sum_j W_j phi'(k_j) u_j^T)
     // multiplies the fp32 results instead of a rounded operand.
     const float fct =
         sscale * (kUpd ? (g.gated ? __expf(lamlog[s * g.n + k] - lt) : 1.f) : g.scale * g.scale * __expf(lt));
-    {
-      // stage this token's row: fp32 x and zero dx (thread-private float4 columns), fp16 x
+#pragma unroll
+    for (int i = 0; i < 16; ++i) dx_s[i * 128 + row] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (grp == 0) {
+      // stage this token's row: fp32 x (thread-private float4 columns) and fp16 x
       const uint4* src = (const uint4*)(xraw + rowid(g, s, tok) * HD);
 #pragma unroll
       for (int c8 = 0; c8 < 8; ++c8) {
@@ -202,28 +229,57 @@ __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
         }
         x_s[(2 * c8) * 128 + row] = make_float4(f[0], f[1], f[2], f[3]);
         x_s[(2 * c8 + 1) * 128 + row] = make_float4(f[4], f[5], f[6], f[7]);
-        dx_s[(2 * c8) * 128 + row] = make_float4(0.f, 0.f, 0.f, 0.f);
-        dx_s[(2 * c8 + 1) * 128 + row] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (kUpd)
           xh_s[c8 * 128 + row] =
               make_uint4(pack_f16(f[0], f[1]), pack_f16(f[2], f[3]), pack_f16(f[4], f[5]), pack_f16(f[6], f[7]));
       }
     }
-    if (kUpd && den) {
-      // score-sum A tile for the update side, [v | 1]: row = token, column 0 = 1 (SW32 layout)
-      uint32_t* rowp = (uint32_t*)(a16_s + (size_t)row * 32);
+    if (grp == 0) {
+      // the A operand of the dphi GEMM goes to TMEM (one row per lane): the MMA then
+      // reads only the state tile from shared memory
+      uint32_t ar[32];
+      const uint4* src = (const uint4*)(a_rows + ((size_t)s * g.t + tok) * HD);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) rowp[i] = 0u;
-      *(__half*)(a16_s + ((uint32_t)row * 32u + ((0u ^ (((uint32_t)row >> 2) & 1u)) << 4))) = __float2half_rn(1.f);
-      fence_async_smem();
+      for (int c8 = 0; c8 < 8; ++c8) *(uint4*)&ar[c8 * 4] = src[c8];
+      tmem_st16(tm + TA + lane_off, ar);
+      tmem_st16(tm + TA + 16 + lane_off, ar + 16);
+      if (kUpd) {
+        uint32_t z[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) z[i] = 0u;
+#pragma unroll
+        for (int c = 0; c < 64; c += 16) tmem_st16(tm + 256u + lane_off + c, z);   // dv accumulator
+      }
+      if (den) {
+        uint32_t a16[8];
+        if (kUpd) {
+          // [v | 1]: column 0 = 1
+          a16[0] = pack_f16(1.f, 0.f);
+#pragma unroll
+          for (int i = 1; i < 8; ++i) a16[i] = 0u;
+        } else {
+          const uint4* s16 = (const uint4*)(a16_rows + ((size_t)s * g.t + tok) * 16);
+          *(uint4*)&a16[0] = s16[0];
+          *(uint4*)&a16[4] = s16[1];
+        }
+        tmem_st8(tm + TA16 + lane_off, a16);
+      }
+      tc_wait_st();
+      tc_fence_before();
     }
     __syncwarp();
-    if (l == 0) mbar_arrive(a_ready);
+    if (grp == 0 && l == 0) mbar_arrive(a_ready);
+    asm volatile("bar.sync 1, 256;" ::: "memory");   // x staged for both groups
 
     // generate phi'(k~) for the 128 slots of tile nt into TMEM buffer nt % 2
+#ifdef PA_TRACE
+    const bool trc = kUpd && blockIdx.x == 0 && blockIdx.y == 5 && blockIdx.z == 3 && (w & 3) == 0 && l == 0;
+#endif
     auto gen = [&](int nt) {
       const int db = nt & 1;
+      PA_TR3(trc, 300 + nt * 3 + 0);
       if (nt >= 2) mbar_wait(&g_empty[db], ((nt >> 1) + 1) & 1);
+      PA_TR3(trc, 300 + nt * 3 + 1);
       const uint32_t gb = tm + 384u + (uint32_t)(db * 64) + lane_off;
 #pragma unroll
       for (int cb = 0; cb < 4; ++cb) {
@@ -241,12 +297,13 @@ __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
         tmem_st16(gb + (uint32_t)(cb * 16), o);
       }
       tc_wait_st();
+      PA_TR3(trc, 300 + nt * 3 + 2);
       tc_fence_before();
       __syncwarp();
       if (l == 0) mbar_arrive(&g_full[db]);
     };
 
-    if (kUpd) gen(0);
+    if (kUpd) gen(grp);
     ff2 dxb[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};   // dx of the current b-block (8 dims)
     int cur_be = 0;
     float4 xb0 = x_s[0 * 128 + row], xb1 = x_s[1 * 128 + row];
@@ -263,10 +320,12 @@ __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
       dx_s[(2 * be) * 128 + row] = d0;
       dx_s[(2 * be + 1) * 128 + row] = d1;
     };
-    for (int nt = 0; nt < NT; ++nt) {
-      if (kUpd && nt + 1 < NT) gen(nt + 1);
+    for (int nt = grp; nt < NT; nt += 2) {
+      PA_TR3(trc, 100 + nt * 4 + 0);
       const int db = nt & 1;
+      PA_TR3(trc, 100 + nt * 4 + 1);
       mbar_wait(&d_full[db], (nt >> 1) & 1);
+      PA_TR3(trc, 100 + nt * 4 + 2);
       tc_fence_after();
       const uint32_t dt = tm + (uint32_t)(db * 128) + lane_off;
 #pragma unroll 1
@@ -305,20 +364,29 @@ __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
         da.w += dxa[3];
         dx_s[al * 128 + row] = da;
       }
+      PA_TR3(trc, 100 + nt * 4 + 3);
       tc_fence_before();
       __syncwarp();
       if (l == 0) mbar_arrive(&d_empty[db]);
+      if (kUpd && nt + 2 < NT) gen(nt + 2);
     }
     flush_b(cur_be);
+    PA_TR3(trc, 200);
+    asm volatile("bar.sync 1, 256;" ::: "memory");   // both dx copies complete
 
-    // epilogue: final gradient rows (intra-chunk part + state part), stored once in bf16
+    // epilogue: group 0 writes the final gradient rows (intra-chunk part + state
+    // part, stored once in bf16); group 1 the dv rows on the update side
     float c = 0.f;
-    {
+    if (grp == 0) {
+      const float4* dx1 = dx_all + 16 * 128;
       const float* o = dx32 + ((size_t)s * g.t + tok) * HD;
       uint4* dst = (uint4*)(dxo + rowid(g, s, tok) * HD);
 #pragma unroll
       for (int a8 = 0; a8 < 8; ++a8) {
-        const float4 d0 = dx_s[(2 * a8) * 128 + row], d1 = dx_s[(2 * a8 + 1) * 128 + row];
+        float4 d0 = dx_s[(2 * a8) * 128 + row], d1 = dx_s[(2 * a8 + 1) * 128 + row];
+        const float4 e0 = dx1[(2 * a8) * 128 + row], e1 = dx1[(2 * a8 + 1) * 128 + row];
+        d0 = make_float4(d0.x + e0.x, d0.y + e0.y, d0.z + e0.z, d0.w + e0.w);
+        d1 = make_float4(d1.x + e1.x, d1.y + e1.y, d1.z + e1.z, d1.w + e1.w);
         const float4 x0 = x_s[(2 * a8) * 128 + row], x1 = x_s[(2 * a8 + 1) * 128 + row];
         c += d0.x * x0.x + d0.y * x0.y + d0.z * x0.z + d0.w * x0.w + d1.x * x1.x + d1.y * x1.y + d1.z * x1.z +
              d1.w * x1.w;
@@ -331,12 +399,15 @@ __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
     }
     c *= 0.5f * fct;   // = d<.,.>/d(log factor): degree-2 homogeneity of phi'
     if (!kUpd) {
-      if (g.gated) dell[(size_t)s * g.t + tok] += c;   // gp_m = exp(ell_m)
-    } else {
+      if (grp == 0 && g.gated) dell[(size_t)s * g.t + tok] += c;   // gp_m = exp(ell_m)
+    } else if (grp == 0) {
       // suffix-decay cotangent: -c on ell_tok and +c on ell_end; summed over the
       // chunk this is an exclusive prefix sum (no cancellation), done in gate_finish
       if (g.gated) dellend[(size_t)s * g.t + tok] = c;
+    } else {
+      PA_TR3(trc, 201);
       mbar_wait(fin, 0);
+      PA_TR3(trc, 202);
       tc_fence_after();
       uint32_t r[64];
       tmem_ld32(tm + 256u + lane_off, r);
@@ -355,13 +426,13 @@ __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
       }
     }
   }
-  if (!kUpd && w < 4) mbar_wait(fin, 0);   // the MMA stream must drain before TMEM is released
+  if (w < 8) mbar_wait(fin, 0);   // the MMA stream must drain before TMEM is released
   tc_fence_before();
   __syncthreads();
   if (w == W_TMEM) tmem_dealloc<512>(tm);
 }
 
-int tc_dphi(const Geo& g, bool upd, const CUtensorMap& m_a, const CUtensorMap& m_a16, const void* xraw,
+int tc_dphi(const Geo& g, bool upd, const __half* a_rows, const __half* a16_rows, const void* xraw,
             const float* ell, const float* lamlog, const __half* b_main, const __half* b_den, const float* dx32,
             const float* dv32, float* dell, float* dellend, void* dxo, void* dvo, cudaStream_t st) {
   using namespace dp2;
@@ -369,7 +440,7 @@ int tc_dphi(const Geo& g, bool upd, const CUtensorMap& m_a, const CUtensorMap& m
   auto fn = upd ? (den ? k_tc_dphi2<true, 1> : k_tc_dphi2<true, 0>)
                 : (den ? k_tc_dphi2<false, 1> : k_tc_dphi2<false, 0>);
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-  fn<<<dim3(g.c / 128, g.n, g.ns), THREADS, SMEM, st>>>(m_a, m_a16, g, (const __nv_bfloat16*)xraw, ell, lamlog,
+  fn<<<dim3(g.c / 128, g.n, g.ns), THREADS, SMEM, st>>>(a_rows, a16_rows, g, (const __nv_bfloat16*)xraw, ell, lamlog,
                                                          b_main, b_den, dx32, dv32, dell, dellend,
                                                          (__nv_bfloat16*)dxo, (__nv_bfloat16*)dvo);
   return 0;

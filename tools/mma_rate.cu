@@ -11,6 +11,15 @@
 
 using namespace pa::sm100;
 
+__device__ __forceinline__ void mma_ts_elect(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+
 __global__ void __launch_bounds__(128, 1) rate(int var, int ts, int bmn, int N, int R, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -170,6 +179,36 @@ __global__ void __launch_bounds__(128, 1) rate(int var, int ts, int bmn, int N, 
     long long t1 = clock64();
     out[blockIdx.x] = (unsigned long long)(t1 - t0);
   }
+  else if (var == 9 && tid < 32) {
+    // whole warp, descriptor arithmetic per MMA, elect inside the asm
+    const uint32_t id = idesc_f16(128, N, false, false);
+    const uint32_t b = smem_u32(smem + 32768);
+    long long t0 = clock64();
+    for (int i = 0; i < R; ++i) {
+      const int kk = i & 3;
+      mma_ts_elect(tm, tm + 256u + (uint32_t)(kk * 8), smem_desc(b + (i & 7) * 2048 + kk * 32, 16, 1024, 2), id,
+                   i > 0 ? 1u : 0u);
+    }
+    if (elect_one()) tc_commit(&bar);
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    if (tid == 0) out[blockIdx.x] = (unsigned long long)(t1 - t0);
+  } else if (var == 10 && tid == 0) {
+    // single thread, descriptor arithmetic per MMA (like the kernels)
+    const uint32_t id = idesc_f16(128, N, false, false);
+    const uint32_t b = smem_u32(smem + 32768);
+    long long t0 = clock64();
+    for (int i = 0; i < R; ++i) {
+      const int kk = i & 3;
+      mma_ts(tm, tm + 256u + (uint32_t)(kk * 8), smem_desc(b + (i & 7) * 2048 + kk * 32, 16, 1024, 2), id,
+             i > 0 ? 1u : 0u);
+    }
+    tc_commit(&bar);
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    out[blockIdx.x] = (unsigned long long)(t1 - t0);
+  }
   tc_fence_before();
   __syncthreads();
   if (tid < 32) tmem_dealloc<512>(tm);
@@ -214,48 +253,83 @@ __global__ void __launch_bounds__(128, 1) rate2(int N, int R, unsigned long long
   if (tid < 32) tmem_dealloc<COLS>(tm);
 }
 
+__global__ void __launch_bounds__(128, 1) rate3(int N, int R, int mode, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, w = tid >> 5;
+  if (tid < 32) tmem_alloc<512>(&tbase);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  for (int i = tid; i < 40 * 1024 / 4; i += 128) ((uint32_t*)smem)[i] = 0x3c003c00u;
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tbase;
+  if (tid == 0) {
+    const uint32_t id = idesc_f16(128, N, false, false);
+    const uint32_t b = smem_u32(smem + 16384);
+    uint64_t bd[4];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) bd[kk] = smem_desc(b + kk * 32, 16, 1024, 2);
+    long long t0 = clock64();
+    for (int i = 0; i < R; i += 4) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) mma_ts(tm, tm + 256u + (uint32_t)(kk * 8), bd[kk], id, 1u);
+    }
+    tc_commit(&bar);
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    out[blockIdx.x] = (unsigned long long)(t1 - t0);
+  } else if (w >= 1 && mode > 0) {
+    // other warps: tcgen05.ld (mode 1) or tcgen05.st (mode 2) traffic on columns [384, 512)
+    const uint32_t lane_off = (uint32_t)((w & 3) * 32) << 16;
+    uint32_t r[16];
+    for (int i = 0; i < 16; ++i) r[i] = i;
+    float acc = 0.f;
+    for (int it = 0; it < R / 8; ++it) {
+      if (mode == 1) {
+        tmem_ld16(tm + 384u + lane_off + (uint32_t)((it & 7) * 16), r);
+        tc_wait_ld();
+        acc += __uint_as_float(r[it & 15]);
+      } else {
+        tmem_st16(tm + 384u + lane_off + (uint32_t)((it & 7) * 16), r);
+        tc_wait_st();
+      }
+    }
+    if (acc == 12345.f) out[0] = 0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (tid < 32) tmem_dealloc<512>(tm);
+}
+
 int main() {
   unsigned long long* d;
   cudaMalloc(&d, 148 * 8);
   cudaFuncSetAttribute(rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   const int R = 8192;
   {
-    unsigned long long* d2;
-    cudaMalloc(&d2, 296 * 8);
-    cudaFuncSetAttribute(rate2<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
-    cudaFuncSetAttribute(rate2<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
-    for (int cols : {256, 512})
-      for (int sm : {48, 100})
-        for (int N : {64, 128}) {
-          auto fn = cols == 256 ? rate2<256> : rate2<512>;
-          fn<<<148, 128, sm * 1024>>>(N, 8192, d2);
-          fn<<<148, 128, sm * 1024>>>(N, 8192, d2);
-          cudaError_t e = cudaDeviceSynchronize();
-          unsigned long long h[296];
-          cudaMemcpy(h, d2, sizeof h, cudaMemcpyDeviceToHost);
-          double avg = 0;
-          for (int i = 0; i < 148; ++i) avg += h[i];
-          avg /= 148;
-          printf("rate2 cols %d smem %dKB N=%d: %.2f cyc per MMA (%s)\n", cols, sm, N, avg / 8192,
-                 e ? cudaGetErrorString(e) : "ok");
-        }
-  }
-  for (int var = 6; var < 6; ++var)
-  for (int ts = 1; ts < 2; ++ts)
-    for (int bmn : {128, 192, 256, 320, 384, 448})
-      for (int N : {32, 64, 128}) {
-        
-        rate<<<148, 128, 100 * 1024>>>(var, ts, bmn, N, R, d);
-        rate<<<148, 128, 100 * 1024>>>(var, ts, bmn, N, R, d);
+    unsigned long long* d3;
+    cudaMalloc(&d3, 148 * 8);
+    cudaFuncSetAttribute(rate3, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024);
+    for (int mode = 0; mode < 3; ++mode)
+      for (int N : {64, 128}) {
+        rate3<<<148, 128, 48 * 1024>>>(N, 8192, mode, d3);
+        rate3<<<148, 128, 48 * 1024>>>(N, 8192, mode, d3);
         cudaError_t e = cudaDeviceSynchronize();
         unsigned long long h[148];
-        cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+        cudaMemcpy(h, d3, sizeof h, cudaMemcpyDeviceToHost);
         double avg = 0;
         for (int i = 0; i < 148; ++i) avg += h[i];
         avg /= 148;
-        const double cyc = avg / R;
-        printf("var%d %s Acol %d N=%3d : %6.2f cyc/MMA  ideal %5.1f  -> %5.1f%% of 8192 FLOP/clk  %s\n", var, ts ? "TS" : "SS",
-               bmn, N, cyc, N / 2.0, 100.0 * (N / 2.0) / cyc, e ? cudaGetErrorString(e) : "");
+        printf("rate3 mode %d (0 none, 1 concurrent tcgen05.ld, 2 concurrent tcgen05.st) N=%d: %.2f cyc/MMA (%s)\n", mode,
+               N, avg / 8192, e ? cudaGetErrorString(e) : "ok");
       }
+  }
   return 0;
 }

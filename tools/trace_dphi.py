@@ -20,11 +20,12 @@ for _ in range(2):
     torch.autograd.grad(y, [Q, K, V, lg], torch.ones_like(y))
 torch.cuda.synchronize()
 buf = (ctypes.c_longlong * 512)()
-_lib.load().pa_debug_trace2(buf, 512)
+_lib.load().pa_debug_trace3(buf, 512)
 base = buf[99]
 for nt in range(18):
-    m = [buf[nt * 4 + i] - base for i in range(3)]
-    c = [buf[100 + nt * 4 + i] - base for i in range(3)]
-    print(f"tile {nt:2d}: mma b_full {m[0]:7d} d_empty {m[1]:7d} issued {m[2]:7d} | epi wait {c[0]:7d} got {c[1]:7d} done {c[2]:7d}")
-print("phase2 gen start", buf[200] - base, "gen done", buf[201] - base, "fin", buf[202] - base)
-print("phase2 kb issue", [buf[210 + kb] - base for kb in range(36)])
+    m = [buf[nt * 4 + i] - base for i in range(4)]
+    c = [buf[100 + nt * 4 + i] - base for i in range(4)]
+    gg = [buf[300 + nt * 3 + i] - base for i in range(3)]
+    print(f"tile {nt:2d}: MMA b_full {m[0]:6d} d_empty {m[1]:6d} dphi_iss {buf[400 + nt] - base:6d} g_full {m[2]:6d} "
+          f"dv_iss {m[3]:6d} | GEN start {gg[0]:6d} g_empty {gg[1]:6d} st_done {gg[2]:6d} | EPI got_d {c[2]:6d} "
+          f"done {c[3]:6d}")
