@@ -404,12 +404,16 @@ namespace outk {
 constexpr int QB = 128 * 128;           // Q tile bytes (128 tok x 64 dims bf16)
 constexpr int KB = 128 * 128;           // K tile
 constexpr int VB = 128 * 128;           // V tile
-constexpr int STB = 64 * 128;           // state K-block: 64 slots x 64 values
-constexpr int STD = 64 * 32;            // state K-block score-sum part
+// state query in steps of 128 slots (2 K-blocks): one barrier round trip per
+// 8 MMAs (each wait costs ~160 cycles even when the phase is complete)
+constexpr int STB = 128 * 128;          // state step: 128 slots x 64 values
+constexpr int STD = 128 * 32;           // state step score-sum part
+constexpr int NSTEP = NKB / 2;          // 18
 constexpr int KV_ST = 3;
-constexpr int ST_ST = 8;
-constexpr int NA = 4;                   // TMEM A buffers (64 slots each)
-constexpr int SMEM = 1024 + QB + KV_ST * (KB + VB) + ST_ST * (STB + STD) + 2048 + 4096 + 1024 + 512;
+constexpr int ST_ST = 4;
+constexpr int NA = 2;                   // TMEM A buffers (128 slots = 64 columns each)
+constexpr int XH = 8 * 128 * 16;        // fp16 q rows, thread-private uint4 columns
+constexpr int SMEM = 1024 + QB + KV_ST * (KB + VB) + ST_ST * (STB + STD) + XH + 2048 + 4096 + 1024 + 512;
 }  // namespace outk
 
 // compute warps: phi'(x) for the 36 K blocks of one token row, each written to
@@ -430,6 +434,40 @@ __device__ __forceinline__ void gen_all_kblocks(const uint32_t (&xp)[32], uint32
   __syncwarp();
   if (l == 0) mbar_arrive(&a_full[bb]);
   if constexpr (KB + 1 < NKB) gen_all_kblocks<KB + 1, NA>(xp, a_base, lane_off, a_full, a_empty, l);
+}
+
+// phi'(x) for the 2304 slots in 18 steps of 128 slots (4 feature blocks, 64
+// TMEM columns), alternating over 2 TMEM A buffers.  x is this thread's row as
+// fp16 pairs in shared memory ([8][128] uint4, thread-private columns), so the
+// loop body is one copy of the code with runtime block indices (the per-block
+// unrolled version was ~40 KB of SASS and stalled on instruction fetch).
+__device__ __forceinline__ void gen_steps(const uint4* xh_s, int row, uint32_t a_base, uint32_t lane_off,
+                                          uint64_t* a_full, uint64_t* a_empty, int l) {
+#pragma unroll 1
+  for (int stp = 0; stp < NKB / 2; ++stp) {
+    const int bb = stp & 1;
+    if (stp >= 2) mbar_wait(&a_empty[bb], ((stp >> 1) + 1) & 1);
+    const uint32_t ab = a_base + (uint32_t)(bb * 64) + lane_off;
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      const int blk = stp * 4 + f, al = c_blk.al[blk], be = c_blk.be[blk];
+      const uint2 xa = *(const uint2*)((const uint32_t*)&xh_s[(al >> 1) * 128 + row] + (al & 1) * 2);
+      const uint4 xb = xh_s[be * 128 + row];
+      const uint32_t xbv[4] = {xb.x, xb.y, xb.z, xb.w};
+      const uint32_t bc[4] = {__byte_perm(xa.x, 0, 0x1010), __byte_perm(xa.x, 0, 0x3232),
+                              __byte_perm(xa.y, 0, 0x1010), __byte_perm(xa.y, 0, 0x3232)};
+      uint32_t o[16];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int jp = 0; jp < 4; ++jp) o[i * 4 + jp] = hmul2_f16(bc[i], xbv[jp]);
+      tmem_st16(ab + (uint32_t)(f * 16), o);
+    }
+    tc_wait_st();
+    tc_fence_before();
+    __syncwarp();
+    if (l == 0) mbar_arrive(&a_full[bb]);
+  }
 }
 
 // a bf16 row of 64 as fp16 pairs (exact for |x| < 65504)
@@ -478,7 +516,8 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
   uint8_t* v_s = k_s + KV_ST * KB;
   uint8_t* st_s = v_s + KV_ST * VB;
   uint8_t* sd_s = st_s + ST_ST * STB;
-  uint8_t* ones = sd_s + ST_ST * STD;
+  uint4* xh_s = (uint4*)(sd_s + ST_ST * STD);
+  uint8_t* ones = (uint8_t*)(xh_s + 8 * 128);
   float* ell_s = (float*)(ones + 2048);       // [1024]
   float* cj = ell_s + 1024;                   // [2][128]
   uint64_t* bars = (uint64_t*)(cj + 256);
@@ -559,12 +598,12 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
       if (has_state) {
         const __half* srcm = st_main + (size_t)(s * g.n + (k - 1)) * ST_MAIN;
         const __half* srcd = st_den + (size_t)(s * g.n + (k - 1)) * ST_DEN;
-        for (int kb = 0; kb < NKB; ++kb) {
-          const int sb = kb % ST_ST;
-          if (kb >= ST_ST) mbar_wait(&st_empty[sb], ((kb / ST_ST) + 1) & 1);
+        for (int stp = 0; stp < NSTEP; ++stp) {
+          const int sb = stp % ST_ST;
+          if (stp >= ST_ST) mbar_wait(&st_empty[sb], ((stp / ST_ST) + 1) & 1);
           mbar_expect_tx(&st_full[sb], STB + (den ? STD : 0));
-          bulk_load(st_s + sb * STB, srcm + (size_t)kb * 64 * 64, STB, &st_full[sb]);
-          if (den) bulk_load(sd_s + sb * STD, srcd + (size_t)kb * 64 * 16, STD, &st_full[sb]);
+          bulk_load(st_s + sb * STB, srcm + (size_t)stp * 128 * 64, STB, &st_full[sb]);
+          if (den) bulk_load(sd_s + sb * STD, srcd + (size_t)stp * 128 * 16, STD, &st_full[sb]);
         }
       }
       for (int J = early; J <= I; ++J) kv(J);
@@ -578,18 +617,21 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
       const uint32_t id16k = idesc_bf16(128, 16, false, false);
       const uint32_t id128 = idesc_bf16(128, 128, false, false);
       if (has_state) {
-        for (int kb = 0; kb < NKB; ++kb) {
-          const int bb = kb % NA, sb = kb % ST_ST;
-          mbar_wait(&a_full[bb], (kb / NA) & 1);
-          mbar_wait(&st_full[sb], (kb / ST_ST) & 1);
+        const uint64_t sm0 = smem_desc(smem_u32(st_s), 8192, 1024, 2);
+        const uint64_t sd0 = smem_desc(smem_u32(sd_s), 2048, 256, 6);
+        for (int stp = 0; stp < NSTEP; ++stp) {
+          const int bb = stp % NA, sb = stp % ST_ST;
+          mbar_wait(&a_full[bb], (stp / NA) & 1);
+          mbar_wait(&st_full[sb], (stp / ST_ST) & 1);
           tc_fence_after();
-          const uint32_t sm = smem_u32(st_s + sb * STB), sdn = smem_u32(sd_s + sb * STD);
-          const uint32_t ab = a_base + (uint32_t)(bb * 32);
+          const uint64_t so = (uint64_t)((sb * STB) >> 4), sdo = (uint64_t)((sb * STD) >> 4);
+          const uint32_t ab = a_base + (uint32_t)(bb * 64);
+          const uint32_t first = stp > 0 ? 1u : 0u;
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const uint32_t f = (kb > 0 || kk > 0) ? 1u : 0u;
-            mma_ts(tm, ab + kk * 8, smem_desc(sm + kk * 2048, 8192, 1024, 2), id64mn_h, f);
-            if (den) mma_ts(tm + 64, ab + kk * 8, smem_desc(sdn + kk * 512, 2048, 256, 6), id16mn_h, f);
+          for (int kk = 0; kk < 8; ++kk) {   // 16 slots per MMA: 2048 B of [slot][64] rows, 512 B of [slot][16]
+            const uint32_t f = kk > 0 ? 1u : first;
+            mma_ts(tm, ab + kk * 8, sm0 + so + (uint64_t)(kk * 128), id64mn_h, f);
+            if (den) mma_ts(tm + 64, ab + kk * 8, sd0 + sdo + (uint64_t)(kk * 32), id16mn_h, f);
           }
           tc_commit(&a_empty[bb]);
           tc_commit(&st_empty[sb]);
@@ -638,9 +680,13 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
     if (has_state) {
       // phi'(q) from the exact bf16 q (one rounding per feature); the query
       // scale sigma^2 * gp_m (chunked.py:379-385) is applied to the fp32 row
-      uint32_t qp[32];
-      load_row_f16(qraw + rowid(g, s, tok) * HD, qp);
-      gen_all_kblocks<0, NA>(qp, a_base, lane_off, a_full, a_empty, l);
+      {
+        uint32_t qp[32];
+        load_row_f16(qraw + rowid(g, s, tok) * HD, qp);
+#pragma unroll
+        for (int c8 = 0; c8 < 8; ++c8) xh_s[c8 * 128 + row] = *(const uint4*)&qp[c8 * 4];
+      }
+      gen_steps(xh_s, row, a_base, lane_off, a_full, a_empty, l);
       mbar_wait(a_done, 0);
       tc_fence_after();
       const float cm = sig2 * __expf(li) / pow2_neg_bits(k - 1);   // undo the stored-state scale
