@@ -194,8 +194,13 @@ __global__ void __launch_bounds__(fm::THREADS, 1) k_tc_featmajor(const __grid_co
   const int grp = blockIdx.x, kin = blockIdx.y + (kBwd ? 1 : 0), s = blockIdx.z;
   const int slot = kBwd ? kin - 1 : kin;
   const int t0 = grp * 4, nt = min(4, NTH - t0);
-  const int nsub = g.c / 32, nstage = g.c / TOK;
   constexpr bool den = kDen != 0;   // compile-time: a predicated-off tcgen05.mma still costs an issue slot
+  // tokens per MMA/generation step: 64 (one barrier round trip per 16 MMAs) when the
+  // 4 accumulators are 64 columns wide; 32 when they carry the 16 score-sum columns
+  constexpr int SUB = den ? 32 : 64, SPS = TOK / SUB, NBk = den ? 3 : 2;
+  constexpr int ACC_W = den ? UW : 64;
+  constexpr uint32_t ABASE = den ? 320u : 256u;   // A buffers: NBk x 4 tiles x SUB/2 columns
+  const int nsub = g.c / SUB, nstage = g.c / TOK;
 
   if (w == 2) tmem_alloc<512>(&tmem_base);
   if (tid == 0) {
@@ -203,7 +208,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1) k_tc_featmajor(const __grid_co
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    for (int i = 0; i < NB; ++i) {
+    for (int i = 0; i < NBk; ++i) {
       mbar_init(&afull[i], GEN_WARPS);
       mbar_init(&aempty[i], 1);
     }
@@ -237,29 +242,27 @@ __global__ void __launch_bounds__(fm::THREADS, 1) k_tc_featmajor(const __grid_co
     if (l == 0) {
       const uint32_t id64 = idesc_f16(128, 64, false, true);
       const uint32_t id16 = idesc_f16(128, 16, false, true);
+      const uint64_t bn0 = smem_desc(smem_u32(b_s), 8192, 1024, 2);
+      const uint64_t b160 = smem_desc(smem_u32(b16_s), 512, 256, 6);
       for (int i = 0; i < nsub; ++i) {
-        const int j = i >> 1, h = i & 1, st = j % ST, buf = i % NB;
+        const int j = i / SPS, h = i % SPS, st = j % ST, buf = i % NBk;
         mbar_wait(&full[st], (j / ST) & 1);
-        mbar_wait(&afull[buf], (i / NB) & 1);
+        mbar_wait(&afull[buf], (i / NBk) & 1);
         tc_fence_after();
-        const uint32_t bsm = smem_u32(b_s + st * B_B);
-        const uint32_t b16 = smem_u32(b16_s + st * B16_B);
+        const uint32_t first = i > 0 ? 1u : 0u;
         for (int t = 0; t < nt; ++t) {
-          const uint32_t acc = tm + (uint32_t)(t * UW);
-          const uint32_t ab = tm + 320u + (uint32_t)((buf * 4 + t) * 16);
+          const uint32_t acc = tm + (uint32_t)(t * ACC_W);
+          const uint32_t ab = tm + ABASE + (uint32_t)((buf * 4 + t) * (SUB / 2));
 #pragma unroll
-          for (int kk = 0; kk < 2; ++kk) {
-            const uint32_t f = (i > 0 || kk > 0) ? 1u : 0u;
-            const int trow = h * 32 + kk * 16;  // token row inside the 64-token stage
-            mma_ts(acc, ab + kk * 8, smem_desc(bsm + trow * 128, 8192, 1024, 2), id64, f);
-            if (den) {
-              const uint64_t dd = smem_desc(b16 + trow * 32, 512, 256, 6);
-              mma_ts(acc + 64, ab + kk * 8, dd, id16, f);
-            }
+          for (int kk = 0; kk < SUB / 16; ++kk) {
+            const uint32_t f = kk > 0 ? 1u : first;
+            const int trow = h * SUB + kk * 16;   // token row inside the 64-token stage
+            mma_ts(acc, ab + kk * 8, bn0 + (uint64_t)((st * B_B + trow * 128) >> 4), id64, f);
+            if (den) mma_ts(acc + 64, ab + kk * 8, b160 + (uint64_t)((st * B16_B + trow * 32) >> 4), id16, f);
           }
         }
         tc_commit(&aempty[buf]);
-        if (h == 1) tc_commit(&empty[st]);
+        if (h == SPS - 1) tc_commit(&empty[st]);
       }
       tc_commit(fin);
     }
@@ -278,26 +281,25 @@ __global__ void __launch_bounds__(fm::THREADS, 1) k_tc_featmajor(const __grid_co
     }
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     for (int i = 0; i < nsub; ++i) {
-      const int j = i >> 1, h = i & 1, st = j % ST, buf = i % NB;
+      const int j = i / SPS, h = i % SPS, st = j % ST, buf = i % NBk;
       mbar_wait(&full[st], (j / ST) & 1);
-      if (i >= NB) mbar_wait(&aempty[buf], ((i / NB) + 1) & 1);
+      if (i >= NBk) mbar_wait(&aempty[buf], ((i / NBk) + 1) & 1);
       const uint8_t* xs = xt_s + st * XT_B;
-      uint32_t va[2][16], vb[2][16];
-#pragma unroll
-      for (int u = 0; u < 2; ++u)
-#pragma unroll
-        for (int c4 = 0; c4 < 4; ++c4) {
-          const int ch = h * 4 + c4;
-          *(uint4*)&va[u][c4 * 4] = *(const uint4*)(xs + sw128_off(ra[u], ch));
-          *(uint4*)&vb[u][c4 * 4] = *(const uint4*)(xs + sw128_off(rb[u], ch));
-        }
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         if (act[u]) {
-          uint32_t o[16];
+          uint32_t va[SUB / 2], vb[SUB / 2], o[SUB / 2];
 #pragma unroll
-          for (int c = 0; c < 16; ++c) o[c] = hmul2_f16(va[u][c], vb[u][c]);
-          tmem_st16(tm + 320u + (uint32_t)((buf * 4 + tp * 2 + u) * 16) + lane_off, o);
+          for (int c4 = 0; c4 < SUB / 8; ++c4) {
+            const int ch = h * (SUB / 8) + c4;   // 16-byte chunk (8 tokens) of the 128-byte row
+            *(uint4*)&va[c4 * 4] = *(const uint4*)(xs + sw128_off(ra[u], ch));
+            *(uint4*)&vb[c4 * 4] = *(const uint4*)(xs + sw128_off(rb[u], ch));
+          }
+#pragma unroll
+          for (int c = 0; c < SUB / 2; ++c) o[c] = hmul2_f16(va[c], vb[c]);
+          const uint32_t ad = tm + ABASE + (uint32_t)((buf * 4 + tp * 2 + u) * (SUB / 2)) + lane_off;
+#pragma unroll
+          for (int c16 = 0; c16 < SUB / 2; c16 += 16) tmem_st16(ad + c16, o + c16);
         }
       }
       tc_wait_st();
@@ -316,7 +318,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1) k_tc_featmajor(const __grid_co
       float* dst = out + (((size_t)(s * g.n + slot) * FH) + (size_t)(t0 + t) * 128 + q * 32 + l) * UW;
       for (int c0 = 0; c0 < ncols; c0 += 16) {
         uint32_t r[16];
-        tmem_ld16(tm + (uint32_t)(t * UW) + lane_off + c0, r);
+        tmem_ld16(tm + (uint32_t)(t * ACC_W) + lane_off + c0, r);
         tc_wait_ld();
 #pragma unroll
         for (int c = 0; c < 16; c += 4)
