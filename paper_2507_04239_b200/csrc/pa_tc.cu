@@ -72,30 +72,30 @@ __global__ void __launch_bounds__(128) k_tc_prep_gates(Geo g, const float* __res
   if (lane == 0) lamlog[wid] = carry;
 }
 
-// X~^T [((s*n + k)*64 + dim)][tok] = x_j * exp(mode) for 64-token blocks;
-// mode 0: exp((lend - ell_j)/2) (keys, suffix decay); 1: scale*exp(ell_j/2) (queries, prefix); 2: 1 (exact copy)
-__global__ void __launch_bounds__(256) k_tc_prep_xt(Geo g, const __nv_bfloat16* __restrict__ x,
-                                                    const float* __restrict__ ell,
-                                                    const float* __restrict__ lamlog, int mode,
-                                                    __half* xt) {
-  __shared__ float tile[64][65];
+// X^T [((s*n + k)*64 + dim)][tok] (fp16, exact copy of the bf16 input) for the
+// feature-major GEMMs, 64-token x 64-dim tiles: 16-byte loads of token rows,
+// transpose through shared memory, 16-byte stores of dim rows.
+__global__ void __launch_bounds__(256) k_tc_prep_xt(Geo g, const __nv_bfloat16* __restrict__ x, __half* xt) {
+  constexpr int P = 72;                       // row pitch in halves (144 B: 16-byte aligned, spreads banks)
+  __shared__ __align__(16) __half tile[64 * P];
   const int tb = blockIdx.x, k = blockIdx.y, s = blockIdx.z;
   const int j0 = k * g.c + tb * 64;
-  // load 64 tokens x 64 dims (coalesced rows), scale per token
-  for (int i = threadIdx.x; i < 64 * 64; i += 256) {
-    const int r = i >> 6, dcol = i & 63;
-    const int j = j0 + r;
-    const float lj = ell[(size_t)s * g.t + j];
-    const float f = mode == 2 ? 1.f
-                    : mode == 0 ? __expf(0.5f * (lamlog[s * g.n + k] - lj))
-                                : g.scale * __expf(0.5f * lj);
-    tile[r][dcol] = __bfloat162float(x[rowid(g, s, j) * HD + dcol]) * f;
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const int i = threadIdx.x + it * 256;     // 512 = 64 tokens x 8 chunks of 8 dims
+    const int r = i >> 3, c8 = i & 7;
+    const uint4 v4 = *(const uint4*)(x + rowid(g, s, j0 + r) * HD + c8 * 8);
+    const __nv_bfloat16* e = (const __nv_bfloat16*)&v4;
+#pragma unroll
+    for (int z = 0; z < 8; ++z) tile[(c8 * 8 + z) * P + r] = __float2half_rn(__bfloat162float(e[z]));
   }
   __syncthreads();
   __half* dst = xt + ((size_t)(s * g.n + k) * HD) * g.c + tb * 64;
-  for (int i = threadIdx.x; i < 64 * 64; i += 256) {
-    const int dim = i >> 6, r = i & 63;
-    dst[(size_t)dim * g.c + r] = __float2half_rn(tile[r][dim]);
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const int i = threadIdx.x + it * 256;     // 64 dims x 8 chunks of 8 tokens
+    const int dim = i >> 3, c8 = i & 7;
+    *(uint4*)(dst + (size_t)dim * g.c + c8 * 8) = *(const uint4*)&tile[dim * P + c8 * 8];
   }
 }
 
@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(256) k_tc_prep_xt(Geo g, const __nv_bfloat16* 
 // per-token decay/scale rides on the other operand:
 //   mode 0 (forward):  rows = W_m v_m,        aux = (W_m, 0...)      W_m = exp(lend - ell_m)
 //   mode 1 (backward): rows = c_m dnum_m,     aux = (c_m dden_m, 0...)  c_m = sigma^2 exp(ell_m)
+//   mode 3: as mode 1 with dnum = dy read in the [b, t, h, 64] layout (no normalization)
 // rows [ns*t][64] bf16, aux [ns*t][16] bf16 (may be null).
 __global__ void __launch_bounds__(256) k_tc_prep_rows(Geo g, int mode, const __nv_bfloat16* __restrict__ src,
                                                       const float* __restrict__ ell,
@@ -123,7 +124,7 @@ __global__ void __launch_bounds__(256) k_tc_prep_rows(Geo g, int mode, const __n
   } else {
     f = g.scale * g.scale * __expf(lm);
     a = dden ? f * dden[it] : 0.f;
-    row = src + it * HD;
+    row = src + (mode == 3 ? rowid(g, s, m) : it) * HD;
   }
   const uint4* in = (const uint4*)row;
   uint4* out = (uint4*)(rows + it * HD);
@@ -1508,7 +1509,6 @@ struct TcBwdWs {
   __nv_bfloat16* dN;     // dnum (bf16, intra-chunk GEMMs)
   __half* dN16;          // dnum (fp16, state GEMMs)
   __half* dD;            // (dden, 0..) fp16
-  __half* v16;           // v rows fp16 [ns*t][64]
   float* dden;
   __half* dsm;
   __half* dsd;
@@ -1556,7 +1556,6 @@ static TcBwdWs carve_bwd(const Geo& g, void* base, size_t* bytes) {
   b.dN = (__nv_bfloat16*)take(2ull * g.ns * g.t * HD);
   b.dN16 = (__half*)take(2ull * g.ns * g.t * HD);
   b.dD = (__half*)take(2ull * g.ns * g.t * 16);
-  b.v16 = (__half*)take(2ull * g.ns * g.t * HD);
   b.dden = (float*)take(4ull * g.ns * g.t);
   b.dsm = (__half*)take(2ull * g.ns * g.n * ST_MAIN);
   b.dsd = (__half*)take(2ull * g.ns * g.n * ST_DEN);
@@ -1668,7 +1667,7 @@ int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const 
   {
     StageTimer tmr("fwd_prep", st);
     k_tc_prep_gates<<<(g.ns * g.n + 3) / 4, 128, 0, st>>>(g, log_g, w.ell, w.lamlog);
-    k_tc_prep_xt<<<dim3(g.c / 64, g.n, g.ns), 256, 0, st>>>(g, (const __nv_bfloat16*)k, w.ell, w.lamlog, 2, w.kt);
+    k_tc_prep_xt<<<dim3(g.c / 64, g.n, g.ns), 256, 0, st>>>(g, (const __nv_bfloat16*)k, w.kt);
     k_tc_prep_rows<<<(unsigned)(((size_t)g.ns * g.t + 255) / 256), 256, 0, st>>>(
         g, 0, (const __nv_bfloat16*)v, w.ell, w.lamlog, nullptr, w.vr, with_den ? w.wa : nullptr);
   }
@@ -1712,26 +1711,23 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
       !map_bth(&m_v128, v, g, 128)) {
     return 3;
   }
-  CUtensorMap m_dn128, m_dd128, m_dn16, m_v16;
-  if (!map_2d(&m_dn128, b.dN, (size_t)g.ns * g.t, HD, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !map_2d(&m_dn16, b.dN16, (size_t)g.ns * g.t, HD, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !map_2d(&m_v16, b.v16, (size_t)g.ns * g.t, HD, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !map_2d(&m_dd128, b.dD, (size_t)g.ns * g.t, 16, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B)) {
-    return 3;
-  }
+  CUtensorMap m_dn128;
+  if (!map_2d(&m_dn128, b.dN, (size_t)g.ns * g.t, HD, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)) return 3;
   m_dummy = m_dn;
   {
     StageTimer tmr("bwd_prep", st);
     cudaMemsetAsync(b.dell, 0, 4ull * g.ns * g.t, st);
     cudaMemsetAsync(b.cu, 0, 4ull * g.ns * g.t, st);
     cudaMemsetAsync(b.dlam, 0, 4ull * g.ns * g.n * scan_blocks(uc), st);
-    k_tc_bwd_prep<<<(unsigned)(((size_t)g.ns * g.t + 255) / 256), 256, 0, st>>>(
-        g, (const __nv_bfloat16*)dy, w.y32, rowsum, b.dN, b.dN16, den ? b.dD : nullptr, b.dden);
+    // without normalization dnum = dy: the kernels read dy in place (TMA / row loads
+    // with bf16 -> fp16 conversion), so only the normalized path materialises rows
+    if (den)
+      k_tc_bwd_prep<<<(unsigned)(((size_t)g.ns * g.t + 255) / 256), 256, 0, st>>>(
+          g, (const __nv_bfloat16*)dy, w.y32, rowsum, b.dN, b.dN16, b.dD, b.dden);
+    k_tc_prep_xt<<<dim3(g.c / 64, g.n, g.ns), 256, 0, st>>>(g, (const __nv_bfloat16*)q, w.kt);
     k_tc_prep_rows<<<(unsigned)(((size_t)g.ns * g.t + 255) / 256), 256, 0, st>>>(
-        g, 2, (const __nv_bfloat16*)v, w.ell, w.lamlog, nullptr, b.v16, nullptr);
-    k_tc_prep_xt<<<dim3(g.c / 64, g.n, g.ns), 256, 0, st>>>(g, (const __nv_bfloat16*)q, w.ell, w.lamlog, 2, w.kt);
-    k_tc_prep_rows<<<(unsigned)(((size_t)g.ns * g.t + 255) / 256), 256, 0, st>>>(
-        g, 1, b.dN, w.ell, w.lamlog, den ? b.dden : nullptr, w.vr, den ? w.wa : nullptr);
+        g, den ? 1 : 3, den ? b.dN : (const __nv_bfloat16*)dy, w.ell, w.lamlog, den ? b.dden : nullptr, w.vr,
+        den ? w.wa : nullptr);
   }
   if (g.n > 1) {
     StageTimer tmr("bwd_query_state_dA", st);
@@ -1753,16 +1749,19 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
     if (!map_bth(&m_q128, q, g, 128) || !map_bth(&m_k128, k, g, 128)) {
       return 3;
     }
-    tc_intra_bwd(g, m_q128, m_k128, m_v128, m_dn128, w.ell, b.dden, b.dk32, b.dv32, b.dq32, b.dell, st);
+    CUtensorMap m_dy128;
+    if (!den && !map_bth(&m_dy128, dy, g, 128)) return 3;
+    tc_intra_bwd(g, m_q128, m_k128, m_v128, den ? m_dn128 : m_dy128, w.ell, b.dden, b.dk32, b.dv32, b.dq32, b.dell,
+                 st);
   }
   {
     StageTimer tmr("bwd_query_state_dq", st);
-    tc_dphi(g, false, b.dN16, b.dD, q, w.ell, w.lamlog, w.stm, w.std_, b.dq32, nullptr, b.dell, nullptr, dq,
+    tc_dphi(g, false, den ? (const void*)b.dN16 : dy, den ? 0 : 1, b.dD, q, w.ell, w.lamlog, w.stm, w.std_, b.dq32, nullptr, b.dell, nullptr, dq,
             nullptr, st);
   }
   {
     StageTimer tmr("bwd_update_state", st);
-    tc_dphi(g, true, b.v16, nullptr, k, w.ell, w.lamlog, b.dsm, b.dsd, b.dk32, b.dv32, b.dell, b.cu, dk, dv, st);
+    tc_dphi(g, true, v, 1, nullptr, k, w.ell, w.lamlog, b.dsm, b.dsd, b.dk32, b.dv32, b.dell, b.cu, dk, dv, st);
   }
   {
     StageTimer tmr("bwd_finish", st);

@@ -66,6 +66,20 @@ constexpr uint32_t TA = 320, TA16 = 352;
 constexpr int W_TMEM = 8, W_TMA = 9, W_MMA = 10;   // MMA issuers: w10, w11
 }  // namespace dp2
 
+__device__ __forceinline__ void load_row_f16_any(const __nv_bfloat16* src, uint32_t (&xp)[32]) {
+  const uint4* row = (const uint4*)src;
+#pragma unroll
+  for (int c8 = 0; c8 < 8; ++c8) {
+    const uint4 v4 = row[c8];
+    const uint32_t* pv = (const uint32_t*)&v4;
+#pragma unroll
+    for (int e2 = 0; e2 < 4; ++e2) {
+      const float2 f2 = __bfloat1622float2(*(const __nv_bfloat162*)&pv[e2]);
+      xp[c8 * 4 + e2] = pack_f16(f2.x, f2.y);
+    }
+  }
+}
+
 struct ff2 {
   float x, y;
 };
@@ -79,7 +93,7 @@ __device__ __forceinline__ ff2 ffma2(ff2 a, ff2 b, ff2 c) {
 
 template <bool kUpd, int kDen>
 __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
-    const __half* __restrict__ a_rows, const __half* __restrict__ a16_rows, Geo g,
+    const void* __restrict__ a_rows, int a_bf16_bth, const __half* __restrict__ a16_rows, Geo g,
     const __nv_bfloat16* __restrict__ xraw, const float* __restrict__ ell, const float* __restrict__ lamlog,
     const __half* __restrict__ b_main, const __half* __restrict__ b_den, const float* __restrict__ dx32,
     const float* __restrict__ dv32, float* dell, float* dellend, __nv_bfloat16* dxo, __nv_bfloat16* dvo) {
@@ -238,9 +252,14 @@ __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
       // the A operand of the dphi GEMM goes to TMEM (one row per lane): the MMA then
       // reads only the state tile from shared memory
       uint32_t ar[32];
-      const uint4* src = (const uint4*)(a_rows + ((size_t)s * g.t + tok) * HD);
+      if (a_bf16_bth) {
+        // bf16 rows in the reference layout, converted to fp16 pairs (exact for |x| < 65504)
+        load_row_f16_any((const __nv_bfloat16*)a_rows + rowid(g, s, tok) * HD, ar);
+      } else {
+        const uint4* src = (const uint4*)((const __half*)a_rows + ((size_t)s * g.t + tok) * HD);
 #pragma unroll
-      for (int c8 = 0; c8 < 8; ++c8) *(uint4*)&ar[c8 * 4] = src[c8];
+        for (int c8 = 0; c8 < 8; ++c8) *(uint4*)&ar[c8 * 4] = src[c8];
+      }
       tmem_st16(tm + TA + lane_off, ar);
       tmem_st16(tm + TA + 16 + lane_off, ar + 16);
       if (kUpd) {
@@ -432,7 +451,7 @@ __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
   if (w == W_TMEM) tmem_dealloc<512>(tm);
 }
 
-int tc_dphi(const Geo& g, bool upd, const __half* a_rows, const __half* a16_rows, const void* xraw,
+int tc_dphi(const Geo& g, bool upd, const void* a_rows, int a_bf16_bth, const __half* a16_rows, const void* xraw,
             const float* ell, const float* lamlog, const __half* b_main, const __half* b_den, const float* dx32,
             const float* dv32, float* dell, float* dellend, void* dxo, void* dvo, cudaStream_t st) {
   using namespace dp2;
@@ -440,7 +459,7 @@ int tc_dphi(const Geo& g, bool upd, const __half* a_rows, const __half* a16_rows
   auto fn = upd ? (den ? k_tc_dphi2<true, 1> : k_tc_dphi2<true, 0>)
                 : (den ? k_tc_dphi2<false, 1> : k_tc_dphi2<false, 0>);
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-  fn<<<dim3(g.c / 128, g.n, g.ns), THREADS, SMEM, st>>>(a_rows, a16_rows, g, (const __nv_bfloat16*)xraw, ell, lamlog,
+  fn<<<dim3(g.c / 128, g.n, g.ns), THREADS, SMEM, st>>>(a_rows, a_bf16_bth, a16_rows, g, (const __nv_bfloat16*)xraw, ell, lamlog,
                                                          b_main, b_den, dx32, dv32, dell, dellend,
                                                          (__nv_bfloat16*)dxo, (__nv_bfloat16*)dvo);
   return 0;

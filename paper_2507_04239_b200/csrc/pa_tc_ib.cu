@@ -156,6 +156,13 @@ __global__ void __launch_bounds__(ib2::THREADS, 2) k_tc_ib(const __grid_constant
   const uint32_t tS = tm, tDP = tm + 64, tA = tm + 128, tB = tm + 192;
 
   if (w == W_TMA) {
+    // dnum rows: stream-major [ns*t][64] when normalizing, else dy itself ([b, t, h, 64])
+    auto load_dn = [&](void* dst, uint64_t* bar, int blk) {
+      if (kNorm)
+        tma_load_2d(dst, &tm_dn, bar, 0, s * g.t + c0 + blk * 128);
+      else
+        tma_load_4d(dst, &tm_dn, bar, 0, hi, c0 + blk * 128, bi);
+    };
     if (l == 0) {
       tma_prefetch(&tm_q);
       tma_prefetch(&tm_k);
@@ -167,7 +174,7 @@ __global__ void __launch_bounds__(ib2::THREADS, 2) k_tc_ib(const __grid_constant
         tma_load_4d(f1, &tm_v, f_full, 0, hi, c0 + B0 * 128, bi);
       } else {
         tma_load_4d(f0, &tm_q, f_full, 0, hi, c0 + B0 * 128, bi);
-        tma_load_2d(f1, &tm_dn, f_full, 0, s * g.t + c0 + B0 * 128);
+        load_dn(f1, f_full, B0);
       }
       for (int it = 0; it < nblk; ++it) {
         const int X = kKV ? B0 + it : it, st = it % NST;
@@ -176,7 +183,7 @@ __global__ void __launch_bounds__(ib2::THREADS, 2) k_tc_ib(const __grid_constant
         uint8_t* d0 = s0 + st * 2 * T128;
         if (kKV) {
           tma_load_4d(d0, &tm_q, &t_full[st], 0, hi, c0 + X * 128, bi);
-          tma_load_2d(d0 + T128, &tm_dn, &t_full[st], 0, s * g.t + c0 + X * 128);
+          load_dn(d0 + T128, &t_full[st], X);
         } else {
           tma_load_4d(d0, &tm_k, &t_full[st], 0, hi, c0 + X * 128, bi);
           tma_load_4d(d0 + T128, &tm_v, &t_full[st], 0, hi, c0 + X * 128, bi);
