@@ -52,7 +52,8 @@ constexpr int NST = 4;
 constexpr int NT = FH / 128;     // 18 slot tiles
 constexpr int XS = 16 * 128 * 16;   // fp32 x or dx: [16 float4][128 threads]
 constexpr int XH = 8 * 128 * 16;    // fp16 x: [8 uint4][128 threads]
-constexpr int SMEM = 1024 + NST * (BM + BD) + 3 * XS + XH + 256;
+constexpr int AS = 128 * 128, AS16 = 128 * 32;   // query side: A rows staged in shared memory
+constexpr int SMEM = 1024 + NST * (BM + BD) + 3 * XS + XH + AS + AS16 + 256;
 // w0..w7 compute (two groups of four: group g owns the slot tiles nt = g mod 2,
 // i.e. TMEM buffer g, and its own dx copy), w8 TMEM, w9 TMA, w10/w11 MMA
 // (issuer m owns the tiles nt = m mod 2: each barrier wait costs ~160 cycles
@@ -60,8 +61,8 @@ constexpr int SMEM = 1024 + NST * (BM + BD) + 3 * XS + XH + 256;
 // commit latencies).  The issuing warps take the highest ids (the scheduler
 // prefers high warp ids).
 constexpr int THREADS = 384;
-// TMEM columns: dphi buffers [0, 256), dv accumulator [256, 320), A [320, 352),
-// score-sum A [352, 360), generated phi'(k) buffers [384, 512)
+// TMEM columns (update side): dphi buffers [0, 256), dv accumulator [256, 320), A [320, 352),
+// score-sum A [352, 360), generated phi'(k) buffers [384, 512); query side: 4 dphi buffers [0, 512)
 constexpr uint32_t TA = 320, TA16 = 352;
 constexpr int W_TMEM = 8, W_TMA = 9, W_MMA = 10;   // MMA issuers: w10, w11
 }  // namespace dp2
@@ -105,13 +106,19 @@ __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
   float4* x_s = (float4*)(bd_s + NST * BD);
   float4* dx_all = x_s + 16 * 128;          // [2 groups][16][128]
   uint4* xh_s = (uint4*)(dx_all + 2 * 16 * 128);
-  uint64_t* bars = (uint64_t*)(xh_s + 8 * 128);
+  uint8_t* as_s = (uint8_t*)(xh_s + 8 * 128);   // [128 tok][64] fp16 SW128 (query side)
+  uint8_t* as16_s = as_s + AS;                    // [128 tok][16] fp16 SW32 (query side, normalize)
+  uint64_t* bars = (uint64_t*)(as16_s + AS16);
   uint64_t* a_ready = bars;          // A operand in TMEM: 4 compute-warp arrivals
   uint64_t* b_full = a_ready + 1;    // NST
   uint64_t* b_empty = b_full + NST;  // NST
-  uint64_t* d_full = b_empty + NST;  // 2
-  uint64_t* d_empty = d_full + 2;    // 2
-  uint64_t* g_full = d_empty + 2;    // 2
+  // dphi TMEM buffers: update side 2 (TMEM also holds dv, phi'(k) and A), query
+  // side 4 (A in shared memory): each compute group then owns two buffers, so
+  // the MMA of its next tile overlaps its expand-VJP of the current one
+  constexpr int NDB = kUpd ? 2 : 4;
+  uint64_t* d_full = b_empty + NST;  // 4
+  uint64_t* d_empty = d_full + 4;    // 4
+  uint64_t* g_full = d_empty + 4;    // 2
   uint64_t* g_empty = g_full + 2;    // 2
   uint64_t* fin = g_empty + 2;
   __shared__ uint32_t tmem_base;
@@ -142,9 +149,11 @@ __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
       mbar_init(&b_full[i], 1);
       mbar_init(&b_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 4; ++i) {
       mbar_init(&d_full[i], 1);
       mbar_init(&d_empty[i], 4);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&g_full[i], 4);
       mbar_init(&g_empty[i], 1);
     }
@@ -178,35 +187,44 @@ __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
       const uint64_t bk0 = smem_desc(smem_u32(bm_s), 16, 1024, 2);      // K-major view of a state stage
       const uint64_t bn0 = smem_desc(smem_u32(bm_s), 8192, 1024, 2);    // MN-major view of the same stage
       const uint64_t bd0 = smem_desc(smem_u32(bd_s), 16, 256, 6);
+      const uint64_t ak0 = smem_desc(smem_u32(as_s), 16, 1024, 2);
+      const uint64_t a160 = smem_desc(smem_u32(as16_s), 16, 256, 6);
 #ifdef PA_TRACE
       const bool trm = kUpd && blockIdx.x == 0 && blockIdx.y == 5 && blockIdx.z == 3 && mw == 0;
 #endif
       PA_TR3(trm, 99);
       for (int nt = mw; nt < NT; nt += 2) {
-        const int st = nt % NST, db = nt & 1;
+        const int st = nt % NST, db = nt % NDB;
         mbar_wait(&b_full[st], (nt / NST) & 1);
         PA_TR3(trm, nt * 4 + 0);
-        if (nt >= 2) mbar_wait(&d_empty[db], ((nt >> 1) + 1) & 1);
+        if (nt >= NDB) mbar_wait(&d_empty[db], ((nt / NDB) + 1) & 1);
         PA_TR3(trm, nt * 4 + 1);
         tc_fence_after();
         const uint64_t so = (uint64_t)((st * BM) >> 4);
         const uint32_t dt = tm + (uint32_t)(db * 128);
+        if (kUpd) {
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          mma_ts(dt, tm + TA + (uint32_t)(kk * 8), bk0 + so + (uint64_t)(kk * 2), id128, kk > 0 ? 1u : 0u);
-        if (den) mma_ts(dt, tm + TA16, bd0 + (uint64_t)((st * BD) >> 4), id128, 1u);
+          for (int kk = 0; kk < 4; ++kk)
+            mma_ts(dt, tm + TA + (uint32_t)(kk * 8), bk0 + so + (uint64_t)(kk * 2), id128, kk > 0 ? 1u : 0u);
+          if (den) mma_ts(dt, tm + TA16, bd0 + (uint64_t)((st * BD) >> 4), id128, 1u);
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_ss(dt, ak0 + (uint64_t)(kk * 2), bk0 + so + (uint64_t)(kk * 2), id128, kk > 0 ? 1u : 0u);
+          if (den) mma_ss(dt, a160, bd0 + (uint64_t)((st * BD) >> 4), id128, 1u);
+        }
         tc_commit(&d_full[db]);
         PA_TR3(trm, 400 + nt);
         if (kUpd) {
           // dv += phi'(k) [128 tok x 128 slots] * dS~ tile [128 slots x 64] (same stage, MN-major)
-          mbar_wait(&g_full[db], (nt >> 1) & 1);
+          mbar_wait(&g_full[nt & 1], (nt >> 1) & 1);
           PA_TR3(trm, nt * 4 + 2);
           tc_fence_after();
-          const uint32_t ab = tm + 384u + (uint32_t)(db * 64);
+          const uint32_t ab = tm + 384u + (uint32_t)((nt & 1) * 64);
           // both issuers accumulate into the zero-initialised dv columns
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) mma_ts(tm + 256u, ab + kk * 8, bn0 + so + (uint64_t)(kk * 128), id64mn, 1u);
-          tc_commit(&g_empty[db]);
+          tc_commit(&g_empty[nt & 1]);
         }
         tc_commit(&b_empty[st]);
         PA_TR3(trm, nt * 4 + 3);
@@ -260,14 +278,18 @@ __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
 #pragma unroll
         for (int c8 = 0; c8 < 8; ++c8) *(uint4*)&ar[c8 * 4] = src[c8];
       }
-      tmem_st16(tm + TA + lane_off, ar);
-      tmem_st16(tm + TA + 16 + lane_off, ar + 16);
       if (kUpd) {
+        tmem_st16(tm + TA + lane_off, ar);
+        tmem_st16(tm + TA + 16 + lane_off, ar + 16);
         uint32_t z[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) z[i] = 0u;
 #pragma unroll
         for (int c = 0; c < 64; c += 16) tmem_st16(tm + 256u + lane_off + c, z);   // dv accumulator
+      } else {
+        // K-major SW128 row of the shared-memory A tile
+#pragma unroll
+        for (int c8 = 0; c8 < 8; ++c8) *(uint4*)(as_s + sw128_off(row, c8)) = *(const uint4*)&ar[c8 * 4];
       }
       if (den) {
         uint32_t a16[8];
@@ -276,13 +298,16 @@ __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
           a16[0] = pack_f16(1.f, 0.f);
 #pragma unroll
           for (int i = 1; i < 8; ++i) a16[i] = 0u;
+          tmem_st8(tm + TA16 + lane_off, a16);
         } else {
           const uint4* s16 = (const uint4*)(a16_rows + ((size_t)s * g.t + tok) * 16);
-          *(uint4*)&a16[0] = s16[0];
-          *(uint4*)&a16[4] = s16[1];
+          // SW32 row: 16-byte chunk c at ((c ^ ((row >> 2) & 1)) << 4)
+          const uint32_t xr = ((uint32_t)row >> 2) & 1u;
+          *(uint4*)(as16_s + row * 32 + ((0u ^ xr) << 4)) = s16[0];
+          *(uint4*)(as16_s + row * 32 + ((1u ^ xr) << 4)) = s16[1];
         }
-        tmem_st8(tm + TA16 + lane_off, a16);
       }
+      if (!kUpd) fence_async_smem();
       tc_wait_st();
       tc_fence_before();
     }
@@ -341,9 +366,9 @@ __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
     };
     for (int nt = grp; nt < NT; nt += 2) {
       PA_TR3(trc, 100 + nt * 4 + 0);
-      const int db = nt & 1;
+      const int db = nt % NDB;
       PA_TR3(trc, 100 + nt * 4 + 1);
-      mbar_wait(&d_full[db], (nt >> 1) & 1);
+      mbar_wait(&d_full[db], (nt / NDB) & 1);
       PA_TR3(trc, 100 + nt * 4 + 2);
       tc_fence_after();
       const uint32_t dt = tm + (uint32_t)(db * 128) + lane_off;
