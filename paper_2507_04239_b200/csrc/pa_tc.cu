@@ -34,17 +34,6 @@ using namespace tc;
 
 __constant__ BlkTab c_blk = make_blk_tab();
 
-#ifdef PA_TRACE
-// debug build only (tools/trace_dphi.py): clock64 stamps of one dphi CTA
-__device__ long long g_trace2[512];
-extern "C" int pa_debug_trace2(long long* host, int n) {
-  return (int)cudaMemcpyFromSymbol(host, g_trace2, sizeof(long long) * n);
-}
-#define PA_TR2(c, i) \
-  if (c) g_trace2[(i)] = clock64()
-#else
-#define PA_TR2(c, i)
-#endif
 
 // ==========================================================================
 // prep kernels
@@ -418,26 +407,6 @@ constexpr int NA = 2;                   // TMEM A buffers (128 slots = 64 column
 constexpr int XH = 8 * 128 * 16;        // fp16 q rows, thread-private uint4 columns
 constexpr int SMEM = 1024 + QB + KV_ST * (KB + VB) + ST_ST * (STB + STD) + XH + 2048 + 4096 + 1024 + 512;
 }  // namespace outk
-
-// compute warps: phi'(x) for the 36 K blocks of one token row, each written to
-// a TMEM A buffer and handed to the MMA warp.
-template <int KB, int NA>
-__device__ __forceinline__ void gen_all_kblocks(const uint32_t (&xp)[32], uint32_t a_base, uint32_t lane_off,
-                                                uint64_t* a_full, uint64_t* a_empty, int l) {
-  constexpr int bb = KB % NA;
-  if (KB >= NA) mbar_wait(&a_empty[bb], ((KB / NA) + 1) & 1);
-  uint32_t o[32];
-  gen_fblock<2 * KB>(xp, o);
-  gen_fblock<2 * KB + 1>(xp, o + 16);
-  const uint32_t ast = a_base + (uint32_t)(bb * 32) + lane_off;
-  tmem_st16(ast, o);
-  tmem_st16(ast + 16, o + 16);
-  tc_wait_st();
-  tc_fence_before();
-  __syncwarp();
-  if (l == 0) mbar_arrive(&a_full[bb]);
-  if constexpr (KB + 1 < NKB) gen_all_kblocks<KB + 1, NA>(xp, a_base, lane_off, a_full, a_empty, l);
-}
 
 // phi'(x) for the 2304 slots in 18 steps of 128 slots (4 feature blocks, 64
 // TMEM columns), alternating over 2 TMEM A buffers.  x is this thread's row as
@@ -930,525 +899,6 @@ __global__ void __launch_bounds__(256) k_tc_scan_bwd(Geo g, int ucols, const flo
     for (int i = 0; i < 8; ++i) t += red[k * 8 + i];
     dlam_part[((size_t)s * g.n + k) * gridDim.x + blockIdx.x] = t;
   }
-}
-
-// --------------------------------------------------------------------------
-// token-major dphi GEMM + fused expand_vjp (gradients.py:46-76):
-//   query  (gradients.py:406-431): dphi'(q~) = [dnum|dden] A'^T_{k-1}
-//          -> dq += sigma e^{ell/2} dq~,  dell += dq~.q~ / 2
-//   update (gradients.py:191-213): dphi'(k~) = [v|1] dS~_k^T
-//          -> dk += e^{(lend-ell)/2} dk~, dell -= dk~.k~/2, dell_end += dk~.k~/2;
-//          then dv = phi'(k~) dS~_k (second GEMM, A generated into TMEM)
-// Warp roles as above.  TMEM: dphi buffers [0,256), dU [256,320), A [384,512).
-// grid (token tile of 128, chunk, stream)
-// --------------------------------------------------------------------------
-namespace dp {
-constexpr int AB = 128 * 128;    // A main tile (128 tok x 64)
-constexpr int A16 = 128 * 32;    // A score-sum tile (128 tok x 16)
-constexpr int BM = 128 * 128;    // B stage: 128 slots x 64
-constexpr int BD = 128 * 32;     // B stage score-sum part
-constexpr int NST = 4;
-constexpr int NA = 4;
-constexpr int NT = FH / 128;     // 18 dphi tiles
-constexpr int SMEM = 1024 + AB + A16 + NST * (BM + BD) + 256;
-}  // namespace dp
-
-template <int NTI>
-__device__ __forceinline__ void dphi_tiles(const float (&x)[64], float (&dx)[64], uint32_t dbase, uint32_t lane_off,
-                                           uint64_t* d_full, uint64_t* d_empty, int l, bool tr) {
-  constexpr int db = NTI & 1;
-  PA_TR2(tr, 100 + NTI * 4 + 0);
-  mbar_wait(&d_full[db], (NTI >> 1) & 1);
-  PA_TR2(tr, 100 + NTI * 4 + 1);
-  tc_fence_after();
-#pragma unroll
-  for (int ch = 0; ch < 4; ++ch) {
-    uint32_t r[32];
-    tmem_ld32(dbase + (uint32_t)(db * 128) + lane_off + ch * 32, r);
-    tc_wait_ld();
-    if (ch == 0) evjp_fblock<NTI * 4 + 0>(x, dx, r);
-    if (ch == 1) evjp_fblock<NTI * 4 + 1>(x, dx, r);
-    if (ch == 2) evjp_fblock<NTI * 4 + 2>(x, dx, r);
-    if (ch == 3) evjp_fblock<NTI * 4 + 3>(x, dx, r);
-  }
-  PA_TR2(tr, 100 + NTI * 4 + 2);
-  tc_fence_before();
-  __syncwarp();
-  if (l == 0) mbar_arrive(&d_empty[db]);
-  if constexpr (NTI + 1 < dp::NT) dphi_tiles<NTI + 1>(x, dx, dbase, lane_off, d_full, d_empty, l, tr);
-}
-
-template <bool kUpd, int kDen>
-__global__ void __launch_bounds__(256, 1) k_tc_dphi(const __grid_constant__ CUtensorMap tm_a,
-                                                    const __grid_constant__ CUtensorMap tm_a16, Geo g,
-                                                    const __nv_bfloat16* __restrict__ xraw,
-                                                    const float* __restrict__ ell,
-                                                    const float* __restrict__ lamlog,
-                                                    const __half* __restrict__ b_main,
-                                                    const __half* __restrict__ b_den,
-                                                    const float* __restrict__ dx32, const float* __restrict__ dv32,
-                                                    float* dell, float* dellend, __nv_bfloat16* dxo,
-                                                    __nv_bfloat16* dvo) {
-  using namespace dp;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* a_s = smem;
-  uint8_t* a16_s = a_s + AB;
-  uint8_t* bm_s = a16_s + A16;
-  uint8_t* bd_s = bm_s + NST * BM;
-  uint64_t* bars = (uint64_t*)(bd_s + NST * BD);
-  uint64_t* a_ready = bars;              // 1 (TMA tx + 4 compute-warp arrivals)
-  uint64_t* b_full = a_ready + 1;        // NST
-  uint64_t* b_empty = b_full + NST;      // NST
-  uint64_t* d_full = b_empty + NST;      // 2
-  uint64_t* d_empty = d_full + 2;        // 2
-  uint64_t* g_full = d_empty + 2;        // NA
-  uint64_t* g_empty = g_full + NA;       // NA
-  uint64_t* fin = g_empty + NA;          // 1
-  __shared__ uint32_t tmem_base;
-  __shared__ float red_s[4];
-
-  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
-  const int I = blockIdx.x, k = blockIdx.y, s = blockIdx.z;
-  const int tok0 = k * g.c + I * 128;
-  constexpr bool den = kDen != 0;
-  if (!kUpd && k == 0) {
-    // chunk 0 has no state query: its dq is the intra-chunk part alone
-    for (int i = tid; i < 128 * 16; i += 256) {
-      const int r = i >> 4, c4 = (i & 15) * 4;
-      const float4 v = *(const float4*)(dx32 + ((size_t)s * g.t + tok0 + r) * HD + c4);
-      uint2 o2 = make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
-      *(uint2*)(dxo + rowid(g, s, tok0 + r) * HD + c4) = o2;
-    }
-    return;
-  }
-  const int bslot = kUpd ? k : k - 1;    // state index the B operand comes from
-  const __half* bm = b_main + (size_t)(s * g.n + bslot) * ST_MAIN;
-  const __half* bd = b_den + (size_t)(s * g.n + bslot) * ST_DEN;
-  // undo the stored-state scale (A'_{k-1} for the query side, G_k for the update side)
-  const float sscale = 1.f / (kUpd ? pow2_neg_bits(g.n - 1 - k) : pow2_neg_bits(k - 1));
-
-  if (w == 2) tmem_alloc<512>(&tmem_base);
-  if (tid == 0) {
-    mbar_init(a_ready, 5);
-    for (int i = 0; i < NST; ++i) {
-      mbar_init(&b_full[i], 1);
-      mbar_init(&b_empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&d_full[i], 1);
-      mbar_init(&d_empty[i], 4);
-    }
-    for (int i = 0; i < NA; ++i) {
-      mbar_init(&g_full[i], 4);
-      mbar_init(&g_empty[i], 1);
-    }
-    mbar_init(fin, 1);
-    fence_barrier_init();
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tm = tmem_base;
-
-  if (w == 0) {
-    if (l == 0) {
-      tma_prefetch(&tm_a);
-      mbar_expect_tx(a_ready, AB + ((!kUpd && den) ? A16 : 0));
-      tma_load_2d(a_s, &tm_a, a_ready, 0, s * g.t + tok0);
-      if (!kUpd && den) tma_load_2d(a16_s, &tm_a16, a_ready, 0, s * g.t + tok0);
-      int j = 0;
-      auto stage = [&](const __half* m, uint32_t mb, const __half* d, uint32_t dbytes) {
-        const int st = j % NST;
-        if (j >= NST) mbar_wait(&b_empty[st], ((j / NST) + 1) & 1);
-        mbar_expect_tx(&b_full[st], mb + dbytes);
-        bulk_load(bm_s + st * BM, m, mb, &b_full[st]);
-        if (dbytes) bulk_load(bd_s + st * BD, d, dbytes, &b_full[st]);
-        ++j;
-      };
-      for (int nt = 0; nt < NT; ++nt) stage(bm + (size_t)nt * 128 * 64, BM, bd + (size_t)nt * 128 * 16, den ? BD : 0);
-      if (kUpd)
-        for (int kb = 0; kb < NKB; ++kb) stage(bm + (size_t)kb * 64 * 64, 64 * 128, nullptr, 0);
-    }
-  } else if (w == 1) {
-    if (l == 0) {
-      const uint32_t id128 = idesc_f16(128, 128, false, false);
-      const uint32_t id64mn = idesc_f16(128, 64, false, true);
-      mbar_wait(a_ready, 0);
-      tc_fence_after();
-      const uint32_t am = smem_u32(a_s), a16 = smem_u32(a16_s);
-      int j = 0;
-#ifdef PA_TRACE
-      const bool trm = kUpd && blockIdx.x == 0 && blockIdx.y == 5 && blockIdx.z == 3;
-#endif
-      PA_TR2(trm, 99);
-      for (int nt = 0; nt < NT; ++nt, ++j) {
-        const int st = j % NST, db = nt & 1;
-        mbar_wait(&b_full[st], (j / NST) & 1);
-        PA_TR2(trm, nt * 4 + 0);
-        if (nt >= 2) mbar_wait(&d_empty[db], ((nt >> 1) + 1) & 1);
-        PA_TR2(trm, nt * 4 + 1);
-        tc_fence_after();
-        const uint32_t bmm = smem_u32(bm_s + st * BM), bdd = smem_u32(bd_s + st * BD);
-        const uint32_t dt = tm + (uint32_t)(db * 128);
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          mma_ss(dt, smem_desc(am + kk * 32, 16, 1024, 2), smem_desc(bmm + kk * 32, 16, 1024, 2), id128,
-                 kk > 0 ? 1u : 0u);
-        if (den) mma_ss(dt, smem_desc(a16, 16, 256, 6), smem_desc(bdd, 16, 256, 6), id128, 1u);
-        tc_commit(&d_full[db]);
-        tc_commit(&b_empty[st]);
-        PA_TR2(trm, nt * 4 + 2);
-      }
-      if (kUpd) {
-        for (int kb = 0; kb < NKB; ++kb, ++j) {
-          const int st = j % NST, bb = kb % NA;
-          mbar_wait(&g_full[bb], (kb / NA) & 1);
-          mbar_wait(&b_full[st], (j / NST) & 1);
-          tc_fence_after();
-          const uint32_t bmm = smem_u32(bm_s + st * BM);
-          const uint32_t ab = tm + 384u + (uint32_t)(bb * 32);
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            mma_ts(tm + 256u, ab + kk * 8, smem_desc(bmm + kk * 2048, 8192, 1024, 2), id64mn,
-                   (kb > 0 || kk > 0) ? 1u : 0u);
-          tc_commit(&g_empty[bb]);
-          tc_commit(&b_empty[st]);
-          PA_TR2(trm, 210 + kb);
-        }
-      }
-      tc_commit(fin);
-    }
-  } else if (w >= 4) {
-    const int q = w & 3, row = q * 32 + l;
-    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    const int tok = tok0 + row;
-    const float lt = ell[(size_t)s * g.t + tok];
-    // phi' is generated from the exact bf16 row; the per-token factor
-    //   query : c_m = sigma^2 gp_m (y_state = c_m phi'(q) A')
-    //   update: W_j = exp(lend - ell_j) (S' = sum_j W_j phi'(k_j) u_j^T)
-    // multiplies the fp32 results instead of a rounded operand.
-    const float fct =
-        sscale * (kUpd ? (g.gated ? __expf(lamlog[s * g.n + k] - lt) : 1.f) : g.scale * g.scale * __expf(lt));
-    uint32_t xp[32];
-    load_row_f16(xraw + rowid(g, s, tok) * HD, xp);
-    if (kUpd && den) {
-      // A score-sum tile for the update side: [v | 1]: row = token, column 0 = 1 (SW32 layout)
-      uint32_t* rowp = (uint32_t*)(a16_s + (size_t)row * 32);
-      for (int i = 0; i < 8; ++i) rowp[i] = 0u;
-      *(__half*)(a16_s + sw32_elem(row, 0)) = __float2half_rn(1.f);
-      fence_async_smem();
-    }
-    __syncwarp();
-    if (l == 0) mbar_arrive(a_ready);
-    float x[64], dx[64];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const float2 f2 = __half22float2(*(const __half2*)&xp[i]);
-      x[2 * i] = f2.x;
-      x[2 * i + 1] = f2.y;
-      dx[2 * i] = 0.f;
-      dx[2 * i + 1] = 0.f;
-    }
-#ifdef PA_TRACE
-    const bool trc = kUpd && blockIdx.x == 0 && blockIdx.y == 5 && blockIdx.z == 3 && w == 4 && l == 0;
-#else
-    const bool trc = false;
-#endif
-    dphi_tiles<0>(x, dx, tm, lane_off, d_full, d_empty, l, trc);
-    float c = 0.f;
-#pragma unroll
-    for (int a = 0; a < 64; ++a) c = fmaf(dx[a], x[a], c);
-    c *= 0.5f * fct;   // = d<.,.>/d(log factor): degree-2 homogeneity of phi'
-    {
-      // final gradient row = intra-chunk part (fp32) + this state part, stored once in bf16
-      const float* o = dx32 + ((size_t)s * g.t + tok) * HD;
-      uint4* dst = (uint4*)(dxo + rowid(g, s, tok) * HD);
-#pragma unroll
-      for (int a = 0; a < 64; a += 8) {
-        const float4 v0 = *(const float4*)(o + a), v1 = *(const float4*)(o + a + 4);
-        dst[a / 8] = make_uint4(pack_bf16(fmaf(dx[a], fct, v0.x), fmaf(dx[a + 1], fct, v0.y)),
-                                pack_bf16(fmaf(dx[a + 2], fct, v0.z), fmaf(dx[a + 3], fct, v0.w)),
-                                pack_bf16(fmaf(dx[a + 4], fct, v1.x), fmaf(dx[a + 5], fct, v1.y)),
-                                pack_bf16(fmaf(dx[a + 6], fct, v1.z), fmaf(dx[a + 7], fct, v1.w)));
-      }
-    }
-    if (!kUpd) {
-      if (g.gated) dell[(size_t)s * g.t + tok] += c;   // gp_m = exp(ell_m)
-    } else {
-      // suffix-decay cotangent: -c on ell_tok and +c on ell_end; summed over the
-      // chunk this is an exclusive prefix sum (no cancellation), done in gate_finish
-      if (g.gated) dellend[(size_t)s * g.t + tok] = c;
-      // second GEMM: dU = W_j phi'(k_j) dS~  (A generated, 36 K blocks)
-      PA_TR2(trc, 200);
-      gen_all_kblocks<0, NA>(xp, tm + 384u, lane_off, g_full, g_empty, l);
-      PA_TR2(trc, 201);
-      mbar_wait(fin, 0);
-      PA_TR2(trc, 202);
-      tc_fence_after();
-      uint32_t r[64];
-      tmem_ld32(tm + 256u + lane_off, r);
-      tmem_ld32(tm + 256u + lane_off + 32, r + 32);
-      tc_wait_ld();
-      const float* ov = dv32 + ((size_t)s * g.t + tok) * HD;
-      uint4* dst = (uint4*)(dvo + rowid(g, s, tok) * HD);
-#pragma unroll
-      for (int a = 0; a < 64; a += 8) {
-        const float4 v0 = *(const float4*)(ov + a), v1 = *(const float4*)(ov + a + 4);
-        float f[8];
-#pragma unroll
-        for (int z = 0; z < 8; ++z) f[z] = __uint_as_float(r[a + z]) * fct;
-        dst[a / 8] = make_uint4(pack_bf16(f[0] + v0.x, f[1] + v0.y), pack_bf16(f[2] + v0.z, f[3] + v0.w),
-                                pack_bf16(f[4] + v1.x, f[5] + v1.y), pack_bf16(f[6] + v1.z, f[7] + v1.w));
-      }
-    }
-    (void)red_s;
-  }
-  if (!kUpd && w >= 4) {
-    // query side has no second GEMM; fin still closes the MMA stream
-    mbar_wait(fin, 0);
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (w == 2) tmem_dealloc<512>(tm);
-}
-
-// --------------------------------------------------------------------------
-// intra-chunk backward on tcgen05 (gradients.py:98-176 power branch, with the
-// pairwise-decay rule 79-95 in log space):
-//   P = E sig^2 s^2,  dP' = dnum.v + dden,  dS = dP' E 2 sig^2 s   (s = q.k raw)
-//   key side  : dV_J += P^T dnum_I, dK_J += dS^T Q_I, dell_j -= sum_i dP' P
-//   query side: dQ_I += dS K_J,                       dell_i += sum_j dP' P
-// E_ij = exp(ell_i - ell_j): exact per element on the diagonal block,
-// factored r_i c_j (both <= 1) off it.
-// --------------------------------------------------------------------------
-namespace ib {
-constexpr int T128 = 128 * 128;   // one 128-token x 64 bf16 tile
-constexpr int NST = 2;            // streamed-tile stages
-constexpr int SMEM = 1024 + 2 * T128 + NST * 2 * T128 + 4096 + 2048 + 512;
-}  // namespace ib
-
-// kKV = true: one CTA per key block J, loops query blocks I = J..nq-1.
-// kKV = false: one CTA per query block I, loops key blocks J = 0..I.
-template <bool kKV>
-__global__ void __launch_bounds__(256, 1) k_tc_intra_bwd(const __grid_constant__ CUtensorMap tm_q,
-                                                         const __grid_constant__ CUtensorMap tm_k,
-                                                         const __grid_constant__ CUtensorMap tm_v,
-                                                         const __grid_constant__ CUtensorMap tm_dn, Geo g,
-                                                         const float* __restrict__ ell,
-                                                         const float* __restrict__ dden, float* out_a,
-                                                         float* out_b, float* dell) {
-  using namespace ib;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  // fixed tiles: kKV: K_J, V_J   | q-side: Q_I, dN_I
-  uint8_t* f0 = smem;
-  uint8_t* f1 = f0 + T128;
-  // streamed tiles per stage: kKV: Q_I, dN_I | q-side: K_J, V_J
-  uint8_t* s0 = f1 + T128;
-  float* ell_s = (float*)(s0 + NST * 2 * T128);   // [1024]
-  float* sc = ell_s + 1024;                        // [2][128] per-column decay factor
-  float* sd = sc + 256;                            // [2][128] per-column dden (kKV)
-  uint64_t* bars = (uint64_t*)(sd + 256);
-  uint64_t* f_full = bars;            // 1
-  uint64_t* t_full = f_full + 1;      // NST
-  uint64_t* t_empty = t_full + NST;   // NST
-  uint64_t* s_full = t_empty + NST;   // 1  (S and dP of the current block)
-  uint64_t* pd_full = s_full + 1;     // 1  (P/dS written, S/dP consumed)
-  uint64_t* pd_free = pd_full + 1;    // 1  (gradient MMAs of the block done)
-  uint64_t* fin = pd_free + 1;        // 1
-  __shared__ uint32_t tmem_base;
-
-  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
-  const int B0 = blockIdx.x, k = blockIdx.y, s = blockIdx.z;
-  const int bi = s / g.h, hi = s % g.h;
-  const int c0 = k * g.c, nq = g.c / 128;
-  const int first = kKV ? B0 : 0, last = kKV ? nq - 1 : B0;
-  const int nblk = last - first + 1;
-
-  if (w == 2) tmem_alloc<512>(&tmem_base);
-  if (tid == 0) {
-    mbar_init(f_full, 1);
-    for (int i = 0; i < NST; ++i) {
-      mbar_init(&t_full[i], 1);
-      mbar_init(&t_empty[i], 1);
-    }
-    mbar_init(s_full, 1);
-    mbar_init(pd_full, 4);
-    mbar_init(pd_free, 1);
-    mbar_init(fin, 1);
-    fence_barrier_init();
-  }
-  for (int i = tid; i < g.c; i += 256) ell_s[i] = ell[(size_t)s * g.t + c0 + i];
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tm = tmem_base;
-  // TMEM: S [0,128) dP [128,256) P [256,320) dS [320,384) acc_a [384,448) acc_b [448,512)
-  const uint32_t tS = tm, tDP = tm + 128, tP = tm + 256, tDS = tm + 320, tA = tm + 384, tB = tm + 448;
-
-  if (w == 0) {
-    if (l == 0) {
-      tma_prefetch(&tm_q);
-      tma_prefetch(&tm_k);
-      tma_prefetch(&tm_v);
-      tma_prefetch(&tm_dn);
-      mbar_expect_tx(f_full, 2 * T128);
-      if (kKV) {
-        tma_load_4d(f0, &tm_k, f_full, 0, hi, c0 + B0 * 128, bi);
-        tma_load_4d(f1, &tm_v, f_full, 0, hi, c0 + B0 * 128, bi);
-      } else {
-        tma_load_4d(f0, &tm_q, f_full, 0, hi, c0 + B0 * 128, bi);
-        tma_load_2d(f1, &tm_dn, f_full, 0, s * g.t + c0 + B0 * 128);
-      }
-      for (int it = 0; it < nblk; ++it) {
-        const int X = first + it, st = it % NST;
-        if (it >= NST) mbar_wait(&t_empty[st], ((it / NST) + 1) & 1);
-        mbar_expect_tx(&t_full[st], 2 * T128);
-        uint8_t* d0 = s0 + st * 2 * T128;
-        if (kKV) {
-          tma_load_4d(d0, &tm_q, &t_full[st], 0, hi, c0 + X * 128, bi);
-          tma_load_2d(d0 + T128, &tm_dn, &t_full[st], 0, s * g.t + c0 + X * 128);
-        } else {
-          tma_load_4d(d0, &tm_k, &t_full[st], 0, hi, c0 + X * 128, bi);
-          tma_load_4d(d0 + T128, &tm_v, &t_full[st], 0, hi, c0 + X * 128, bi);
-        }
-      }
-    }
-  } else if (w == 1) {
-    if (l == 0) {
-      const uint32_t id128 = idesc_bf16(128, 128, false, false);
-      const uint32_t id64mn = idesc_bf16(128, 64, false, true);
-      mbar_wait(f_full, 0);
-      const uint32_t F0 = smem_u32(f0), F1 = smem_u32(f1);
-      for (int it = 0; it < nblk; ++it) {
-        const int st = it % NST;
-        mbar_wait(&t_full[st], (it / NST) & 1);
-        if (it >= 1) mbar_wait(pd_full, (it - 1) & 1);   // S/dP of the previous block consumed
-        tc_fence_after();
-        const uint32_t T0 = smem_u32(s0 + st * 2 * T128), T1 = T0 + T128;
-        // S (or S^T) and dP (or dP^T): kKV rows = keys: A = K_J / V_J, B = Q_I / dN_I
-        //                               q-side rows = queries: A = Q_I / dN_I, B = K_J / V_J
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          mma_ss(tS, smem_desc(F0 + kk * 32, 16, 1024, 2), smem_desc(T0 + kk * 32, 16, 1024, 2), id128, kk > 0);
-          mma_ss(tDP, smem_desc(F1 + kk * 32, 16, 1024, 2), smem_desc(T1 + kk * 32, 16, 1024, 2), id128, kk > 0);
-        }
-        tc_commit(s_full);
-        // gradient MMAs of this block once P / dS are in TMEM
-        mbar_wait(pd_full, it & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t f = (it > 0 || kk > 0) ? 1u : 0u;
-          if (kKV) {
-            mma_ts(tB, tP + kk * 8, smem_desc(T1 + kk * 2048, 8192, 1024, 2), id64mn, f);   // dV += P^T dN
-            mma_ts(tA, tDS + kk * 8, smem_desc(T0 + kk * 2048, 8192, 1024, 2), id64mn, f);  // dK += dS^T Q
-          } else {
-            mma_ts(tA, tDS + kk * 8, smem_desc(T0 + kk * 2048, 8192, 1024, 2), id64mn, f);  // dQ += dS K
-          }
-        }
-        tc_commit(pd_free);
-        tc_commit(&t_empty[st]);
-      }
-      tc_commit(fin);
-    }
-  } else if (w >= 4) {
-    const int q = w & 3, row = q * 32 + l;
-    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    const float sig2 = g.scale * g.scale;
-    const float l_own = ell_s[B0 * 128 + row];
-    const float dden_own = kKV ? 0.f : dden[(size_t)s * g.t + c0 + B0 * 128 + row];
-    float red = 0.f;  // kKV: col sum of dP'P (-> -dell_j); q-side: row sum (-> +dell_i)
-    for (int it = 0; it < nblk; ++it) {
-      const int X = first + it, sb = it & 1;
-      const bool diag = (X == B0);
-      // per-column factors of block X (columns = the streamed tokens)
-      const int J = kKV ? B0 : X;                      // key block of this (I, J) pair
-      const float lref = ell_s[J * 128 + 127];
-      const float lcol = ell_s[X * 128 + row];
-      if (kKV) {
-        sc[sb * 128 + row] = diag ? lcol : __expf(lcol - lref);        // r_i for query column i
-        sd[sb * 128 + row] = dden[(size_t)s * g.t + c0 + X * 128 + row];
-      } else {
-        sc[sb * 128 + row] = diag ? lcol : __expf(lref - lcol);        // c_j for key column j
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      // own-row factor
-      const float fo = kKV ? __expf(lref - l_own) : __expf(l_own - lref);  // c_j (keys) or r_i (queries)
-      mbar_wait(s_full, it & 1);
-      if (it >= 1) mbar_wait(pd_free, (it - 1) & 1);   // P/dS regions free again
-      tc_fence_after();
-      const float* scs = sc + sb * 128;
-      const float* sds = sd + sb * 128;
-#pragma unroll
-      for (int ch = 0; ch < 4; ++ch) {
-        uint32_t rs[32], rd[32], pp[16], pdsv[16];
-        tmem_ld32(tS + lane_off + ch * 32, rs);
-        tmem_ld32(tDP + lane_off + ch * 32, rd);
-        tc_wait_ld();
-#pragma unroll
-        for (int e2 = 0; e2 < 16; ++e2) {
-          float pv[2], dv[2];
-#pragma unroll
-          for (int z = 0; z < 2; ++z) {
-            const int col = ch * 32 + e2 * 2 + z;
-            const float sv = __uint_as_float(rs[e2 * 2 + z]);
-            const float dd = kKV ? sds[col] : dden_own;
-            const float dpv = __uint_as_float(rd[e2 * 2 + z]) + dd;
-            float E;
-            if (diag) {
-              // kKV: row = key j, col = query i (valid i >= j); q-side: row = query i, col = key j (j <= i)
-              const bool valid = kKV ? (col >= row) : (col <= row);
-              const float li = kKV ? scs[col] : l_own, lj = kKV ? l_own : scs[col];
-              E = valid ? __expf(fminf(li - lj, 0.f)) : 0.f;
-            } else {
-              E = fo * scs[col];
-            }
-            const float P = E * sig2 * sv * sv;
-            red = fmaf(dpv, P, red);
-            pv[z] = P;
-            dv[z] = dpv * E * 2.f * sig2 * sv;
-          }
-          pp[e2] = pack_bf16(pv[0], pv[1]);
-          pdsv[e2] = pack_bf16(dv[0], dv[1]);
-        }
-        if (kKV) tmem_st16(tP + lane_off + ch * 16, pp);
-        tmem_st16(tDS + lane_off + ch * 16, pdsv);
-      }
-      tc_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (l == 0) mbar_arrive(pd_full);
-    }
-    // epilogue: accumulate gradients (fp32, stream-major) and the gate cotangent
-    mbar_wait(fin, 0);
-    tc_fence_after();
-    const size_t tokr = (size_t)s * g.t + c0 + B0 * 128 + row;
-    uint32_t r[64];
-    tmem_ld32(tA + lane_off, r);
-    tmem_ld32(tA + lane_off + 32, r + 32);
-    tc_wait_ld();
-    float* oa = out_a + tokr * HD;
-#pragma unroll
-    for (int a = 0; a < 64; a += 4)
-      *(float4*)(oa + a) = make_float4(__uint_as_float(r[a]), __uint_as_float(r[a + 1]), __uint_as_float(r[a + 2]),
-                                       __uint_as_float(r[a + 3]));
-    if (kKV) {
-      tmem_ld32(tB + lane_off, r);
-      tmem_ld32(tB + lane_off + 32, r + 32);
-      tc_wait_ld();
-      float* ob = out_b + tokr * HD;
-#pragma unroll
-      for (int a = 0; a < 64; a += 4)
-        *(float4*)(ob + a) = make_float4(__uint_as_float(r[a]), __uint_as_float(r[a + 1]), __uint_as_float(r[a + 2]),
-                                         __uint_as_float(r[a + 3]));
-    }
-    if (g.gated) dell[tokr] += kKV ? -red : red;
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (w == 2) tmem_dealloc<512>(tm);
 }
 
 // gate finish (gradients.py:79-95, 245-264 in log space), one warp per chunk:
