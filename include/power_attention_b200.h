@@ -77,6 +77,42 @@ int pa_power_full_bwd(const pa_problem* pr, const void* q, const void* k, const 
                       void* dq, void* dk, void* dv, float* dlog_g, const void* fwd_ws,
                       void* bwd_ws, size_t bwd_ws_bytes, pa_stream_t stream);
 
+/* ---------------------------------------------------------------- sequence parallel
+ * A sequence split into contiguous chunk ranges, one per rank (
+ * the reference runs the discumsum of chunked.py:356-367 serially over all
+ * chunks).  discumsum is a linear recurrence with the associative combine
+ * (l1, S1) o (l2, S2) = (l1 l2, l2 S1 + S2), so each rank runs:
+ *   fwd: pa_sp_fwd_local -> E_r (its end state from a zero carry);
+ *        carry chain: C_0 = 0, C_{r+1} = pa_sp_combine(C_r, E_r)  (rank-to-rank P2P);
+ *        pa_sp_fwd_finish(C_r) -> y
+ *   bwd: pa_sp_bwd_local -> P_r (cotangent of its incoming state from a zero carry);
+ *        reverse chain: H_{R-1} = 0, H_{r-1} = pa_sp_combine(H_r, P_r);
+ *        pa_sp_bwd_finish(H_r) -> dq, dk, dv, dlog_g
+ * Carries are fp32 [b*h][2304][80] (pa_sp_state_floats), zero-initialised by
+ * the caller.  Tensor-core path only (bf16, p = 2, d = e = 64, t % chunk == 0). */
+typedef struct pa_sp_part {
+  int32_t chunk0;  /* global index of this rank's first chunk                    */
+  int32_t nchunks; /* chunks of the whole sequence                              */
+} pa_sp_part;
+
+size_t pa_sp_state_floats(const pa_problem* pr);
+int pa_sp_fwd_local(const pa_problem* pr, const pa_sp_part* sp, const void* q, const void* k, const void* v,
+                    const float* log_g, void* ws, size_t ws_bytes, float* end_state, pa_stream_t stream);
+int pa_sp_fwd_finish(const pa_problem* pr, const pa_sp_part* sp, const void* q, const void* k, const void* v,
+                     const float* log_g, void* y, float* rowsum, void* ws, size_t ws_bytes, const float* carry,
+                     pa_stream_t stream);
+int pa_sp_bwd_local(const pa_problem* pr, const pa_sp_part* sp, const void* q, const void* k, const void* v,
+                    const float* log_g, const void* y, const float* rowsum, const void* dy, const void* fwd_ws,
+                    void* bwd_ws, size_t bwd_ws_bytes, float* prefix_cot, pa_stream_t stream);
+int pa_sp_bwd_finish(const pa_problem* pr, const pa_sp_part* sp, const void* q, const void* k, const void* v,
+                     const float* log_g, const void* y, const float* rowsum, const void* dy, void* dq, void* dk,
+                     void* dv, float* dlog_g, const void* fwd_ws, void* bwd_ws, size_t bwd_ws_bytes,
+                     const float* carry_cot, pa_stream_t stream);
+/* out = exp(sum of this rank's chunk log-decays) * carry + local, per stream
+ * (carry may be NULL = zero).  Needs the rank's forward workspace. */
+int pa_sp_combine(const pa_problem* pr, const pa_sp_part* sp, const void* fwd_ws, const float* carry,
+                  const float* local, float* out, pa_stream_t stream);
+
 /* Device-side status of the last forward: number of non-positive score sums
  * seen while normalizing (the reference raises ZeroDenominator,
  * chunked.py:392-395).  Reads 4 bytes from ws; synchronises the stream. */

@@ -28,6 +28,12 @@ _ERRORS = {
 }
 
 
+class PaSpPart(ctypes.Structure):
+    """pa_sp_part: this rank's chunk range inside the whole sequence."""
+
+    _fields_ = [("chunk0", ctypes.c_int32), ("nchunks", ctypes.c_int32)]
+
+
 class PaProblem(ctypes.Structure):
     _fields_ = [
         ("b", ctypes.c_int32),
@@ -70,6 +76,14 @@ _SIGS = {
     "pa_profile_enable": (ctypes.c_int, [_I32]),
     "pa_profile_reset": (None, []),
     "pa_profile_read": (ctypes.c_int, [_VP, _VP, _VP, _I32]),
+    "pa_sp_state_floats": (_SZ, [_PP]),
+    "pa_sp_fwd_local": (ctypes.c_int, [_PP, _VP, _VP, _VP, _VP, _VP, _VP, _SZ, _VP, _VP]),
+    "pa_sp_fwd_finish": (ctypes.c_int, [_PP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _SZ, _VP, _VP]),
+    "pa_sp_bwd_local": (ctypes.c_int, [_PP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _SZ, _VP,
+                                        _VP]),
+    "pa_sp_bwd_finish": (ctypes.c_int, [_PP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
+                                         _VP, _VP, _SZ, _VP, _VP]),
+    "pa_sp_combine": (ctypes.c_int, [_PP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "pa_last_error": (ctypes.c_char_p, []),
     "pa_launch_count": (_I64, []),
 }

@@ -136,6 +136,10 @@ static int make_geo(const pa_problem* pr, Geo* g) {
   g->normalize = pr->normalize ? 1 : 0;
   g->gated = pr->gated ? 1 : 0;
   g->bth = 1;
+  g->k0 = 0;
+  g->ng = g->n;
+  g->prefix = 0;
+  g->nsl = g->n + 1;
   return PA_OK;
 }
 
@@ -282,6 +286,105 @@ int pa_power_full_bwd(const pa_problem* pr, const void* q, const void* k, const 
     return PA_ERR_WORKSPACE;
   }
   return simt_backward(g, pr->dtype, q, k, v, y, rowsum, dy, dq, dk, dv, dlog_g, w, b, st);
+}
+
+// ---------------------------------------------------------------- sequence parallel
+static int make_sp_geo(const pa_problem* pr, const pa_sp_part* sp, Geo* g) {
+  if (int rc = make_geo(pr, g)) return rc;
+  if (!sp || sp->chunk0 < 0 || sp->nchunks < g->n || sp->chunk0 + g->n > sp->nchunks) {
+    set_error("sequence-parallel partition: need 0 <= chunk0 and chunk0 + local chunks <= nchunks");
+    return PA_ERR_INVALID_SPEC;
+  }
+  if (!tc_supported(*g, pr->dtype) || g->t % g->c) {
+    set_error("sequence parallelism runs on the tensor-core path (bf16, p=2, d=e=64, t a multiple of the chunk)");
+    return PA_ERR_UNSUPPORTED;
+  }
+  g->k0 = sp->chunk0;
+  g->ng = sp->nchunks;
+  g->prefix = sp->chunk0 > 0 ? 1 : 0;
+  return PA_OK;
+}
+
+size_t pa_sp_state_floats(const pa_problem* pr) {
+  return pr ? (size_t)pr->b * pr->h * kSpStateFloatsPerStream : 0;
+}
+
+int pa_sp_fwd_local(const pa_problem* pr, const pa_sp_part* sp, const void* q, const void* k, const void* v,
+                    const float* log_g, void* ws, size_t ws_bytes, float* end_state, pa_stream_t stream) {
+  Geo g;
+  if (int rc = make_sp_geo(pr, sp, &g)) return rc;
+  if (!q || !k || !v || !ws || !end_state || (g.gated && !log_g)) {
+    set_error("null tensor pointer");
+    return PA_ERR_INVALID_SPEC;
+  }
+  if (ws_bytes < tc_fwd_workspace_bytes(g)) {
+    set_error("forward workspace too small");
+    return PA_ERR_WORKSPACE;
+  }
+  return tc_forward(g, q, k, v, log_g, nullptr, nullptr, ws, (cudaStream_t)stream, 1, nullptr, end_state);
+}
+
+int pa_sp_fwd_finish(const pa_problem* pr, const pa_sp_part* sp, const void* q, const void* k, const void* v,
+                     const float* log_g, void* y, float* rowsum, void* ws, size_t ws_bytes, const float* carry,
+                     pa_stream_t stream) {
+  Geo g;
+  if (int rc = make_sp_geo(pr, sp, &g)) return rc;
+  if (!q || !k || !v || !y || !ws || (g.gated && !log_g) || (g.prefix && !carry)) {
+    set_error("null tensor pointer (a partition after the first needs the incoming state)");
+    return PA_ERR_INVALID_SPEC;
+  }
+  if (ws_bytes < tc_fwd_workspace_bytes(g)) {
+    set_error("forward workspace too small");
+    return PA_ERR_WORKSPACE;
+  }
+  return tc_forward(g, q, k, v, log_g, y, rowsum, ws, (cudaStream_t)stream, 2, g.prefix ? carry : nullptr, nullptr);
+}
+
+int pa_sp_bwd_local(const pa_problem* pr, const pa_sp_part* sp, const void* q, const void* k, const void* v,
+                    const float* log_g, const void* y, const float* rowsum, const void* dy, const void* fwd_ws,
+                    void* bwd_ws, size_t bwd_ws_bytes, float* prefix_cot, pa_stream_t stream) {
+  Geo g;
+  if (int rc = make_sp_geo(pr, sp, &g)) return rc;
+  if (!q || !k || !v || !dy || !fwd_ws || !bwd_ws || !prefix_cot || (g.normalize && !rowsum)) {
+    set_error("null tensor pointer");
+    return PA_ERR_INVALID_SPEC;
+  }
+  if (bwd_ws_bytes < tc_bwd_workspace_bytes(g)) {
+    set_error("backward workspace too small");
+    return PA_ERR_WORKSPACE;
+  }
+  return tc_backward(g, q, k, v, log_g, y, rowsum, dy, nullptr, nullptr, nullptr, nullptr, fwd_ws, bwd_ws,
+                     (cudaStream_t)stream, 1, nullptr, prefix_cot);
+}
+
+int pa_sp_bwd_finish(const pa_problem* pr, const pa_sp_part* sp, const void* q, const void* k, const void* v,
+                     const float* log_g, const void* y, const float* rowsum, const void* dy, void* dq, void* dk,
+                     void* dv, float* dlog_g, const void* fwd_ws, void* bwd_ws, size_t bwd_ws_bytes,
+                     const float* carry_cot, pa_stream_t stream) {
+  Geo g;
+  if (int rc = make_sp_geo(pr, sp, &g)) return rc;
+  if (!q || !k || !v || !dy || !dq || !dk || !dv || !fwd_ws || !bwd_ws || (g.normalize && !rowsum)) {
+    set_error("null tensor pointer");
+    return PA_ERR_INVALID_SPEC;
+  }
+  if (bwd_ws_bytes < tc_bwd_workspace_bytes(g)) {
+    set_error("backward workspace too small");
+    return PA_ERR_WORKSPACE;
+  }
+  if (!g.gated) dlog_g = nullptr;
+  return tc_backward(g, q, k, v, log_g, y, rowsum, dy, dq, dk, dv, dlog_g, fwd_ws, bwd_ws, (cudaStream_t)stream, 2,
+                     carry_cot, nullptr);
+}
+
+int pa_sp_combine(const pa_problem* pr, const pa_sp_part* sp, const void* fwd_ws, const float* carry,
+                  const float* local, float* out, pa_stream_t stream) {
+  Geo g;
+  if (int rc = make_sp_geo(pr, sp, &g)) return rc;
+  if (!fwd_ws || !local || !out) {
+    set_error("null tensor pointer");
+    return PA_ERR_INVALID_SPEC;
+  }
+  return tc_sp_combine(g, fwd_ws, carry, local, out, (cudaStream_t)stream);
 }
 
 int pa_fwd_zero_denominators(const pa_problem* pr, const void* ws, pa_stream_t stream,

@@ -18,6 +18,11 @@ struct Geo {
   int p, c, n, D, ns;     // degree, chunk, chunks, features, streams
   float scale;
   int normalize, gated, bth;
+  // Sequence-parallel partition (tensor-core path): this launch holds global
+  // chunks [k0, k0 + n) of a sequence of ng chunks; prefix = 1 when a state
+  // flows in from earlier chunks.  Chunk-state buffers hold nsl = n + 1 slots
+  // per stream: slot j is the state before local chunk j (slot 0 = prefix).
+  int k0, ng, prefix, nsl;
 };
 
 __host__ __device__ __forceinline__ size_t rowid(const Geo& g, int s, int m) {

@@ -181,8 +181,10 @@ __global__ void __launch_bounds__(fm::THREADS, 1) k_tc_featmajor(const __grid_co
   __shared__ uint32_t tmem_base;
 
   const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
-  const int grp = blockIdx.x, kin = blockIdx.y + (kBwd ? 1 : 0), s = blockIdx.z;
-  const int slot = kBwd ? kin - 1 : kin;
+  // forward: S'_kin; backward: dA' of the state slot kin (the state before chunk
+  // kin, read by chunk kin's queries; slot 0 only exists with a prefix state)
+  const int grp = blockIdx.x, kin = blockIdx.y + ((kBwd && !g.prefix) ? 1 : 0), s = blockIdx.z;
+  const int slot = kin;
   const int t0 = grp * 4, nt = min(4, NTH - t0);
   constexpr bool den = kDen != 0;   // compile-time: a predicated-off tcgen05.mma still costs an issue slot
   // tokens per MMA/generation step: 64 (one barrier round trip per 16 MMAs) when the
@@ -305,7 +307,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1) k_tc_featmajor(const __grid_co
     for (int u = 0; u < 2; ++u) {
       const int t = tp * 2 + u;
       if (!act[u]) continue;
-      float* dst = out + (((size_t)(s * g.n + slot) * FH) + (size_t)(t0 + t) * 128 + q * 32 + l) * UW;
+      float* dst = out + (((size_t)(s * g.nsl + slot) * FH) + (size_t)(t0 + t) * 128 + q * 32 + l) * UW;
       for (int c0 = 0; c0 < ncols; c0 += 16) {
         uint32_t r[16];
         tmem_ld16(tm + (uint32_t)(t * ACC_W) + lane_off + c0, r);
@@ -354,15 +356,24 @@ __device__ __forceinline__ uint8_t* state_elem_ptr(__half* st_main, __half* st_d
 
 __global__ void __launch_bounds__(256) k_tc_scan_fwd(Geo g, int ucols, const float* __restrict__ lamlog,
                                                      const float* __restrict__ sp, __half* st_main,
-                                                     __half* st_den) {
+                                                     __half* st_den, const float* __restrict__ carry,
+                                                     float* end_out, int write) {
+  // slot j+1 = lambda_j slot_j + omega S'_j; slot 0 = carry (the state flowing in
+  // from earlier chunks, zero without one).  write = 0: only the end state.
   const int s = blockIdx.y;
   const int e = (blockIdx.x * 256 + threadIdx.x) * 4;
   if (e >= FH * ucols) return;
   const int f = e / ucols, u = e - f * ucols;
   const float om = slot_omega(f);
-  const float* src = sp + ((size_t)s * g.n * FH + f) * UW + u;
+  const float* src = sp + ((size_t)s * g.nsl * FH + f) * UW + u;
   const size_t kstride = (size_t)FH * UW;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  const size_t cidx = ((size_t)s * FH + f) * UW + u;
+  float4 acc = carry ? *(const float4*)(carry + cidx) : make_float4(0.f, 0.f, 0.f, 0.f);
+  if (write && g.prefix) {
+    const float sc = pow2_neg_bits(g.k0 - 1);
+    *(uint2*)state_elem_ptr(st_main, st_den, (size_t)s * g.nsl, f, u) =
+        make_uint2(pack_f16(acc.x * sc, acc.y * sc), pack_f16(acc.z * sc, acc.w * sc));
+  }
   for (int k0 = 0; k0 < g.n; k0 += SCAN_PF) {
     float4 x[SCAN_PF];
 #pragma unroll
@@ -372,15 +383,43 @@ __global__ void __launch_bounds__(256) k_tc_scan_fwd(Geo g, int ucols, const flo
     for (int i = 0; i < SCAN_PF; ++i) {
       const int k = k0 + i;
       if (k >= g.n) break;
-      const float lam = k == 0 ? 0.f : (g.gated ? __expf(lamlog[s * g.n + k]) : 1.f);
+      const float lam = g.gated ? __expf(lamlog[s * g.n + k]) : 1.f;
       acc.x = fmaf(lam, acc.x, om * x[i].x);
       acc.y = fmaf(lam, acc.y, om * x[i].y);
       acc.z = fmaf(lam, acc.z, om * x[i].z);
       acc.w = fmaf(lam, acc.w, om * x[i].w);
-      const float sc = pow2_neg_bits(k);
-      *(uint2*)state_elem_ptr(st_main, st_den, (size_t)s * g.n + k, f, u) =
-          make_uint2(pack_f16(acc.x * sc, acc.y * sc), pack_f16(acc.z * sc, acc.w * sc));
+      if (write) {
+        const float sc = pow2_neg_bits(g.k0 + k);
+        *(uint2*)state_elem_ptr(st_main, st_den, (size_t)s * g.nsl + k + 1, f, u) =
+            make_uint2(pack_f16(acc.x * sc, acc.y * sc), pack_f16(acc.z * sc, acc.w * sc));
+      }
     }
+  }
+  if (end_out) *(float4*)(end_out + cidx) = acc;
+}
+
+// Sequence-parallel carry combine (the associative discumsum step across
+// partitions): out = exp(sum of this partition's log lambda) * carry + local,
+// per stream.  Used for both the forward state and the backward cotangent.
+__global__ void __launch_bounds__(256) k_tc_sp_combine(Geo g, const float* __restrict__ lamlog,
+                                                       const float* __restrict__ carry,
+                                                       const float* __restrict__ local, float* out) {
+  const int s = blockIdx.y;
+  __shared__ float lam_s;
+  if (threadIdx.x < 32) {
+    float a = 0.f;
+    for (int k = threadIdx.x; k < g.n; k += 32) a += g.gated ? lamlog[s * g.n + k] : 0.f;
+    a = warp_sum(a);
+    if (threadIdx.x == 0) lam_s = __expf(a);
+  }
+  __syncthreads();
+  const float lam = lam_s;
+  const size_t base = (size_t)s * FH * UW;
+  for (size_t i = blockIdx.x * 256 + threadIdx.x; i < (size_t)FH * UW / 4; i += (size_t)gridDim.x * 256) {
+    const float4 l4 = *(const float4*)(local + base + 4 * i);
+    float4 c4 = carry ? *(const float4*)(carry + base + 4 * i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    *(float4*)(out + base + 4 * i) =
+        make_float4(fmaf(lam, c4.x, l4.x), fmaf(lam, c4.y, l4.y), fmaf(lam, c4.z, l4.z), fmaf(lam, c4.w, l4.w));
   }
 }
 
@@ -513,7 +552,7 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
   const int bi = s / g.h, hi = s % g.h;
   const int c0 = k * g.c;
   constexpr bool den = kDen != 0;
-  const bool has_state = k >= 1;
+  const bool has_state = k >= 1 || g.prefix;   // state before chunk k = slot k
 
   if (w == 2) tmem_alloc<512>(&tmem_base);
   if (tid == 0) {
@@ -568,8 +607,8 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
       const int early = min(I + 1, KV_ST);
       for (int J = 0; J < early; ++J) kv(J);
       if (has_state) {
-        const __half* srcm = st_main + (size_t)(s * g.n + (k - 1)) * ST_MAIN;
-        const __half* srcd = st_den + (size_t)(s * g.n + (k - 1)) * ST_DEN;
+        const __half* srcm = st_main + (size_t)(s * g.nsl + k) * ST_MAIN;
+        const __half* srcd = st_den + (size_t)(s * g.nsl + k) * ST_DEN;
         for (int stp = 0; stp < NSTEP; ++stp) {
           const int sb = stp % ST_ST;
           if (stp >= ST_ST) mbar_wait(&st_empty[sb], ((stp / ST_ST) + 1) & 1);
@@ -661,7 +700,7 @@ __global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUten
       gen_steps(xh_s, row, a_base, lane_off, a_full, a_empty, l);
       mbar_wait(a_done, 0);
       tc_fence_after();
-      const float cm = sig2 * __expf(li) / pow2_neg_bits(k - 1);   // undo the stored-state scale
+      const float cm = sig2 * __expf(li) / pow2_neg_bits(g.k0 + k - 1);   // undo the stored-state scale
       uint32_t r[32];
 #pragma unroll
       for (int h2 = 0; h2 < 2; ++h2) {
@@ -834,9 +873,14 @@ __global__ void __launch_bounds__(256) k_tc_bwd_prep(Geo g, const __nv_bfloat16*
   }
 }
 
-// backward scan (discumsum VJP, gradients.py:267-288) over chunk states:
-//   G_k = dA'_k + lambda_{k+1} G_{k+1};  dlambda_k = <A'_{k-1}, G_k>;  dS~_k = omega G_k
-// dA'_k comes from the feature-major GEMM (fp32, slot k holds dA'_k for k <= n-2).
+// backward scan (discumsum VJP, gradients.py:267-288) over the state slots
+// (slot j = state before local chunk j, slot n = end state):
+//   Gs_n = carry (cotangent of the end state from later chunks, zero without)
+//   for j = n-1 .. 0:  dS~_j = omega Gs_{j+1};  dlambda_j = <slot_j, Gs_{j+1}>;
+//                      Gs_j = dA'[slot j] + lambda_j Gs_{j+1}
+// dA'[slot j] (fp32) comes from the feature-major GEMM of chunk j's queries
+// (slot 0 only with a prefix).  write = 0: only the prefix cotangent Gs_0
+// (pre_out), used by the sequence-parallel two-level scan.
 // 4 columns per thread with SCAN_PF-deep prefetch; the dlambda reduction is
 // per-warp into shared memory, then one non-atomic partial per (block, chunk):
 // dlam_part[(s*n + k) * gridDim.x + block], summed by k_tc_gate_finish.
@@ -845,16 +889,18 @@ __global__ void __launch_bounds__(256) k_tc_scan_bwd(Geo g, int ucols, const flo
                                                      const float* __restrict__ dA,
                                                      const __half* __restrict__ st_main,
                                                      const __half* __restrict__ st_den,
-                                                     __half* ds_main, __half* ds_den, float* dlam_part) {
+                                                     __half* ds_main, __half* ds_den, float* dlam_part,
+                                                     const float* __restrict__ carry, float* pre_out, int write) {
   extern __shared__ float red[];  // [n][8]
   const int s = blockIdx.y, wq = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int e = (blockIdx.x * 256 + threadIdx.x) * 4;
   const bool ok = e < FH * ucols;
   const int f = ok ? e / ucols : 0, u = ok ? e - f * ucols : 0;
   const float om = ok ? slot_omega(f) : 0.f;
-  const float* src = dA + ((size_t)s * g.n * FH + f) * UW + u;
+  const float* src = dA + ((size_t)s * g.nsl * FH + f) * UW + u;
   const size_t kstride = (size_t)FH * UW;
-  float4 G = make_float4(0.f, 0.f, 0.f, 0.f);
+  const size_t cidx = ((size_t)s * FH + f) * UW + u;
+  float4 G = (ok && carry) ? *(const float4*)(carry + cidx) : make_float4(0.f, 0.f, 0.f, 0.f);
   for (int k1 = g.n - 1; k1 >= 0; k1 -= SCAN_PF) {
     float4 x[SCAN_PF];
     uint2 a[SCAN_PF];
@@ -863,37 +909,41 @@ __global__ void __launch_bounds__(256) k_tc_scan_bwd(Geo g, int ucols, const flo
       const int k = k1 - i;
       x[i] = make_float4(0.f, 0.f, 0.f, 0.f);
       a[i] = make_uint2(0u, 0u);
-      if (ok && k >= 0) {
-        if (k + 1 < g.n) x[i] = __ldcs((const float4*)(src + (size_t)k * kstride));
-        if (k >= 1)
+      if (ok && k >= 0 && (k >= 1 || g.prefix)) {
+        x[i] = __ldcs((const float4*)(src + (size_t)k * kstride));
+        if (write)
           a[i] = *(const uint2*)state_elem_ptr(const_cast<__half*>(st_main), const_cast<__half*>(st_den),
-                                               (size_t)s * g.n + k - 1, f, u);
+                                               (size_t)s * g.nsl + k, f, u);
       }
     }
 #pragma unroll
     for (int i = 0; i < SCAN_PF; ++i) {
       const int k = k1 - i;
       if (k < 0) break;
-      const float lam_next = (k + 1 < g.n) ? (g.gated ? __expf(lamlog[s * g.n + k + 1]) : 1.f) : 0.f;
-      G.x = fmaf(lam_next, G.x, x[i].x);
-      G.y = fmaf(lam_next, G.y, x[i].y);
-      G.z = fmaf(lam_next, G.z, x[i].z);
-      G.w = fmaf(lam_next, G.w, x[i].w);
-      if (ok) {
-        const float sc = om * pow2_neg_bits(g.n - 1 - k);
-        *(uint2*)state_elem_ptr(ds_main, ds_den, (size_t)s * g.n + k, f, u) =
-            make_uint2(pack_f16(G.x * sc, G.y * sc), pack_f16(G.z * sc, G.w * sc));
+      if (write) {
+        if (ok) {
+          const float sc = om * pow2_neg_bits(g.ng - 1 - (g.k0 + k));
+          *(uint2*)state_elem_ptr(ds_main, ds_den, (size_t)s * g.nsl + k, f, u) =
+              make_uint2(pack_f16(G.x * sc, G.y * sc), pack_f16(G.z * sc, G.w * sc));
+        }
+        if (k >= 1 || g.prefix) {
+          const float2 a01 = __half22float2(*(const __half2*)&a[i].x), a23 = __half22float2(*(const __half2*)&a[i].y);
+          float t = a01.x * G.x + a01.y * G.y + a23.x * G.z + a23.y * G.w;
+          t = warp_sum(t);
+          if (lane == 0) red[k * 8 + wq] = t / pow2_neg_bits(g.k0 + k - 1);
+        }
       }
-      if (k >= 1) {
-        const float2 a01 = __half22float2(*(const __half2*)&a[i].x), a23 = __half22float2(*(const __half2*)&a[i].y);
-        float t = a01.x * G.x + a01.y * G.y + a23.x * G.z + a23.y * G.w;
-        t = warp_sum(t);
-        if (lane == 0) red[k * 8 + wq] = t / pow2_neg_bits(k - 1);
-      }
+      const float lam = g.gated ? __expf(lamlog[s * g.n + k]) : 1.f;
+      G.x = fmaf(lam, G.x, x[i].x);
+      G.y = fmaf(lam, G.y, x[i].y);
+      G.z = fmaf(lam, G.z, x[i].z);
+      G.w = fmaf(lam, G.w, x[i].w);
     }
   }
+  if (ok && pre_out) *(float4*)(pre_out + cidx) = G;
+  if (!write) return;
   __syncthreads();
-  for (int k = 1 + threadIdx.x; k < g.n; k += 256) {
+  for (int k = (g.prefix ? 0 : 1) + threadIdx.x; k < g.n; k += 256) {
     float t = 0.f;
 #pragma unroll
     for (int i = 0; i < 8; ++i) t += red[k * 8 + i];
@@ -914,7 +964,7 @@ __global__ void __launch_bounds__(128) k_tc_gate_finish(Geo g, const float* __re
   float dl = 0.f;
   for (int i = lane; i < nparts; i += 32) dl += dlam_part[(size_t)wid * nparts + i];
   dl = warp_sum(dl);
-  const float base = k >= 1 ? dl * __expf(lamlog[wid]) : 0.f;
+  const float base = (k >= 1 || g.prefix) ? dl * __expf(lamlog[wid]) : 0.f;
   // pass 1: prefix of cu (exclusive) and suffix of dell (inclusive) in 32-token steps
   float tot_dell = 0.f;
   for (int m0 = s0; m0 < s1; m0 += 32) tot_dell += warp_sum(dell[(size_t)s * g.t + m0 + lane]);
@@ -992,9 +1042,9 @@ static TcFwdWs carve_fwd(const Geo& g, void* base, size_t* bytes) {
   w.kt = (__half*)take(2ull * g.ns * g.t * HD);
   w.vr = (__half*)take(2ull * g.ns * g.t * HD);
   w.wa = (__half*)take(2ull * g.ns * g.t * 16);
-  w.sp = (float*)take(4ull * g.ns * g.n * FH * UW);
-  w.stm = (__half*)take(2ull * g.ns * g.n * ST_MAIN);
-  w.std_ = (__half*)take(2ull * g.ns * g.n * ST_DEN);
+  w.sp = (float*)take(4ull * g.ns * g.nsl * FH * UW);
+  w.stm = (__half*)take(2ull * g.ns * g.nsl * ST_MAIN);
+  w.std_ = (__half*)take(2ull * g.ns * g.nsl * ST_DEN);
   w.y32 = (float*)take(g.normalize ? 4ull * g.ns * g.t * HD : 0);
   *bytes = take.off;
   return w;
@@ -1007,8 +1057,8 @@ static TcBwdWs carve_bwd(const Geo& g, void* base, size_t* bytes) {
   b.dN16 = (__half*)take(2ull * g.ns * g.t * HD);
   b.dD = (__half*)take(2ull * g.ns * g.t * 16);
   b.dden = (float*)take(4ull * g.ns * g.t);
-  b.dsm = (__half*)take(2ull * g.ns * g.n * ST_MAIN);
-  b.dsd = (__half*)take(2ull * g.ns * g.n * ST_DEN);
+  b.dsm = (__half*)take(2ull * g.ns * g.nsl * ST_MAIN);
+  b.dsd = (__half*)take(2ull * g.ns * g.nsl * ST_DEN);
   b.dq32 = (float*)take(4ull * g.ns * g.t * HD);
   b.dk32 = (float*)take(4ull * g.ns * g.t * HD);
   b.dv32 = (float*)take(4ull * g.ns * g.t * HD);
@@ -1101,7 +1151,7 @@ static void bind_context_of(const void* ptr) {
 }
 
 int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const float* log_g, void* y, float* rowsum,
-               void* ws, cudaStream_t st) {
+               void* ws, cudaStream_t st, int mode, const float* carry, float* end_out) {
   size_t need;
   TcFwdWs w = carve_fwd(g, ws, &need);
   bind_context_of(q);
@@ -1112,6 +1162,28 @@ int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const 
       !map_2d(&m_wa, w.wa, (size_t)g.ns * g.t, 16, 16, 64, CU_TENSOR_MAP_SWIZZLE_32B) ||
       !map_2d(&m_kt, w.kt, (size_t)g.ns * g.n * HD, g.c, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B)) {
     return 3;
+  }
+  // mode 0: the whole forward; SP mode 1 (local): update + end state of this
+  // partition from a zero carry; SP mode 2 (finish): discumsum from the incoming
+  // carry + attention/query (the workspace of mode 1 is reused)
+  const int uc = with_den ? UW : 64;
+  if (mode == 2) {
+    cudaMemsetAsync(w.zflag, 0, 4, st);
+    {
+      StageTimer tmr("fwd_discumsum", st);
+      k_tc_scan_fwd<<<dim3((FH * uc / 4 + 255) / 256, g.ns), 256, 0, st>>>(g, uc, w.lamlog, w.sp, w.stm, w.std_,
+                                                                           carry, nullptr, 1);
+    }
+    {
+      StageTimer tmr("fwd_attn_query", st);
+      auto fn = with_den ? k_tc_out<1> : k_tc_out<0>;
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, outk::SMEM);
+      fn<<<dim3(g.c / 128, g.n, g.ns), 256, outk::SMEM, st>>>(m_q, m_k, m_v, g, (const __nv_bfloat16*)q, w.ell,
+                                                              w.stm, w.std_, (__nv_bfloat16*)y, rowsum, w.y32,
+                                                              w.zflag);
+    }
+    count_launch(2);
+    return cuda_check("tc forward (sp finish)");
   }
   cudaMemsetAsync(w.zflag, 0, 4, st);
   {
@@ -1129,8 +1201,12 @@ int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const 
   }
   {
     StageTimer tmr("fwd_discumsum", st);
-    const int uc = with_den ? UW : 64;
-    k_tc_scan_fwd<<<dim3((FH * uc / 4 + 255) / 256, g.ns), 256, 0, st>>>(g, uc, w.lamlog, w.sp, w.stm, w.std_);
+    k_tc_scan_fwd<<<dim3((FH * uc / 4 + 255) / 256, g.ns), 256, 0, st>>>(g, uc, w.lamlog, w.sp, w.stm, w.std_,
+                                                                         carry, end_out, mode == 1 ? 0 : 1);
+  }
+  if (mode == 1) {
+    count_launch(4);
+    return cuda_check("tc forward (sp local)");
   }
   {
     StageTimer tmr("fwd_attn_query", st);
@@ -1143,9 +1219,21 @@ int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const 
   return cuda_check("tc forward");
 }
 
+int tc_sp_combine(const Geo& g, const void* fwd_ws, const float* carry, const float* local, float* out,
+                  cudaStream_t st) {
+  size_t need;
+  TcFwdWs w = carve_fwd(g, const_cast<void*>(fwd_ws), &need);
+  k_tc_sp_combine<<<dim3(16, g.ns), 256, 0, st>>>(g, w.lamlog, carry, local, out);
+  count_launch();
+  return cuda_check("sp combine");
+}
+
 int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const float* log_g, const void* y,
                 const float* rowsum, const void* dy, void* dq, void* dk, void* dv, float* dlog_g, const void* fwd_ws,
-                void* bwd_ws, cudaStream_t st) {
+                void* bwd_ws, cudaStream_t st, int mode, const float* carry, float* pre_out) {
+  // mode 0: the whole backward; SP mode 1 (local): dA' of this partition and the
+  // prefix cotangent from a zero end-state carry; SP mode 2 (finish): reverse
+  // discumsum from the incoming end-state cotangent + every gradient kernel
   (void)log_g;
   (void)y;
   size_t n1, n2;
@@ -1164,6 +1252,10 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
   CUtensorMap m_dn128;
   if (!map_2d(&m_dn128, b.dN, (size_t)g.ns * g.t, HD, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)) return 3;
   m_dummy = m_dn;
+  const int red_bytes = 8 * 4 * g.n;
+  if (red_bytes > 48 * 1024)
+    cudaFuncSetAttribute(k_tc_scan_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, red_bytes);
+  if (mode != 2) {
   {
     StageTimer tmr("bwd_prep", st);
     cudaMemsetAsync(b.dell, 0, 4ull * g.ns * g.t, st);
@@ -1179,19 +1271,24 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
         g, den ? 1 : 3, den ? b.dN : (const __nv_bfloat16*)dy, w.ell, w.lamlog, den ? b.dden : nullptr, w.vr,
         den ? w.wa : nullptr);
   }
-  if (g.n > 1) {
+  if (g.n - 1 + g.prefix > 0) {
     StageTimer tmr("bwd_query_state_dA", st);
     auto fn = den ? k_tc_featmajor<true, 1> : k_tc_featmajor<true, 0>;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, fm::SMEM);
-    fn<<<dim3((NTH + 3) / 4, g.n - 1, g.ns), fm::THREADS, fm::SMEM, st>>>(m_qt, m_dn, m_dd, g, w.sp);
+    fn<<<dim3((NTH + 3) / 4, g.n - 1 + g.prefix, g.ns), fm::THREADS, fm::SMEM, st>>>(m_qt, m_dn, m_dd, g, w.sp);
+  }
+  if (mode == 1) {
+    StageTimer tmr("bwd_discumsum", st);
+    k_tc_scan_bwd<<<dim3(scan_blocks(uc), g.ns), 256, red_bytes, st>>>(g, uc, w.lamlog, w.sp, w.stm, w.std_,
+                                                                          b.dsm, b.dsd, b.dlam, nullptr, pre_out, 0);
+    count_launch(4);
+    return cuda_check("tc backward (sp local)");
+  }
   }
   {
     StageTimer tmr("bwd_discumsum", st);
-    const int red_bytes = 8 * 4 * g.n;
-    if (red_bytes > 48 * 1024)
-      cudaFuncSetAttribute(k_tc_scan_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, red_bytes);
     k_tc_scan_bwd<<<dim3(scan_blocks(uc), g.ns), 256, red_bytes, st>>>(g, uc, w.lamlog, w.sp, w.stm, w.std_,
-                                                                          b.dsm, b.dsd, b.dlam);
+                                                                          b.dsm, b.dsd, b.dlam, carry, pre_out, 1);
   }
   {
     StageTimer tmr("bwd_intra", st);

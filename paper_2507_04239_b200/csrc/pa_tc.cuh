@@ -9,11 +9,22 @@ namespace pa {
 bool tc_supported(const Geo& g, int dtype);
 size_t tc_fwd_workspace_bytes(const Geo& g);
 size_t tc_bwd_workspace_bytes(const Geo& g);
+// mode 0: whole pass.  Sequence-parallel (Geo k0/ng/prefix): mode 1 = local
+// phase (forward: end state of this partition from a zero carry -> end_out;
+// backward: prefix cotangent from a zero end-state cotangent -> pre_out),
+// mode 2 = finish with the incoming carry (state / end-state cotangent).
+// Carries are fp32 [ns][2304][80] in the feature-slot order of the states.
 int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const float* log_g, void* y,
-               float* rowsum, void* ws, cudaStream_t st);
+               float* rowsum, void* ws, cudaStream_t st, int mode = 0, const float* carry = nullptr,
+               float* end_out = nullptr);
 int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const float* log_g,
                 const void* y, const float* rowsum, const void* dy, void* dq, void* dk, void* dv,
-                float* dlog_g, const void* fwd_ws, void* bwd_ws, cudaStream_t st);
+                float* dlog_g, const void* fwd_ws, void* bwd_ws, cudaStream_t st, int mode = 0,
+                const float* carry = nullptr, float* pre_out = nullptr);
+// out = exp(sum of this partition's log lambda) * carry + local (per stream)
+int tc_sp_combine(const Geo& g, const void* fwd_ws, const float* carry, const float* local, float* out,
+                  cudaStream_t st);
+constexpr size_t kSpStateFloatsPerStream = 2304 * 80;
 
 // intra-chunk backward (pa_tc_ib.cu): dK, dV (fp32, =), dQ (fp32, =), dell (+=)
 int tc_intra_bwd(const Geo& g, const CUtensorMap& m_q, const CUtensorMap& m_k, const CUtensorMap& m_v,

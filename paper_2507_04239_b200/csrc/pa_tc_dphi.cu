@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
   const int I = blockIdx.x, k = blockIdx.y, s = blockIdx.z;
   const int tok0 = k * g.c + I * 128;
   constexpr bool den = kDen != 0;
-  if (!kUpd && k == 0) {
+  if (!kUpd && k == 0 && !g.prefix) {
     // chunk 0 has no state query: its dq is the intra-chunk part alone
     for (int i = tid; i < 128 * 16; i += THREADS) {
       const int r = i >> 4, c4 = (i & 15) * 4;
@@ -136,11 +136,11 @@ __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
     }
     return;
   }
-  const int bslot = kUpd ? k : k - 1;   // state the B operand comes from
-  const __half* bm = b_main + (size_t)(s * g.n + bslot) * ((size_t)FH * 64);
-  const __half* bd = b_den + (size_t)(s * g.n + bslot) * ((size_t)FH * 16);
-  // undo the stored-state scale (A'_{k-1} for the query side, G_k for the update side)
-  const float sscale = 1.f / (kUpd ? pow2_neg_bits(g.n - 1 - k) : pow2_neg_bits(k - 1));
+  // B operand: query side the state before chunk k (slot k), update side dS~_k;
+  // undo their stored power-of-two scales
+  const __half* bm = b_main + (size_t)(s * g.nsl + k) * ((size_t)FH * 64);
+  const __half* bd = b_den + (size_t)(s * g.nsl + k) * ((size_t)FH * 16);
+  const float sscale = 1.f / (kUpd ? pow2_neg_bits(g.ng - 1 - (g.k0 + k)) : pow2_neg_bits(g.k0 + k - 1));
 
   if (w == W_TMEM) tmem_alloc<512>(&tmem_base);
   if (tid == 0) {
