@@ -35,6 +35,11 @@ sys.path.insert(0, ROOT)
 METRIC = "power-attn fwd+bwd tokens/sec at p=2,d=64,64k ctx; % of BF16 tensor peak"
 CFG = dict(b=4, h=16, t=65536, d=64, e=64, p=2, chunk=1024, gated=True, normalize=False)
 WORKLOAD = "configs[1]: power_full fwd+bwd bf16 p=2 d=64 b=4 h=16 t=65536 chunk=1024 gated"
+# --workload sp1m: BASELINE configs[3], one 1,048,576-token sequence (b=1, h=16)
+# split over the ranks by chunk range (sequence parallelism, NCCL carry chain)
+CFG_SP = dict(b=1, h=16, t=1048576, d=64, e=64, p=2, chunk=1024, gated=True, normalize=False)
+WORKLOAD_SP = ("configs[3]: sequence-parallel power_full fwd+bwd bf16 p=2 d=64 b=1 h=16 t=1048576 chunk=1024 "
+               "gated, chunk ranges split over the ranks")
 
 
 # --------------------------------------------------------------------------
@@ -191,7 +196,12 @@ def run_gpu(args):
     import torch.distributed as dist
 
     from paper_2507_04239_b200 import _lib, power_full
+    from paper_2507_04239_b200.parallel import power_full_sp
 
+    global CFG, WORKLOAD
+    sp = args.workload == "sp1m"
+    if sp:
+        CFG, WORKLOAD = CFG_SP, WORKLOAD_SP
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -200,6 +210,8 @@ def run_gpu(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     b, h, t, d, e, c = (CFG[k] for k in ("b", "h", "t", "d", "e", "chunk"))
+    if sp:
+        t = t // world   # this rank's contiguous token range
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
     Q = (torch.rand(b, t, h, d, device=dev, generator=g) * 2 - 1).bfloat16().requires_grad_()
     K = (torch.rand(b, t, h, d, device=dev, generator=g) * 2 - 1).bfloat16().requires_grad_()
@@ -208,7 +220,10 @@ def run_gpu(args):
     dY = (torch.rand(b, t, h, e, device=dev, generator=g) * 2 - 1).bfloat16()
 
     def step():
-        y = power_full(Q, K, V, LG, p=CFG["p"], chunk_size=c, normalize=CFG["normalize"])
+        if sp:
+            y = power_full_sp(Q, K, V, LG, p=CFG["p"], chunk_size=c, normalize=CFG["normalize"])
+        else:
+            y = power_full(Q, K, V, LG, p=CFG["p"], chunk_size=c, normalize=CFG["normalize"])
         return torch.autograd.grad(y, [Q, K, V, LG], dY)
 
     def barrier():
@@ -257,7 +272,8 @@ def run_gpu(args):
             dq, dk, dv, dl, ddy = (x.to(dev, non_blocking=True) for x in (hQ, hK, hV, hL, hdY))
             for x in (dq, dk, dv, dl):
                 x.requires_grad_()
-            y = power_full(dq, dk, dv, dl, p=CFG["p"], chunk_size=c, normalize=CFG["normalize"])
+            fn = power_full_sp if sp else power_full
+            y = fn(dq, dk, dv, dl, p=CFG["p"], chunk_size=c, normalize=CFG["normalize"])
             gr = torch.autograd.grad(y, [dq, dk, dv, dl], ddy)
             for o, gx in zip(outs, gr):
                 o.copy_(gx, non_blocking=True)
@@ -285,7 +301,8 @@ def run_gpu(args):
 
     peak, peak_sus, hbm, peak_kind = load_peaks()
     fl = flops(CFG)
-    tflops = fl["total"] / (ms / 1000.0) / 1e12
+    jobs = 1 if sp else world   # the whole-job algorithmic FLOPs
+    tflops = jobs * fl["total"] / (ms / 1000.0) / 1e12
     # dominant kernel (largest share of step time) and its roofline
     stage_ms = {k: v[0] / args.steps for k, v in stages.items()}
     stage_n = {k: v[1] / args.steps for k, v in stages.items()}
@@ -293,6 +310,8 @@ def run_gpu(args):
     if stage_ms:
         dom = max(stage_ms, key=stage_ms.get)
         per = stage_flops(dom, fl)
+        if per is not None and sp:
+            per /= world   # stage times are per rank; fl is the whole sequence
         if per is not None:
             launch_ms = stage_ms[dom] / max(stage_n[dom], 1)
             achieved = per / max(stage_n[dom], 1) / (launch_ms / 1000.0) / 1e12
@@ -302,9 +321,12 @@ def run_gpu(args):
                     "share_of_step": stage_ms[dom] / ms}
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if sp else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform q,k,v in [-1,1], gates in [0.9,1])",
-        "config": {"workload": WORKLOAD, **CFG, "parallelism": f"streams (b*h) per rank, {world} rank(s)",
+        "config": {"workload": WORKLOAD, **CFG,
+                   "parallelism": (f"sequence chunk ranges over {world} rank(s), NCCL P2P carry chain" if sp
+                                   else f"streams (b*h) per rank, {world} rank(s)"),
                    "l2": "inputs 512 MiB each >> 126 MB L2; no flush"},
         "tflops_algorithmic": tflops, "frac_of_peak": tflops / peak, "frac_of_sustained_peak": tflops / peak_sus,
         "gpu_launches": launches, "stages_ms": stage_ms, "clocks": ck, "e2e": e2e, "roofline": roof,
@@ -351,6 +373,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "sp1m"],
+                    help="cfg2: BASELINE configs[1] (default, streams sharded over ranks); "
+                         "sp1m: configs[3], one 1M-token sequence split over the ranks")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -126,14 +126,17 @@ class _Rank:
 
     def fwd_finish(self, carry, want_rowsum):
         Q, V = self.Q, self.V
-        self.y = torch.empty(*Q.shape[:3], V.shape[-1], dtype=Q.dtype, device=Q.device)
+        y = torch.empty(*Q.shape[:3], V.shape[-1], dtype=Q.dtype, device=Q.device)
+        # keep a detached alias only: holding the autograd output here would make a
+        # reference cycle (output -> grad_fn -> ctx -> this object) and delay freeing
+        self.y = y.detach()
         need_rs = bool(self.normalize or want_rowsum)
         self.rowsum = torch.empty(*Q.shape[:3] if need_rs else (0,), dtype=torch.float32, device=Q.device)
         _lib.check(self.lib.pa_sp_fwd_finish(ctypes.byref(self.pr), ctypes.byref(self.sp), _ptr(Q), _ptr(self.K),
                                              _ptr(V), _ptr(self.lg), _ptr(self.y),
                                              _ptr(self.rowsum if need_rs else None), _ptr(self.ws), self.wsb,
                                              _ptr(carry), _stream(Q.device)), "sp forward (finish)")
-        return self.y
+        return y
 
     def bwd_local(self, dy):
         lib = self.lib
