@@ -308,28 +308,74 @@ __global__ void __launch_bounds__(128, 1) rate3(int N, int R, int mode, unsigned
   if (tid < 32) tmem_dealloc<512>(tm);
 }
 
+// alternating pattern of the intra-chunk backward: (acc0, A0, B0) / (acc1, A1, B1), K-steps interleaved
+__global__ void __launch_bounds__(128, 1) rate4(int mode, int R, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x;
+  if (tid < 32) tmem_alloc<512>(&tbase);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  for (int i = tid; i < 64 * 1024 / 4; i += 128) ((uint32_t*)smem)[i] = 0x3c003c00u;
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tbase;
+  if (tid == 0) {
+    const uint32_t id = idesc_bf16(128, 64, false, mode >= 2);
+    const uint64_t b0 = smem_desc(smem_u32(smem), mode >= 2 ? 8192 : 16, 1024, 2);
+    const uint64_t b1 = smem_desc(smem_u32(smem + 16384), mode >= 2 ? 8192 : 16, 1024, 2);
+    long long t0 = clock64();
+    for (int i = 0; i < R; i += 8) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        if (mode == 0 || mode == 2) {
+          // two accumulators, two A operands, interleaved
+          mma_ts(tm, tm + 384u + kk * 8, b0 + kk * (mode >= 2 ? 128 : 2), id, 1u);
+          mma_ts(tm + 64, tm + 416u + kk * 8, b1 + kk * (mode >= 2 ? 128 : 2), id, 1u);
+        } else {
+          // same accumulator / A for all (baseline)
+          mma_ts(tm, tm + 384u + kk * 8, b0 + kk * 2, id, 1u);
+          mma_ts(tm, tm + 384u + kk * 8, b0 + kk * 2, id, 1u);
+        }
+      }
+    }
+    tc_commit(&bar);
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    out[blockIdx.x] = (unsigned long long)(t1 - t0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (tid < 32) tmem_dealloc<512>(tm);
+}
+
 int main() {
   unsigned long long* d;
   cudaMalloc(&d, 148 * 8);
   cudaFuncSetAttribute(rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   const int R = 8192;
   {
-    unsigned long long* d3;
-    cudaMalloc(&d3, 148 * 8);
-    cudaFuncSetAttribute(rate3, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024);
-    for (int mode = 0; mode < 3; ++mode)
-      for (int N : {64, 128}) {
-        rate3<<<148, 128, 48 * 1024>>>(N, 8192, mode, d3);
-        rate3<<<148, 128, 48 * 1024>>>(N, 8192, mode, d3);
-        cudaError_t e = cudaDeviceSynchronize();
-        unsigned long long h[148];
-        cudaMemcpy(h, d3, sizeof h, cudaMemcpyDeviceToHost);
-        double avg = 0;
-        for (int i = 0; i < 148; ++i) avg += h[i];
-        avg /= 148;
-        printf("rate3 mode %d (0 none, 1 concurrent tcgen05.ld, 2 concurrent tcgen05.st) N=%d: %.2f cyc/MMA (%s)\n", mode,
-               N, avg / 8192, e ? cudaGetErrorString(e) : "ok");
-      }
+    unsigned long long* d4;
+    cudaMalloc(&d4, 148 * 8);
+    cudaFuncSetAttribute(rate4, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
+    const char* nm[] = {"two acc/A interleaved, B K-major", "one acc/A, B K-major", "two acc/A interleaved, B MN-major"};
+    for (int mode = 0; mode < 3; ++mode) {
+      rate4<<<148, 128, 80 * 1024>>>(mode, 8192, d4);
+      rate4<<<148, 128, 80 * 1024>>>(mode, 8192, d4);
+      cudaError_t e = cudaDeviceSynchronize();
+      unsigned long long h[148];
+      cudaMemcpy(h, d4, sizeof h, cudaMemcpyDeviceToHost);
+      double avg = 0;
+      for (int i = 0; i < 148; ++i) avg += h[i];
+      avg /= 148;
+      printf("rate4 %-40s N=64: %.2f cyc/MMA (%s)\n", nm[mode], avg / 8192, e ? cudaGetErrorString(e) : "ok");
+    }
   }
   return 0;
 }

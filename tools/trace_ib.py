@@ -1,4 +1,4 @@
-"""Run one backward with the trace build and print the intra-backward pipeline stamps."""
+"""Run one backward with the trace build and print the intra-backward (key side) pipeline stamps."""
 import ctypes
 import os
 import sys
@@ -22,7 +22,7 @@ torch.cuda.synchronize()
 buf = (ctypes.c_longlong * 1024)()
 _lib.load().pa_debug_trace(buf, 1024)
 base = buf[0]
-names = ["S_issue", "S_commit", "P_seen", "G_issued", "c_wait", "c_got_S", "c_done"]
+names = ["S_commit", "P_seen", "G_issued", "c_wait", "c_got_S", "c_done"]
 for n in range(16):
-    row = [buf[n * 8 + i] - base for i in range(7)]
+    row = [buf[8 + n * 8 + i] - base for i in range(6)]
     print(n, "  ".join(f"{nm}={v:7d}" for nm, v in zip(names, row)))
