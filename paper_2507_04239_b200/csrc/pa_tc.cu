@@ -155,13 +155,14 @@ constexpr int XT_B = 64 * 128;        // 64 dims x 64 tokens bf16
 constexpr int B_B = 64 * 128;         // 64 tokens x 64 values bf16
 constexpr int B16_B = 64 * 32;        // 64 tokens x 16 bf16 (SW32)
 constexpr int SMEM_USED = 1024 + ST * (XT_B + B_B + B16_B) + 2048 + 512;
-constexpr int SMEM = SMEM_USED > 120 * 1024 ? SMEM_USED : 120 * 1024;  // 1 CTA (512 TMEM cols) per SM
+constexpr int SMEM = SMEM_USED;   // two CTAs per SM (256 TMEM columns each)
+constexpr int TPC = 2;            // 128-slot tiles per CTA
 constexpr int THREADS = 384;
 constexpr int GEN_WARPS = 8;
 }  // namespace fm
 
 template <bool kBwd, int kDen>
-__global__ void __launch_bounds__(fm::THREADS, 1) k_tc_featmajor(const __grid_constant__ CUtensorMap tm_xt,
+__global__ void __launch_bounds__(fm::THREADS, 2) k_tc_featmajor(const __grid_constant__ CUtensorMap tm_xt,
                                                          const __grid_constant__ CUtensorMap tm_b,
                                                          const __grid_constant__ CUtensorMap tm_b16, Geo g,
                                                          float* out) {
@@ -185,16 +186,16 @@ __global__ void __launch_bounds__(fm::THREADS, 1) k_tc_featmajor(const __grid_co
   // kin, read by chunk kin's queries; slot 0 only exists with a prefix state)
   const int grp = blockIdx.x, kin = blockIdx.y + ((kBwd && !g.prefix) ? 1 : 0), s = blockIdx.z;
   const int slot = kin;
-  const int t0 = grp * 4, nt = min(4, NTH - t0);
+  const int t0 = grp * TPC, nt = min(TPC, NTH - t0);
   constexpr bool den = kDen != 0;   // compile-time: a predicated-off tcgen05.mma still costs an issue slot
   // tokens per MMA/generation step: 64 (one barrier round trip per 16 MMAs) when the
   // 4 accumulators are 64 columns wide; 32 when they carry the 16 score-sum columns
   constexpr int SUB = den ? 32 : 64, SPS = TOK / SUB, NBk = den ? 3 : 2;
   constexpr int ACC_W = den ? UW : 64;
-  constexpr uint32_t ABASE = den ? 320u : 256u;   // A buffers: NBk x 4 tiles x SUB/2 columns
+  constexpr uint32_t ABASE = TPC * ACC_W;   // A buffers: NBk x TPC tiles x SUB/2 columns (ends at 256)
   const int nsub = g.c / SUB, nstage = g.c / TOK;
 
-  if (w == 2) tmem_alloc<512>(&tmem_base);
+  if (w == 2) tmem_alloc<256>(&tmem_base);
   if (tid == 0) {
     for (int i = 0; i < ST; ++i) {
       mbar_init(&full[i], 1);
@@ -244,7 +245,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1) k_tc_featmajor(const __grid_co
         const uint32_t first = i > 0 ? 1u : 0u;
         for (int t = 0; t < nt; ++t) {
           const uint32_t acc = tm + (uint32_t)(t * ACC_W);
-          const uint32_t ab = tm + ABASE + (uint32_t)((buf * 4 + t) * (SUB / 2));
+          const uint32_t ab = tm + ABASE + (uint32_t)((buf * TPC + t) * (SUB / 2));
 #pragma unroll
           for (int kk = 0; kk < SUB / 16; ++kk) {
             const uint32_t f = kk > 0 ? 1u : first;
@@ -261,11 +262,12 @@ __global__ void __launch_bounds__(fm::THREADS, 1) k_tc_featmajor(const __grid_co
   } else if (w >= 4) {
     // ---------------- A generation (phi'(X~)^T into TMEM) ----------------
     const int q = w & 3, tp = (w - 4) >> 2;   // lane quadrant, tile pair
-    int ra[2], rb[2];
-    bool act[2];
+    constexpr int TPW = TPC / 2;   // tiles per generation warp
+    int ra[TPW], rb[TPW];
+    bool act[TPW];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int t = tp * 2 + u;
+    for (int u = 0; u < TPW; ++u) {
+      const int t = tp * TPW + u;
       act[u] = t < nt;
       const int blk = act[u] ? (t0 + t) * 4 + q : 0;
       ra[u] = 4 * c_blk.al[blk] + (l >> 3);
@@ -278,7 +280,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1) k_tc_featmajor(const __grid_co
       if (i >= NBk) mbar_wait(&aempty[buf], ((i / NBk) + 1) & 1);
       const uint8_t* xs = xt_s + st * XT_B;
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < TPW; ++u) {
         if (act[u]) {
           uint32_t va[SUB / 2], vb[SUB / 2], o[SUB / 2];
 #pragma unroll
@@ -289,7 +291,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1) k_tc_featmajor(const __grid_co
           }
 #pragma unroll
           for (int c = 0; c < SUB / 2; ++c) o[c] = hmul2_f16(va[c], vb[c]);
-          const uint32_t ad = tm + ABASE + (uint32_t)((buf * 4 + tp * 2 + u) * (SUB / 2)) + lane_off;
+          const uint32_t ad = tm + ABASE + (uint32_t)((buf * TPC + tp * TPW + u) * (SUB / 2)) + lane_off;
 #pragma unroll
           for (int c16 = 0; c16 < SUB / 2; c16 += 16) tmem_st16(ad + c16, o + c16);
         }
@@ -304,8 +306,8 @@ __global__ void __launch_bounds__(fm::THREADS, 1) k_tc_featmajor(const __grid_co
     tc_fence_after();
     const int ncols = den ? UW : 64;
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int t = tp * 2 + u;
+    for (int u = 0; u < TPW; ++u) {
+      const int t = tp * TPW + u;
       if (!act[u]) continue;
       float* dst = out + (((size_t)(s * g.nsl + slot) * FH) + (size_t)(t0 + t) * 128 + q * 32 + l) * UW;
       for (int c0 = 0; c0 < ncols; c0 += 16) {
@@ -321,7 +323,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1) k_tc_featmajor(const __grid_co
   }
   tc_fence_before();
   __syncthreads();
-  if (w == 2) tmem_dealloc<512>(tm);
+  if (w == 2) tmem_dealloc<256>(tm);
 }
 
 // ==========================================================================
@@ -1197,7 +1199,7 @@ int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const 
     StageTimer tmr("fwd_update_state", st);
     auto fn = with_den ? k_tc_featmajor<false, 1> : k_tc_featmajor<false, 0>;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, fm::SMEM);
-    fn<<<dim3((NTH + 3) / 4, g.n, g.ns), fm::THREADS, fm::SMEM, st>>>(m_kt, m_vr, m_wa, g, w.sp);
+    fn<<<dim3((NTH + fm::TPC - 1) / fm::TPC, g.n, g.ns), fm::THREADS, fm::SMEM, st>>>(m_kt, m_vr, m_wa, g, w.sp);
   }
   {
     StageTimer tmr("fwd_discumsum", st);
@@ -1275,7 +1277,8 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
     StageTimer tmr("bwd_query_state_dA", st);
     auto fn = den ? k_tc_featmajor<true, 1> : k_tc_featmajor<true, 0>;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, fm::SMEM);
-    fn<<<dim3((NTH + 3) / 4, g.n - 1 + g.prefix, g.ns), fm::THREADS, fm::SMEM, st>>>(m_qt, m_dn, m_dd, g, w.sp);
+    fn<<<dim3((NTH + fm::TPC - 1) / fm::TPC, g.n - 1 + g.prefix, g.ns), fm::THREADS, fm::SMEM, st>>>(m_qt, m_dn,
+                                                                                                 m_dd, g, w.sp);
   }
   if (mode == 1) {
     StageTimer tmr("bwd_discumsum", st);
