@@ -372,26 +372,38 @@ __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
       PA_TR3(trc, 100 + nt * 4 + 2);
       tc_fence_after();
       const uint32_t dt = tm + (uint32_t)(db * 128) + lane_off;
-#pragma unroll 1
-      for (int cb = 0; cb < 4; ++cb) {
-        const int blk = nt * 4 + cb, al = c_blk_d.al[blk], be = c_blk_d.be[blk];
-        uint32_t gr[32];
-        tmem_ld32(dt + (uint32_t)(cb * 32), gr);
-        if (be != cur_be) {
-          flush_b(cur_be);
-          cur_be = be;
-          dxb[0] = dxb[1] = dxb[2] = dxb[3] = ff2{0.f, 0.f};
-          xb0 = x_s[(2 * be) * 128 + row];
-          xb1 = x_s[(2 * be + 1) * 128 + row];
+      // 8 half-blocks (16 columns: a-rows 2hh, 2hh+1 of a 4x8 block); the TMEM load
+      // of half-block u+1 is in flight while u is processed (a load round trip
+      // costs ~130 cycles, tools/tmem_rate.cu)
+      uint32_t gbuf[2][16];
+      tmem_ld16(dt, gbuf[0]);
+      float dxa[4];
+      float4 xa = make_float4(0.f, 0.f, 0.f, 0.f);
+      int al = 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int cb = u >> 1, hh = u & 1;
+        if (hh == 0) {
+          const int blk = nt * 4 + cb, be = c_blk_d.be[blk];
+          al = c_blk_d.al[blk];
+          if (be != cur_be) {
+            flush_b(cur_be);
+            cur_be = be;
+            dxb[0] = dxb[1] = dxb[2] = dxb[3] = ff2{0.f, 0.f};
+            xb0 = x_s[(2 * be) * 128 + row];
+            xb1 = x_s[(2 * be + 1) * 128 + row];
+          }
+          xa = x_s[al * 128 + row];
         }
-        const float4 xa = x_s[al * 128 + row];
         tc_wait_ld();
+        if (u + 1 < 8) tmem_ld16(dt + (uint32_t)((u + 1) * 16), gbuf[(u + 1) & 1]);
+        const uint32_t* gr = gbuf[u & 1];
         const float xav[4] = {xa.x, xa.y, xa.z, xa.w};
         const ff2 xbp[4] = {{xb0.x, xb0.y}, {xb0.z, xb0.w}, {xb1.x, xb1.y}, {xb1.z, xb1.w}};
-        float dxa[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const ff2 xai = {xav[i], xav[i]};
+        for (int i = 0; i < 2; ++i) {
+          const int ia = 2 * hh + i;
+          const ff2 xai = {xav[ia], xav[ia]};
           ff2 t = {0.f, 0.f};
 #pragma unroll
           for (int jp = 0; jp < 4; ++jp) {
@@ -399,14 +411,16 @@ __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
             dxb[jp] = ffma2(gg, xai, dxb[jp]);   // dx[b] += g x[a]
             t = ffma2(gg, xbp[jp], t);           // dx[a] += g x[b]
           }
-          dxa[i] = t.x + t.y;
+          dxa[ia] = t.x + t.y;
         }
-        float4 da = dx_s[al * 128 + row];
-        da.x += dxa[0];
-        da.y += dxa[1];
-        da.z += dxa[2];
-        da.w += dxa[3];
-        dx_s[al * 128 + row] = da;
+        if (hh == 1) {
+          float4 da = dx_s[al * 128 + row];
+          da.x += dxa[0];
+          da.y += dxa[1];
+          da.z += dxa[2];
+          da.w += dxa[3];
+          dx_s[al * 128 + row] = da;
+        }
       }
       PA_TR3(trc, 100 + nt * 4 + 3);
       tc_fence_before();
