@@ -1178,11 +1178,7 @@ int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const 
     }
     {
       StageTimer tmr("fwd_attn_query", st);
-      auto fn = with_den ? k_tc_out<1> : k_tc_out<0>;
-      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, outk::SMEM);
-      fn<<<dim3(g.c / 128, g.n, g.ns), 256, outk::SMEM, st>>>(m_q, m_k, m_v, g, (const __nv_bfloat16*)q, w.ell,
-                                                              w.stm, w.std_, (__nv_bfloat16*)y, rowsum, w.y32,
-                                                              w.zflag);
+      tc_out(g, m_q, m_k, m_v, q, w.ell, w.stm, w.std_, with_den, y, rowsum, w.y32, w.zflag, st);
     }
     count_launch(2);
     return cuda_check("tc forward (sp finish)");
@@ -1212,10 +1208,7 @@ int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const 
   }
   {
     StageTimer tmr("fwd_attn_query", st);
-    auto fn = with_den ? k_tc_out<1> : k_tc_out<0>;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, outk::SMEM);
-    fn<<<dim3(g.c / 128, g.n, g.ns), 256, outk::SMEM, st>>>(m_q, m_k, m_v, g, (const __nv_bfloat16*)q, w.ell, w.stm,
-                                                            w.std_, (__nv_bfloat16*)y, rowsum, w.y32, w.zflag);
+    tc_out(g, m_q, m_k, m_v, q, w.ell, w.stm, w.std_, with_den, y, rowsum, w.y32, w.zflag, st);
   }
   count_launch(5);
   return cuda_check("tc forward");

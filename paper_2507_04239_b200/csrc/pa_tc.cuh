@@ -26,6 +26,11 @@ int tc_sp_combine(const Geo& g, const void* fwd_ws, const float* carry, const fl
                   cudaStream_t st);
 constexpr size_t kSpStateFloatsPerStream = 2304 * 80;
 
+// forward output: intra-chunk attention + state query + combine + normalize (pa_tc_out.cu)
+int tc_out(const Geo& g, const CUtensorMap& m_q, const CUtensorMap& m_k, const CUtensorMap& m_v, const void* q,
+           const float* ell, const __half* st_main, const __half* st_den, int with_den, void* y, float* rowsum,
+           float* y32, int* zflag, cudaStream_t st);
+
 // intra-chunk backward (pa_tc_ib.cu): dK, dV (fp32, =), dQ (fp32, =), dell (+=)
 int tc_intra_bwd(const Geo& g, const CUtensorMap& m_q, const CUtensorMap& m_k, const CUtensorMap& m_v,
                  const CUtensorMap& m_dn, const float* ell, const float* dden, float* dk32, float* dv32,
