@@ -30,6 +30,18 @@ using namespace tc;
 
 static __constant__ BlkTab c_blk_o = make_blk_tab();
 
+#ifdef PA_TRACE
+// debug build only (tools/trace_out.py): clock64 stamps of one CTA
+__device__ long long g_trace4[512];
+extern "C" int pa_debug_trace4(long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_trace4, sizeof(long long) * n);
+}
+#define PA_TR4(c, i) \
+  if (c) g_trace4[(i)] = clock64()
+#else
+#define PA_TR4(c, i)
+#endif
+
 namespace out2 {
 constexpr int QB = 128 * 128;           // Q tile bytes (128 tok x 64 dims bf16)
 constexpr int KB = 128 * 128;           // K tile
@@ -89,6 +101,11 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
   const int bi = s / g.h, hi = s % g.h;
   const int c0 = k * g.c;
   const bool has_state = k >= 1 || g.prefix;   // state before chunk k = slot k
+#ifdef PA_TRACE
+  const bool trb = blockIdx.x == 7 && blockIdx.y == 5 && blockIdx.z == 3;
+#else
+  const bool trb = false;
+#endif
 
   if (w == W_TMEM) tmem_alloc<512>(&tmem_base);
   if (tid == 0) {
@@ -156,10 +173,13 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
         constexpr uint32_t id16mn_h = idesc_f16(128, 16, false, true);
         const uint64_t sm0 = smem_desc(smem_u32(st_s), 8192, 1024, 2);
         const uint64_t sd0 = smem_desc(smem_u32(sd_s), 2048, 256, 6);
+        PA_TR4(trb && mw == 0, 0);
         for (int stp = mw; stp < NSTEP; stp += 2) {
           const int bb = stp & 1, sb = stp % ST_ST;
           mbar_wait(&a_full[bb], (stp >> 1) & 1);
+          PA_TR4(trb, 10 + stp * 3 + 0);
           mbar_wait(&st_full[sb], (stp / ST_ST) & 1);
+          PA_TR4(trb, 10 + stp * 3 + 1);
           tc_fence_after();
           const uint64_t so = (uint64_t)((sb * STB) >> 4), sdo = (uint64_t)((sb * STD) >> 4);
           const uint32_t ab = tm + TA + (uint32_t)(bb * 64);
@@ -171,6 +191,7 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
           }
           tc_commit(&a_empty[bb]);
           tc_commit(&st_empty[sb]);
+          PA_TR4(trb, 10 + stp * 3 + 2);
         }
       }
       tc_commit(a_done);
@@ -202,7 +223,9 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
       for (int J = 0; J <= I; ++J) {
         if (NSB == 2 && J + 1 <= I) issue_s(J + 1);
         const int sb = J % NSB, st = J % KV_ST;
+        PA_TR4(trb, 100 + J * 3 + 0);
         mbar_wait(&p_full[sb], (J / NSB) & 1);
+        PA_TR4(trb, 100 + J * 3 + 1);
         tc_fence_after();
         const uint64_t vo = (uint64_t)((st * VB) >> 4);
         const uint32_t pb = tm + TSP + (uint32_t)(sb * 128);
@@ -214,6 +237,7 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
         }
         tc_commit(&pv_done[sb]);
         tc_commit(&kv_empty[st]);
+        PA_TR4(trb, 100 + J * 3 + 2);
         if (NSB == 1 && J + 1 <= I) issue_s(J + 1);
       }
       tc_commit(fin);
@@ -252,7 +276,9 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
 #pragma unroll 1
       for (int stp = 0; stp < NSTEP; ++stp) {
         const int bb = stp & 1;
+        PA_TR4(trb && w == 0 && l == 0, 200 + stp * 2 + 0);
         if (stp >= 2) mbar_wait(&a_empty[bb], ((stp >> 1) + 1) & 1);
+        PA_TR4(trb && w == 0 && l == 0, 200 + stp * 2 + 1);
         const uint32_t ab = tm + TA + (uint32_t)(bb * 64) + lane_off;
 #pragma unroll
         for (int f = 0; f < 4; ++f) {
@@ -276,8 +302,11 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
       }
     }
     // ---------------- epilogue: y = cm O_state + O_intra -------------------------
+    PA_TR4(trb && w == 0 && l == 0, 300);
     if (has_state) mbar_wait(a_done, 0);
+    PA_TR4(trb && w == 0 && l == 0, 301);
     mbar_wait(fin, 0);
+    PA_TR4(trb && w == 0 && l == 0, 302);
     tc_fence_after();
     const float cm = has_state ? sig2 * __expf(li) / pow2_neg_bits(g.k0 + k - 1) : 0.f;  // undo the slot scale
     uint32_t oi[64];
@@ -338,7 +367,9 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
       const float lref = ell_s[J * 128 + 127];
       cj[cb * 128 + row] = diag ? ell_s[J * 128 + row] : __expf(lref - ell_s[J * 128 + row]);
       asm volatile("bar.sync 1, 128;" ::: "memory");
+      PA_TR4(trb && w == 4 && l == 0, 400 + J * 3 + 0);
       mbar_wait(&s_full[sb], (J / NSB) & 1);
+      PA_TR4(trb && w == 4 && l == 0, 400 + J * 3 + 1);
       tc_fence_after();
       const float ri = __expf(li - lref) * sig2;
       const float* cjs = cj + cb * 128;
@@ -380,6 +411,7 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
         tmem_st16(sp + ch * 16, pk);
       }
       tc_wait_st();
+      PA_TR4(trb && w == 4 && l == 0, 400 + J * 3 + 2);
       tc_fence_before();
       __syncwarp();
       if (l == 0) mbar_arrive(&p_full[sb]);
