@@ -42,6 +42,15 @@ extern "C" int pa_debug_trace4(long long* host, int n) {
 #define PA_TR4(c, i)
 #endif
 
+struct of2 {
+  float x, y;
+};
+__device__ __forceinline__ of2 omul2(of2 a, of2 b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(*(uint64_t*)&a), "l"(*(uint64_t*)&b));
+  return *(of2*)&r;
+}
+
 namespace out2 {
 constexpr int QB = 128 * 128;           // Q tile bytes (128 tok x 64 dims bf16)
 constexpr int KB = 128 * 128;           // K tile
@@ -380,14 +389,17 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
         tmem_ld32(sp + ch * 32, r);
         tc_wait_ld();
         if (!diag) {
+          // P = r_i c_j s^2 in packed f32x2 arithmetic (3 FMUL2 per pair)
+          const of2 ri2 = {ri, ri};
 #pragma unroll
           for (int e4 = 0; e4 < 8; ++e4) {
             const float4 c4 = *(const float4*)(cjs + ch * 32 + e4 * 4);
-            const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
 #pragma unroll
-            for (int z = 0; z < 4; z += 2) {
-              const float s0 = __uint_as_float(r[e4 * 4 + z]), s1 = __uint_as_float(r[e4 * 4 + z + 1]);
-              pk[e4 * 2 + z / 2] = pack_bf16(ri * cc[z] * s0 * s0, ri * cc[z + 1] * s1 * s1);
+            for (int z = 0; z < 2; ++z) {
+              const of2 sv = {__uint_as_float(r[e4 * 4 + 2 * z]), __uint_as_float(r[e4 * 4 + 2 * z + 1])};
+              const of2 cc = z ? of2{c4.z, c4.w} : of2{c4.x, c4.y};
+              const of2 pv = omul2(omul2(omul2(sv, sv), cc), ri2);
+              pk[e4 * 2 + z] = pack_bf16(pv.x, pv.y);
             }
           }
         } else {
