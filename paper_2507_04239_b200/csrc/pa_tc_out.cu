@@ -383,11 +383,14 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
       const float ri = __expf(li - lref) * sig2;
       const float* cjs = cj + cb * 128;
       const uint32_t sp = tm + TSP + (uint32_t)(sb * 128) + lane_off;
+      uint32_t rb[2][32];
+      tmem_ld32(sp, rb[0]);
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
-        uint32_t r[32], pk[16];
-        tmem_ld32(sp + ch * 32, r);
+        uint32_t pk[16];
         tc_wait_ld();
+        if (ch + 1 < 4) tmem_ld32(sp + (ch + 1) * 32, rb[(ch + 1) & 1]);   // next chunk in flight
+        const uint32_t* r = rb[ch & 1];
         if (!diag) {
           // P = r_i c_j s^2 in packed f32x2 arithmetic (3 FMUL2 per pair)
           const of2 ri2 = {ri, ri};
