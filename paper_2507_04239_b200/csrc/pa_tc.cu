@@ -64,27 +64,32 @@ __global__ void __launch_bounds__(128) k_tc_prep_gates(Geo g, const float* __res
 // X^T [((s*n + k)*64 + dim)][tok] (fp16, exact copy of the bf16 input) for the
 // feature-major GEMMs, 64-token x 64-dim tiles: 16-byte loads of token rows,
 // transpose through shared memory, 16-byte stores of dim rows.
-__global__ void __launch_bounds__(256) k_tc_prep_xt(Geo g, const __nv_bfloat16* __restrict__ x, __half* xt) {
-  constexpr int P = 72;                       // row pitch in halves (144 B: 16-byte aligned, spreads banks)
-  __shared__ __align__(16) __half tile[64 * P];
+__global__ void __launch_bounds__(256) k_tc_prep_xt(Geo g, const __nv_bfloat16* __restrict__ x,
+                                                    __half* __restrict__ xt) {
+  // token pairs packed as half2 in a [64 dims][33] u32 tile: odd pitch keeps the
+  // transposed writes at most 2-way bank conflicted and the reads conflict-free
+  __shared__ uint32_t tile[64 * 33];
   const int tb = blockIdx.x, k = blockIdx.y, s = blockIdx.z;
   const int j0 = k * g.c + tb * 64;
+  {
+    const int p = threadIdx.x >> 3, c8 = threadIdx.x & 7;   // tokens 2p, 2p+1; dims 8 c8 .. 8 c8 + 7
+    const uint4 a4 = *(const uint4*)(x + rowid(g, s, j0 + 2 * p) * HD + c8 * 8);
+    const uint4 b4 = *(const uint4*)(x + rowid(g, s, j0 + 2 * p + 1) * HD + c8 * 8);
+    const __nv_bfloat16* ea = (const __nv_bfloat16*)&a4;
+    const __nv_bfloat16* eb = (const __nv_bfloat16*)&b4;
 #pragma unroll
-  for (int it = 0; it < 2; ++it) {
-    const int i = threadIdx.x + it * 256;     // 512 = 64 tokens x 8 chunks of 8 dims
-    const int r = i >> 3, c8 = i & 7;
-    const uint4 v4 = *(const uint4*)(x + rowid(g, s, j0 + r) * HD + c8 * 8);
-    const __nv_bfloat16* e = (const __nv_bfloat16*)&v4;
-#pragma unroll
-    for (int z = 0; z < 8; ++z) tile[(c8 * 8 + z) * P + r] = __float2half_rn(__bfloat162float(e[z]));
+    for (int z = 0; z < 8; ++z)
+      tile[(c8 * 8 + z) * 33 + p] = pack_f16(__bfloat162float(ea[z]), __bfloat162float(eb[z]));
   }
   __syncthreads();
-  __half* dst = xt + ((size_t)(s * g.n + k) * HD) * g.c + tb * 64;
+  {
+    const int dim = threadIdx.x >> 2, qq = threadIdx.x & 3;   // 16 tokens (8 pairs) per thread
+    uint32_t v[8];
 #pragma unroll
-  for (int it = 0; it < 2; ++it) {
-    const int i = threadIdx.x + it * 256;     // 64 dims x 8 chunks of 8 tokens
-    const int dim = i >> 3, c8 = i & 7;
-    *(uint4*)(dst + (size_t)dim * g.c + c8 * 8) = *(const uint4*)&tile[dim * P + c8 * 8];
+    for (int j = 0; j < 8; ++j) v[j] = tile[dim * 33 + qq * 8 + j];
+    __half* dst = xt + ((size_t)(s * g.n + k) * HD + dim) * g.c + tb * 64 + qq * 16;
+    *(uint4*)dst = make_uint4(v[0], v[1], v[2], v[3]);
+    *(uint4*)(dst + 8) = make_uint4(v[4], v[5], v[6], v[7]);
   }
 }
 
@@ -98,8 +103,8 @@ __global__ void __launch_bounds__(256) k_tc_prep_xt(Geo g, const __nv_bfloat16* 
 __global__ void __launch_bounds__(256) k_tc_prep_rows(Geo g, int mode, const __nv_bfloat16* __restrict__ src,
                                                       const float* __restrict__ ell,
                                                       const float* __restrict__ lamlog,
-                                                      const float* __restrict__ dden, __half* rows,
-                                                      __half* aux) {
+                                                      const float* __restrict__ dden, __half* __restrict__ rows,
+                                                      __half* __restrict__ aux) {
   const size_t it = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (it >= (size_t)g.ns * g.t) return;
   const int s = (int)(it / g.t), m = (int)(it - (size_t)s * g.t);
@@ -117,9 +122,12 @@ __global__ void __launch_bounds__(256) k_tc_prep_rows(Geo g, int mode, const __n
   }
   const uint4* in = (const uint4*)row;
   uint4* out = (uint4*)(rows + it * HD);
+  uint4 vin[8];
+#pragma unroll
+  for (int c8 = 0; c8 < 8; ++c8) vin[c8] = __ldcs(in + c8);   // all loads in flight first
 #pragma unroll
   for (int c8 = 0; c8 < 8; ++c8) {
-    uint4 v4 = in[c8];
+    uint4 v4 = vin[c8];
     uint32_t* pv = (uint32_t*)&v4;
 #pragma unroll
     for (int e2 = 0; e2 < 4; ++e2) {
