@@ -63,13 +63,18 @@ __host__ __device__ constexpr int slot_b(int f, const BlkTab& t) { return 8 * t.
 // states carry a per-chunk power-of-two scale so long ungated sums stay in
 // range: A'_k is stored as A'_k * 2^-nbits(k), the backward state cotangent
 // G_k as G_k * 2^-nbits(n-1-k).
-__host__ __device__ inline float pow2_neg_bits(int k) {  // 2^-(number of bits of k)
+__host__ __device__ inline float pow2_neg_bits(int k) {  // 2^-(number of bits of k), k >= 0
+#ifdef __CUDA_ARCH__
+  const int e = 32 - __clz(k);
+  return __int_as_float((127 - e) << 23);
+#else
   int e = 0;
   while (k) {
     ++e;
     k >>= 1;
   }
   return 1.f / (float)(1 << e);
+#endif
 }
 
 // ---------------------------------------------------------------- generation
