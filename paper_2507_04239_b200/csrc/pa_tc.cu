@@ -207,13 +207,13 @@ __global__ void __launch_bounds__(fm::THREADS, 2) k_tc_featmajor(const __grid_co
   if (tid == 0) {
     for (int i = 0; i < ST; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&empty[i], SPS);   // every step of the stage (either issuer) commits
     }
     for (int i = 0; i < NBk; ++i) {
       mbar_init(&afull[i], GEN_WARPS);
       mbar_init(&aempty[i], 1);
     }
-    mbar_init(fin, 1);
+    mbar_init(fin, 2);
     fence_barrier_init();
   }
   fence_async_smem();
@@ -238,32 +238,33 @@ __global__ void __launch_bounds__(fm::THREADS, 2) k_tc_featmajor(const __grid_co
         if (den) tma_load_2d(b16_s + st * B16_B, &tm_b16, &full[st], 0, s * g.t + kin * g.c + j * TOK);
       }
     }
-  } else if (w == 1) {
-    // ---------------- MMA issuer ----------------
+  } else if (w == 1 || w == 3) {
+    // ---------------- MMA issuers: w1 even steps, w3 odd steps ----------------
+    // (each barrier round trip costs ~160 cycles; two issuers overlap them and
+    // accumulate into the zero-initialised accumulators)
     if (l == 0) {
+      const int mw = w >> 1;
       const uint32_t id64 = idesc_f16(128, 64, false, true);
       const uint32_t id16 = idesc_f16(128, 16, false, true);
       const uint64_t bn0 = smem_desc(smem_u32(b_s), 8192, 1024, 2);
       const uint64_t b160 = smem_desc(smem_u32(b16_s), 512, 256, 6);
-      for (int i = 0; i < nsub; ++i) {
+      for (int i = mw; i < nsub; i += 2) {
         const int j = i / SPS, h = i % SPS, st = j % ST, buf = i % NBk;
         mbar_wait(&full[st], (j / ST) & 1);
         mbar_wait(&afull[buf], (i / NBk) & 1);
         tc_fence_after();
-        const uint32_t first = i > 0 ? 1u : 0u;
         for (int t = 0; t < nt; ++t) {
           const uint32_t acc = tm + (uint32_t)(t * ACC_W);
           const uint32_t ab = tm + ABASE + (uint32_t)((buf * TPC + t) * (SUB / 2));
 #pragma unroll
           for (int kk = 0; kk < SUB / 16; ++kk) {
-            const uint32_t f = kk > 0 ? 1u : first;
             const int trow = h * SUB + kk * 16;   // token row inside the 64-token stage
-            mma_ts(acc, ab + kk * 8, bn0 + (uint64_t)((st * B_B + trow * 128) >> 4), id64, f);
-            if (den) mma_ts(acc + 64, ab + kk * 8, b160 + (uint64_t)((st * B16_B + trow * 32) >> 4), id16, f);
+            mma_ts(acc, ab + kk * 8, bn0 + (uint64_t)((st * B_B + trow * 128) >> 4), id64, 1u);
+            if (den) mma_ts(acc + 64, ab + kk * 8, b160 + (uint64_t)((st * B16_B + trow * 32) >> 4), id16, 1u);
           }
         }
         tc_commit(&aempty[buf]);
-        if (h == SPS - 1) tc_commit(&empty[st]);
+        tc_commit(&empty[st]);
       }
       tc_commit(fin);
     }
@@ -282,6 +283,15 @@ __global__ void __launch_bounds__(fm::THREADS, 2) k_tc_featmajor(const __grid_co
       rb[u] = 8 * c_blk.be[blk] + (l & 7);
     }
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    {
+      uint32_t z[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) z[c] = 0u;
+#pragma unroll
+      for (int u = 0; u < TPW; ++u)
+        if (act[u])
+          for (int c = 0; c < ACC_W; c += 16) tmem_st16(tm + (uint32_t)((tp * TPW + u) * ACC_W + c) + lane_off, z);
+    }
     for (int i = 0; i < nsub; ++i) {
       const int j = i / SPS, h = i % SPS, st = j % ST, buf = i % NBk;
       mbar_wait(&full[st], (j / ST) & 1);
