@@ -34,6 +34,18 @@ using namespace tc;
 
 __constant__ BlkTab c_blk = make_blk_tab();
 
+#ifdef PA_TRACE
+// debug build only (tools/trace_fm.py): clock64 stamps of one feature-major CTA
+__device__ long long g_trace5[1024];
+extern "C" int pa_debug_trace5(long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_trace5, sizeof(long long) * n);
+}
+#define PA_TR5(c, i) \
+  if (c) g_trace5[(i)] = clock64()
+#else
+#define PA_TR5(c, i)
+#endif
+
 
 // ==========================================================================
 // prep kernels
@@ -248,10 +260,16 @@ __global__ void __launch_bounds__(fm::THREADS, 2) k_tc_featmajor(const __grid_co
       const uint32_t id16 = idesc_f16(128, 16, false, true);
       const uint64_t bn0 = smem_desc(smem_u32(b_s), 8192, 1024, 2);
       const uint64_t b160 = smem_desc(smem_u32(b16_s), 512, 256, 6);
+#ifdef PA_TRACE
+      const bool trm = !kBwd && blockIdx.x == 3 && blockIdx.y == 5 && blockIdx.z == 3;
+#endif
+      PA_TR5(trm && mw == 0, 0);
       for (int i = mw; i < nsub; i += 2) {
         const int j = i / SPS, h = i % SPS, st = j % ST, buf = i % NBk;
         mbar_wait(&full[st], (j / ST) & 1);
+        PA_TR5(trm, 8 + i * 4 + 0);
         mbar_wait(&afull[buf], (i / NBk) & 1);
+        PA_TR5(trm, 8 + i * 4 + 1);
         tc_fence_after();
         for (int t = 0; t < nt; ++t) {
           const uint32_t acc = tm + (uint32_t)(t * ACC_W);
@@ -265,6 +283,7 @@ __global__ void __launch_bounds__(fm::THREADS, 2) k_tc_featmajor(const __grid_co
         }
         tc_commit(&aempty[buf]);
         tc_commit(&empty[st]);
+        PA_TR5(trm, 8 + i * 4 + 2);
       }
       tc_commit(fin);
     }
@@ -292,10 +311,16 @@ __global__ void __launch_bounds__(fm::THREADS, 2) k_tc_featmajor(const __grid_co
         if (act[u])
           for (int c = 0; c < ACC_W; c += 16) tmem_st16(tm + (uint32_t)((tp * TPW + u) * ACC_W + c) + lane_off, z);
     }
+#ifdef PA_TRACE
+    const bool trg = !kBwd && blockIdx.x == 3 && blockIdx.y == 5 && blockIdx.z == 3 && w == 4 && l == 0;
+#endif
     for (int i = 0; i < nsub; ++i) {
       const int j = i / SPS, h = i % SPS, st = j % ST, buf = i % NBk;
+      PA_TR5(trg, 200 + i * 4 + 0);
       mbar_wait(&full[st], (j / ST) & 1);
+      PA_TR5(trg, 200 + i * 4 + 1);
       if (i >= NBk) mbar_wait(&aempty[buf], ((i / NBk) + 1) & 1);
+      PA_TR5(trg, 200 + i * 4 + 2);
       const uint8_t* xs = xt_s + st * XT_B;
 #pragma unroll
       for (int u = 0; u < TPW; ++u) {
@@ -315,12 +340,15 @@ __global__ void __launch_bounds__(fm::THREADS, 2) k_tc_featmajor(const __grid_co
         }
       }
       tc_wait_st();
+      PA_TR5(trg, 200 + i * 4 + 3);
       tc_fence_before();
       __syncwarp();
       if (l == 0) mbar_arrive(&afull[buf]);
     }
     // ---------------- epilogue ----------------
+    PA_TR5(trg, 190);
     mbar_wait(fin, 0);
+    PA_TR5(trg, 191);
     tc_fence_after();
     const int ncols = den ? UW : 64;
 #pragma unroll
@@ -339,6 +367,7 @@ __global__ void __launch_bounds__(fm::THREADS, 2) k_tc_featmajor(const __grid_co
       }
     }
   }
+  PA_TR5(!kBwd && blockIdx.x == 3 && blockIdx.y == 5 && blockIdx.z == 3 && tid == 128, 192);
   tc_fence_before();
   __syncthreads();
   if (w == 2) tmem_dealloc<256>(tm);
