@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(fm::THREADS, 2) k_tc_featmajor(const __grid_co
     // ---------------- MMA issuers: w1 even steps, w3 odd steps ----------------
     // (each barrier round trip costs ~160 cycles; two issuers overlap them and
     // accumulate into the zero-initialised accumulators)
-    if (l == 0) {
+    {
       const int mw = w >> 1;
       const uint32_t id64 = idesc_f16(128, 64, false, true);
       const uint32_t id16 = idesc_f16(128, 16, false, true);
@@ -266,9 +266,9 @@ __global__ void __launch_bounds__(fm::THREADS, 2) k_tc_featmajor(const __grid_co
       PA_TR5(trm && mw == 0, 0);
       for (int i = mw; i < nsub; i += 2) {
         const int j = i / SPS, h = i % SPS, st = j % ST, buf = i % NBk;
-        mbar_wait(&full[st], (j / ST) & 1);
+        mbar_wait_w(&full[st], (j / ST) & 1);
         PA_TR5(trm, 8 + i * 4 + 0);
-        mbar_wait(&afull[buf], (i / NBk) & 1);
+        mbar_wait_w(&afull[buf], (i / NBk) & 1);
         PA_TR5(trm, 8 + i * 4 + 1);
         tc_fence_after();
         for (int t = 0; t < nt; ++t) {
@@ -277,15 +277,15 @@ __global__ void __launch_bounds__(fm::THREADS, 2) k_tc_featmajor(const __grid_co
 #pragma unroll
           for (int kk = 0; kk < SUB / 16; ++kk) {
             const int trow = h * SUB + kk * 16;   // token row inside the 64-token stage
-            mma_ts(acc, ab + kk * 8, bn0 + (uint64_t)((st * B_B + trow * 128) >> 4), id64, 1u);
-            if (den) mma_ts(acc + 64, ab + kk * 8, b160 + (uint64_t)((st * B16_B + trow * 32) >> 4), id16, 1u);
+            mma_ts_w(acc, ab + kk * 8, bn0 + (uint64_t)((st * B_B + trow * 128) >> 4), id64, 1u);
+            if (den) mma_ts_w(acc + 64, ab + kk * 8, b160 + (uint64_t)((st * B16_B + trow * 32) >> 4), id16, 1u);
           }
         }
-        tc_commit(&aempty[buf]);
-        tc_commit(&empty[st]);
+        tc_commit_w(&aempty[buf]);
+        tc_commit_w(&empty[st]);
         PA_TR5(trm, 8 + i * 4 + 2);
       }
-      tc_commit(fin);
+      tc_commit_w(fin);
     }
   } else if (w >= 4) {
     // ---------------- A generation (phi'(X~)^T into TMEM) ----------------
@@ -470,408 +470,6 @@ __global__ void __launch_bounds__(256) k_tc_sp_combine(Geo g, const float* __res
     *(float4*)(out + base + 4 * i) =
         make_float4(fmaf(lam, c4.x, l4.x), fmaf(lam, c4.y, l4.y), fmaf(lam, c4.z, l4.z), fmaf(lam, c4.w, l4.w));
   }
-}
-
-// ==========================================================================
-// out: fused intra-chunk power attention + state query + combine + normalize
-// (attention.py:273-309 per chunk, kernels.py:86-110, chunked.py:372-395)
-// Warp roles (256 threads): w0 loads (TMA Q/K/V, bulk state blocks), w1 MMA
-// issuer, w2 TMEM owner, w4..w7 compute (phi'(q~) generation, P = decay*s^2,
-// epilogue).  TMEM: O [0,80), A buffers [128,256), S/P buffers [256,512).
-// grid (query tile of 128, chunk, stream)
-// ==========================================================================
-namespace outk {
-constexpr int QB = 128 * 128;           // Q tile bytes (128 tok x 64 dims bf16)
-constexpr int KB = 128 * 128;           // K tile
-constexpr int VB = 128 * 128;           // V tile
-// state query in steps of 128 slots (2 K-blocks): one barrier round trip per
-// 8 MMAs (each wait costs ~160 cycles even when the phase is complete)
-constexpr int STB = 128 * 128;          // state step: 128 slots x 64 values
-constexpr int STD = 128 * 32;           // state step score-sum part
-constexpr int NSTEP = NKB / 2;          // 18
-constexpr int KV_ST = 3;
-constexpr int ST_ST = 4;
-constexpr int NA = 2;                   // TMEM A buffers (128 slots = 64 columns each)
-constexpr int XH = 8 * 128 * 16;        // fp16 q rows, thread-private uint4 columns
-constexpr int SMEM = 1024 + QB + KV_ST * (KB + VB) + ST_ST * (STB + STD) + XH + 2048 + 4096 + 1024 + 512;
-}  // namespace outk
-
-// phi'(x) for the 2304 slots in 18 steps of 128 slots (4 feature blocks, 64
-// TMEM columns), alternating over 2 TMEM A buffers.  x is this thread's row as
-// fp16 pairs in shared memory ([8][128] uint4, thread-private columns), so the
-// loop body is one copy of the code with runtime block indices (the per-block
-// unrolled version was ~40 KB of SASS and stalled on instruction fetch).
-__device__ __forceinline__ void gen_steps(const uint4* xh_s, int row, uint32_t a_base, uint32_t lane_off,
-                                          uint64_t* a_full, uint64_t* a_empty, int l) {
-#pragma unroll 1
-  for (int stp = 0; stp < NKB / 2; ++stp) {
-    const int bb = stp & 1;
-    if (stp >= 2) mbar_wait(&a_empty[bb], ((stp >> 1) + 1) & 1);
-    const uint32_t ab = a_base + (uint32_t)(bb * 64) + lane_off;
-#pragma unroll
-    for (int f = 0; f < 4; ++f) {
-      const int blk = stp * 4 + f, al = c_blk.al[blk], be = c_blk.be[blk];
-      const uint2 xa = *(const uint2*)((const uint32_t*)&xh_s[(al >> 1) * 128 + row] + (al & 1) * 2);
-      const uint4 xb = xh_s[be * 128 + row];
-      const uint32_t xbv[4] = {xb.x, xb.y, xb.z, xb.w};
-      const uint32_t bc[4] = {__byte_perm(xa.x, 0, 0x1010), __byte_perm(xa.x, 0, 0x3232),
-                              __byte_perm(xa.y, 0, 0x1010), __byte_perm(xa.y, 0, 0x3232)};
-      uint32_t o[16];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int jp = 0; jp < 4; ++jp) o[i * 4 + jp] = hmul2_f16(bc[i], xbv[jp]);
-      tmem_st16(ab + (uint32_t)(f * 16), o);
-    }
-    tc_wait_st();
-    tc_fence_before();
-    __syncwarp();
-    if (l == 0) mbar_arrive(&a_full[bb]);
-  }
-}
-
-// a bf16 row of 64 as fp16 pairs (exact for |x| < 65504)
-__device__ __forceinline__ void load_row_f16(const __nv_bfloat16* src, uint32_t (&xp)[32]) {
-  const uint4* row = (const uint4*)src;
-#pragma unroll
-  for (int c8 = 0; c8 < 8; ++c8) {
-    uint4 v4 = row[c8];
-    const uint32_t* pv = (const uint32_t*)&v4;
-#pragma unroll
-    for (int e2 = 0; e2 < 4; ++e2) {
-      float2 f2 = __bfloat1622float2(*(const __nv_bfloat162*)&pv[e2]);
-      xp[c8 * 4 + e2] = pack_f16(f2.x, f2.y);
-    }
-  }
-}
-
-__device__ __forceinline__ void load_scaled_row(const __nv_bfloat16* src, float f, uint32_t (&xp)[32]) {
-  const uint4* row = (const uint4*)src;
-#pragma unroll
-  for (int c8 = 0; c8 < 8; ++c8) {
-    uint4 v4 = row[c8];
-    const uint32_t* pv = (const uint32_t*)&v4;
-#pragma unroll
-    for (int e2 = 0; e2 < 4; ++e2) {
-      float2 f2 = __bfloat1622float2(*(const __nv_bfloat162*)&pv[e2]);
-      xp[c8 * 4 + e2] = pack_bf16(f2.x * f, f2.y * f);
-    }
-  }
-}
-
-template <int kDen>
-__global__ void __launch_bounds__(256, 1) k_tc_out(const __grid_constant__ CUtensorMap tm_q,
-                                                   const __grid_constant__ CUtensorMap tm_k,
-                                                   const __grid_constant__ CUtensorMap tm_v, Geo g,
-                                                   const __nv_bfloat16* __restrict__ qraw,
-                                                   const float* __restrict__ ell,
-                                                   const __half* __restrict__ st_main,
-                                                   const __half* __restrict__ st_den,
-                                                   __nv_bfloat16* y, float* rowsum, float* y32, int* zflag) {
-  using namespace outk;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* q_s = smem;
-  uint8_t* k_s = q_s + QB;
-  uint8_t* v_s = k_s + KV_ST * KB;
-  uint8_t* st_s = v_s + KV_ST * VB;
-  uint8_t* sd_s = st_s + ST_ST * STB;
-  uint4* xh_s = (uint4*)(sd_s + ST_ST * STD);
-  uint8_t* ones = (uint8_t*)(xh_s + 8 * 128);
-  float* ell_s = (float*)(ones + 2048);       // [1024]
-  float* cj = ell_s + 1024;                   // [2][128]
-  uint64_t* bars = (uint64_t*)(cj + 256);
-  uint64_t* q_full = bars;                    // 1
-  uint64_t* kv_full = q_full + 1;             // KV_ST
-  uint64_t* kv_empty = kv_full + KV_ST;       // KV_ST
-  uint64_t* st_full = kv_empty + KV_ST;       // ST_ST
-  uint64_t* st_empty = st_full + ST_ST;       // ST_ST
-  uint64_t* a_full = st_empty + ST_ST;        // NA
-  uint64_t* a_empty = a_full + NA;            // NA
-  uint64_t* s_full = a_empty + NA;            // 2
-  uint64_t* p_full = s_full + 2;              // 2
-  uint64_t* pv_done = p_full + 2;             // 2
-  uint64_t* fin = pv_done + 2;                // 1
-  uint64_t* a_done = fin + 1;                 // 1  (all state-query MMAs complete)
-  uint64_t* o_ready = a_done + 1;             // 1  (state rows rescaled by the compute warps)
-  __shared__ uint32_t tmem_base;
-
-  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
-  const int I = blockIdx.x, k = blockIdx.y, s = blockIdx.z;
-  const int bi = s / g.h, hi = s % g.h;
-  const int c0 = k * g.c;
-  constexpr bool den = kDen != 0;
-  const bool has_state = k >= 1 || g.prefix;   // state before chunk k = slot k
-
-  if (w == 2) tmem_alloc<512>(&tmem_base);
-  if (tid == 0) {
-    mbar_init(q_full, 1);
-    for (int i = 0; i < KV_ST; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
-    }
-    for (int i = 0; i < ST_ST; ++i) {
-      mbar_init(&st_full[i], 1);
-      mbar_init(&st_empty[i], 1);
-    }
-    for (int i = 0; i < NA; ++i) {
-      mbar_init(&a_full[i], 4);
-      mbar_init(&a_empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 4);
-      mbar_init(&pv_done[i], 1);
-    }
-    mbar_init(fin, 1);
-    mbar_init(a_done, 1);
-    mbar_init(o_ready, 4);
-    fence_barrier_init();
-  }
-  for (int i = tid; i < 2048 / 4; i += 256) ((uint32_t*)ones)[i] = (i < 32) ? 0x3F803F80u : 0u;
-  for (int i = tid; i < g.c; i += 256) ell_s[i] = ell[(size_t)s * g.t + c0 + i];
-  fence_async_smem();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tm = tmem_base;
-  const uint32_t a_base = tm + 128u;
-  auto sbuf = [&](int b) { return tm + 256u + (uint32_t)(b * 128); };
-
-  if (w == 0) {
-    // ---------------- loads ----------------
-    if (l == 0) {
-      tma_prefetch(&tm_q);
-      tma_prefetch(&tm_k);
-      tma_prefetch(&tm_v);
-      mbar_expect_tx(q_full, QB);
-      tma_load_4d(q_s, &tm_q, q_full, 0, hi, c0 + I * 128, bi);
-      auto kv = [&](int J) {
-        const int st = J % KV_ST;
-        if (J >= KV_ST) mbar_wait(&kv_empty[st], ((J / KV_ST) + 1) & 1);
-        mbar_expect_tx(&kv_full[st], KB + VB);
-        tma_load_4d(k_s + st * KB, &tm_k, &kv_full[st], 0, hi, c0 + J * 128, bi);
-        tma_load_4d(v_s + st * VB, &tm_v, &kv_full[st], 0, hi, c0 + J * 128, bi);
-      };
-      const int early = min(I + 1, KV_ST);
-      for (int J = 0; J < early; ++J) kv(J);
-      if (has_state) {
-        const __half* srcm = st_main + (size_t)(s * g.nsl + k) * ST_MAIN;
-        const __half* srcd = st_den + (size_t)(s * g.nsl + k) * ST_DEN;
-        for (int stp = 0; stp < NSTEP; ++stp) {
-          const int sb = stp % ST_ST;
-          if (stp >= ST_ST) mbar_wait(&st_empty[sb], ((stp / ST_ST) + 1) & 1);
-          mbar_expect_tx(&st_full[sb], STB + (den ? STD : 0));
-          bulk_load(st_s + sb * STB, srcm + (size_t)stp * 128 * 64, STB, &st_full[sb]);
-          if (den) bulk_load(sd_s + sb * STD, srcd + (size_t)stp * 128 * 16, STD, &st_full[sb]);
-        }
-      }
-      for (int J = early; J <= I; ++J) kv(J);
-    }
-  } else if (w == 1) {
-    // ---------------- MMA issuer ----------------
-    if (l == 0) {
-      const uint32_t id64mn = idesc_bf16(128, 64, false, true);     // P V (bf16)
-      const uint32_t id64mn_h = idesc_f16(128, 64, false, true);    // phi'(q) A' (fp16)
-      const uint32_t id16mn_h = idesc_f16(128, 16, false, true);
-      const uint32_t id16k = idesc_bf16(128, 16, false, false);
-      const uint32_t id128 = idesc_bf16(128, 128, false, false);
-      if (has_state) {
-        const uint64_t sm0 = smem_desc(smem_u32(st_s), 8192, 1024, 2);
-        const uint64_t sd0 = smem_desc(smem_u32(sd_s), 2048, 256, 6);
-        for (int stp = 0; stp < NSTEP; ++stp) {
-          const int bb = stp % NA, sb = stp % ST_ST;
-          mbar_wait(&a_full[bb], (stp / NA) & 1);
-          mbar_wait(&st_full[sb], (stp / ST_ST) & 1);
-          tc_fence_after();
-          const uint64_t so = (uint64_t)((sb * STB) >> 4), sdo = (uint64_t)((sb * STD) >> 4);
-          const uint32_t ab = a_base + (uint32_t)(bb * 64);
-          const uint32_t first = stp > 0 ? 1u : 0u;
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {   // 16 slots per MMA: 2048 B of [slot][64] rows, 512 B of [slot][16]
-            const uint32_t f = kk > 0 ? 1u : first;
-            mma_ts(tm, ab + kk * 8, sm0 + so + (uint64_t)(kk * 128), id64mn_h, f);
-            if (den) mma_ts(tm + 64, ab + kk * 8, sd0 + sdo + (uint64_t)(kk * 32), id16mn_h, f);
-          }
-          tc_commit(&a_empty[bb]);
-          tc_commit(&st_empty[sb]);
-        }
-        tc_commit(a_done);
-      }
-      mbar_wait(q_full, 0);
-      auto issue_s = [&](int J) {
-        const int st = J % KV_ST, sb = J & 1;
-        mbar_wait(&kv_full[st], (J / KV_ST) & 1);
-        if (J >= 2) mbar_wait(&pv_done[sb], ((J >> 1) + 1) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          mma_ss(sbuf(sb), smem_desc(smem_u32(q_s) + kk * 32, 16, 1024, 2),
-                 smem_desc(smem_u32(k_s + st * KB) + kk * 32, 16, 1024, 2), id128, kk > 0 ? 1u : 0u);
-        tc_commit(&s_full[sb]);
-      };
-      issue_s(0);
-      if (has_state) mbar_wait(o_ready, 0);   // O holds the rescaled state query before P V accumulates
-      for (int J = 0; J <= I; ++J) {
-        if (J + 1 <= I) issue_s(J + 1);
-        const int sb = J & 1, st = J % KV_ST;
-        mbar_wait(&p_full[sb], (J >> 1) & 1);
-        tc_fence_after();
-        const uint32_t vb = smem_u32(v_s + st * VB);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t f = (has_state || J > 0 || kk > 0) ? 1u : 0u;
-          mma_ts(tm, sbuf(sb) + kk * 8, smem_desc(vb + kk * 2048, 8192, 1024, 2), id64mn, f);
-          if (den)
-            mma_ts(tm + 64, sbuf(sb) + kk * 8, smem_desc(smem_u32(ones) + (kk & 3) * 32, 16, 1024, 2), id16k, f);
-        }
-        tc_commit(&pv_done[sb]);
-        tc_commit(&kv_empty[st]);
-      }
-      tc_commit(fin);
-    }
-  } else if (w >= 4) {
-    // ---------------- compute warps ----------------
-    const int q = w & 3, row = q * 32 + l;      // TMEM lane == query row in the tile
-    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    const int tok = c0 + I * 128 + row;
-    const float li = ell_s[I * 128 + row];
-    const float sig2 = g.scale * g.scale;
-    if (has_state) {
-      // phi'(q) from the exact bf16 q (one rounding per feature); the query
-      // scale sigma^2 * gp_m (chunked.py:379-385) is applied to the fp32 row
-      {
-        uint32_t qp[32];
-        load_row_f16(qraw + rowid(g, s, tok) * HD, qp);
-#pragma unroll
-        for (int c8 = 0; c8 < 8; ++c8) xh_s[c8 * 128 + row] = *(const uint4*)&qp[c8 * 4];
-      }
-      gen_steps(xh_s, row, a_base, lane_off, a_full, a_empty, l);
-      mbar_wait(a_done, 0);
-      tc_fence_after();
-      const float cm = sig2 * __expf(li) / pow2_neg_bits(g.k0 + k - 1);   // undo the stored-state scale
-      uint32_t r[32];
-#pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
-        tmem_ld32(tm + lane_off + h2 * 32, r);
-        tc_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * cm);
-        tmem_st16(tm + lane_off + h2 * 32, r);
-        tmem_st16(tm + lane_off + h2 * 32 + 16, r + 16);
-      }
-      if (den) {
-        tmem_ld16(tm + lane_off + 64, r);
-        tc_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * cm);
-        tmem_st16(tm + lane_off + 64, r);
-      }
-      tc_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (l == 0) mbar_arrive(o_ready);
-    }
-    for (int J = 0; J <= I; ++J) {
-      const int sb = J & 1;
-      const bool diag = (J == I);
-      const float lref = ell_s[J * 128 + 127];
-      cj[sb * 128 + row] = diag ? ell_s[J * 128 + row] : __expf(lref - ell_s[J * 128 + row]);
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      mbar_wait(&s_full[sb], (J >> 1) & 1);
-      tc_fence_after();
-      const float ri = __expf(li - lref) * sig2;
-      const float* cjs = cj + sb * 128;
-      if (!diag) {
-#pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
-          uint32_t r[32], pk[16];
-          tmem_ld32(sbuf(sb) + lane_off + ch * 32, r);
-          tc_wait_ld();
-#pragma unroll
-          for (int e4 = 0; e4 < 8; ++e4) {
-            const float4 c4 = *(const float4*)(cjs + ch * 32 + e4 * 4);
-            const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
-#pragma unroll
-            for (int z = 0; z < 4; z += 2) {
-              const float s0 = __uint_as_float(r[e4 * 4 + z]), s1 = __uint_as_float(r[e4 * 4 + z + 1]);
-              pk[e4 * 2 + z / 2] = pack_bf16(ri * cc[z] * s0 * s0, ri * cc[z + 1] * s1 * s1);
-            }
-          }
-          tmem_st16(sbuf(sb) + lane_off + ch * 16, pk);
-        }
-      } else {
-        // diagonal block: exact pairwise decay exp(ell_i - ell_j), causal mask j <= i
-#pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
-          uint32_t r[32], pk[16];
-          tmem_ld32(sbuf(sb) + lane_off + ch * 32, r);
-          tc_wait_ld();
-#pragma unroll
-          for (int e4 = 0; e4 < 8; ++e4) {
-            const float4 c4 = *(const float4*)(cjs + ch * 32 + e4 * 4);
-            const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
-            float pv[4];
-#pragma unroll
-            for (int z = 0; z < 4; ++z) {
-              const int jj = ch * 32 + e4 * 4 + z;
-              const float sv = __uint_as_float(r[e4 * 4 + z]);
-              const float e = __expf(fminf(li - cc[z], 0.f)) * sig2 * sv * sv;
-              pv[z] = (jj <= row) ? e : 0.f;
-            }
-            pk[e4 * 2] = pack_bf16(pv[0], pv[1]);
-            pk[e4 * 2 + 1] = pack_bf16(pv[2], pv[3]);
-          }
-          tmem_st16(sbuf(sb) + lane_off + ch * 16, pk);
-        }
-      }
-      tc_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (l == 0) mbar_arrive(&p_full[sb]);
-    }
-    // ---------------- epilogue -------------------------------------------
-    mbar_wait(fin, 0);
-    tc_fence_after();
-    uint32_t o[64];
-    tmem_ld32(tm + lane_off, o);
-    tmem_ld32(tm + lane_off + 32, o + 32);
-    float dn = 0.f;
-    if (den) {
-      uint32_t r[16];
-      tmem_ld16(tm + lane_off + 64, r);
-      tc_wait_ld();
-      dn = __uint_as_float(r[0]);
-    }
-    tc_wait_ld();
-    const size_t rw = rowid(g, s, tok);
-    float inv = 1.f;
-    if (g.normalize) {
-      if (!(dn > 0.f)) atomicAdd(zflag, 1);
-      inv = 1.f / dn;
-    }
-    if (rowsum) rowsum[rw] = dn;
-    uint4* yrow = (uint4*)(y + rw * HD);
-#pragma unroll
-    for (int c8 = 0; c8 < 8; ++c8) {
-      uint4 v4;
-      uint32_t* pv = (uint32_t*)&v4;
-#pragma unroll
-      for (int e2 = 0; e2 < 4; ++e2)
-        pv[e2] = pack_bf16(__uint_as_float(o[c8 * 8 + e2 * 2]) * inv, __uint_as_float(o[c8 * 8 + e2 * 2 + 1]) * inv);
-      yrow[c8] = v4;
-    }
-    if (g.normalize && y32) {
-      float4* dst = (float4*)(y32 + ((size_t)s * g.t + tok) * HD);
-#pragma unroll
-      for (int c4 = 0; c4 < 16; ++c4)
-        dst[c4] = make_float4(__uint_as_float(o[c4 * 4]) * inv, __uint_as_float(o[c4 * 4 + 1]) * inv,
-                              __uint_as_float(o[c4 * 4 + 2]) * inv, __uint_as_float(o[c4 * 4 + 3]) * inv);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (w == 2) tmem_dealloc<512>(tm);
 }
 
 // ==========================================================================

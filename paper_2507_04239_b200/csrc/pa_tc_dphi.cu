@@ -177,11 +177,11 @@ __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
       }
     }
   } else if (w >= W_MMA) {
-    if (l == 0) {
+    {
       const int mw = w - W_MMA;
       constexpr uint32_t id128 = idesc_f16(128, 128, false, false);
       constexpr uint32_t id64mn = idesc_f16(128, 64, false, true);
-      mbar_wait(a_ready, 0);
+      mbar_wait_w(a_ready, 0);
       tc_fence_after();
       // descriptors are built once; per-MMA work is a 64-bit add of (byte offset >> 4)
       const uint64_t bk0 = smem_desc(smem_u32(bm_s), 16, 1024, 2);      // K-major view of a state stage
@@ -195,9 +195,9 @@ __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
       PA_TR3(trm, 99);
       for (int nt = mw; nt < NT; nt += 2) {
         const int st = nt % NST, db = nt % NDB;
-        mbar_wait(&b_full[st], (nt / NST) & 1);
+        mbar_wait_w(&b_full[st], (nt / NST) & 1);
         PA_TR3(trm, nt * 4 + 0);
-        if (nt >= NDB) mbar_wait(&d_empty[db], ((nt / NDB) + 1) & 1);
+        if (nt >= NDB) mbar_wait_w(&d_empty[db], ((nt / NDB) + 1) & 1);
         PA_TR3(trm, nt * 4 + 1);
         tc_fence_after();
         const uint64_t so = (uint64_t)((st * BM) >> 4);
@@ -205,31 +205,31 @@ __global__ void __launch_bounds__(dp2::THREADS, 1) k_tc_dphi2(
         if (kUpd) {
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            mma_ts(dt, tm + TA + (uint32_t)(kk * 8), bk0 + so + (uint64_t)(kk * 2), id128, kk > 0 ? 1u : 0u);
-          if (den) mma_ts(dt, tm + TA16, bd0 + (uint64_t)((st * BD) >> 4), id128, 1u);
+            mma_ts_w(dt, tm + TA + (uint32_t)(kk * 8), bk0 + so + (uint64_t)(kk * 2), id128, kk > 0 ? 1u : 0u);
+          if (den) mma_ts_w(dt, tm + TA16, bd0 + (uint64_t)((st * BD) >> 4), id128, 1u);
         } else {
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            mma_ss(dt, ak0 + (uint64_t)(kk * 2), bk0 + so + (uint64_t)(kk * 2), id128, kk > 0 ? 1u : 0u);
-          if (den) mma_ss(dt, a160, bd0 + (uint64_t)((st * BD) >> 4), id128, 1u);
+            mma_ss_w(dt, ak0 + (uint64_t)(kk * 2), bk0 + so + (uint64_t)(kk * 2), id128, kk > 0 ? 1u : 0u);
+          if (den) mma_ss_w(dt, a160, bd0 + (uint64_t)((st * BD) >> 4), id128, 1u);
         }
-        tc_commit(&d_full[db]);
+        tc_commit_w(&d_full[db]);
         PA_TR3(trm, 400 + nt);
         if (kUpd) {
           // dv += phi'(k) [128 tok x 128 slots] * dS~ tile [128 slots x 64] (same stage, MN-major)
-          mbar_wait(&g_full[nt & 1], (nt >> 1) & 1);
+          mbar_wait_w(&g_full[nt & 1], (nt >> 1) & 1);
           PA_TR3(trm, nt * 4 + 2);
           tc_fence_after();
           const uint32_t ab = tm + 384u + (uint32_t)((nt & 1) * 64);
           // both issuers accumulate into the zero-initialised dv columns
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) mma_ts(tm + 256u, ab + kk * 8, bn0 + so + (uint64_t)(kk * 128), id64mn, 1u);
-          tc_commit(&g_empty[nt & 1]);
+          for (int kk = 0; kk < 8; ++kk) mma_ts_w(tm + 256u, ab + kk * 8, bn0 + so + (uint64_t)(kk * 128), id64mn, 1u);
+          tc_commit_w(&g_empty[nt & 1]);
         }
-        tc_commit(&b_empty[st]);
+        tc_commit_w(&b_empty[st]);
         PA_TR3(trm, nt * 4 + 3);
       }
-      tc_commit(fin);
+      tc_commit_w(fin);
     }
   } else if (w < 8) {
     const int q = w & 3, grp = w >> 2, row = q * 32 + l;

@@ -191,14 +191,14 @@ __global__ void __launch_bounds__(ib2::THREADS, 2) k_tc_ib(const __grid_constant
       }
     }
   } else if (w == W_MMA) {
-    if (l == 0) {
+    {
       constexpr uint32_t idS = idesc_bf16(128, 64, false, false);   // S / dP: both K-major
       constexpr uint32_t idG = idesc_bf16(128, 64, false, true);    // gradients: B MN-major
-      mbar_wait(f_full, 0);
+      mbar_wait_w(f_full, 0);
       const uint32_t F0 = smem_u32(f0), F1 = smem_u32(f1);
       for (int it = 0; it < nblk; ++it) {
         const int st = it % NST;
-        mbar_wait(&t_full[st], (it / NST) & 1);
+        mbar_wait_w(&t_full[st], (it / NST) & 1);
         tc_fence_after();
         const uint32_t T0 = smem_u32(s0 + st * 2 * T128), T1 = T0 + T128;
 #pragma unroll
@@ -212,31 +212,31 @@ __global__ void __launch_bounds__(ib2::THREADS, 2) k_tc_ib(const __grid_constant
           // kKV: S^T = K_J Q_h^T, dP^T = V_J dN_h^T   | q-side: S = Q_I K_h^T, dP = dN_I V_h^T
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            mma_ss(tS, smem_desc(F0 + kk * 32, 16, 1024, 2), smem_desc(T0 + hb + kk * 32, 16, 1024, 2), idS,
+            mma_ss_w(tS, smem_desc(F0 + kk * 32, 16, 1024, 2), smem_desc(T0 + hb + kk * 32, 16, 1024, 2), idS,
                    kk > 0 ? 1u : 0u);
-            mma_ss(tDP, smem_desc(F1 + kk * 32, 16, 1024, 2), smem_desc(T1 + hb + kk * 32, 16, 1024, 2), idS,
+            mma_ss_w(tDP, smem_desc(F1 + kk * 32, 16, 1024, 2), smem_desc(T1 + hb + kk * 32, 16, 1024, 2), idS,
                    kk > 0 ? 1u : 0u);
           }
-          tc_commit(s_full);
+          tc_commit_w(s_full);
           PA_TR(n * 8 + 1);
-          mbar_wait(p_full, n & 1);
+          mbar_wait_w(p_full, n & 1);
           PA_TR(n * 8 + 2);
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             const uint32_t acc = (n > 0 || kk > 0) ? 1u : 0u;
             if (kKV) {
-              mma_ts(tA, tS + pcol(kk), smem_desc(T1 + hb + kk * 2048, 8192, 1024, 2), idG, acc);   // dV += P^T dN
-              mma_ts(tB, tDP + pcol(kk), smem_desc(T0 + hb + kk * 2048, 8192, 1024, 2), idG, acc);  // dK += dS^T Q
+              mma_ts_w(tA, tS + pcol(kk), smem_desc(T1 + hb + kk * 2048, 8192, 1024, 2), idG, acc);   // dV += P^T dN
+              mma_ts_w(tB, tDP + pcol(kk), smem_desc(T0 + hb + kk * 2048, 8192, 1024, 2), idG, acc);  // dK += dS^T Q
             } else {
-              mma_ts(tA, tDP + pcol(kk), smem_desc(T0 + hb + kk * 2048, 8192, 1024, 2), idG, acc);  // dQ += dS K
+              mma_ts_w(tA, tDP + pcol(kk), smem_desc(T0 + hb + kk * 2048, 8192, 1024, 2), idG, acc);  // dQ += dS K
             }
           }
           PA_TR(n * 8 + 3);
         }
-        tc_commit(&t_empty[st]);
+        tc_commit_w(&t_empty[st]);
       }
-      tc_commit(fin);
+      tc_commit_w(fin);
     }
   } else if (w < 8) {
     // 8 compute warps: lane quadrant q = w % 4, column half grp = w / 4 of

@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
     }
   } else if (w == W_MMA_ST || w == W_MMA_ST + 1) {
     // ---------------- state query: O_state += phi'(q) slot_k ------------------
-    if (l == 0) {
+    {
       const int mw = w - W_MMA_ST;
       if (has_state) {
         constexpr uint32_t id64mn_h = idesc_f16(128, 64, false, true);
@@ -185,9 +185,9 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
         PA_TR4(trb && mw == 0, 0);
         for (int stp = mw; stp < NSTEP; stp += 2) {
           const int bb = stp & 1, sb = stp % ST_ST;
-          mbar_wait(&a_full[bb], (stp >> 1) & 1);
+          mbar_wait_w(&a_full[bb], (stp >> 1) & 1);
           PA_TR4(trb, 10 + stp * 3 + 0);
-          mbar_wait(&st_full[sb], (stp / ST_ST) & 1);
+          mbar_wait_w(&st_full[sb], (stp / ST_ST) & 1);
           PA_TR4(trb, 10 + stp * 3 + 1);
           tc_fence_after();
           const uint64_t so = (uint64_t)((sb * STB) >> 4), sdo = (uint64_t)((sb * STD) >> 4);
@@ -195,19 +195,19 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
           // both issuers accumulate into the zero-initialised O_state
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {   // 16 slots per MMA: 2048 B of [slot][64] rows, 512 B of [slot][16]
-            mma_ts(tm + TOS, ab + kk * 8, sm0 + so + (uint64_t)(kk * 128), id64mn_h, 1u);
-            if (den) mma_ts(tm + TOS + 64, ab + kk * 8, sd0 + sdo + (uint64_t)(kk * 32), id16mn_h, 1u);
+            mma_ts_w(tm + TOS, ab + kk * 8, sm0 + so + (uint64_t)(kk * 128), id64mn_h, 1u);
+            if (den) mma_ts_w(tm + TOS + 64, ab + kk * 8, sd0 + sdo + (uint64_t)(kk * 32), id16mn_h, 1u);
           }
-          tc_commit(&a_empty[bb]);
-          tc_commit(&st_empty[sb]);
+          tc_commit_w(&a_empty[bb]);
+          tc_commit_w(&st_empty[sb]);
           PA_TR4(trb, 10 + stp * 3 + 2);
         }
       }
-      tc_commit(a_done);
+      tc_commit_w(a_done);
     }
   } else if (w == W_MMA_IN) {
     // ---------------- intra-chunk: S = Q K_J^T, O_intra += P V_J ---------------
-    if (l == 0) {
+    {
       constexpr uint32_t id128 = idesc_bf16(128, 128, false, false);
       constexpr uint32_t id64mn = idesc_bf16(128, 64, false, true);
       constexpr uint32_t id16k = idesc_bf16(128, 16, false, false);
@@ -215,25 +215,25 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
       const uint64_t kd0 = smem_desc(smem_u32(k_s), 16, 1024, 2);
       const uint64_t vd0 = smem_desc(smem_u32(v_s), 8192, 1024, 2);
       const uint64_t od0 = smem_desc(smem_u32(ones), 16, 1024, 2);
-      mbar_wait(q_full, 0);
+      mbar_wait_w(q_full, 0);
       auto issue_s = [&](int J) {
         const int st = J % KV_ST, sb = J % NSB;
-        mbar_wait(&kv_full[st], (J / KV_ST) & 1);
-        if (J >= NSB) mbar_wait(&pv_done[sb], ((J / NSB) + 1) & 1);
+        mbar_wait_w(&kv_full[st], (J / KV_ST) & 1);
+        if (J >= NSB) mbar_wait_w(&pv_done[sb], ((J / NSB) + 1) & 1);
         tc_fence_after();
         const uint64_t ko = (uint64_t)((st * KB) >> 4);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          mma_ss(tm + TSP + (uint32_t)(sb * 128), qd0 + (uint64_t)(kk * 2), kd0 + ko + (uint64_t)(kk * 2), id128,
+          mma_ss_w(tm + TSP + (uint32_t)(sb * 128), qd0 + (uint64_t)(kk * 2), kd0 + ko + (uint64_t)(kk * 2), id128,
                  kk > 0 ? 1u : 0u);
-        tc_commit(&s_full[sb]);
+        tc_commit_w(&s_full[sb]);
       };
       issue_s(0);
       for (int J = 0; J <= I; ++J) {
         if (NSB == 2 && J + 1 <= I) issue_s(J + 1);
         const int sb = J % NSB, st = J % KV_ST;
         PA_TR4(trb, 100 + J * 3 + 0);
-        mbar_wait(&p_full[sb], (J / NSB) & 1);
+        mbar_wait_w(&p_full[sb], (J / NSB) & 1);
         PA_TR4(trb, 100 + J * 3 + 1);
         tc_fence_after();
         const uint64_t vo = (uint64_t)((st * VB) >> 4);
@@ -241,15 +241,15 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t f = (J > 0 || kk > 0) ? 1u : 0u;
-          mma_ts(tm + TOI, pb + kk * 8, vd0 + vo + (uint64_t)(kk * 128), id64mn, f);
-          if (den) mma_ts(tm + TOI + 64, pb + kk * 8, od0 + (uint64_t)((kk & 3) * 2), id16k, f);
+          mma_ts_w(tm + TOI, pb + kk * 8, vd0 + vo + (uint64_t)(kk * 128), id64mn, f);
+          if (den) mma_ts_w(tm + TOI + 64, pb + kk * 8, od0 + (uint64_t)((kk & 3) * 2), id16k, f);
         }
-        tc_commit(&pv_done[sb]);
-        tc_commit(&kv_empty[st]);
+        tc_commit_w(&pv_done[sb]);
+        tc_commit_w(&kv_empty[st]);
         PA_TR4(trb, 100 + J * 3 + 2);
         if (NSB == 1 && J + 1 <= I) issue_s(J + 1);
       }
-      tc_commit(fin);
+      tc_commit_w(fin);
     }
   } else if (w < 4) {
     // ---------------- phi'(q) generation, then the epilogue --------------------
