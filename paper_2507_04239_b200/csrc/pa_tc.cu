@@ -520,6 +520,22 @@ __global__ void __launch_bounds__(256) k_tc_bwd_prep(Geo g, const __nv_bfloat16*
   }
 }
 
+// Expanded state (pa_tc_zvjp.cu): per (stream, slot) nbt tiles of [64 c][64 e]
+// fp16, SW128 rows; tile b row c = T_{cb}.  Slot (a, b), a <= b, goes to tile b
+// row a and tile a row b.  Columns u >= 64: the score-sum column (u == 64 only)
+// goes to tile 64, element [c][b'].
+__device__ __forceinline__ void e_store(__half* et, int a, int b, int u, uint2 v) {
+  uint8_t* base = (uint8_t*)et;
+  if (u < 64) {
+    *(uint2*)(base + (size_t)b * 8192 + sw128_elem(a, u)) = v;
+    if (a != b) *(uint2*)(base + (size_t)a * 8192 + sw128_elem(b, u)) = v;
+  } else if (u == 64) {
+    const unsigned short h = (unsigned short)(v.x & 0xffffu);
+    *(unsigned short*)(base + (size_t)64 * 8192 + sw128_elem(a, b)) = h;
+    if (a != b) *(unsigned short*)(base + (size_t)64 * 8192 + sw128_elem(b, a)) = h;
+  }
+}
+
 // backward scan (discumsum VJP, gradients.py:267-288) over the state slots
 // (slot j = state before local chunk j, slot n = end state):
 //   Gs_n = carry (cotangent of the end state from later chunks, zero without)
@@ -537,13 +553,15 @@ __global__ void __launch_bounds__(256) k_tc_scan_bwd(Geo g, int ucols, const flo
                                                      const __half* __restrict__ st_main,
                                                      const __half* __restrict__ st_den,
                                                      __half* ds_main, __half* ds_den, float* dlam_part,
-                                                     const float* __restrict__ carry, float* pre_out, int write) {
+                                                     const float* __restrict__ carry, float* pre_out, int write,
+                                                     __half* ea, __half* eg, int nbt) {
   extern __shared__ float red[];  // [n][8]
   const int s = blockIdx.y, wq = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int e = (blockIdx.x * 256 + threadIdx.x) * 4;
   const bool ok = e < FH * ucols;
   const int f = ok ? e / ucols : 0, u = ok ? e - f * ucols : 0;
   const float om = ok ? slot_omega(f) : 0.f;
+  const int fa = 4 * c_blk.al[f >> 5] + ((f >> 3) & 3), fb = 8 * c_blk.be[f >> 5] + (f & 7);
   const float* src = dA + ((size_t)s * g.nsl * FH + f) * UW + u;
   const size_t kstride = (size_t)FH * UW;
   const size_t cidx = ((size_t)s * FH + f) * UW + u;
@@ -568,10 +586,26 @@ __global__ void __launch_bounds__(256) k_tc_scan_bwd(Geo g, int ucols, const flo
       const int k = k1 - i;
       if (k < 0) break;
       if (write) {
-        if (ok) {
+        if (ok && eg) {
+          // expanded form for the state-VJP GEMMs: E = 2 sc G on every ordered pair
+          if (fa <= fb) {
+            const float sc = 2.f * pow2_neg_bits(g.ng - 1 - (g.k0 + k));
+            e_store(eg + ((size_t)s * g.nsl + k) * nbt * 4096, fa, fb, u,
+                    make_uint2(pack_f16(G.x * sc, G.y * sc), pack_f16(G.z * sc, G.w * sc)));
+          }
+        } else if (ok) {
           const float sc = om * pow2_neg_bits(g.ng - 1 - (g.k0 + k));
           *(uint2*)state_elem_ptr(ds_main, ds_den, (size_t)s * g.nsl + k, f, u) =
               make_uint2(pack_f16(G.x * sc, G.y * sc), pack_f16(G.z * sc, G.w * sc));
+        }
+        if (ok && ea && fa <= fb && (k >= 1 || g.prefix)) {
+          // expanded forward state: slot values, doubled on the diagonal
+          uint2 av = a[i];
+          if (fa == fb) {
+            av.x = hmul2_f16(av.x, 0x40004000u);
+            av.y = hmul2_f16(av.y, 0x40004000u);
+          }
+          e_store(ea + ((size_t)s * g.nsl + k) * nbt * 4096, fa, fb, u, av);
         }
         if (k >= 1 || g.prefix) {
           const float2 a01 = __half22float2(*(const __half2*)&a[i].x), a23 = __half22float2(*(const __half2*)&a[i].y);
@@ -665,6 +699,8 @@ struct TcBwdWs {
   float* dell;
   float* cu;
   float* dlam;
+  __half* ea;            // expanded forward states E(A'_k) (pa_tc_zvjp.cu)
+  __half* eg;            // expanded state cotangents E(dS~_k)
 };
 
 static int scan_blocks(int ucols) { return (FH * ucols / 4 + 255) / 256; }
@@ -712,6 +748,9 @@ static TcBwdWs carve_bwd(const Geo& g, void* base, size_t* bytes) {
   b.dell = (float*)take(4ull * g.ns * g.t);
   b.cu = (float*)take(4ull * g.ns * g.t);
   b.dlam = (float*)take(4ull * g.ns * g.n * scan_blocks(UW));   // per-block dlambda partials
+  const size_t etiles = (size_t)g.ns * g.nsl * (64 + (g.normalize ? 1 : 0));
+  b.ea = (__half*)take(8192ull * etiles);
+  b.eg = (__half*)take(8192ull * etiles);
   *bytes = take.off;
   return b;
 }
@@ -893,6 +932,14 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
   if (!map_2d(&m_dn128, b.dN, (size_t)g.ns * g.t, HD, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)) return 3;
   m_dummy = m_dn;
   const int red_bytes = 8 * 4 * g.n;
+  const int nbt = 64 + den;
+  // state VJP: expanded-state GEMMs (pa_tc_zvjp.cu); PA_DPHI_OLD=1 selects the
+  // slot-form GEMM + expand-VJP kernels (pa_tc_dphi.cu) for comparison
+  static const bool old_dphi = [] {
+    const char* e = getenv("PA_DPHI_OLD");
+    return e && e[0] == '1';
+  }();
+  const bool zf = !old_dphi;
   if (red_bytes > 48 * 1024)
     cudaFuncSetAttribute(k_tc_scan_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, red_bytes);
   if (mode != 2) {
@@ -921,7 +968,8 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
   if (mode == 1) {
     StageTimer tmr("bwd_discumsum", st);
     k_tc_scan_bwd<<<dim3(scan_blocks(uc), g.ns), 256, red_bytes, st>>>(g, uc, w.lamlog, w.sp, w.stm, w.std_,
-                                                                          b.dsm, b.dsd, b.dlam, nullptr, pre_out, 0);
+                                                                          b.dsm, b.dsd, b.dlam, nullptr, pre_out, 0,
+                                                                          nullptr, nullptr, nbt);
     count_launch(4);
     return cuda_check("tc backward (sp local)");
   }
@@ -929,7 +977,8 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
   {
     StageTimer tmr("bwd_discumsum", st);
     k_tc_scan_bwd<<<dim3(scan_blocks(uc), g.ns), 256, red_bytes, st>>>(g, uc, w.lamlog, w.sp, w.stm, w.std_,
-                                                                          b.dsm, b.dsd, b.dlam, carry, pre_out, 1);
+                                                                          b.dsm, b.dsd, b.dlam, carry, pre_out, 1,
+                                                                          zf ? b.ea : nullptr, zf ? b.eg : nullptr, nbt);
   }
   {
     StageTimer tmr("bwd_intra", st);
@@ -938,18 +987,34 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
       return 3;
     }
     CUtensorMap m_dy128;
-    if (!den && !map_bth(&m_dy128, dy, g, 128)) return 3;
-    tc_intra_bwd(g, m_q128, m_k128, m_v128, den ? m_dn128 : m_dy128, w.ell, b.dden, b.dk32, b.dv32, b.dq32, b.dell,
-                 st);
+    if (!map_bth(&m_dy128, dy, g, 128)) return 3;
+    tc_intra_bwd(g, m_q128, m_k128, m_v128, m_dy128, w.ell, b.dden, rowsum, b.dk32, b.dv32, b.dq32, b.dell, st);
   }
   {
     StageTimer tmr("bwd_query_state_dq", st);
-    tc_dphi(g, false, den ? (const void*)b.dN16 : dy, den ? 0 : 1, b.dD, q, w.ell, w.lamlog, w.stm, w.std_, b.dq32, nullptr, b.dell, nullptr, dq,
-            nullptr, st);
+    if (zf) {
+      CUtensorMap m_xq, m_uq;
+      if (!map_bth(&m_xq, q, g, 128)) return 3;
+      if (den ? !map_2d(&m_uq, b.dN16, (size_t)g.ns * g.t, HD, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)
+              : !map_bth(&m_uq, dy, g, 128))
+        return 3;
+      tc_zvjp(g, false, m_xq, m_uq, den ? 0 : 1, b.dD, q, w.ell, w.lamlog, b.ea, b.dq32, nullptr, b.dell, nullptr,
+              dq, nullptr, st);
+    }
+    else
+      tc_dphi(g, false, den ? (const void*)b.dN16 : dy, den ? 0 : 1, b.dD, q, w.ell, w.lamlog, w.stm, w.std_,
+              b.dq32, nullptr, b.dell, nullptr, dq, nullptr, st);
   }
   {
     StageTimer tmr("bwd_update_state", st);
-    tc_dphi(g, true, v, 1, nullptr, k, w.ell, w.lamlog, b.dsm, b.dsd, b.dk32, b.dv32, b.dell, b.cu, dk, dv, st);
+    if (zf) {
+      CUtensorMap m_xk, m_uv;
+      if (!map_bth(&m_xk, k, g, 128) || !map_bth(&m_uv, v, g, 128)) return 3;
+      tc_zvjp(g, true, m_xk, m_uv, 1, nullptr, k, w.ell, w.lamlog, b.eg, b.dk32, b.dv32, b.dell, b.cu, dk, dv,
+              st);
+    }
+    else
+      tc_dphi(g, true, v, 1, nullptr, k, w.ell, w.lamlog, b.dsm, b.dsd, b.dk32, b.dv32, b.dell, b.cu, dk, dv, st);
   }
   {
     StageTimer tmr("bwd_finish", st);

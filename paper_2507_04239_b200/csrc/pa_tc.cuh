@@ -31,10 +31,11 @@ int tc_out(const Geo& g, const CUtensorMap& m_q, const CUtensorMap& m_k, const C
            const float* ell, const __half* st_main, const __half* st_den, int with_den, void* y, float* rowsum,
            float* y32, int* zflag, cudaStream_t st);
 
-// intra-chunk backward (pa_tc_ib.cu): dK, dV (fp32, =), dQ (fp32, =), dell (+=)
+// intra-chunk backward (pa_tc_ib.cu): dK, dV (fp32, =), dQ (fp32, =), dell (+=); m_dn maps dy
+// (normalization is applied in fp32 from dden and the forward rowsum)
 int tc_intra_bwd(const Geo& g, const CUtensorMap& m_q, const CUtensorMap& m_k, const CUtensorMap& m_v,
-                 const CUtensorMap& m_dn, const float* ell, const float* dden, float* dk32, float* dv32,
-                 float* dq32, float* dell, cudaStream_t st);
+                 const CUtensorMap& m_dn, const float* ell, const float* dden, const float* rsum, float* dk32,
+                 float* dv32, float* dq32, float* dell, cudaStream_t st);
 
 // token-major state VJP + fused expand-VJP (pa_tc_dphi.cu): final bf16 dq (query side)
 // or dk, dv (update side)
@@ -42,5 +43,11 @@ int tc_intra_bwd(const Geo& g, const CUtensorMap& m_q, const CUtensorMap& m_k, c
 int tc_dphi(const Geo& g, bool upd, const void* a_rows, int a_bf16_bth, const __half* a16_rows, const void* xraw,
             const float* ell, const float* lamlog, const __half* b_main, const __half* b_den, const float* dx32,
             const float* dv32, float* dell, float* dellend, void* dxo, void* dvo, cudaStream_t st);
+
+// expanded-state VJP GEMMs (pa_tc_zvjp.cu): E = expanded A'_{k-1} (query side) or dS~_k (update side)
+int tc_zvjp(const Geo& g, bool upd, const CUtensorMap& m_x, const CUtensorMap& m_u, int u_bf16_bth,
+            const __half* u16, const void* xraw, const float* ell, const float* lamlog, const __half* E,
+            const float* dx32, const float* dv32, float* dell, float* dellend, void* dxo, void* dvo,
+            cudaStream_t st);
 
 }  // namespace pa

@@ -49,7 +49,7 @@ constexpr int NST = 2;            // streamed-tile stages
 // compute warps cannot starve the MMA / TMA issue.
 constexpr int THREADS = 352;
 constexpr int W_TMEM = 8, W_TMA = 9, W_MMA = 10;
-constexpr int SMEM = 1024 + 2 * T128 + NST * 2 * T128 + 3 * 4096 + 256;
+constexpr int SMEM = 1024 + 2 * T128 + NST * 2 * T128 + 3 * 4096 + 512 + 256;
 }  // namespace ib2
 
 struct f2 {
@@ -90,7 +90,8 @@ __global__ void __launch_bounds__(ib2::THREADS, 2) k_tc_ib(const __grid_constant
                                                   const __grid_constant__ CUtensorMap tm_v,
                                                   const __grid_constant__ CUtensorMap tm_dn, Geo g,
                                                   const float* __restrict__ ell, const float* __restrict__ dden,
-                                                  float* out_a, float* out_b, float* dell) {
+                                                  const float* __restrict__ rsum, float* out_a, float* out_b,
+                                                  float* dell) {
   using namespace ib2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -100,7 +101,8 @@ __global__ void __launch_bounds__(ib2::THREADS, 2) k_tc_ib(const __grid_constant
   float* ell_s = (float*)(s0 + NST * 2 * T128);   // [1024] in-chunk log prefix
   float* colf = ell_s + 1024;                       // [1024] off-diagonal column factor
   float* cold = colf + 1024;                        // [1024] dden per query column (kKV, normalize)
-  uint64_t* bars = (uint64_t*)(cold + 1024);
+  float* cinv = cold + 1024;                        // [128] 1/rowsum of the diagonal block's query columns
+  uint64_t* bars = (uint64_t*)(cinv + 128);
   uint64_t* f_full = bars;
   uint64_t* t_full = f_full + 1;         // NST
   uint64_t* t_empty = t_full + NST;      // NST
@@ -146,7 +148,16 @@ __global__ void __launch_bounds__(ib2::THREADS, 2) k_tc_ib(const __grid_constant
         colf[i] = sig2 * exp2_approx(fminf(ell_s[i] - lrefJ, 0.f));
       else
         colf[i] = exp2_approx(fminf(ell_s[(i | 127)] - ell_s[i], 0.f));
-      if (kKV && kNorm) cold[i] = dden[(size_t)s * g.t + c0 + i];
+      if (kKV && kNorm) {
+        // normalization (gradients.py:381-386) with the 1/rowsum folded into the
+        // column factor: the dP GEMM runs on the exact bf16 dy, and
+        //   dP' = (dy.v - dy.y) / R = (acc + dden R) / R
+        // so with c' = c / R: P' = P / R (the dV operand, = P^T dnum), dS = (acc + dden R) T'
+        const float R = rsum[rowid(g, s, c0 + i)];
+        colf[i] *= 1.f / R;
+        cold[i] = dden[(size_t)s * g.t + c0 + i] * R;
+        if ((i >> 7) == B0) cinv[i & 127] = 1.f / R;
+      }
     }
   }
   tc_fence_before();
@@ -156,13 +167,8 @@ __global__ void __launch_bounds__(ib2::THREADS, 2) k_tc_ib(const __grid_constant
   const uint32_t tS = tm, tDP = tm + 64, tA = tm + 128, tB = tm + 192;
 
   if (w == W_TMA) {
-    // dnum rows: stream-major [ns*t][64] when normalizing, else dy itself ([b, t, h, 64])
-    auto load_dn = [&](void* dst, uint64_t* bar, int blk) {
-      if (kNorm)
-        tma_load_2d(dst, &tm_dn, bar, 0, s * g.t + c0 + blk * 128);
-      else
-        tma_load_4d(dst, &tm_dn, bar, 0, hi, c0 + blk * 128, bi);
-    };
+    // dy rows ([b, t, h, 64]); normalization is applied in fp32 (see cold / rinv_own)
+    auto load_dn = [&](void* dst, uint64_t* bar, int blk) { tma_load_4d(dst, &tm_dn, bar, 0, hi, c0 + blk * 128, bi); };
     if (l == 0) {
       tma_prefetch(&tm_q);
       tma_prefetch(&tm_k);
@@ -245,7 +251,10 @@ __global__ void __launch_bounds__(ib2::THREADS, 2) k_tc_ib(const __grid_constant
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const int own = B0 * 128 + row;            // chunk-relative token of this TMEM lane
     const float l_own = ell_s[own];            // log2 units
-    const float dden_own = (!kKV && kNorm) ? dden[(size_t)s * g.t + c0 + own] : 0.f;
+    // q-side normalization: the row factor takes 1/R_own, dden takes R_own (see cold above)
+    const float R_own = (!kKV && kNorm) ? rsum[rowid(g, s, c0 + own)] : 1.f;
+    const float dden_own = (!kKV && kNorm) ? dden[(size_t)s * g.t + c0 + own] * R_own : 0.f;
+    const float rinv_own = 1.f / R_own;
     // kKV: c_own = 2^(ell_endJ - ell_own) (<= 1); q-side: r_own = sigma^2 2^(ell_own - ell_endJ) per J
     const float c_own = kKV ? exp2_approx(fminf(ell_s[B0 * 128 + 127] - l_own, 0.f)) : 0.f;
     f2 red = {0.f, 0.f};
@@ -253,7 +262,8 @@ __global__ void __launch_bounds__(ib2::THREADS, 2) k_tc_ib(const __grid_constant
       const int it = n >> 1, h = n & 1;
       const int X = kKV ? B0 + it : it;
       const bool diag = (X == B0);
-      const float rowf = kKV ? c_own : sig2 * exp2_approx(fminf(l_own - ell_s[X * 128 + 127], 0.f));
+      const float rowf =
+          kKV ? c_own : sig2 * exp2_approx(fminf(l_own - ell_s[X * 128 + 127], 0.f)) * rinv_own;
       const f2 rowf2 = {rowf, rowf};
 #ifdef PA_TRACE
       const bool tr = tr0 && n < 64 && w == 0 && l == 0;
@@ -314,7 +324,8 @@ __global__ void __launch_bounds__(ib2::THREADS, 2) k_tc_ib(const __grid_constant
               if (kNorm) dp += kKV ? cdv[z] : dden_own;
               const bool valid = kKV ? (col >= own) : (col <= own);
               const float d = kKV ? lcv[z] - l_own : l_own - lcv[z];
-              const float E = valid ? sig2 * exp2_approx(fminf(d, 0.f)) : 0.f;
+              float E = valid ? sig2 * exp2_approx(fminf(d, 0.f)) : 0.f;
+              if (kNorm) E *= kKV ? cinv[col & 127] : rinv_own;
               const float T = E * sv;
               Pv[z] = T * sv;
               dSv[z] = dp * T;
@@ -368,16 +379,16 @@ __global__ void __launch_bounds__(ib2::THREADS, 2) k_tc_ib(const __grid_constant
 }
 
 int tc_intra_bwd(const Geo& g, const CUtensorMap& m_q, const CUtensorMap& m_k, const CUtensorMap& m_v,
-                 const CUtensorMap& m_dn, const float* ell, const float* dden, float* dk32, float* dv32,
-                 float* dq32, float* dell, cudaStream_t st) {
+                 const CUtensorMap& m_dn, const float* ell, const float* dden, const float* rsum, float* dk32,
+                 float* dv32, float* dq32, float* dell, cudaStream_t st) {
   using namespace ib2;
   const dim3 grid(g.c / 128, g.n, g.ns);
   auto kv = g.normalize ? k_tc_ib<true, true> : k_tc_ib<true, false>;
   auto qs = g.normalize ? k_tc_ib<false, true> : k_tc_ib<false, false>;
   cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
   cudaFuncSetAttribute(qs, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-  kv<<<grid, THREADS, SMEM, st>>>(m_q, m_k, m_v, m_dn, g, ell, dden, dk32, dv32, dell);
-  qs<<<grid, THREADS, SMEM, st>>>(m_q, m_k, m_v, m_dn, g, ell, dden, dq32, nullptr, dell);
+  kv<<<grid, THREADS, SMEM, st>>>(m_q, m_k, m_v, m_dn, g, ell, dden, rsum, dk32, dv32, dell);
+  qs<<<grid, THREADS, SMEM, st>>>(m_q, m_k, m_v, m_dn, g, ell, dden, rsum, dq32, nullptr, dell);
   return 0;
 }
 

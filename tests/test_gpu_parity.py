@@ -191,3 +191,23 @@ def test_bf16_forward_tensor_core_shape(t, c, normalize, gated):
     assert err <= BF16_TOL, err
     if normalize:
         assert O.max_rel_error(r["rowsum"], rs_ref) <= BF16_TOL
+
+
+@pytest.mark.parametrize("gated", [True, False])
+@pytest.mark.parametrize("normalize", [False, True])
+@pytest.mark.parametrize("t,c", [(1024, 256), (2048, 1024), (512, 128), (768, 384)])
+def test_bf16_backward_tensor_core_shape(t, c, normalize, gated):
+    """p=2, d=e=64 bf16 backward on the tcgen05 path: intra-chunk VJP, dA' GEMM,
+    reverse scan with the expanded states, and the state-VJP GEMMs (pa_tc_zvjp.cu),
+    including chunks that are not a multiple of the 256-token query tile."""
+    q, k, v, g = O.generate_inputs(1, t, 2, 64, 64, seed=t + 7 * c, gating=gated)
+    q, k, v = (torch.tensor(x).bfloat16().double().numpy() for x in (q, k, v))
+    dy = np.random.default_rng(t + c).uniform(-1, 1, (1, t, 2, 64))
+    dyb = torch.tensor(dy).bfloat16().double().numpy()
+    r = run_full(q, k, v, g, 2, c, normalize, dtype=torch.bfloat16, dy=dyb)
+    dq, dk, dv, dg = O.chunked_backward(q, k, v, g, 2, c, dyb, normalize=normalize)
+    metric = O.max_rel_error if (gated or normalize) else norm_rel_error
+    for name, a, b in (("dq", r["dq"], dq), ("dk", r["dk"], dk), ("dv", r["dv"], dv)):
+        assert metric(a, b) <= BF16_TOL, (name, metric(a, b))
+    if gated:
+        assert metric(r["dlogg"], dg * g) <= BF16_TOL, ("dlogg", metric(r["dlogg"], dg * g))
