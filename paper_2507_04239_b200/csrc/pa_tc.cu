@@ -236,18 +236,25 @@ __global__ void __launch_bounds__(fm::THREADS, 2) k_tc_featmajor(const __grid_co
 
   if (w == 0) {
     // ---------------- producer ----------------
-    if (l == 0) {
-      tma_prefetch(&tm_xt);
-      tma_prefetch(&tm_b);
+    // one issuing lane per tensor: a thread completes one TMA copy per ~610
+    // cycles whatever its size (profiles/r01_bulk_copy_probe.txt), lanes overlap
+    constexpr int NL = den ? 3 : 2;
+    constexpr unsigned LM = (1u << NL) - 1u;
+    if (l < NL) {
+      if (l == 0) {
+        tma_prefetch(&tm_xt);
+        tma_prefetch(&tm_b);
+      }
       const int row0 = (s * g.n + kin) * HD;
       for (int j = 0; j < nstage; ++j) {
         const int st = j % ST;
         if (j >= ST) mbar_wait(&empty[st], ((j / ST) + 1) & 1);
         const uint32_t bytes = XT_B + B_B + (den ? B16_B : 0);
-        mbar_expect_tx(&full[st], bytes);
-        tma_load_2d(xt_s + st * XT_B, &tm_xt, &full[st], j * TOK, row0);
-        tma_load_2d(b_s + st * B_B, &tm_b, &full[st], 0, s * g.t + kin * g.c + j * TOK);
-        if (den) tma_load_2d(b16_s + st * B16_B, &tm_b16, &full[st], 0, s * g.t + kin * g.c + j * TOK);
+        if (l == 0) mbar_expect_tx(&full[st], bytes);
+        __syncwarp(LM);
+        if (l == 0) tma_load_2d(xt_s + st * XT_B, &tm_xt, &full[st], j * TOK, row0);
+        if (l == 1) tma_load_2d(b_s + st * B_B, &tm_b, &full[st], 0, s * g.t + kin * g.c + j * TOK);
+        if (den && l == 2) tma_load_2d(b16_s + st * B16_B, &tm_b16, &full[st], 0, s * g.t + kin * g.c + j * TOK);
       }
     }
   } else if (w == 1 || w == 3) {

@@ -169,30 +169,36 @@ __global__ void __launch_bounds__(ib2::THREADS, 2) k_tc_ib(const __grid_constant
   if (w == W_TMA) {
     // dy rows ([b, t, h, 64]); normalization is applied in fp32 (see cold / rinv_own)
     auto load_dn = [&](void* dst, uint64_t* bar, int blk) { tma_load_4d(dst, &tm_dn, bar, 0, hi, c0 + blk * 128, bi); };
-    if (l == 0) {
-      tma_prefetch(&tm_q);
-      tma_prefetch(&tm_k);
-      tma_prefetch(&tm_v);
-      tma_prefetch(&tm_dn);
-      mbar_expect_tx(f_full, 2 * T128);
+    // two issuing lanes (one per tensor): a thread completes one TMA copy per ~610
+    // cycles whatever its size (profiles/r01_bulk_copy_probe.txt)
+    if (l < 2) {
+      if (l == 0) {
+        tma_prefetch(&tm_q);
+        tma_prefetch(&tm_k);
+        tma_prefetch(&tm_v);
+        tma_prefetch(&tm_dn);
+        mbar_expect_tx(f_full, 2 * T128);
+      }
+      __syncwarp(3u);
       if (kKV) {
-        tma_load_4d(f0, &tm_k, f_full, 0, hi, c0 + B0 * 128, bi);
-        tma_load_4d(f1, &tm_v, f_full, 0, hi, c0 + B0 * 128, bi);
+        if (l == 0) tma_load_4d(f0, &tm_k, f_full, 0, hi, c0 + B0 * 128, bi);
+        if (l == 1) tma_load_4d(f1, &tm_v, f_full, 0, hi, c0 + B0 * 128, bi);
       } else {
-        tma_load_4d(f0, &tm_q, f_full, 0, hi, c0 + B0 * 128, bi);
-        load_dn(f1, f_full, B0);
+        if (l == 0) tma_load_4d(f0, &tm_q, f_full, 0, hi, c0 + B0 * 128, bi);
+        if (l == 1) load_dn(f1, f_full, B0);
       }
       for (int it = 0; it < nblk; ++it) {
         const int X = kKV ? B0 + it : it, st = it % NST;
         if (it >= NST) mbar_wait(&t_empty[st], ((it / NST) + 1) & 1);
-        mbar_expect_tx(&t_full[st], 2 * T128);
+        if (l == 0) mbar_expect_tx(&t_full[st], 2 * T128);
+        __syncwarp(3u);
         uint8_t* d0 = s0 + st * 2 * T128;
         if (kKV) {
-          tma_load_4d(d0, &tm_q, &t_full[st], 0, hi, c0 + X * 128, bi);
-          load_dn(d0 + T128, &t_full[st], X);
+          if (l == 0) tma_load_4d(d0, &tm_q, &t_full[st], 0, hi, c0 + X * 128, bi);
+          if (l == 1) load_dn(d0 + T128, &t_full[st], X);
         } else {
-          tma_load_4d(d0, &tm_k, &t_full[st], 0, hi, c0 + X * 128, bi);
-          tma_load_4d(d0 + T128, &tm_v, &t_full[st], 0, hi, c0 + X * 128, bi);
+          if (l == 0) tma_load_4d(d0, &tm_k, &t_full[st], 0, hi, c0 + X * 128, bi);
+          if (l == 1) tma_load_4d(d0 + T128, &tm_v, &t_full[st], 0, hi, c0 + X * 128, bi);
         }
       }
     }

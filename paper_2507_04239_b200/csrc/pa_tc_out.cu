@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
     }
     for (int i = 0; i < ST_ST; ++i) {
       mbar_init(&st_full[i], 1);
-      mbar_init(&st_empty[i], 1);
+      mbar_init(&st_empty[i], 2);   // a step pair: one commit per state-query issuer
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&a_full[i], 4);
@@ -147,30 +147,40 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
   const uint32_t tm = tmem_base;
 
   if (w == W_TMA_KV) {
-    if (l == 0) {
-      tma_prefetch(&tm_q);
-      tma_prefetch(&tm_k);
-      tma_prefetch(&tm_v);
-      mbar_expect_tx(q_full, QB);
-      tma_load_4d(q_s, &tm_q, q_full, 0, hi, c0 + I * 128, bi);
+    // one issuing lane per tensor: a thread completes one TMA copy per ~610 cycles
+    // whatever its size (profiles/r01_bulk_copy_probe.txt)
+    if (l < 2) {
+      if (l == 0) {
+        tma_prefetch(&tm_q);
+        tma_prefetch(&tm_k);
+        tma_prefetch(&tm_v);
+        mbar_expect_tx(q_full, QB);
+        tma_load_4d(q_s, &tm_q, q_full, 0, hi, c0 + I * 128, bi);
+      }
       for (int J = 0; J <= I; ++J) {
         const int st = J % KV_ST;
         if (J >= KV_ST) mbar_wait(&kv_empty[st], ((J / KV_ST) + 1) & 1);
-        mbar_expect_tx(&kv_full[st], KB + VB);
-        tma_load_4d(k_s + st * KB, &tm_k, &kv_full[st], 0, hi, c0 + J * 128, bi);
-        tma_load_4d(v_s + st * VB, &tm_v, &kv_full[st], 0, hi, c0 + J * 128, bi);
+        if (l == 0) mbar_expect_tx(&kv_full[st], KB + VB);
+        __syncwarp(3u);
+        if (l == 0) tma_load_4d(k_s + st * KB, &tm_k, &kv_full[st], 0, hi, c0 + J * 128, bi);
+        if (l == 1) tma_load_4d(v_s + st * VB, &tm_v, &kv_full[st], 0, hi, c0 + J * 128, bi);
       }
     }
   } else if (w == W_TMA_ST) {
-    if (l == 0 && has_state) {
+    constexpr int NL = den ? 3 : 2;
+    if (l < NL && has_state) {
       const __half* srcm = st_main + (size_t)(s * g.nsl + k) * ((size_t)FH * 64);
       const __half* srcd = st_den + (size_t)(s * g.nsl + k) * ((size_t)FH * 16);
-      for (int stp = 0; stp < NSTEP; ++stp) {
-        const int sb = stp % ST_ST;
+      // a PAIR of 128-slot steps per barrier, one 16 KB copy per lane: a thread
+      // completes one copy per ~690 cycles whatever its size
+      // (profiles/r01_bulk_copy_probe.txt), lanes overlap
+      for (int stp = 0; stp < NSTEP; stp += 2) {
+        const int sb = stp % ST_ST;   // 0 or 2: the pair occupies slots sb, sb + 1
         if (stp >= ST_ST) mbar_wait(&st_empty[sb], ((stp / ST_ST) + 1) & 1);
-        mbar_expect_tx(&st_full[sb], STB + (den ? STD : 0));
-        bulk_load(st_s + sb * STB, srcm + (size_t)stp * 128 * 64, STB, &st_full[sb]);
-        if (den) bulk_load(sd_s + sb * STD, srcd + (size_t)stp * 128 * 16, STD, &st_full[sb]);
+        if (l == 0) mbar_expect_tx(&st_full[sb], 2 * (STB + (den ? STD : 0)));
+        __syncwarp((1u << NL) - 1u);
+        if (l < 2) bulk_load(st_s + (sb + l) * STB, srcm + (size_t)(stp + l) * 128 * 64, STB, &st_full[sb]);
+        if (den && l == 2) bulk_load(sd_s + sb * STD, srcd + (size_t)stp * 128 * 16, 2 * STD, &st_full[sb]);
       }
     }
   } else if (w == W_MMA_ST || w == W_MMA_ST + 1) {
@@ -187,7 +197,7 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
           const int bb = stp & 1, sb = stp % ST_ST;
           mbar_wait_w(&a_full[bb], (stp >> 1) & 1);
           PA_TR4(trb, 10 + stp * 3 + 0);
-          mbar_wait_w(&st_full[sb], (stp / ST_ST) & 1);
+          mbar_wait_w(&st_full[sb & ~1], (stp / ST_ST) & 1);
           PA_TR4(trb, 10 + stp * 3 + 1);
           tc_fence_after();
           const uint64_t so = (uint64_t)((sb * STB) >> 4), sdo = (uint64_t)((sb * STD) >> 4);
@@ -199,7 +209,7 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
             if (den) mma_ts_w(tm + TOS + 64, ab + kk * 8, sd0 + sdo + (uint64_t)(kk * 32), id16mn_h, 1u);
           }
           tc_commit_w(&a_empty[bb]);
-          tc_commit_w(&st_empty[sb]);
+          tc_commit_w(&st_empty[sb & ~1]);
           PA_TR4(trb, 10 + stp * 3 + 2);
         }
       }

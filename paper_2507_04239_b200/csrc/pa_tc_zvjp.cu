@@ -186,7 +186,10 @@ __global__ void __launch_bounds__(zv::THREADS, 1)
   PA_TR6(trc && tid == 0, 0);
 
   if (w == W_TMA) {
-    if (l == 0) {
+    // four issuing lanes: a thread completes one copy per ~690 cycles whatever its
+    // size (profiles/r01_bulk_copy_probe.txt); lane i copies E tile i of a stage
+    // and row box i of a tile
+    if (l < 4) {
       int gb = 0;
       for (int it = 0, ti = blockIdx.x; ti < ntiles; ++it, ti += gridDim.x) {
         const ZvTile t = zv_tile(ti, nI, nk, kbeg);
@@ -195,25 +198,27 @@ __global__ void __launch_bounds__(zv::THREADS, 1)
         // token rows of this tile (single buffer: the generating warps release it
         // as soon as their rows are in registers)
         if (it >= 1) mbar_wait(rows_empty, (it - 1) & 1);
-        mbar_expect_tx(rows_full, 2 * TOK * 128);
-#pragma unroll
-        for (int bx = 0; bx < NBOX; ++bx) {
-          tma_load_4d(xrow_s + bx * 16384, &tm_x, rows_full, 0, hi, tok0 + bx * 128, bi);
-          if (kUpd || u_bf16_bth)
+        if (l == 0) mbar_expect_tx(rows_full, 2 * TOK * 128);
+        __syncwarp(15u);
+        if (l < 2 * NBOX) {
+          const int bx = l >> 1;
+          if ((l & 1) == 0)
+            tma_load_4d(xrow_s + bx * 16384, &tm_x, rows_full, 0, hi, tok0 + bx * 128, bi);
+          else if (kUpd || u_bf16_bth)
             tma_load_4d(urow_s + bx * 16384, &tm_u, rows_full, 0, hi, tok0 + bx * 128, bi);
           else
             tma_load_2d(urow_s + bx * 16384, &tm_u, rows_full, 0, t.s * g.t + tok0 + bx * 128);
         }
         const uint8_t* Eb = (const uint8_t*)(E + (size_t)(t.s * g.nsl + t.k) * NBT * (TILE / 2));
-        // one thread completes one bulk copy per ~690 cycles whatever its size
-        // (tools/l2_stream.cu): 32 KB copies of four E tiles keep up with the MMAs
         for (int m = 0; m < NBS; ++m, ++gb) {
           const int sb = gb % NSB;
           const int ntl = (m + 1) * TPS <= NBT ? TPS : NBT - m * TPS;
           if (gb >= NSB) mbar_wait(&b_empty[sb], ((gb / NSB) + 1) & 1);
-          PA_TR6(trc && it == 2, 100 + m);
-          mbar_expect_tx(&b_full[sb], ntl * TILE);
-          bulk_load(b_s + sb * TPS * TILE, Eb + (size_t)m * TPS * TILE, ntl * TILE, &b_full[sb]);
+          PA_TR6(trc && it == 2 && l == 0, 100 + m);
+          if (l == 0) mbar_expect_tx(&b_full[sb], ntl * TILE);
+          __syncwarp(15u);
+          if (l < ntl)
+            bulk_load(b_s + (sb * TPS + l) * TILE, Eb + (size_t)(m * TPS + l) * TILE, TILE, &b_full[sb]);
         }
       }
     }
