@@ -27,8 +27,8 @@
 // Persistent, one CTA per SM, tiles of (stream, chunk, token block) strided over
 // the grid.  Warp roles: w0..w7 generate A (group gq = w/4 owns TMEM lane
 // quadrant w%4; query: gq = token half, update: gq = 0 -> Z (dk), 1 -> Y (dv));
-// w8 TMA (E tiles, token rows); w9/w10 MMA issuers over alternating stages;
-// w11..w18 epilogue.  TMEM: one accumulator [0, 128), zeroed and handed back by
+// w8 TMA (E tiles); w19 TMA (token rows, one tile ahead); w9/w10 MMA issuers
+// over alternating stages; w11..w18 epilogue.  TMEM: one accumulator [0, 128), zeroed and handed back by
 // the epilogue right after it is read (the stores run under the next tile's
 // MMAs, the generators run up to three stages into the next tile); A stages
 // 3 x 128 columns [128, 512) (two E tiles x two groups x 32 columns): 16 MMAs
@@ -67,11 +67,11 @@ constexpr int TPS = 4;           // E tiles per B stage
 constexpr int NSA = 3;           // A stages in TMEM (two E tiles each)
 constexpr int NGEN = 256;        // token rows per tile (x words are kept per row)
 constexpr int NGW = 8;           // generating warps: 2 groups x 4 lane quadrants
-constexpr int THREADS = 608;
-constexpr int W_TMA = 8, W_MMA = 9, W_EPI = 11;   // MMA issuers: w9 (even stages), w10 (odd stages)
+constexpr int THREADS = 640;
+constexpr int W_TMA = 8, W_MMA = 9, W_EPI = 11, W_ROWS = 19;   // MMA issuers: w9 (even stages), w10 (odd stages)
 constexpr int ROWS = 256 * 128;  // token rows of one operand (up to 256 tokens, bf16, SW128)
 constexpr int XW = 32 * NGEN * 4;   // fp16 x words, [word][thread]
-constexpr int SMEM = 1024 + NSB * TPS * TILE + 2 * ROWS + XW + 2 * 256 * 4 + 512;
+constexpr int SMEM = 1024 + NSB * TPS * TILE + 2 * ROWS + XW + 4 * 256 * 4 + 16 + 512;
 }  // namespace zv
 
 // 2^-floor(log2(m)) for m > 0 (so m * p in [1, 2)), 1 for m == 0
@@ -142,7 +142,8 @@ __global__ void __launch_bounds__(zv::THREADS, 1)
   uint8_t* urow_s = xrow_s + ROWS;
   uint32_t* xw = (uint32_t*)(urow_s + ROWS);
   float* meta = (float*)(xw + 32 * NGEN);   // [2][256] per-token factor
-  uint64_t* bars = (uint64_t*)(meta + 2 * 256);
+  float* scal = meta + 2 * 256;             // [2][256] this tile's ell, dden (loaded with the rows) + lamlog
+  uint64_t* bars = (uint64_t*)(scal + 2 * 256 + 4);
   uint64_t* b_full = bars;
   uint64_t* b_empty = b_full + NSB;
   uint64_t* a_full = b_empty + NSB;
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(zv::THREADS, 1)
       mbar_init(&meta_full[i], 8);
       mbar_init(&meta_empty[i], 8);
     }
-    mbar_init(rows_full, 1);
+    mbar_init(rows_full, 2);   // TMA bytes + the loader warp's scalar stores
     mbar_init(rows_empty, NGW);
     fence_barrier_init();
   }
@@ -193,22 +194,6 @@ __global__ void __launch_bounds__(zv::THREADS, 1)
       int gb = 0;
       for (int it = 0, ti = blockIdx.x; ti < ntiles; ++it, ti += gridDim.x) {
         const ZvTile t = zv_tile(ti, nI, nk, kbeg);
-        const int tok0 = t.k * g.c + t.I * TOK;
-        const int bi = t.s / g.h, hi = t.s - bi * g.h;
-        // token rows of this tile (single buffer: the generating warps release it
-        // as soon as their rows are in registers)
-        if (it >= 1) mbar_wait(rows_empty, (it - 1) & 1);
-        if (l == 0) mbar_expect_tx(rows_full, 2 * TOK * 128);
-        __syncwarp(15u);
-        if (l < 2 * NBOX) {
-          const int bx = l >> 1;
-          if ((l & 1) == 0)
-            tma_load_4d(xrow_s + bx * 16384, &tm_x, rows_full, 0, hi, tok0 + bx * 128, bi);
-          else if (kUpd || u_bf16_bth)
-            tma_load_4d(urow_s + bx * 16384, &tm_u, rows_full, 0, hi, tok0 + bx * 128, bi);
-          else
-            tma_load_2d(urow_s + bx * 16384, &tm_u, rows_full, 0, t.s * g.t + tok0 + bx * 128);
-        }
         const uint8_t* Eb = (const uint8_t*)(E + (size_t)(t.s * g.nsl + t.k) * NBT * (TILE / 2));
         for (int m = 0; m < NBS; ++m, ++gb) {
           const int sb = gb % NSB;
@@ -222,6 +207,38 @@ __global__ void __launch_bounds__(zv::THREADS, 1)
         }
       }
     }
+  } else if (w == W_ROWS) {
+    // token rows, one tile ahead of the generating warps (single buffer: they
+    // release it as soon as their rows are in registers), in its own warp so the
+    // next tile's rows do not queue behind this tile's E stream; the tile's
+    // per-token scalars go to shared memory with them (loaded by the generating
+    // warps themselves, their HBM latency sat in every tile prologue)
+    for (int it = 0, ti = blockIdx.x; ti < ntiles; ++it, ti += gridDim.x) {
+      const ZvTile t = zv_tile(ti, nI, nk, kbeg);
+      const int tok0 = t.k * g.c + t.I * TOK;
+      const int bi = t.s / g.h, hi = t.s - bi * g.h;
+      if (it >= 1) mbar_wait(rows_empty, (it - 1) & 1);
+      __syncwarp();
+      if (l == 0) mbar_expect_tx(rows_full, 2 * TOK * 128);
+      __syncwarp();
+      if (l < 2 * NBOX) {
+        const int bx = l >> 1;
+        if ((l & 1) == 0)
+          tma_load_4d(xrow_s + bx * 16384, &tm_x, rows_full, 0, hi, tok0 + bx * 128, bi);
+        else if (kUpd || u_bf16_bth)
+          tma_load_4d(urow_s + bx * 16384, &tm_u, rows_full, 0, hi, tok0 + bx * 128, bi);
+        else
+          tma_load_2d(urow_s + bx * 16384, &tm_u, rows_full, 0, t.s * g.t + tok0 + bx * 128);
+      }
+      for (int i = l; i < TOK; i += 32) {
+        const bool in = t.I * TOK + i < g.c;
+        scal[i] = in ? ell[(size_t)t.s * g.t + tok0 + i] : 0.f;
+        if (den && !kUpd) scal[256 + i] = in ? __half2float(u16[((size_t)t.s * g.t + tok0 + i) * 16]) : 0.f;
+      }
+      if (l == 0) scal[512] = (kUpd && g.gated) ? lamlog[t.s * g.n + t.k] : 0.f;
+      __syncwarp();
+      if (l == 0) mbar_arrive(rows_full);
+    }
   } else if (w == W_MMA || w == W_MMA + 1) {
     // two issuers over alternating stages (global stage parity): one waits on its
     // barriers while the other's MMAs run.  Accumulators are zeroed by the
@@ -233,7 +250,7 @@ __global__ void __launch_bounds__(zv::THREADS, 1)
     const uint64_t bn0 = smem_desc(smem_u32(b_s), 8192, 1024, 2);
     int gs0 = 0;
 #ifdef PA_TRACE
-    long long wb = 0, wa = 0, wi = 0;
+    long long wb = 0, wa = 0, wi = 0, we = 0;
 #endif
     for (int it = 0, ti = blockIdx.x; ti < ntiles; ++it, ti += gridDim.x, gs0 += NJ) {
       bool first = true;
@@ -241,7 +258,13 @@ __global__ void __launch_bounds__(zv::THREADS, 1)
         const int gs = gs0 + j;
         if ((gs & 1) != mw) continue;
         if (first) {
+#ifdef PA_TRACE
+          long long c9 = clock64();
+#endif
           mbar_wait_w(acc_empty, it & 1);
+#ifdef PA_TRACE
+          we += clock64() - c9;
+#endif
           first = false;
         }
         const int m = (2 * j) / TPS, gb = it * NBS + m, sb = gb % NSB, sa = gs % NSA;
@@ -304,7 +327,7 @@ __global__ void __launch_bounds__(zv::THREADS, 1)
       g_trace6[(kUpd ? 0 : 1024) + 700 + mw * 4 + 0] = wb;
       g_trace6[(kUpd ? 0 : 1024) + 700 + mw * 4 + 1] = wa;
       g_trace6[(kUpd ? 0 : 1024) + 700 + mw * 4 + 2] = wi;
-      g_trace6[(kUpd ? 0 : 1024) + 700 + mw * 4 + 3] = clock64();
+      g_trace6[(kUpd ? 0 : 1024) + 700 + mw * 4 + 3] = we;
     }
 #endif
   } else if (w < NGW) {
@@ -316,79 +339,115 @@ __global__ void __launch_bounds__(zv::THREADS, 1)
     const bool ub = kUpd || u_bf16_bth;
     const int rr = kUpd ? row : gq * 128 + row;   // row in the tile's row buffers
     const uint32_t roff = (uint32_t)(rr >> 7) * 16384u + (uint32_t)(rr & 127) * 128u;
-    // per-token scalars of the next tile are loaded one tile ahead
-    auto scalars = [&](int ti, float& lt, float& lend, float& dsc) {
-      lt = 0.f;
-      lend = 0.f;
-      dsc = 0.f;
-      if (ti >= ntiles) return;
-      const ZvTile t = zv_tile(ti, nI, nk, kbeg);
-      const int tok = t.k * g.c + t.I * TOK + rr;
-      if (t.I * TOK + rr >= g.c) return;
-      lt = ell[(size_t)t.s * g.t + tok];
-      if (kUpd && g.gated) lend = lamlog[t.s * g.n + t.k];
-      if (den) dsc = kUpd ? 1.f : __half2float(u16[((size_t)t.s * g.t + tok) * 16]);
-    };
 #ifdef PA_TRACE
-    long long gw = 0;
+    long long gw = 0, gp = 0, gr = 0, gm = 0;
 #endif
-    float n_lt, n_lend, n_dsc;
-    scalars(blockIdx.x, n_lt, n_lend, n_dsc);
     int gs0 = 0;
     for (int it = 0, ti = blockIdx.x; ti < ntiles; ++it, ti += gridDim.x, gs0 += NJ) {
       const ZvTile t = zv_tile(ti, nI, nk, kbeg);
       const int ab = it & 1;
       const bool live = t.I * TOK + rr < g.c;
-      const float lt = n_lt, lend = n_lend, dsc = n_dsc;
-      scalars(ti + gridDim.x, n_lt, n_lend, n_dsc);
       // undo the stored power-of-two scale of the state
       const float sscale =
           1.f / (kUpd ? pow2_neg_bits(g.ng - 1 - (g.k0 + t.k)) : pow2_neg_bits(g.k0 + t.k - 1));
       uint32_t vr[32];
-      float px, pv;
+      float px, pv, lt, lend, dsc;
+      PA_TR6(trc && it == 5 && tid == 0, 805);
+      PA_TR6(trc && it == 4 && tid == 0, 806);
+#ifdef PA_TRACE
+      long long cp0 = clock64();
+#endif
       {
         mbar_wait(rows_full, it & 1);
-        uint4 xv[8], uv[8];
+#ifdef PA_TRACE
+        gr += clock64() - cp0;
+#endif
+        PA_TR6(trc && it == 5 && tid == 0, 800);
+        lt = scal[rr];
+        lend = scal[512];
+        dsc = (den && !kUpd) ? scal[256 + rr] : (kUpd ? 1.f : 0.f);
+        // two passes over each shared-memory row (max, then scaled conversion) keep
+        // the register footprint at the 32 words of u: holding both rows and their
+        // conversions spilled and cost ~7K cycles per tile
+        auto chunk = [&](const uint8_t* base, int c8) {
+          return *(const uint4*)(base + roff + (((uint32_t)c8 ^ (uint32_t)(rr & 7)) << 4));
+        };
+        auto chunk_max = [&](uint4 v4, bool is_bf16, float m) {
+          const uint32_t* pv4 = (const uint32_t*)&v4;
+#pragma unroll
+          for (int e2 = 0; e2 < 4; ++e2) {
+            const float2 f2 = is_bf16 ? __bfloat1622float2(*(const __nv_bfloat162*)&pv4[e2])
+                                      : __half22float2(*(const __half2*)&pv4[e2]);
+            m = fmaxf(m, fmaxf(fabsf(f2.x), fabsf(f2.y)));
+          }
+          return m;
+        };
+        auto chunk_f16 = [&](uint4 v4, bool is_bf16, float p, uint32_t* o) {
+          const uint32_t* pv4 = (const uint32_t*)&v4;
+#pragma unroll
+          for (int e2 = 0; e2 < 4; ++e2) {
+            const float2 f2 = is_bf16 ? __bfloat1622float2(*(const __nv_bfloat162*)&pv4[e2])
+                                      : __half22float2(*(const __half2*)&pv4[e2]);
+            o[e2] = pack_f16(f2.x * p, f2.y * p);
+          }
+        };
+        float mx = 0.f, mu = fabsf(dsc);
 #pragma unroll
         for (int c8 = 0; c8 < 8; ++c8) {
-          const uint32_t o = roff + (((uint32_t)c8 ^ (uint32_t)(rr & 7)) << 4);
-          xv[c8] = *(const uint4*)(xrow_s + o);
-          if (!u_is_x) uv[c8] = *(const uint4*)(urow_s + o);
+          mx = chunk_max(chunk(xrow_s, c8), true, mx);
+          if (!u_is_x) mu = chunk_max(chunk(urow_s, c8), ub, mu);
         }
-        __syncwarp();
-        if (l == 0) mbar_arrive(rows_empty);
         // x (the bcast factor) and the vector operand u, both scaled by powers of two
         // into [1, 2) so fp16 products keep their precision for any input range
-        px = pow2_norm(row_max(xv, true));
-        uint32_t xh[32];
-        row_f16(xv, true, px, xh);
+        px = pow2_norm(mx);
+        pv = u_is_x ? px : pow2_norm(mu);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) xw[i * NGEN + xt] = live ? xh[i] : 0u;
-        if (u_is_x) {
-          pv = px;
+        for (int c8 = 0; c8 < 8; ++c8) {
+          uint32_t o[4];
+          chunk_f16(chunk(xrow_s, c8), true, px, o);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) vr[i] = live ? xh[i] : 0u;
-        } else {
-          pv = pow2_norm(fmaxf(row_max(uv, ub), fabsf(dsc)));
-          row_f16(uv, ub, pv, vr);
+          for (int e2 = 0; e2 < 4; ++e2) {
+            xw[(c8 * 4 + e2) * NGEN + xt] = live ? o[e2] : 0u;
+            if (u_is_x) vr[c8 * 4 + e2] = live ? o[e2] : 0u;
+          }
+          if (!u_is_x) chunk_f16(chunk(urow_s, c8), ub, pv, &vr[c8 * 4]);
         }
+        PA_TR6(trc && it == 5 && tid == 0, 801);
+        __syncwarp();
+        if (l == 0) mbar_arrive(rows_empty);
+        PA_TR6(trc && it == 5 && tid == 0, 802);
       }
       // per-token factor for the epilogue: query c_m = sigma^2 gp_m, update
       // W_j = exp(lend - ell_j); dv counts each unordered pair twice (1/2)
       float fct = sscale * (kUpd ? (g.gated ? __expf(lend - lt) : 1.f) : g.scale * g.scale * __expf(lt));
       fct /= px * pv;
       if (kUpd && gq == 1) fct *= 0.5f;
+#ifdef PA_TRACE
+      long long cm0 = clock64();
+#endif
+      PA_TR6(trc && it == 5 && tid == 0, 803);
       if (it >= 2) mbar_wait(&meta_empty[ab], ((it >> 1) + 1) & 1);   // the epilogue of tile it-2 has read its factors
+      PA_TR6(trc && it == 5 && tid == 0, 804);
+#ifdef PA_TRACE
+      gm += clock64() - cm0;
+#endif
       meta[ab * 256 + gq * 128 + row] = fct;
       __syncwarp();
       if (l == 0) mbar_arrive(&meta_full[ab]);
+#ifdef PA_TRACE
+      gp += clock64() - cp0;
+#endif
+      PA_TR6(trc && it == 5 && tid == 0, 807);
 
+      // the release of the next stage's A slot is tested while this stage's stores
+      // drain (a blocking wait costs ~160 cycles even on a completed phase)
+      bool nxt_ready = gs0 < NSA;
       for (int j = 0; j < NJ; ++j) {
         const int gs = gs0 + j, sa = gs % NSA;
 #ifdef PA_TRACE
         long long c0 = clock64();
 #endif
-        if (gs >= NSA) mbar_wait(&a_empty[sa], ((gs / NSA) + 1) & 1);
+        if (gs >= NSA && !__all_sync(0xffffffffu, nxt_ready)) mbar_wait(&a_empty[sa], ((gs / NSA) + 1) & 1);
 #ifdef PA_TRACE
         gw += clock64() - c0;
 #endif
@@ -420,6 +479,10 @@ __global__ void __launch_bounds__(zv::THREADS, 1)
             }
           }
         }
+        {
+          const int g1 = gs + 1;
+          nxt_ready = g1 < NSA || mbar_test_wait(&a_empty[g1 % NSA], ((g1 / NSA) + 1) & 1);
+        }
         tc_wait_st();
         tc_fence_before();
         __syncwarp();
@@ -430,10 +493,12 @@ __global__ void __launch_bounds__(zv::THREADS, 1)
 #ifdef PA_TRACE
     if (trc && l == 0) {
       g_trace6[(kUpd ? 0 : 1024) + 720 + w * 2] = gw;
-      g_trace6[(kUpd ? 0 : 1024) + 721 + w * 2] = clock64();
+      g_trace6[(kUpd ? 0 : 1024) + 721 + w * 2] = gp;
+      g_trace6[(kUpd ? 0 : 1024) + 760 + w * 2] = gr;
+      g_trace6[(kUpd ? 0 : 1024) + 761 + w * 2] = gm;
     }
 #endif
-  } else if (w >= W_EPI) {
+  } else if (w >= W_EPI && w < W_EPI + 8) {
     // epilogue: read the accumulator, zero it and hand it back, then add the fp32
     // intra-chunk part and store the final bf16 gradient rows
     const int e = w - W_EPI, gq = e >> 2, qd = w & 3, row = qd * 32 + l;
@@ -456,6 +521,21 @@ __global__ void __launch_bounds__(zv::THREADS, 1)
       const bool live = t.I * TOK + rr < g.c;
       const int tok = t.k * g.c + t.I * TOK + rr;
       const bool is_dv = kUpd && gq == 1;
+      {
+        // the next tile's epilogue operands go to L2 now (a tile ahead): from HBM under
+        // this kernel's load each dependent round trip costs several thousand cycles
+        const int tn = ti + (int)gridDim.x;
+        if (tn < ntiles) {
+          const ZvTile u = zv_tile(tn, nI, nk, kbeg);
+          const int tokn = u.k * g.c + u.I * TOK + rr;
+          if (u.I * TOK + rr < g.c) {
+            const char* o = (const char*)((is_dv ? dv32 : dx32) + ((size_t)u.s * g.t + tokn) * HD);
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(o));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(o + 128));
+            if (!is_dv) asm volatile("prefetch.global.L2 [%0];" ::"l"(xraw + rowid(g, u.s, tokn) * HD));
+          }
+        }
+      }
       mbar_wait(&meta_full[ab], (it >> 1) & 1);
       const float fct = meta[ab * 256 + gq * 128 + row];
       __syncwarp();
