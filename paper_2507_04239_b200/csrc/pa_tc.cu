@@ -914,6 +914,16 @@ int tc_sp_combine(const Geo& g, const void* fwd_ws, const float* carry, const fl
   return cuda_check("sp combine");
 }
 
+// one non-blocking side stream per device (created on first use)
+static cudaStream_t side_stream() {
+  static cudaStream_t ss[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!ss[dev]) cudaStreamCreateWithFlags(&ss[dev], cudaStreamNonBlocking);
+  return ss[dev];
+}
+
 int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const float* log_g, const void* y,
                 const float* rowsum, const void* dy, void* dq, void* dk, void* dv, float* dlog_g, const void* fwd_ws,
                 void* bwd_ws, cudaStream_t st, int mode, const float* carry, float* pre_out) {
@@ -949,6 +959,39 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
   const bool zf = !old_dphi;
   if (red_bytes > 48 * 1024)
     cudaFuncSetAttribute(k_tc_scan_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, red_bytes);
+  // The intra-chunk VJP depends only on the prologue; PA_BWD_OVERLAP=1 runs it on a
+  // side stream next to the dA' GEMM and the reverse scan.  Measured on B200 it
+  // does not pay (22.3 vs 21.9 ms per step: the dA' CTAs take every SM first, then
+  // the intra-chunk kernel and the scan slow each other), so one stream is the default.
+  static const bool serial = [] {
+    const char* e = getenv("PA_BWD_OVERLAP");
+    return !(e && e[0] == '1');
+  }();
+  cudaStream_t st2 = serial ? st : side_stream();
+  cudaEvent_t ev_in = nullptr, ev_ib = nullptr;
+  auto launch_intra = [&]() -> int {
+    if (!serial) {
+      cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&ev_ib, cudaEventDisableTiming);
+      cudaEventRecord(ev_in, st);
+      cudaStreamWaitEvent(st2, ev_in, 0);
+    }
+    {
+      StageTimer tmr("bwd_intra", st2);
+      CUtensorMap m_q128, m_k128, m_dy128;
+      if (!map_bth(&m_q128, q, g, 128) || !map_bth(&m_k128, k, g, 128) || !map_bth(&m_dy128, dy, g, 128)) return 3;
+      tc_intra_bwd(g, m_q128, m_k128, m_v128, m_dy128, w.ell, b.dden, rowsum, b.dk32, b.dv32, b.dq32, b.dell,
+                   st2);
+    }
+    if (!serial) cudaEventRecord(ev_ib, st2);
+    return 0;
+  };
+  auto join_intra = [&]() {
+    if (serial) return;
+    cudaStreamWaitEvent(st, ev_ib, 0);
+    cudaEventDestroy(ev_in);
+    cudaEventDestroy(ev_ib);
+  };
   if (mode != 2) {
   {
     StageTimer tmr("bwd_prep", st);
@@ -965,6 +1008,7 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
         g, den ? 1 : 3, den ? b.dN : (const __nv_bfloat16*)dy, w.ell, w.lamlog, den ? b.dden : nullptr, w.vr,
         den ? w.wa : nullptr);
   }
+  if (mode == 0 && launch_intra()) return 3;
   if (g.n - 1 + g.prefix > 0) {
     StageTimer tmr("bwd_query_state_dA", st);
     auto fn = den ? k_tc_featmajor<true, 1> : k_tc_featmajor<true, 0>;
@@ -981,22 +1025,14 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
     return cuda_check("tc backward (sp local)");
   }
   }
+  if (mode == 2 && launch_intra()) return 3;
   {
     StageTimer tmr("bwd_discumsum", st);
     k_tc_scan_bwd<<<dim3(scan_blocks(uc), g.ns), 256, red_bytes, st>>>(g, uc, w.lamlog, w.sp, w.stm, w.std_,
                                                                           b.dsm, b.dsd, b.dlam, carry, pre_out, 1,
                                                                           zf ? b.ea : nullptr, zf ? b.eg : nullptr, nbt);
   }
-  {
-    StageTimer tmr("bwd_intra", st);
-    CUtensorMap m_q128, m_k128;
-    if (!map_bth(&m_q128, q, g, 128) || !map_bth(&m_k128, k, g, 128)) {
-      return 3;
-    }
-    CUtensorMap m_dy128;
-    if (!map_bth(&m_dy128, dy, g, 128)) return 3;
-    tc_intra_bwd(g, m_q128, m_k128, m_v128, m_dy128, w.ell, b.dden, rowsum, b.dk32, b.dv32, b.dq32, b.dell, st);
-  }
+  join_intra();
   {
     StageTimer tmr("bwd_query_state_dq", st);
     if (zf) {
