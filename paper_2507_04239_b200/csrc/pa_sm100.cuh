@@ -5,6 +5,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <cstdio>
 
 namespace pa {
 namespace sm100 {
@@ -71,7 +72,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
   uint32_t spins = 0;
   while (!mbar_try_wait(bar, parity)) {
-    if (++spins > 20000000u) __trap();
+    if (++spins > 20000000u) {
+#ifdef PA_MBAR_DEBUG
+      printf("mbar timeout: block %d thread %d bar smem+0x%x parity %u\n", (int)blockIdx.x, (int)threadIdx.x,
+             smem_u32(bar), parity);
+#endif
+      __trap();
+    }
   }
 }
 
