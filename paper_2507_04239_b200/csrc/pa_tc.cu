@@ -185,7 +185,7 @@ template <bool kBwd, int kDen>
 __global__ void __launch_bounds__(fm::THREADS, 2) k_tc_featmajor(const __grid_constant__ CUtensorMap tm_xt,
                                                          const __grid_constant__ CUtensorMap tm_b,
                                                          const __grid_constant__ CUtensorMap tm_b16, Geo g,
-                                                         float* out) {
+                                                         void* out) {
   using namespace fm;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keep the shared address space
@@ -362,15 +362,29 @@ __global__ void __launch_bounds__(fm::THREADS, 2) k_tc_featmajor(const __grid_co
     for (int u = 0; u < TPW; ++u) {
       const int t = tp * TPW + u;
       if (!act[u]) continue;
-      float* dst = out + (((size_t)(s * g.nsl + slot) * FH) + (size_t)(t0 + t) * 128 + q * 32 + l) * UW;
+      const size_t row = ((size_t)(s * g.nsl + slot) * FH) + (size_t)(t0 + t) * 128 + q * 32 + l;
       for (int c0 = 0; c0 < ncols; c0 += 16) {
         uint32_t r[16];
         tmem_ld16(tm + (uint32_t)(t * ACC_W) + lane_off + c0, r);
         tc_wait_ld();
+        if (kBwd) {
+          // dA' stays fp32: its rounding reaches the gate gradient through
+          // dlambda = <slot, G> (fp16 dA' moved dlog g past the 2e-2 bar)
+          float* dst = (float*)out + row * UW;
 #pragma unroll
-        for (int c = 0; c < 16; c += 4)
-          *(float4*)(dst + c0 + c) = make_float4(__uint_as_float(r[c]), __uint_as_float(r[c + 1]),
-                                                 __uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
+          for (int c = 0; c < 16; c += 4)
+            *(float4*)(dst + c0 + c) = make_float4(__uint_as_float(r[c]), __uint_as_float(r[c + 1]),
+                                                   __uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
+        } else {
+          // S'_k goes to HBM as fp16 x 2^-10 (the scan accumulates in fp32)
+          __half* dst = (__half*)out + row * UW;
+          uint32_t h[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            h[c] = pack_f16(__uint_as_float(r[2 * c]) * kSpScale, __uint_as_float(r[2 * c + 1]) * kSpScale);
+          *(uint4*)(dst + c0) = make_uint4(h[0], h[1], h[2], h[3]);
+          *(uint4*)(dst + c0 + 8) = make_uint4(h[4], h[5], h[6], h[7]);
+        }
       }
     }
   }
@@ -410,8 +424,16 @@ __device__ __forceinline__ uint8_t* state_elem_ptr(__half* st_main, __half* st_d
                 : (uint8_t*)(st_den + sk * ST_DEN) + sw32_elem(f, u - 64);
 }
 
+// 4 consecutive fp16 partial sums (x 2^-10, see the feature-major epilogue) -> fp32
+__device__ __forceinline__ float4 ld_sp4(const __half* p) {
+  const uint2 v = __ldcs((const uint2*)p);
+  const float2 a = __half22float2(*(const __half2*)&v.x), b = __half22float2(*(const __half2*)&v.y);
+  constexpr float inv = 1.f / kSpScale;
+  return make_float4(a.x * inv, a.y * inv, b.x * inv, b.y * inv);
+}
+
 __global__ void __launch_bounds__(256) k_tc_scan_fwd(Geo g, int ucols, const float* __restrict__ lamlog,
-                                                     const float* __restrict__ sp, __half* st_main,
+                                                     const __half* __restrict__ sp, __half* st_main,
                                                      __half* st_den, const float* __restrict__ carry,
                                                      float* end_out, int write) {
   // slot j+1 = lambda_j slot_j + omega S'_j; slot 0 = carry (the state flowing in
@@ -421,7 +443,7 @@ __global__ void __launch_bounds__(256) k_tc_scan_fwd(Geo g, int ucols, const flo
   if (e >= FH * ucols) return;
   const int f = e / ucols, u = e - f * ucols;
   const float om = slot_omega(f);
-  const float* src = sp + ((size_t)s * g.nsl * FH + f) * UW + u;
+  const __half* src = sp + ((size_t)s * g.nsl * FH + f) * UW + u;
   const size_t kstride = (size_t)FH * UW;
   const size_t cidx = ((size_t)s * FH + f) * UW + u;
   float4 acc = carry ? *(const float4*)(carry + cidx) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -434,7 +456,7 @@ __global__ void __launch_bounds__(256) k_tc_scan_fwd(Geo g, int ucols, const flo
     float4 x[SCAN_PF];
 #pragma unroll
     for (int i = 0; i < SCAN_PF; ++i)
-      if (k0 + i < g.n) x[i] = __ldcs((const float4*)(src + (size_t)(k0 + i) * kstride));
+      if (k0 + i < g.n) x[i] = ld_sp4(src + (size_t)(k0 + i) * kstride);
 #pragma unroll
     for (int i = 0; i < SCAN_PF; ++i) {
       const int k = k0 + i;
@@ -687,7 +709,7 @@ struct TcFwdWs {
   __half* kt;            // K^T   [ns*n*64][c]  exact fp16 transposed copy (reused for Q^T in the backward)
   __half* vr;            // W_m v_m rows [ns*t][64] (reused for c_m dnum_m in the backward)
   __half* wa;            // (W_m, 0..) rows [ns*t][16] (reused for (c_m dden_m, 0..))
-  float* sp;             // S'_k fp32 [ns][n][FH][80] (reused for dA' in the backward)
+  void* sp;              // S'_k x 2^-10, fp16 [ns][n][FH][80]; reused for dA' (fp32) in the backward
   __half* stm;           // A'_k 2^-nbits(k) [ns][n][FH][64]
   __half* std_;          // score-sum part [ns][n][FH][16]
   float* y32;
@@ -732,7 +754,7 @@ static TcFwdWs carve_fwd(const Geo& g, void* base, size_t* bytes) {
   w.kt = (__half*)take(2ull * g.ns * g.t * HD);
   w.vr = (__half*)take(2ull * g.ns * g.t * HD);
   w.wa = (__half*)take(2ull * g.ns * g.t * 16);
-  w.sp = (float*)take(4ull * g.ns * g.nsl * FH * UW);
+  w.sp = take(4ull * g.ns * g.nsl * FH * UW);
   w.stm = (__half*)take(2ull * g.ns * g.nsl * ST_MAIN);
   w.std_ = (__half*)take(2ull * g.ns * g.nsl * ST_DEN);
   w.y32 = (float*)take(g.normalize ? 4ull * g.ns * g.t * HD : 0);
@@ -864,7 +886,7 @@ int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const 
     cudaMemsetAsync(w.zflag, 0, 4, st);
     {
       StageTimer tmr("fwd_discumsum", st);
-      k_tc_scan_fwd<<<dim3((FH * uc / 4 + 255) / 256, g.ns), 256, 0, st>>>(g, uc, w.lamlog, w.sp, w.stm, w.std_,
+      k_tc_scan_fwd<<<dim3((FH * uc / 4 + 255) / 256, g.ns), 256, 0, st>>>(g, uc, w.lamlog, (const __half*)w.sp, w.stm, w.std_,
                                                                            carry, nullptr, 1);
     }
     {
@@ -890,7 +912,7 @@ int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const 
   }
   {
     StageTimer tmr("fwd_discumsum", st);
-    k_tc_scan_fwd<<<dim3((FH * uc / 4 + 255) / 256, g.ns), 256, 0, st>>>(g, uc, w.lamlog, w.sp, w.stm, w.std_,
+    k_tc_scan_fwd<<<dim3((FH * uc / 4 + 255) / 256, g.ns), 256, 0, st>>>(g, uc, w.lamlog, (const __half*)w.sp, w.stm, w.std_,
                                                                          carry, end_out, mode == 1 ? 0 : 1);
   }
   if (mode == 1) {
@@ -1018,7 +1040,7 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
   }
   if (mode == 1) {
     StageTimer tmr("bwd_discumsum", st);
-    k_tc_scan_bwd<<<dim3(scan_blocks(uc), g.ns), 256, red_bytes, st>>>(g, uc, w.lamlog, w.sp, w.stm, w.std_,
+    k_tc_scan_bwd<<<dim3(scan_blocks(uc), g.ns), 256, red_bytes, st>>>(g, uc, w.lamlog, (const float*)w.sp, w.stm, w.std_,
                                                                           b.dsm, b.dsd, b.dlam, nullptr, pre_out, 0,
                                                                           nullptr, nullptr, nbt);
     count_launch(4);
@@ -1028,7 +1050,7 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
   if (mode == 2 && launch_intra()) return 3;
   {
     StageTimer tmr("bwd_discumsum", st);
-    k_tc_scan_bwd<<<dim3(scan_blocks(uc), g.ns), 256, red_bytes, st>>>(g, uc, w.lamlog, w.sp, w.stm, w.std_,
+    k_tc_scan_bwd<<<dim3(scan_blocks(uc), g.ns), 256, red_bytes, st>>>(g, uc, w.lamlog, (const float*)w.sp, w.stm, w.std_,
                                                                           b.dsm, b.dsd, b.dlam, carry, pre_out, 1,
                                                                           zf ? b.ea : nullptr, zf ? b.eg : nullptr, nbt);
   }
