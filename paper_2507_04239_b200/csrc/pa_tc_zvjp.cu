@@ -60,6 +60,9 @@ extern "C" int pa_debug_trace6(long long* host, int n) {
 #define PA_TR6(c, i)
 #endif
 
+#ifndef ZV_EXPERIMENT
+#define ZV_EXPERIMENT 0
+#endif
 namespace zv {
 constexpr int TILE = 64 * 128;   // bytes of one E tile: 64 rows (c) x 64 fp16 (e), SW128
 constexpr int NSB = 3;           // B ring: 4 E tiles (32 KB, one bulk copy) per stage
@@ -391,26 +394,39 @@ __global__ void __launch_bounds__(zv::THREADS, 1)
             o[e2] = pack_f16(f2.x * p, f2.y * p);
           }
         };
-        float mx = 0.f, mu = fabsf(dsc);
+        // one row at a time in registers (max, then scaled conversion): a separate
+        // max pass over shared memory cost ~10K cycles per tile, holding both rows
+        // and their conversions spilled
+        uint4 v8[8];
 #pragma unroll
-        for (int c8 = 0; c8 < 8; ++c8) {
-          mx = chunk_max(chunk(xrow_s, c8), true, mx);
-          if (!u_is_x) mu = chunk_max(chunk(urow_s, c8), ub, mu);
-        }
+        for (int c8 = 0; c8 < 8; ++c8) v8[c8] = chunk(xrow_s, c8);
+        float mx = 0.f;
+#pragma unroll
+        for (int c8 = 0; c8 < 8; ++c8) mx = chunk_max(v8[c8], true, mx);
         // x (the bcast factor) and the vector operand u, both scaled by powers of two
         // into [1, 2) so fp16 products keep their precision for any input range
         px = pow2_norm(mx);
-        pv = u_is_x ? px : pow2_norm(mu);
 #pragma unroll
         for (int c8 = 0; c8 < 8; ++c8) {
           uint32_t o[4];
-          chunk_f16(chunk(xrow_s, c8), true, px, o);
+          chunk_f16(v8[c8], true, px, o);
 #pragma unroll
           for (int e2 = 0; e2 < 4; ++e2) {
             xw[(c8 * 4 + e2) * NGEN + xt] = live ? o[e2] : 0u;
             if (u_is_x) vr[c8 * 4 + e2] = live ? o[e2] : 0u;
           }
-          if (!u_is_x) chunk_f16(chunk(urow_s, c8), ub, pv, &vr[c8 * 4]);
+        }
+        if (u_is_x) {
+          pv = px;
+        } else {
+#pragma unroll
+          for (int c8 = 0; c8 < 8; ++c8) v8[c8] = chunk(urow_s, c8);
+          float mu = fabsf(dsc);
+#pragma unroll
+          for (int c8 = 0; c8 < 8; ++c8) mu = chunk_max(v8[c8], ub, mu);
+          pv = pow2_norm(mu);
+#pragma unroll
+          for (int c8 = 0; c8 < 8; ++c8) chunk_f16(v8[c8], ub, pv, &vr[c8 * 4]);
         }
         PA_TR6(trc && it == 5 && tid == 0, 801);
         __syncwarp();
