@@ -1057,27 +1057,17 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
   join_intra();
   {
     StageTimer tmr("bwd_query_state_dq", st);
-    if (zf) {
-      CUtensorMap m_xq, m_uq;
-      if (!map_bth(&m_xq, q, g, 128)) return 3;
-      if (den ? !map_2d(&m_uq, b.dN16, (size_t)g.ns * g.t, HD, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)
-              : !map_bth(&m_uq, dy, g, 128))
-        return 3;
-      tc_zvjp(g, false, m_xq, m_uq, den ? 0 : 1, b.dD, q, w.ell, w.lamlog, b.ea, b.dq32, nullptr, b.dell, nullptr,
-              dq, nullptr, st);
-    }
+    if (zf)
+      tc_zvjp(g, false, den ? 0 : 1, den ? (const void*)b.dN16 : dy, b.dD, q, w.ell, w.lamlog, b.ea, b.dq32,
+              nullptr, b.dell, nullptr, dq, nullptr, st);
     else
       tc_dphi(g, false, den ? (const void*)b.dN16 : dy, den ? 0 : 1, b.dD, q, w.ell, w.lamlog, w.stm, w.std_,
               b.dq32, nullptr, b.dell, nullptr, dq, nullptr, st);
   }
   {
     StageTimer tmr("bwd_update_state", st);
-    if (zf) {
-      CUtensorMap m_xk, m_uv;
-      if (!map_bth(&m_xk, k, g, 128) || !map_bth(&m_uv, v, g, 128)) return 3;
-      tc_zvjp(g, true, m_xk, m_uv, 1, nullptr, k, w.ell, w.lamlog, b.eg, b.dk32, b.dv32, b.dell, b.cu, dk, dv,
-              st);
-    }
+    if (zf)
+      tc_zvjp(g, true, 1, v, nullptr, k, w.ell, w.lamlog, b.eg, b.dk32, b.dv32, b.dell, b.cu, dk, dv, st);
     else
       tc_dphi(g, true, v, 1, nullptr, k, w.ell, w.lamlog, b.dsm, b.dsd, b.dk32, b.dv32, b.dell, b.cu, dk, dv, st);
   }

@@ -45,9 +45,8 @@ int tc_dphi(const Geo& g, bool upd, const void* a_rows, int a_bf16_bth, const __
             const float* dv32, float* dell, float* dellend, void* dxo, void* dvo, cudaStream_t st);
 
 // expanded-state VJP GEMMs (pa_tc_zvjp.cu): E = expanded A'_{k-1} (query side) or dS~_k (update side)
-int tc_zvjp(const Geo& g, bool upd, const CUtensorMap& m_x, const CUtensorMap& m_u, int u_bf16_bth,
-            const __half* u16, const void* xraw, const float* ell, const float* lamlog, const __half* E,
-            const float* dx32, const float* dv32, float* dell, float* dellend, void* dxo, void* dvo,
-            cudaStream_t st);
+int tc_zvjp(const Geo& g, bool upd, int u_bf16_bth, const void* u_rows, const __half* u16, const void* xraw,
+            const float* ell, const float* lamlog, const __half* E, const float* dx32, const float* dv32,
+            float* dell, float* dellend, void* dxo, void* dvo, cudaStream_t st);
 
 }  // namespace pa
