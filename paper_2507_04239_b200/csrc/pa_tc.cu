@@ -358,6 +358,34 @@ __global__ void __launch_bounds__(fm::THREADS, 2) k_tc_featmajor(const __grid_co
     PA_TR5(trg, 191);
     tc_fence_after();
     const int ncols = den ? UW : 64;
+    if (kBwd && !den) {
+      // dA' rows (fp32, 64 of 80 columns): through shared memory (the drained
+      // operand stages; 32 rows x 68 floats per warp, padded against bank
+      // conflicts) so each warp store writes one contiguous 256-byte row instead
+      // of 32 rows x 16 bytes
+      float* stg = (float*)smem + (w - 4) * (32 * 68);
+#pragma unroll
+      for (int u = 0; u < TPW; ++u) {
+        const int t = tp * TPW + u;
+        if (!act[u]) continue;
+#pragma unroll
+        for (int c0 = 0; c0 < 64; c0 += 16) {
+          uint32_t r[16];
+          tmem_ld16(tm + (uint32_t)(t * ACC_W) + lane_off + c0, r);
+          tc_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 16; c += 4)
+            *(float4*)(stg + l * 68 + c0 + c) = make_float4(__uint_as_float(r[c]), __uint_as_float(r[c + 1]),
+                                                            __uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
+        }
+        __syncwarp();
+        float* dst0 = (float*)out + (((size_t)(s * g.nsl + slot) * FH) + (size_t)(t0 + t) * 128 + q * 32) * UW;
+#pragma unroll 8
+        for (int r = 0; r < 32; ++r)
+          *(float2*)(dst0 + (size_t)r * UW + 2 * l) = *(const float2*)(stg + r * 68 + 2 * l);
+        __syncwarp();
+      }
+    } else
 #pragma unroll
     for (int u = 0; u < TPW; ++u) {
       const int t = tp * TPW + u;
