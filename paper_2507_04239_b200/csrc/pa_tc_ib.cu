@@ -361,20 +361,29 @@ __global__ void __launch_bounds__(ib2::THREADS, 2) k_tc_ib(const __grid_constant
     uint32_t r[32];
     tmem_ld32(tA + lane_off + grp * 32, r);
     tc_wait_ld();
-    const float fa = kKV ? 1.f : 2.f;   // dS carries a factor 1/2
-    float* oa = (kKV ? out_b : out_a) + tokr * HD + grp * 32;   // kKV: dV; q-side: dQ
+    // rows go out through shared memory (the drained operand tiles; 32 rows x 36
+    // floats per warp, padded against bank conflicts): each warp store then writes
+    // four contiguous 128-byte half-rows instead of 32 scattered 16-byte pieces
+    float* stg = (float*)smem + w * (32 * 36);
+    const size_t tok0r = (size_t)s * g.t + c0 + own - l;   // row of lane 0
+    auto put = [&](float* base, float f) {
 #pragma unroll
-    for (int a = 0; a < 32; a += 4)
-      *(float4*)(oa + a) = make_float4(fa * __uint_as_float(r[a]), fa * __uint_as_float(r[a + 1]),
-                                       fa * __uint_as_float(r[a + 2]), fa * __uint_as_float(r[a + 3]));
+      for (int a = 0; a < 32; a += 4)
+        *(float4*)(stg + l * 36 + a) = make_float4(f * __uint_as_float(r[a]), f * __uint_as_float(r[a + 1]),
+                                                   f * __uint_as_float(r[a + 2]), f * __uint_as_float(r[a + 3]));
+      __syncwarp();
+#pragma unroll
+      for (int r4 = 0; r4 < 32; r4 += 4) {
+        const int rw = r4 + (l >> 3), cc = (l & 7) * 4;
+        *(float4*)(base + (tok0r + rw) * HD + grp * 32 + cc) = *(const float4*)(stg + rw * 36 + cc);
+      }
+      __syncwarp();
+    };
+    put(kKV ? out_b : out_a, kKV ? 1.f : 2.f);   // kKV: dV; q-side: dQ (dS carries a factor 1/2)
     if (kKV) {
       tmem_ld32(tB + lane_off + grp * 32, r);
       tc_wait_ld();
-      float* ob = out_a + tokr * HD + grp * 32;   // dK
-#pragma unroll
-      for (int a = 0; a < 32; a += 4)
-        *(float4*)(ob + a) = make_float4(2.f * __uint_as_float(r[a]), 2.f * __uint_as_float(r[a + 1]),
-                                         2.f * __uint_as_float(r[a + 2]), 2.f * __uint_as_float(r[a + 3]));
+      put(out_a, 2.f);   // dK
     }
     const float rr = red.x + red.y;
     if (g.gated) atomicAdd(dell + tokr, kKV ? -rr : rr);
