@@ -385,6 +385,35 @@ __global__ void __launch_bounds__(fm::THREADS, 2) k_tc_featmajor(const __grid_co
           *(float2*)(dst0 + (size_t)r * UW + 2 * l) = *(const float2*)(stg + r * 68 + 2 * l);
         __syncwarp();
       }
+    } else if (!kBwd && !den) {
+      // S' rows (fp16 x 2^-10, 64 of 80 columns) through shared memory as above:
+      // each warp store writes four contiguous 128-byte rows
+      uint8_t* stg = smem + (w - 4) * (32 * 144);
+#pragma unroll
+      for (int u = 0; u < TPW; ++u) {
+        const int t = tp * TPW + u;
+        if (!act[u]) continue;
+#pragma unroll
+        for (int c0 = 0; c0 < 64; c0 += 16) {
+          uint32_t r[16];
+          tmem_ld16(tm + (uint32_t)(t * ACC_W) + lane_off + c0, r);
+          tc_wait_ld();
+          uint32_t h[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            h[c] = pack_f16(__uint_as_float(r[2 * c]) * kSpScale, __uint_as_float(r[2 * c + 1]) * kSpScale);
+          *(uint4*)(stg + l * 144 + c0 * 2) = make_uint4(h[0], h[1], h[2], h[3]);
+          *(uint4*)(stg + l * 144 + c0 * 2 + 16) = make_uint4(h[4], h[5], h[6], h[7]);
+        }
+        __syncwarp();
+        __half* dst0 = (__half*)out + (((size_t)(s * g.nsl + slot) * FH) + (size_t)(t0 + t) * 128 + q * 32) * UW;
+#pragma unroll
+        for (int r4 = 0; r4 < 32; r4 += 4) {
+          const int rw = r4 + (l >> 3), cc = (l & 7) * 8;
+          *(uint4*)(dst0 + (size_t)rw * UW + cc) = *(const uint4*)(stg + rw * 144 + cc * 2);
+        }
+        __syncwarp();
+      }
     } else
 #pragma unroll
     for (int u = 0; u < TPW; ++u) {

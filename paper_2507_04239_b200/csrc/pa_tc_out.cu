@@ -361,13 +361,25 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
       inv = 1.f / dn;
     }
     if (rowsum) rowsum[rw] = dn;
-    uint4* yrow = (uint4*)(y + rw * HD);
+    {
+      // y rows go out through shared memory (the drained state stages; 32 rows x
+      // 144 B per warp, padded against bank conflicts): each warp store writes four
+      // whole 128-byte rows instead of 32 scattered 16-byte pieces
+      uint8_t* stg = st_s + w * (32 * 144);
 #pragma unroll
-    for (int c8 = 0; c8 < 8; ++c8)
-      yrow[c8] = make_uint4(pack_bf16(yv[c8 * 8] * inv, yv[c8 * 8 + 1] * inv),
-                            pack_bf16(yv[c8 * 8 + 2] * inv, yv[c8 * 8 + 3] * inv),
-                            pack_bf16(yv[c8 * 8 + 4] * inv, yv[c8 * 8 + 5] * inv),
-                            pack_bf16(yv[c8 * 8 + 6] * inv, yv[c8 * 8 + 7] * inv));
+      for (int c8 = 0; c8 < 8; ++c8)
+        *(uint4*)(stg + l * 144 + c8 * 16) =
+            make_uint4(pack_bf16(yv[c8 * 8] * inv, yv[c8 * 8 + 1] * inv),
+                       pack_bf16(yv[c8 * 8 + 2] * inv, yv[c8 * 8 + 3] * inv),
+                       pack_bf16(yv[c8 * 8 + 4] * inv, yv[c8 * 8 + 5] * inv),
+                       pack_bf16(yv[c8 * 8 + 6] * inv, yv[c8 * 8 + 7] * inv));
+      __syncwarp();
+#pragma unroll
+      for (int r4 = 0; r4 < 32; r4 += 4) {
+        const int rw4 = r4 + (l >> 3), c8 = l & 7;
+        *(uint4*)(y + rowid(g, s, tok - l + rw4) * HD + c8 * 8) = *(const uint4*)(stg + rw4 * 144 + c8 * 16);
+      }
+    }
     if (g.normalize && y32) {
       float4* dst = (float4*)(y32 + ((size_t)s * g.t + tok) * HD);
 #pragma unroll
