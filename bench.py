@@ -95,6 +95,9 @@ class Clocks:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def mark(self):
+        self.m = len(self.lines)
+
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -105,7 +108,9 @@ class Clocks:
             self.proc.kill()
         sm, mx, reasons, power = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        m = getattr(self, "m", 0)
+        timed = self.lines[m:] if len(self.lines) > m else self.lines[-2:]
+        for ln in timed:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -231,11 +236,16 @@ def run_gpu(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    # the clock sampler starts before the warm-up (nvidia-smi needs a few hundred ms
+    # to produce its first line); only samples taken after the mark -- inside the
+    # timed region -- count, or the last warm-up samples if the region was shorter
+    # than the sampling interval
+    clocks = Clocks(local)
+    clocks.start()
     for _ in range(args.warmup):
         step()
     barrier()
-    clocks = Clocks(local)
-    clocks.start()
+    clocks.mark()
     _lib.profile_reset()
     _lib.profile_enable(True)
     n0 = _lib.launch_count()

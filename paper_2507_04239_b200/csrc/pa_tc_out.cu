@@ -62,8 +62,10 @@ constexpr int KV_ST = 3;
 constexpr int ST_ST = 4;
 constexpr int XH = 8 * 128 * 16;        // fp16 q rows, thread-private uint4 columns
 constexpr int SMEM = 1024 + QB + KV_ST * (KB + VB) + ST_ST * (STB + STD) + XH + 2048 + 4096 + 1024 + 512;
-constexpr int THREADS = 448;
-constexpr int W_TMEM = 8, W_TMA_KV = 9, W_TMA_ST = 10, W_MMA_ST = 11, W_MMA_IN = 13;
+constexpr int THREADS = 576;
+// w0..w3 phi'(q) + epilogue, w4..w11 P (two warps per lane quadrant, 64 columns
+// each), then the issuing warps on the highest ids
+constexpr int W_TMEM = 12, W_TMA_KV = 13, W_TMA_ST = 14, W_MMA_ST = 15, W_MMA_IN = 17;
 }  // namespace out2
 
 template <int kDen>
@@ -131,7 +133,7 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
       mbar_init(&a_full[i], 4);
       mbar_init(&a_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 4);
+      mbar_init(&p_full[i], 8);
       mbar_init(&pv_done[i], 1);
     }
     mbar_init(a_done, 2);
@@ -386,9 +388,10 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
       for (int c4 = 0; c4 < 16; ++c4)
         dst[c4] = make_float4(yv[c4 * 4] * inv, yv[c4 * 4 + 1] * inv, yv[c4 * 4 + 2] * inv, yv[c4 * 4 + 3] * inv);
     }
-  } else if (w < 8) {
+  } else if (w < 12) {
     // ---------------- P = decayed (sigma q.k)^2 under the causal mask ------------
-    const int q = w & 3, row = q * 32 + l;
+    // two warps per lane quadrant: half ph takes S columns [64 ph, 64 ph + 64)
+    const int q = w & 3, row = q * 32 + l, ph = (w - 4) >> 2;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const float li = ell_s[I * 128 + row];
     const float sig2 = g.scale * g.scale;
@@ -396,8 +399,8 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
       const int sb = J % NSB, cb = J & 1;
       const bool diag = (J == I);
       const float lref = ell_s[J * 128 + 127];
-      cj[cb * 128 + row] = diag ? ell_s[J * 128 + row] : __expf(lref - ell_s[J * 128 + row]);
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (ph == 0) cj[cb * 128 + row] = diag ? ell_s[J * 128 + row] : __expf(lref - ell_s[J * 128 + row]);
+      asm volatile("bar.sync 1, 256;" ::: "memory");
       PA_TR4(trb && w == 4 && l == 0, 400 + J * 3 + 0);
       mbar_wait(&s_full[sb], (J / NSB) & 1);
       PA_TR4(trb && w == 4 && l == 0, 400 + J * 3 + 1);
@@ -406,12 +409,15 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
       const float* cjs = cj + cb * 128;
       const uint32_t sp = tm + TSP + (uint32_t)(sb * 128) + lane_off;
       uint32_t rb[2][32];
-      tmem_ld32(sp, rb[0]);
+      tmem_ld32(sp + ph * 64, rb[0]);
+      tmem_ld32(sp + ph * 64 + 32, rb[1]);
+      tc_wait_ld();
+      // P is written back in place as bf16 pairs: the half-1 warp's P lands on S
+      // columns [32, 64), which the half-0 warp of this quadrant must have read
+      asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
 #pragma unroll
-      for (int ch = 0; ch < 4; ++ch) {
+      for (int ch = 2 * ph; ch < 2 * ph + 2; ++ch) {
         uint32_t pk[16];
-        tc_wait_ld();
-        if (ch + 1 < 4) tmem_ld32(sp + (ch + 1) * 32, rb[(ch + 1) & 1]);   // next chunk in flight
         const uint32_t* r = rb[ch & 1];
         if (!diag) {
           // P = r_i c_j s^2 in packed f32x2 arithmetic (3 FMUL2 per pair)
