@@ -291,11 +291,11 @@ __global__ void __launch_bounds__(zv::THREADS, 1)
             const uint32_t xb = xw[(jt >> 1) * NGEN + tid];
             const uint32_t bc = __byte_perm(xb, 0, (jt & 1) ? 0x3232 : 0x1010);
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              uint32_t o[16];
+            {
+              uint32_t o[32];
 #pragma unroll
-              for (int q = 0; q < 16; ++q) o[q] = hmul2_f16(bc, vr[h * 16 + q]);
-              tmem_st16(base + (uint32_t)(h * 16), o);
+              for (int q = 0; q < 32; ++q) o[q] = hmul2_f16(bc, vr[q]);
+              tmem_st32(base, o);
             }
           } else if (jt < NBT && (!kUpd || gq == 0)) {
             // score-sum tile E_G[c][b]: A_b = x_b * (dden | 1) pv
