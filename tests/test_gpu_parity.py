@@ -211,3 +211,35 @@ def test_bf16_backward_tensor_core_shape(t, c, normalize, gated):
         assert metric(a, b) <= BF16_TOL, (name, metric(a, b))
     if gated:
         assert metric(r["dlogg"], dg * g) <= BF16_TOL, ("dlogg", metric(r["dlogg"], dg * g))
+
+
+@pytest.mark.gpu
+def test_bf16_full_length_size_independent_properties():
+    """configs[1] length (t = 65536, c = 1024) on the tcgen05 path, checked through
+    properties that hold at any size: chunk-size independence (c = 1024 vs 512),
+    homogeneity in V (scaling by 2 only shifts exponents, so y(2V) = 2 y(V) up to
+    fp16 subnormal rounding of tiny decayed terms), and zero-gate erasure (a gate
+    of 0 cuts all earlier influence: perturbing q, k, v before it moves later
+    outputs only at rounding level -- the two MMA issuers of a GEMM accumulate in
+    a timing-dependent order, so runs are not bit-identical -- while earlier
+    outputs move by O(1))."""
+    torch.manual_seed(0)
+    b, t, h, d, c = 1, 65536, 2, 64, 1024
+    Q, K, V = ((torch.rand(b, t, h, d, device="cuda") * 2 - 1).bfloat16() for _ in range(3))
+    lg = torch.log(torch.rand(b, t, h, device="cuda") * 0.1 + 0.9)
+    y = P.power_full(Q, K, V, lg, p=2, chunk_size=c)
+    y512 = P.power_full(Q, K, V, lg, p=2, chunk_size=512)
+    assert norm_rel_error(y512.float().cpu().numpy(), y.float().cpu().numpy()) <= BF16_TOL
+    y2 = P.power_full(Q, K, 2 * V, lg, p=2, chunk_size=c)
+    assert norm_rel_error(y2.float().cpu().numpy(), 2 * y.float().cpu().numpy()) <= 1e-3
+    m0 = 40000   # inside chunk 39
+    lg0 = lg.clone()
+    lg0[:, m0] = float("-inf")
+    ya = P.power_full(Q, K, V, lg0, p=2, chunk_size=c)
+    Qb, Kb, Vb = Q.clone(), K.clone(), V.clone()
+    for X in (Qb, Kb, Vb):
+        X[:, :m0] = (torch.rand_like(X[:, :m0].float()) * 2 - 1).bfloat16()
+    yb = P.power_full(Qb, Kb, Vb, lg0, p=2, chunk_size=c)
+    after = norm_rel_error(yb[:, m0:].float().cpu().numpy(), ya[:, m0:].float().cpu().numpy())
+    before = norm_rel_error(yb[:, :m0].float().cpu().numpy(), ya[:, :m0].float().cpu().numpy())
+    assert after <= 1e-3 and before >= 0.3, (after, before)
