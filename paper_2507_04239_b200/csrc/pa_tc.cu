@@ -117,35 +117,40 @@ __global__ void __launch_bounds__(256) k_tc_prep_rows(Geo g, int mode, const __n
                                                       const float* __restrict__ lamlog,
                                                       const float* __restrict__ dden, __half* __restrict__ rows,
                                                       __half* __restrict__ aux) {
-  // eight threads per token row, 16 bytes each: loads and stores are whole
-  // 128-byte rows per eight lanes (one row per thread left every warp store
-  // scattered over 32 rows)
+  // four threads per token row, two 16-byte chunks each (c4, c4 + 4): a warp's
+  // loads and stores are whole 128-byte rows, and each thread keeps two loads in
+  // flight (one row per thread left every warp store scattered over 32 rows)
   const size_t gi = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  const size_t it = gi >> 3;
-  const int c8 = (int)(gi & 7);
+  const size_t it = gi >> 2;
+  const int c4 = (int)(gi & 3);
   if (it >= (size_t)g.ns * g.t) return;
   const int s = (int)(it / g.t), m = (int)(it - (size_t)s * g.t);
+  const __nv_bfloat16* row;
+  if (mode == 0 || mode == 2) row = src + rowid(g, s, m) * HD;
+  else row = src + (mode == 3 ? rowid(g, s, m) : it) * HD;
+  uint4 v4[2];
+  v4[0] = __ldcs((const uint4*)row + c4);
+  v4[1] = __ldcs((const uint4*)row + c4 + 4);
   const float lm = ell[it];
   float f, a;
-  const __nv_bfloat16* row;
   if (mode == 0 || mode == 2) {
     f = (mode == 0 && g.gated) ? __expf(lamlog[s * g.n + m / g.c] - lm) : 1.f;
     a = f;
-    row = src + rowid(g, s, m) * HD;
   } else {
     f = g.scale * g.scale * __expf(lm);
     a = dden ? f * dden[it] : 0.f;
-    row = src + (mode == 3 ? rowid(g, s, m) : it) * HD;
   }
-  uint4 v4 = __ldcs((const uint4*)row + c8);
-  uint32_t* pv = (uint32_t*)&v4;
 #pragma unroll
-  for (int e2 = 0; e2 < 4; ++e2) {
-    const float2 f2 = __bfloat1622float2(*(const __nv_bfloat162*)&pv[e2]);
-    pv[e2] = pack_f16(f2.x * f, f2.y * f);
+  for (int hh = 0; hh < 2; ++hh) {
+    uint32_t* pv = (uint32_t*)&v4[hh];
+#pragma unroll
+    for (int e2 = 0; e2 < 4; ++e2) {
+      const float2 f2 = __bfloat1622float2(*(const __nv_bfloat162*)&pv[e2]);
+      pv[e2] = pack_f16(f2.x * f, f2.y * f);
+    }
+    ((uint4*)(rows + it * HD))[c4 + 4 * hh] = v4[hh];
   }
-  ((uint4*)(rows + it * HD))[c8] = v4;
-  if (aux && c8 < 2) ((uint4*)(aux + it * 16))[c8] = make_uint4(c8 == 0 ? pack_f16(a, 0.f) : 0u, 0u, 0u, 0u);
+  if (aux && c4 < 2) ((uint4*)(aux + it * 16))[c4] = make_uint4(c4 == 0 ? pack_f16(a, 0.f) : 0u, 0u, 0u, 0u);
 }
 
 // ==========================================================================
@@ -951,7 +956,7 @@ int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const 
     StageTimer tmr("fwd_prep", st);
     k_tc_prep_gates<<<(g.ns * g.n + 3) / 4, 128, 0, st>>>(g, log_g, w.ell, w.lamlog);
     k_tc_prep_xt<<<dim3(g.c / 64, g.n, g.ns), 256, 0, st>>>(g, (const __nv_bfloat16*)k, w.kt);
-    k_tc_prep_rows<<<(unsigned)(((size_t)g.ns * g.t * 8 + 255) / 256), 256, 0, st>>>(
+    k_tc_prep_rows<<<(unsigned)(((size_t)g.ns * g.t * 4 + 255) / 256), 256, 0, st>>>(
         g, 0, (const __nv_bfloat16*)v, w.ell, w.lamlog, nullptr, w.vr, with_den ? w.wa : nullptr);
   }
   {
@@ -1076,7 +1081,7 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
       k_tc_bwd_prep<<<(unsigned)(((size_t)g.ns * g.t + 255) / 256), 256, 0, st>>>(
           g, (const __nv_bfloat16*)dy, w.y32, rowsum, b.dN, b.dN16, b.dD, b.dden);
     k_tc_prep_xt<<<dim3(g.c / 64, g.n, g.ns), 256, 0, st>>>(g, (const __nv_bfloat16*)q, w.kt);
-    k_tc_prep_rows<<<(unsigned)(((size_t)g.ns * g.t * 8 + 255) / 256), 256, 0, st>>>(
+    k_tc_prep_rows<<<(unsigned)(((size_t)g.ns * g.t * 4 + 255) / 256), 256, 0, st>>>(
         g, den ? 1 : 3, den ? b.dN : (const __nv_bfloat16*)dy, w.ell, w.lamlog, den ? b.dden : nullptr, w.vr,
         den ? w.wa : nullptr);
   }
