@@ -61,9 +61,6 @@ extern "C" int pa_debug_trace6(long long* host, int n) {
 #define PA_TR6(c, i)
 #endif
 
-#ifndef ZV_EXPERIMENT
-#define ZV_EXPERIMENT 0
-#endif
 namespace zv {
 constexpr int TILE = 64 * 128;   // bytes of one E tile: 64 rows (c) x 64 fp16 (e), SW128
 constexpr int NSB = 3;           // B ring: 4 E tiles (32 KB, one bulk copy) per stage
