@@ -1,4 +1,5 @@
 #!/bin/bash
+# GPU tests + a quick bench line (stage times), used between kernel changes
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
 timeout 600 python bench.py --no-e2e --no-cpu > gpurun_out/bench.log 2>&1
