@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(256) k_tc_prep_xt(Geo g, const __nv_bfloat16* 
 // per-token decay/scale rides on the other operand:
 //   mode 0 (forward):  rows = W_m v_m,        aux = (W_m, 0...)      W_m = exp(lend - ell_m)
 //   mode 1 (backward): rows = c_m dnum_m,     aux = (c_m dden_m, 0...)  c_m = sigma^2 exp(ell_m)
+//                      (dnum read as the fp16 stream-major rows of k_tc_bwd_prep)
 //   mode 3: as mode 1 with dnum = dy read in the [b, t, h, 64] layout (no normalization)
 // rows [ns*t][64] bf16, aux [ns*t][16] bf16 (may be null).
 __global__ void __launch_bounds__(256) k_tc_prep_rows(Geo g, int mode, const __nv_bfloat16* __restrict__ src,
@@ -131,6 +132,7 @@ __global__ void __launch_bounds__(256) k_tc_prep_rows(Geo g, int mode, const __n
   uint4 v4[2];
   v4[0] = __ldcs((const uint4*)row + c4);
   v4[1] = __ldcs((const uint4*)row + c4 + 4);
+  const bool src_f16 = mode == 1;   // normalized dnum rows (fp16, stream-major)
   const float lm = ell[it];
   float f, a;
   if (mode == 0 || mode == 2) {
@@ -145,7 +147,8 @@ __global__ void __launch_bounds__(256) k_tc_prep_rows(Geo g, int mode, const __n
     uint32_t* pv = (uint32_t*)&v4[hh];
 #pragma unroll
     for (int e2 = 0; e2 < 4; ++e2) {
-      const float2 f2 = __bfloat1622float2(*(const __nv_bfloat162*)&pv[e2]);
+      const float2 f2 = src_f16 ? __half22float2(*(const __half2*)&pv[e2])
+                                : __bfloat1622float2(*(const __nv_bfloat162*)&pv[e2]);
       pv[e2] = pack_f16(f2.x * f, f2.y * f);
     }
     ((uint4*)(rows + it * HD))[c4 + 4 * hh] = v4[hh];
@@ -560,48 +563,42 @@ __global__ void __launch_bounds__(256) k_tc_sp_combine(Geo g, const float* __res
 // BACKWARD
 // ==========================================================================
 // prep: normalization cotangents (gradients.py:381-386) in the layouts the
-// tensor-core kernels read: dN [ns*t][64] bf16 (dnum), dD [ns*t][16] bf16
-// (col 0 = dden), and dden [ns*t] fp32 for the intra-chunk kernels.
+// tensor-core kernels read: dN16 [ns*t][64] fp16 (dnum = dy / R), dD [ns*t][16]
+// fp16 (col 0 = dden), and dden [ns*t] fp32 (dden = -<dy, y> / R).  Eight threads
+// per token row (16 bytes of dy, 32 bytes of y each), the dot product reduced
+// over the eight lanes: whole-row loads and stores per warp.
 __global__ void __launch_bounds__(256) k_tc_bwd_prep(Geo g, const __nv_bfloat16* __restrict__ dy,
                                                      const float* __restrict__ y32,
-                                                     const float* __restrict__ rowsum, __nv_bfloat16* dN,
-                                                     __half* dN16, __half* dD, float* dden_out) {
-  const size_t it = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  if (it >= (size_t)g.ns * g.t) return;
-  const int s = (int)(it / g.t), m = (int)(it - (size_t)s * g.t);
-  const size_t r = rowid(g, s, m);
-  float R = 1.f, dot = 0.f;
-  if (g.normalize) R = rowsum[r];
-  const float inv = 1.f / R;
-  const uint4* src = (const uint4*)(dy + r * HD);
-  uint4* dst = (uint4*)(dN + it * HD);
-  uint4* dst16 = (uint4*)(dN16 + it * HD);
-#pragma unroll
-  for (int c8 = 0; c8 < 8; ++c8) {
-    uint4 v4 = src[c8];
+                                                     const float* __restrict__ rowsum, __half* dN16, __half* dD,
+                                                     float* dden_out) {
+  const size_t gi = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  const size_t it = gi >> 3;
+  const int c8 = (int)(gi & 7);
+  const bool ok = it < (size_t)g.ns * g.t;   // whole 8-lane groups share ok
+  float dot = 0.f, inv = 1.f;
+  if (ok) {
+    const int s = (int)(it / g.t), m = (int)(it - (size_t)s * g.t);
+    const size_t r = rowid(g, s, m);
+    uint4 v4 = ((const uint4*)(dy + r * HD))[c8];
+    const float4 ya = ((const float4*)(y32 + it * HD))[2 * c8], yb = ((const float4*)(y32 + it * HD))[2 * c8 + 1];
+    inv = 1.f / rowsum[r];
+    const float yv[8] = {ya.x, ya.y, ya.z, ya.w, yb.x, yb.y, yb.z, yb.w};
     uint32_t* pv = (uint32_t*)&v4;
 #pragma unroll
-    uint4 h4;
-    uint32_t* ph = (uint32_t*)&h4;
     for (int e2 = 0; e2 < 4; ++e2) {
-      float2 f2 = __bfloat1622float2(*(const __nv_bfloat162*)&pv[e2]);
-      const int u = c8 * 8 + e2 * 2;
-      if (g.normalize) dot += f2.x * y32[it * HD + u] + f2.y * y32[it * HD + u + 1];
-      f2.x *= inv;
-      f2.y *= inv;
-      pv[e2] = pack_bf16(f2.x, f2.y);
-      ph[e2] = pack_f16(f2.x, f2.y);
+      const float2 f2 = __bfloat1622float2(*(const __nv_bfloat162*)&pv[e2]);
+      dot = fmaf(f2.x, yv[2 * e2], fmaf(f2.y, yv[2 * e2 + 1], dot));
+      pv[e2] = pack_f16(f2.x * inv, f2.y * inv);
     }
-    dst[c8] = v4;
-    dst16[c8] = h4;
+    ((uint4*)(dN16 + it * HD))[c8] = v4;
   }
-  const float dden = g.normalize ? -dot * inv : 0.f;
-  dden_out[it] = dden;
-  if (dD) {
-    uint4* dd = (uint4*)(dD + it * 16);
-    dd[0] = make_uint4(pack_f16(dden, 0.f), 0u, 0u, 0u);
-    dd[1] = make_uint4(0u, 0u, 0u, 0u);
-  }
+  dot += __shfl_xor_sync(0xffffffffu, dot, 1);
+  dot += __shfl_xor_sync(0xffffffffu, dot, 2);
+  dot += __shfl_xor_sync(0xffffffffu, dot, 4);
+  if (!ok) return;
+  const float dden = -dot * inv;
+  if (c8 == 0) dden_out[it] = dden;
+  if (dD && c8 < 2) ((uint4*)(dD + it * 16))[c8] = make_uint4(c8 == 0 ? pack_f16(dden, 0.f) : 0u, 0u, 0u, 0u);
 }
 
 // Expanded state (pa_tc_zvjp.cu): per (stream, slot) nbt tiles of [64 c][64 e]
@@ -771,7 +768,6 @@ struct TcFwdWs {
 };
 
 struct TcBwdWs {
-  __nv_bfloat16* dN;     // dnum (bf16, intra-chunk GEMMs)
   __half* dN16;          // dnum (fp16, state GEMMs)
   __half* dD;            // (dden, 0..) fp16
   float* dden;
@@ -820,7 +816,6 @@ static TcFwdWs carve_fwd(const Geo& g, void* base, size_t* bytes) {
 static TcBwdWs carve_bwd(const Geo& g, void* base, size_t* bytes) {
   Take take{(char*)base};
   TcBwdWs b;
-  b.dN = (__nv_bfloat16*)take(2ull * g.ns * g.t * HD);
   b.dN16 = (__half*)take(2ull * g.ns * g.t * HD);
   b.dD = (__half*)take(2ull * g.ns * g.t * 16);
   b.dden = (float*)take(4ull * g.ns * g.t);
@@ -1022,8 +1017,6 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
       !map_bth(&m_v128, v, g, 128)) {
     return 3;
   }
-  CUtensorMap m_dn128;
-  if (!map_2d(&m_dn128, b.dN, (size_t)g.ns * g.t, HD, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)) return 3;
   m_dummy = m_dn;
   const int red_bytes = 8 * 4 * g.n;
   const int nbt = 64 + den;
@@ -1078,11 +1071,12 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
     // without normalization dnum = dy: the kernels read dy in place (TMA / row loads
     // with bf16 -> fp16 conversion), so only the normalized path materialises rows
     if (den)
-      k_tc_bwd_prep<<<(unsigned)(((size_t)g.ns * g.t + 255) / 256), 256, 0, st>>>(
-          g, (const __nv_bfloat16*)dy, w.y32, rowsum, b.dN, b.dN16, b.dD, b.dden);
+      k_tc_bwd_prep<<<(unsigned)(((size_t)g.ns * g.t * 8 + 255) / 256), 256, 0, st>>>(
+          g, (const __nv_bfloat16*)dy, w.y32, rowsum, b.dN16, b.dD, b.dden);
     k_tc_prep_xt<<<dim3(g.c / 64, g.n, g.ns), 256, 0, st>>>(g, (const __nv_bfloat16*)q, w.kt);
     k_tc_prep_rows<<<(unsigned)(((size_t)g.ns * g.t * 4 + 255) / 256), 256, 0, st>>>(
-        g, den ? 1 : 3, den ? b.dN : (const __nv_bfloat16*)dy, w.ell, w.lamlog, den ? b.dden : nullptr, w.vr,
+        g, den ? 1 : 3, den ? (const __nv_bfloat16*)b.dN16 : (const __nv_bfloat16*)dy, w.ell, w.lamlog,
+        den ? b.dden : nullptr, w.vr,
         den ? w.wa : nullptr);
   }
   if (mode == 0 && launch_intra()) return 3;
