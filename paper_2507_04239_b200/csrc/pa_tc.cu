@@ -386,6 +386,39 @@ __global__ void __launch_bounds__(fm::THREADS, 2) k_tc_featmajor(const __grid_co
           *(float2*)(dst0 + (size_t)r * UW + 2 * l) = *(const float2*)(stg + r * 68 + 2 * l);
         __syncwarp();
       }
+    } else if (kBwd && den) {
+      // dA' rows with the score-sum block (all 80 fp32 columns, so a warp's 32
+      // rows are one contiguous 10 KB block): staged in two column passes
+      // ([0, 48), [48, 80); 32 x 52 floats per warp) and stored as consecutive
+      // float2 runs
+      float* stg = (float*)smem + (w - 4) * (32 * 52);
+#pragma unroll
+      for (int u = 0; u < TPW; ++u) {
+        const int t = tp * TPW + u;
+        if (!act[u]) continue;
+        float* dst0 = (float*)out + (((size_t)(s * g.nsl + slot) * FH) + (size_t)(t0 + t) * 128 + q * 32) * UW;
+#pragma unroll
+        for (int pass = 0; pass < 2; ++pass) {
+          const int cb = pass * 48, nc = pass ? 32 : 48;
+#pragma unroll
+          for (int c0 = 0; c0 < nc; c0 += 16) {
+            uint32_t r[16];
+            tmem_ld16(tm + (uint32_t)(t * ACC_W) + lane_off + cb + c0, r);
+            tc_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 16; c += 4)
+              *(float4*)(stg + l * 52 + c0 + c) = make_float4(__uint_as_float(r[c]), __uint_as_float(r[c + 1]),
+                                                              __uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
+          }
+          __syncwarp();
+          const int n2 = nc / 2;   // float2 per row in this pass
+          for (int i = l; i < 32 * n2; i += 32) {
+            const int rw = i / n2, c2 = i - rw * n2;
+            *(float2*)(dst0 + (size_t)rw * UW + cb + 2 * c2) = *(const float2*)(stg + rw * 52 + 2 * c2);
+          }
+          __syncwarp();
+        }
+      }
     } else if (!kBwd && !den) {
       // S' rows (fp16 x 2^-10, 64 of 80 columns) through shared memory as above:
       // each warp store writes four contiguous 128-byte rows
