@@ -419,6 +419,35 @@ __global__ void __launch_bounds__(fm::THREADS, 2) k_tc_featmajor(const __grid_co
           __syncwarp();
         }
       }
+    } else if (!kBwd && den) {
+      // S' rows with the score-sum block (80 fp16 columns: a warp's 32 rows are
+      // one contiguous 5 KB block), staged (32 x 88 halves per warp) and stored as
+      // consecutive 16-byte runs
+      uint8_t* stg = smem + (w - 4) * (32 * 176);
+#pragma unroll
+      for (int u = 0; u < TPW; ++u) {
+        const int t = tp * TPW + u;
+        if (!act[u]) continue;
+#pragma unroll
+        for (int c0 = 0; c0 < 80; c0 += 16) {
+          uint32_t r[16];
+          tmem_ld16(tm + (uint32_t)(t * ACC_W) + lane_off + c0, r);
+          tc_wait_ld();
+          uint32_t h[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            h[c] = pack_f16(__uint_as_float(r[2 * c]) * kSpScale, __uint_as_float(r[2 * c + 1]) * kSpScale);
+          *(uint4*)(stg + l * 176 + c0 * 2) = make_uint4(h[0], h[1], h[2], h[3]);
+          *(uint4*)(stg + l * 176 + c0 * 2 + 16) = make_uint4(h[4], h[5], h[6], h[7]);
+        }
+        __syncwarp();
+        uint8_t* dst0 = (uint8_t*)((__half*)out + (((size_t)(s * g.nsl + slot) * FH) + (size_t)(t0 + t) * 128 + q * 32) * UW);
+        for (int i = l; i < 32 * 10; i += 32) {
+          const int rw = i / 10, cc = i - rw * 10;
+          *(uint4*)(dst0 + (size_t)rw * (UW * 2) + cc * 16) = *(const uint4*)(stg + rw * 176 + cc * 16);
+        }
+        __syncwarp();
+      }
     } else if (!kBwd && !den) {
       // S' rows (fp16 x 2^-10, 64 of 80 columns) through shared memory as above:
       // each warp store writes four contiguous 128-byte rows
