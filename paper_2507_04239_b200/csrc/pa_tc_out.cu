@@ -383,10 +383,22 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
       }
     }
     if (g.normalize && y32) {
-      float4* dst = (float4*)(y32 + ((size_t)s * g.t + tok) * HD);
+      // fp32 y rows (read by the backward prologue): the warp's 32 rows are one
+      // contiguous 8 KB block of the stream-major buffer -- staged (32 x 68 floats,
+      // after the bf16 rows above) and stored as consecutive 16-byte runs
+      __syncwarp();
+      float* sf = (float*)(st_s + 4 * (32 * 144)) + w * (32 * 68);
 #pragma unroll
       for (int c4 = 0; c4 < 16; ++c4)
-        dst[c4] = make_float4(yv[c4 * 4] * inv, yv[c4 * 4 + 1] * inv, yv[c4 * 4 + 2] * inv, yv[c4 * 4 + 3] * inv);
+        *(float4*)(sf + l * 68 + c4 * 4) =
+            make_float4(yv[c4 * 4] * inv, yv[c4 * 4 + 1] * inv, yv[c4 * 4 + 2] * inv, yv[c4 * 4 + 3] * inv);
+      __syncwarp();
+      float* dst0 = y32 + ((size_t)s * g.t + tok - l) * HD;
+#pragma unroll 4
+      for (int i = l; i < 32 * 16; i += 32) {
+        const int rw = i >> 4, cc = i & 15;
+        *(float4*)(dst0 + (size_t)rw * HD + cc * 4) = *(const float4*)(sf + rw * 68 + cc * 4);
+      }
     }
   } else if (w < 12) {
     // ---------------- P = decayed (sigma q.k)^2 under the causal mask ------------
