@@ -435,7 +435,11 @@ __global__ void __launch_bounds__(zv::THREADS, 1)
         const size_t xr = rowid(g, t.s, tok);
         const float4* o32 = (const float4*)((is_dv ? dv32 : dx32) + ((size_t)t.s * g.t + tok) * HD);
         const uint4* xsrc = (const uint4*)(xraw + xr * HD);
-        uint4* dst = (uint4*)((is_dv ? dvo : dxo) + xr * HD);
+        // the bf16 rows go out through shared memory: this tile's operand-word buffer
+        // (xw2[it & 1]) is free once its accumulator is full (every generator read
+        // of it precedes the last a_full arrival); 32 rows x 128 B per warp, 16-byte
+        // chunks XOR-swizzled by row, then four whole 128-byte rows per warp store
+        uint8_t* stg = (uint8_t*)(xw2 + (it & 1) * 32 * NGEN) + e * 4096;
         float c = 0.f;
 #pragma unroll
         for (int a4 = 0; a4 < 8; a4 += 4) {
@@ -460,10 +464,21 @@ __global__ void __launch_bounds__(zv::THREADS, 1)
               }
             }
             const float4 v0 = ov[2 * i], v1 = ov[2 * i + 1];
-            dst[a] = make_uint4(pack_bf16(fmaf(f[0], fct, v0.x), fmaf(f[1], fct, v0.y)),
-                                pack_bf16(fmaf(f[2], fct, v0.z), fmaf(f[3], fct, v0.w)),
-                                pack_bf16(fmaf(f[4], fct, v1.x), fmaf(f[5], fct, v1.y)),
-                                pack_bf16(fmaf(f[6], fct, v1.z), fmaf(f[7], fct, v1.w)));
+            *(uint4*)(stg + l * 128 + ((a ^ (l & 7)) << 4)) =
+                make_uint4(pack_bf16(fmaf(f[0], fct, v0.x), fmaf(f[1], fct, v0.y)),
+                           pack_bf16(fmaf(f[2], fct, v0.z), fmaf(f[3], fct, v0.w)),
+                           pack_bf16(fmaf(f[4], fct, v1.x), fmaf(f[5], fct, v1.y)),
+                           pack_bf16(fmaf(f[6], fct, v1.z), fmaf(f[7], fct, v1.w)));
+          }
+        }
+        __syncwarp();
+        {
+          __nv_bfloat16* outp = is_dv ? dvo : dxo;
+#pragma unroll
+          for (int r4 = 0; r4 < 32; r4 += 4) {
+            const int rw = r4 + (l >> 3), ch = l & 7;
+            *(uint4*)(outp + rowid(g, t.s, tok - l + rw) * HD + ch * 8) =
+                *(const uint4*)(stg + rw * 128 + ((ch ^ (rw & 7)) << 4));
           }
         }
         // d<., .>/d(log factor) = <dx~, x~>/2 (degree-2 homogeneity of phi')
