@@ -17,6 +17,7 @@
  *   pa_power_full_fwd <- chunked_power_attention chunked.py:287-413 (attention form when chunk >= t,
  *                        attention.py:273-309), with log-gates g = exp(log_g)
  *   pa_power_full_bwd <- vjp_chunked          gradients.py:361-483 (dlog_g = g * dgates)
+ *   pa_power_logspace_fwd <- power_attention_form use_log_space branch attention.py:289-305
  *   pa_feature_dim / pa_feature_table <- expansion_dim / monomial_table expansions.py:87-99, 171-198
  */
 #ifndef POWER_ATTENTION_B200_H
@@ -76,6 +77,16 @@ int pa_power_full_bwd(const pa_problem* pr, const void* q, const void* k, const 
                       const float* log_g, const void* y, const float* rowsum, const void* dy,
                       void* dq, void* dk, void* dv, float* dlog_g, const void* fwd_ws,
                       void* bwd_ws, size_t bwd_ws_bytes, pa_stream_t stream);
+
+/* Log-space (stabilised) attention form, reference attention.py:289-305
+ * (power_attention_form with use_log_space; even p only): scores
+ * p*log(|s|+eps) + log-decay, row-max shifted, exponentiated.  q, k, v, y of
+ * `pr->dtype` (F32 or F64), log_g and rowsum [b,t,h] of the same dtype (log_g
+ * may hold -inf for zero gates; NULL when ungated).  pr->chunk is ignored (one
+ * chunk spans the sequence); t <= 16384, e <= 128.  No workspace. */
+int pa_power_logspace_fwd(const pa_problem* pr, double eps, const void* q, const void* k,
+                          const void* v, const void* log_g, void* y, void* rowsum,
+                          pa_stream_t stream);
 
 /* ---------------------------------------------------------------- sequence parallel
  * A sequence split into contiguous chunk ranges, one per rank (

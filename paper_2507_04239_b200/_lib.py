@@ -67,6 +67,7 @@ _SIGS = {
     "pa_power_full_fwd": (ctypes.c_int, [_PP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _SZ, _VP]),
     "pa_power_full_bwd": (ctypes.c_int, [_PP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
                                           _VP, _VP, _VP, _SZ, _VP]),
+    "pa_power_logspace_fwd": (ctypes.c_int, [_PP, ctypes.c_double, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "pa_fwd_zero_denominators": (ctypes.c_int, [_PP, _VP, _VP, ctypes.POINTER(_I32)]),
     "pa_update_state": (ctypes.c_int, [_I32, _I32, _I32, _I32, _I32, _I32, _VP, _VP, _VP, _VP,
                                         _VP, _I32, _VP]),

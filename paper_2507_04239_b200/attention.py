@@ -143,8 +143,39 @@ def run_power(batch: SequenceBatch, cfg: AttentionConfig, chunk: int | None) -> 
 def power_attention_form(batch: SequenceBatch, cfg: AttentionConfig) -> AttentionOutput:
     """Quadratic form (attention.py:273-309): one chunk spanning the sequence."""
     if cfg.use_log_space:
-        raise InvalidSpec("the log-space scoring path is not on the CUDA path (SURVEY §8f)")
+        return run_log_space(batch, cfg)
     return run_power(batch, cfg, None)
+
+
+def run_log_space(batch: SequenceBatch, cfg: AttentionConfig) -> AttentionOutput:
+    """attention.py:289-305: the stabilised scores p*log(|s|+eps) + log-decay,
+    row-max shifted (pa_power_logspace_fwd).  f64 inputs compute in f64, f32 in
+    f32, half types in f32; eps = cfg.epsilon_for(dtype) (attention.py:152-155)."""
+    from .power import power_logspace_forward
+
+    if cfg.mechanism is not Mechanism.POWER:
+        raise InvalidSpec(f"only the power mechanism runs on the CUDA path, got {cfg.mechanism.value}")
+    spec = cfg.expansion.require_spow()
+    if spec.d != batch.d:
+        raise ShapeMismatch(f"spec.d={spec.d} but q has d={batch.d}")
+    host = batch.on_host
+    if host:
+        np_dt = np.result_type(_np(batch.q).dtype, _np(batch.v).dtype)
+        tdt = torch.float64 if np_dt == np.float64 else torch.float32
+    else:
+        np_dt = None
+        tdt = torch.float64 if batch.q.dtype == torch.float64 else torch.float32
+    q, k, v = (to_dev(x, tdt) for x in (batch.q, batch.k, batch.v))
+    lg = None
+    if batch.gates is not None:
+        g = to_dev(batch.gates, tdt)
+        lg = torch.log(g)  # -inf for zero gates: handled exactly by the kernel
+    eps = cfg.epsilon if cfg.epsilon is not None else (1e-12 if tdt == torch.float64 else 1e-7)
+    y, rs = power_logspace_forward(q, k, v, lg, p=spec.p, scale=cfg.scale, normalize=cfg.normalize,
+                                   eps=eps)
+    if not host and batch.q.dtype not in (torch.float32, torch.float64):
+        y = y.to(batch.q.dtype)
+    return AttentionOutput(back(y, host, np_dt), back(rs, host, np_dt))
 
 
 def attention(batch: SequenceBatch, cfg: AttentionConfig) -> AttentionOutput:

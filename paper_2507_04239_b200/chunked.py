@@ -11,7 +11,8 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from .attention import AttentionConfig, AttentionOutput, Mechanism, SequenceBatch, run_power
+from .attention import (AttentionConfig, AttentionOutput, Mechanism, SequenceBatch,
+                        power_attention_form, run_power)
 from .errors import InvalidSpec, ShapeMismatch, StateTooLarge, ZeroDenominator
 from .expansions import ExpansionSpec, expansion_dim
 from .kernels import discumsum_kernel, query_state_kernel, update_state_kernel
@@ -152,7 +153,14 @@ def query_state(state, q_chunk, y_attn=None, zeta=None, gates_prefix=None, scale
 def chunked_power_attention(batch: SequenceBatch, cfg: AttentionConfig, plan: ChunkPlan | None = None,
                             state_budget: int = DEFAULT_STATE_BUDGET, backend=None, op_timer=None):
     """chunked.py:287-413 as one CUDA pipeline call.  op_timer (if given)
-    accumulates wall ns of the whole fused pipeline under "power_full"."""
+    accumulates wall ns of the whole fused pipeline under "power_full".
+
+    cfg.use_log_space: the fused pipeline computes the intra-chunk scores in the
+    direct form (fp32 accumulation).  The reference's log-space intra-chunk path
+    (chunked.py:336 via attention.py:289-305) equals it within eps for
+    well-separated scores (test_chunked.py:318-330 bar 1e-6); the stabilised
+    kernel runs for the attention form (power_attention_form), where the
+    reference applies it to the whole row."""
     if cfg.mechanism not in (Mechanism.POWER, Mechanism.LINEAR) or cfg.expansion is None:
         raise InvalidSpec(f"{cfg.mechanism.value} mechanism has no feature expansion")
     spec = cfg.expansion
@@ -176,7 +184,7 @@ def chunked_power_attention(batch: SequenceBatch, cfg: AttentionConfig, plan: Ch
 def power_attention(batch, cfg, form="attention", plan=None, backend=None, op_timer=None):
     """chunked.py:461-476 (the recurrent form is an oracle-only form)."""
     if form == "attention":
-        return run_power(batch, cfg, None)
+        return power_attention_form(batch, cfg)
     if form == "chunked":
         return chunked_power_attention(batch, cfg, plan, backend=backend, op_timer=op_timer)
     if form == "recurrent":

@@ -137,3 +137,42 @@ def power_full(Q, K, V, log_G=None, *, p=2, chunk_size=None, scale=None, normali
 
 def default_scale(d: int) -> float:
     return 1.0 / math.sqrt(d)
+
+
+_LS_DTYPES = {torch.float32: _lib.PA_F32, torch.float64: _lib.PA_F64}
+
+
+def power_logspace_forward(Q, K, V, log_G=None, *, p=2, scale=None, normalize=False, eps=None):
+    """Stabilised attention form (reference attention.py:289-305, use_log_space):
+    forward only, through pa_power_logspace_fwd.  Q, K, V, log_G share one dtype
+    (float32 or float64); log_G may hold -inf for zero gates.  eps defaults to
+    the reference's DEFAULT_EPSILON (1e-7 f32, 1e-12 f64, attention.py:42).
+    Returns (y, rowsum).  Gradients of the log-space form are those of the
+    direct form (reference SPEC.md:325): use power_full / vjp_chunked."""
+    for name, x in (("Q", Q), ("K", K), ("V", V)):
+        if not isinstance(x, torch.Tensor) or x.dim() != 4:
+            raise ShapeMismatch(f"{name} must be a [b, t, h, feature] tensor")
+        if not x.is_cuda:
+            raise InvalidSpec(f"{name} must be a CUDA tensor (this package has no CPU path)")
+    if Q.dtype not in _LS_DTYPES or K.dtype != Q.dtype or V.dtype != Q.dtype:
+        raise InvalidSpec("log-space form: Q, K, V must share float32 or float64")
+    if K.shape != Q.shape or V.shape[:3] != Q.shape[:3]:
+        raise ShapeMismatch("log-space form: Q, K, V disagree on [b, t, h, d]")
+    if p % 2:
+        raise InvalidSpec(f"log-space scoring needs even p, got p={p}")
+    if eps is None:
+        eps = 1e-7 if Q.dtype == torch.float32 else 1e-12
+    lib = _lib.load()
+    Q, K, V = Q.contiguous(), K.contiguous(), V.contiguous()
+    lg = None if log_G is None else log_G.detach().to(Q.dtype).contiguous()
+    if lg is not None and tuple(lg.shape) != tuple(Q.shape[:3]):
+        raise ShapeMismatch(f"log_G shape {tuple(lg.shape)} != [b, t, h] {tuple(Q.shape[:3])}")
+    b, t, h, d = Q.shape
+    pr = _lib.PaProblem(b, t, h, d, V.shape[-1], int(p), t, float(scale) if scale else 0.0,
+                        int(bool(normalize)), _LS_DTYPES[Q.dtype], int(lg is not None))
+    y = torch.empty_like(V)
+    rowsum = torch.empty(Q.shape[:3], dtype=Q.dtype, device=Q.device)
+    rc = lib.pa_power_logspace_fwd(ctypes.byref(pr), float(eps), _ptr(Q), _ptr(K), _ptr(V), _ptr(lg),
+                                   _ptr(y), _ptr(rowsum), _stream(Q.device))
+    _lib.check(rc, "pa_power_logspace_fwd")
+    return y, rowsum
