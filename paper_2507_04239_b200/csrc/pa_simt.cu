@@ -918,6 +918,8 @@ template <typename T>
 static int simt_forward_dm(const Geo& g, const void* q, const void* k, const void* v, const float* lg,
                            void* y, float* rs, const SimtWs& w, cudaStream_t st) {
   const int mx = std::max(g.d, g.e);
+  if (mx <= 32)  // d = e = 32 (configs[2]): half the register rows and FMAs of DM = 64
+    return simt_forward_t<T, 32>(g, (const T*)q, (const T*)k, (const T*)v, lg, (T*)y, rs, w, st);
   if (mx <= 64)
     return simt_forward_t<T, 64>(g, (const T*)q, (const T*)k, (const T*)v, lg, (T*)y, rs, w, st);
   return simt_forward_t<T, 128>(g, (const T*)q, (const T*)k, (const T*)v, lg, (T*)y, rs, w, st);
@@ -939,6 +941,9 @@ static int simt_backward_dm(const Geo& g, const void* q, const void* k, const vo
                             const float* rs, const void* dy, void* dq, void* dk, void* dv,
                             float* dlogg, const SimtWs& w, const SimtBwdWs& b, cudaStream_t st) {
   const int mx = std::max(g.d, g.e);
+  if (mx <= 32)
+    return simt_backward_t<T, 32>(g, (const T*)q, (const T*)k, (const T*)v, (const T*)y, rs, (const T*)dy,
+                                  (T*)dq, (T*)dk, (T*)dv, dlogg, w, b, st);
   if (mx <= 64)
     return simt_backward_t<T, 64>(g, (const T*)q, (const T*)k, (const T*)v, (const T*)y, rs, (const T*)dy,
                                   (T*)dq, (T*)dk, (T*)dv, dlogg, w, b, st);
