@@ -428,6 +428,10 @@ __global__ void k_bwd_prep(Geo g, const T* __restrict__ dy, const float* __restr
   }
 }
 
+// staged state rows [D-block of 32][AS]: e + 1 columns padded with zeros to a
+// multiple of four floats, so the token-side kernels read them as LDS.128
+template <int DM> __host__ __device__ constexpr int state_row_stride() { return (DM + 1 + 3) / 4 * 4; }
+
 // accumulate d phi_f into dx (expand_vjp, gradients.py:46-76) -- shared row
 __device__ __forceinline__ void phi_vjp_add(const float* xrow, float* dxrow, const int* id, float gw,
                                             int p) {
@@ -458,12 +462,13 @@ __global__ void __launch_bounds__(64) k_query_bwd(Geo g, const T* __restrict__ q
                                                   float* dell) {
   extern __shared__ float sm_dyn[];
   float* sm_ptr = sm_dyn;
+  constexpr int AS = state_row_stride<DM>();
+  float (*As)[AS] = reinterpret_cast<float (*)[AS]>(sm_ptr);  // first: 16-byte aligned rows
+  sm_ptr += (32) * AS;
   float (*Qs)[DM + 1] = reinterpret_cast<float (*)[DM + 1]>(sm_ptr);
   sm_ptr += (64) * (DM + 1);
   float (*Dq)[DM + 1] = reinterpret_cast<float (*)[DM + 1]>(sm_ptr);
   sm_ptr += (64) * (DM + 1);
-  float (*As)[DM + 2] = reinterpret_cast<float (*)[DM + 2]>(sm_ptr);
-  sm_ptr += (32) * (DM + 2);
   __shared__ int Is[32][4];
   __shared__ float Ws[32];
   const int tpc = (g.c + 63) / 64;
@@ -477,24 +482,24 @@ __global__ void __launch_bounds__(64) k_query_bwd(Geo g, const T* __restrict__ q
     Qs[threadIdx.x][a] = (act && a < g.d) ? g.scale * to_f(q[rowid(g, s, i) * g.d + a]) : 0.f;
     Dq[threadIdx.x][a] = 0.f;
   }
-  float dzr[DM + 1];
+  // dz row in state-column order: [dnum (e) | dden | 0 ...] (AS columns)
+  float dzr[AS];
 #pragma unroll
-  for (int u = 0; u <= DM; ++u) dzr[u] = 0.f;
+  for (int u = 0; u < AS; ++u) dzr[u] = 0.f;
   if (act) {
     const float* dzi = dz + ((size_t)s * g.t + i) * g.E1;
 #pragma unroll
-    for (int u = 0; u < DM; ++u)
-      if (u < g.e) dzr[u] = dzi[u];
-    dzr[DM] = dzi[g.e];
+    for (int u = 0; u < AS; ++u)
+      if (u <= g.e) dzr[u] = dzi[u];
   }
   const float gp = (act && g.gated) ? expf(ell[(size_t)s * g.t + i]) : 1.f;
   float dl = 0.f;
   const float* Ak = A + ((size_t)s * g.n + (kch - 1)) * g.D * g.E1;
   for (int f0 = 0; f0 < g.D; f0 += 32) {
     __syncthreads();
-    for (int el = threadIdx.x; el < 32 * g.E1; el += 64) {
-      int r = el / g.E1, u = el - r * g.E1;
-      As[r][u] = (f0 + r < g.D) ? Ak[(size_t)(f0 + r) * g.E1 + u] : 0.f;
+    for (int el = threadIdx.x; el < 32 * AS; el += 64) {
+      int r = el / AS, u = el - r * AS;
+      As[r][u] = (f0 + r < g.D && u < g.E1) ? Ak[(size_t)(f0 + r) * g.E1 + u] : 0.f;
     }
     if (threadIdx.x < 32) {
       int f = f0 + threadIdx.x;
@@ -504,10 +509,15 @@ __global__ void __launch_bounds__(64) k_query_bwd(Geo g, const T* __restrict__ q
     __syncthreads();
     const int fn = min(32, g.D - f0);
     for (int fl = 0; fl < fn; ++fl) {
-      float tf = 0.f;
+      const float4* ar = reinterpret_cast<const float4*>(As[fl]);
+      float tf = 0.f, tf2 = 0.f;
 #pragma unroll
-      for (int u = 0; u < DM; ++u) tf += As[fl][u] * dzr[u];
-      tf += As[fl][g.e] * dzr[DM];
+      for (int q4 = 0; q4 < AS / 4; ++q4) {
+        const float4 a4 = ar[q4];
+        tf += a4.x * dzr[4 * q4] + a4.z * dzr[4 * q4 + 2];
+        tf2 += a4.y * dzr[4 * q4 + 1] + a4.w * dzr[4 * q4 + 3];
+      }
+      tf += tf2;
       const float ph = phi_at(Qs[threadIdx.x], Is[fl], Ws[fl], g.p);
       dl += ph * tf;
       phi_vjp_add(Qs[threadIdx.x], Dq[threadIdx.x], Is[fl], Ws[fl] * gp * tf, g.p);
@@ -562,12 +572,13 @@ __global__ void __launch_bounds__(64) k_update_bwd(Geo g, const T* __restrict__ 
                                                    float* dv32, float* dell, float* dellend) {
   extern __shared__ float sm_dyn[];
   float* sm_ptr = sm_dyn;
+  constexpr int AS = state_row_stride<DM>();
+  float (*Ss)[AS] = reinterpret_cast<float (*)[AS]>(sm_ptr);  // first: 16-byte aligned rows
+  sm_ptr += (32) * AS;
   float (*Ks)[DM + 1] = reinterpret_cast<float (*)[DM + 1]>(sm_ptr);
   sm_ptr += (64) * (DM + 1);
   float (*Dk)[DM + 1] = reinterpret_cast<float (*)[DM + 1]>(sm_ptr);
   sm_ptr += (64) * (DM + 1);
-  float (*Ss)[DM + 2] = reinterpret_cast<float (*)[DM + 2]>(sm_ptr);
-  sm_ptr += (32) * (DM + 2);
   __shared__ int Is[32][4];
   __shared__ float Ws[32];
   __shared__ float red[32];
@@ -582,21 +593,21 @@ __global__ void __launch_bounds__(64) k_update_bwd(Geo g, const T* __restrict__ 
     Ks[threadIdx.x][a] = (act && a < g.d) ? to_f(k[rowid(g, s, j) * g.d + a]) : 0.f;
     Dk[threadIdx.x][a] = 0.f;
   }
-  float vr[DM + 1], dvr[DM];
+  // [v_j | 1 | 0 ...] in state-column order (AS columns)
+  float vr[AS], dvr[AS];
 #pragma unroll
-  for (int u = 0; u < DM; ++u) {
-    vr[u] = (act && u < g.e) ? to_f(v[rowid(g, s, j) * g.e + u]) : 0.f;
+  for (int u = 0; u < AS; ++u) {
+    vr[u] = (act && u < g.e) ? to_f(v[rowid(g, s, j) * g.e + u]) : (u == g.e ? 1.f : 0.f);
     dvr[u] = 0.f;
   }
-  vr[DM] = 1.f;
   const float W = (act && g.gated) ? expf(lamlog[s * g.n + kch] - ell[(size_t)s * g.t + j]) : 1.f;
   float dW = 0.f;
   const float* Sk = dS + ((size_t)s * g.n + kch) * g.D * g.E1;
   for (int f0 = 0; f0 < g.D; f0 += 32) {
     __syncthreads();
-    for (int el = threadIdx.x; el < 32 * g.E1; el += 64) {
-      int r = el / g.E1, u = el - r * g.E1;
-      Ss[r][u] = (f0 + r < g.D) ? Sk[(size_t)(f0 + r) * g.E1 + u] : 0.f;
+    for (int el = threadIdx.x; el < 32 * AS; el += 64) {
+      int r = el / AS, u = el - r * AS;
+      Ss[r][u] = (f0 + r < g.D && u < g.E1) ? Sk[(size_t)(f0 + r) * g.E1 + u] : 0.f;
     }
     if (threadIdx.x < 32) {
       int f = f0 + threadIdx.x;
@@ -606,15 +617,27 @@ __global__ void __launch_bounds__(64) k_update_bwd(Geo g, const T* __restrict__ 
     __syncthreads();
     const int fn = min(32, g.D - f0);
     for (int fl = 0; fl < fn; ++fl) {
-      float tf = Ss[fl][g.e];
+      const float4* sr = reinterpret_cast<const float4*>(Ss[fl]);
+      float tf = 0.f, tf2 = 0.f;
 #pragma unroll
-      for (int u = 0; u < DM; ++u) tf += Ss[fl][u] * vr[u];
+      for (int q4 = 0; q4 < AS / 4; ++q4) {
+        const float4 s4 = sr[q4];
+        tf += s4.x * vr[4 * q4] + s4.z * vr[4 * q4 + 2];
+        tf2 += s4.y * vr[4 * q4 + 1] + s4.w * vr[4 * q4 + 3];
+      }
+      tf += tf2;
       const float ph = phi_at(Ks[threadIdx.x], Is[fl], Ws[fl], g.p);
       dW += ph * tf;
       phi_vjp_add(Ks[threadIdx.x], Dk[threadIdx.x], Is[fl], Ws[fl] * W * tf, g.p);
       const float wp = W * ph;
 #pragma unroll
-      for (int u = 0; u < DM; ++u) dvr[u] += wp * Ss[fl][u];
+      for (int q4 = 0; q4 < AS / 4; ++q4) {
+        const float4 s4 = sr[q4];
+        dvr[4 * q4] += wp * s4.x;
+        dvr[4 * q4 + 1] += wp * s4.y;
+        dvr[4 * q4 + 2] += wp * s4.z;
+        dvr[4 * q4 + 3] += wp * s4.w;
+      }
     }
   }
   const float contrib = act ? W * dW : 0.f;
@@ -912,7 +935,7 @@ __global__ void k_pub_discumsum(int n, int64_t L, int64_t M, const A* __restrict
 // dynamic shared memory per block for the kernels above (floats -> bytes)
 template <int DM> constexpr size_t smb_intra_fwd() { return 4 * (2 * 64 * (DM + 1)); }
 template <int DM> constexpr size_t smb_query_combine() { return 4 * (64 * (DM + 1) + 32 * (DM + 2)); }
-template <int DM> constexpr size_t smb_query_bwd() { return 4 * (2 * 64 * (DM + 1) + 32 * (DM + 2)); }
+template <int DM> constexpr size_t smb_query_bwd() { return 4 * (2 * 64 * (DM + 1) + 32 * state_row_stride<DM>()); }
 template <int DM> constexpr size_t smb_update_bwd() { return smb_query_bwd<DM>(); }
 template <int DM> constexpr size_t smb_intra_bwd() { return 4 * (3 * 64 * (DM + 1) + 64 * (DM + 2)); }
 
