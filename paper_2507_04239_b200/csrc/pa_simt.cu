@@ -447,6 +447,32 @@ __device__ __forceinline__ void phi_vjp_add(const float* xrow, float* dxrow, con
   }
 }
 
+// phi_f and its expand-VJP from one read of the p coordinates: the partial
+// derivatives are products of the other three factors (padded with ones for
+// z >= p), formed from pairwise products instead of p reloads per factor.
+struct PhiParts {
+  float ph, d[4];
+};
+__device__ __forceinline__ PhiParts phi_parts(const float* xrow, const int* id, float w, int p) {
+  float x[4];
+#pragma unroll
+  for (int z = 0; z < 4; ++z) x[z] = z < p ? xrow[id[z]] : 1.f;
+  const float p01 = x[0] * x[1], p23 = x[2] * x[3];
+  PhiParts r;
+  r.ph = w * p01 * p23;
+  r.d[0] = x[1] * p23;
+  r.d[1] = x[0] * p23;
+  r.d[2] = p01 * x[3];
+  r.d[3] = p01 * x[2];
+  return r;
+}
+__device__ __forceinline__ void phi_parts_vjp_add(float* dxrow, const int* id, const PhiParts& pp,
+                                                  float gw, int p) {
+#pragma unroll
+  for (int z = 0; z < 4; ++z)
+    if (z < p) dxrow[id[z]] += gw * pp.d[z];
+}
+
 // --------------------------------------------------------------------------
 // query-state backward, token side (gradients.py:406-431):
 //   t_f = A_{k-1}[f,:] . dz_i ; dq_i += sigma * expand_vjp(sigma q_i, gp_i t)
@@ -518,9 +544,9 @@ __global__ void __launch_bounds__(64) k_query_bwd(Geo g, const T* __restrict__ q
         tf2 += a4.y * dzr[4 * q4 + 1] + a4.w * dzr[4 * q4 + 3];
       }
       tf += tf2;
-      const float ph = phi_at(Qs[threadIdx.x], Is[fl], Ws[fl], g.p);
-      dl += ph * tf;
-      phi_vjp_add(Qs[threadIdx.x], Dq[threadIdx.x], Is[fl], Ws[fl] * gp * tf, g.p);
+      const PhiParts pp = phi_parts(Qs[threadIdx.x], Is[fl], Ws[fl], g.p);
+      dl += pp.ph * tf;
+      phi_parts_vjp_add(Dq[threadIdx.x], Is[fl], pp, Ws[fl] * gp * tf, g.p);
     }
   }
   if (!act) return;
@@ -626,10 +652,10 @@ __global__ void __launch_bounds__(64) k_update_bwd(Geo g, const T* __restrict__ 
         tf2 += s4.y * vr[4 * q4 + 1] + s4.w * vr[4 * q4 + 3];
       }
       tf += tf2;
-      const float ph = phi_at(Ks[threadIdx.x], Is[fl], Ws[fl], g.p);
-      dW += ph * tf;
-      phi_vjp_add(Ks[threadIdx.x], Dk[threadIdx.x], Is[fl], Ws[fl] * W * tf, g.p);
-      const float wp = W * ph;
+      const PhiParts pp = phi_parts(Ks[threadIdx.x], Is[fl], Ws[fl], g.p);
+      dW += pp.ph * tf;
+      phi_parts_vjp_add(Dk[threadIdx.x], Is[fl], pp, Ws[fl] * W * tf, g.p);
+      const float wp = W * pp.ph;
 #pragma unroll
       for (int q4 = 0; q4 < AS / 4; ++q4) {
         const float4 s4 = sr[q4];
