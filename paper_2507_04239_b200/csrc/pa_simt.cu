@@ -341,10 +341,11 @@ __global__ void __launch_bounds__(64) k_query_combine(Geo g, const T* __restrict
                                                       float* rowsum, int* zflag, float* y32) {
   extern __shared__ float sm_dyn[];
   float* sm_ptr = sm_dyn;
+  constexpr int AS = (DM + 1 + 3) / 4 * 4;  // state_row_stride<DM>()
+  float (*As)[AS] = reinterpret_cast<float (*)[AS]>(sm_ptr);  // first: 16-byte aligned rows
+  sm_ptr += (32) * AS;
   float (*Qs)[DM + 1] = reinterpret_cast<float (*)[DM + 1]>(sm_ptr);
   sm_ptr += (64) * (DM + 1);
-  float (*As)[DM + 2] = reinterpret_cast<float (*)[DM + 2]>(sm_ptr);
-  sm_ptr += (32) * (DM + 2);
   __shared__ int Is[32][4];
   __shared__ float Ws[32];
   const int tpc = (g.c + 63) / 64;
@@ -355,16 +356,16 @@ __global__ void __launch_bounds__(64) k_query_combine(Geo g, const T* __restrict
   const int i = q0 + threadIdx.x;
   const bool act = i < s1;
   for (int a = 0; a < DM; ++a) Qs[threadIdx.x][a] = (act && a < g.d) ? g.scale * to_f(q[rowid(g, s, i) * g.d + a]) : 0.f;
-  float acc[DM + 1];
+  float acc[AS], accs = 0.f;  // state columns (score column e included) | score sum
 #pragma unroll
-  for (int u = 0; u <= DM; ++u) acc[u] = 0.f;
+  for (int u = 0; u < AS; ++u) acc[u] = 0.f;
   if (kch >= 1) {
     const float* Ak = A + ((size_t)s * g.n + (kch - 1)) * g.D * g.E1;
     for (int f0 = 0; f0 < g.D; f0 += 32) {
       __syncthreads();
-      for (int el = threadIdx.x; el < 32 * g.E1; el += 64) {
-        int r = el / g.E1, u = el - r * g.E1;
-        As[r][u] = (f0 + r < g.D) ? Ak[(size_t)(f0 + r) * g.E1 + u] : 0.f;
+      for (int el = threadIdx.x; el < 32 * AS; el += 64) {
+        int r = el / AS, u = el - r * AS;
+        As[r][u] = (f0 + r < g.D && u < g.E1) ? Ak[(size_t)(f0 + r) * g.E1 + u] : 0.f;
       }
       if (threadIdx.x < 32) {
         int f = f0 + threadIdx.x;
@@ -375,16 +376,23 @@ __global__ void __launch_bounds__(64) k_query_combine(Geo g, const T* __restrict
       const int fn = min(32, g.D - f0);
       for (int fl = 0; fl < fn; ++fl) {
         const float ph = phi_at(Qs[threadIdx.x], Is[fl], Ws[fl], g.p);
+        const float4* ar = reinterpret_cast<const float4*>(As[fl]);
 #pragma unroll
-        for (int u = 0; u < DM; ++u) acc[u] += ph * As[fl][u];
-        acc[DM] += ph * As[fl][g.e];
+        for (int q4 = 0; q4 < AS / 4; ++q4) {
+          const float4 a4 = ar[q4];
+          acc[4 * q4] += ph * a4.x;
+          acc[4 * q4 + 1] += ph * a4.y;
+          acc[4 * q4 + 2] += ph * a4.z;
+          acc[4 * q4 + 3] += ph * a4.w;
+        }
+        accs += ph * As[fl][g.e];
       }
     }
   }
   if (!act) return;
   const float gp = g.gated ? expf(ell[(size_t)s * g.t + i]) : 1.f;
   const float* ya = yat + ((size_t)s * g.t + i) * g.E1;
-  const float R = ya[g.e] + gp * acc[DM];
+  const float R = ya[g.e] + gp * accs;
   const size_t r = rowid(g, s, i);
   if (rowsum) rowsum[r] = R;
   float inv = 1.f;
@@ -643,6 +651,10 @@ __global__ void __launch_bounds__(64) k_update_bwd(Geo g, const T* __restrict__ 
     __syncthreads();
     const int fn = min(32, g.D - f0);
     for (int fl = 0; fl < fn; ++fl) {
+      // phi_f depends on k only: one pass over the state row feeds both
+      // t_f = S_f . [v|1] and dv += W phi_f S_f
+      const PhiParts pp = phi_parts(Ks[threadIdx.x], Is[fl], Ws[fl], g.p);
+      const float wp = W * pp.ph;
       const float4* sr = reinterpret_cast<const float4*>(Ss[fl]);
       float tf = 0.f, tf2 = 0.f;
 #pragma unroll
@@ -650,20 +662,14 @@ __global__ void __launch_bounds__(64) k_update_bwd(Geo g, const T* __restrict__ 
         const float4 s4 = sr[q4];
         tf += s4.x * vr[4 * q4] + s4.z * vr[4 * q4 + 2];
         tf2 += s4.y * vr[4 * q4 + 1] + s4.w * vr[4 * q4 + 3];
-      }
-      tf += tf2;
-      const PhiParts pp = phi_parts(Ks[threadIdx.x], Is[fl], Ws[fl], g.p);
-      dW += pp.ph * tf;
-      phi_parts_vjp_add(Dk[threadIdx.x], Is[fl], pp, Ws[fl] * W * tf, g.p);
-      const float wp = W * pp.ph;
-#pragma unroll
-      for (int q4 = 0; q4 < AS / 4; ++q4) {
-        const float4 s4 = sr[q4];
         dvr[4 * q4] += wp * s4.x;
         dvr[4 * q4 + 1] += wp * s4.y;
         dvr[4 * q4 + 2] += wp * s4.z;
         dvr[4 * q4 + 3] += wp * s4.w;
       }
+      tf += tf2;
+      dW += pp.ph * tf;
+      phi_parts_vjp_add(Dk[threadIdx.x], Is[fl], pp, Ws[fl] * W * tf, g.p);
     }
   }
   const float contrib = act ? W * dW : 0.f;
@@ -960,7 +966,7 @@ __global__ void k_pub_discumsum(int n, int64_t L, int64_t M, const A* __restrict
 
 // dynamic shared memory per block for the kernels above (floats -> bytes)
 template <int DM> constexpr size_t smb_intra_fwd() { return 4 * (2 * 64 * (DM + 1)); }
-template <int DM> constexpr size_t smb_query_combine() { return 4 * (64 * (DM + 1) + 32 * (DM + 2)); }
+template <int DM> constexpr size_t smb_query_combine() { return 4 * (64 * (DM + 1) + 32 * state_row_stride<DM>()); }
 template <int DM> constexpr size_t smb_query_bwd() { return 4 * (2 * 64 * (DM + 1) + 32 * state_row_stride<DM>()); }
 template <int DM> constexpr size_t smb_update_bwd() { return smb_query_bwd<DM>(); }
 template <int DM> constexpr size_t smb_intra_bwd() { return 4 * (3 * 64 * (DM + 1) + 64 * (DM + 2)); }
