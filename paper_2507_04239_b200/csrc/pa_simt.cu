@@ -243,8 +243,10 @@ __global__ void __launch_bounds__(256) k_state_accum(Geo g, const TX* __restrict
 // per token and feeds all ncol columns from broadcast LDS.128 reads of the
 // staged value row, instead of eight threads each regenerating phi_f for
 // every eighth column (3x fewer instructions per feature-token at p = 4).
+// features per CTA: the staged token rows are shared by this many features
+constexpr int kSaThreads = 256;
 template <typename TX, typename TV, int DM>
-__global__ void __launch_bounds__(128) k_state_accum_f(Geo g, const TX* __restrict__ x, float xs,
+__global__ void __launch_bounds__(kSaThreads) k_state_accum_f(Geo g, const TX* __restrict__ x, float xs,
                                                        int wmode, const float* __restrict__ ell,
                                                        const float* __restrict__ lamlog,
                                                        const TV* __restrict__ vec, int vec_bth, int ldv,
@@ -254,7 +256,7 @@ __global__ void __launch_bounds__(128) k_state_accum_f(Geo g, const TX* __restri
   constexpr int US = (DM + 1 + 3) / 4 * 4;  // value row stride, 16-byte aligned
   __shared__ float Xs[32][DM + 1];
   __shared__ __align__(16) float Us[32][US];
-  const int f = blockIdx.x * 128 + threadIdx.x;
+  const int f = blockIdx.x * kSaThreads + threadIdx.x;
   const int kin = kfirst + blockIdx.y, s = blockIdx.z;
   const int s0 = kin * g.c, s1 = min(s0 + g.c, g.t);
   const int ncol = ev + (ones ? 1 : 0);
@@ -272,7 +274,7 @@ __global__ void __launch_bounds__(128) k_state_accum_f(Geo g, const TX* __restri
   gv.bth = vec_bth;
   for (int j0 = s0; j0 < s1; j0 += 32) {
     __syncthreads();
-    for (int el = threadIdx.x; el < 32 * US; el += 128) {
+    for (int el = threadIdx.x; el < 32 * US; el += kSaThreads) {
       int r = el / US, a = el - r * US;
       int j = j0 + r;
       bool ok = j < s1;
@@ -992,7 +994,7 @@ static int simt_forward_t(const Geo& g, const T* q, const T* k, const T* v, cons
   k_gate_prep<<<(g.ns * g.n + 127) / 128, 128, 0, st>>>(g, log_g, w.ell, w.lamlog);
   k_intra_fwd<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_intra_fwd<T, DM>, smb_intra_fwd<DM>()), st>>>(g, q, k, v, w.ell, w.yat);
   if constexpr (DM <= 64)
-    k_state_accum_f<T, T, DM><<<dim3((g.D + 127) / 128, g.n, g.ns), 128, 0, st>>>(
+    k_state_accum_f<T, T, DM><<<dim3((g.D + kSaThreads - 1) / kSaThreads, g.n, g.ns), kSaThreads, 0, st>>>(
         g, k, 1.f, g.gated ? 1 : 0, w.ell, w.lamlog, v, 1, g.e, g.e, 1, w.idx, w.wt, 0, 0, w.A);
   else
     k_state_accum<T, T, DM><<<dim3((g.D + 31) / 32, g.n, g.ns), 256, 0, st>>>(
@@ -1023,7 +1025,7 @@ static int simt_backward_t(const Geo& g, const T* q, const T* k, const T* v, con
     k_query_bwd<T, DM><<<dim3((g.n - 1) * tpc, g.ns), 64, dyn_smem(k_query_bwd<T, DM>, smb_query_bwd<DM>()), st>>>(g, q, w.A, w.idx, w.wt, w.ell, b.dz, b.dq32, b.dell);
     Geo gz = g;
     if constexpr (DM <= 64)
-      k_state_accum_f<T, float, DM><<<dim3((g.D + 127) / 128, g.n - 1, g.ns), 128, 0, st>>>(
+      k_state_accum_f<T, float, DM><<<dim3((g.D + kSaThreads - 1) / kSaThreads, g.n - 1, g.ns), kSaThreads, 0, st>>>(
           gz, q, g.scale, g.gated ? 2 : 0, w.ell, w.lamlog, b.dz, 0, g.E1, g.E1, 0, w.idx, w.wt, 1, 1, b.dA);
     else
       k_state_accum<T, float, DM><<<dim3((g.D + 31) / 32, g.n - 1, g.ns), 256, 0, st>>>(
