@@ -597,8 +597,12 @@ __global__ void __launch_bounds__(256) k_discumsum_bwd(Geo g, const float* __res
 //   t_f = dS_k[f,:] . [v_j,1];  dk_j += expand_vjp(k_j, W_j t);  dv_j += W_j phi(k_j)^T dS_k
 //   dW_j = phi(k_j).t  ->  dell_j -= W_j dW_j,  dell_end(k) += W_j dW_j
 // --------------------------------------------------------------------------
+// tokens per CTA of the update VJP: each staged block of 32 state rows is
+// shared by this many tokens (64 at DM = 128, where shared memory limits it)
+template <int DM> __host__ __device__ constexpr int ub_tokens() { return DM <= 64 ? 128 : 64; }
+
 template <typename T, int DM>
-__global__ void __launch_bounds__(64) k_update_bwd(Geo g, const T* __restrict__ k,
+__global__ void __launch_bounds__(ub_tokens<DM>()) k_update_bwd(Geo g, const T* __restrict__ k,
                                                    const T* __restrict__ v,
                                                    const float* __restrict__ dS,
                                                    const int* __restrict__ idx,
@@ -611,17 +615,18 @@ __global__ void __launch_bounds__(64) k_update_bwd(Geo g, const T* __restrict__ 
   constexpr int AS = state_row_stride<DM>();
   float (*Ss)[AS] = reinterpret_cast<float (*)[AS]>(sm_ptr);  // first: 16-byte aligned rows
   sm_ptr += (32) * AS;
+  constexpr int TOK = ub_tokens<DM>();
   float (*Ks)[DM + 1] = reinterpret_cast<float (*)[DM + 1]>(sm_ptr);
-  sm_ptr += (64) * (DM + 1);
+  sm_ptr += (TOK) * (DM + 1);
   float (*Dk)[DM + 1] = reinterpret_cast<float (*)[DM + 1]>(sm_ptr);
-  sm_ptr += (64) * (DM + 1);
+  sm_ptr += (TOK) * (DM + 1);
   __shared__ int Is[32][4];
   __shared__ float Ws[32];
   __shared__ float red[32];
-  const int tpc = (g.c + 63) / 64;
+  const int tpc = (g.c + TOK - 1) / TOK;
   const int kch = blockIdx.x / tpc, tile = blockIdx.x % tpc, s = blockIdx.y;
   const int s0 = kch * g.c, s1 = min(s0 + g.c, g.t);
-  const int q0 = s0 + tile * 64;
+  const int q0 = s0 + tile * TOK;
   if (q0 >= s1) return;
   const int j = q0 + threadIdx.x;
   const bool act = j < s1;
@@ -641,7 +646,7 @@ __global__ void __launch_bounds__(64) k_update_bwd(Geo g, const T* __restrict__ 
   const float* Sk = dS + ((size_t)s * g.n + kch) * g.D * g.E1;
   for (int f0 = 0; f0 < g.D; f0 += 32) {
     __syncthreads();
-    for (int el = threadIdx.x; el < 32 * AS; el += 64) {
+    for (int el = threadIdx.x; el < 32 * AS; el += TOK) {
       int r = el / AS, u = el - r * AS;
       Ss[r][u] = (f0 + r < g.D && u < g.E1) ? Sk[(size_t)(f0 + r) * g.E1 + u] : 0.f;
     }
@@ -970,7 +975,7 @@ __global__ void k_pub_discumsum(int n, int64_t L, int64_t M, const A* __restrict
 template <int DM> constexpr size_t smb_intra_fwd() { return 4 * (2 * 64 * (DM + 1)); }
 template <int DM> constexpr size_t smb_query_combine() { return 4 * (64 * (DM + 1) + 32 * state_row_stride<DM>()); }
 template <int DM> constexpr size_t smb_query_bwd() { return 4 * (2 * 64 * (DM + 1) + 32 * state_row_stride<DM>()); }
-template <int DM> constexpr size_t smb_update_bwd() { return smb_query_bwd<DM>(); }
+template <int DM> constexpr size_t smb_update_bwd() { return 4 * (2 * ub_tokens<DM>() * (DM + 1) + 32 * state_row_stride<DM>()); }
 template <int DM> constexpr size_t smb_intra_bwd() { return 4 * (3 * 64 * (DM + 1) + 64 * (DM + 2)); }
 
 template <typename K>
@@ -1033,7 +1038,8 @@ static int simt_backward_t(const Geo& g, const T* q, const T* k, const T* v, con
     k_discumsum_bwd<<<dim3((unsigned)((per + 255) / 256), g.ns), 256, 0, st>>>(g, w.lamlog, w.A, b.dA, b.dlam);
     launches += 3;
   }
-  k_update_bwd<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_update_bwd<T, DM>, smb_update_bwd<DM>()), st>>>(g, k, v, b.dA, w.idx, w.wt, w.ell, w.lamlog, b.dk32, b.dv32, b.dell, b.dellend);
+  k_update_bwd<T, DM><<<dim3(g.n * ((g.c + ub_tokens<DM>() - 1) / ub_tokens<DM>()), g.ns), ub_tokens<DM>(),
+                        dyn_smem(k_update_bwd<T, DM>, smb_update_bwd<DM>()), st>>>(g, k, v, b.dA, w.idx, w.wt, w.ell, w.lamlog, b.dk32, b.dv32, b.dell, b.dellend);
   k_intra_bwd_q<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_intra_bwd_q<T, DM>, smb_intra_bwd<DM>()), st>>>(g, q, k, v, w.ell, b.dz, b.dq32, b.dell);
   k_intra_bwd_kv<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_intra_bwd_kv<T, DM>, smb_intra_bwd<DM>()), st>>>(g, q, k, v, w.ell, b.dz, b.dk32, b.dv32, b.dell);
   launches += 3;
