@@ -438,6 +438,10 @@ __global__ void k_bwd_prep(Geo g, const T* __restrict__ dy, const float* __restr
   }
 }
 
+// tokens per CTA of the token-side state VJPs: each staged block of 32 state rows is
+// shared by this many tokens (64 at DM = 128, where shared memory limits it)
+template <int DM> __host__ __device__ constexpr int ub_tokens() { return DM <= 64 ? 128 : 64; }
+
 // staged state rows [D-block of 32][AS]: e + 1 columns padded with zeros to a
 // multiple of four floats, so the token-side kernels read them as LDS.128
 template <int DM> __host__ __device__ constexpr int state_row_stride() { return (DM + 1 + 3) / 4 * 4; }
@@ -489,7 +493,7 @@ __device__ __forceinline__ void phi_parts_vjp_add(float* dxrow, const int* id, c
 //   dell_i += gp_i * sum_f phi_f(sigma q_i) t_f      (gate prefix, 260-264)
 // --------------------------------------------------------------------------
 template <typename T, int DM>
-__global__ void __launch_bounds__(64) k_query_bwd(Geo g, const T* __restrict__ q,
+__global__ void __launch_bounds__(ub_tokens<DM>()) k_query_bwd(Geo g, const T* __restrict__ q,
                                                   const float* __restrict__ A,
                                                   const int* __restrict__ idx,
                                                   const float* __restrict__ wt,
@@ -501,16 +505,17 @@ __global__ void __launch_bounds__(64) k_query_bwd(Geo g, const T* __restrict__ q
   constexpr int AS = state_row_stride<DM>();
   float (*As)[AS] = reinterpret_cast<float (*)[AS]>(sm_ptr);  // first: 16-byte aligned rows
   sm_ptr += (32) * AS;
+  constexpr int TOK = ub_tokens<DM>();
   float (*Qs)[DM + 1] = reinterpret_cast<float (*)[DM + 1]>(sm_ptr);
-  sm_ptr += (64) * (DM + 1);
+  sm_ptr += (TOK) * (DM + 1);
   float (*Dq)[DM + 1] = reinterpret_cast<float (*)[DM + 1]>(sm_ptr);
-  sm_ptr += (64) * (DM + 1);
+  sm_ptr += (TOK) * (DM + 1);
   __shared__ int Is[32][4];
   __shared__ float Ws[32];
-  const int tpc = (g.c + 63) / 64;
+  const int tpc = (g.c + TOK - 1) / TOK;
   const int kch = 1 + blockIdx.x / tpc, tile = blockIdx.x % tpc, s = blockIdx.y;
   const int s0 = kch * g.c, s1 = min(s0 + g.c, g.t);
-  const int q0 = s0 + tile * 64;
+  const int q0 = s0 + tile * TOK;
   if (q0 >= s1) return;
   const int i = q0 + threadIdx.x;
   const bool act = i < s1;
@@ -533,7 +538,7 @@ __global__ void __launch_bounds__(64) k_query_bwd(Geo g, const T* __restrict__ q
   const float* Ak = A + ((size_t)s * g.n + (kch - 1)) * g.D * g.E1;
   for (int f0 = 0; f0 < g.D; f0 += 32) {
     __syncthreads();
-    for (int el = threadIdx.x; el < 32 * AS; el += 64) {
+    for (int el = threadIdx.x; el < 32 * AS; el += TOK) {
       int r = el / AS, u = el - r * AS;
       As[r][u] = (f0 + r < g.D && u < g.E1) ? Ak[(size_t)(f0 + r) * g.E1 + u] : 0.f;
     }
@@ -597,10 +602,6 @@ __global__ void __launch_bounds__(256) k_discumsum_bwd(Geo g, const float* __res
 //   t_f = dS_k[f,:] . [v_j,1];  dk_j += expand_vjp(k_j, W_j t);  dv_j += W_j phi(k_j)^T dS_k
 //   dW_j = phi(k_j).t  ->  dell_j -= W_j dW_j,  dell_end(k) += W_j dW_j
 // --------------------------------------------------------------------------
-// tokens per CTA of the update VJP: each staged block of 32 state rows is
-// shared by this many tokens (64 at DM = 128, where shared memory limits it)
-template <int DM> __host__ __device__ constexpr int ub_tokens() { return DM <= 64 ? 128 : 64; }
-
 template <typename T, int DM>
 __global__ void __launch_bounds__(ub_tokens<DM>()) k_update_bwd(Geo g, const T* __restrict__ k,
                                                    const T* __restrict__ v,
@@ -974,7 +975,7 @@ __global__ void k_pub_discumsum(int n, int64_t L, int64_t M, const A* __restrict
 // dynamic shared memory per block for the kernels above (floats -> bytes)
 template <int DM> constexpr size_t smb_intra_fwd() { return 4 * (2 * 64 * (DM + 1)); }
 template <int DM> constexpr size_t smb_query_combine() { return 4 * (64 * (DM + 1) + 32 * state_row_stride<DM>()); }
-template <int DM> constexpr size_t smb_query_bwd() { return 4 * (2 * 64 * (DM + 1) + 32 * state_row_stride<DM>()); }
+template <int DM> constexpr size_t smb_query_bwd() { return 4 * (2 * ub_tokens<DM>() * (DM + 1) + 32 * state_row_stride<DM>()); }
 template <int DM> constexpr size_t smb_update_bwd() { return 4 * (2 * ub_tokens<DM>() * (DM + 1) + 32 * state_row_stride<DM>()); }
 template <int DM> constexpr size_t smb_intra_bwd() { return 4 * (3 * 64 * (DM + 1) + 64 * (DM + 2)); }
 
@@ -1027,7 +1028,8 @@ static int simt_backward_t(const Geo& g, const T* q, const T* k, const T* v, con
   k_bwd_prep<T><<<nblk((size_t)g.ns * g.t, 256), 256, 0, st>>>(g, dy, w.y32, rowsum, b.dz);
   ++launches;
   if (g.n > 1) {
-    k_query_bwd<T, DM><<<dim3((g.n - 1) * tpc, g.ns), 64, dyn_smem(k_query_bwd<T, DM>, smb_query_bwd<DM>()), st>>>(g, q, w.A, w.idx, w.wt, w.ell, b.dz, b.dq32, b.dell);
+    k_query_bwd<T, DM><<<dim3((g.n - 1) * ((g.c + ub_tokens<DM>() - 1) / ub_tokens<DM>()), g.ns), ub_tokens<DM>(),
+                          dyn_smem(k_query_bwd<T, DM>, smb_query_bwd<DM>()), st>>>(g, q, w.A, w.idx, w.wt, w.ell, b.dz, b.dq32, b.dell);
     Geo gz = g;
     if constexpr (DM <= 64)
       k_state_accum_f<T, float, DM><<<dim3((g.D + kSaThreads - 1) / kSaThreads, g.n - 1, g.ns), kSaThreads, 0, st>>>(
