@@ -333,8 +333,11 @@ __global__ void k_discumsum_states(Geo g, const float* __restrict__ lamlog, floa
 // query-state + combine + normalize (kernels.py:86-110, chunked.py:372-395):
 //   y_i = yat_i + gp_i phi(sigma q_i)^T A_{k-1};  optional y /= rowsum
 // --------------------------------------------------------------------------
+// tokens per CTA of the query-combine kernel (shares each staged state block)
+template <int DM> __host__ __device__ constexpr int qc_tokens() { return DM <= 64 ? 128 : 64; }
+
 template <typename T, int DM>
-__global__ void __launch_bounds__(64) k_query_combine(Geo g, const T* __restrict__ q,
+__global__ void __launch_bounds__(qc_tokens<DM>()) k_query_combine(Geo g, const T* __restrict__ q,
                                                       const float* __restrict__ A,
                                                       const int* __restrict__ idx,
                                                       const float* __restrict__ wt,
@@ -346,14 +349,15 @@ __global__ void __launch_bounds__(64) k_query_combine(Geo g, const T* __restrict
   constexpr int AS = (DM + 1 + 3) / 4 * 4;  // state_row_stride<DM>()
   float (*As)[AS] = reinterpret_cast<float (*)[AS]>(sm_ptr);  // first: 16-byte aligned rows
   sm_ptr += (32) * AS;
+  constexpr int TOK = qc_tokens<DM>();
   float (*Qs)[DM + 1] = reinterpret_cast<float (*)[DM + 1]>(sm_ptr);
-  sm_ptr += (64) * (DM + 1);
+  sm_ptr += (TOK) * (DM + 1);
   __shared__ int Is[32][4];
   __shared__ float Ws[32];
-  const int tpc = (g.c + 63) / 64;
+  const int tpc = (g.c + TOK - 1) / TOK;
   const int kch = blockIdx.x / tpc, tile = blockIdx.x - kch * tpc, s = blockIdx.y;
   const int s0 = kch * g.c, s1 = min(s0 + g.c, g.t);
-  const int q0 = s0 + tile * 64;
+  const int q0 = s0 + tile * TOK;
   if (q0 >= s1) return;
   const int i = q0 + threadIdx.x;
   const bool act = i < s1;
@@ -365,7 +369,7 @@ __global__ void __launch_bounds__(64) k_query_combine(Geo g, const T* __restrict
     const float* Ak = A + ((size_t)s * g.n + (kch - 1)) * g.D * g.E1;
     for (int f0 = 0; f0 < g.D; f0 += 32) {
       __syncthreads();
-      for (int el = threadIdx.x; el < 32 * AS; el += 64) {
+      for (int el = threadIdx.x; el < 32 * AS; el += TOK) {
         int r = el / AS, u = el - r * AS;
         As[r][u] = (f0 + r < g.D && u < g.E1) ? Ak[(size_t)(f0 + r) * g.E1 + u] : 0.f;
       }
@@ -974,7 +978,7 @@ __global__ void k_pub_discumsum(int n, int64_t L, int64_t M, const A* __restrict
 
 // dynamic shared memory per block for the kernels above (floats -> bytes)
 template <int DM> constexpr size_t smb_intra_fwd() { return 4 * (2 * 64 * (DM + 1)); }
-template <int DM> constexpr size_t smb_query_combine() { return 4 * (64 * (DM + 1) + 32 * state_row_stride<DM>()); }
+template <int DM> constexpr size_t smb_query_combine() { return 4 * (qc_tokens<DM>() * (DM + 1) + 32 * state_row_stride<DM>()); }
 template <int DM> constexpr size_t smb_query_bwd() { return 4 * (2 * ub_tokens<DM>() * (DM + 1) + 32 * state_row_stride<DM>()); }
 template <int DM> constexpr size_t smb_update_bwd() { return 4 * (2 * ub_tokens<DM>() * (DM + 1) + 32 * state_row_stride<DM>()); }
 template <int DM> constexpr size_t smb_intra_bwd() { return 4 * (3 * 64 * (DM + 1) + 64 * (DM + 2)); }
@@ -1006,7 +1010,8 @@ static int simt_forward_t(const Geo& g, const T* q, const T* k, const T* v, cons
     k_state_accum<T, T, DM><<<dim3((g.D + 31) / 32, g.n, g.ns), 256, 0, st>>>(
         g, k, 1.f, g.gated ? 1 : 0, w.ell, w.lamlog, v, 1, g.e, g.e, 1, w.idx, w.wt, 0, 0, w.A);
   if (g.n > 1) k_discumsum_states<<<dim3((unsigned)std::min<size_t>(((size_t)g.D * g.E1 + 255) / 256, 512), g.ns), 256, 0, st>>>(g, w.lamlog, w.A);
-  k_query_combine<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_query_combine<T, DM>, smb_query_combine<DM>()), st>>>(g, q, w.A, w.idx, w.wt, w.ell, w.yat, y, rowsum, w.zflag, w.y32);
+  k_query_combine<T, DM><<<dim3(g.n * ((g.c + qc_tokens<DM>() - 1) / qc_tokens<DM>()), g.ns), qc_tokens<DM>(),
+                           dyn_smem(k_query_combine<T, DM>, smb_query_combine<DM>()), st>>>(g, q, w.A, w.idx, w.wt, w.ell, w.yat, y, rowsum, w.zflag, w.y32);
   count_launch(g.n > 1 ? 5 : 4);
   return cuda_check("simt forward");
 }
