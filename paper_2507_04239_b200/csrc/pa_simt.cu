@@ -295,13 +295,14 @@ __global__ void __launch_bounds__(kSaThreads) k_state_accum_f(Geo g, const TX* _
       const float ph = phi_at(Xs[jj], id, w, g.p);
       const float4* ur = reinterpret_cast<const float4*>(Us[jj]);
 #pragma unroll
-      for (int q4 = 0; q4 < US / 4; ++q4) {
+      for (int q4 = 0; q4 < DM / 4; ++q4) {  // columns 0..DM-1, then column DM alone
         const float4 u4 = ur[q4];
         acc[4 * q4 + 0] += ph * u4.x;
         acc[4 * q4 + 1] += ph * u4.y;
         acc[4 * q4 + 2] += ph * u4.z;
         acc[4 * q4 + 3] += ph * u4.w;
       }
+      acc[DM] += ph * Us[jj][DM];
     }
   }
   if (f >= g.D) return;
@@ -384,7 +385,7 @@ __global__ void __launch_bounds__(qc_tokens<DM>()) k_query_combine(Geo g, const 
         const float ph = phi_at(Qs[threadIdx.x], Is[fl], Ws[fl], g.p);
         const float4* ar = reinterpret_cast<const float4*>(As[fl]);
 #pragma unroll
-        for (int q4 = 0; q4 < AS / 4; ++q4) {
+        for (int q4 = 0; q4 < DM / 4; ++q4) {  // y columns are < e <= DM
           const float4 a4 = ar[q4];
           acc[4 * q4] += ph * a4.x;
           acc[4 * q4 + 1] += ph * a4.y;
@@ -557,12 +558,12 @@ __global__ void __launch_bounds__(ub_tokens<DM>()) k_query_bwd(Geo g, const T* _
       const float4* ar = reinterpret_cast<const float4*>(As[fl]);
       float tf = 0.f, tf2 = 0.f;
 #pragma unroll
-      for (int q4 = 0; q4 < AS / 4; ++q4) {
+      for (int q4 = 0; q4 < DM / 4; ++q4) {
         const float4 a4 = ar[q4];
         tf += a4.x * dzr[4 * q4] + a4.z * dzr[4 * q4 + 2];
         tf2 += a4.y * dzr[4 * q4 + 1] + a4.w * dzr[4 * q4 + 3];
       }
-      tf += tf2;
+      tf += tf2 + As[fl][DM] * dzr[DM];  // column DM: the score column when e = DM, else 0
       const PhiParts pp = phi_parts(Qs[threadIdx.x], Is[fl], Ws[fl], g.p);
       dl += pp.ph * tf;
       phi_parts_vjp_add(Dq[threadIdx.x], Is[fl], pp, Ws[fl] * gp * tf, g.p);
@@ -670,7 +671,7 @@ __global__ void __launch_bounds__(ub_tokens<DM>()) k_update_bwd(Geo g, const T* 
       const float4* sr = reinterpret_cast<const float4*>(Ss[fl]);
       float tf = 0.f, tf2 = 0.f;
 #pragma unroll
-      for (int q4 = 0; q4 < AS / 4; ++q4) {
+      for (int q4 = 0; q4 < DM / 4; ++q4) {  // dv columns are < e <= DM
         const float4 s4 = sr[q4];
         tf += s4.x * vr[4 * q4] + s4.z * vr[4 * q4 + 2];
         tf2 += s4.y * vr[4 * q4 + 1] + s4.w * vr[4 * q4 + 3];
@@ -679,7 +680,7 @@ __global__ void __launch_bounds__(ub_tokens<DM>()) k_update_bwd(Geo g, const T* 
         dvr[4 * q4 + 2] += wp * s4.z;
         dvr[4 * q4 + 3] += wp * s4.w;
       }
-      tf += tf2;
+      tf += tf2 + Ss[fl][DM] * vr[DM];  // column DM: the score column when e = DM, else 0
       dW += pp.ph * tf;
       phi_parts_vjp_add(Dk[threadIdx.x], Is[fl], pp, Ws[fl] * W * tf, g.p);
     }
