@@ -79,3 +79,19 @@ def test_cpu_inputs_fail_loudly():
     q = torch.zeros(1, 4, 1, 2)
     with pytest.raises(P.InvalidSpec):
         P.power_full(q, q, q)
+
+
+def test_logspace_entry_validates_before_launch():
+    """pa_power_logspace_fwd (attention.py:289-305) rejects bad problems with
+    the reference's error classes before touching the device."""
+    lib = _lib.load()
+    dummy = ctypes.c_void_p(16)  # never dereferenced: validation fails first
+    args = [dummy] * 6 + [None]
+    rc = lib.pa_power_logspace_fwd(ctypes.byref(_problem(p=3)), 1e-12, *args)
+    assert rc == 1 and b"even p" in lib.pa_last_error()          # InvalidSpec
+    rc = lib.pa_power_logspace_fwd(ctypes.byref(_problem()), 0.0, *args)
+    assert rc == 1 and b"epsilon" in lib.pa_last_error()
+    rc = lib.pa_power_logspace_fwd(ctypes.byref(_problem()), 1e-12, None, *args[1:])
+    assert rc == 2                                               # ShapeMismatch
+    rc = lib.pa_power_logspace_fwd(ctypes.byref(_problem(dtype=1)), 1e-12, *args)
+    assert rc == 4 and b"f32 or f64" in lib.pa_last_error()      # bf16 unsupported here
