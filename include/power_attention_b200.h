@@ -44,17 +44,42 @@ enum pa_status {
   PA_ERR_ODD_NORMALIZE = 6   /* -> errors.OddPowerWithNormalize (errors.py:24) */
 };
 
+/* Behaviour flags (pa_problem.flags). */
+enum pa_flags {
+  /* Fixed accumulation order: every tensor-core accumulator is fed by one MMA
+   * issuer in a fixed order, so repeated calls are bit-identical (slower). */
+  PA_FLAG_DETERMINISTIC = 1,
+  /* Refuse (PA_ERR_UNSUPPORTED) instead of running a 16-bit problem on the fp32
+   * CUDA-core kernels when the tensor-core kernels do not cover its shape. */
+  PA_FLAG_STRICT_TC = 2
+};
+
 /* One power_full problem (reference AttentionConfig attention.py:106-171 +
  * ChunkPlan chunked.py:66-86). */
 typedef struct pa_problem {
   int32_t b, t, h, d, e; /* batch, tokens, heads, q/k width, value width      */
   int32_t p;             /* degree of the SPOW_p expansion (1..4)             */
   int32_t chunk;         /* chunk size c; c >= t selects the attention form   */
-  float scale;           /* sigma; <= 0 means 1/sqrt(d) (attention.py:149)    */
   int32_t normalize;     /* 1: divide by the score sum (even p only)          */
   int32_t dtype;         /* pa_dtype of q, k, v, y, dy, dq, dk, dv            */
   int32_t gated;         /* 1: log_g is read; 0: ungated (log_g ignored)      */
+  int32_t has_scale;     /* 1: use `scale` exactly (any sign); 0: 1/sqrt(d)   */
+  int32_t flags;         /* pa_flags                                          */
+  double scale;          /* sigma (attention.py:149-150), when has_scale      */
 } pa_problem;
+
+/* 1 when the problem runs on the tcgen05 tensor-core kernels, 0 when it runs
+ * on the fp32 CUDA-core kernels, negative PA_ERR_* when it is invalid. */
+int pa_uses_tensor_cores(const pa_problem* pr);
+
+/* Expansion kinds (reference expansions.py:41-44). */
+enum pa_expansion { PA_SPOW = 0, PA_TPOW = 1, PA_TSPOW = 2 };
+/* D of an expansion (d_tile only for TSPOW, must divide d); -1 if invalid.
+ * Reference expansion_dim expansions.py:87-99. */
+int64_t pa_expansion_dim(int32_t kind, int32_t p, int32_t d, int32_t d_tile);
+/* Host buffers idx [D*p] int32, w [D] double: the reference monomial_table
+ * (expansions.py:171-198) for SPOW, TPOW or TSPOW, same row order. */
+int pa_expansion_table(int32_t kind, int32_t p, int32_t d, int32_t d_tile, int32_t* idx, double* w);
 
 /* D = C(d+p-1, p); -1 on overflow. */
 int64_t pa_feature_dim(int32_t p, int32_t d);
@@ -144,6 +169,17 @@ int pa_update_state(int32_t n, int32_t c, int32_t d, int32_t e, int32_t p, int32
 int pa_query_state(int32_t n, int32_t c, int32_t d, int32_t e, int32_t p, int32_t dtype,
                    const void* q, const void* state, const void* key_sum, void* y, void* denom,
                    int32_t accumulate, pa_stream_t stream);
+
+/* The same two operators with the caller's monomial table (the reference
+ * _core ABI passes idx and weights too, _core.pyx:18-20, 46-48), so any
+ * expansion kind runs: idx [D*p] int32 and weights [D] f64 in DEVICE memory
+ * (pa_expansion_table fills host buffers).  p <= 4. */
+int pa_update_state_table(int32_t n, int32_t c, int32_t d, int32_t e, int32_t p, int64_t D, int32_t dtype,
+                          const void* k, const void* v, const void* w, const int32_t* idx, const double* weights,
+                          void* state, void* key_sum, int32_t accumulate, pa_stream_t stream);
+int pa_query_state_table(int32_t n, int32_t c, int32_t d, int32_t e, int32_t p, int64_t D, int32_t dtype,
+                         const void* q, const void* state, const void* key_sum, const int32_t* idx,
+                         const double* weights, void* y, void* denom, int32_t accumulate, pa_stream_t stream);
 
 /* Reference discumsum: out[0] = values[0]; out[k] = lams[k-1, l] * out[k-1, l, m]
  * + values[k, l, m] with a separate multiply and add (bit-exact with the

@@ -17,6 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PA_B200_LIB") or os.path.join(HERE, "libpa_b200.so")
 
 PA_F32, PA_BF16, PA_F16, PA_F64 = 0, 1, 2, 3
+PA_FLAG_DETERMINISTIC, PA_FLAG_STRICT_TC = 1, 2
 
 _ERRORS = {
     1: InvalidSpec,
@@ -43,10 +44,12 @@ class PaProblem(ctypes.Structure):
         ("e", ctypes.c_int32),
         ("p", ctypes.c_int32),
         ("chunk", ctypes.c_int32),
-        ("scale", ctypes.c_float),
         ("normalize", ctypes.c_int32),
         ("dtype", ctypes.c_int32),
         ("gated", ctypes.c_int32),
+        ("has_scale", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
+        ("scale", ctypes.c_double),
     ]
 
 
@@ -62,6 +65,13 @@ _PP = ctypes.POINTER(PaProblem)
 _SIGS = {
     "pa_feature_dim": (_I64, [_I32, _I32]),
     "pa_feature_table": (ctypes.c_int, [_I32, _I32, _VP, _VP]),
+    "pa_uses_tensor_cores": (ctypes.c_int, [_PP]),
+    "pa_expansion_dim": (_I64, [_I32, _I32, _I32, _I32]),
+    "pa_expansion_table": (ctypes.c_int, [_I32, _I32, _I32, _I32, _VP, _VP]),
+    "pa_update_state_table": (ctypes.c_int, [_I32, _I32, _I32, _I32, _I32, _I64, _I32, _VP, _VP, _VP, _VP, _VP,
+                                              _VP, _VP, _I32, _VP]),
+    "pa_query_state_table": (ctypes.c_int, [_I32, _I32, _I32, _I32, _I32, _I64, _I32, _VP, _VP, _VP, _VP, _VP,
+                                             _VP, _VP, _I32, _VP]),
     "pa_fwd_workspace_bytes": (_SZ, [_PP]),
     "pa_bwd_workspace_bytes": (_SZ, [_PP]),
     "pa_power_full_fwd": (ctypes.c_int, [_PP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _SZ, _VP]),

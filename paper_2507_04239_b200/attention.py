@@ -124,7 +124,9 @@ def run_power(batch: SequenceBatch, cfg: AttentionConfig, chunk: int | None) -> 
 
     if cfg.mechanism is not Mechanism.POWER:
         raise InvalidSpec(f"only the power mechanism runs on the CUDA path, got {cfg.mechanism.value}")
-    spec = cfg.expansion.require_spow()
+    # every expansion kind gives <phi(x), phi(y)> = (x . y)^p (expansions.py:3-5):
+    # the output does not depend on the kind
+    spec = cfg.expansion
     if spec.d != batch.d:
         raise ShapeMismatch(f"spec.d={spec.d} but q has d={batch.d}")
     host = batch.on_host
@@ -134,7 +136,7 @@ def run_power(batch: SequenceBatch, cfg: AttentionConfig, chunk: int | None) -> 
     q, k, v = (to_dev(x, tdt) for x in (batch.q, batch.k, batch.v))
     lg = None if batch.gates is None else torch.log(to_dev(batch.gates, torch.float32))
     y, rs = power_full_with_rowsum(q, k, v, lg, p=spec.p, chunk_size=chunk, scale=cfg.scale,
-                                   normalize=cfg.normalize)
+                                   normalize=cfg.normalize, check_denominator="sync")
     if not host and src_dt == torch.float64:
         y = y.to(torch.float64)
     return AttentionOutput(back(y, host, np_dt), back(rs, host, np_dt))
@@ -155,7 +157,9 @@ def run_log_space(batch: SequenceBatch, cfg: AttentionConfig) -> AttentionOutput
 
     if cfg.mechanism is not Mechanism.POWER:
         raise InvalidSpec(f"only the power mechanism runs on the CUDA path, got {cfg.mechanism.value}")
-    spec = cfg.expansion.require_spow()
+    # every expansion kind gives <phi(x), phi(y)> = (x . y)^p (expansions.py:3-5):
+    # the output does not depend on the kind
+    spec = cfg.expansion
     if spec.d != batch.d:
         raise ShapeMismatch(f"spec.d={spec.d} but q has d={batch.d}")
     host = batch.on_host

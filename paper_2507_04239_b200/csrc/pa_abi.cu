@@ -9,6 +9,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/power_attention_b200.h"
@@ -132,7 +133,8 @@ static int make_geo(const pa_problem* pr, Geo* g) {
   }
   g->D = (int)D;
   g->ns = pr->b * pr->h;
-  g->scale = pr->scale > 0.f ? pr->scale : 1.0f / sqrtf((float)pr->d);
+  g->scale = pr->has_scale ? (float)pr->scale : 1.0f / sqrtf((float)pr->d);
+  g->det = (pr->flags & PA_FLAG_DETERMINISTIC) ? 1 : 0;
   g->normalize = pr->normalize ? 1 : 0;
   g->gated = pr->gated ? 1 : 0;
   g->bth = 1;
@@ -140,6 +142,19 @@ static int make_geo(const pa_problem* pr, Geo* g) {
   g->ng = g->n;
   g->prefix = 0;
   g->nsl = g->n + 1;
+  return PA_OK;
+}
+
+// Which kernel family runs the problem; with PA_FLAG_STRICT_TC a 16-bit
+// problem the tensor-core kernels do not cover is an error, not a silent
+// switch to the fp32 CUDA-core kernels.
+static int route(const pa_problem* pr, const Geo& g, bool* tc) {
+  *tc = tc_supported(g, pr->dtype);
+  if (!*tc && (pr->flags & PA_FLAG_STRICT_TC) && pr->dtype != PA_F32) {
+    set_error("strict tensor-core mode: the tcgen05 kernels cover bf16, p = 2, d = e = 64, chunk a multiple of "
+              "128 up to 1024 and t a multiple of the chunk");
+    return PA_ERR_UNSUPPORTED;
+  }
   return PA_OK;
 }
 
@@ -212,10 +227,20 @@ int pa_feature_table(int32_t p, int32_t d, int32_t* idx, double* w) {
   return PA_OK;
 }
 
+int pa_uses_tensor_cores(const pa_problem* pr) {
+  Geo g;
+  if (int rc = make_geo(pr, &g)) return -rc;
+  bool tc;
+  if (int rc = route(pr, g, &tc)) return -rc;
+  return tc ? 1 : 0;
+}
+
 size_t pa_fwd_workspace_bytes(const pa_problem* pr) {
   Geo g;
   if (make_geo(pr, &g)) return 0;
-  if (tc_supported(g, pr->dtype)) return tc_fwd_workspace_bytes(g);
+  bool tc;
+  if (route(pr, g, &tc)) return 0;
+  if (tc) return tc_fwd_workspace_bytes(g);
   size_t n;
   carve_simt_fwd(g, nullptr, &n);
   return n;
@@ -224,7 +249,9 @@ size_t pa_fwd_workspace_bytes(const pa_problem* pr) {
 size_t pa_bwd_workspace_bytes(const pa_problem* pr) {
   Geo g;
   if (make_geo(pr, &g)) return 0;
-  if (tc_supported(g, pr->dtype)) return tc_bwd_workspace_bytes(g);
+  bool tc;
+  if (route(pr, g, &tc)) return 0;
+  if (tc) return tc_bwd_workspace_bytes(g);
   size_t n;
   carve_simt_bwd(g, nullptr, &n);
   return n;
@@ -240,7 +267,9 @@ int pa_power_full_fwd(const pa_problem* pr, const void* q, const void* k, const 
     return PA_ERR_INVALID_SPEC;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  if (tc_supported(g, pr->dtype)) {
+  bool tc;
+  if (int rc = route(pr, g, &tc)) return rc;
+  if (tc) {
     if (ws_bytes < tc_fwd_workspace_bytes(g)) {
       set_error("forward workspace too small");
       return PA_ERR_WORKSPACE;
@@ -271,7 +300,9 @@ int pa_power_full_bwd(const pa_problem* pr, const void* q, const void* k, const 
   }
   if (!g.gated) dlog_g = nullptr;
   cudaStream_t st = (cudaStream_t)stream;
-  if (tc_supported(g, pr->dtype)) {
+  bool tc;
+  if (int rc = route(pr, g, &tc)) return rc;
+  if (tc) {
     if (bwd_ws_bytes < tc_bwd_workspace_bytes(g)) {
       set_error("backward workspace too small");
       return PA_ERR_WORKSPACE;
@@ -417,51 +448,49 @@ static int check_op(int n, int c, int d, int e, int p, int dtype) {
   return PA_OK;
 }
 
-// The per-operator entry points keep a tiny cached table per (p, d) on the
-// device: they are reference-compatibility shims, not the hot path.
-static int op_table(int p, int d, int** idx, float** wt, cudaStream_t st) {
+// The SPOW per-operator entry points keep one device copy of the monomial
+// table per (p, d, device), built on the host and copied synchronously before
+// it is published, so no stream can read a half-built table.  They are
+// reference-compatibility shims, not the hot path.
+static int op_table(int p, int d, const int** idx, const double** wt) {
   struct Ent {
-    int p, d, dev;
     int* idx;
-    float* wt;
+    double* wt;
   };
-  static Ent cache[16];
-  static int used = 0;
-  static std::atomic_flag lock = ATOMIC_FLAG_INIT;
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int>, Ent> cache;
   int dev = 0;
-  cudaGetDevice(&dev);
-  while (lock.test_and_set()) {
-  }
-  for (int i = 0; i < used; ++i)
-    if (cache[i].p == p && cache[i].d == d && cache[i].dev == dev) {
-      *idx = cache[i].idx;
-      *wt = cache[i].wt;
-      lock.clear();
-      return PA_OK;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cuda_check("cudaGetDevice");
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find({p, d, dev});
+  if (it == cache.end()) {
+    const int64_t D = host_binom(d + p - 1, p);
+    std::vector<int> hi((size_t)D * p);
+    std::vector<double> hw((size_t)D);
+    host_feature_table(p, d, hi.data(), hw.data());
+    Ent e{nullptr, nullptr};
+    if (cudaMalloc(&e.idx, sizeof(int) * hi.size()) != cudaSuccess ||
+        cudaMalloc(&e.wt, sizeof(double) * hw.size()) != cudaSuccess ||
+        cudaMemcpy(e.idx, hi.data(), sizeof(int) * hi.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(e.wt, hw.data(), sizeof(double) * hw.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaFree(e.idx);
+      cudaFree(e.wt);
+      return cuda_check("feature table upload");
     }
-  int D = (int)host_binom(d + p - 1, p);
-  int* di = nullptr;
-  float* dw = nullptr;
-  if (cudaMalloc(&di, sizeof(int) * D * p) != cudaSuccess || cudaMalloc(&dw, sizeof(float) * D) != cudaSuccess) {
-    lock.clear();
-    set_error("cudaMalloc for the feature table failed");
-    return PA_ERR_CUDA;
+    it = cache.emplace(std::make_tuple(p, d, dev), e).first;
   }
-  int rc = simt_build_table(p, d, D, di, dw, st);
-  if (rc == PA_OK && used < 16) cache[used++] = Ent{p, d, dev, di, dw};
-  lock.clear();
-  *idx = di;
-  *wt = dw;
-  return rc;
+  *idx = it->second.idx;
+  *wt = it->second.wt;
+  return PA_OK;
 }
 
 int pa_update_state(int32_t n, int32_t c, int32_t d, int32_t e, int32_t p, int32_t dtype,
                     const void* k, const void* v, const void* w, void* state, void* key_sum,
                     int32_t accumulate, pa_stream_t stream) {
   if (int rc = check_op(n, c, d, e, p, dtype)) return rc;
-  int* idx;
-  float* wt;
-  if (int rc = op_table(p, d, &idx, &wt, (cudaStream_t)stream)) return rc;
+  const int* idx;
+  const double* wt;
+  if (int rc = op_table(p, d, &idx, &wt)) return rc;
   int D = (int)host_binom(d + p - 1, p);
   return pub_update(n, c, d, e, p, D, dtype, k, v, w, idx, wt, state, key_sum, accumulate, (cudaStream_t)stream);
 }
@@ -470,11 +499,52 @@ int pa_query_state(int32_t n, int32_t c, int32_t d, int32_t e, int32_t p, int32_
                    const void* q, const void* state, const void* key_sum, void* y, void* denom,
                    int32_t accumulate, pa_stream_t stream) {
   if (int rc = check_op(n, c, d, e, p, dtype)) return rc;
-  int* idx;
-  float* wt;
-  if (int rc = op_table(p, d, &idx, &wt, (cudaStream_t)stream)) return rc;
+  const int* idx;
+  const double* wt;
+  if (int rc = op_table(p, d, &idx, &wt)) return rc;
   int D = (int)host_binom(d + p - 1, p);
-  return pub_query(n, c, d, e, p, D, dtype, q, state, key_sum, idx, y, denom, accumulate, (cudaStream_t)stream);
+  return pub_query(n, c, d, e, p, D, dtype, q, state, key_sum, idx, wt, y, denom, accumulate, (cudaStream_t)stream);
+}
+
+int64_t pa_expansion_dim(int32_t kind, int32_t p, int32_t d, int32_t d_tile) {
+  if (p < 1 || d < 1 || kind < 0 || kind > 2) return -1;
+  if (kind == PA_TSPOW && (d_tile < 1 || d % d_tile)) return -1;
+  return host_expansion_dim(kind, p, d, d_tile);
+}
+
+int pa_expansion_table(int32_t kind, int32_t p, int32_t d, int32_t d_tile, int32_t* idx, double* w) {
+  if (pa_expansion_dim(kind, p, d, d_tile) < 0 || p > 4 || !idx || !w) {
+    set_error("expansion table needs kind in {spow, tpow, tspow}, 1 <= p <= 4, d >= 1, d_tile | d");
+    return PA_ERR_INVALID_SPEC;
+  }
+  host_expansion_table(kind, p, d, d_tile, idx, w);
+  return PA_OK;
+}
+
+static int check_table_op(int n, int c, int d, int e, int p, int64_t D, int dtype, const void* idx,
+                          const void* wt) {
+  if (int rc = check_op(n, c, d, e, p, dtype)) return rc;
+  if (D < 1 || D > ((int64_t)1 << 30) || !idx || !wt) {
+    set_error("monomial table: need 1 <= D <= 2^30 and device idx / weights");
+    return PA_ERR_INVALID_SPEC;
+  }
+  return PA_OK;
+}
+
+int pa_update_state_table(int32_t n, int32_t c, int32_t d, int32_t e, int32_t p, int64_t D, int32_t dtype,
+                          const void* k, const void* v, const void* w, const int32_t* idx, const double* weights,
+                          void* state, void* key_sum, int32_t accumulate, pa_stream_t stream) {
+  if (int rc = check_table_op(n, c, d, e, p, D, dtype, idx, weights)) return rc;
+  return pub_update(n, c, d, e, p, (int)D, dtype, k, v, w, idx, weights, state, key_sum, accumulate,
+                    (cudaStream_t)stream);
+}
+
+int pa_query_state_table(int32_t n, int32_t c, int32_t d, int32_t e, int32_t p, int64_t D, int32_t dtype,
+                         const void* q, const void* state, const void* key_sum, const int32_t* idx,
+                         const double* weights, void* y, void* denom, int32_t accumulate, pa_stream_t stream) {
+  if (int rc = check_table_op(n, c, d, e, p, D, dtype, idx, weights)) return rc;
+  return pub_query(n, c, d, e, p, (int)D, dtype, q, state, key_sum, idx, weights, y, denom, accumulate,
+                   (cudaStream_t)stream);
 }
 
 int pa_discumsum(int32_t n, int64_t L, int64_t M, int32_t dtype, const void* values,

@@ -23,6 +23,8 @@ struct Geo {
   // flows in from earlier chunks.  Chunk-state buffers hold nsl = n + 1 slots
   // per stream: slot j is the state before local chunk j (slot 0 = prefix).
   int k0, ng, prefix, nsl;
+  // PA_FLAG_DETERMINISTIC: one MMA issuer per accumulator (fixed summation order)
+  int det;
 };
 
 __host__ __device__ __forceinline__ size_t rowid(const Geo& g, int s, int m) {

@@ -178,7 +178,7 @@ int launch(const pa_problem* pr, double eps, const void* q, const void* k, const
   auto kern = k_logspace_attention<T>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return cuda_check("log-space attention smem attribute");
-  const T scale = pr->scale > 0 ? T(pr->scale) : T(1.0 / std::sqrt((double)pr->d));
+  const T scale = pr->has_scale ? T(pr->scale) : T(1.0 / std::sqrt((double)pr->d));
   dim3 grid((t + kRowsPerCta - 1) / kRowsPerCta, pr->b * pr->h);
   StageTimer tm("fwd_logspace_attention", st);
   kern<<<grid, kThreads, smem, st>>>(t, pr->h, pr->d, pr->e, pr->p, scale, T(eps), pr->normalize,

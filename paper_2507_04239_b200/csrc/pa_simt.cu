@@ -63,6 +63,59 @@ __global__ void k_build_table(int p, int d, int D, int* idx, float* wt) {
   wt[f] = w;
 }
 
+// TPOW: every ordered tuple, first index slowest, weight 1; TSPOW: one dense
+// d_tile^p block per NDMI over tiles, the tile NDMI's weight on the whole block
+// (reference expansions.py:171-198).
+int64_t host_expansion_dim(int kind, int p, int d, int d_tile) {
+  if (kind == 1) {
+    int64_t r = 1;
+    for (int z = 0; z < p; ++z) r *= d;
+    return r;
+  }
+  if (kind == 2) {
+    int64_t r = binom(d / d_tile + p - 1, p);
+    for (int z = 0; z < p; ++z) r *= d_tile;
+    return r;
+  }
+  return binom(d + p - 1, p);
+}
+
+void host_expansion_table(int kind, int p, int d, int d_tile, int* idx, double* w) {
+  if (kind == 0) {
+    host_feature_table(p, d, idx, w);
+    return;
+  }
+  if (kind == 1) {
+    const int64_t D = host_expansion_dim(1, p, d, 0);
+    for (int64_t f = 0; f < D; ++f) {
+      int64_t r = f;
+      for (int z = p - 1; z >= 0; --z) {
+        idx[f * p + z] = (int)(r % d);
+        r /= d;
+      }
+      w[f] = 1.0;
+    }
+    return;
+  }
+  const int nt = d / d_tile;
+  const int64_t T = binom(nt + p - 1, p), B = host_expansion_dim(1, p, d_tile, 0);
+  int* tidx = new int[T * p];
+  double* tw = new double[T];
+  host_feature_table(p, nt, tidx, tw);
+  for (int64_t ti = 0; ti < T; ++ti)
+    for (int64_t o = 0; o < B; ++o) {
+      const int64_t f = ti * B + o;
+      int64_t r = o;
+      for (int z = p - 1; z >= 0; --z) {
+        idx[f * p + z] = tidx[ti * p + z] * d_tile + (int)(r % d_tile);
+        r /= d_tile;
+      }
+      w[f] = tw[ti];
+    }
+  delete[] tidx;
+  delete[] tw;
+}
+
 void host_feature_table(int p, int d, int* idx, double* w) {
   int64_t D = binom(d + p - 1, p);
   for (int64_t f = 0; f < D; ++f) {
@@ -889,24 +942,18 @@ __global__ void k_finalize(Geo g, const float* __restrict__ src, int w, T* dst) 
 template <typename A>
 __global__ void k_pub_update(int n, int c, int d, int e, int p, int D, const A* __restrict__ k,
                              const A* __restrict__ v, const A* __restrict__ w,
-                             const int* __restrict__ idx, const float* __restrict__ wt, A* state,
+                             const int* __restrict__ idx, const double* __restrict__ wt, A* state,
                              A* key_sum, int accumulate) {
+  // one thread per (stream, feature, column): the reference's _core.update_state
+  // loop nest (_core.pyx:18-43) with the caller's monomial table (idx, weights)
   const size_t tot = (size_t)n * D * (e + 1);
   for (size_t it = blockIdx.x * (size_t)blockDim.x + threadIdx.x; it < tot; it += (size_t)gridDim.x * blockDim.x) {
     const int u = (int)(it % (e + 1));
     const size_t sf = it / (e + 1);
     const int f = (int)(sf % D), s = (int)(sf / D);
     int id[4] = {0, 0, 0, 0};
-    for (int z = 0; z < p; ++z) id[z] = idx[f * p + z];
-    // exact double weight (table is float): recompute from the run lengths
-    double fact = 1, den = 1;
-    int run = 1;
-    for (int z = 1; z <= p; ++z) fact *= z;
-    for (int z = 1; z < p; ++z) {
-      run = (id[z] == id[z - 1]) ? run + 1 : 1;
-      den *= run;
-    }
-    const A wf = (A)sqrt(fact / den);
+    for (int z = 0; z < p; ++z) id[z] = idx[(size_t)f * p + z];
+    const A wf = (A)wt[f];
     A acc = 0;
     for (int j = 0; j < c; ++j) {
       const A* kr = k + ((size_t)s * c + j) * d;
@@ -923,7 +970,9 @@ __global__ void k_pub_update(int n, int c, int d, int e, int p, int D, const A* 
 template <typename A>
 __global__ void k_pub_query(int n, int c, int d, int e, int p, int D, const A* __restrict__ q,
                             const A* __restrict__ state, const A* __restrict__ key_sum,
-                            const int* __restrict__ idx, A* y, A* denom, int accumulate) {
+                            const int* __restrict__ idx, const double* __restrict__ wt, A* y, A* denom,
+                            int accumulate) {
+  // one thread per (stream, token, column): _core.query_state (_core.pyx:46-64)
   const size_t tot = (size_t)n * c * (e + 1);
   for (size_t it = blockIdx.x * (size_t)blockDim.x + threadIdx.x; it < tot; it += (size_t)gridDim.x * blockDim.x) {
     const int u = (int)(it % (e + 1));
@@ -932,17 +981,8 @@ __global__ void k_pub_query(int n, int c, int d, int e, int p, int D, const A* _
     const A* qr = q + ((size_t)s * c + m) * d;
     A acc = 0;
     for (int f = 0; f < D; ++f) {
-      int id[4] = {0, 0, 0, 0};
-      for (int z = 0; z < p; ++z) id[z] = idx[f * p + z];
-      double fact = 1, den = 1;
-      int run = 1;
-      for (int z = 1; z <= p; ++z) fact *= z;
-      for (int z = 1; z < p; ++z) {
-        run = (id[z] == id[z - 1]) ? run + 1 : 1;
-        den *= run;
-      }
-      A ph = (A)sqrt(fact / den) * qr[id[0]];
-      for (int z = 1; z < p; ++z) ph *= qr[id[z]];
+      A ph = (A)wt[f] * qr[idx[(size_t)f * p]];
+      for (int z = 1; z < p; ++z) ph *= qr[idx[(size_t)f * p + z]];
       acc += ph * ((u < e) ? state[((size_t)s * D + f) * e + u] : key_sum[(size_t)s * D + f]);
     }
     A* o = (u < e) ? y + ((size_t)s * c + m) * e + u : denom + (size_t)s * c + m;
@@ -1113,7 +1153,7 @@ int simt_backward(const Geo& g, int dtype, const void* q, const void* k, const v
 }
 
 int pub_update(int n, int c, int d, int e, int p, int D, int dtype, const void* k, const void* v,
-               const void* w, const int* idx, const float* wt, void* state, void* ks, int acc,
+               const void* w, const int* idx, const double* wt, void* state, void* ks, int acc,
                cudaStream_t st) {
   const size_t tot = (size_t)n * D * (e + 1);
   if (dtype == 3)
@@ -1127,14 +1167,14 @@ int pub_update(int n, int c, int d, int e, int p, int D, int dtype, const void* 
 }
 
 int pub_query(int n, int c, int d, int e, int p, int D, int dtype, const void* q, const void* state,
-              const void* ks, const int* idx, void* y, void* den, int acc, cudaStream_t st) {
+              const void* ks, const int* idx, const double* wt, void* y, void* den, int acc, cudaStream_t st) {
   const size_t tot = (size_t)n * c * (e + 1);
   if (dtype == 3)
     k_pub_query<double><<<nblk(tot, 128), 128, 0, st>>>(n, c, d, e, p, D, (const double*)q, (const double*)state,
-                                                        (const double*)ks, idx, (double*)y, (double*)den, acc);
+                                                        (const double*)ks, idx, wt, (double*)y, (double*)den, acc);
   else
     k_pub_query<float><<<nblk(tot, 128), 128, 0, st>>>(n, c, d, e, p, D, (const float*)q, (const float*)state,
-                                                       (const float*)ks, idx, (float*)y, (float*)den, acc);
+                                                       (const float*)ks, idx, wt, (float*)y, (float*)den, acc);
   count_launch();
   return cuda_check("query_state");
 }

@@ -32,6 +32,9 @@ size_t simt_bwd_bytes(const Geo& g);
 SimtWs simt_carve_fwd(const Geo& g, void* ws);
 SimtBwdWs simt_carve_bwd(const Geo& g, void* ws);
 void host_feature_table(int p, int d, int* idx, double* w);
+// kind 0 = SPOW, 1 = TPOW, 2 = TSPOW (tile edge d_tile)
+int64_t host_expansion_dim(int kind, int p, int d, int d_tile);
+void host_expansion_table(int kind, int p, int d, int d_tile, int* idx, double* w);
 int simt_build_table(int p, int d, int D, int* idx, float* wt, cudaStream_t st);
 int simt_forward(const Geo& g, int dtype, const void* q, const void* k, const void* v, const float* lg,
                  void* y, float* rs, const SimtWs& w, cudaStream_t st);
@@ -45,10 +48,10 @@ int simt_gate_finish(const Geo& g, const float* lamlog, const float* dell, const
                      const float* dlam, float* dlogg, cudaStream_t st);
 int simt_finalize_bf16(const Geo& g, const float* src, int w, void* dst, cudaStream_t st);
 int pub_update(int n, int c, int d, int e, int p, int D, int dtype, const void* k, const void* v,
-               const void* w, const int* idx, const float* wt, void* state, void* ks, int acc,
+               const void* w, const int* idx, const double* wt, void* state, void* ks, int acc,
                cudaStream_t st);
 int pub_query(int n, int c, int d, int e, int p, int D, int dtype, const void* q, const void* state,
-              const void* ks, const int* idx, void* y, void* den, int acc, cudaStream_t st);
+              const void* ks, const int* idx, const double* wt, void* y, void* den, int acc, cudaStream_t st);
 int pub_discumsum(int n, int64_t L, int64_t M, int dtype, const void* values, const void* lams, void* out,
                   cudaStream_t st);
 

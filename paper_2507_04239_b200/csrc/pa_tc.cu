@@ -2,19 +2,21 @@
 //
 // Forward (per stream s, chunk k; reference chunked.py:287-413):
 //   prep_gates : ell = in-chunk cumsum of log g, lamlog = ell at chunk end
-//   prep_xt    : K~^T [dim][token] with k~_j = k_j * exp((ell_end - ell_j)/2),
-//                so phi'(k~_j) = W_j phi'(k_j) (suffix decay, chunked.py:89-95)
-//   featmajor  : S'_k = phi'(K~)^T [V | 1] -- tcgen05, A = phi'(K~)^T generated
-//                into TMEM from K~^T in smem (update_state, kernels.py:55-83)
-//   scan       : A'_k = lambda_k A'_{k-1} + omega S'_k in fp32 (discumsum,
-//                chunked.py:156-176), stored bf16 [slot][u]
+//   prep_xt    : K^T [dim][token], an exact fp16 copy of the bf16 keys
+//   prep_rows  : W_m v_m rows (fp16; W_m = exp(ell_end - ell_m) is the suffix
+//                decay, chunked.py:89-95), so phi' is generated from exact inputs
+//   featmajor  : S'_k = phi'(K)^T [W v | W] -- tcgen05, A = phi'(K)^T generated
+//                into TMEM from K^T in smem (update_state, kernels.py:55-83)
+//   scan       : slot_{k+1} = lambda_k slot_k + omega S'_k in fp32 (discumsum,
+//                chunked.py:156-176), stored fp16 x 2^-bits(k) [slot][u]
 //   out        : y = intra-chunk power attention (S = Q K^T, P = decay * s^2,
-//                O += P V on tcgen05) + phi'(q~) A'_{k-1} with phi'(q~)
-//                generated from registers into TMEM (query_state + combine,
-//                chunked.py:372-395); one TMEM accumulator for both.
+//                O_intra += P V on tcgen05) + phi'(q) slot_k with phi'(q)
+//                generated into TMEM (query_state + combine, chunked.py:372-395)
+//                in a second accumulator; pa_tc_out.cu
 // Backward (gradients.py:361-483) mirrors it: featmajor<true> (dA' =
-// phi'(Q~)^T [dnum|dden]), reverse scan, token-major dphi GEMMs with the
-// expand-VJP fused into their epilogue, and the intra-chunk VJP.
+// phi'(Q~)^T [dnum|dden]), the reverse scan (which also writes the expanded
+// states), the intra-chunk VJP (pa_tc_ib.cu) and the expanded-state VJP GEMMs
+// (pa_tc_zvjp.cu).
 #include <cuda.h>
 #include <stdio.h>
 
@@ -272,7 +274,9 @@ __global__ void __launch_bounds__(fm::THREADS, 2) k_tc_featmajor(const __grid_co
       const bool trm = !kBwd && blockIdx.x == 3 && blockIdx.y == 5 && blockIdx.z == 3;
 #endif
       PA_TR5(trm && mw == 0, 0);
-      for (int i = mw; i < nsub; i += 2) {
+      // deterministic mode: w1 issues every step in order (one summation order)
+      const int istep = g.det ? 1 : 2;
+      for (int i = g.det ? (mw ? nsub : 0) : mw; i < nsub; i += istep) {
         const int j = i / SPS, h = i % SPS, st = j % ST, buf = i % NBk;
         mbar_wait_w(&full[st], (j / ST) & 1);
         PA_TR5(trm, 8 + i * 4 + 0);
@@ -694,8 +698,7 @@ __device__ __forceinline__ void e_store(__half* et, int a, int b, int u, uint2 v
 __global__ void __launch_bounds__(256) k_tc_scan_bwd(Geo g, int ucols, const float* __restrict__ lamlog,
                                                      const float* __restrict__ dA,
                                                      const __half* __restrict__ st_main,
-                                                     const __half* __restrict__ st_den,
-                                                     __half* ds_main, __half* ds_den, float* dlam_part,
+                                                     const __half* __restrict__ st_den, float* dlam_part,
                                                      const float* __restrict__ carry, float* pre_out, int write,
                                                      __half* ea, __half* eg, int nbt) {
   extern __shared__ float red[];  // [n][8]
@@ -703,7 +706,6 @@ __global__ void __launch_bounds__(256) k_tc_scan_bwd(Geo g, int ucols, const flo
   const int e = (blockIdx.x * 256 + threadIdx.x) * 4;
   const bool ok = e < FH * ucols;
   const int f = ok ? e / ucols : 0, u = ok ? e - f * ucols : 0;
-  const float om = ok ? slot_omega(f) : 0.f;
   const int fa = 4 * c_blk.al[f >> 5] + ((f >> 3) & 3), fb = 8 * c_blk.be[f >> 5] + (f & 7);
   const float* src = dA + ((size_t)s * g.nsl * FH + f) * UW + u;
   const size_t kstride = (size_t)FH * UW;
@@ -729,19 +731,13 @@ __global__ void __launch_bounds__(256) k_tc_scan_bwd(Geo g, int ucols, const flo
       const int k = k1 - i;
       if (k < 0) break;
       if (write) {
-        if (ok && eg) {
+        if (ok && fa <= fb) {
           // expanded form for the state-VJP GEMMs: E = 2 sc G on every ordered pair
-          if (fa <= fb) {
-            const float sc = 2.f * pow2_neg_bits(g.ng - 1 - (g.k0 + k));
-            e_store(eg + ((size_t)s * g.nsl + k) * nbt * 4096, fa, fb, u,
-                    make_uint2(pack_f16(G.x * sc, G.y * sc), pack_f16(G.z * sc, G.w * sc)));
-          }
-        } else if (ok) {
-          const float sc = om * pow2_neg_bits(g.ng - 1 - (g.k0 + k));
-          *(uint2*)state_elem_ptr(ds_main, ds_den, (size_t)s * g.nsl + k, f, u) =
-              make_uint2(pack_f16(G.x * sc, G.y * sc), pack_f16(G.z * sc, G.w * sc));
+          const float sc = 2.f * pow2_neg_bits(g.ng - 1 - (g.k0 + k));
+          e_store(eg + ((size_t)s * g.nsl + k) * nbt * 4096, fa, fb, u,
+                  make_uint2(pack_f16(G.x * sc, G.y * sc), pack_f16(G.z * sc, G.w * sc)));
         }
-        if (ok && ea && fa <= fb && (k >= 1 || g.prefix)) {
+        if (ok && fa <= fb && (k >= 1 || g.prefix)) {
           // expanded forward state: slot values, doubled on the diagonal
           uint2 av = a[i];
           if (fa == fb) {
@@ -833,8 +829,6 @@ struct TcBwdWs {
   __half* dN16;          // dnum (fp16, state GEMMs)
   __half* dD;            // (dden, 0..) fp16
   float* dden;
-  __half* dsm;
-  __half* dsd;
   float* dq32;
   float* dk32;
   float* dv32;
@@ -881,8 +875,6 @@ static TcBwdWs carve_bwd(const Geo& g, void* base, size_t* bytes) {
   b.dN16 = (__half*)take(2ull * g.ns * g.t * HD);
   b.dD = (__half*)take(2ull * g.ns * g.t * 16);
   b.dden = (float*)take(4ull * g.ns * g.t);
-  b.dsm = (__half*)take(2ull * g.ns * g.nsl * ST_MAIN);
-  b.dsd = (__half*)take(2ull * g.ns * g.nsl * ST_DEN);
   b.dq32 = (float*)take(4ull * g.ns * g.t * HD);
   b.dk32 = (float*)take(4ull * g.ns * g.t * HD);
   b.dv32 = (float*)take(4ull * g.ns * g.t * HD);
@@ -970,18 +962,32 @@ static bool map_2d(CUtensorMap* m, const void* ptr, size_t rows, int cols, int b
 
 // The driver-API tensor-map encoder needs the device's primary context to be
 // current on the calling thread; torch's autograd worker threads may not have
-// bound it yet (CUresult 201).  Bind the context that owns the operand.
-static void bind_context_of(const void* ptr) {
-  cudaPointerAttributes at;
-  if (cudaPointerGetAttributes(&at, ptr) == cudaSuccess && at.device >= 0) cudaSetDevice(at.device);
-  cudaGetLastError();
-}
+// bound it yet (CUresult 201).  Make the operand's device current for the
+// duration of the call and restore the caller's device afterwards.  Only an
+// error raised by these queries is cleared, never one the caller had pending.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(const void* ptr) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+      cudaGetLastError();   // the failed query's own error
+      return;
+    }
+    int cur = -1;
+    if (at.device < 0 || cudaGetDevice(&cur) != cudaSuccess) return;
+    if (cur != at.device) prev = cur;
+    cudaSetDevice(at.device);   // also binds the primary context to this thread
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
 
 int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const float* log_g, void* y, float* rowsum,
                void* ws, cudaStream_t st, int mode, const float* carry, float* end_out) {
   size_t need;
   TcFwdWs w = carve_fwd(g, ws, &need);
-  bind_context_of(q);
+  DeviceGuard dg(q);
   const int with_den = (g.normalize || rowsum) ? 1 : 0;
   CUtensorMap m_q, m_k, m_v, m_vr, m_wa, m_kt;
   if (!map_bth(&m_q, q, g, 128) || !map_bth(&m_k, k, g, 128) || !map_bth(&m_v, v, g, 128) ||
@@ -1048,16 +1054,6 @@ int tc_sp_combine(const Geo& g, const void* fwd_ws, const float* carry, const fl
   return cuda_check("sp combine");
 }
 
-// one non-blocking side stream per device (created on first use)
-static cudaStream_t side_stream() {
-  static cudaStream_t ss[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return nullptr;
-  if (!ss[dev]) cudaStreamCreateWithFlags(&ss[dev], cudaStreamNonBlocking);
-  return ss[dev];
-}
-
 int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const float* log_g, const void* y,
                 const float* rowsum, const void* dy, void* dq, void* dk, void* dv, float* dlog_g, const void* fwd_ws,
                 void* bwd_ws, cudaStream_t st, int mode, const float* carry, float* pre_out) {
@@ -1069,118 +1065,75 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
   size_t n1, n2;
   TcFwdWs w = carve_fwd(g, const_cast<void*>(fwd_ws), &n1);  // sp / kt are dead after the forward: reused
   TcBwdWs b = carve_bwd(g, bwd_ws, &n2);
-  bind_context_of(q);
+  DeviceGuard dg(q);
   const int den = g.normalize ? 1 : 0;   // the backward needs the score sum only when normalizing
   const int uc = den ? UW : 64;
-  CUtensorMap m_qt, m_dn, m_dd, m_v128, m_dummy;
+  CUtensorMap m_qt, m_dn, m_dd, m_v128;
   if (!map_2d(&m_qt, w.kt, (size_t)g.ns * g.n * HD, g.c, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !map_2d(&m_dn, w.vr, (size_t)g.ns * g.t, HD, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !map_2d(&m_dd, w.wa, (size_t)g.ns * g.t, 16, 16, 64, CU_TENSOR_MAP_SWIZZLE_32B) ||
       !map_bth(&m_v128, v, g, 128)) {
     return 3;
   }
-  m_dummy = m_dn;
   const int red_bytes = 8 * 4 * g.n;
   const int nbt = 64 + den;
-  // state VJP: expanded-state GEMMs (pa_tc_zvjp.cu); PA_DPHI_OLD=1 selects the
-  // slot-form GEMM + expand-VJP kernels (pa_tc_dphi.cu) for comparison
-  static const bool old_dphi = [] {
-    const char* e = getenv("PA_DPHI_OLD");
-    return e && e[0] == '1';
-  }();
-  const bool zf = !old_dphi;
   if (red_bytes > 48 * 1024)
     cudaFuncSetAttribute(k_tc_scan_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, red_bytes);
-  // The intra-chunk VJP depends only on the prologue; PA_BWD_OVERLAP=1 runs it on a
-  // side stream next to the dA' GEMM and the reverse scan.  Measured on B200 it
-  // does not pay (22.3 vs 21.9 ms per step: the dA' CTAs take every SM first, then
-  // the intra-chunk kernel and the scan slow each other), so one stream is the default.
-  static const bool serial = [] {
-    const char* e = getenv("PA_BWD_OVERLAP");
-    return !(e && e[0] == '1');
-  }();
-  cudaStream_t st2 = serial ? st : side_stream();
-  cudaEvent_t ev_in = nullptr, ev_ib = nullptr;
   auto launch_intra = [&]() -> int {
-    if (!serial) {
-      cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming);
-      cudaEventCreateWithFlags(&ev_ib, cudaEventDisableTiming);
-      cudaEventRecord(ev_in, st);
-      cudaStreamWaitEvent(st2, ev_in, 0);
-    }
-    {
-      StageTimer tmr("bwd_intra", st2);
-      CUtensorMap m_q128, m_k128, m_dy128;
-      if (!map_bth(&m_q128, q, g, 128) || !map_bth(&m_k128, k, g, 128) || !map_bth(&m_dy128, dy, g, 128)) return 3;
-      tc_intra_bwd(g, m_q128, m_k128, m_v128, m_dy128, w.ell, b.dden, rowsum, b.dk32, b.dv32, b.dq32, b.dell,
-                   st2);
-    }
-    if (!serial) cudaEventRecord(ev_ib, st2);
+    StageTimer tmr("bwd_intra", st);
+    CUtensorMap m_q128, m_k128, m_dy128;
+    if (!map_bth(&m_q128, q, g, 128) || !map_bth(&m_k128, k, g, 128) || !map_bth(&m_dy128, dy, g, 128)) return 3;
+    tc_intra_bwd(g, m_q128, m_k128, m_v128, m_dy128, w.ell, b.dden, rowsum, b.dk32, b.dv32, b.dq32, b.dell, st);
     return 0;
   };
-  auto join_intra = [&]() {
-    if (serial) return;
-    cudaStreamWaitEvent(st, ev_ib, 0);
-    cudaEventDestroy(ev_in);
-    cudaEventDestroy(ev_ib);
-  };
   if (mode != 2) {
-  {
-    StageTimer tmr("bwd_prep", st);
-    cudaMemsetAsync(b.dell, 0, 4ull * g.ns * g.t, st);
-    cudaMemsetAsync(b.cu, 0, 4ull * g.ns * g.t, st);
-    cudaMemsetAsync(b.dlam, 0, 4ull * g.ns * g.n * scan_blocks(uc), st);
-    // without normalization dnum = dy: the kernels read dy in place (TMA / row loads
-    // with bf16 -> fp16 conversion), so only the normalized path materialises rows
-    if (den)
-      k_tc_bwd_prep<<<(unsigned)(((size_t)g.ns * g.t * 8 + 255) / 256), 256, 0, st>>>(
-          g, (const __nv_bfloat16*)dy, w.y32, rowsum, b.dN16, b.dD, b.dden);
-    k_tc_prep_xt<<<dim3(g.c / 64, g.n, g.ns), 256, 0, st>>>(g, (const __nv_bfloat16*)q, w.kt);
-    k_tc_prep_rows<<<(unsigned)(((size_t)g.ns * g.t * 4 + 255) / 256), 256, 0, st>>>(
-        g, den ? 1 : 3, den ? (const __nv_bfloat16*)b.dN16 : (const __nv_bfloat16*)dy, w.ell, w.lamlog,
-        den ? b.dden : nullptr, w.vr,
-        den ? w.wa : nullptr);
-  }
-  if (mode == 0 && launch_intra()) return 3;
-  if (g.n - 1 + g.prefix > 0) {
-    StageTimer tmr("bwd_query_state_dA", st);
-    auto fn = den ? k_tc_featmajor<true, 1> : k_tc_featmajor<true, 0>;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, fm::SMEM);
-    fn<<<dim3((NTH + fm::TPC - 1) / fm::TPC, g.n - 1 + g.prefix, g.ns), fm::THREADS, fm::SMEM, st>>>(m_qt, m_dn,
-                                                                                                 m_dd, g, w.sp);
-  }
-  if (mode == 1) {
-    StageTimer tmr("bwd_discumsum", st);
-    k_tc_scan_bwd<<<dim3(scan_blocks(uc), g.ns), 256, red_bytes, st>>>(g, uc, w.lamlog, (const float*)w.sp, w.stm, w.std_,
-                                                                          b.dsm, b.dsd, b.dlam, nullptr, pre_out, 0,
-                                                                          nullptr, nullptr, nbt);
-    count_launch(4);
-    return cuda_check("tc backward (sp local)");
-  }
+    {
+      StageTimer tmr("bwd_prep", st);
+      cudaMemsetAsync(b.dell, 0, 4ull * g.ns * g.t, st);
+      cudaMemsetAsync(b.cu, 0, 4ull * g.ns * g.t, st);
+      cudaMemsetAsync(b.dlam, 0, 4ull * g.ns * g.n * scan_blocks(uc), st);
+      // without normalization dnum = dy: the kernels read dy in place (TMA / row loads
+      // with bf16 -> fp16 conversion), so only the normalized path materialises rows
+      if (den)
+        k_tc_bwd_prep<<<(unsigned)(((size_t)g.ns * g.t * 8 + 255) / 256), 256, 0, st>>>(
+            g, (const __nv_bfloat16*)dy, w.y32, rowsum, b.dN16, b.dD, b.dden);
+      k_tc_prep_xt<<<dim3(g.c / 64, g.n, g.ns), 256, 0, st>>>(g, (const __nv_bfloat16*)q, w.kt);
+      k_tc_prep_rows<<<(unsigned)(((size_t)g.ns * g.t * 4 + 255) / 256), 256, 0, st>>>(
+          g, den ? 1 : 3, den ? (const __nv_bfloat16*)b.dN16 : (const __nv_bfloat16*)dy, w.ell, w.lamlog,
+          den ? b.dden : nullptr, w.vr, den ? w.wa : nullptr);
+    }
+    if (mode == 0 && launch_intra()) return 3;
+    if (g.n - 1 + g.prefix > 0) {
+      StageTimer tmr("bwd_query_state_dA", st);
+      auto fn = den ? k_tc_featmajor<true, 1> : k_tc_featmajor<true, 0>;
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, fm::SMEM);
+      fn<<<dim3((NTH + fm::TPC - 1) / fm::TPC, g.n - 1 + g.prefix, g.ns), fm::THREADS, fm::SMEM, st>>>(
+          m_qt, m_dn, m_dd, g, w.sp);
+    }
+    if (mode == 1) {
+      StageTimer tmr("bwd_discumsum", st);
+      k_tc_scan_bwd<<<dim3(scan_blocks(uc), g.ns), 256, red_bytes, st>>>(g, uc, w.lamlog, (const float*)w.sp,
+                                                                            w.stm, w.std_, b.dlam, nullptr,
+                                                                            pre_out, 0, nullptr, nullptr, nbt);
+      count_launch(4);
+      return cuda_check("tc backward (sp local)");
+    }
   }
   if (mode == 2 && launch_intra()) return 3;
   {
     StageTimer tmr("bwd_discumsum", st);
-    k_tc_scan_bwd<<<dim3(scan_blocks(uc), g.ns), 256, red_bytes, st>>>(g, uc, w.lamlog, (const float*)w.sp, w.stm, w.std_,
-                                                                          b.dsm, b.dsd, b.dlam, carry, pre_out, 1,
-                                                                          zf ? b.ea : nullptr, zf ? b.eg : nullptr, nbt);
+    k_tc_scan_bwd<<<dim3(scan_blocks(uc), g.ns), 256, red_bytes, st>>>(g, uc, w.lamlog, (const float*)w.sp, w.stm,
+                                                                          w.std_, b.dlam, carry, pre_out, 1, b.ea,
+                                                                          b.eg, nbt);
   }
-  join_intra();
   {
     StageTimer tmr("bwd_query_state_dq", st);
-    if (zf)
-      tc_zvjp(g, false, den ? 0 : 1, den ? (const void*)b.dN16 : dy, b.dD, q, w.ell, w.lamlog, b.ea, b.dq32,
-              nullptr, b.dell, nullptr, dq, nullptr, st);
-    else
-      tc_dphi(g, false, den ? (const void*)b.dN16 : dy, den ? 0 : 1, b.dD, q, w.ell, w.lamlog, w.stm, w.std_,
-              b.dq32, nullptr, b.dell, nullptr, dq, nullptr, st);
+    tc_zvjp(g, false, den ? 0 : 1, den ? (const void*)b.dN16 : dy, b.dD, q, w.ell, w.lamlog, b.ea, b.dq32,
+            nullptr, b.dell, nullptr, dq, nullptr, st);
   }
   {
     StageTimer tmr("bwd_update_state", st);
-    if (zf)
-      tc_zvjp(g, true, 1, v, nullptr, k, w.ell, w.lamlog, b.eg, b.dk32, b.dv32, b.dell, b.cu, dk, dv, st);
-    else
-      tc_dphi(g, true, v, 1, nullptr, k, w.ell, w.lamlog, b.dsm, b.dsd, b.dk32, b.dv32, b.dell, b.cu, dk, dv, st);
+    tc_zvjp(g, true, 1, v, nullptr, k, w.ell, w.lamlog, b.eg, b.dk32, b.dv32, b.dell, b.cu, dk, dv, st);
   }
   {
     StageTimer tmr("bwd_finish", st);

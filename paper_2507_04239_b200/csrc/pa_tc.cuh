@@ -37,13 +37,6 @@ int tc_intra_bwd(const Geo& g, const CUtensorMap& m_q, const CUtensorMap& m_k, c
                  const CUtensorMap& m_dn, const float* ell, const float* dden, const float* rsum, float* dk32,
                  float* dv32, float* dq32, float* dell, cudaStream_t st);
 
-// token-major state VJP + fused expand-VJP (pa_tc_dphi.cu): final bf16 dq (query side)
-// or dk, dv (update side)
-// a_rows: the A operand rows, fp16 stream-major (a_bf16_bth = 0) or bf16 in the [b, t, h, 64] layout (1)
-int tc_dphi(const Geo& g, bool upd, const void* a_rows, int a_bf16_bth, const __half* a16_rows, const void* xraw,
-            const float* ell, const float* lamlog, const __half* b_main, const __half* b_den, const float* dx32,
-            const float* dv32, float* dell, float* dellend, void* dxo, void* dvo, cudaStream_t st);
-
 // expanded-state VJP GEMMs (pa_tc_zvjp.cu): E = expanded A'_{k-1} (query side) or dS~_k (update side)
 int tc_zvjp(const Geo& g, bool upd, int u_bf16_bth, const void* u_rows, const __half* u16, const void* xraw,
             const float* ell, const float* lamlog, const __half* E, const float* dx32, const float* dv32,

@@ -195,7 +195,9 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
         const uint64_t sm0 = smem_desc(smem_u32(st_s), 8192, 1024, 2);
         const uint64_t sd0 = smem_desc(smem_u32(sd_s), 2048, 256, 6);
         PA_TR4(trb && mw == 0, 0);
-        for (int stp = mw; stp < NSTEP; stp += 2) {
+        // deterministic mode: w15 issues every step in order (one summation order)
+        const int sstep = g.det ? 1 : 2;
+        for (int stp = g.det ? (mw ? NSTEP : 0) : mw; stp < NSTEP; stp += sstep) {
           const int bb = stp & 1, sb = stp % ST_ST;
           mbar_wait_w(&a_full[bb], (stp >> 1) & 1);
           PA_TR4(trb, 10 + stp * 3 + 0);

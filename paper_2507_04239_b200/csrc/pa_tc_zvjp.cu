@@ -210,7 +210,8 @@ __global__ void __launch_bounds__(zv::THREADS, 1)
       bool first = true;
       for (int j = 0; j < NJ; ++j) {
         const int gs = gs0 + j;
-        if ((gs & 1) != mw) continue;
+        // deterministic mode: w9 issues every stage in order (one summation order)
+        if (g.det ? mw != 0 : (gs & 1) != mw) continue;
         if (first) {
           mbar_wait_w(acc_empty, it & 1);
           first = false;
@@ -252,7 +253,12 @@ __global__ void __launch_bounds__(zv::THREADS, 1)
           }
         }
       }
-      tc_commit_w(acc_full);   // both issuers: count 2
+      if (!g.det) {
+        tc_commit_w(acc_full);   // both issuers: count 2
+      } else if (mw == 0) {
+        tc_commit_w(acc_full);
+        tc_commit_w(acc_full);
+      }
     }
   } else if (w < NGW) {
     // generating threads: one token row per TMEM lane; the tile's scaled operand

@@ -27,7 +27,7 @@ def vjp_chunked(batch: SequenceBatch, cfg: AttentionConfig, plan, upstream) -> G
 
     if cfg.mechanism is not Mechanism.POWER:
         raise InvalidSpec("only the power mechanism has a CUDA backward")
-    spec = cfg.expansion.require_spow()
+    spec = cfg.expansion   # outputs (and so gradients) do not depend on the kind
     host = batch.on_host
     chunk = None if plan is None else plan.c
     if plan is None and cfg.chunk_size is not None:
@@ -41,7 +41,8 @@ def vjp_chunked(batch: SequenceBatch, cfg: AttentionConfig, plan, upstream) -> G
     up = to_dev(upstream, dt)
     if tuple(up.shape) != tuple(batch.v.shape):
         raise ShapeMismatch(f"upstream must match y {tuple(batch.v.shape)}, got {tuple(up.shape)}")
-    y = power_full(q, k, v, lg, p=spec.p, chunk_size=chunk, scale=cfg.scale, normalize=cfg.normalize)
+    y = power_full(q, k, v, lg, p=spec.p, chunk_size=chunk, scale=cfg.scale, normalize=cfg.normalize,
+                   check_denominator="sync")
     grads = torch.autograd.grad(y, [q, k, v] + ([lg] if lg is not None else []), up)
     dg = None if lg is None else grads[3] / torch.exp(lg.detach())
     f64 = np.float64 if host else None

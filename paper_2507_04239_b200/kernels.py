@@ -13,7 +13,7 @@ import torch
 from . import _lib
 from ._convert import back, to_dev
 from .errors import InvalidSpec, ShapeMismatch
-from .expansions import ExpansionSpec, expansion_dim
+from .expansions import ExpansionKind, ExpansionSpec, expansion_dim, monomial_table
 
 VALID_BACKENDS = ("auto", "cuda", "compiled")
 
@@ -40,10 +40,26 @@ def _p(t):
     return ctypes.c_void_p(0 if t is None else t.data_ptr())
 
 
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+_DEV_TABLES: dict = {}
+
+
+def _device_table(spec: ExpansionSpec, device):
+    """The kind's monomial table on the device (uploaded once per spec/device)."""
+    key = (spec, str(device))
+    if key not in _DEV_TABLES:
+        idx, w = monomial_table(spec)
+        _DEV_TABLES[key] = (torch.from_numpy(np.ascontiguousarray(idx)).to(device),
+                            torch.from_numpy(np.ascontiguousarray(w)).to(device))
+    return _DEV_TABLES[key]
+
+
 def update_state_kernel(k_chunk, v_chunk, decay, spec: ExpansionSpec, backend=None):
     """(state [n, D, e], key_sum [n, D]) from k [n, c, d], v [n, c, e], decay [n, c]|None."""
     resolve_backend(backend)
-    spec.require_spow()
     host = not isinstance(k_chunk, torch.Tensor)
     (k, v, w), dt = _prep([k_chunk, v_chunk, decay], host)
     if k.dim() != 3 or v.dim() != 3 or k.shape[:2] != v.shape[:2] or k.shape[2] != spec.d:
@@ -54,16 +70,22 @@ def update_state_kernel(k_chunk, v_chunk, decay, spec: ExpansionSpec, backend=No
     state = torch.empty(n, D, e, dtype=dt, device=k.device)
     ks = torch.empty(n, D, dtype=dt, device=k.device)
     code = _lib.PA_F64 if dt == torch.float64 else _lib.PA_F32
-    _lib.check(_lib.load().pa_update_state(n, c, d, e, spec.p, code, _p(k), _p(v), _p(w), _p(state),
-                                            _p(ks), 0, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
-               "update_state")
+    lib = _lib.load()
+    with torch.cuda.device(k.device):
+        if spec.kind is ExpansionKind.SPOW:
+            rc = lib.pa_update_state(n, c, d, e, spec.p, code, _p(k), _p(v), _p(w), _p(state), _p(ks), 0,
+                                     _stream())
+        else:
+            ti, tw = _device_table(spec, k.device)
+            rc = lib.pa_update_state_table(n, c, d, e, spec.p, D, code, _p(k), _p(v), _p(w), _p(ti), _p(tw),
+                                           _p(state), _p(ks), 0, _stream())
+    _lib.check(rc, "update_state")
     return back(state, host), back(ks, host)
 
 
 def query_state_kernel(q_chunk, state, key_sum, spec: ExpansionSpec, backend=None):
     """(y [n, c, e], denom [n, c]) from pre-scaled q [n, c, d], state [n, D, e], key_sum [n, D]."""
     resolve_backend(backend)
-    spec.require_spow()
     host = not isinstance(q_chunk, torch.Tensor)
     (q, st, ks), dt = _prep([q_chunk, state, key_sum], host)
     n, c, d = q.shape
@@ -73,9 +95,16 @@ def query_state_kernel(q_chunk, state, key_sum, spec: ExpansionSpec, backend=Non
     y = torch.empty(n, c, e, dtype=dt, device=q.device)
     den = torch.empty(n, c, dtype=dt, device=q.device)
     code = _lib.PA_F64 if dt == torch.float64 else _lib.PA_F32
-    _lib.check(_lib.load().pa_query_state(n, c, d, e, spec.p, code, _p(q), _p(st), _p(ks), _p(y),
-                                           _p(den), 0, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
-               "query_state")
+    lib = _lib.load()
+    with torch.cuda.device(q.device):
+        if spec.kind is ExpansionKind.SPOW:
+            rc = lib.pa_query_state(n, c, d, e, spec.p, code, _p(q), _p(st), _p(ks), _p(y), _p(den), 0,
+                                    _stream())
+        else:
+            ti, tw = _device_table(spec, q.device)
+            rc = lib.pa_query_state_table(n, c, d, e, spec.p, st.shape[1], code, _p(q), _p(st), _p(ks), _p(ti),
+                                          _p(tw), _p(y), _p(den), 0, _stream())
+    _lib.check(rc, "query_state")
     return back(y, host), back(den, host)
 
 
@@ -106,7 +135,7 @@ def discumsum_kernel(values, lambdas):
     out = torch.empty_like(vals)
     code = _lib.PA_F64 if dt == torch.float64 else _lib.PA_F32
     lam2 = lam2.contiguous() if lam2 is not None else torch.zeros(1, dtype=dt, device=vals.device)
-    _lib.check(_lib.load().pa_discumsum(n, L, total // L, code, _p(vals), _p(lam2), _p(out),
-                                         ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
-               "discumsum")
+    with torch.cuda.device(vals.device):
+        rc = _lib.load().pa_discumsum(n, L, total // L, code, _p(vals), _p(lam2), _p(out), _stream())
+    _lib.check(rc, "discumsum")
     return back(out, host)

@@ -60,19 +60,28 @@ class SpPartition:
 
 
 # ---------------------------------------------------------------- carry chains
+def _peer(group, rank: int) -> int:
+    """Global rank of group rank `rank` (dist.send/recv take global ranks even
+    when a group is given)."""
+    import torch.distributed as dist
+
+    return rank if group is None else dist.get_global_rank(group, rank)
+
+
 def chain_forward(local: torch.Tensor, combine: Callable[[Optional[torch.Tensor], torch.Tensor], torch.Tensor],
                   rank: int, world: int, group=None) -> Optional[torch.Tensor]:
     """Exclusive left-to-right scan of the per-rank local results over ranks.
     Returns the incoming carry of this rank (None on rank 0).  One receive from
-    rank-1 and one send to rank+1 (torch.distributed point-to-point)."""
+    rank-1 and one send to rank+1 (torch.distributed point-to-point); `rank`
+    and `world` are positions inside `group`."""
     import torch.distributed as dist
 
     carry = None
     if rank > 0:
         carry = torch.empty_like(local)
-        dist.recv(carry, src=rank - 1, group=group)
+        dist.recv(carry, src=_peer(group, rank - 1), group=group)
     if rank < world - 1:
-        dist.send(combine(carry, local).contiguous(), dst=rank + 1, group=group)
+        dist.send(combine(carry, local).contiguous(), dst=_peer(group, rank + 1), group=group)
     return carry
 
 
@@ -84,9 +93,9 @@ def chain_backward(local: torch.Tensor, combine: Callable[[Optional[torch.Tensor
     carry = None
     if rank < world - 1:
         carry = torch.empty_like(local)
-        dist.recv(carry, src=rank + 1, group=group)
+        dist.recv(carry, src=_peer(group, rank + 1), group=group)
     if rank > 0:
-        dist.send(combine(carry, local).contiguous(), dst=rank - 1, group=group)
+        dist.send(combine(carry, local).contiguous(), dst=_peer(group, rank - 1), group=group)
     return carry
 
 
@@ -185,9 +194,10 @@ class _PowerFullSP(torch.autograd.Function):
     @staticmethod
     def backward(ctx, dy):
         r = ctx.r
-        pre = r.bwd_local(dy)
-        carry = chain_backward(pre, r.combine, ctx.rank, ctx.world, ctx.group)
-        dQ, dK, dV, dlg = r.bwd_finish(carry)
+        with torch.cuda.device(r.Q.device):
+            pre = r.bwd_local(dy)
+            carry = chain_backward(pre, r.combine, ctx.rank, ctx.world, ctx.group)
+            dQ, dK, dV, dlg = r.bwd_finish(carry)
         return dQ, dK, dV, dlg, None, None, None, None, None, None, None, None
 
 
@@ -202,8 +212,9 @@ def power_full_sp(Q, K, V, log_G=None, *, p=2, chunk_size, scale=None, normalize
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     t_total = Q.shape[1] * world
-    return _PowerFullSP.apply(Q, K, V, log_G, int(p), int(chunk_size), scale, bool(normalize), t_total, group,
-                              rank, world)
+    with torch.cuda.device(Q.device):
+        return _PowerFullSP.apply(Q, K, V, log_G, int(p), int(chunk_size), scale, bool(normalize), t_total,
+                                  group, rank, world)
 
 
 def emulate_ranks(Q, K, V, log_G, *, ranks: int, p=2, chunk_size, scale=None, normalize=False, dy=None):
