@@ -5,10 +5,13 @@
 
 One step = power_full forward + backward over the whole synthetic batch
 (inputs resident in HBM, each 512 MiB >> the 126 MB L2, so no L2 flush is
-needed).  Multi-GPU: one process per GPU (torchrun), each rank runs the full
-per-GPU workload on its own (batch, head) streams with no data-path collective
-(weak scaling: streams are independent).  Timing: CUDA events on
-the launching stream, barrier + synchronize on both sides, max over ranks.
+needed).  Multi-GPU (--gpus N; bench.py re-launches itself under
+torch.distributed.run when started without it): one process per GPU, by
+default the sequence-parallel 1M-token config (configs[3], chunk ranges per
+rank, carry chain over NCCL point-to-point; strong scaling); --workload cfg2
+shards configs[1]'s streams instead (weak scaling, no data-path collective).
+Timing: CUDA events on the launching stream, barrier + synchronize on both
+sides, max over ranks.
 
 --impl reference times the reference's own CPU algorithm (the numpy oracle
 port, oracle/power_oracle.py, which is pinned to the reference by
@@ -33,13 +36,22 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "power-attn fwd+bwd tokens/sec at p=2,d=64,64k ctx; % of BF16 tensor peak"
-CFG = dict(b=4, h=16, t=65536, d=64, e=64, p=2, chunk=1024, gated=True, normalize=False)
-WORKLOAD = "configs[1]: power_full fwd+bwd bf16 p=2 d=64 b=4 h=16 t=65536 chunk=1024 gated"
-# --workload sp1m: BASELINE configs[3], one 1,048,576-token sequence (b=1, h=16)
-# split over the ranks by chunk range (sequence parallelism, NCCL carry chain)
-CFG_SP = dict(b=1, h=16, t=1048576, d=64, e=64, p=2, chunk=1024, gated=True, normalize=False)
-WORKLOAD_SP = ("configs[3]: sequence-parallel power_full fwd+bwd bf16 p=2 d=64 b=1 h=16 t=1048576 chunk=1024 "
-               "gated, chunk ranges split over the ranks")
+# BASELINE.json configs, numbered as in SURVEY.md (cfg1 = configs[0], ...)
+WORKLOADS = {
+    "cfg1": (dict(b=1, h=2, t=1024, d=32, e=32, p=2, chunk=128, gated=True, normalize=False, dtype="f32"),
+             "configs[0]: power_full fwd+bwd fp32 p=2 d=32 b=1 h=2 t=1024 chunk=128 gated"),
+    "cfg2": (dict(b=4, h=16, t=65536, d=64, e=64, p=2, chunk=1024, gated=True, normalize=False, dtype="bf16"),
+             "configs[1]: power_full fwd+bwd bf16 p=2 d=64 b=4 h=16 t=65536 chunk=1024 gated"),
+    "cfg3": (dict(b=1, h=16, t=16384, d=32, e=32, p=4, chunk=1024, gated=False, normalize=True, dtype="bf16"),
+             "configs[2]: power_full fwd+bwd bf16 p=4 d=32 (D=52360) b=1 h=16 t=16384 chunk=1024 ungated, "
+             "normalized"),
+    # one 1,048,576-token sequence (b=1, h=16) split over the ranks by chunk range
+    # (sequence parallelism, carry chain over NCCL point-to-point)
+    "sp1m": (dict(b=1, h=16, t=1048576, d=64, e=64, p=2, chunk=1024, gated=True, normalize=False, dtype="bf16"),
+             "configs[3]: sequence-parallel power_full fwd+bwd bf16 p=2 d=64 b=1 h=16 t=1048576 chunk=1024 "
+             "gated, chunk ranges split over the ranks"),
+}
+CFG, WORKLOAD = WORKLOADS["cfg2"]
 
 
 # --------------------------------------------------------------------------
@@ -132,7 +144,7 @@ class Clocks:
 # CPU reference arm / baseline (oracle port of the reference algorithm)
 # --------------------------------------------------------------------------
 def _cpu_worker(args):
-    t_slice, c, seed = args
+    cfg, t_slice, seed = args
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     import numpy as np
     from threadpoolctl import threadpool_limits
@@ -140,53 +152,75 @@ def _cpu_worker(args):
     from oracle import power_oracle as O
 
     with threadpool_limits(1):
-        q, k, v, g = O.generate_inputs(1, t_slice, 1, 64, 64, seed=seed, dtype=np.float32, gating=True)
+        q, k, v, g = O.generate_inputs(1, t_slice, 1, cfg["d"], cfg["e"], seed=seed, dtype=np.float32,
+                                       gating=cfg["gated"])
         dy = np.ones_like(v)
         t0 = time.perf_counter()
-        O.chunked_forward(q, k, v, g, 2, c)
-        O.chunked_backward(q, k, v, g, 2, c, dy)
+        O.chunked_forward(q, k, v, g, cfg["p"], cfg["chunk"], normalize=cfg["normalize"])
+        O.chunked_backward(q, k, v, g, cfg["p"], cfg["chunk"], dy, normalize=cfg["normalize"])
         return time.perf_counter() - t0
 
 
-def cpu_sample(cores: int, t_slice: int = 4096):
-    """One bounded sample: `cores` processes, each fwd+bwd over one stream
-    slice of t_slice tokens (c=1024, d=64).  Returns (tokens/s of the full
-    b*t metric, seconds, description)."""
+def cpu_sample(cfg, cores: int, t_slice: int | None = None):
+    """One bounded sample of the workload on the host: `cores` processes, each
+    fwd+bwd over one (batch, head) stream slice of t_slice tokens.  Returns
+    (tokens/s of the b*t metric, seconds, description)."""
     import multiprocessing as mp
 
+    if t_slice is None:
+        # 8 chunks (query runs on 7 of 8, the full stream on 63 of 64); p=4 streams
+        # cost ~50x more per token, so they get one chunk pair
+        t_slice = min(cfg["t"], cfg["chunk"] * (2 if cfg["p"] > 2 else 8))
+    n_proc = min(cores, cfg["b"] * cfg["h"]) if t_slice >= cfg["t"] else cores
     ctx = mp.get_context("fork")
     t0 = time.perf_counter()
-    with ctx.Pool(cores) as pool:
-        pool.map(_cpu_worker, [(t_slice, CFG["chunk"], i) for i in range(cores)])
+    with ctx.Pool(n_proc) as pool:
+        pool.map(_cpu_worker, [(cfg, t_slice, i) for i in range(n_proc)])
     wall = time.perf_counter() - t0
-    stream_tok_s = cores * t_slice / wall
-    tok_s = stream_tok_s / CFG["h"]  # metric counts b*t tokens; each token spans h streams
-    desc = (f"{cores} processes x 1 stream x {t_slice} tokens (c=1024, d=64, gated) fwd+bwd, numpy oracle "
-            f"(port of reference chunked.py/gradients.py), 1 BLAS thread each; tokens/s = stream-tokens/s / h, "
-            f"linear in t")
+    stream_tok_s = n_proc * t_slice / wall
+    tok_s = stream_tok_s / cfg["h"]  # the metric counts b*t tokens; each token spans h streams
+    desc = (f"{n_proc} processes x 1 stream x {t_slice} tokens (p={cfg['p']}, d={cfg['d']}, c={cfg['chunk']}, "
+            f"gated={cfg['gated']}, normalize={cfg['normalize']}) fwd+bwd, numpy oracle (port of reference "
+            f"chunked.py/gradients.py), 1 BLAS thread each; tokens/s = stream-tokens/s / h (linear in t, "
+            f"reference test_acceptance.py:345-354)")
     return tok_s, wall, desc
+
+
+def pick_workload(args, world: int):
+    name = args.workload
+    if name == "auto":
+        name = "cfg2" if world == 1 else "sp1m"
+    return name
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
+    name = pick_workload(args, world)
+    if name == "lm124m":
+        print(json.dumps({"impl": "reference", "unavailable": "configs[4] is a model stack; the reference has no "
+                          "LM (its CPU path is the attention operator only)"}), flush=True)
+        return
+    cfg, workload = WORKLOADS[name]
     cores = os.cpu_count() or 1
     for _ in range(args.warmup):
-        cpu_sample(cores, 1024)
+        cpu_sample(cfg, cores, cfg["chunk"])
     vals = []
     t_all = time.perf_counter()
+    desc = ""
     for _ in range(args.steps):
-        v, wall, desc = cpu_sample(cores)
+        v, wall, desc = cpu_sample(cfg, cores)
         vals.append(v)
     elapsed = time.perf_counter() - t_all
     val = statistics.median(vals)
     line = {
-        "impl": "reference", "metric": METRIC, "value": val, "unit": "tokens/s", "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * elapsed / max(args.steps, 1),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (Philox, reference inputs.py distributions)",
-        "config": {"workload": WORKLOAD + " (bounded CPU sample, extrapolated)", **CFG},
+        "higher_is_better": True, "scaling": "strong" if name == "sp1m" else "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (Philox, reference inputs.py distributions)",
+        "config": {"workload": workload + " (bounded CPU sample, extrapolated)", **cfg},
         "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": desc},
         "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -196,6 +230,17 @@ def run_reference(args):
 # --------------------------------------------------------------------------
 # GPU arm
 # --------------------------------------------------------------------------
+def scan_bytes(cfg):
+    """Algorithmic HBM bytes of the two scans per step, fp16 state
+    storage: forward reads S_k and writes A_k; backward reads dA_k and A_k and
+    writes the state cotangent."""
+    D = math.comb(cfg["d"] + cfg["p"] - 1, cfg["p"])
+    n, ns = cfg["t"] // cfg["chunk"], cfg["b"] * cfg["h"]
+    cols = cfg["e"] + (1 if cfg["normalize"] else 0)
+    unit = n * ns * D * cols * 2
+    return {"fwd_discumsum": 2 * unit, "bwd_discumsum": 3 * unit}
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -203,33 +248,43 @@ def run_gpu(args):
     from paper_2507_04239_b200 import _lib, power_full
     from paper_2507_04239_b200.parallel import power_full_sp
 
-    global CFG, WORKLOAD
-    sp = args.workload == "sp1m"
-    if sp:
-        CFG, WORKLOAD = CFG_SP, WORKLOAD_SP
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    name = pick_workload(args, world)
+    if name == "lm124m":
+        import lm_bench
+
+        return lm_bench.run(args, world, rank, local)
+    cfg, workload = WORKLOADS[name]
+    sp = name == "sp1m"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    b, h, t, d, e, c = (CFG[k] for k in ("b", "h", "t", "d", "e", "chunk"))
+    b, h, t, d, e, c = (cfg[k] for k in ("b", "h", "t", "d", "e", "chunk"))
     if sp:
         t = t // world   # this rank's contiguous token range
+    dt = torch.float32 if cfg["dtype"] == "f32" else torch.bfloat16
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
-    Q = (torch.rand(b, t, h, d, device=dev, generator=g) * 2 - 1).bfloat16().requires_grad_()
-    K = (torch.rand(b, t, h, d, device=dev, generator=g) * 2 - 1).bfloat16().requires_grad_()
-    V = (torch.rand(b, t, h, e, device=dev, generator=g) * 2 - 1).bfloat16().requires_grad_()
-    LG = torch.log(torch.rand(b, t, h, device=dev, generator=g) * 0.1 + 0.9).requires_grad_()
-    dY = (torch.rand(b, t, h, e, device=dev, generator=g) * 2 - 1).bfloat16()
+    Q = (torch.rand(b, t, h, d, device=dev, generator=g) * 2 - 1).to(dt).requires_grad_()
+    K = (torch.rand(b, t, h, d, device=dev, generator=g) * 2 - 1).to(dt).requires_grad_()
+    V = (torch.rand(b, t, h, e, device=dev, generator=g) * 2 - 1).to(dt).requires_grad_()
+    LG = None
+    if cfg["gated"]:
+        LG = torch.log(torch.rand(b, t, h, device=dev, generator=g) * 0.1 + 0.9).requires_grad_()
+    dY = (torch.rand(b, t, h, e, device=dev, generator=g) * 2 - 1).to(dt)
+    ins = [x for x in (Q, K, V, LG) if x is not None]
+
+    def op(q, k, v, lg):
+        if sp:
+            return power_full_sp(q, k, v, lg, p=cfg["p"], chunk_size=c, normalize=cfg["normalize"])
+        return power_full(q, k, v, lg, p=cfg["p"], chunk_size=c, normalize=cfg["normalize"],
+                          check_denominator=False)
 
     def step():
-        if sp:
-            y = power_full_sp(Q, K, V, LG, p=CFG["p"], chunk_size=c, normalize=CFG["normalize"])
-        else:
-            y = power_full(Q, K, V, LG, p=CFG["p"], chunk_size=c, normalize=CFG["normalize"])
-        return torch.autograd.grad(y, [Q, K, V, LG], dY)
+        y = op(Q, K, V, LG)
+        return torch.autograd.grad(y, ins, dY)
 
     def barrier():
         if world > 1:
@@ -271,11 +326,11 @@ def run_gpu(args):
     # ---- e2e: reference-facing call with HOST buffers (copies timed) ------
     e2e = None
     if not args.no_e2e:
-        hQ, hK, hV = (x.detach().cpu().pin_memory() for x in (Q, K, V))
-        hL = LG.detach().cpu().pin_memory()
-        hdY = dY.cpu().pin_memory()
-        outs = [torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in (Q, K, V, LG)]
-        h2d = sum(x.numel() * x.element_size() for x in (hQ, hK, hV, hL, hdY))
+        host_in = [x.detach().cpu().pin_memory() for x in ins] + [dY.cpu().pin_memory()]
+        # y and every gradient come back to the host each step
+        outs = [torch.empty((b, t, h, e), dtype=dt).pin_memory()] + \
+               [torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in ins]
+        h2d = sum(x.numel() * x.element_size() for x in host_in)
         d2h = sum(x.numel() * x.element_size() for x in outs)
 
         # Pipelined like a training loop that prefetches its next batch: the
@@ -284,30 +339,30 @@ def run_gpu(args):
         # crosses PCIe inside the timed region, every step).
         s_comp = torch.cuda.current_stream(dev)
         s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-        dbuf = [[torch.empty(x.shape, dtype=x.dtype, device=dev) for x in (hQ, hK, hV, hL, hdY)] for _ in range(2)]
+        dbuf = [[torch.empty(x.shape, dtype=x.dtype, device=dev) for x in host_in] for _ in range(2)]
         ev_in = [torch.cuda.Event() for _ in range(2)]
         ev_free = [torch.cuda.Event() for _ in range(2)]
         ev_done = torch.cuda.Event()
-        for e in ev_free:
-            e.record(s_comp)
+        for ev in ev_free:
+            ev.record(s_comp)
 
         def e2e_step(i):
-            b = i % 2
+            bi = i % 2
             with torch.cuda.stream(s_in):
-                s_in.wait_event(ev_free[b])
-                for d, h in zip(dbuf[b], (hQ, hK, hV, hL, hdY)):
-                    d.copy_(h, non_blocking=True)
-                ev_in[b].record(s_in)
-            s_comp.wait_event(ev_in[b])
-            dq, dk, dv, dl = (x.detach().requires_grad_() for x in dbuf[b][:4])
-            fn = power_full_sp if sp else power_full
-            y = fn(dq, dk, dv, dl, p=CFG["p"], chunk_size=c, normalize=CFG["normalize"])
-            gr = torch.autograd.grad(y, [dq, dk, dv, dl], dbuf[b][4])
-            ev_free[b].record(s_comp)
+                s_in.wait_event(ev_free[bi])
+                for dst, src in zip(dbuf[bi], host_in):
+                    dst.copy_(src, non_blocking=True)
+                ev_in[bi].record(s_in)
+            s_comp.wait_event(ev_in[bi])
+            xs = [x.detach().requires_grad_() for x in dbuf[bi][:-1]]
+            xs4 = xs + [None] * (4 - len(xs))
+            y = op(*xs4)
+            gr = torch.autograd.grad(y, xs, dbuf[bi][-1])
+            ev_free[bi].record(s_comp)
             ev_done.record(s_comp)
             with torch.cuda.stream(s_out):
                 s_out.wait_event(ev_done)
-                for o, gx in zip(outs, gr):
+                for o, gx in zip(outs, (y.detach(),) + tuple(gr)):
                     gx.record_stream(s_out)
                     o.copy_(gx, non_blocking=True)
 
@@ -331,7 +386,7 @@ def run_gpu(args):
             ems = float(tt.item())
         e2e = {"value": tokens / (ems / 1000.0), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": ems,
-               "pipeline": "H2D of step i+1 and D2H of step i-1 overlap step i (separate streams)"}
+               "pipeline": "H2D of step i+1 and D2H (y and all gradients) of step i-1 overlap step i"}
 
     if rank != 0:
         if world > 1:
@@ -339,7 +394,7 @@ def run_gpu(args):
         return
 
     peak, peak_sus, hbm, peak_kind = load_peaks()
-    fl = flops(CFG)
+    fl = flops(cfg)
     jobs = 1 if sp else world   # the whole-job algorithmic FLOPs
     tflops = jobs * fl["total"] / (ms / 1000.0) / 1e12
     # dominant kernel (largest share of step time) and its roofline
@@ -354,26 +409,35 @@ def run_gpu(args):
         if per is not None:
             launch_ms = stage_ms[dom] / max(stage_n[dom], 1)
             achieved = per / max(stage_n[dom], 1) / (launch_ms / 1000.0) / 1e12
-            roof = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peak_sus, "unit": "TFLOP/s",
-                    "frac": achieved / peak_sus, "traffic": traffic_for(dom),
-                    "peak_kind": f"{peak_kind} sustained bf16 (cuBLAS, MEASURED_PEAKS.json)",
-                    "share_of_step": stage_ms[dom] / ms}
+            roof = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "traffic": traffic_for(dom),
+                    "peak_kind": f"{peak_kind} burst bf16 (cuBLAS, MEASURED_PEAKS.json); sustained {peak_sus}",
+                    "frac_of_sustained": achieved / peak_sus, "share_of_step": stage_ms[dom] / ms}
+    scans = {}
+    for st_name, nbytes in scan_bytes(cfg).items():
+        if st_name in stage_ms and stage_ms[st_name] > 0:
+            per_rank = nbytes / (world if sp else 1)
+            gbs = per_rank / (stage_ms[st_name] / 1000.0) / 1e9
+            scans[st_name] = {"GB/s": gbs, "frac_of_hbm": gbs / hbm, "algorithmic_bytes": per_rank}
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong" if sp else "weak",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform q,k,v in [-1,1], gates in [0.9,1])",
-        "config": {"workload": WORKLOAD, **CFG,
+        "vs_baseline": None, "dtype": cfg["dtype"],
+        "data": "synthetic (uniform q,k,v in [-1,1]" + (", gates in [0.9,1])" if cfg["gated"] else ", ungated)"),
+        "config": {"workload": workload, **cfg,
                    "parallelism": (f"sequence chunk ranges over {world} rank(s), NCCL P2P carry chain" if sp
                                    else f"streams (b*h) per rank, {world} rank(s)"),
-                   "l2": "inputs 512 MiB each >> 126 MB L2; no flush"},
+                   "l2": "inputs >= 512 MiB each >> 126 MB L2; no flush" if t * b * h * d >= 2 ** 28 else
+                         "small config: inputs fit in L2 (no flush)"},
         "tflops_algorithmic": tflops, "frac_of_peak": tflops / peak, "frac_of_sustained_peak": tflops / peak_sus,
-        "gpu_launches": launches, "stages_ms": stage_ms, "clocks": ck, "e2e": e2e, "roofline": roof,
+        "gpu_launches": launches, "stages_ms": stage_ms, "scans": scans, "clocks": ck, "e2e": e2e,
+        "roofline": roof,
     }
     if world == 1 and not args.no_cpu:
         try:
             cores = os.cpu_count() or 1
-            v, wall, desc = cpu_sample(cores)
+            v, wall, desc = cpu_sample(cfg, cores)
             line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": desc,
                                     "sample_seconds": wall}
         except Exception as exc:  # the CPU leg must not sink the GPU number
@@ -404,6 +468,19 @@ def traffic_for(stage: str):
         return None
 
 
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: re-launch under torch.distributed.run
+    with one process per GPU (rendezvous on 127.0.0.1)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -412,10 +489,13 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "sp1m"],
-                    help="cfg2: BASELINE configs[1] (default, streams sharded over ranks); "
-                         "sp1m: configs[3], one 1M-token sequence split over the ranks")
+    ap.add_argument("--workload", default="auto", choices=["auto", *WORKLOADS, "lm124m"],
+                    help="auto: cfg2 (BASELINE configs[1]) on one GPU, sp1m (configs[3], one 1M-token sequence "
+                         "split over the ranks) on several; cfg1 / cfg3: configs[0] / configs[2]; lm124m: "
+                         "configs[4], the 12-layer 124M power-attention LM, data parallel")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -28,6 +28,7 @@ import numpy as np
 
 __all__ = [
     "ndmi_table",
+    "expansion_table",
     "feature_dim",
     "phi",
     "phi_vjp",
@@ -94,6 +95,42 @@ def ndmi_table(p: int, d: int):
     idx.setflags(write=False)
     w.setflags(write=False)
     return idx, w
+
+
+def expansion_table(kind: str, p: int, d: int, d_tile=None):
+    """(idx, w) of the three expansion kinds (expansions.py:171-198):
+    spow = ndmi_table; tpow = every ordered tuple, first index slowest
+    (_cartesian_indices 166-168), weight 1; tspow = for each NDMI over the
+    d/d_tile tiles (weight w_T) the dense d_tile^p block of tile offsets, every
+    entry weighted w_T (188-194)."""
+    if kind == "spow":
+        return ndmi_table(p, d)
+    if kind == "tpow":
+        idx = np.indices((d,) * p).reshape(p, -1).T.astype(np.int32)
+        return idx, np.ones(idx.shape[0])
+    tiles, tw = ndmi_table(p, d // d_tile)
+    offs = np.indices((d_tile,) * p).reshape(p, -1).T
+    idx = (tiles[:, None, :].astype(np.int64) * d_tile + offs[None]).reshape(-1, p).astype(np.int32)
+    return idx, np.repeat(tw, d_tile ** p)
+
+
+def table_update_state(k, v, decay, idx, w):
+    """update_state with an explicit monomial table (_reference.py:16-33):
+    state[s] = sum_j decay_j phi(k_j) (x) v_j, key_sum[s] = sum_j decay_j phi(k_j)."""
+    ph = np.take(k, idx[:, 0], axis=-1) * w
+    for z in range(1, idx.shape[1]):
+        ph = ph * np.take(k, idx[:, z], axis=-1)
+    if decay is not None:
+        ph = ph * decay[..., None]
+    return np.einsum("scf,sce->sfe", ph, v), ph.sum(axis=1)
+
+
+def table_query_state(q, state, key_sum, idx, w):
+    """query_state with an explicit table (_reference.py:36-50)."""
+    ph = np.take(q, idx[:, 0], axis=-1) * w
+    for z in range(1, idx.shape[1]):
+        ph = ph * np.take(q, idx[:, z], axis=-1)
+    return np.einsum("scf,sfe->sce", ph, state), np.einsum("scf,sf->sc", ph, key_sum)
 
 
 def phi(x: np.ndarray, p: int) -> np.ndarray:

@@ -68,6 +68,31 @@ def _peer(group, rank: int) -> int:
     return rank if group is None else dist.get_global_rank(group, rank)
 
 
+def _host_staged(group) -> bool:
+    """gloo moves CPU tensors only: carries are staged through host memory."""
+    import torch.distributed as dist
+
+    return dist.get_backend(group) == "gloo"
+
+
+def _send(x: torch.Tensor, dst: int, group) -> None:
+    import torch.distributed as dist
+
+    dist.send(x.cpu() if (x.is_cuda and _host_staged(group)) else x, dst=dst, group=group)
+
+
+def _recv(like: torch.Tensor, src: int, group) -> torch.Tensor:
+    import torch.distributed as dist
+
+    if like.is_cuda and _host_staged(group):
+        buf = torch.empty(like.shape, dtype=like.dtype)
+        dist.recv(buf, src=src, group=group)
+        return buf.to(like.device)
+    buf = torch.empty_like(like)
+    dist.recv(buf, src=src, group=group)
+    return buf
+
+
 def chain_forward(local: torch.Tensor, combine: Callable[[Optional[torch.Tensor], torch.Tensor], torch.Tensor],
                   rank: int, world: int, group=None) -> Optional[torch.Tensor]:
     """Exclusive left-to-right scan of the per-rank local results over ranks.
@@ -78,10 +103,9 @@ def chain_forward(local: torch.Tensor, combine: Callable[[Optional[torch.Tensor]
 
     carry = None
     if rank > 0:
-        carry = torch.empty_like(local)
-        dist.recv(carry, src=_peer(group, rank - 1), group=group)
+        carry = _recv(local, _peer(group, rank - 1), group)
     if rank < world - 1:
-        dist.send(combine(carry, local).contiguous(), dst=_peer(group, rank + 1), group=group)
+        _send(combine(carry, local).contiguous(), _peer(group, rank + 1), group)
     return carry
 
 
@@ -92,10 +116,9 @@ def chain_backward(local: torch.Tensor, combine: Callable[[Optional[torch.Tensor
 
     carry = None
     if rank < world - 1:
-        carry = torch.empty_like(local)
-        dist.recv(carry, src=_peer(group, rank + 1), group=group)
+        carry = _recv(local, _peer(group, rank + 1), group)
     if rank > 0:
-        dist.send(combine(carry, local).contiguous(), dst=_peer(group, rank - 1), group=group)
+        _send(combine(carry, local).contiguous(), _peer(group, rank - 1), group)
     return carry
 
 

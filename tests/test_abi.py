@@ -9,7 +9,7 @@ import re
 import numpy as np
 import pytest
 
-from conftest import ROOT
+from conftest import ROOT, golden_names, load_golden
 from oracle import power_oracle as O
 
 P = pytest.importorskip("paper_2507_04239_b200")
@@ -43,7 +43,8 @@ def test_feature_table_matches_reference_order(p, d):
 
 
 def _problem(**kw):
-    base = dict(b=1, t=64, h=2, d=16, e=16, p=2, chunk=16, scale=0.0, normalize=0, dtype=0, gated=1)
+    base = dict(b=1, t=64, h=2, d=16, e=16, p=2, chunk=16, normalize=0, dtype=0, gated=1, has_scale=0, flags=0,
+                scale=0.0)
     base.update(kw)
     return _lib.PaProblem(**base)
 
@@ -95,3 +96,32 @@ def test_logspace_entry_validates_before_launch():
     assert rc == 2                                               # ShapeMismatch
     rc = lib.pa_power_logspace_fwd(ctypes.byref(_problem(dtype=1)), 1e-12, *args)
     assert rc == 4 and b"f32 or f64" in lib.pa_last_error()      # bf16 unsupported here
+
+
+@pytest.mark.parametrize("name", golden_names("kinds_"))
+def test_library_expansion_tables_match_reference(name):
+    """pa_expansion_table / pa_expansion_dim (host-side, no GPU) against the
+    reference's monomial_table for SPOW, TPOW and TSPOW."""
+    g = load_golden(name)
+    spec = P.ExpansionSpec(str(g["kind"]), int(g["p"]), int(g["d"]), int(g["d_tile"]) or None)
+    idx, w = P.monomial_table(spec)
+    assert P.expansion_dim(spec) == int(g["D"]) == idx.shape[0]
+    assert (idx == g["idx"]).all()
+    np.testing.assert_allclose(w, g["w"], rtol=1e-15)
+    assert _lib.load().pa_expansion_dim(spec.code, spec.p, spec.d, spec.d_tile or 0) == int(g["D"])
+
+
+def test_route_and_strict_flag():
+    """pa_uses_tensor_cores: tcgen05 for the north-star shape, fp32 kernels
+    otherwise; PA_FLAG_STRICT_TC makes a 16-bit problem outside the tensor-core
+    shapes an error; invalid problems report make_geo's own error code."""
+    lib = _lib.load()
+    tc = _problem(t=2048, d=64, e=64, chunk=1024, dtype=1)
+    assert lib.pa_uses_tensor_cores(ctypes.byref(tc)) == 1
+    off = _problem(t=1000, d=64, e=64, chunk=256, dtype=1)
+    assert lib.pa_uses_tensor_cores(ctypes.byref(off)) == 0
+    off.flags = _lib.PA_FLAG_STRICT_TC
+    assert lib.pa_uses_tensor_cores(ctypes.byref(off)) == -4
+    assert lib.pa_fwd_workspace_bytes(ctypes.byref(off)) == 0
+    assert lib.pa_uses_tensor_cores(ctypes.byref(_problem(dtype=0, flags=_lib.PA_FLAG_STRICT_TC))) == 0
+    assert lib.pa_uses_tensor_cores(ctypes.byref(_problem(p=3, normalize=1))) == -6

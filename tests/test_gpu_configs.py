@@ -1,0 +1,193 @@
+"""Oracle parity at the BASELINE configs' own shapes, on the GPU.
+
+* configs[1] geometry (b=4, h=16, c=1024, bf16) on a t=4096 slice: the
+  tensor-core backward at b>1 and h=16, every stream computed on the GPU and
+  a spread of streams checked against the oracle.
+* full-length t=65536, c=1024 streams with the state path made visible:
+  gates in [0.999, 1] (chunk decay ~e^-0.5 instead of e^-53) and ungated +
+  normalized, so the 64-chunk fp16 scaled-state scan, the state query and the
+  state VJP all carry O(1) weight in the outputs.
+* configs[2]'s shape (p=4, d=32, c=1024, ungated, normalized) on a t=2048 slice.
+* the sequence-parallel protocol at 8 ranks over 32 chunks, ungated-normalized.
+
+Tolerances are the north star's (bf16 mode 2e-2 with the reference metric
+max_rel_error, checks.py:26-31) against the float64 oracle on the same
+bf16-representable inputs; each case prints its errors.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import power_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2507_04239_b200")
+
+BF16_TOL = 2e-2
+
+
+def _bf16_exact(*xs):
+    return [torch.tensor(x).bfloat16().double().numpy() for x in xs]
+
+
+def _gpu_run(q, k, v, g, p, c, normalize, dy, dtype=torch.bfloat16):
+    dev = "cuda"
+    Q, K, V = (torch.tensor(x, device=dev, dtype=dtype, requires_grad=True) for x in (q, k, v))
+    lg = None if g is None else torch.tensor(np.log(g), device=dev, dtype=torch.float32, requires_grad=True)
+    y = P.power_full(Q, K, V, lg, p=p, chunk_size=c, normalize=normalize, check_denominator="sync")
+    ins = [Q, K, V] + ([lg] if lg is not None else [])
+    gr = torch.autograd.grad(y, ins, torch.tensor(dy, device=dev, dtype=dtype))
+    out = {"y": y.detach().double().cpu().numpy(), "dq": gr[0].double().cpu().numpy(),
+           "dk": gr[1].double().cpu().numpy(), "dv": gr[2].double().cpu().numpy()}
+    if lg is not None:
+        out["dlogg"] = gr[3].double().cpu().numpy()
+    return out
+
+
+def _compare(tag, r, q, k, v, g, p, c, normalize, dy, tol=BF16_TOL):
+    y_ref, _ = O.chunked_forward(q, k, v, g, p, c, normalize=normalize)
+    dq, dk, dv, dg = O.chunked_backward(q, k, v, g, p, c, dy, normalize=normalize)
+    errs = {"y": O.max_rel_error(r["y"], y_ref), "dq": O.max_rel_error(r["dq"], dq),
+            "dk": O.max_rel_error(r["dk"], dk), "dv": O.max_rel_error(r["dv"], dv)}
+    if g is not None:
+        errs["dlog_g"] = O.max_rel_error(r["dlogg"], dg * g)
+    print(f"{tag}: max_rel_error {errs}")
+    bad = {kk: e for kk, e in errs.items() if not e <= tol}
+    assert not bad, (tag, bad)
+    return errs
+
+
+def test_config1_geometry_b4_h16_slice():
+    """b=4, h=16, d=64, c=1024, gated bf16 (configs[1] without the length):
+    forward + backward of all 64 streams on the tensor cores, oracle on a spread
+    of (batch, head) streams."""
+    b, t, h, d, c = 4, 4096, 16, 64, 1024
+    q, k, v, g = O.generate_inputs(b, t, h, d, d, seed=21, gating=True)
+    q, k, v = _bf16_exact(q, k, v)
+    dy, = _bf16_exact(np.random.default_rng(22).uniform(-1, 1, (b, t, h, d)))
+    r = _gpu_run(q, k, v, g, 2, c, False, dy)
+    for bi, hi in ((0, 0), (1, 7), (2, 13), (3, 15)):
+        sl = (slice(bi, bi + 1), slice(None), slice(hi, hi + 1))
+        sub = {kk: x[sl] for kk, x in r.items()}
+        _compare(f"b={bi} h={hi}", sub, q[sl], k[sl], v[sl], g[sl], 2, c, False, dy[sl])
+
+
+@pytest.mark.parametrize("case", ["gates_0.999", "ungated_normalized"])
+def test_full_length_65536_state_path_visible(case):
+    """One full t=65536, c=1024 stream against the oracle with the inter-chunk
+    state path carrying real weight (64 chunks of fp16 scaled states)."""
+    t, d, c = 65536, 64, 1024
+    rng = np.random.default_rng(31)
+    q, k, v = (rng.uniform(-1, 1, (1, t, 1, d)) for _ in range(3))
+    q, k, v = _bf16_exact(q, k, v)
+    dy, = _bf16_exact(rng.uniform(-1, 1, (1, t, 1, d)))
+    if case == "gates_0.999":
+        g, normalize = rng.uniform(0.999, 1.0, (1, t, 1)), False
+        # the decay of one chunk is ~e^-0.5: 64 chunks of history still matter
+        assert np.exp(np.log(g[0, :c, 0]).sum()) > 0.5
+    else:
+        g, normalize = None, True
+    r = _gpu_run(q, k, v, g, 2, c, normalize, dy)
+    _compare(case, r, q, k, v, g, 2, c, normalize, dy)
+
+
+def test_config2_shape_p4_d32_c1024_slice():
+    """configs[2] shape: SPOW p=4, d=32 (D=52360), c=1024, ungated, normalized,
+    on a t=2048 slice (the elementwise bar)."""
+    t, d, c = 2048, 32, 1024
+    q, k, v, _ = O.generate_inputs(1, t, 1, d, d, seed=41, gating=False)
+    q, k, v = _bf16_exact(q, k, v)
+    dy, = _bf16_exact(np.random.default_rng(42).uniform(-1, 1, (1, t, 1, d)))
+    r = _gpu_run(q, k, v, None, 4, c, True, dy)
+    _compare("p=4 d=32 c=1024", r, q, k, v, None, 4, c, True, dy)
+
+
+def test_sequence_parallel_8_ranks_32_chunks():
+    """The sequence-parallel protocol (emulated ranks, carries in memory) at 8
+    ranks over 32 chunks, ungated + normalized: against power_full (1e-2) and
+    the oracle (2e-2)."""
+    b, t, h, d, c = 1, 4096, 2, 64, 128
+    q, k, v, _ = O.generate_inputs(b, t, h, d, d, seed=51, gating=False)
+    q, k, v = _bf16_exact(q, k, v)
+    dy, = _bf16_exact(np.random.default_rng(52).uniform(-1, 1, (b, t, h, d)))
+    Q, K, V = (torch.tensor(x, device="cuda", dtype=torch.bfloat16) for x in (q, k, v))
+    dY = torch.tensor(dy, device="cuda", dtype=torch.bfloat16)
+    y, dq, dk, dv, _ = P.parallel.emulate_ranks(Q, K, V, None, ranks=8, p=2, chunk_size=c, normalize=True, dy=dY)
+    r = {"y": y.double().cpu().numpy(), "dq": dq.double().cpu().numpy(), "dk": dk.double().cpu().numpy(),
+         "dv": dv.double().cpu().numpy()}
+    full = _gpu_run(q, k, v, None, 2, c, True, dy)
+    for kk in ("y", "dq", "dk", "dv"):
+        assert O.max_rel_error(r[kk], full[kk]) <= 1e-2, kk
+    _compare("sp 8 ranks", r, q, k, v, None, 2, c, True, dy)
+
+
+@pytest.mark.parametrize("normalize", [False, True])
+def test_deterministic_mode_bit_identical(normalize):
+    """deterministic=True: one MMA issuer per accumulator, so two runs give
+    bit-identical outputs and gradients on the tensor-core path."""
+    torch.manual_seed(3)
+    b, t, h, d, c = 1, 4096, 4, 64, 1024
+    Q, K, V = ((torch.rand(b, t, h, d, device="cuda") * 2 - 1).bfloat16().requires_grad_() for _ in range(3))
+    lg = torch.log(torch.rand(b, t, h, device="cuda") * 0.1 + 0.9).requires_grad_()
+    dY = (torch.rand(b, t, h, d, device="cuda") * 2 - 1).bfloat16()
+
+    def run():
+        y = P.power_full(Q, K, V, lg, p=2, chunk_size=c, normalize=normalize, deterministic=True)
+        return [y.detach().clone()] + list(torch.autograd.grad(y, [Q, K, V, lg], dY))
+
+    a, b_ = run(), run()
+    for name, x, z in zip(("y", "dq", "dk", "dv", "dlog_g"), a, b_):
+        assert torch.equal(x, z), name
+
+
+@pytest.mark.parametrize("name", [n for n in __import__("conftest").golden_names("kinds_")])
+def test_expansion_kind_operators_match_reference(name):
+    """update_state_kernel / query_state_kernel with TPOW / TSPOW / SPOW tables
+    (f64, table-driven kernels) against the reference fixtures."""
+    from conftest import load_golden
+
+    g = load_golden(name)
+    spec = P.ExpansionSpec(str(g["kind"]), int(g["p"]), int(g["d"]), int(g["d_tile"]) or None)
+    st, ks = P.update_state_kernel(g["k"], g["v"], g["decay"], spec)
+    np.testing.assert_allclose(st, g["state"], rtol=1e-12, atol=1e-13)
+    np.testing.assert_allclose(ks, g["key_sum"], rtol=1e-12, atol=1e-13)
+    y, den = P.query_state_kernel(g["q"], g["state"], g["key_sum"], spec)
+    np.testing.assert_allclose(y, g["y"], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(den, g["denom"], rtol=1e-12, atol=1e-12)
+
+
+def test_expansion_kinds_give_the_same_attention():
+    """<phi(x), phi(y)> = (x.y)^p for every kind (reference expansions.py:3-5):
+    chunked_power_attention with a TSPOW or TPOW spec equals the SPOW result."""
+    q, k, v, g = O.generate_inputs(1, 96, 2, 8, 8, seed=61, gating=True)
+    batch = P.SequenceBatch(q, k, v, g)
+    outs = []
+    for spec in (P.ExpansionSpec.spow(2, 8), P.ExpansionSpec.tpow(2, 8), P.ExpansionSpec.tspow(2, 8, 4)):
+        cfg = P.AttentionConfig.power(spec, normalize=True)
+        outs.append(P.chunked_power_attention(batch, cfg, P.ChunkPlan(96, 32)).y)
+    y_ref, _ = O.chunked_forward(q, k, v, g, 2, 32, normalize=True)
+    for y in outs:
+        assert O.max_rel_error(y, y_ref) <= 1e-4
+
+
+def test_zero_denominator_sync_and_deferred():
+    q = torch.zeros(1, 4, 1, 2, device="cuda")
+    with pytest.raises(P.ZeroDenominator):
+        P.power_full(q, q, q, None, p=2, chunk_size=2, normalize=True, check_denominator="sync")
+    # deferred: the forward returns; the error surfaces on the next check
+    P.power_full(q, q, q, None, p=2, chunk_size=2, normalize=True)
+    with pytest.raises(P.ZeroDenominator):
+        P.power.check_denominators()
+    ok = torch.ones(1, 4, 1, 2, device="cuda")
+    P.power_full(ok, ok, ok, None, p=2, chunk_size=2, normalize=True)
+    P.power.check_denominators()
+
+
+def test_fallback_warns_and_strict_raises():
+    x = torch.rand(1, 1000, 1, 64, device="cuda").bfloat16()
+    with pytest.warns(RuntimeWarning, match="fp32 CUDA-core"):
+        P.power_full(x, x, x, None, p=2, chunk_size=256)
+    with pytest.raises(P.InvalidSpec, match="strict"):
+        P.power_full(x, x, x, None, p=2, chunk_size=256, strict=True)

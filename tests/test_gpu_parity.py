@@ -144,7 +144,7 @@ def test_reference_named_shims_and_worked_examples():
 def test_zero_denominator_raises():
     q = torch.zeros(1, 4, 1, 2, device="cuda")
     with pytest.raises(P.ZeroDenominator):
-        P.power_full(q, q, q, None, p=2, chunk_size=2, normalize=True)
+        P.power_full(q, q, q, None, p=2, chunk_size=2, normalize=True, check_denominator="sync")
 
 
 def test_vjp_chunked_shim_matches_reference():

@@ -89,3 +89,20 @@ def test_log_gate_surface():
     _, _, _, dlg = O.power_full_vjp(q, k, v, np.log(g), dy, p=2, chunk_size=5)
     _, _, _, dg = O.chunked_backward(q, k, v, g, 2, 5, dy)
     assert O.max_rel_error(dlg, dg * g) < 1e-14
+
+
+@pytest.mark.parametrize("name", golden_names("kinds_"))
+def test_expansion_kinds_match_reference(name):
+    """TPOW / TSPOW / SPOW tables and the table-driven update/query restatements
+    against reference-generated fixtures (make_golden_kinds.py)."""
+    g = load_golden(name)
+    kind, p, d, dt = str(g["kind"]), int(g["p"]), int(g["d"]), int(g["d_tile"]) or None
+    idx, w = O.expansion_table(kind, p, d, dt)
+    assert (idx == g["idx"]).all() and idx.shape[0] == int(g["D"])
+    np.testing.assert_allclose(w, g["w"], rtol=1e-15)
+    st, ks = O.table_update_state(g["k"], g["v"], g["decay"], idx, w)
+    np.testing.assert_allclose(st, g["state"], rtol=1e-12, atol=1e-13)
+    np.testing.assert_allclose(ks, g["key_sum"], rtol=1e-12, atol=1e-13)
+    y, den = O.table_query_state(g["q"], g["state"], g["key_sum"], idx, w)
+    np.testing.assert_allclose(y, g["y"], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(den, g["denom"], rtol=1e-12, atol=1e-12)

@@ -85,6 +85,38 @@ def test_sp_carry_chains_gloo(world):
     mp.spawn(_worker, args=(world, _free_port(), 6 * world), nprocs=world, join=True)
 
 
+def _subgroup_worker(rank, world, port):
+    """A chain over the subgroup {1, 2} of a 3-process job (rank 0 is not in
+    it): the group ranks must map to the right global peers."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2507_04239_b200.parallel import chain_backward, chain_forward
+
+        grp = dist.new_group([1, 2])
+        if rank == 0:
+            return
+        gr = dist.get_rank(grp)
+        local = torch.full((4,), float(10 * rank))
+
+        def combine(carry, loc):
+            return loc if carry is None else 0.5 * carry + loc
+
+        carry = chain_forward(local, combine, gr, 2, grp)
+        back = chain_backward(local, combine, gr, 2, grp)
+        if gr == 0:
+            assert carry is None and torch.equal(back, torch.full((4,), 20.0))
+        else:
+            assert torch.equal(carry, torch.full((4,), 10.0)) and back is None
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sp_chain_on_subgroup_without_rank0():
+    mp.spawn(_subgroup_worker, args=(3, _free_port()), nprocs=3, join=True)
+
+
 def test_sp_partition_math_cpu():
     from paper_2507_04239_b200.parallel import SpPartition
 
