@@ -253,9 +253,7 @@ def run_gpu(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     name = pick_workload(args, world)
     if name == "lm124m":
-        import lm_bench
-
-        return lm_bench.run(args, world, rank, local)
+        return run_lm(args, world, rank, local)
     cfg, workload = WORKLOADS[name]
     sp = name == "sp1m"
     torch.cuda.set_device(local)
@@ -442,6 +440,121 @@ def run_gpu(args):
                                     "sample_seconds": wall}
         except Exception as exc:  # the CPU leg must not sink the GPU number
             line["cpu_baseline"] = {"value": None, "error": repr(exc)}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+LM_WORKLOAD = ("configs[4]: 12-layer 124M power-attention LM (width 768, 12 heads d=64, MLP x4, tied 50257 "
+               "embedding) fwd+bwd+AdamW, bf16 autocast, p=2 chunk=1024 gated, 32768-token sequence per GPU, "
+               "data parallel (DDP bucketed NCCL all-reduce)")
+
+
+def run_lm(args, world, rank, local):
+    """configs[4]: one training step = forward + loss + backward (DDP all-reduce
+    overlapped) + fused AdamW over one 32768-token sequence per GPU."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_04239_b200 import _lib
+    from paper_2507_04239_b200.lm import LMConfig, PowerLM, attention_flops, train_step, weight_flops
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    torch.manual_seed(0)
+    cfg = LMConfig()
+    t = 32768
+    model = PowerLM(cfg).to(dev)
+    net = model
+    if world > 1:
+        net = torch.nn.parallel.DistributedDataParallel(model, device_ids=[local], bucket_cap_mb=25,
+                                                        gradient_as_bucket_view=True)
+    opt = torch.optim.AdamW(model.parameters(), lr=3e-4, fused=True)
+    g = torch.Generator(device=dev).manual_seed(100 + rank)
+    tokens = torch.randint(0, cfg.vocab, (1, t + 1), device=dev, generator=g)
+    x, y = tokens[:, :-1], tokens[:, 1:]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    clocks = Clocks(local)
+    clocks.start()
+    for _ in range(args.warmup):
+        train_step(net, opt, x, y)
+    barrier()
+    clocks.mark()
+    _lib.profile_reset()
+    _lib.profile_enable(True)
+    n0 = _lib.launch_count()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        loss = train_step(net, opt, x, y)
+    e1.record()
+    barrier()
+    launches = _lib.launch_count() - n0
+    _lib.profile_enable(False)
+    stages = _lib.profile_read()
+    ck = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    attn_ms = sum(v[0] for v in stages.values()) / args.steps
+
+    # e2e: token ids from pinned host memory every step, the loss read back every step
+    e2e = None
+    if not args.no_e2e:
+        host = tokens.cpu().pin_memory()
+        dbuf = torch.empty_like(tokens)
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        ne = max(3, args.steps)
+        for _ in range(ne):
+            dbuf.copy_(host, non_blocking=True)
+            lv = train_step(net, opt, dbuf[:, :-1], dbuf[:, 1:]).item()
+        f1.record()
+        barrier()
+        ems = f0.elapsed_time(f1) / ne
+        if world > 1:
+            tt = torch.tensor([ems], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt.item())
+        e2e = {"value": world * t / (ems / 1000.0), "unit": "tokens/s",
+               "h2d_bytes_per_step": host.numel() * host.element_size(), "d2h_bytes_per_step": 4,
+               "ms_per_step": ems, "loss": lv}
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    peak, peak_sus, hbm, peak_kind = load_peaks()
+    af = attention_flops(cfg, t)
+    wf = weight_flops(cfg, t)
+    tflops = world * (af + wf) / (ms / 1000.0) / 1e12
+    attn_tflops = af / (attn_ms / 1000.0) / 1e12 if attn_ms > 0 else None
+    line = {
+        "metric": "LM training tokens/sec (configs[4]), whole job", "value": world * t / (ms / 1000.0),
+        "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic uniform token ids, random-init weights",
+        "config": {"workload": LM_WORKLOAD, "model": "power-attention GPT-2-small geometry", "global_batch": world,
+                   "seq_len": t, "parallelism": f"dp{world}",
+                   "params": sum(p.numel() for p in model.parameters())},
+        "tflops_algorithmic": tflops, "frac_of_peak": tflops / peak,
+        "attention": {"ms_per_step": attn_ms, "share_of_step": attn_ms / ms, "tflops_algorithmic": attn_tflops,
+                      "frac_of_peak": attn_tflops / peak if attn_tflops else None,
+                      "flops_share": af / (af + wf),
+                      "stages_ms": {k: v[0] / args.steps for k, v in stages.items()}},
+        "dense_layers": "torch nn.Linear / cuBLAS (outside the power-attention path)",
+        "gpu_launches": launches, "clocks": ck, "e2e": e2e, "loss": float(loss),
+    }
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
