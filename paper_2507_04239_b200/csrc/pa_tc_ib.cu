@@ -385,8 +385,13 @@ __global__ void __launch_bounds__(ib2::THREADS, 2) k_tc_ib(const __grid_constant
       tc_wait_ld();
       put(out_a, 2.f);   // dK
     }
+    // the two column-half warps of a row combine in shared memory (the drained
+    // operand tiles) so each token gets one addition per kernel: a fixed order
+    float* rsum_s = (float*)smem + 8 * (32 * 36);
     const float rr = red.x + red.y;
-    if (g.gated) atomicAdd(dell + tokr, kKV ? -rr : rr);
+    if (grp == 1) rsum_s[row] = rr;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    if (grp == 0 && g.gated) atomicAdd(dell + tokr, kKV ? -(rr + rsum_s[row]) : rr + rsum_s[row]);
   }
   tc_fence_before();
   __syncthreads();

@@ -495,7 +495,10 @@ __global__ void __launch_bounds__(zv::THREADS, 1)
         }
       }
       PA_TR6(trc && it == 2 && tid == W_EPI * 32, 2);
-      // the operand words of tile it+2 (its buffer was released at the end of tile it)
+      // the operand words of tile it+2 go into the buffer the eight epilogue warps
+      // just staged tile it's rows through, and prepare() writes every warp's part
+      // of it: all staging reads must be done first
+      asm volatile("bar.sync 1, 256;" ::: "memory");
       if (ti + 2 * (int)gridDim.x < ntiles) prepare(it + 2, ti + 2 * gridDim.x);
     }
   }
