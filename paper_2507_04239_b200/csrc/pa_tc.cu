@@ -829,9 +829,9 @@ struct TcBwdWs {
   __half* dN16;          // dnum (fp16, state GEMMs)
   __half* dD;            // (dden, 0..) fp16
   float* dden;
-  float* dq32;
-  float* dk32;
-  float* dv32;
+  float* dq32;           // intra-chunk dq (fp32, reduce-added)
+  __nv_bfloat16* dk16;   // intra-chunk dk, dv (bf16)
+  __nv_bfloat16* dv16;
   float* dell;
   float* cu;
   float* dlam;
@@ -876,8 +876,8 @@ static TcBwdWs carve_bwd(const Geo& g, void* base, size_t* bytes) {
   b.dD = (__half*)take(2ull * g.ns * g.t * 16);
   b.dden = (float*)take(4ull * g.ns * g.t);
   b.dq32 = (float*)take(4ull * g.ns * g.t * HD);
-  b.dk32 = (float*)take(4ull * g.ns * g.t * HD);
-  b.dv32 = (float*)take(4ull * g.ns * g.t * HD);
+  b.dk16 = (__nv_bfloat16*)take(2ull * g.ns * g.t * HD);
+  b.dv16 = (__nv_bfloat16*)take(2ull * g.ns * g.t * HD);
   b.dell = (float*)take(4ull * g.ns * g.t);
   b.cu = (float*)take(4ull * g.ns * g.t);
   b.dlam = (float*)take(4ull * g.ns * g.n * scan_blocks(UW));   // per-block dlambda partials
@@ -926,14 +926,15 @@ static EncodeTiledFn encode_fn() {
 }
 
 static bool encode(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
-                   const cuuint32_t* box, CUtensorMapSwizzle sw) {
+                   const cuuint32_t* box, CUtensorMapSwizzle sw,
+                   CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16) {
   cuuint32_t es[5] = {1, 1, 1, 1, 1};
   EncodeTiledFn fn = encode_fn();
   if (!fn) {
     set_error("cuTensorMapEncodeTiled: driver entry point unavailable");
     return false;
   }
-  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), dims, strides, box, es,
+  const CUresult r = fn(m, dt, rank, const_cast<void*>(ptr), dims, strides, box, es,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -958,6 +959,16 @@ static bool map_2d(CUtensorMap* m, const void* ptr, size_t rows, int cols, int b
   cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
   cuuint32_t box[2] = {(cuuint32_t)bc, (cuuint32_t)br};
   return encode(m, ptr, 2, dims, strides, box, sw);
+}
+bool tc_map_bth(CUtensorMap* m, const void* ptr, const Geo& g, int box_tokens) {
+  return map_bth(m, ptr, g, box_tokens);
+}
+bool tc_map_2d(CUtensorMap* m, const void* ptr, size_t rows, int cols, int bc, int br, int fp32) {
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * (fp32 ? 4 : 2)};
+  cuuint32_t box[2] = {(cuuint32_t)bc, (cuuint32_t)br};
+  return encode(m, ptr, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B,
+                fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16);
 }
 
 // The driver-API tensor-map encoder needs the device's primary context to be
@@ -1081,9 +1092,13 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
     cudaFuncSetAttribute(k_tc_scan_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, red_bytes);
   auto launch_intra = [&]() -> int {
     StageTimer tmr("bwd_intra", st);
-    CUtensorMap m_q128, m_k128, m_dy128;
-    if (!map_bth(&m_q128, q, g, 128) || !map_bth(&m_k128, k, g, 128) || !map_bth(&m_dy128, dy, g, 128)) return 3;
-    tc_intra_bwd(g, m_q128, m_k128, m_v128, m_dy128, w.ell, b.dden, rowsum, b.dk32, b.dv32, b.dq32, b.dell, st);
+    if (tc_intra_bwd_fused(g, q, k, v, dy, w.ell, b.dden, rowsum, b.dk16, b.dv16, b.dq32, b.dell, st)) return 3;
+    if (g.det) {
+      // fixed-order dQ: the query-side pass (the fused kernel skipped its reduce-adds)
+      CUtensorMap m_q128, m_k128, m_dy128;
+      if (!map_bth(&m_q128, q, g, 128) || !map_bth(&m_k128, k, g, 128) || !map_bth(&m_dy128, dy, g, 128)) return 3;
+      tc_intra_bwd_q(g, m_q128, m_k128, m_v128, m_dy128, w.ell, b.dden, rowsum, b.dq32, b.dell, st);
+    }
     return 0;
   };
   if (mode != 2) {
@@ -1133,7 +1148,7 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
   }
   {
     StageTimer tmr("bwd_update_state", st);
-    tc_zvjp(g, true, 1, v, nullptr, k, w.ell, w.lamlog, b.eg, b.dk32, b.dv32, b.dell, b.cu, dk, dv, st);
+    tc_zvjp(g, true, 1, v, nullptr, k, w.ell, w.lamlog, b.eg, b.dk16, b.dv16, b.dell, b.cu, dk, dv, st);
   }
   {
     StageTimer tmr("bwd_finish", st);

@@ -31,15 +31,28 @@ int tc_out(const Geo& g, const CUtensorMap& m_q, const CUtensorMap& m_k, const C
            const float* ell, const __half* st_main, const __half* st_den, int with_den, void* y, float* rowsum,
            float* y32, int* zflag, cudaStream_t st);
 
-// intra-chunk backward (pa_tc_ib.cu): dK, dV (fp32, =), dQ (fp32, =), dell (+=); m_dn maps dy
-// (normalization is applied in fp32 from dden and the forward rowsum)
-int tc_intra_bwd(const Geo& g, const CUtensorMap& m_q, const CUtensorMap& m_k, const CUtensorMap& m_v,
-                 const CUtensorMap& m_dn, const float* ell, const float* dden, const float* rsum, float* dk32,
-                 float* dv32, float* dq32, float* dell, cudaStream_t st);
+// TMA maps: [b][t][h][64] bf16 with a box of `box_tokens` tokens of one stream;
+// row-major [rows][cols] bf16 (fp32 = 0) or fp32 (fp32 = 1) with a bc x br box, SW128
+bool tc_map_bth(CUtensorMap* m, const void* ptr, const Geo& g, int box_tokens);
+bool tc_map_2d(CUtensorMap* m, const void* ptr, size_t rows, int cols, int bc, int br, int fp32);
+
+// intra-chunk backward in one pass (pa_tc_intra_bwd.cu): dK, dV as bf16 rows
+// [ns*t][64], dQ reduce-added into a zeroed fp32 [ns*t][64] (deterministic
+// mode: the query side runs as tc_intra_bwd_q instead).  Normalization is
+// applied in fp32 from dden and the forward rowsum.  Log-gate cotangents:
+// dell += (zeroed by the caller).
+int tc_intra_bwd_fused(const Geo& g, const void* q, const void* k, const void* v, const void* dy, const float* ell,
+                       const float* dden, const float* rsum, __nv_bfloat16* dk16, __nv_bfloat16* dv16, float* dq32,
+                       float* dell, cudaStream_t st);
+// query side alone (pa_tc_ib.cu; fixed accumulation order): dq32 (=), the
+// query-side log-gate cotangents (dell +=, one addition per token)
+int tc_intra_bwd_q(const Geo& g, const CUtensorMap& m_q, const CUtensorMap& m_k, const CUtensorMap& m_v,
+                   const CUtensorMap& m_dn, const float* ell, const float* dden, const float* rsum, float* dq32,
+                   float* dell, cudaStream_t st);
 
 // expanded-state VJP GEMMs (pa_tc_zvjp.cu): E = expanded A'_{k-1} (query side) or dS~_k (update side)
 int tc_zvjp(const Geo& g, bool upd, int u_bf16_bth, const void* u_rows, const __half* u16, const void* xraw,
-            const float* ell, const float* lamlog, const __half* E, const float* dx32, const float* dv32,
+            const float* ell, const float* lamlog, const __half* E, const void* dx32, const void* dv32,
             float* dell, float* dellend, void* dxo, void* dvo, cudaStream_t st);
 
 }  // namespace pa

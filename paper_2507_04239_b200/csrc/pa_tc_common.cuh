@@ -128,3 +128,27 @@ __device__ __forceinline__ void evjp_fblock(const float (&x)[64], float (&dx)[64
 
 }  // namespace tc
 }  // namespace pa
+
+namespace pa {
+namespace tc {
+// packed fp32 pairs (FMUL2 / FADD2 / FFMA2 on sm_100a)
+struct f2v {
+  float x, y;
+};
+__device__ __forceinline__ f2v mul2v(f2v a, f2v b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(*(uint64_t*)&a), "l"(*(uint64_t*)&b));
+  return *(f2v*)&r;
+}
+__device__ __forceinline__ f2v fma2v(f2v a, f2v b, f2v c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(*(uint64_t*)&a), "l"(*(uint64_t*)&b), "l"(*(uint64_t*)&c));
+  return *(f2v*)&r;
+}
+__device__ __forceinline__ f2v add2v(f2v a, f2v b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(*(uint64_t*)&a), "l"(*(uint64_t*)&b));
+  return *(f2v*)&r;
+}
+}  // namespace tc
+}  // namespace pa

@@ -1,5 +1,8 @@
 // Intra-chunk backward on tcgen05 (reference gradients.py:98-176, power branch,
-// with the pairwise-decay chain rule 79-95 taken in log space).
+// with the pairwise-decay chain rule 79-95 taken in log space) -- the
+// two-kernel form.  Only its query side is launched: in deterministic mode
+// (PA_FLAG_DETERMINISTIC) it computes dQ with a fixed summation order, next to
+// the one-pass kernel of pa_tc_intra_bwd.cu running without its dQ reduce-adds.
 //
 // Per chunk, with s = q.k (raw), E_ij = exp(ell_i - ell_j) for j <= i:
 //   P = sigma^2 E s^2,   dP' = dnum.v + dden,   dS = 2 sigma^2 E dP' s
@@ -391,24 +394,22 @@ __global__ void __launch_bounds__(ib2::THREADS, 2) k_tc_ib(const __grid_constant
     const float rr = red.x + red.y;
     if (grp == 1) rsum_s[row] = rr;
     asm volatile("bar.sync 1, 256;" ::: "memory");
-    if (grp == 0 && g.gated) atomicAdd(dell + tokr, kKV ? -(rr + rsum_s[row]) : rr + rsum_s[row]);
+    if (grp == 0 && g.gated && dell) atomicAdd(dell + tokr, kKV ? -(rr + rsum_s[row]) : rr + rsum_s[row]);
   }
   tc_fence_before();
   __syncthreads();
   if (w == W_TMEM) tmem_dealloc<256>(tm);
 }
 
-int tc_intra_bwd(const Geo& g, const CUtensorMap& m_q, const CUtensorMap& m_k, const CUtensorMap& m_v,
-                 const CUtensorMap& m_dn, const float* ell, const float* dden, const float* rsum, float* dk32,
-                 float* dv32, float* dq32, float* dell, cudaStream_t st) {
+int tc_intra_bwd_q(const Geo& g, const CUtensorMap& m_q, const CUtensorMap& m_k, const CUtensorMap& m_v,
+                   const CUtensorMap& m_dn, const float* ell, const float* dden, const float* rsum, float* dq32,
+                   float* dell, cudaStream_t st) {
   using namespace ib2;
   const dim3 grid(g.c / 128, g.n, g.ns);
-  auto kv = g.normalize ? k_tc_ib<true, true> : k_tc_ib<true, false>;
   auto qs = g.normalize ? k_tc_ib<false, true> : k_tc_ib<false, false>;
-  cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
   cudaFuncSetAttribute(qs, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-  kv<<<grid, THREADS, SMEM, st>>>(m_q, m_k, m_v, m_dn, g, ell, dden, rsum, dk32, dv32, dell);
   qs<<<grid, THREADS, SMEM, st>>>(m_q, m_k, m_v, m_dn, g, ell, dden, rsum, dq32, nullptr, dell);
+  count_launch();
   return 0;
 }
 

@@ -121,8 +121,8 @@ template <bool kUpd, int kDen>
 __global__ void __launch_bounds__(zv::THREADS, 1)
     k_tc_zvjp(Geo g, int u_bf16_bth, const void* __restrict__ u_rows, const __half* __restrict__ u16,
               const __nv_bfloat16* __restrict__ xraw, const float* __restrict__ ell,
-              const float* __restrict__ lamlog, const __half* __restrict__ E, const float* __restrict__ dx32,
-              const float* __restrict__ dv32, float* dell, float* dellend, __nv_bfloat16* dxo,
+              const float* __restrict__ lamlog, const __half* __restrict__ E, const void* __restrict__ dx32,
+              const void* __restrict__ dv32, float* dell, float* dellend, __nv_bfloat16* dxo,
               __nv_bfloat16* dvo, int ntiles, int nI, int nk, int kbeg) {
   using namespace zv;
   constexpr bool den = kDen != 0;
@@ -439,22 +439,38 @@ __global__ void __launch_bounds__(zv::THREADS, 1)
       if (l == 0) mbar_arrive(acc_empty);
       if (live) {
         const size_t xr = rowid(g, t.s, tok);
-        const float4* o32 = (const float4*)((is_dv ? dv32 : dx32) + ((size_t)t.s * g.t + tok) * HD);
+        // intra-chunk part: fp32 rows (query side, reduce-added by the intra kernel)
+        // or bf16 rows (update side)
+        const size_t orow = ((size_t)t.s * g.t + tok) * HD;
+        const float4* o32 = (const float4*)((const float*)dx32 + orow);
+        const uint4* o16 = (const uint4*)((const __nv_bfloat16*)(is_dv ? dv32 : dx32) + orow);
         const uint4* xsrc = (const uint4*)(xraw + xr * HD);
         // the bf16 rows go out through shared memory: this tile's operand-word buffer
         // (xw2[it & 1]) is free once its accumulator is full (every generator read
         // of it precedes the last a_full arrival); 32 rows x 128 B per warp, 16-byte
         // chunks XOR-swizzled by row, then four whole 128-byte rows per warp store
         uint8_t* stg = (uint8_t*)(xw2 + (it & 1) * 32 * NGEN) + e * 4096;
-        float c = 0.f;
+        float c = 0.f, ci = 0.f;
 #pragma unroll
         for (int a4 = 0; a4 < 8; a4 += 4) {
-          float4 ov[8];
+          float ov[4][8];
           uint4 xv[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            ov[2 * i] = o32[2 * (a4 + i)];
-            ov[2 * i + 1] = o32[2 * (a4 + i) + 1];
+            if (kUpd) {
+              const uint4 h8 = o16[a4 + i];
+              const uint32_t* ph = (const uint32_t*)&h8;
+#pragma unroll
+              for (int e2 = 0; e2 < 4; ++e2) {
+                const float2 f2 = __bfloat1622float2(*(const __nv_bfloat162*)&ph[e2]);
+                ov[i][2 * e2] = f2.x;
+                ov[i][2 * e2 + 1] = f2.y;
+              }
+            } else {
+              const float4 v0 = o32[2 * (a4 + i)], v1 = o32[2 * (a4 + i) + 1];
+              ov[i][0] = v0.x; ov[i][1] = v0.y; ov[i][2] = v0.z; ov[i][3] = v0.w;
+              ov[i][4] = v1.x; ov[i][5] = v1.y; ov[i][6] = v1.z; ov[i][7] = v1.w;
+            }
             if (!is_dv) xv[i] = xsrc[a4 + i];
           }
 #pragma unroll
@@ -467,14 +483,15 @@ __global__ void __launch_bounds__(zv::THREADS, 1)
               for (int e2 = 0; e2 < 4; ++e2) {
                 const float2 x2 = __bfloat1622float2(*(const __nv_bfloat162*)&pxv[e2]);
                 c = fmaf(f[2 * e2], x2.x, fmaf(f[2 * e2 + 1], x2.y, c));
+                if (!kUpd) ci = fmaf(ov[i][2 * e2], x2.x, fmaf(ov[i][2 * e2 + 1], x2.y, ci));
               }
             }
-            const float4 v0 = ov[2 * i], v1 = ov[2 * i + 1];
+            const float* o = ov[i];
             *(uint4*)(stg + l * 128 + ((a ^ (l & 7)) << 4)) =
-                make_uint4(pack_bf16(fmaf(f[0], fct, v0.x), fmaf(f[1], fct, v0.y)),
-                           pack_bf16(fmaf(f[2], fct, v0.z), fmaf(f[3], fct, v0.w)),
-                           pack_bf16(fmaf(f[4], fct, v1.x), fmaf(f[5], fct, v1.y)),
-                           pack_bf16(fmaf(f[6], fct, v1.z), fmaf(f[7], fct, v1.w)));
+                make_uint4(pack_bf16(fmaf(f[0], fct, o[0]), fmaf(f[1], fct, o[1])),
+                           pack_bf16(fmaf(f[2], fct, o[2]), fmaf(f[3], fct, o[3])),
+                           pack_bf16(fmaf(f[4], fct, o[4]), fmaf(f[5], fct, o[5])),
+                           pack_bf16(fmaf(f[6], fct, o[6]), fmaf(f[7], fct, o[7])));
           }
         }
         __syncwarp();
@@ -487,10 +504,13 @@ __global__ void __launch_bounds__(zv::THREADS, 1)
                 *(const uint4*)(stg + rw * 128 + ((ch ^ (rw & 7)) << 4));
           }
         }
-        // d<., .>/d(log factor) = <dx~, x~>/2 (degree-2 homogeneity of phi')
+        // d<., .>/d(log factor) = <dx~, x~>/2 (degree-2 homogeneity of phi'); the
+        // intra-chunk query side follows the same way from the fp32 intra-chunk dq
+        // rows (sum_j dP'_mj P_mj = <q_m, dq_m>/2; the intra-chunk kernel wrote the
+        // key side; deterministic mode: the query-side pass added it instead)
         c *= 0.5f * fct;
         if (g.gated) {
-          if (!kUpd) dell[(size_t)t.s * g.t + tok] += c;            // gp_m = exp(ell_m)
+          if (!kUpd) dell[(size_t)t.s * g.t + tok] += c + (g.det ? 0.f : 0.5f * ci);   // gp_m = exp(ell_m)
           else if (gq == 0) dellend[(size_t)t.s * g.t + tok] = c;   // suffix decay, finished in gate_finish
         }
       }
@@ -507,18 +527,29 @@ __global__ void __launch_bounds__(zv::THREADS, 1)
   if (w == W_TMA) tmem_dealloc<512>(tm);
 }
 
-// chunk 0 without a prefix has no state query: dq is the intra-chunk part alone
-__global__ void __launch_bounds__(256) k_tc_dq_chunk0(Geo g, const float* __restrict__ dx32, __nv_bfloat16* dxo) {
+// chunk 0 without a prefix has no state query: dq is the intra-chunk part
+// alone; its log-gate cotangent <q, dq>/2 as in the epilogue above
+__global__ void __launch_bounds__(256) k_tc_dq_chunk0(Geo g, const float* __restrict__ dx32,
+                                                      const __nv_bfloat16* __restrict__ xraw, float* dell,
+                                                      __nv_bfloat16* dxo) {
   const int s = blockIdx.y;
   for (int i = blockIdx.x * 256 + threadIdx.x; i < g.c * 16; i += gridDim.x * 256) {
     const int r = i >> 4, c4 = (i & 15) * 4;
     const float4 v = *(const float4*)(dx32 + ((size_t)s * g.t + r) * HD + c4);
+    const uint2 xq = *(const uint2*)(xraw + rowid(g, s, r) * HD + c4);
+    const float2 x01 = __bfloat1622float2(*(const __nv_bfloat162*)&xq.x);
+    const float2 x23 = __bfloat1622float2(*(const __nv_bfloat162*)&xq.y);
+    float dot = v.x * x01.x + v.y * x01.y + v.z * x23.x + v.w * x23.y;
+    // the 16 lanes (i & 15) of a row sit in one half-warp
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
     *(uint2*)(dxo + rowid(g, s, r) * HD + c4) = make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
+    if (g.gated && !g.det && (i & 15) == 0) dell[(size_t)s * g.t + r] += 0.5f * dot;
   }
 }
 
 int tc_zvjp(const Geo& g, bool upd, int u_bf16_bth, const void* u_rows, const __half* u16, const void* xraw,
-            const float* ell, const float* lamlog, const __half* E, const float* dx32, const float* dv32,
+            const float* ell, const float* lamlog, const __half* E, const void* dx32, const void* dv32,
             float* dell, float* dellend, void* dxo, void* dvo, cudaStream_t st) {
   using namespace zv;
   const int den = g.normalize ? 1 : 0;
@@ -529,7 +560,8 @@ int tc_zvjp(const Geo& g, bool upd, int u_bf16_bth, const void* u_rows, const __
   const int kbeg = (!upd && !g.prefix) ? 1 : 0;
   const int nI = (g.c + tok - 1) / tok, nk = g.n - kbeg;
   if (kbeg) {
-    k_tc_dq_chunk0<<<dim3(8, g.ns), 256, 0, st>>>(g, dx32, (__nv_bfloat16*)dxo);
+    k_tc_dq_chunk0<<<dim3(8, g.ns), 256, 0, st>>>(g, (const float*)dx32, (const __nv_bfloat16*)xraw, dell,
+                                                   (__nv_bfloat16*)dxo);
     count_launch();
   }
   const int ntiles = nI * nk * g.ns;
