@@ -142,21 +142,100 @@ static int make_geo(const pa_problem* pr, Geo* g) {
   g->ng = g->n;
   g->prefix = 0;
   g->nsl = g->n + 1;
+  g->treal = g->t;
   return PA_OK;
 }
 
-// Which kernel family runs the problem; with PA_FLAG_STRICT_TC a 16-bit
-// problem the tensor-core kernels do not cover is an error, not a silent
-// switch to the fp32 CUDA-core kernels.
-static int route(const pa_problem* pr, const Geo& g, bool* tc) {
+// A tensor-core problem whose last chunk is partial (or whose single chunk is
+// not a multiple of 128 tokens) runs on a zero-padded copy of the sequence
+// (reference ChunkPlan.bounds chunked.py:85-86 ends the last chunk early).
+// Padded keys and values are zero and padded log-gates are 0, so the padding
+// adds nothing to any real token's output, chunk state or gradient; padded
+// rows are dropped.  The returned geometry has t = the padded length and
+// treal = the caller's.
+static bool pad_geo(const pa_problem* pr, const Geo& g, Geo* gp) {
+  if (pr->dtype != PA_BF16) return false;
+  Geo p = g;
+  if (g.n == 1) {
+    p.c = (g.t + 127) / 128 * 128;
+    p.t = p.c;
+  } else {
+    p.t = g.n * g.c;
+  }
+  if (p.t == g.t) return false;
+  p.n = p.t / p.c;
+  p.nsl = p.n + 1;
+  p.ng = p.n;
+  if (!tc_supported(p, pr->dtype)) return false;
+  *gp = p;
+  return true;
+}
+
+// Which kernel family runs the problem (g becomes the padded geometry when
+// padding applies); with PA_FLAG_STRICT_TC a 16-bit problem the tensor-core
+// kernels do not cover is an error, not a silent switch to the fp32 CUDA-core
+// kernels.
+static int route(const pa_problem* pr, Geo& g, bool* tc) {
   *tc = tc_supported(g, pr->dtype);
+  Geo gp;
+  if (!*tc && pad_geo(pr, g, &gp)) {
+    g = gp;
+    *tc = true;
+  }
   if (!*tc && (pr->flags & PA_FLAG_STRICT_TC) && pr->dtype != PA_F32) {
-    set_error("strict tensor-core mode: the tcgen05 kernels cover bf16, p = 2, d = e = 64, chunk a multiple of "
-              "128 up to 1024 and t a multiple of the chunk");
+    set_error("strict tensor-core mode: the tcgen05 kernels cover bf16, p = 2, d = e = 64 and a chunk that is a "
+              "multiple of 128 up to 1024 (or one chunk of at most 1024 tokens)");
     return PA_ERR_UNSUPPORTED;
   }
   return PA_OK;
 }
+
+// zero-padded copies for the padded tensor-core path: per batch, t real rows of
+// `rb` bytes then t_pad - t zero rows
+struct PadFwd {
+  char *q, *k, *v, *y;
+  float *lg, *rs;
+};
+struct PadBwd {
+  char *dy, *dq, *dk, *dv;
+  float* dlg;
+};
+static PadFwd carve_pad_fwd(const Geo& g, void* base, size_t* bytes) {
+  Carver c(base);
+  PadFwd p;
+  const size_t rows = (size_t)g.b * g.t * g.h;
+  p.q = c.take<char>(rows * g.d * 2);
+  p.k = c.take<char>(rows * g.d * 2);
+  p.v = c.take<char>(rows * g.e * 2);
+  p.y = c.take<char>(rows * g.e * 2);
+  p.lg = c.take<float>(rows);
+  p.rs = c.take<float>(rows);
+  *bytes = c.off;
+  return p;
+}
+static PadBwd carve_pad_bwd(const Geo& g, void* base, size_t* bytes) {
+  Carver c(base);
+  PadBwd p;
+  const size_t rows = (size_t)g.b * g.t * g.h;
+  p.dy = c.take<char>(rows * g.e * 2);
+  p.dq = c.take<char>(rows * g.d * 2);
+  p.dk = c.take<char>(rows * g.d * 2);
+  p.dv = c.take<char>(rows * g.e * 2);
+  p.dlg = c.take<float>(rows);
+  *bytes = c.off;
+  return p;
+}
+static void pad_rows(void* dst, const void* src, const Geo& g, size_t row_bytes, cudaStream_t st) {
+  const size_t rb = (size_t)g.h * row_bytes;   // one token of every head
+  cudaMemcpy2DAsync(dst, g.t * rb, src, g.treal * rb, g.treal * rb, g.b, cudaMemcpyDeviceToDevice, st);
+  cudaMemset2DAsync((char*)dst + g.treal * rb, g.t * rb, 0, (g.t - g.treal) * rb, g.b, st);
+}
+static void unpad_rows(void* dst, const void* src, const Geo& g, size_t row_bytes, cudaStream_t st) {
+  const size_t rb = (size_t)g.h * row_bytes;
+  cudaMemcpy2DAsync(dst, g.treal * rb, src, g.t * rb, g.treal * rb, g.b, cudaMemcpyDeviceToDevice, st);
+}
+static size_t inner_fwd_bytes(const Geo& g) { return align_up(tc_fwd_workspace_bytes(g)); }
+static size_t inner_bwd_bytes(const Geo& g) { return align_up(tc_bwd_workspace_bytes(g)); }
 
 SimtWs carve_simt_fwd(const Geo& g, void* ws, size_t* bytes) {
   Carver c(ws);
@@ -240,6 +319,11 @@ size_t pa_fwd_workspace_bytes(const pa_problem* pr) {
   if (make_geo(pr, &g)) return 0;
   bool tc;
   if (route(pr, g, &tc)) return 0;
+  if (tc && g.t != g.treal) {
+    size_t extra;
+    carve_pad_fwd(g, nullptr, &extra);
+    return inner_fwd_bytes(g) + extra;
+  }
   if (tc) return tc_fwd_workspace_bytes(g);
   size_t n;
   carve_simt_fwd(g, nullptr, &n);
@@ -251,6 +335,11 @@ size_t pa_bwd_workspace_bytes(const pa_problem* pr) {
   if (make_geo(pr, &g)) return 0;
   bool tc;
   if (route(pr, g, &tc)) return 0;
+  if (tc && g.t != g.treal) {
+    size_t extra;
+    carve_pad_bwd(g, nullptr, &extra);
+    return inner_bwd_bytes(g) + extra;
+  }
   if (tc) return tc_bwd_workspace_bytes(g);
   size_t n;
   carve_simt_bwd(g, nullptr, &n);
@@ -269,6 +358,23 @@ int pa_power_full_fwd(const pa_problem* pr, const void* q, const void* k, const 
   cudaStream_t st = (cudaStream_t)stream;
   bool tc;
   if (int rc = route(pr, g, &tc)) return rc;
+  if (tc && g.t != g.treal) {
+    size_t extra;
+    PadFwd p = carve_pad_fwd(g, (char*)ws + inner_fwd_bytes(g), &extra);
+    if (ws_bytes < inner_fwd_bytes(g) + extra) {
+      set_error("forward workspace too small");
+      return PA_ERR_WORKSPACE;
+    }
+    pad_rows(p.q, q, g, (size_t)g.d * 2, st);
+    pad_rows(p.k, k, g, (size_t)g.d * 2, st);
+    pad_rows(p.v, v, g, (size_t)g.e * 2, st);
+    if (g.gated) pad_rows(p.lg, log_g, g, 4, st);
+    const bool rs = rowsum || g.normalize;
+    if (int rc = tc_forward(g, p.q, p.k, p.v, g.gated ? p.lg : nullptr, p.y, rs ? p.rs : nullptr, ws, st)) return rc;
+    unpad_rows(y, p.y, g, (size_t)g.e * 2, st);
+    if (rowsum) unpad_rows(rowsum, p.rs, g, 4, st);
+    return cuda_check("padded forward");
+  }
   if (tc) {
     if (ws_bytes < tc_fwd_workspace_bytes(g)) {
       set_error("forward workspace too small");
@@ -302,6 +408,24 @@ int pa_power_full_bwd(const pa_problem* pr, const void* q, const void* k, const 
   cudaStream_t st = (cudaStream_t)stream;
   bool tc;
   if (int rc = route(pr, g, &tc)) return rc;
+  if (tc && g.t != g.treal) {
+    size_t extra;
+    PadFwd pf = carve_pad_fwd(g, (char*)fwd_ws + inner_fwd_bytes(g), &extra);
+    PadBwd pb = carve_pad_bwd(g, (char*)bwd_ws + inner_bwd_bytes(g), &extra);
+    if (bwd_ws_bytes < inner_bwd_bytes(g) + extra) {
+      set_error("backward workspace too small");
+      return PA_ERR_WORKSPACE;
+    }
+    pad_rows(pb.dy, dy, g, (size_t)g.e * 2, st);
+    if (int rc = tc_backward(g, pf.q, pf.k, pf.v, g.gated ? pf.lg : nullptr, pf.y, g.normalize ? pf.rs : nullptr,
+                             pb.dy, pb.dq, pb.dk, pb.dv, dlog_g ? pb.dlg : nullptr, fwd_ws, bwd_ws, st))
+      return rc;
+    unpad_rows(dq, pb.dq, g, (size_t)g.d * 2, st);
+    unpad_rows(dk, pb.dk, g, (size_t)g.d * 2, st);
+    unpad_rows(dv, pb.dv, g, (size_t)g.e * 2, st);
+    if (dlog_g) unpad_rows(dlog_g, pb.dlg, g, 4, st);
+    return cuda_check("padded backward");
+  }
   if (tc) {
     if (bwd_ws_bytes < tc_bwd_workspace_bytes(g)) {
       set_error("backward workspace too small");

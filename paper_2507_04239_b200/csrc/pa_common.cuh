@@ -25,6 +25,9 @@ struct Geo {
   int k0, ng, prefix, nsl;
   // PA_FLAG_DETERMINISTIC: one MMA issuer per accumulator (fixed summation order)
   int det;
+  // tokens of the caller's sequence; t > treal when a partial last chunk runs on a
+  // zero-padded copy (tensor-core path)
+  int treal;
 };
 
 __host__ __device__ __forceinline__ size_t rowid(const Geo& g, int s, int m) {

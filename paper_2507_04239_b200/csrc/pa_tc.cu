@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(256) k_tc_bwd_prep(Geo g, const __nv_bfloat16*
     const size_t r = rowid(g, s, m);
     uint4 v4 = ((const uint4*)(dy + r * HD))[c8];
     const float4 ya = ((const float4*)(y32 + it * HD))[2 * c8], yb = ((const float4*)(y32 + it * HD))[2 * c8 + 1];
-    inv = 1.f / rowsum[r];
+    inv = m < g.treal ? 1.f / rowsum[r] : 0.f;   // zero padding past the sequence end
     const float yv[8] = {ya.x, ya.y, ya.z, ya.w, yb.x, yb.y, yb.z, yb.w};
     uint32_t* pv = (uint32_t*)&v4;
 #pragma unroll

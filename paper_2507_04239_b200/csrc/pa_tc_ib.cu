@@ -157,9 +157,10 @@ __global__ void __launch_bounds__(ib2::THREADS, 2) k_tc_ib(const __grid_constant
         //   dP' = (dy.v - dy.y) / R = (acc + dden R) / R
         // so with c' = c / R: P' = P / R (the dV operand, = P^T dnum), dS = (acc + dden R) T'
         const float R = rsum[rowid(g, s, c0 + i)];
-        colf[i] *= 1.f / R;
+        const float Ri = c0 + i < g.treal ? 1.f / R : 0.f;   // zero padding past the sequence: weight 0
+        colf[i] *= Ri;
         cold[i] = dden[(size_t)s * g.t + c0 + i] * R;
-        if ((i >> 7) == B0) cinv[i & 127] = 1.f / R;
+        if ((i >> 7) == B0) cinv[i & 127] = Ri;
       }
     }
   }
@@ -263,7 +264,7 @@ __global__ void __launch_bounds__(ib2::THREADS, 2) k_tc_ib(const __grid_constant
     // q-side normalization: the row factor takes 1/R_own, dden takes R_own (see cold above)
     const float R_own = (!kKV && kNorm) ? rsum[rowid(g, s, c0 + own)] : 1.f;
     const float dden_own = (!kKV && kNorm) ? dden[(size_t)s * g.t + c0 + own] * R_own : 0.f;
-    const float rinv_own = 1.f / R_own;
+    const float rinv_own = c0 + own < g.treal ? 1.f / R_own : 0.f;   // zero padding: weight 0
     // kKV: c_own = 2^(ell_endJ - ell_own) (<= 1); q-side: r_own = sigma^2 2^(ell_own - ell_endJ) per J
     const float c_own = kKV ? exp2_approx(fminf(ell_s[B0 * 128 + 127] - l_own, 0.f)) : 0.f;
     f2 red = {0.f, 0.f};

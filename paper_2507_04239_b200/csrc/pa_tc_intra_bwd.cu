@@ -334,7 +334,8 @@ __global__ void __launch_bounds__(ibx::THREADS, 1)
         if (i < g.c) {
           ell_s[i] = LOG2E * pf_l[r];
           if (kNorm) {
-            rinv[i] = 1.f / pf_r[r];
+            // rows past the caller's sequence (zero padding) have R = 0: weight 0
+            rinv[i] = c0 + i < g.treal ? 1.f / pf_r[r] : 0.f;
             cold[i] = pf_d[r] * pf_r[r];
           }
         }

@@ -361,8 +361,12 @@ __global__ void __launch_bounds__(out2::THREADS, 1) k_tc_out2(
     const size_t rw = rowid(g, s, tok);
     float inv = 1.f;
     if (g.normalize) {
-      if (!(dn > 0.f)) atomicAdd(zflag, 1);
-      inv = 1.f / dn;
+      if (tok >= g.treal) {
+        inv = 0.f;   // zero padding past the sequence end (partial last chunk): y = 0
+      } else {
+        if (!(dn > 0.f)) atomicAdd(zflag, 1);
+        inv = 1.f / dn;
+      }
     }
     if (rowsum) rowsum[rw] = dn;
     {

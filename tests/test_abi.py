@@ -118,7 +118,10 @@ def test_route_and_strict_flag():
     lib = _lib.load()
     tc = _problem(t=2048, d=64, e=64, chunk=1024, dtype=1)
     assert lib.pa_uses_tensor_cores(ctypes.byref(tc)) == 1
-    off = _problem(t=1000, d=64, e=64, chunk=256, dtype=1)
+    # a partial last chunk runs on a zero-padded copy on the tensor cores
+    assert lib.pa_uses_tensor_cores(ctypes.byref(_problem(t=1000, d=64, e=64, chunk=256, dtype=1))) == 1
+    assert lib.pa_uses_tensor_cores(ctypes.byref(_problem(t=700, d=64, e=64, chunk=4096, dtype=1))) == 1
+    off = _problem(t=1024, d=32, e=32, chunk=256, dtype=1)
     assert lib.pa_uses_tensor_cores(ctypes.byref(off)) == 0
     off.flags = _lib.PA_FLAG_STRICT_TC
     assert lib.pa_uses_tensor_cores(ctypes.byref(off)) == -4

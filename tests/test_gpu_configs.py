@@ -201,8 +201,26 @@ def test_zero_denominator_sync_and_deferred():
 
 
 def test_fallback_warns_and_strict_raises():
-    x = torch.rand(1, 1000, 1, 64, device="cuda").bfloat16()
+    x = torch.rand(1, 1024, 1, 32, device="cuda").bfloat16()
     with pytest.warns(RuntimeWarning, match="fp32 CUDA-core"):
         P.power_full(x, x, x, None, p=2, chunk_size=256)
     with pytest.raises(P.InvalidSpec, match="strict"):
         P.power_full(x, x, x, None, p=2, chunk_size=256, strict=True)
+
+
+@pytest.mark.parametrize("normalize", [False, True])
+@pytest.mark.parametrize("t,c", [(1000, 256), (700, None), (1300, 1024)])
+def test_partial_last_chunk_on_tensor_cores(t, c, normalize):
+    """A partial last chunk (reference ChunkPlan.bounds, chunked.py:85-86) runs on
+    the tcgen05 kernels over a zero-padded copy: strict mode accepts it, and
+    outputs and gradients match the oracle on the caller's t tokens."""
+    q, k, v, g = O.generate_inputs(1, t, 2, 64, 64, seed=t + 5, gating=True)
+    q, k, v = _bf16_exact(q, k, v)
+    dy, = _bf16_exact(np.random.default_rng(t).uniform(-1, 1, (1, t, 2, 64)))
+    Q, K, V = (torch.tensor(x, device="cuda", dtype=torch.bfloat16, requires_grad=True) for x in (q, k, v))
+    lg = torch.tensor(np.log(g), device="cuda", dtype=torch.float32, requires_grad=True)
+    y = P.power_full(Q, K, V, lg, p=2, chunk_size=c, normalize=normalize, strict=True, check_denominator="sync")
+    gr = torch.autograd.grad(y, [Q, K, V, lg], torch.tensor(dy, device="cuda", dtype=torch.bfloat16))
+    r = {"y": y.detach().double().cpu().numpy(), "dq": gr[0].double().cpu().numpy(),
+         "dk": gr[1].double().cpu().numpy(), "dv": gr[2].double().cpu().numpy(), "dlogg": gr[3].double().cpu().numpy()}
+    _compare(f"t={t} c={c} normalize={normalize}", r, q, k, v, g, 2, c if c is not None else t, normalize, dy)
