@@ -68,8 +68,9 @@ typedef struct pa_problem {
   double scale;          /* sigma (attention.py:149-150), when has_scale      */
 } pa_problem;
 
-/* 1 when the problem runs on the tcgen05 tensor-core kernels, 0 when it runs
- * on the fp32 CUDA-core kernels, negative PA_ERR_* when it is invalid. */
+/* 1 when the problem runs on the tcgen05 tensor-core kernels (p = 2), 2 when
+ * its state GEMMs do (the degree-4 path: bf16, p = 4, d = e = 32), 0 when it
+ * runs on the fp32 CUDA-core kernels, negative PA_ERR_* when it is invalid. */
 int pa_uses_tensor_cores(const pa_problem* pr);
 
 /* Expansion kinds (reference expansions.py:41-44). */

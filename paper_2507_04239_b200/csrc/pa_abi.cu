@@ -143,6 +143,10 @@ static int make_geo(const pa_problem* pr, Geo* g) {
   g->prefix = 0;
   g->nsl = g->n + 1;
   g->treal = g->t;
+  g->dtype = pr->dtype;
+  // the degree-4 tensor-core path orders features in blocks of four (pa_tc4.cu):
+  // its states hold tc4_slots() rows (zero-weight duplicates included)
+  if (tc4_supported(*g, pr->dtype)) g->D = tc4_slots();
   return PA_OK;
 }
 
@@ -182,7 +186,7 @@ static int route(const pa_problem* pr, Geo& g, bool* tc) {
     g = gp;
     *tc = true;
   }
-  if (!*tc && (pr->flags & PA_FLAG_STRICT_TC) && pr->dtype != PA_F32) {
+  if (!*tc && !tc4_supported(g, pr->dtype) && (pr->flags & PA_FLAG_STRICT_TC) && pr->dtype != PA_F32) {
     set_error("strict tensor-core mode: the tcgen05 kernels cover bf16, p = 2, d = e = 64 and a chunk that is a "
               "multiple of 128 up to 1024 (or one chunk of at most 1024 tokens)");
     return PA_ERR_UNSUPPORTED;
@@ -248,6 +252,7 @@ SimtWs carve_simt_fwd(const Geo& g, void* ws, size_t* bytes) {
   w.A = c.take<float>((size_t)g.ns * g.n * g.D * g.E1);
   w.yat = c.take<float>((size_t)g.ns * g.t * g.E1);
   w.y32 = c.take<float>(g.normalize ? (size_t)g.ns * g.t * g.e : 0);
+  w.tc4 = c.take<char>(tc4_supported(g, g.dtype) ? tc4_extra_bytes(g) : 0);
   *bytes = c.off;
   return w;
 }
@@ -311,7 +316,8 @@ int pa_uses_tensor_cores(const pa_problem* pr) {
   if (int rc = make_geo(pr, &g)) return -rc;
   bool tc;
   if (int rc = route(pr, g, &tc)) return -rc;
-  return tc ? 1 : 0;
+  if (tc) return 1;
+  return tc4_supported(g, pr->dtype) ? 2 : 0;
 }
 
 size_t pa_fwd_workspace_bytes(const pa_problem* pr) {
@@ -389,7 +395,11 @@ int pa_power_full_fwd(const pa_problem* pr, const void* q, const void* k, const 
     return PA_ERR_WORKSPACE;
   }
   cudaMemsetAsync(w.zflag, 0, sizeof(int), st);
-  if (int rc = simt_build_table(g.p, g.d, g.D, w.idx, w.wt, st)) return rc;
+  if (tc4_supported(g, pr->dtype)) {
+    if (int rc = tc4_copy_tables(w.idx, w.wt, st)) return rc;
+  } else if (int rc = simt_build_table(g.p, g.d, g.D, w.idx, w.wt, st)) {
+    return rc;
+  }
   return simt_forward(g, pr->dtype, q, k, v, log_g, y, rowsum, w, st);
 }
 

@@ -28,6 +28,7 @@ struct Geo {
   // tokens of the caller's sequence; t > treal when a partial last chunk runs on a
   // zero-padded copy (tensor-core path)
   int treal;
+  int dtype;   // pa_dtype of q, k, v
 };
 
 __host__ __device__ __forceinline__ size_t rowid(const Geo& g, int s, int m) {

@@ -1044,13 +1044,20 @@ static int simt_forward_t(const Geo& g, const T* q, const T* k, const T* v, cons
   const int tpc = (g.c + 63) / 64;
   k_gate_prep<<<(g.ns * g.n + 127) / 128, 128, 0, st>>>(g, log_g, w.ell, w.lamlog);
   k_intra_fwd<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_intra_fwd<T, DM>, smb_intra_fwd<DM>()), st>>>(g, q, k, v, w.ell, w.yat);
-  if constexpr (DM <= 64)
+  if (tc4_supported(g, g.dtype)) {
+    if (int rc = tc4_state(g, false, k, v, nullptr, w.ell, w.lamlog, w.idx, w.wt, w.tc4, w.A, st)) return rc;
+  } else if constexpr (DM <= 64)
     k_state_accum_f<T, T, DM><<<dim3((g.D + kSaThreads - 1) / kSaThreads, g.n, g.ns), kSaThreads, 0, st>>>(
         g, k, 1.f, g.gated ? 1 : 0, w.ell, w.lamlog, v, 1, g.e, g.e, 1, w.idx, w.wt, 0, 0, w.A);
   else
     k_state_accum<T, T, DM><<<dim3((g.D + 31) / 32, g.n, g.ns), 256, 0, st>>>(
         g, k, 1.f, g.gated ? 1 : 0, w.ell, w.lamlog, v, 1, g.e, g.e, 1, w.idx, w.wt, 0, 0, w.A);
   if (g.n > 1) k_discumsum_states<<<dim3((unsigned)std::min<size_t>(((size_t)g.D * g.E1 + 255) / 256, 512), g.ns), 256, 0, st>>>(g, w.lamlog, w.A);
+  if (tc4_supported(g, g.dtype)) {
+    // state query + combine on the tensor cores (phi(q) generated on chip)
+    if (int rc = tc4_states16(g, 0, w.A, w.wt, w.tc4, st)) return rc;
+    if (int rc = tc4_tok(g, 0, q, w.ell, w.lamlog, w.yat, y, rowsum, w.y32, w.zflag, nullptr, w.tc4, st)) return rc;
+  } else
   k_query_combine<T, DM><<<dim3(g.n * ((g.c + qc_tokens<DM>() - 1) / qc_tokens<DM>()), g.ns), qc_tokens<DM>(),
                            dyn_smem(k_query_combine<T, DM>, smb_query_combine<DM>()), st>>>(g, q, w.A, w.idx, w.wt, w.ell, w.yat, y, rowsum, w.zflag, w.y32);
   count_launch(g.n > 1 ? 5 : 4);
@@ -1073,11 +1080,27 @@ static int simt_backward_t(const Geo& g, const T* q, const T* k, const T* v, con
   int launches = 0;
   k_bwd_prep<T><<<nblk((size_t)g.ns * g.t, 256), 256, 0, st>>>(g, dy, w.y32, rowsum, b.dz);
   ++launches;
+  if (tc4_supported(g, g.dtype)) {
+    // degree 4 on the tensor cores (pa_tc4.cu): dA (feature-major GEMM), the
+    // query- and update-side state VJPs (dphi GEMM + expand-VJP) and dv
+    if (g.n > 1) {
+      if (int rc = tc4_state(g, true, q, nullptr, b.dz, w.ell, w.lamlog, w.idx, w.wt, w.tc4, b.dA, st)) return rc;
+      if (int rc = tc4_vjp(g, false, q, b.dq32, b.dell, nullptr, w.tc4, st)) return rc;
+      k_discumsum_bwd<<<dim3((unsigned)((per + 255) / 256), g.ns), 256, 0, st>>>(g, w.lamlog, w.A, b.dA, b.dlam);
+      ++launches;
+    }
+    if (int rc = tc4_states16(g, 1, b.dA, w.wt, w.tc4, st)) return rc;
+    if (int rc = tc4_vjp(g, true, k, b.dk32, nullptr, b.dellend, w.tc4, st)) return rc;
+    if (int rc = tc4_tok(g, 1, k, w.ell, w.lamlog, nullptr, nullptr, nullptr, nullptr, nullptr, b.dv32, w.tc4, st))
+      return rc;
+  } else {
   if (g.n > 1) {
     k_query_bwd<T, DM><<<dim3((g.n - 1) * ((g.c + ub_tokens<DM>() - 1) / ub_tokens<DM>()), g.ns), ub_tokens<DM>(),
                           dyn_smem(k_query_bwd<T, DM>, smb_query_bwd<DM>()), st>>>(g, q, w.A, w.idx, w.wt, w.ell, b.dz, b.dq32, b.dell);
     Geo gz = g;
-    if constexpr (DM <= 64)
+    if (tc4_supported(g, g.dtype)) {
+      if (int rc = tc4_state(g, true, q, nullptr, b.dz, w.ell, w.lamlog, w.idx, w.wt, w.tc4, b.dA, st)) return rc;
+    } else if constexpr (DM <= 64)
       k_state_accum_f<T, float, DM><<<dim3((g.D + kSaThreads - 1) / kSaThreads, g.n - 1, g.ns), kSaThreads, 0, st>>>(
           gz, q, g.scale, g.gated ? 2 : 0, w.ell, w.lamlog, b.dz, 0, g.E1, g.E1, 0, w.idx, w.wt, 1, 1, b.dA);
     else
@@ -1088,6 +1111,8 @@ static int simt_backward_t(const Geo& g, const T* q, const T* k, const T* v, con
   }
   k_update_bwd<T, DM><<<dim3(g.n * ((g.c + ub_tokens<DM>() - 1) / ub_tokens<DM>()), g.ns), ub_tokens<DM>(),
                         dyn_smem(k_update_bwd<T, DM>, smb_update_bwd<DM>()), st>>>(g, k, v, b.dA, w.idx, w.wt, w.ell, w.lamlog, b.dk32, b.dv32, b.dell, b.dellend);
+  ++launches;
+  }
   k_intra_bwd_q<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_intra_bwd_q<T, DM>, smb_intra_bwd<DM>()), st>>>(g, q, k, v, w.ell, b.dz, b.dq32, b.dell);
   k_intra_bwd_kv<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_intra_bwd_kv<T, DM>, smb_intra_bwd<DM>()), st>>>(g, q, k, v, w.ell, b.dz, b.dk32, b.dv32, b.dell);
   launches += 3;

@@ -13,7 +13,23 @@ struct SimtWs {           // forward workspace, kept for the backward
   float* yat;             // [ns, t, E1]
   int* zflag;             // [1]
   float* y32;             // [ns, t, e] normalized output in fp32 (normalize only)
+  char* tc4;              // scratch of the degree-4 tensor-core state GEMMs (pa_tc4.cu), or empty
 };
+
+// degree-4 state GEMMs on the tensor cores (pa_tc4.cu): bf16, p = 4, d = e = 32
+bool tc4_supported(const Geo& g, int dtype);
+size_t tc4_extra_bytes(const Geo& g);
+// out [ns, n, D, e+1] (fwd: S_k from x = k, v; bwd: dA of slot k-1 from x = q, dz)
+int tc4_state(const Geo& g, bool bwd, const void* x, const void* v, const float* dz, const float* ell,
+              const float* lamlog, const int* idx, const float* wt, void* scratch, float* out, cudaStream_t st);
+// slot count of the degree-4 block order; copies its (idx, wt) table into a workspace
+int tc4_slots();
+int tc4_copy_tables(int* idx, float* wt, cudaStream_t st);
+int tc4_states16(const Geo& g, int which, const float* A, const float* wt, void* scratch, cudaStream_t st);
+int tc4_vjp(const Geo& g, bool upd, const void* x, float* dx32, float* dell, float* dellend, void* scratch,
+            cudaStream_t st);
+int tc4_tok(const Geo& g, int mode, const void* x, const float* ell, const float* lamlog, const float* yat, void* y,
+            float* rowsum, float* y32, int* zflag, float* dv32, void* scratch, cudaStream_t st);
 
 struct SimtBwdWs {
   float* dz;              // [ns, t, E1]

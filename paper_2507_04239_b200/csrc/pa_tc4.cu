@@ -1,0 +1,958 @@
+// Degree-4 symmetric power (SPOW_4, d = e = 32, D = 52360) on the tensor
+// cores: the chunk-state GEMMs of the fp32 pipeline (pa_simt.cu) with the
+// feature expansion generated on chip -- phi(X) never reaches HBM.
+//
+//   update_state (reference _core.pyx:18-43, kernels.py:55-83):
+//       S_k[f][u] = sum_j w_f x_a x_b x_c x_d (j) U_j[u],  U_j = W_j [v_j | 1]
+//   query-state VJP dA (gradients.py:406-431):  the same contraction with
+//       X = sigma q, U_j = c_j [dnum_j | dden_j], written to the slot before the chunk
+//
+// One CTA = one tile of 128 NDMI features (reference expansions.py:106-123 order)
+// x one (stream, chunk): M = 128 features on the TMEM lanes, K = the chunk's
+// tokens, N = 48 (33 value + key-sum columns, zero padded).  A = phi'(X)^T is
+// generated into TMEM by four warps (one per lane quadrant) from the chunk's
+// X^T tiles in shared memory (three HMUL2 per token pair: x_a x_b x_c x_d);
+// B = the U rows (MN-major).  X and U are staged by k_tc4_prep as fp16 with a
+// per-(stream, chunk) power-of-two scale (so x^4 and U keep fp16 precision for
+// any input range), undone with the SPOW weight w_f in the fp32 epilogue.
+#include <cuda.h>
+#include <math.h>
+
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "pa_common.cuh"
+#include "pa_simt.cuh"
+#include "pa_sm100.cuh"
+#include "pa_tc.cuh"
+#include "pa_tc_common.cuh"
+
+namespace pa {
+using namespace sm100;
+
+namespace t4 {
+constexpr int DX = 32;                // d = e = 32
+constexpr int TOK = 64;               // tokens per stage
+constexpr int XT_B = DX * TOK * 2;    // X^T stage: 32 dims x 64 tokens fp16 (SW128 rows)
+constexpr int UB_B = TOK * 128;       // U stage: 64 tokens x 64 fp16 (SW128 rows)
+constexpr int ST = 4;                 // stages
+constexpr int NB = 4;                 // TMEM A buffers (one stage each, 32 columns)
+constexpr int NCOL = 48;              // MMA N: 33 columns used
+constexpr int UC = 64;                // U row width (fp16)
+constexpr int THREADS = 192;          // w0 TMA + TMEM, w1 MMA, w2..w5 generate + epilogue
+constexpr int SMEM = 1024 + ST * (XT_B + UB_B) + 512;
+// VJP GEMMs (k_tc4_vjp): dphi = U S^T in TMEM, expand-VJP on the CUDA cores
+constexpr int VS = 2;                 // B stages
+constexpr int VR = 36;                // fp32 per private row (x and dx; 144-byte rows)
+constexpr int VTHREADS = 320;         // w0 TMA + TMEM, w1 MMA, w2..w9 expand-VJP
+constexpr int VSMEM = 1024 + 16384 + VS * 16384 + 3 * 128 * VR * 4 + 512;
+// token-major GEMMs (k_tc4_tok): B = fp16 states [slot][64] in stages of 128 slots
+constexpr int SL = 128;
+constexpr int BST = SL * 128;         // 16 KB
+constexpr int TS = 4;                 // B stages
+constexpr int TNB = 3;                // TMEM A buffers (64 columns = 128 slots each)
+constexpr int TTHREADS = 320;         // w0 TMA + TMEM, w1 MMA, w2..w9 generate (w2..w5 + epilogue)
+constexpr int XR = 36;                // fp16 per private token row (32 + pad: 72-byte rows, 8-byte loads
+                                      // from 32 lanes hit 16 distinct bank pairs)
+constexpr int TSMEM = 1024 + TS * BST + 128 * XR * 2 + 512;
+}  // namespace t4
+
+bool tc4_supported(const Geo& g, int dtype) {
+  static const bool disabled = [] {
+    const char* e = getenv("PA_DISABLE_TC");
+    return e && e[0] == '1';
+  }();
+  return !disabled && dtype == 1 && g.p == 4 && g.d == t4::DX && g.e == t4::DX && g.c % t4::TOK == 0 &&
+         g.t % g.c == 0;
+}
+
+// 2^-floor(log2 m) (m * s in [1, 2)); 1 for m = 0
+__device__ __forceinline__ float pow2_inv(float m) {
+  if (!(m > 0.f)) return 1.f;
+  const int e = ((__float_as_int(m) >> 23) & 255) - 127;
+  return __int_as_float((127 - e) << 23);
+}
+
+// ---------------------------------------------------------------- slot order
+// The tensor-core degree-4 pipeline orders features in blocks of four: block
+// (a, b, c, beta) holds the slots x_a x_b x_c x_d for d = 4 beta .. 4 beta + 3
+// (a <= b <= c, 4 beta + 3 >= c), blocks in lexicographic order.  Slots with
+// d < c repeat a feature and carry weight 0, so each NDMI feature (reference
+// expansions.py:106-123) appears once with its weight sqrt(4! / prod hist!)
+// (149-163); 62016 slots for D = 52360.  A token's slot row is generated from
+// one triple product per (a, b, c) and one 8-byte load per block.
+struct Tc4Tab {
+  int* idx = nullptr;        // [slots][4]
+  float* wt = nullptr;       // [slots]
+  uint32_t* blk = nullptr;   // [slots / 4]: a | b << 8 | c << 16 | beta << 24
+};
+static std::vector<uint32_t> tc4_blocks() {
+  std::vector<uint32_t> v;
+  for (int a = 0; a < t4::DX; ++a)
+    for (int b = a; b < t4::DX; ++b)
+      for (int c = b; c < t4::DX; ++c)
+        for (int be = c / 4; be < t4::DX / 4; ++be) v.push_back((uint32_t)(a | b << 8 | c << 16 | be << 24));
+  return v;
+}
+int tc4_slots() {
+  static const int n = (int)tc4_blocks().size() * 4;
+  return n;
+}
+static int tc4_padded_slots() { return (tc4_slots() + 127) / 128 * 128; }
+static const Tc4Tab* tc4_tab() {
+  static std::mutex mu;
+  static std::map<int, Tc4Tab> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return &it->second;
+  const std::vector<uint32_t> blk = tc4_blocks();
+  const int ns = (int)blk.size() * 4;
+  std::vector<int> idx((size_t)ns * 4);
+  std::vector<float> wt(ns);
+  for (size_t i = 0; i < blk.size(); ++i) {
+    const int a = blk[i] & 255, b = (blk[i] >> 8) & 255, c = (blk[i] >> 16) & 255, be = blk[i] >> 24;
+    for (int z = 0; z < 4; ++z) {
+      const int d = 4 * be + z, f = (int)i * 4 + z;
+      const int o[4] = {a, b, c, d};
+      for (int y = 0; y < 4; ++y) idx[(size_t)f * 4 + y] = o[y];
+      if (d < c) {
+        wt[f] = 0.f;
+        continue;
+      }
+      double den = 1;
+      int run = 1;
+      for (int y = 1; y < 4; ++y) {
+        run = (o[y] == o[y - 1]) ? run + 1 : 1;
+        den *= run;
+      }
+      wt[f] = (float)sqrt(24.0 / den);
+    }
+  }
+  Tc4Tab t;
+  if (cudaMalloc(&t.idx, sizeof(int) * idx.size()) != cudaSuccess ||
+      cudaMalloc(&t.wt, sizeof(float) * wt.size()) != cudaSuccess ||
+      cudaMalloc(&t.blk, sizeof(uint32_t) * blk.size()) != cudaSuccess ||
+      cudaMemcpy(t.idx, idx.data(), sizeof(int) * idx.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(t.wt, wt.data(), sizeof(float) * wt.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(t.blk, blk.data(), sizeof(uint32_t) * blk.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(t.idx);
+    cudaFree(t.wt);
+    cudaFree(t.blk);
+    return nullptr;
+  }
+  return &cache.emplace(dev, t).first->second;
+}
+
+int tc4_copy_tables(int* idx, float* wt, cudaStream_t st) {
+  const Tc4Tab* t = tc4_tab();
+  if (!t) {
+    set_error("degree-4 slot table upload failed");
+    return 3;
+  }
+  cudaMemcpyAsync(idx, t->idx, sizeof(int) * 4 * tc4_slots(), cudaMemcpyDeviceToDevice, st);
+  cudaMemcpyAsync(wt, t->wt, sizeof(float) * tc4_slots(), cudaMemcpyDeviceToDevice, st);
+  return cuda_check("degree-4 slot table");
+}
+
+// Per (chunk, stream): X^T [(s n + k) 32 + dim][c] fp16 and U rows [s t + j][64]
+// fp16, each with its own power-of-two scale: scl[s n + k] = (sx, su).
+//   fwd (kBwd = 0): X = k,  U_j = W_j [v_j | 1],   W_j = exp(ell_end - ell_j)
+//   bwd (kBwd = 1): X = q,  U_j = c_j dz_j (33),   c_j = exp(ell_j); dz fp32 [ns][t][33]
+template <bool kBwd>
+__global__ void __launch_bounds__(256) k_tc4_prep(Geo g, const __nv_bfloat16* __restrict__ x,
+                                                  const __nv_bfloat16* __restrict__ v, const float* __restrict__ dz,
+                                                  const float* __restrict__ ell, const float* __restrict__ lamlog,
+                                                  __half* xt, __half* ub, float2* scl_out) {
+  using namespace t4;
+  __shared__ float red[8];
+  __shared__ float scl[2];
+  float2* sc_out = scl_out;
+  __shared__ uint16_t tile[DX][TOK + 2];
+  const int k = blockIdx.x, s = blockIdx.y, tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  const int c0 = k * g.c;
+  const float lend = (!kBwd && g.gated) ? lamlog[s * g.n + k] : 0.f;
+  auto ufac = [&](int j) {   // per-token factor of U
+    if (!g.gated) return 1.f;
+    const float lj = ell[(size_t)s * g.t + j];
+    return kBwd ? __expf(lj) : __expf(lend - lj);
+  };
+  // pass 1: max |x|, max |U|
+  float mx = 0.f, mu = 0.f;
+  for (int i = tid; i < g.c * DX; i += 256) {
+    const int j = c0 + i / DX, a = i % DX;
+    mx = fmaxf(mx, fabsf(__bfloat162float(x[rowid(g, s, j) * DX + a])));
+  }
+  for (int i = tid; i < g.c * (DX + 1); i += 256) {
+    const int j = c0 + i / (DX + 1), u = i % (DX + 1);
+    float val;
+    if (kBwd) val = dz[((size_t)s * g.t + j) * (DX + 1) + u];
+    else val = u < DX ? __bfloat162float(v[rowid(g, s, j) * DX + u]) : 1.f;
+    mu = fmaxf(mu, fabsf(val * ufac(j)));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mu = fmaxf(mu, __shfl_xor_sync(0xffffffffu, mu, o));
+  }
+  if (l == 0) {
+    red[w] = mx;
+    if (w == 0) scl[0] = 0.f;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    float m = 0.f;
+    for (int i = 0; i < 8; ++i) m = fmaxf(m, red[i]);
+    scl[0] = pow2_inv(m);
+  }
+  __syncthreads();
+  if (l == 0) red[w] = mu;
+  __syncthreads();
+  if (tid == 0) {
+    float m = 0.f;
+    for (int i = 0; i < 8; ++i) m = fmaxf(m, red[i]);
+    scl[1] = pow2_inv(m);
+    sc_out[s * g.n + k] = make_float2(scl[0], scl[1]);
+  }
+  __syncthreads();
+  const float sx = scl[0], su = scl[1];
+  // pass 2: X^T through a shared tile of 64 tokens, U rows straight through
+  __half* xdst = xt + (size_t)(s * g.n + k) * DX * g.c;
+  for (int j0 = 0; j0 < g.c; j0 += TOK) {
+    for (int i = tid; i < TOK * DX; i += 256) {
+      const int jj = i / DX, a = i % DX;
+      tile[a][jj] = __half_as_ushort(__float2half_rn(sx * __bfloat162float(x[rowid(g, s, c0 + j0 + jj) * DX + a])));
+    }
+    __syncthreads();
+    for (int i = tid; i < TOK * DX; i += 256) {
+      const int a = i / TOK, jj = i % TOK;
+      ((uint16_t*)xdst)[(size_t)a * g.c + j0 + jj] = tile[a][jj];
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < g.c * UC; i += 256) {
+    const int j = c0 + i / UC, u = i % UC;
+    float val = 0.f;
+    if (kBwd) {
+      if (u <= DX) val = dz[((size_t)s * g.t + j) * (DX + 1) + u];
+    } else {
+      if (u < DX) val = __bfloat162float(v[rowid(g, s, j) * DX + u]);
+      else if (u == DX) val = 1.f;
+    }
+    ub[((size_t)s * g.t + j) * UC + u] = __float2half_rn(val * ufac(j) * su);
+  }
+}
+
+// grid (feature tiles, chunks, streams); kBwd: chunk kin = blockIdx.y + 1 writes slot kin - 1
+template <bool kBwd>
+__global__ void __launch_bounds__(t4::THREADS) k_tc4_state(const __grid_constant__ CUtensorMap tm_xt,
+                                                           const __grid_constant__ CUtensorMap tm_ub, Geo g,
+                                                           const int* __restrict__ idx, const float* __restrict__ wt,
+                                                           const float2* __restrict__ scl, float xs4, float* out) {
+  using namespace t4;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* xt_s = smem;
+  uint8_t* ub_s = xt_s + ST * XT_B;
+  uint64_t* bars = (uint64_t*)(ub_s + ST * UB_B);
+  uint64_t* full = bars;             // ST
+  uint64_t* empty = full + ST;       // ST
+  uint64_t* afull = empty + ST;      // NB: 4 generating warps
+  uint64_t* aempty = afull + NB;     // NB
+  uint64_t* fin = aempty + NB;       // 1
+  __shared__ uint32_t tmem_base;
+
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  const int tile = blockIdx.x, kin = blockIdx.y + (kBwd ? 1 : 0), s = blockIdx.z;
+  const int kout = kBwd ? kin - 1 : kin;
+  const int nst = g.c / TOK;
+  if (w == 0) tmem_alloc<256>(&tmem_base);
+  if (tid == 0) {
+    for (int i = 0; i < ST; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < NB; ++i) {
+      mbar_init(&afull[i], 4);
+      mbar_init(&aempty[i], 1);
+    }
+    mbar_init(fin, 1);
+    fence_barrier_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tmem_base;   // accumulator [0, 64), A buffers [64 + 32 b, ...)
+
+  if (w == 0) {
+    if (l < 2) {
+      if (l == 0) {
+        tma_prefetch(&tm_xt);
+        tma_prefetch(&tm_ub);
+      }
+      const int xrow = (s * g.n + kin) * DX;
+      for (int j = 0; j < nst; ++j) {
+        const int st = j % ST;
+        if (j >= ST) mbar_wait(&empty[st], ((j / ST) + 1) & 1);
+        if (l == 0) mbar_expect_tx(&full[st], XT_B + UB_B);
+        __syncwarp(3u);
+        if (l == 0) tma_load_2d(xt_s + st * XT_B, &tm_xt, &full[st], j * TOK, xrow);
+        if (l == 1) tma_load_2d(ub_s + st * UB_B, &tm_ub, &full[st], 0, s * g.t + kin * g.c + j * TOK);
+      }
+    }
+  } else if (w == 1) {
+    constexpr uint32_t idn = idesc_f16(128, NCOL, false, true);   // A TMEM, B MN-major
+    const uint64_t b0 = smem_desc(smem_u32(ub_s), 8192, 1024, 2);
+    for (int j = 0; j < nst; ++j) {
+      const int st = j % ST, bf = j % NB;
+      mbar_wait_w(&full[st], (j / ST) & 1);
+      mbar_wait_w(&afull[bf], (j / NB) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < TOK / 16; ++kk)
+        mma_ts_w(tm, tm + 64u + (uint32_t)(bf * 32 + kk * 8), b0 + (uint64_t)((st * UB_B + kk * 2048) >> 4), idn,
+                 (j > 0 || kk > 0) ? 1u : 0u);
+      tc_commit_w(&empty[st]);
+      tc_commit_w(&aempty[bf]);
+    }
+    tc_commit_w(fin);
+  } else {
+    // generators: lane quadrant q = w % 4; this thread's feature f and its four dims
+    const int q = w & 3, row = q * 32 + l, f = tile * 128 + row;
+    const bool live = f < g.D;
+    const int fi = live ? f : 0;
+    const int ia = idx[fi * 4], ib = idx[fi * 4 + 1], ic = idx[fi * 4 + 2], id = idx[fi * 4 + 3];
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    for (int j = 0; j < nst; ++j) {
+      const int st = j % ST, bf = j % NB;
+      mbar_wait(&full[st], (j / ST) & 1);
+      if (j >= NB) mbar_wait(&aempty[bf], ((j / NB) + 1) & 1);
+      const uint8_t* xs = xt_s + st * XT_B;
+      uint32_t o[32];
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {   // 8 tokens per 16-byte chunk
+        const uint4 va = *(const uint4*)(xs + sw128_off(ia, ch));
+        const uint4 vb = *(const uint4*)(xs + sw128_off(ib, ch));
+        const uint4 vc = *(const uint4*)(xs + sw128_off(ic, ch));
+        const uint4 vd = *(const uint4*)(xs + sw128_off(id, ch));
+        o[ch * 4 + 0] = hmul2_f16(hmul2_f16(va.x, vb.x), hmul2_f16(vc.x, vd.x));
+        o[ch * 4 + 1] = hmul2_f16(hmul2_f16(va.y, vb.y), hmul2_f16(vc.y, vd.y));
+        o[ch * 4 + 2] = hmul2_f16(hmul2_f16(va.z, vb.z), hmul2_f16(vc.z, vd.z));
+        o[ch * 4 + 3] = hmul2_f16(hmul2_f16(va.w, vb.w), hmul2_f16(vc.w, vd.w));
+      }
+      tmem_st32(tm + 64u + (uint32_t)(bf * 32) + lane_off, o);
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (l == 0) mbar_arrive(&afull[bf]);
+    }
+    // epilogue: 33 fp32 columns x w_f x the chunk's scale factors, staged so the
+    // tile's 128 x 33 block goes out as one contiguous, coalesced run
+    mbar_wait(fin, 0);
+    tc_fence_after();
+    float* stg = (float*)smem;   // [128][33] over the drained stages
+    const float2 sc = scl[s * g.n + kin];
+    const float fw = live ? wt[f] * xs4 / (sc.x * sc.x * sc.x * sc.x * sc.y) : 0.f;
+#pragma unroll
+    for (int c0 = 0; c0 < 48; c0 += 16) {
+      uint32_t r[16];
+      tmem_ld16(tm + lane_off + c0, r);
+      tc_wait_ld();
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        if (c0 + c <= DX) stg[row * (DX + 1) + c0 + c] = fw * __uint_as_float(r[c]);
+    }
+    named_bar(1, 128);
+    const int nf = min(128, g.D - tile * 128);
+    float* dst = out + (((size_t)s * g.n + kout) * g.D + (size_t)tile * 128) * (DX + 1);
+    for (int i = tid - 64; i < nf * (DX + 1); i += 128) dst[i] = stg[i];
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (w == 0) tmem_dealloc<256>(tm);
+}
+
+// ---------------------------------------------------------------- fp16 states
+// States (fp32 [sk][slots][33]) as the fp16 B operand of the token-major GEMMs:
+// bs[sk][slot][0..63] = w_slot x state x sB(sk), sB a power of two from the
+// block's max (pass 1), zero in the padding columns and slots.
+__global__ void __launch_bounds__(256) k_tc4_max(int D, const float* __restrict__ A, const float* __restrict__ wt,
+                                                 unsigned* mx) {
+  __shared__ float red[8];
+  const int sk = blockIdx.y;
+  const float* a = A + (size_t)sk * D * 33;
+  float m = 0.f;
+  for (size_t i = blockIdx.x * 256 + threadIdx.x; i < (size_t)D * 33; i += (size_t)gridDim.x * 256)
+    m = fmaxf(m, fabsf(a[i] * wt[i / 33]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < 8; ++i) m = fmaxf(m, red[i]);
+    atomicMax(mx + sk, __float_as_uint(m));
+  }
+}
+__global__ void __launch_bounds__(256) k_tc4_to16(int D, int Dp, const float* __restrict__ A,
+                                                  const float* __restrict__ wt, const unsigned* __restrict__ mx,
+                                                  __half* bs, float* sb) {
+  const int sk = blockIdx.y;
+  const float sB = pow2_inv(__uint_as_float(mx[sk]));
+  if (blockIdx.x == 0 && threadIdx.x == 0) sb[sk] = sB;
+  const float* a = A + (size_t)sk * D * 33;
+  uint32_t* o = (uint32_t*)bs + (size_t)sk * Dp * 32;
+  for (size_t i = blockIdx.x * 256 + threadIdx.x; i < (size_t)Dp * 32; i += (size_t)gridDim.x * 256) {
+    const int f = (int)(i >> 5), c2 = (int)(i & 31) * 2;
+    float v0 = 0.f, v1 = 0.f;
+    if (f < D && c2 < 33) {
+      const float w = wt[f] * sB;
+      v0 = a[(size_t)f * 33 + c2] * w;
+      if (c2 + 1 < 33) v1 = a[(size_t)f * 33 + c2 + 1] * w;
+    }
+    o[i] = pack_f16(v0, v1);
+  }
+}
+
+// ---------------------------------------------------------------- token-major GEMM
+// Y[m][u] = sum_slot phi'_slot(x_m) bs[slot][u]: M = 128 tokens on the TMEM
+// lanes, K = slots, N = 48.  A = phi'(x) generated into TMEM by four warps from
+// each token's row (fp16, scaled by a power of two into [1, 2)) in private
+// shared memory: per block (a, b, c, beta) one 8-byte load and two HMUL2 with the
+// cached triple product x_a x_b x_c.  B = the fp16 states, TMA-staged.
+//   kMode 0 (query_state + combine, chunked.py:372-395): x = q, states A_{k-1};
+//            y = (yat + gp sigma^4 Y) / R in the epilogue (the fp32 path's combine)
+//   kMode 1 (update-state VJP, dv, gradients.py:191-213): x = k, states dS_k;
+//            dv32 += W_j Y
+// grid (c / 128 token tiles, chunks, streams)
+template <int kMode>
+__global__ void __launch_bounds__(t4::TTHREADS) k_tc4_tok(const __grid_constant__ CUtensorMap tm_bs, Geo g,
+                                                          const __nv_bfloat16* __restrict__ x,
+                                                          const uint32_t* __restrict__ blk, int nblk,
+                                                          const float* __restrict__ sb, const float* __restrict__ ell,
+                                                          const float* __restrict__ lamlog,
+                                                          const float* __restrict__ yat, __nv_bfloat16* y,
+                                                          float* rowsum, float* y32, int* zflag, float* dv32) {
+  using namespace t4;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* bs_s = smem;
+  __half* xr_s = (__half*)(bs_s + TS * BST);
+  uint64_t* bars = (uint64_t*)(xr_s + 128 * XR);
+  uint64_t* full = bars;             // TS
+  uint64_t* empty = full + TS;       // TS
+  uint64_t* afull = empty + TS;      // TNB: 4 generating warps
+  uint64_t* aempty = afull + TNB;    // TNB
+  uint64_t* fin = aempty + TNB;      // 1
+  __shared__ uint32_t tmem_base;
+
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  const int tile = blockIdx.x, k = blockIdx.y, s = blockIdx.z;
+  const int kst = kMode == 0 ? k - 1 : k;
+  const bool has = kst >= 0;
+  const int Dp = (g.D + 127) / 128 * 128, nst = has ? Dp / SL : 0;
+  if (w == 0) tmem_alloc<256>(&tmem_base);
+  if (tid == 0) {
+    for (int i = 0; i < TS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < TNB; ++i) {
+      mbar_init(&afull[i], 8);
+      mbar_init(&aempty[i], 1);
+    }
+    mbar_init(fin, 1);
+    fence_barrier_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tmem_base;   // accumulator [0, 64), A buffers [64 + 64 b, ...)
+
+  if (w == 0) {
+    if (l == 0 && has) {
+      tma_prefetch(&tm_bs);
+      const int row0 = (s * g.n + kst) * Dp;
+      for (int j = 0; j < nst; ++j) {
+        const int st = j % TS;
+        if (j >= TS) mbar_wait(&empty[st], ((j / TS) + 1) & 1);
+        mbar_expect_tx(&full[st], BST);
+        tma_load_2d(bs_s + st * BST, &tm_bs, &full[st], 0, row0 + j * SL);
+      }
+    }
+  } else if (w == 1) {
+    if (has) {
+      constexpr uint32_t idn = idesc_f16(128, NCOL, false, true);   // A TMEM, B MN-major
+      const uint64_t b0 = smem_desc(smem_u32(bs_s), 8192, 1024, 2);
+      for (int j = 0; j < nst; ++j) {
+        const int st = j % TS, bf = j % TNB;
+        mbar_wait_w(&full[st], (j / TS) & 1);
+        mbar_wait_w(&afull[bf], (j / TNB) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < SL / 16; ++kk)
+          mma_ts_w(tm, tm + 64u + (uint32_t)(bf * 64 + kk * 8), b0 + (uint64_t)((st * BST + kk * 2048) >> 4), idn,
+                   (j > 0 || kk > 0) ? 1u : 0u);
+        tc_commit_w(&empty[st]);
+        tc_commit_w(&aempty[bf]);
+      }
+    }
+    tc_commit_w(fin);
+  } else {
+    // eight warps: lane quadrant q, half gsub of every stage's 128 slots
+    const int q = w & 3, gsub = (w - 2) >> 2, row = q * 32 + l;
+    const int m = k * g.c + tile * 128 + row;   // token of this lane
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    __half* xr = xr_s + row * XR;
+    float sx;
+    {
+      const uint4* src = (const uint4*)(x + rowid(g, s, m) * DX);
+      // (both warps of a quadrant stage the same row; identical values)
+      uint4 v4[4];
+      float mx = 0.f;
+#pragma unroll
+      for (int c8 = 0; c8 < 4; ++c8) {
+        v4[c8] = src[c8];
+        const uint32_t* pv = (const uint32_t*)&v4[c8];
+#pragma unroll
+        for (int e2 = 0; e2 < 4; ++e2) {
+          const float2 f2 = __bfloat1622float2(*(const __nv_bfloat162*)&pv[e2]);
+          mx = fmaxf(mx, fmaxf(fabsf(f2.x), fabsf(f2.y)));
+        }
+      }
+      sx = pow2_inv(mx);
+#pragma unroll
+      for (int c8 = 0; c8 < 4; ++c8) {
+        const uint32_t* pv = (const uint32_t*)&v4[c8];
+        uint32_t o[4];
+#pragma unroll
+        for (int e2 = 0; e2 < 4; ++e2) {
+          const float2 f2 = __bfloat1622float2(*(const __nv_bfloat162*)&pv[e2]);
+          o[e2] = pack_f16(f2.x * sx, f2.y * sx);
+        }
+        *(uint2*)(xr + c8 * 8) = make_uint2(o[0], o[1]);
+        *(uint2*)(xr + c8 * 8 + 4) = make_uint2(o[2], o[3]);
+      }
+    }
+    __syncwarp();
+    uint32_t prev = 0xffffffffu, p3 = 0u;
+    for (int j = 0; j < nst; ++j) {
+      const int bf = j % TNB;
+      const int bi = j * (SL / 4) + gsub * (SL / 8) + (l & 15);
+      const uint32_t mye = (l < 16 && bi < nblk) ? __ldg(blk + bi) : 0xffffffffu;
+      if (j >= TNB) mbar_wait(&aempty[bf], ((j / TNB) + 1) & 1);
+      uint32_t o[32];
+#pragma unroll
+      for (int i = 0; i < SL / 8; ++i) {
+        const uint32_t e = __shfl_sync(0xffffffffu, mye, i);
+        if (e == 0xffffffffu) {   // padding slots past the table
+          o[2 * i] = o[2 * i + 1] = 0u;
+          continue;
+        }
+        const uint32_t abc = e & 0xffffffu;
+        if (abc != prev) {
+          prev = abc;
+          const __half t = __hmul(__hmul(xr[abc & 255], xr[(abc >> 8) & 255]), xr[abc >> 16]);
+          const __half2 t2 = __half2half2(t);
+          p3 = *(const uint32_t*)&t2;
+        }
+        const uint2 pr = *(const uint2*)(xr + 4 * (e >> 24));
+        o[2 * i] = hmul2_f16(p3, pr.x);
+        o[2 * i + 1] = hmul2_f16(p3, pr.y);
+      }
+      // this warp's half of the stage: 64 slots = 32 TMEM columns
+      tmem_st32(tm + 64u + (uint32_t)(bf * 64 + gsub * 32) + lane_off, o);
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (l == 0) mbar_arrive(&afull[bf]);
+    }
+    // epilogue (the gsub 0 warps)
+    if (!gsub) {
+    mbar_wait(fin, 0);
+    tc_fence_after();
+    float acc[DX + 1];
+    {
+      uint32_t r[16];
+#pragma unroll
+      for (int c0 = 0; c0 < 48; c0 += 16) {
+        tmem_ld16(tm + lane_off + c0, r);
+        tc_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          if (c0 + c <= DX) acc[c0 + c] = has ? __uint_as_float(r[c]) : 0.f;
+      }
+    }
+    const float sx2 = sx * sx;
+    const float fsc = has ? 1.f / (sx2 * sx2 * sb[s * g.n + kst]) : 0.f;
+    const size_t it = (size_t)s * g.t + m;
+    if (kMode == 0) {
+      const float s2 = g.scale * g.scale;
+      const float gp = g.gated ? __expf(ell[it]) : 1.f;
+      const float f = gp * s2 * s2 * fsc;   // phi(sigma q) = sigma^4 phi(q)
+      const float* ya = yat + it * (DX + 1);
+      const float R = ya[DX] + f * acc[DX];
+      const size_t r = rowid(g, s, m);
+      if (rowsum) rowsum[r] = R;
+      float inv = 1.f;
+      if (g.normalize) {
+        if (!(R > 0.f)) atomicAdd(zflag, 1);
+        inv = 1.f / R;
+      }
+      uint32_t ob[16];
+#pragma unroll
+      for (int u = 0; u < DX; u += 2) {
+        const float y0 = (ya[u] + f * acc[u]) * inv, y1 = (ya[u + 1] + f * acc[u + 1]) * inv;
+        ob[u / 2] = pack_bf16(y0, y1);
+        if (g.normalize) *(float2*)(y32 + it * DX + u) = make_float2(y0, y1);
+      }
+      uint4* dst = (uint4*)(y + r * DX);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) dst[c] = make_uint4(ob[4 * c], ob[4 * c + 1], ob[4 * c + 2], ob[4 * c + 3]);
+    } else {
+      const float W = g.gated ? __expf(lamlog[s * g.n + k] - ell[it]) : 1.f;
+      float* o = dv32 + it * DX;
+#pragma unroll
+      for (int u = 0; u < DX; ++u) o[u] += W * fsc * acc[u];
+    }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (w == 0) tmem_dealloc<256>(tm);
+}
+
+// ---------------------------------------------------------------- state VJP
+// Token-side state VJP (reference expand_vjp gradients.py:46-76 with the
+// query-state VJP 406-431 and the update-state VJP 191-213):
+//   dphi_m[slot] = sum_u U_m[u] S[slot][u]  -- tcgen05, M = 128 tokens, N = 128
+//                  slots per stage, K = 48 (U rows and the fp16 states from smem)
+//   dx_m += sum_slot dphi_m[slot] d phi'_slot(x_m) / dx  -- CUDA cores, per block
+//           (a, b, c, beta): dx_d += dphi P3 for the four d, and the triple's
+//           T = sum dphi x_d feeds dx_a, dx_b, dx_c once per (a, b, c)
+//   dl_m = sum_slot phi'_slot(x_m) dphi_m[slot]   (the log-gate cotangent term)
+// kUpd = false (query side): x = sigma q, U = c dz, S = A_{k-1}: dq32 += sigma dx,
+//                            dell += dl
+// kUpd = true  (update side): x = k, U = W [v | 1], S = dS_k:  dk32 += dx,
+//                            dellend[chunk] += sum dl
+template <bool kUpd>
+__global__ void __launch_bounds__(t4::VTHREADS) k_tc4_vjp(const __grid_constant__ CUtensorMap tm_ub,
+                                                          const __grid_constant__ CUtensorMap tm_bs, Geo g,
+                                                          const __nv_bfloat16* __restrict__ x,
+                                                          const uint32_t* __restrict__ blk, int nblk,
+                                                          const float* __restrict__ sb,
+                                                          const float2* __restrict__ scl, float* dx32, float* dell,
+                                                          float* dellend) {
+  using namespace t4;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* ub_s = smem;                    // 128 tokens x 64 fp16
+  uint8_t* bs_s = ub_s + 16384;            // VS stages of 128 slots x 64 fp16
+  float* xr_s = (float*)(bs_s + VS * 16384);
+  float* dr_s = xr_s + 128 * VR;           // [2 halves][128][VR]
+  uint64_t* bars = (uint64_t*)(dr_s + 2 * 128 * VR);
+  uint64_t* ufull = bars;            // 1
+  uint64_t* full = ufull + 1;        // VS
+  uint64_t* empty = full + VS;       // VS
+  uint64_t* accf = empty + VS;       // 2
+  uint64_t* acce = accf + 2;         // 2: 4 warps
+  __shared__ uint32_t tmem_base;
+  __shared__ float red[8];
+
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  const int tile = blockIdx.x, k = blockIdx.y + (kUpd ? 0 : 1), s = blockIdx.z;
+  const int kst = kUpd ? k : k - 1;
+  const int Dp = (g.D + 127) / 128 * 128, nst = Dp / SL;
+  if (w == 0) tmem_alloc<256>(&tmem_base);
+  if (tid == 0) {
+    mbar_init(ufull, 1);
+    for (int i = 0; i < VS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&accf[i], 1);
+      mbar_init(&acce[i], 8);
+    }
+    fence_barrier_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tmem_base;   // dphi buffers [128 b, 128 b + 128)
+  const int m0 = k * g.c + tile * 128;
+
+  if (w == 0) {
+    if (l == 0) {
+      tma_prefetch(&tm_ub);
+      tma_prefetch(&tm_bs);
+      mbar_expect_tx(ufull, 16384);
+      tma_load_2d(ub_s, &tm_ub, ufull, 0, s * g.t + m0);
+      const int row0 = (s * g.n + kst) * Dp;
+      for (int j = 0; j < nst; ++j) {
+        const int st = j % VS;
+        if (j >= VS) mbar_wait(&empty[st], ((j / VS) + 1) & 1);
+        mbar_expect_tx(&full[st], 16384);
+        tma_load_2d(bs_s + st * 16384, &tm_bs, &full[st], 0, row0 + j * SL);
+      }
+    }
+  } else if (w == 1) {
+    constexpr uint32_t idk = idesc_f16(128, 128, false, false);   // both K-major
+    const uint64_t a0 = smem_desc(smem_u32(ub_s), 16, 1024, 2);
+    const uint64_t b0 = smem_desc(smem_u32(bs_s), 16, 1024, 2);
+    mbar_wait_w(ufull, 0);
+    for (int j = 0; j < nst; ++j) {
+      const int st = j % VS, bf = j & 1;
+      mbar_wait_w(&full[st], (j / VS) & 1);
+      if (j >= 2) mbar_wait_w(&acce[bf], ((j >> 1) + 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < 3; ++kk)   // K = 48 (33 columns used)
+        mma_ss_w(tm + (uint32_t)(bf * 128), a0 + (uint64_t)(kk * 2), b0 + (uint64_t)((st * 16384) >> 4) + kk * 2,
+                 idk, kk > 0 ? 1u : 0u);
+      tc_commit_w(&empty[st]);
+      tc_commit_w(&accf[bf]);
+    }
+  } else {
+    // eight warps: lane quadrant q, half gsub of every stage's 128 slots; each
+    // half keeps its own dx row, summed at the end
+    const int q = w & 3, gsub = (w - 2) >> 2, row = q * 32 + l, m = m0 + row;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    float* xr = xr_s + row * VR;
+    float* dr = dr_s + (gsub * 128 + row) * VR;
+    {
+      const float xs = kUpd ? 1.f : g.scale;
+      const uint4* src = (const uint4*)(x + rowid(g, s, m) * DX);
+#pragma unroll
+      for (int c8 = 0; c8 < 4; ++c8) {
+        const uint4 v4 = src[c8];
+        const uint32_t* pv = (const uint32_t*)&v4;
+#pragma unroll
+        for (int e2 = 0; e2 < 4; ++e2) {
+          const float2 f2 = __bfloat1622float2(*(const __nv_bfloat162*)&pv[e2]);
+          if (!gsub) {
+            xr[c8 * 8 + 2 * e2] = xs * f2.x;
+            xr[c8 * 8 + 2 * e2 + 1] = xs * f2.y;
+          }
+          dr[c8 * 8 + 2 * e2] = 0.f;
+          dr[c8 * 8 + 2 * e2 + 1] = 0.f;
+        }
+      }
+    }
+    named_bar(1, 256);
+    uint32_t prev = 0xffffffffu;
+    float xa = 0.f, xb = 0.f, xc = 0.f, P3 = 0.f, T = 0.f, dl = 0.f;
+    int ia = 0, ib = 0, ic = 0;
+    auto flush = [&]() {   // the finished triple's share: d/dx_a, d/dx_b, d/dx_c and dl
+      dr[ia] += T * xb * xc;
+      dr[ib] += T * xa * xc;
+      dr[ic] += T * xa * xb;
+      dl += T * P3;
+      T = 0.f;
+    };
+    for (int j = 0; j < nst; ++j) {
+      const int bf = j & 1;
+      const int bi = j * (SL / 4) + gsub * (SL / 8) + (l & 15);
+      const uint32_t mye = (l < 16 && bi < nblk) ? __ldg(blk + bi) : 0xffffffffu;
+      mbar_wait(&accf[bf], (j >> 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c32 = 0; c32 < 2; ++c32) {
+        uint32_t r[32];
+        tmem_ld32(tm + (uint32_t)(bf * 128 + gsub * 64 + c32 * 32) + lane_off, r);
+        tc_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t e = __shfl_sync(0xffffffffu, mye, c32 * 8 + i);
+          if (e == 0xffffffffu) continue;
+          const uint32_t abc = e & 0xffffffu;
+          if (abc != prev) {
+            if (prev != 0xffffffffu) flush();
+            prev = abc;
+            ia = abc & 255;
+            ib = (abc >> 8) & 255;
+            ic = abc >> 16;
+            xa = xr[ia];
+            xb = xr[ib];
+            xc = xr[ic];
+            P3 = xa * xb * xc;
+          }
+          const int d0 = 4 * (e >> 24);
+          const float4 xd = *(const float4*)(xr + d0);
+          const float g0 = __uint_as_float(r[4 * i]), g1 = __uint_as_float(r[4 * i + 1]);
+          const float g2 = __uint_as_float(r[4 * i + 2]), g3 = __uint_as_float(r[4 * i + 3]);
+          T = fmaf(g0, xd.x, fmaf(g1, xd.y, fmaf(g2, xd.z, fmaf(g3, xd.w, T))));
+          float4 dd = *(float4*)(dr + d0);
+          dd.x = fmaf(g0, P3, dd.x);
+          dd.y = fmaf(g1, P3, dd.y);
+          dd.z = fmaf(g2, P3, dd.z);
+          dd.w = fmaf(g3, P3, dd.w);
+          *(float4*)(dr + d0) = dd;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (l == 0) mbar_arrive(&acce[bf]);
+    }
+    if (prev != 0xffffffffu) flush();
+    // combine the two halves: gsub 1 parks dl in its row's padding column
+    if (gsub) dr[DX] = dl;
+    named_bar(1, 256);
+    if (!gsub) {
+      const float* dr1 = dr_s + (128 + row) * VR;
+      dl += dr1[DX];
+      const float2 sc = scl[s * g.n + k];   // (sx, su) of the U rows of this chunk
+      const float inv = 1.f / (sc.y * sb[s * g.n + kst]);
+      const size_t it = (size_t)s * g.t + m;
+      float* o = dx32 + it * DX;
+      const float fx = inv * (kUpd ? 1.f : g.scale);
+#pragma unroll 8
+      for (int a = 0; a < DX; ++a) o[a] += fx * (dr[a] + dr1[a]);
+      dl *= inv;
+      if (!kUpd) {
+        if (g.gated) dell[it] += dl;
+      } else {
+        dl = warp_sum(dl);
+        if (l == 0) red[q] = dl;
+      }
+    }
+    if (kUpd) {
+      named_bar(1, 256);
+      if (tid == 64 && g.gated) atomicAdd(dellend + s * g.n + k, red[0] + red[1] + red[2] + red[3]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (w == 0) tmem_dealloc<256>(tm);
+}
+
+// scratch of the degree-4 pipeline (inside the forward workspace)
+struct Tc4Ws {
+  __half* xt;     // X^T [ns][n][32][c] fp16
+  __half* ubf;    // U rows of the update side  [ns][t][64] fp16 (W [v | 1])
+  __half* ubb;    // U rows of the query side   [ns][t][64] fp16 (c dz)
+  float2* sclf;   // (sx, su) per (stream, chunk), forward staging
+  float2* sclb;   // (sx, su) per (stream, chunk), backward staging
+  __half* bsa;    // forward states A_k as fp16 MMA operands [ns][n][slots_pad][64] (x w_f x sB)
+  __half* bsd;    // backward state cotangents dS_k, same layout
+  float* sba;     // sB per (stream, chunk) of bsa
+  float* sbd;     // sB per (stream, chunk) of bsd
+  unsigned* mx;   // max-reduction scratch [ns][n]
+};
+static Tc4Ws tc4_carve(const Geo& g, void* base, size_t* bytes) {
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  char* p = (char*)base;
+  size_t off = 0;
+  auto take = [&](size_t n) {
+    char* r = p ? p + off : nullptr;
+    off += al(n);
+    return r;
+  };
+  const size_t sk = (size_t)g.ns * g.n, bs = sk * tc4_padded_slots() * t4::UC * 2;
+  Tc4Ws w;
+  w.xt = (__half*)take(sk * t4::DX * g.c * 2);
+  w.ubf = (__half*)take((size_t)g.ns * g.t * t4::UC * 2);
+  w.ubb = (__half*)take((size_t)g.ns * g.t * t4::UC * 2);
+  w.sclf = (float2*)take(sk * 8);
+  w.sclb = (float2*)take(sk * 8);
+  w.bsa = (__half*)take(bs);
+  w.bsd = (__half*)take(bs);
+  w.sba = (float*)take(sk * 4);
+  w.sbd = (float*)take(sk * 4);
+  w.mx = (unsigned*)take(sk * 4);
+  *bytes = off;
+  return w;
+}
+size_t tc4_extra_bytes(const Geo& g) {
+  size_t n;
+  tc4_carve(g, nullptr, &n);
+  return n;
+}
+
+int tc4_state(const Geo& g, bool bwd, const void* x, const void* v, const float* dz, const float* ell,
+              const float* lamlog, const int* idx, const float* wt, void* scratch, float* out, cudaStream_t st) {
+  using namespace t4;
+  size_t nb;
+  Tc4Ws w = tc4_carve(g, scratch, &nb);
+  __half* ub = bwd ? w.ubb : w.ubf;
+  float2* scl = bwd ? w.sclb : w.sclf;
+  const int nk = bwd ? g.n - 1 : g.n;
+  if (bwd)
+    k_tc4_prep<true><<<dim3(g.n, g.ns), 256, 0, st>>>(g, (const __nv_bfloat16*)x, nullptr, dz, ell, lamlog, w.xt, ub,
+                                                        scl);
+  else
+    k_tc4_prep<false><<<dim3(g.n, g.ns), 256, 0, st>>>(g, (const __nv_bfloat16*)x, (const __nv_bfloat16*)v, nullptr,
+                                                         ell, lamlog, w.xt, ub, scl);
+  count_launch();
+  if (nk <= 0) return cuda_check("tc4 prep");
+  CUtensorMap m_xt, m_ub;
+  if (!tc_map_2d(&m_xt, w.xt, (size_t)g.ns * g.n * DX, g.c, TOK, DX, 0) ||
+      !tc_map_2d(&m_ub, ub, (size_t)g.ns * g.t, UC, UC, TOK, 0))
+    return 3;
+  const float s2 = bwd ? g.scale * g.scale : 1.f;
+  auto fn = bwd ? k_tc4_state<true> : k_tc4_state<false>;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  fn<<<dim3((g.D + 127) / 128, nk, g.ns), THREADS, SMEM, st>>>(m_xt, m_ub, g, idx, wt, scl, s2 * s2, out);
+  count_launch();
+  return cuda_check("tc4 state GEMM");
+}
+
+// fp32 states [ns][n][slots][33] -> fp16 MMA operands; which = 0: forward
+// states A (bsa), 1: backward cotangents dS (bsd)
+int tc4_states16(const Geo& g, int which, const float* A, const float* wt, void* scratch, cudaStream_t st) {
+  size_t nb;
+  Tc4Ws w = tc4_carve(g, scratch, &nb);
+  const int nsk = g.ns * g.n, Dp = tc4_padded_slots();
+  cudaMemsetAsync(w.mx, 0, sizeof(unsigned) * nsk, st);
+  k_tc4_max<<<dim3(32, nsk), 256, 0, st>>>(g.D, A, wt, w.mx);
+  k_tc4_to16<<<dim3(64, nsk), 256, 0, st>>>(g.D, Dp, A, wt, w.mx, which ? w.bsd : w.bsa, which ? w.sbd : w.sba);
+  count_launch(2);
+  return cuda_check("tc4 fp16 states");
+}
+
+// mode 0: y = combine(yat, phi(sigma q) A_{k-1}); mode 1: dv32 += W phi(k) dS_k
+int tc4_tok(const Geo& g, int mode, const void* x, const float* ell, const float* lamlog, const float* yat, void* y,
+            float* rowsum, float* y32, int* zflag, float* dv32, void* scratch, cudaStream_t st) {
+  using namespace t4;
+  size_t nb;
+  Tc4Ws w = tc4_carve(g, scratch, &nb);
+  const Tc4Tab* tab = tc4_tab();
+  if (!tab) return 3;
+  const int Dp = tc4_padded_slots();
+  CUtensorMap m_bs;
+  if (!tc_map_2d(&m_bs, mode ? w.bsd : w.bsa, (size_t)g.ns * g.n * Dp, UC, UC, SL, 0)) return 3;
+  auto fn = mode ? k_tc4_tok<1> : k_tc4_tok<0>;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
+  fn<<<dim3(g.c / 128, g.n, g.ns), TTHREADS, TSMEM, st>>>(m_bs, g, (const __nv_bfloat16*)x, tab->blk, tc4_slots() / 4,
+                                                         mode ? w.sbd : w.sba, ell, lamlog, yat,
+                                                         (__nv_bfloat16*)y, rowsum, y32, zflag, dv32);
+  count_launch();
+  return cuda_check("tc4 token-major GEMM");
+}
+
+// token-side state VJPs: query side (dq32, dell) or update side (dk32, dellend)
+int tc4_vjp(const Geo& g, bool upd, const void* x, float* dx32, float* dell, float* dellend, void* scratch,
+            cudaStream_t st) {
+  using namespace t4;
+  size_t nb;
+  Tc4Ws w = tc4_carve(g, scratch, &nb);
+  const Tc4Tab* tab = tc4_tab();
+  if (!tab) return 3;
+  const int nk = upd ? g.n : g.n - 1;
+  if (nk <= 0) return 0;
+  const int Dp = tc4_padded_slots();
+  CUtensorMap m_ub, m_bs;
+  if (!tc_map_2d(&m_ub, upd ? w.ubf : w.ubb, (size_t)g.ns * g.t, UC, UC, 128, 0) ||
+      !tc_map_2d(&m_bs, upd ? w.bsd : w.bsa, (size_t)g.ns * g.n * Dp, UC, UC, SL, 0))
+    return 3;
+  auto fn = upd ? k_tc4_vjp<true> : k_tc4_vjp<false>;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, VSMEM);
+  fn<<<dim3(g.c / 128, nk, g.ns), VTHREADS, VSMEM, st>>>(m_ub, m_bs, g, (const __nv_bfloat16*)x, tab->blk,
+                                                        tc4_slots() / 4, upd ? w.sbd : w.sba,
+                                                        upd ? w.sclf : w.sclb, dx32, dell, dellend);
+  count_launch();
+  return cuda_check("tc4 state VJP");
+}
+
+}  // namespace pa

@@ -74,7 +74,7 @@ def _route(pr) -> bool:
                 f"power_full: p={pr.p} d={pr.d} e={pr.e} chunk={pr.chunk} t={pr.t} dtype={pr.dtype} is outside the "
                 "tcgen05 tensor-core kernels (bf16, p=2, d=e=64, chunk a multiple of 128 up to 1024, t a multiple "
                 "of the chunk); running the fp32 CUDA-core kernels", RuntimeWarning, stacklevel=4)
-    return rc == 1
+    return rc >= 1
 
 
 def _validate(Q, K, V, log_G, p, chunk_size, normalize):

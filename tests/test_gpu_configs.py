@@ -110,13 +110,21 @@ def test_full_length_65536_state_path_visible(case):
 
 def test_config2_shape_p4_d32_c1024_slice():
     """configs[2] shape: SPOW p=4, d=32 (D=52360), c=1024, ungated, normalized,
-    on a t=2048 slice (the elementwise bar)."""
-    t, d, c = 2048, 32, 1024
+    on a t=4096 slice (the elementwise bar).  Four chunks, and
+    the check restricted to what the inter-chunk state path feeds (queries after
+    chunk 0, keys before the last chunk) as well as to everything."""
+    t, d, c = 4096, 32, 1024
     q, k, v, _ = O.generate_inputs(1, t, 1, d, d, seed=41, gating=False)
     q, k, v = _bf16_exact(q, k, v)
     dy, = _bf16_exact(np.random.default_rng(42).uniform(-1, 1, (1, t, 1, d)))
     r = _gpu_run(q, k, v, None, 4, c, True, dy)
     _compare("p=4 d=32 c=1024", r, q, k, v, None, 4, c, True, dy)
+    y_ref, _ = O.chunked_forward(q, k, v, None, 4, c, normalize=True)
+    dq, dk, dv, _ = O.chunked_backward(q, k, v, None, 4, c, dy, normalize=True)
+    st = {"y": O.max_rel_error(r["y"][:, c:], y_ref[:, c:]), "dq": O.max_rel_error(r["dq"][:, c:], dq[:, c:]),
+          "dk": O.max_rel_error(r["dk"][:, :-c], dk[:, :-c]), "dv": O.max_rel_error(r["dv"][:, :-c], dv[:, :-c])}
+    print(f"p=4 state-path rows: max_rel_error {st}")
+    assert all(e <= BF16_TOL for e in st.values()), st
 
 
 def test_sequence_parallel_8_ranks_32_chunks():
