@@ -37,11 +37,12 @@ constexpr int TOK = 64;               // tokens per stage
 constexpr int XT_B = DX * TOK * 2;    // X^T stage: 32 dims x 64 tokens fp16 (SW128 rows)
 constexpr int UB_B = TOK * 128;       // U stage: 64 tokens x 64 fp16 (SW128 rows)
 constexpr int ST = 4;                 // stages
-constexpr int NB = 4;                 // TMEM A buffers (one stage each, 32 columns)
+constexpr int NB = 2;                 // TMEM A buffers per tile (one stage each, 32 columns)
+constexpr int FT = 4;                 // feature tiles per CTA
 constexpr int NCOL = 48;              // MMA N: 33 columns used
 constexpr int UC = 64;                // U row width (fp16)
-constexpr int THREADS = 192;          // w0 TMA + TMEM, w1 MMA, w2..w5 generate + epilogue
-constexpr int SMEM = 1024 + ST * (XT_B + UB_B) + 512;
+constexpr int THREADS = 64 + 128 * FT;   // w0 TMA + TMEM, w1 MMA, 4 generate + epilogue warps per tile
+constexpr int SMEM = 1024 + ST * (XT_B + UB_B) + 16 * 32 * (DX + 1) * 4 + 512;
 // VJP GEMMs (k_tc4_vjp): dphi = U S^T in TMEM, expand-VJP on the CUDA cores
 constexpr int VS = 2;                 // B stages
 constexpr int VR = 36;                // fp32 per private row (x and dx; 144-byte rows)
@@ -245,7 +246,10 @@ __global__ void __launch_bounds__(256) k_tc4_prep(Geo g, const __nv_bfloat16* __
   }
 }
 
-// grid (feature tiles, chunks, streams); kBwd: chunk kin = blockIdx.y + 1 writes slot kin - 1
+// grid (groups of FT feature tiles, chunks, streams); kBwd: chunk kin =
+// blockIdx.y + 1 writes slot kin - 1.  The FT tiles of a CTA share every X^T / U
+// stage (one TMA pair feeds 4 x 128 slots), so the prologue and the staging are
+// amortised over 512 slots.
 template <bool kBwd>
 __global__ void __launch_bounds__(t4::THREADS) k_tc4_state(const __grid_constant__ CUtensorMap tm_xt,
                                                            const __grid_constant__ CUtensorMap tm_ub, Geo g,
@@ -256,26 +260,28 @@ __global__ void __launch_bounds__(t4::THREADS) k_tc4_state(const __grid_constant
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* xt_s = smem;
   uint8_t* ub_s = xt_s + ST * XT_B;
-  uint64_t* bars = (uint64_t*)(ub_s + ST * UB_B);
+  float* stg_s = (float*)(ub_s + ST * UB_B);   // [16 warps][32][33] epilogue staging
+  uint64_t* bars = (uint64_t*)(stg_s + 16 * 32 * (DX + 1));
   uint64_t* full = bars;             // ST
   uint64_t* empty = full + ST;       // ST
-  uint64_t* afull = empty + ST;      // NB: 4 generating warps
+  uint64_t* afull = empty + ST;      // NB: 16 generating warps
   uint64_t* aempty = afull + NB;     // NB
   uint64_t* fin = aempty + NB;       // 1
   __shared__ uint32_t tmem_base;
 
   const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
-  const int tile = blockIdx.x, kin = blockIdx.y + (kBwd ? 1 : 0), s = blockIdx.z;
+  const int grp = blockIdx.x, kin = blockIdx.y + (kBwd ? 1 : 0), s = blockIdx.z;
   const int kout = kBwd ? kin - 1 : kin;
   const int nst = g.c / TOK;
-  if (w == 0) tmem_alloc<256>(&tmem_base);
+  const int ntile = (g.D + 127) / 128, nft = min(FT, ntile - grp * FT);
+  if (w == 0) tmem_alloc<512>(&tmem_base);
   if (tid == 0) {
     for (int i = 0; i < ST; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < NB; ++i) {
-      mbar_init(&afull[i], 4);
+      mbar_init(&afull[i], 4 * FT);
       mbar_init(&aempty[i], 1);
     }
     mbar_init(fin, 1);
@@ -284,7 +290,8 @@ __global__ void __launch_bounds__(t4::THREADS) k_tc4_state(const __grid_constant
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tm = tmem_base;   // accumulator [0, 64), A buffers [64 + 32 b, ...)
+  // TMEM: tile ft's accumulator [64 ft, 64 ft + 64); its A buffers [256 + 64 ft + 32 b, ...)
+  const uint32_t tm = tmem_base;
 
   if (w == 0) {
     if (l < 2) {
@@ -310,18 +317,21 @@ __global__ void __launch_bounds__(t4::THREADS) k_tc4_state(const __grid_constant
       mbar_wait_w(&full[st], (j / ST) & 1);
       mbar_wait_w(&afull[bf], (j / NB) & 1);
       tc_fence_after();
+      for (int ft = 0; ft < nft; ++ft)
 #pragma unroll
-      for (int kk = 0; kk < TOK / 16; ++kk)
-        mma_ts_w(tm, tm + 64u + (uint32_t)(bf * 32 + kk * 8), b0 + (uint64_t)((st * UB_B + kk * 2048) >> 4), idn,
-                 (j > 0 || kk > 0) ? 1u : 0u);
+        for (int kk = 0; kk < TOK / 16; ++kk)
+          mma_ts_w(tm + (uint32_t)(ft * 64), tm + 256u + (uint32_t)(ft * 64 + bf * 32 + kk * 8),
+                   b0 + (uint64_t)((st * UB_B + kk * 2048) >> 4), idn, (j > 0 || kk > 0) ? 1u : 0u);
       tc_commit_w(&empty[st]);
       tc_commit_w(&aempty[bf]);
     }
     tc_commit_w(fin);
   } else {
-    // generators: lane quadrant q = w % 4; this thread's feature f and its four dims
-    const int q = w & 3, row = q * 32 + l, f = tile * 128 + row;
-    const bool live = f < g.D;
+    // generators: tile ft = (w - 2) / 4, lane quadrant q = w % 4; this thread's
+    // slot f and its four dims
+    const int ft = (w - 2) >> 2, q = w & 3, row = q * 32 + l;
+    const int f = (grp * FT + ft) * 128 + row;
+    const bool live = ft < nft && f < g.D;
     const int fi = live ? f : 0;
     const int ia = idx[fi * 4], ib = idx[fi * 4 + 1], ic = idx[fi * 4 + 2], id = idx[fi * 4 + 3];
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
@@ -329,49 +339,54 @@ __global__ void __launch_bounds__(t4::THREADS) k_tc4_state(const __grid_constant
       const int st = j % ST, bf = j % NB;
       mbar_wait(&full[st], (j / ST) & 1);
       if (j >= NB) mbar_wait(&aempty[bf], ((j / NB) + 1) & 1);
-      const uint8_t* xs = xt_s + st * XT_B;
-      uint32_t o[32];
+      if (ft < nft) {
+        const uint8_t* xs = xt_s + st * XT_B;
+        uint32_t o[32];
 #pragma unroll
-      for (int ch = 0; ch < 8; ++ch) {   // 8 tokens per 16-byte chunk
-        const uint4 va = *(const uint4*)(xs + sw128_off(ia, ch));
-        const uint4 vb = *(const uint4*)(xs + sw128_off(ib, ch));
-        const uint4 vc = *(const uint4*)(xs + sw128_off(ic, ch));
-        const uint4 vd = *(const uint4*)(xs + sw128_off(id, ch));
-        o[ch * 4 + 0] = hmul2_f16(hmul2_f16(va.x, vb.x), hmul2_f16(vc.x, vd.x));
-        o[ch * 4 + 1] = hmul2_f16(hmul2_f16(va.y, vb.y), hmul2_f16(vc.y, vd.y));
-        o[ch * 4 + 2] = hmul2_f16(hmul2_f16(va.z, vb.z), hmul2_f16(vc.z, vd.z));
-        o[ch * 4 + 3] = hmul2_f16(hmul2_f16(va.w, vb.w), hmul2_f16(vc.w, vd.w));
+        for (int ch = 0; ch < 8; ++ch) {   // 8 tokens per 16-byte chunk
+          const uint4 va = *(const uint4*)(xs + sw128_off(ia, ch));
+          const uint4 vb = *(const uint4*)(xs + sw128_off(ib, ch));
+          const uint4 vc = *(const uint4*)(xs + sw128_off(ic, ch));
+          const uint4 vd = *(const uint4*)(xs + sw128_off(id, ch));
+          o[ch * 4 + 0] = hmul2_f16(hmul2_f16(va.x, vb.x), hmul2_f16(vc.x, vd.x));
+          o[ch * 4 + 1] = hmul2_f16(hmul2_f16(va.y, vb.y), hmul2_f16(vc.y, vd.y));
+          o[ch * 4 + 2] = hmul2_f16(hmul2_f16(va.z, vb.z), hmul2_f16(vc.z, vd.z));
+          o[ch * 4 + 3] = hmul2_f16(hmul2_f16(va.w, vb.w), hmul2_f16(vc.w, vd.w));
+        }
+        tmem_st32(tm + 256u + (uint32_t)(ft * 64 + bf * 32) + lane_off, o);
+        tc_wait_st();
       }
-      tmem_st32(tm + 64u + (uint32_t)(bf * 32) + lane_off, o);
-      tc_wait_st();
       tc_fence_before();
       __syncwarp();
       if (l == 0) mbar_arrive(&afull[bf]);
     }
-    // epilogue: 33 fp32 columns x w_f x the chunk's scale factors, staged so the
-    // tile's 128 x 33 block goes out as one contiguous, coalesced run
+    // epilogue: 33 fp32 columns x w_f x the chunk's scale factors; each warp's 32
+    // consecutive slots go out as one contiguous, coalesced run
     mbar_wait(fin, 0);
     tc_fence_after();
-    float* stg = (float*)smem;   // [128][33] over the drained stages
-    const float2 sc = scl[s * g.n + kin];
-    const float fw = live ? wt[f] * xs4 / (sc.x * sc.x * sc.x * sc.x * sc.y) : 0.f;
+    if (ft < nft) {
+      float* stg = stg_s + (w - 2) * 32 * (DX + 1);
+      const float2 sc = scl[s * g.n + kin];
+      const float fw = live ? wt[f] * xs4 / (sc.x * sc.x * sc.x * sc.x * sc.y) : 0.f;
 #pragma unroll
-    for (int c0 = 0; c0 < 48; c0 += 16) {
-      uint32_t r[16];
-      tmem_ld16(tm + lane_off + c0, r);
-      tc_wait_ld();
+      for (int c0 = 0; c0 < 48; c0 += 16) {
+        uint32_t r[16];
+        tmem_ld16(tm + (uint32_t)(ft * 64) + lane_off + c0, r);
+        tc_wait_ld();
 #pragma unroll
-      for (int c = 0; c < 16; ++c)
-        if (c0 + c <= DX) stg[row * (DX + 1) + c0 + c] = fw * __uint_as_float(r[c]);
+        for (int c = 0; c < 16; ++c)
+          if (c0 + c <= DX) stg[l * (DX + 1) + c0 + c] = fw * __uint_as_float(r[c]);
+      }
+      __syncwarp();
+      const int f0 = (grp * FT + ft) * 128 + q * 32;
+      const int nf = max(0, min(32, g.D - f0));
+      float* dst = out + (((size_t)s * g.n + kout) * g.D + (size_t)f0) * (DX + 1);
+      for (int i = l; i < nf * (DX + 1); i += 32) dst[i] = stg[i];
     }
-    named_bar(1, 128);
-    const int nf = min(128, g.D - tile * 128);
-    float* dst = out + (((size_t)s * g.n + kout) * g.D + (size_t)tile * 128) * (DX + 1);
-    for (int i = tid - 64; i < nf * (DX + 1); i += 128) dst[i] = stg[i];
   }
   tc_fence_before();
   __syncthreads();
-  if (w == 0) tmem_dealloc<256>(tm);
+  if (w == 0) tmem_dealloc<512>(tm);
 }
 
 // ---------------------------------------------------------------- fp16 states
@@ -893,7 +908,8 @@ int tc4_state(const Geo& g, bool bwd, const void* x, const void* v, const float*
   const float s2 = bwd ? g.scale * g.scale : 1.f;
   auto fn = bwd ? k_tc4_state<true> : k_tc4_state<false>;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-  fn<<<dim3((g.D + 127) / 128, nk, g.ns), THREADS, SMEM, st>>>(m_xt, m_ub, g, idx, wt, scl, s2 * s2, out);
+  fn<<<dim3(((g.D + 127) / 128 + FT - 1) / FT, nk, g.ns), THREADS, SMEM, st>>>(m_xt, m_ub, g, idx, wt, scl, s2 * s2,
+                                                                                out);
   count_launch();
   return cuda_check("tc4 state GEMM");
 }

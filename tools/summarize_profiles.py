@@ -24,9 +24,9 @@ STAGES = {
     "bwd_prep": ["k_tc_bwd_prep", "k_tc_prep_xt#bwd", "k_tc_prep_rows#bwd"],
     "bwd_query_state_dA": ["k_tc_featmajor<1"],
     "bwd_discumsum": ["k_tc_scan_bwd"],
-    "bwd_intra": ["k_tc_ib"],
-    "bwd_query_state_dq": ["k_tc_zvjp<0", "k_tc_dq_chunk0", "k_tc_dphi2<0"],
-    "bwd_update_state": ["k_tc_zvjp<1", "k_tc_dphi2<1"],
+    "bwd_intra": ["k_tc_intra_bwd", "k_tc_ib"],
+    "bwd_query_state_dq": ["k_tc_zvjp<0", "k_tc_dq_chunk0"],
+    "bwd_update_state": ["k_tc_zvjp<1"],
     "bwd_finish": ["k_tc_gate_finish"],
 }
 
