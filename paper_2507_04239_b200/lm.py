@@ -35,6 +35,13 @@ class LMConfig:
     def head_dim(self) -> int:
         return self.width // self.heads
 
+    @property
+    def padded_vocab(self) -> int:
+        """Embedding / LM-head rows: the vocabulary rounded up to a multiple of 64
+        so the head GEMMs run on the aligned cuBLAS kernels (50257 -> 50304; the
+        padded logits are never targets)."""
+        return (self.vocab + 63) // 64 * 64
+
 
 def non_embedding_params(cfg: LMConfig) -> int:
     """(4 + 2 mlp_ratio) width^2 layers (reference flops.py:92-94)."""
@@ -49,7 +56,11 @@ class PowerAttentionBlock(nn.Module):
         super().__init__()
         self.cfg = cfg
         self.norm = nn.LayerNorm(cfg.width)
-        self.qkv = nn.Linear(cfg.width, 3 * cfg.width, bias=False)
+        # separate projections: q, k, v come out contiguous in [b, t, h, d], the
+        # layout power_full reads in place (a fused qkv would need three copies)
+        self.q = nn.Linear(cfg.width, cfg.width, bias=False)
+        self.k = nn.Linear(cfg.width, cfg.width, bias=False)
+        self.v = nn.Linear(cfg.width, cfg.width, bias=False)
         self.gate = nn.Linear(cfg.width, cfg.heads)
         self.proj = nn.Linear(cfg.width, cfg.width, bias=False)
         self.attn_fn = attn_fn
@@ -58,7 +69,7 @@ class PowerAttentionBlock(nn.Module):
         cfg = self.cfg
         b, t, _ = x.shape
         h = self.norm(x)
-        q, k, v = self.qkv(h).view(b, t, 3, cfg.heads, cfg.head_dim).unbind(2)
+        q, k, v = (proj(h).view(b, t, cfg.heads, cfg.head_dim) for proj in (self.q, self.k, self.v))
         log_g = F.logsigmoid(self.gate(h).float())
         if self.attn_fn is None:
             from .power import power_full
@@ -87,7 +98,7 @@ class PowerLM(nn.Module):
     def __init__(self, cfg: LMConfig = LMConfig(), attn_fn=None):
         super().__init__()
         self.cfg = cfg
-        self.embed = nn.Embedding(cfg.vocab, cfg.width)
+        self.embed = nn.Embedding(cfg.padded_vocab, cfg.width)
         self.blocks = nn.ModuleList()
         for _ in range(cfg.layers):
             self.blocks.append(PowerAttentionBlock(cfg, attn_fn))
@@ -116,9 +127,10 @@ class PowerLM(nn.Module):
 
 
 def lm_loss(model, tokens, targets):
-    """Mean next-token cross-entropy (fp32 logits); `model` may be DDP-wrapped."""
+    """Mean next-token cross-entropy; `model` may be DDP-wrapped.  The logits stay
+    in the autocast dtype (the softmax accumulates in fp32 inside the kernel)."""
     logits = model(tokens)
-    return F.cross_entropy(logits.float().view(-1, logits.shape[-1]), targets.reshape(-1))
+    return F.cross_entropy(logits.view(-1, logits.shape[-1]), targets.reshape(-1))
 
 
 def train_step(model, opt, tokens, targets, autocast=True):
@@ -148,4 +160,4 @@ def attention_flops(cfg: LMConfig, t: int, b: int = 1) -> float:
 
 def weight_flops(cfg: LMConfig, tokens: int) -> float:
     """6 N tokens for the dense weights (non-embedding + the tied LM head)."""
-    return 6.0 * (non_embedding_params(cfg) + cfg.vocab * cfg.width) * tokens
+    return 6.0 * (non_embedding_params(cfg) + cfg.padded_vocab * cfg.width) * tokens
