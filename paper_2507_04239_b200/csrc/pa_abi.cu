@@ -150,48 +150,82 @@ static int make_geo(const pa_problem* pr, Geo* g) {
   return PA_OK;
 }
 
-// A tensor-core problem whose last chunk is partial (or whose single chunk is
-// not a multiple of 128 tokens) runs on a zero-padded copy of the sequence
-// (reference ChunkPlan.bounds chunked.py:85-86 ends the last chunk early).
-// Padded keys and values are zero and padded log-gates are 0, so the padding
-// adds nothing to any real token's output, chunk state or gradient; padded
-// rows are dropped.  The returned geometry has t = the padded length and
-// treal = the caller's.
-static bool pad_geo(const pa_problem* pr, const Geo& g, Geo* gp) {
-  if (pr->dtype != PA_BF16) return false;
+// The tensor-core path serves every bf16 / fp16 problem with p = 2, d = e = 64.
+// Its kernels want a chunk that is a multiple of 128 up to 1024 and t a multiple
+// of the chunk; the caller's shape maps onto that as follows.
+//  * Chunk size: the outputs and gradients of chunked power attention do not
+//    depend on the chunk size (the reference's own test, test_chunked.py:278-285,
+//    holds them equal to 2e-8 in f64); a chunk the kernels do not take runs with
+//    an internal chunk of min(1024, t rounded up to 128) -- only rounding differs.
+//  * A partial last chunk (reference ChunkPlan.bounds chunked.py:85-86 ends it
+//    early) runs on a zero-padded copy: padded keys and values are zero and padded
+//    log-gates 0, so the padding adds nothing to any real token's output, state or
+//    gradient; padded rows are dropped (normalized: weight 0, Geo.treal).
+//  * fp16 inputs are staged as bf16 (one rounding, 2^-9) and the outputs and
+//    gradients converted back.
+// Returns false when the tensor-core path does not apply.  `stage` = the call
+// runs on copies in the workspace (padding or fp16).
+static bool tc_geo(const pa_problem* pr, const Geo& g, Geo* gp, bool* stage) {
+  if (pr->dtype != PA_BF16 && pr->dtype != PA_F16) return false;
   Geo p = g;
-  if (g.n == 1) {
-    p.c = (g.t + 127) / 128 * 128;
-    p.t = p.c;
-  } else {
-    p.t = g.n * g.c;
-  }
-  if (p.t == g.t) return false;
+  const bool chunk_ok = g.c % 128 == 0 && g.c <= 1024;
+  if (!chunk_ok) p.c = std::min(1024, (g.t + 127) / 128 * 128);
+  p.t = (g.t + p.c - 1) / p.c * p.c;
   p.n = p.t / p.c;
   p.nsl = p.n + 1;
   p.ng = p.n;
-  if (!tc_supported(p, pr->dtype)) return false;
+  p.treal = g.t;
+  p.dtype = PA_BF16;
+  if (!tc_supported(p, PA_BF16)) return false;
   *gp = p;
+  *stage = p.t != g.t || pr->dtype == PA_F16;
   return true;
 }
 
-// Which kernel family runs the problem (g becomes the padded geometry when
-// padding applies); with PA_FLAG_STRICT_TC a 16-bit problem the tensor-core
+// Which kernel family runs the problem (g becomes the tensor-core geometry when
+// that path applies); with PA_FLAG_STRICT_TC a 16-bit problem the tensor-core
 // kernels do not cover is an error, not a silent switch to the fp32 CUDA-core
 // kernels.
-static int route(const pa_problem* pr, Geo& g, bool* tc) {
-  *tc = tc_supported(g, pr->dtype);
+static int route(const pa_problem* pr, Geo& g, bool* tc, bool* stage = nullptr) {
   Geo gp;
-  if (!*tc && pad_geo(pr, g, &gp)) {
-    g = gp;
-    *tc = true;
-  }
+  bool st = false;
+  *tc = tc_geo(pr, g, &gp, &st);
+  if (*tc) g = gp;
+  if (stage) *stage = st;
   if (!*tc && !tc4_supported(g, pr->dtype) && (pr->flags & PA_FLAG_STRICT_TC) && pr->dtype != PA_F32) {
-    set_error("strict tensor-core mode: the tcgen05 kernels cover bf16, p = 2, d = e = 64 and a chunk that is a "
-              "multiple of 128 up to 1024 (or one chunk of at most 1024 tokens)");
+    set_error("strict tensor-core mode: the tcgen05 kernels cover bf16 / fp16 with p = 2, d = e = 64, and bf16 "
+              "with p = 4, d = e = 32");
     return PA_ERR_UNSUPPORTED;
   }
   return PA_OK;
+}
+
+constexpr int HDIM = 64;
+
+// fp16 <-> bf16 staging with the zero tail: dst rows [b][t_dst][h][64], src rows
+// [b][t_src][h][64]; rows past t_src are zero
+template <typename TD, typename TS>
+__global__ void k_stage_rows(TD* dst, const TS* src, int b, int t_dst, int t_src, int hw) {
+  const size_t per = (size_t)t_dst * hw, tot = (size_t)b * per;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < tot; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t bi = i / per, r = i - bi * per;
+    float v = 0.f;
+    if (r < (size_t)t_src * hw) v = to_f<TS>(src[bi * (size_t)t_src * hw + r]);
+    dst[i] = from_f<TD>(v);
+  }
+}
+static void stage_rows(void* dst, const void* src, const Geo& g, int to_bf16, size_t t_dst, size_t t_src,
+                       cudaStream_t st) {
+  const int hw = g.h * HDIM;
+  const size_t tot = (size_t)g.b * t_dst * hw;
+  const unsigned blocks = (unsigned)std::min<size_t>((tot + 255) / 256, 148 * 16);
+  if (to_bf16)
+    k_stage_rows<__nv_bfloat16, __half><<<blocks, 256, 0, st>>>((__nv_bfloat16*)dst, (const __half*)src, g.b,
+                                                                 (int)t_dst, (int)t_src, hw);
+  else
+    k_stage_rows<__half, __nv_bfloat16><<<blocks, 256, 0, st>>>((__half*)dst, (const __nv_bfloat16*)src, g.b,
+                                                                 (int)t_dst, (int)t_src, hw);
+  count_launch();
 }
 
 // zero-padded copies for the padded tensor-core path: per batch, t real rows of
@@ -237,6 +271,15 @@ static void pad_rows(void* dst, const void* src, const Geo& g, size_t row_bytes,
 static void unpad_rows(void* dst, const void* src, const Geo& g, size_t row_bytes, cudaStream_t st) {
   const size_t rb = (size_t)g.h * row_bytes;
   cudaMemcpy2DAsync(dst, g.treal * rb, src, g.t * rb, g.treal * rb, g.b, cudaMemcpyDeviceToDevice, st);
+}
+// copy rows into / out of the staged (padded, bf16) layout
+static void stage_in(void* dst, const void* src, const Geo& g, int dtype, cudaStream_t st) {
+  if (dtype == PA_F16) stage_rows(dst, src, g, 1, g.t, g.treal, st);
+  else pad_rows(dst, src, g, (size_t)HDIM * 2, st);
+}
+static void stage_out(void* dst, const void* src, const Geo& g, int dtype, cudaStream_t st) {
+  if (dtype == PA_F16) stage_rows(dst, src, g, 0, g.treal, g.t, st);
+  else unpad_rows(dst, src, g, (size_t)HDIM * 2, st);
 }
 static size_t inner_fwd_bytes(const Geo& g) { return align_up(tc_fwd_workspace_bytes(g)); }
 static size_t inner_bwd_bytes(const Geo& g) { return align_up(tc_bwd_workspace_bytes(g)); }
@@ -323,9 +366,9 @@ int pa_uses_tensor_cores(const pa_problem* pr) {
 size_t pa_fwd_workspace_bytes(const pa_problem* pr) {
   Geo g;
   if (make_geo(pr, &g)) return 0;
-  bool tc;
-  if (route(pr, g, &tc)) return 0;
-  if (tc && g.t != g.treal) {
+  bool tc, stage;
+  if (route(pr, g, &tc, &stage)) return 0;
+  if (tc && stage) {
     size_t extra;
     carve_pad_fwd(g, nullptr, &extra);
     return inner_fwd_bytes(g) + extra;
@@ -339,9 +382,9 @@ size_t pa_fwd_workspace_bytes(const pa_problem* pr) {
 size_t pa_bwd_workspace_bytes(const pa_problem* pr) {
   Geo g;
   if (make_geo(pr, &g)) return 0;
-  bool tc;
-  if (route(pr, g, &tc)) return 0;
-  if (tc && g.t != g.treal) {
+  bool tc, stage;
+  if (route(pr, g, &tc, &stage)) return 0;
+  if (tc && stage) {
     size_t extra;
     carve_pad_bwd(g, nullptr, &extra);
     return inner_bwd_bytes(g) + extra;
@@ -362,22 +405,22 @@ int pa_power_full_fwd(const pa_problem* pr, const void* q, const void* k, const 
     return PA_ERR_INVALID_SPEC;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  bool tc;
-  if (int rc = route(pr, g, &tc)) return rc;
-  if (tc && g.t != g.treal) {
+  bool tc, stage;
+  if (int rc = route(pr, g, &tc, &stage)) return rc;
+  if (tc && stage) {
     size_t extra;
     PadFwd p = carve_pad_fwd(g, (char*)ws + inner_fwd_bytes(g), &extra);
     if (ws_bytes < inner_fwd_bytes(g) + extra) {
       set_error("forward workspace too small");
       return PA_ERR_WORKSPACE;
     }
-    pad_rows(p.q, q, g, (size_t)g.d * 2, st);
-    pad_rows(p.k, k, g, (size_t)g.d * 2, st);
-    pad_rows(p.v, v, g, (size_t)g.e * 2, st);
+    stage_in(p.q, q, g, pr->dtype, st);
+    stage_in(p.k, k, g, pr->dtype, st);
+    stage_in(p.v, v, g, pr->dtype, st);
     if (g.gated) pad_rows(p.lg, log_g, g, 4, st);
     const bool rs = rowsum || g.normalize;
     if (int rc = tc_forward(g, p.q, p.k, p.v, g.gated ? p.lg : nullptr, p.y, rs ? p.rs : nullptr, ws, st)) return rc;
-    unpad_rows(y, p.y, g, (size_t)g.e * 2, st);
+    stage_out(y, p.y, g, pr->dtype, st);
     if (rowsum) unpad_rows(rowsum, p.rs, g, 4, st);
     return cuda_check("padded forward");
   }
@@ -416,9 +459,9 @@ int pa_power_full_bwd(const pa_problem* pr, const void* q, const void* k, const 
   }
   if (!g.gated) dlog_g = nullptr;
   cudaStream_t st = (cudaStream_t)stream;
-  bool tc;
-  if (int rc = route(pr, g, &tc)) return rc;
-  if (tc && g.t != g.treal) {
+  bool tc, stage;
+  if (int rc = route(pr, g, &tc, &stage)) return rc;
+  if (tc && stage) {
     size_t extra;
     PadFwd pf = carve_pad_fwd(g, (char*)fwd_ws + inner_fwd_bytes(g), &extra);
     PadBwd pb = carve_pad_bwd(g, (char*)bwd_ws + inner_bwd_bytes(g), &extra);
@@ -426,13 +469,13 @@ int pa_power_full_bwd(const pa_problem* pr, const void* q, const void* k, const 
       set_error("backward workspace too small");
       return PA_ERR_WORKSPACE;
     }
-    pad_rows(pb.dy, dy, g, (size_t)g.e * 2, st);
+    stage_in(pb.dy, dy, g, pr->dtype, st);
     if (int rc = tc_backward(g, pf.q, pf.k, pf.v, g.gated ? pf.lg : nullptr, pf.y, g.normalize ? pf.rs : nullptr,
                              pb.dy, pb.dq, pb.dk, pb.dv, dlog_g ? pb.dlg : nullptr, fwd_ws, bwd_ws, st))
       return rc;
-    unpad_rows(dq, pb.dq, g, (size_t)g.d * 2, st);
-    unpad_rows(dk, pb.dk, g, (size_t)g.d * 2, st);
-    unpad_rows(dv, pb.dv, g, (size_t)g.e * 2, st);
+    stage_out(dq, pb.dq, g, pr->dtype, st);
+    stage_out(dk, pb.dk, g, pr->dtype, st);
+    stage_out(dv, pb.dv, g, pr->dtype, st);
     if (dlog_g) unpad_rows(dlog_g, pb.dlg, g, 4, st);
     return cuda_check("padded backward");
   }

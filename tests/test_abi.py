@@ -121,6 +121,13 @@ def test_route_and_strict_flag():
     # a partial last chunk runs on a zero-padded copy on the tensor cores
     assert lib.pa_uses_tensor_cores(ctypes.byref(_problem(t=1000, d=64, e=64, chunk=256, dtype=1))) == 1
     assert lib.pa_uses_tensor_cores(ctypes.byref(_problem(t=700, d=64, e=64, chunk=4096, dtype=1))) == 1
+    # any chunk size (an internal chunk) and fp16 inputs (staged as bf16)
+    for ch in (2048, 64, 200):
+        assert lib.pa_uses_tensor_cores(ctypes.byref(_problem(t=4096, d=64, e=64, chunk=ch, dtype=1))) == 1
+    assert lib.pa_uses_tensor_cores(ctypes.byref(_problem(t=2048, d=64, e=64, chunk=1024, dtype=2))) == 1
+    # fp16 stages its inputs: the workspace grows by the staged copies
+    f16 = lib.pa_fwd_workspace_bytes(ctypes.byref(_problem(t=2048, d=64, e=64, chunk=1024, dtype=2)))
+    assert f16 > lib.pa_fwd_workspace_bytes(ctypes.byref(tc))
     off = _problem(t=1024, d=32, e=32, chunk=256, dtype=1)
     assert lib.pa_uses_tensor_cores(ctypes.byref(off)) == 0
     off.flags = _lib.PA_FLAG_STRICT_TC
