@@ -600,6 +600,211 @@ __global__ void __launch_bounds__(256) k_tc_scan_fwd(Geo g, int ucols, const flo
   if (end_out) *(float4*)(end_out + cidx) = acc;
 }
 
+// ==========================================================================
+// fused update_state + discumsum (the whole-sequence forward, no carry):
+//   R_{k+1} = lambda_k R_k + S'_k in the fp32 TMEM accumulator, slot_{k+1} =
+//   omega R_{k+1} 2^-nbits(k) stored fp16 straight from the accumulator
+// One CTA = one group of TPC 128-slot tiles x one stream, walking the stream's
+// chunks in order: the feature-major GEMM of k_tc_featmajor<false> (same warp
+// roles, same A generation) with the accumulator kept across chunks.  Between
+// chunks the generation warps read R out of TMEM, store the state slot, scale
+// R by the next chunk's lambda and write it back (the only serial part; the
+// co-resident CTA keeps the tensor pipe busy).  Replaces the S'_k round trip
+// through HBM (k_tc_featmajor -> k_tc_scan_fwd) and accumulates S'_k in fp32
+// instead of fp16.  grid (NTH / TPC, stream)
+// ==========================================================================
+template <int kDen>
+__global__ void __launch_bounds__(fm::THREADS, 2) k_tc_featscan(const __grid_constant__ CUtensorMap tm_xt,
+                                                        const __grid_constant__ CUtensorMap tm_b,
+                                                        const __grid_constant__ CUtensorMap tm_b16, Geo g,
+                                                        const float* __restrict__ lamlog, __half* st_main,
+                                                        __half* st_den) {
+  using namespace fm;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* xt_s = smem;
+  uint8_t* b_s = xt_s + ST * XT_B;
+  uint8_t* b16_s = b_s + ST * B_B;
+  uint8_t* ones = b16_s + ST * B16_B;
+  uint64_t* bars = (uint64_t*)(ones + 2048);
+  uint64_t* full = bars;                 // [ST]
+  uint64_t* empty = bars + ST;           // [ST]
+  uint64_t* afull = bars + 2 * ST;       // [NB]
+  uint64_t* aempty = afull + NB;         // [NB]
+  uint64_t* fin = aempty + NB;           // chunk's MMAs done (2 issuers)
+  uint64_t* rdy = fin + 1;               // accumulator rescaled for the next chunk (8 warps)
+  __shared__ uint32_t tmem_base;
+
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  const int grp = blockIdx.x, s = blockIdx.y;
+  const int t0 = grp * TPC, nt = min(TPC, NTH - t0);
+  constexpr bool den = kDen != 0;
+  constexpr int SUB = den ? 32 : 64, SPS = TOK / SUB, NBk = den ? 3 : 2;
+  constexpr int ACC_W = den ? UW : 64;
+  constexpr uint32_t ABASE = TPC * ACC_W;
+  const int nsub = g.c / SUB, nstage = g.c / TOK, total = g.n * nsub;
+
+  if (w == 2) tmem_alloc<256>(&tmem_base);
+  if (tid == 0) {
+    for (int i = 0; i < ST; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], SPS);
+    }
+    for (int i = 0; i < NBk; ++i) {
+      mbar_init(&afull[i], GEN_WARPS);
+      mbar_init(&aempty[i], 1);
+    }
+    mbar_init(fin, 2);
+    mbar_init(rdy, GEN_WARPS);
+    fence_barrier_init();
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tmem_base;
+
+  if (w == 0) {
+    constexpr int NL = den ? 3 : 2;
+    constexpr unsigned LM = (1u << NL) - 1u;
+    if (l < NL) {
+      if (l == 0) {
+        tma_prefetch(&tm_xt);
+        tma_prefetch(&tm_b);
+      }
+      for (int jj = 0; jj < g.n * nstage; ++jj) {
+        const int kin = jj / nstage, j = jj - kin * nstage, st = jj % ST;
+        if (jj >= ST) mbar_wait(&empty[st], ((jj / ST) + 1) & 1);
+        const uint32_t bytes = XT_B + B_B + (den ? B16_B : 0);
+        if (l == 0) mbar_expect_tx(&full[st], bytes);
+        __syncwarp(LM);
+        const int row0 = (s * g.n + kin) * HD;
+        if (l == 0) tma_load_2d(xt_s + st * XT_B, &tm_xt, &full[st], j * TOK, row0);
+        if (l == 1) tma_load_2d(b_s + st * B_B, &tm_b, &full[st], 0, s * g.t + kin * g.c + j * TOK);
+        if (den && l == 2) tma_load_2d(b16_s + st * B16_B, &tm_b16, &full[st], 0, s * g.t + kin * g.c + j * TOK);
+      }
+    }
+  } else if (w == 1 || w == 3) {
+    const int mw = w >> 1;
+    const uint32_t id64 = idesc_f16(128, 64, false, true);
+    const uint32_t id16 = idesc_f16(128, 16, false, true);
+    const uint64_t bn0 = smem_desc(smem_u32(b_s), 8192, 1024, 2);
+    const uint64_t b160 = smem_desc(smem_u32(b16_s), 512, 256, 6);
+    // deterministic mode: w1 issues every step in order and commits fin twice
+    const int istep = g.det ? 1 : 2;
+    const int first = g.det ? 0 : mw, last = g.det ? nsub - 1 : nsub - 2 + mw;
+    for (int i = g.det ? (mw ? total : 0) : mw; i < total; i += istep) {
+      const int kin = i / nsub, li = i - kin * nsub;
+      const int j = li / SPS, h = li % SPS, jj = kin * nstage + j, st = jj % ST, buf = i % NBk;
+      if (li == first && kin > 0) mbar_wait_w(rdy, (kin - 1) & 1);
+      mbar_wait_w(&full[st], (jj / ST) & 1);
+      mbar_wait_w(&afull[buf], (i / NBk) & 1);
+      tc_fence_after();
+      for (int t = 0; t < nt; ++t) {
+        const uint32_t acc = tm + (uint32_t)(t * ACC_W);
+        const uint32_t ab = tm + ABASE + (uint32_t)((buf * TPC + t) * (SUB / 2));
+#pragma unroll
+        for (int kk = 0; kk < SUB / 16; ++kk) {
+          const int trow = h * SUB + kk * 16;
+          mma_ts_w(acc, ab + kk * 8, bn0 + (uint64_t)((st * B_B + trow * 128) >> 4), id64, 1u);
+          if (den) mma_ts_w(acc + 64, ab + kk * 8, b160 + (uint64_t)((st * B16_B + trow * 32) >> 4), id16, 1u);
+        }
+      }
+      tc_commit_w(&aempty[buf]);
+      tc_commit_w(&empty[st]);
+      if (li == last) {
+        tc_commit_w(fin);
+        if (g.det) tc_commit_w(fin);
+      }
+    }
+  } else if (w >= 4) {
+    const int q = w & 3, t = (w - 4) >> 2;   // lane quadrant, tile (one per warp: TPC = 2)
+    const bool act = t < nt;
+    const int blk = act ? (t0 + t) * 4 + q : 0;
+    const int ra = 4 * c_blk.al[blk] + (l >> 3), rb = 8 * c_blk.be[blk] + (l & 7);
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const int f = (t0 + t) * 128 + q * 32 + l;   // this thread's slot (accumulator row)
+    const float om = act ? slot_omega(f) : 0.f;
+    if (act) {
+      uint32_t z[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) z[c] = 0u;
+      for (int c = 0; c < ACC_W; c += 16) tmem_st16(tm + (uint32_t)(t * ACC_W + c) + lane_off, z);
+    }
+    // slot kin + 1 = omega R 2^-nbits(kin) (fp16, the scan's layout); then R *= lambda_{kin+1}
+    auto finish_chunk = [&](int kin) {
+      mbar_wait(fin, kin & 1);
+      tc_fence_after();
+      if (act) {
+        const float sc = om * pow2_neg_bits(g.k0 + kin);
+        const bool more = kin + 1 < g.n;
+        const bool rescale = more && g.gated;
+        const float lam = rescale ? __expf(lamlog[s * g.n + kin + 1]) : 1.f;
+        const size_t sk = (size_t)s * g.nsl + kin + 1;
+        uint8_t* rowm = (uint8_t*)(st_main + sk * ST_MAIN) + (size_t)f * 128;
+#pragma unroll
+        for (int c0 = 0; c0 < ACC_W; c0 += 16) {
+          uint32_t r[16];
+          tmem_ld16(tm + (uint32_t)(t * ACC_W + c0) + lane_off, r);
+          tc_wait_ld();
+          uint32_t hv[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) hv[c] = pack_f16(__uint_as_float(r[2 * c]) * sc, __uint_as_float(r[2 * c + 1]) * sc);
+          if (c0 < 64) {
+            const int ch = c0 >> 3;
+            *(uint4*)(rowm + (((ch) ^ (f & 7)) << 4)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+            *(uint4*)(rowm + (((ch + 1) ^ (f & 7)) << 4)) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
+          } else {
+            uint8_t* rowd = (uint8_t*)(st_den + sk * ST_DEN) + (size_t)f * 32;
+            const uint32_t x = (f >> 2) & 1;
+            *(uint4*)(rowd + ((0u ^ x) << 4)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+            *(uint4*)(rowd + ((1u ^ x) << 4)) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
+          }
+          if (rescale) {
+#pragma unroll
+            for (int c = 0; c < 16; ++c) r[c] = __float_as_uint(__uint_as_float(r[c]) * lam);
+            tmem_st16(tm + (uint32_t)(t * ACC_W + c0) + lane_off, r);
+          }
+        }
+        if (rescale) tc_wait_st();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (l == 0) mbar_arrive(rdy);
+    };
+    for (int i = 0; i < total; ++i) {
+      const int kin = i / nsub, li = i - kin * nsub;
+      if (li == 0 && kin > 0) finish_chunk(kin - 1);
+      const int j = li / SPS, h = li % SPS, jj = kin * nstage + j, st = jj % ST, buf = i % NBk;
+      mbar_wait(&full[st], (jj / ST) & 1);
+      if (i >= NBk) mbar_wait(&aempty[buf], ((i / NBk) + 1) & 1);
+      const uint8_t* xs = xt_s + st * XT_B;
+      if (act) {
+        uint32_t va[SUB / 2], vb[SUB / 2], o[SUB / 2];
+#pragma unroll
+        for (int c4 = 0; c4 < SUB / 8; ++c4) {
+          const int ch = h * (SUB / 8) + c4;
+          *(uint4*)&va[c4 * 4] = *(const uint4*)(xs + sw128_off(ra, ch));
+          *(uint4*)&vb[c4 * 4] = *(const uint4*)(xs + sw128_off(rb, ch));
+        }
+#pragma unroll
+        for (int c = 0; c < SUB / 2; ++c) o[c] = hmul2_f16(va[c], vb[c]);
+        const uint32_t ad = tm + ABASE + (uint32_t)((buf * TPC + t) * (SUB / 2)) + lane_off;
+#pragma unroll
+        for (int c16 = 0; c16 < SUB / 2; c16 += 16) tmem_st16(ad + c16, o + c16);
+      }
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (l == 0) mbar_arrive(&afull[buf]);
+    }
+    finish_chunk(g.n - 1);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (w == 2) tmem_dealloc<256>(tm);
+}
+
 // Sequence-parallel carry combine (the associative discumsum step across
 // partitions): out = exp(sum of this partition's log lambda) * carry + local,
 // per stream.  Used for both the forward state and the backward cotangent.
@@ -994,6 +1199,15 @@ struct DeviceGuard {
   }
 };
 
+// PA_FUSED_SCAN=0: the separate update GEMM + scan (the sequence-parallel path's kernels)
+static bool fused_scan_off() {
+  static const bool off = [] {
+    const char* e = getenv("PA_FUSED_SCAN");
+    return e && e[0] == '0';
+  }();
+  return off;
+}
+
 int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const float* log_g, void* y, float* rowsum,
                void* ws, cudaStream_t st, int mode, const float* carry, float* end_out) {
   size_t need;
@@ -1033,6 +1247,14 @@ int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const 
     k_tc_prep_rows<<<(unsigned)(((size_t)g.ns * g.t * 4 + 255) / 256), 256, 0, st>>>(
         g, 0, (const __nv_bfloat16*)v, w.ell, w.lamlog, nullptr, w.vr, with_den ? w.wa : nullptr);
   }
+  if (mode == 0 && !g.prefix && !fused_scan_off()) {
+    // update_state and the discumsum in one kernel (the stage keeps the update name)
+    StageTimer tmr("fwd_update_state", st);
+    auto fn = with_den ? k_tc_featscan<1> : k_tc_featscan<0>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, fm::SMEM);
+    fn<<<dim3((NTH + fm::TPC - 1) / fm::TPC, g.ns), fm::THREADS, fm::SMEM, st>>>(m_kt, m_vr, m_wa, g, w.lamlog,
+                                                                              w.stm, w.std_);
+  } else {
   {
     StageTimer tmr("fwd_update_state", st);
     auto fn = with_den ? k_tc_featmajor<false, 1> : k_tc_featmajor<false, 0>;
@@ -1044,6 +1266,7 @@ int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const 
     k_tc_scan_fwd<<<dim3((FH * uc / 4 + 255) / 256, g.ns), 256, 0, st>>>(g, uc, w.lamlog, (const __half*)w.sp, w.stm, w.std_,
                                                                          carry, end_out, mode == 1 ? 0 : 1);
   }
+  }
   if (mode == 1) {
     count_launch(4);
     return cuda_check("tc forward (sp local)");
@@ -1052,7 +1275,7 @@ int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const 
     StageTimer tmr("fwd_attn_query", st);
     tc_out(g, m_q, m_k, m_v, q, w.ell, w.stm, w.std_, with_den, y, rowsum, w.y32, w.zflag, st);
   }
-  count_launch(5);
+  count_launch(mode == 0 && !g.prefix && !fused_scan_off() ? 4 : 5);
   return cuda_check("tc forward");
 }
 
