@@ -180,6 +180,10 @@ constexpr int B16_B = 64 * 32;        // 64 tokens x 16 bf16 (SW32)
 constexpr int SMEM_USED = 1024 + ST * (XT_B + B_B + B16_B) + 2048 + 512;
 constexpr int SMEM = SMEM_USED;   // two CTAs per SM (256 TMEM columns each)
 constexpr int TPC = 2;            // 128-slot tiles per CTA
+// fused-scan kernels: a warp-private staging area (32 rows x 144 bytes) per
+// generation warp, so the per-chunk state stores leave as whole 128-byte lines
+constexpr int STG_ROW = 144;
+constexpr int SMEM_FS = SMEM_USED + 8 * 32 * STG_ROW;
 constexpr int THREADS = 384;
 constexpr int GEN_WARPS = 8;
 }  // namespace fm
@@ -731,17 +735,18 @@ __global__ void __launch_bounds__(fm::THREADS, 2) k_tc_featscan(const __grid_con
       for (int c = 0; c < 16; ++c) z[c] = 0u;
       for (int c = 0; c < ACC_W; c += 16) tmem_st16(tm + (uint32_t)(t * ACC_W + c) + lane_off, z);
     }
-    // slot kin + 1 = omega R 2^-nbits(kin) (fp16, the scan's layout); then R *= lambda_{kin+1}
+    // slot kin + 1 = omega R 2^-nbits(kin) (fp16, the scan's layout); then R *= lambda_{kin+1}.
+    // Rows are staged in this warp's shared-memory area and stored four 128-byte
+    // rows per instruction.
+    uint8_t* stg = ones + 2048 + 512 + (w - 4) * 32 * STG_ROW;
     auto finish_chunk = [&](int kin) {
       mbar_wait(fin, kin & 1);
       tc_fence_after();
+      const size_t sk = (size_t)s * g.nsl + kin + 1;
       if (act) {
         const float sc = om * pow2_neg_bits(g.k0 + kin);
-        const bool more = kin + 1 < g.n;
-        const bool rescale = more && g.gated;
+        const bool rescale = kin + 1 < g.n && g.gated;
         const float lam = rescale ? __expf(lamlog[s * g.n + kin + 1]) : 1.f;
-        const size_t sk = (size_t)s * g.nsl + kin + 1;
-        uint8_t* rowm = (uint8_t*)(st_main + sk * ST_MAIN) + (size_t)f * 128;
 #pragma unroll
         for (int c0 = 0; c0 < ACC_W; c0 += 16) {
           uint32_t r[16];
@@ -751,9 +756,8 @@ __global__ void __launch_bounds__(fm::THREADS, 2) k_tc_featscan(const __grid_con
 #pragma unroll
           for (int c = 0; c < 8; ++c) hv[c] = pack_f16(__uint_as_float(r[2 * c]) * sc, __uint_as_float(r[2 * c + 1]) * sc);
           if (c0 < 64) {
-            const int ch = c0 >> 3;
-            *(uint4*)(rowm + (((ch) ^ (f & 7)) << 4)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
-            *(uint4*)(rowm + (((ch + 1) ^ (f & 7)) << 4)) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
+            *(uint4*)(stg + l * STG_ROW + c0 * 2) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+            *(uint4*)(stg + l * STG_ROW + c0 * 2 + 16) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
           } else {
             uint8_t* rowd = (uint8_t*)(st_den + sk * ST_DEN) + (size_t)f * 32;
             const uint32_t x = (f >> 2) & 1;
@@ -770,7 +774,18 @@ __global__ void __launch_bounds__(fm::THREADS, 2) k_tc_featscan(const __grid_con
       }
       tc_fence_before();
       __syncwarp();
-      if (l == 0) mbar_arrive(rdy);
+      if (l == 0) mbar_arrive(rdy);   // the accumulator is free: the stores below overlap the next chunk
+      if (act) {
+        // the warp's 32 slots are consecutive rows: 4 rows (512 bytes) per store
+        const int fw = (t0 + t) * 128 + q * 32;
+        uint8_t* dst = (uint8_t*)(st_main + sk * ST_MAIN) + (size_t)fw * 128;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int pr = 4 * i + (l >> 3), ch = l & 7;
+          *(uint4*)(dst + pr * 128 + ((ch ^ ((fw + pr) & 7)) << 4)) = *(const uint4*)(stg + pr * STG_ROW + ch * 16);
+        }
+      }
+      __syncwarp();
     };
     for (int i = 0; i < total; ++i) {
       const int kin = i / nsub, li = i - kin * nsub;
@@ -976,6 +991,304 @@ __global__ void __launch_bounds__(256) k_tc_scan_bwd(Geo g, int ucols, const flo
   }
 }
 
+// ==========================================================================
+// fused query-state VJP (dA') + reverse discumsum (the whole-sequence backward,
+// no carry): the running cotangent Gs lives in the fp32 TMEM accumulator.
+// For j = n-1 .. 0 (epilogue of slot j, then the GEMM of chunk j's queries):
+//   dS~_j = omega Gs_{j+1} -> expanded E(dS~_j) (2 x 2^-nbits(n-1-j), fp16)
+//   E(A_j) from the stored forward slot j (doubled on the diagonal)
+//   dlambda_j = <slot_j, Gs_{j+1}>  (one partial per generation warp)
+//   Gs_j = dA'_j + lambda_j Gs_{j+1}: R *= lambda_j, then the feature-major GEMM
+//          phi'(Q~_j)^T [dnum | dden] accumulates onto R (chunk j >= 1)
+// Same warp roles and A generation as k_tc_featmajor<true>; replaces the fp32
+// dA' round trip through HBM (k_tc_featmajor<true> -> k_tc_scan_bwd).
+// dlam_part[(s n + j) * NTH * 4 + tile * 4 + quadrant].  grid (NTH / TPC, stream)
+// ==========================================================================
+constexpr int kFsBwdParts = NTH * 4;
+
+template <int kDen>
+__global__ void __launch_bounds__(fm::THREADS, 2) k_tc_featscan_bwd(const __grid_constant__ CUtensorMap tm_xt,
+                                                            const __grid_constant__ CUtensorMap tm_b,
+                                                            const __grid_constant__ CUtensorMap tm_b16, Geo g,
+                                                            const float* __restrict__ lamlog,
+                                                            const __half* __restrict__ st_main,
+                                                            const __half* __restrict__ st_den, float* dlam_part,
+                                                            __half* ea, __half* eg) {
+  using namespace fm;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* xt_s = smem;
+  uint8_t* b_s = xt_s + ST * XT_B;
+  uint8_t* b16_s = b_s + ST * B_B;
+  uint8_t* ones = b16_s + ST * B16_B;
+  uint64_t* bars = (uint64_t*)(ones + 2048);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + ST;
+  uint64_t* afull = bars + 2 * ST;
+  uint64_t* aempty = afull + NB;
+  uint64_t* fin = aempty + NB;
+  uint64_t* rdy = fin + 1;
+  __shared__ uint32_t tmem_base;
+
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  const int grp = blockIdx.x, s = blockIdx.y;
+  const int t0 = grp * TPC, nt = min(TPC, NTH - t0);
+  constexpr bool den = kDen != 0;
+  constexpr int SUB = den ? 32 : 64, SPS = TOK / SUB, NBk = den ? 3 : 2;
+  constexpr int ACC_W = den ? UW : 64;
+  constexpr uint32_t ABASE = TPC * ACC_W;
+  constexpr int nbt = 64 + (den ? 1 : 0);
+  const int nsub = g.c / SUB, nstage = g.c / TOK, total = (g.n - 1) * nsub;   // chunks n-1 .. 1
+
+  if (w == 2) tmem_alloc<256>(&tmem_base);
+  if (tid == 0) {
+    for (int i = 0; i < ST; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], SPS);
+    }
+    for (int i = 0; i < NBk; ++i) {
+      mbar_init(&afull[i], GEN_WARPS);
+      mbar_init(&aempty[i], 1);
+    }
+    mbar_init(fin, 2);
+    mbar_init(rdy, GEN_WARPS);
+    fence_barrier_init();
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tmem_base;
+
+  if (w == 0) {
+    constexpr int NL = den ? 3 : 2;
+    constexpr unsigned LM = (1u << NL) - 1u;
+    if (l < NL) {
+      if (l == 0) {
+        tma_prefetch(&tm_xt);
+        tma_prefetch(&tm_b);
+      }
+      for (int jj = 0; jj < (g.n - 1) * nstage; ++jj) {
+        const int ci = jj / nstage, j = jj - ci * nstage, st = jj % ST, kin = g.n - 1 - ci;
+        if (jj >= ST) mbar_wait(&empty[st], ((jj / ST) + 1) & 1);
+        const uint32_t bytes = XT_B + B_B + (den ? B16_B : 0);
+        if (l == 0) mbar_expect_tx(&full[st], bytes);
+        __syncwarp(LM);
+        const int row0 = (s * g.n + kin) * HD;
+        if (l == 0) tma_load_2d(xt_s + st * XT_B, &tm_xt, &full[st], j * TOK, row0);
+        if (l == 1) tma_load_2d(b_s + st * B_B, &tm_b, &full[st], 0, s * g.t + kin * g.c + j * TOK);
+        if (den && l == 2) tma_load_2d(b16_s + st * B16_B, &tm_b16, &full[st], 0, s * g.t + kin * g.c + j * TOK);
+      }
+    }
+  } else if (w == 1 || w == 3) {
+    const int mw = w >> 1;
+    const uint32_t id64 = idesc_f16(128, 64, false, true);
+    const uint32_t id16 = idesc_f16(128, 16, false, true);
+    const uint64_t bn0 = smem_desc(smem_u32(b_s), 8192, 1024, 2);
+    const uint64_t b160 = smem_desc(smem_u32(b16_s), 512, 256, 6);
+    const int istep = g.det ? 1 : 2;
+    const int first = g.det ? 0 : mw, last = g.det ? nsub - 1 : nsub - 2 + mw;
+    for (int i = g.det ? (mw ? total : 0) : mw; i < total; i += istep) {
+      const int ci = i / nsub, li = i - ci * nsub;
+      const int j = li / SPS, h = li % SPS, jj = ci * nstage + j, st = jj % ST, buf = i % NBk;
+      if (li == first) mbar_wait_w(rdy, ci & 1);
+      mbar_wait_w(&full[st], (jj / ST) & 1);
+      mbar_wait_w(&afull[buf], (i / NBk) & 1);
+      tc_fence_after();
+      for (int t = 0; t < nt; ++t) {
+        const uint32_t acc = tm + (uint32_t)(t * ACC_W);
+        const uint32_t ab = tm + ABASE + (uint32_t)((buf * TPC + t) * (SUB / 2));
+#pragma unroll
+        for (int kk = 0; kk < SUB / 16; ++kk) {
+          const int trow = h * SUB + kk * 16;
+          mma_ts_w(acc, ab + kk * 8, bn0 + (uint64_t)((st * B_B + trow * 128) >> 4), id64, 1u);
+          if (den) mma_ts_w(acc + 64, ab + kk * 8, b160 + (uint64_t)((st * B16_B + trow * 32) >> 4), id16, 1u);
+        }
+      }
+      tc_commit_w(&aempty[buf]);
+      tc_commit_w(&empty[st]);
+      if (li == last) {
+        tc_commit_w(fin);
+        if (g.det) tc_commit_w(fin);
+      }
+    }
+  } else if (w >= 4) {
+    const int q = w & 3, t = (w - 4) >> 2;
+    const bool act = t < nt;
+    const int blk = act ? (t0 + t) * 4 + q : 0;
+    const int ra = 4 * c_blk.al[blk] + (l >> 3), rb = 8 * c_blk.be[blk] + (l & 7);
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const int f = (t0 + t) * 128 + q * 32 + l;
+    const int fa = ra, fb = rb;   // the slot's feature pair (a, b); a > b: a zero duplicate
+    const bool up = fa <= fb;
+    if (act) {
+      uint32_t z[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) z[c] = 0u;
+      for (int c = 0; c < ACC_W; c += 16) tmem_st16(tm + (uint32_t)(t * ACC_W + c) + lane_off, z);
+      tc_wait_st();
+    }
+    // epilogue of slot j: R = Gs_{j+1} on entry, lambda_j Gs_{j+1} on exit.
+    // Two passes of 32 value columns: the owner thread stages its fp32 row in the
+    // warp's shared-memory area and rescales R; then the warp walks (slot pair,
+    // 16-byte chunk) cells -- lane = (a, b, chunk) of its 4 x 8 block -- so every
+    // load of the stored forward state and every store of the expanded tiles
+    // covers whole row segments.  The score-sum column (u = 64) stays per thread.
+    float* stg = (float*)(ones + 2048 + 512) + (w - 4) * 32 * (STG_ROW / 4);
+    const int bal = act ? c_blk.al[blk] : 0, bbe = act ? c_blk.be[blk] : 0;
+    auto slot_epi = [&](int j, int ci) {
+      if (ci > 0) {
+        mbar_wait(fin, (ci - 1) & 1);
+        tc_fence_after();
+      }
+      const bool hasA = j >= 1;
+      const bool rescale = j >= 1 && g.gated;
+      const float lam = rescale ? __expf(lamlog[s * g.n + j]) : 1.f;
+      const float sg = 2.f * pow2_neg_bits(g.ng - 1 - (g.k0 + j));
+      const size_t sk = (size_t)s * g.nsl + j;
+      uint8_t* egb = (uint8_t*)(eg + sk * nbt * 4096);
+      uint8_t* eab = (uint8_t*)(ea + sk * nbt * 4096);
+      const uint8_t* sta = (const uint8_t*)(st_main + sk * ST_MAIN);
+      const int fw = (t0 + t) * 128 + q * 32;   // the warp's first slot
+      float dot = 0.f;
+      if (act && den) {
+        // u = 64..79 (the owner thread): the score-sum column of E and dlambda
+        uint32_t r[16];
+        tmem_ld16(tm + (uint32_t)(t * ACC_W + 64) + lane_off, r);
+        uint4 a0 = make_uint4(0u, 0u, 0u, 0u), a1 = a0;
+        if (hasA) {
+          const uint8_t* rowd = (const uint8_t*)(st_den + sk * ST_DEN) + (size_t)f * 32;
+          const uint32_t x = (f >> 2) & 1;
+          a0 = *(const uint4*)(rowd + ((0u ^ x) << 4));
+          a1 = *(const uint4*)(rowd + ((1u ^ x) << 4));
+        }
+        tc_wait_ld();
+        const uint32_t av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float2 af = __half22float2(*(const __half2*)&av[c]);
+          dot = fmaf(af.x, __uint_as_float(r[2 * c]), fmaf(af.y, __uint_as_float(r[2 * c + 1]), dot));
+        }
+        if (up) {
+          const unsigned short hg = (unsigned short)(pack_f16(__uint_as_float(r[0]) * sg, 0.f) & 0xffffu);
+          unsigned short ha = (unsigned short)(a0.x & 0xffffu);
+          if (fa == fb) ha = (unsigned short)(hmul2_f16(a0.x, 0x40004000u) & 0xffffu);
+          uint8_t* tg = egb + (size_t)64 * 8192;
+          uint8_t* ta = eab + (size_t)64 * 8192;
+          *(unsigned short*)(tg + sw128_elem(fa, fb)) = hg;
+          if (hasA) *(unsigned short*)(ta + sw128_elem(fa, fb)) = ha;
+          if (fa != fb) {
+            *(unsigned short*)(tg + sw128_elem(fb, fa)) = hg;
+            if (hasA) *(unsigned short*)(ta + sw128_elem(fb, fa)) = ha;
+          }
+        }
+        if (rescale) {
+#pragma unroll
+          for (int c = 0; c < 16; ++c) r[c] = __float_as_uint(__uint_as_float(r[c]) * lam);
+          tmem_st16(tm + (uint32_t)(t * ACC_W + 64) + lane_off, r);
+        }
+      }
+#pragma unroll 1
+      for (int pass = 0; pass < 2; ++pass) {
+        if (act) {
+#pragma unroll
+          for (int c0 = 0; c0 < 32; c0 += 16) {
+            uint32_t r[16];
+            tmem_ld16(tm + (uint32_t)(t * ACC_W + pass * 32 + c0) + lane_off, r);
+            tc_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 16; c += 4)
+              *(uint4*)(stg + l * (STG_ROW / 4) + c0 + c) = make_uint4(r[c], r[c + 1], r[c + 2], r[c + 3]);
+            if (rescale) {
+#pragma unroll
+              for (int c = 0; c < 16; ++c) r[c] = __float_as_uint(__uint_as_float(r[c]) * lam);
+              tmem_st16(tm + (uint32_t)(t * ACC_W + pass * 32 + c0) + lane_off, r);
+            }
+          }
+        }
+        if (pass == 1) {
+          // the accumulator is read and rescaled: release it before the last stores
+          if (act && rescale) tc_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (l == 0) mbar_arrive(rdy);
+        }
+        __syncwarp();
+        if (act) {
+#pragma unroll 2
+          for (int i = 0; i < 4; ++i) {
+            const int pa_ = (l >> 2) & 3, pb = 2 * i + (l >> 4), cc = l & 3;   // cell: slot (pa_, pb), chunk cc
+            const int pp = pa_ * 8 + pb;
+            const int ga = 4 * bal + pa_, gb = 8 * bbe + pb;
+            const int fp = fw + pp;
+            const int chg = pass * 4 + cc;   // 16-byte chunk of the 128-byte row
+            const float4 g0 = *(const float4*)(stg + pp * (STG_ROW / 4) + cc * 8);
+            const float4 g1 = *(const float4*)(stg + pp * (STG_ROW / 4) + cc * 8 + 4);
+            uint4 av = make_uint4(0u, 0u, 0u, 0u);
+            if (hasA) av = *(const uint4*)(sta + (size_t)fp * 128 + ((chg ^ (fp & 7)) << 4));
+            const float2 a01 = __half22float2(*(const __half2*)&av.x), a23 = __half22float2(*(const __half2*)&av.y);
+            const float2 a45 = __half22float2(*(const __half2*)&av.z), a67 = __half22float2(*(const __half2*)&av.w);
+            dot = fmaf(a01.x, g0.x, fmaf(a01.y, g0.y, fmaf(a23.x, g0.z, fmaf(a23.y, g0.w, dot))));
+            dot = fmaf(a45.x, g1.x, fmaf(a45.y, g1.y, fmaf(a67.x, g1.z, fmaf(a67.y, g1.w, dot))));
+            if (ga <= gb) {
+              const uint4 hg = make_uint4(pack_f16(g0.x * sg, g0.y * sg), pack_f16(g0.z * sg, g0.w * sg),
+                                          pack_f16(g1.x * sg, g1.y * sg), pack_f16(g1.z * sg, g1.w * sg));
+              uint4 ha = av;
+              if (ga == gb)
+                ha = make_uint4(hmul2_f16(av.x, 0x40004000u), hmul2_f16(av.y, 0x40004000u),
+                                hmul2_f16(av.z, 0x40004000u), hmul2_f16(av.w, 0x40004000u));
+              const size_t o1 = (size_t)gb * 8192 + (size_t)ga * 128 + ((chg ^ (ga & 7)) << 4);   // tile b row a
+              *(uint4*)(egb + o1) = hg;
+              if (hasA) *(uint4*)(eab + o1) = ha;
+              if (ga != gb) {
+                const size_t o2 = (size_t)ga * 8192 + (size_t)gb * 128 + ((chg ^ (gb & 7)) << 4);   // tile a row b
+                *(uint4*)(egb + o2) = hg;
+                if (hasA) *(uint4*)(eab + o2) = ha;
+              }
+            }
+          }
+        }
+        __syncwarp();
+      }
+      if (act && hasA) {
+        dot = warp_sum(dot);
+        if (l == 0)
+          dlam_part[((size_t)s * g.n + j) * kFsBwdParts + (t0 + t) * 4 + q] = dot / pow2_neg_bits(g.k0 + j - 1);
+      }
+    };
+    for (int i = 0; i < total; ++i) {
+      const int ci = i / nsub, li = i - ci * nsub;
+      if (li == 0) slot_epi(g.n - 1 - ci, ci);
+      const int j = li / SPS, h = li % SPS, jj = ci * nstage + j, st = jj % ST, buf = i % NBk;
+      mbar_wait(&full[st], (jj / ST) & 1);
+      if (i >= NBk) mbar_wait(&aempty[buf], ((i / NBk) + 1) & 1);
+      const uint8_t* xs = xt_s + st * XT_B;
+      if (act) {
+        uint32_t va[SUB / 2], vb[SUB / 2], o[SUB / 2];
+#pragma unroll
+        for (int c4 = 0; c4 < SUB / 8; ++c4) {
+          const int ch = h * (SUB / 8) + c4;
+          *(uint4*)&va[c4 * 4] = *(const uint4*)(xs + sw128_off(ra, ch));
+          *(uint4*)&vb[c4 * 4] = *(const uint4*)(xs + sw128_off(rb, ch));
+        }
+#pragma unroll
+        for (int c = 0; c < SUB / 2; ++c) o[c] = hmul2_f16(va[c], vb[c]);
+        const uint32_t ad = tm + ABASE + (uint32_t)((buf * TPC + t) * (SUB / 2)) + lane_off;
+#pragma unroll
+        for (int c16 = 0; c16 < SUB / 2; c16 += 16) tmem_st16(ad + c16, o + c16);
+      }
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (l == 0) mbar_arrive(&afull[buf]);
+    }
+    slot_epi(0, g.n - 1);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (w == 2) tmem_dealloc<256>(tm);
+}
+
 // gate finish (gradients.py:79-95, 245-264 in log space), one warp per chunk:
 //   dlog g_u = sum_{m >= u} dell_m + dlam_k lam_k + sum_{m < u} cu_m
 __global__ void __launch_bounds__(128) k_tc_gate_finish(Geo g, const float* __restrict__ lamlog,
@@ -1085,7 +1398,7 @@ static TcBwdWs carve_bwd(const Geo& g, void* base, size_t* bytes) {
   b.dv16 = (__nv_bfloat16*)take(2ull * g.ns * g.t * HD);
   b.dell = (float*)take(4ull * g.ns * g.t);
   b.cu = (float*)take(4ull * g.ns * g.t);
-  b.dlam = (float*)take(4ull * g.ns * g.n * scan_blocks(UW));   // per-block dlambda partials
+  b.dlam = (float*)take(4ull * g.ns * g.n * std::max(scan_blocks(UW), kFsBwdParts));   // dlambda partials
   const size_t etiles = (size_t)g.ns * g.nsl * (64 + (g.normalize ? 1 : 0));
   b.ea = (__half*)take(8192ull * etiles);
   b.eg = (__half*)take(8192ull * etiles);
@@ -1251,8 +1564,8 @@ int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const 
     // update_state and the discumsum in one kernel (the stage keeps the update name)
     StageTimer tmr("fwd_update_state", st);
     auto fn = with_den ? k_tc_featscan<1> : k_tc_featscan<0>;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, fm::SMEM);
-    fn<<<dim3((NTH + fm::TPC - 1) / fm::TPC, g.ns), fm::THREADS, fm::SMEM, st>>>(m_kt, m_vr, m_wa, g, w.lamlog,
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, fm::SMEM_FS);
+    fn<<<dim3((NTH + fm::TPC - 1) / fm::TPC, g.ns), fm::THREADS, fm::SMEM_FS, st>>>(m_kt, m_vr, m_wa, g, w.lamlog,
                                                                               w.stm, w.std_);
   } else {
   {
@@ -1310,6 +1623,8 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
     return 3;
   }
   const int red_bytes = 8 * 4 * g.n;
+  // whole-sequence backward: dA' GEMM + reverse scan fused (k_tc_featscan_bwd)
+  const bool fused = mode == 0 && !g.prefix && !carry && !pre_out && !fused_scan_off();
   const int nbt = 64 + den;
   if (red_bytes > 48 * 1024)
     cudaFuncSetAttribute(k_tc_scan_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, red_bytes);
@@ -1329,7 +1644,7 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
       StageTimer tmr("bwd_prep", st);
       cudaMemsetAsync(b.dell, 0, 4ull * g.ns * g.t, st);
       cudaMemsetAsync(b.cu, 0, 4ull * g.ns * g.t, st);
-      cudaMemsetAsync(b.dlam, 0, 4ull * g.ns * g.n * scan_blocks(uc), st);
+      cudaMemsetAsync(b.dlam, 0, 4ull * g.ns * g.n * std::max(scan_blocks(uc), kFsBwdParts), st);
       // without normalization dnum = dy: the kernels read dy in place (TMA / row loads
       // with bf16 -> fp16 conversion), so only the normalized path materialises rows
       if (den)
@@ -1341,7 +1656,14 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
           den ? b.dden : nullptr, w.vr, den ? w.wa : nullptr);
     }
     if (mode == 0 && launch_intra()) return 3;
-    if (g.n - 1 + g.prefix > 0) {
+    if (fused) {
+      // dA' and the reverse discumsum in one kernel (the stage keeps the dA name)
+      StageTimer tmr("bwd_query_state_dA", st);
+      auto fn = den ? k_tc_featscan_bwd<1> : k_tc_featscan_bwd<0>;
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, fm::SMEM_FS);
+      fn<<<dim3((NTH + fm::TPC - 1) / fm::TPC, g.ns), fm::THREADS, fm::SMEM_FS, st>>>(
+          m_qt, m_dn, m_dd, g, w.lamlog, w.stm, w.std_, b.dlam, b.ea, b.eg);
+    } else if (g.n - 1 + g.prefix > 0) {
       StageTimer tmr("bwd_query_state_dA", st);
       auto fn = den ? k_tc_featmajor<true, 1> : k_tc_featmajor<true, 0>;
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, fm::SMEM);
@@ -1358,7 +1680,7 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
     }
   }
   if (mode == 2 && launch_intra()) return 3;
-  {
+  if (!fused) {
     StageTimer tmr("bwd_discumsum", st);
     k_tc_scan_bwd<<<dim3(scan_blocks(uc), g.ns), 256, red_bytes, st>>>(g, uc, w.lamlog, (const float*)w.sp, w.stm,
                                                                           w.std_, b.dlam, carry, pre_out, 1, b.ea,
@@ -1376,12 +1698,12 @@ int tc_backward(const Geo& g, const void* q, const void* k, const void* v, const
   {
     StageTimer tmr("bwd_finish", st);
     if (dlog_g) {
-      k_tc_gate_finish<<<(g.ns * g.n + 3) / 4, 128, 0, st>>>(g, w.lamlog, b.dell, b.cu, b.dlam, scan_blocks(uc),
-                                                             dlog_g);
+      k_tc_gate_finish<<<(g.ns * g.n + 3) / 4, 128, 0, st>>>(g, w.lamlog, b.dell, b.cu, b.dlam,
+                                                             fused ? kFsBwdParts : scan_blocks(uc), dlog_g);
       count_launch();
     }
   }
-  count_launch(8);
+  count_launch(fused ? 7 : 8);
   return cuda_check("tc backward");
 }
 
