@@ -1090,7 +1090,7 @@ static int simt_backward_t(const Geo& g, const T* q, const T* k, const T* v, con
       ++launches;
     }
     if (int rc = tc4_states16(g, 1, b.dA, w.wt, w.tc4, st)) return rc;
-    if (int rc = tc4_vjp(g, true, k, b.dk32, nullptr, b.dellend, w.tc4, st)) return rc;
+    if (int rc = tc4_vjp(g, true, k, b.dk32, b.dell, b.dellend, w.tc4, st)) return rc;
     if (int rc = tc4_tok(g, 1, k, w.ell, w.lamlog, nullptr, nullptr, nullptr, nullptr, nullptr, b.dv32, w.tc4, st))
       return rc;
   } else {

@@ -45,7 +45,7 @@ constexpr int THREADS = 64 + 128 * FT;   // w0 TMA + TMEM, w1 MMA, 4 generate + 
 constexpr int SMEM = 1024 + ST * (XT_B + UB_B) + 16 * 32 * (DX + 1) * 4 + 512;
 // VJP GEMMs (k_tc4_vjp): dphi = U S^T in TMEM, expand-VJP on the CUDA cores
 constexpr int VS = 2;                 // B stages
-constexpr int VR = 36;                // fp32 per private row (x and dx; 144-byte rows)
+constexpr int VR = 36;                // sizes the x / dx shared area (3 x 128 x 36 fp32 >= 3 x 32 x 128 + 128)
 constexpr int VTHREADS = 320;         // w0 TMA + TMEM, w1 MMA, w2..w9 expand-VJP
 constexpr int VSMEM = 1024 + 16384 + VS * 16384 + 3 * 128 * VR * 4 + 512;
 // token-major GEMMs (k_tc4_tok): B = fp16 states [slot][64] in stages of 128 slots
@@ -78,22 +78,37 @@ __device__ __forceinline__ float pow2_inv(float m) {
 // ---------------------------------------------------------------- slot order
 // The tensor-core degree-4 pipeline orders features in blocks of four: block
 // (a, b, c, beta) holds the slots x_a x_b x_c x_d for d = 4 beta .. 4 beta + 3
-// (a <= b <= c, 4 beta + 3 >= c), blocks in lexicographic order.  Slots with
-// d < c repeat a feature and carry weight 0, so each NDMI feature (reference
-// expansions.py:106-123) appears once with its weight sqrt(4! / prod hist!)
-// (149-163); 62016 slots for D = 52360.  A token's slot row is generated from
-// one triple product per (a, b, c) and one 8-byte load per block.
+// (a <= b <= c <= 4 beta + 3).  Slots with d < c repeat a feature and carry
+// weight 0, so each NDMI feature (reference expansions.py:106-123) appears once
+// with its weight sqrt(4! / prod hist!) (149-163).  Blocks are grouped by beta
+// (each group padded with zero-weight blocks to whole 128-slot stages) and
+// ordered (a, b, c) inside a group, so the token-side kernels know a stage's
+// four d dims at compile time (x_d in registers) and reuse x_a x_b over runs of
+// c.  62464 slots for D = 52360.
 struct Tc4Tab {
   int* idx = nullptr;        // [slots][4]
   float* wt = nullptr;       // [slots]
   uint32_t* blk = nullptr;   // [slots / 4]: a | b << 8 | c << 16 | beta << 24
 };
+namespace t4 {
+constexpr int NBETA = t4::DX / 4;
+// 128-slot stages per beta group: ceil(C(4 beta + 6, 3) / 32)
+__host__ __device__ constexpr int beta_stages(int be) {
+  return be == 0 ? 1 : be == 1 ? 4 : be == 2 ? 12 : be == 3 ? 26 : be == 4 ? 49 : be == 5 ? 82 : be == 6 ? 127 : 187;
+}
+}  // namespace t4
 static std::vector<uint32_t> tc4_blocks() {
   std::vector<uint32_t> v;
-  for (int a = 0; a < t4::DX; ++a)
-    for (int b = a; b < t4::DX; ++b)
-      for (int c = b; c < t4::DX; ++c)
-        for (int be = c / 4; be < t4::DX / 4; ++be) v.push_back((uint32_t)(a | b << 8 | c << 16 | be << 24));
+  for (int be = 0; be < t4::NBETA; ++be) {
+    const size_t v0 = v.size();
+    for (int a = 0; a < t4::DX; ++a)
+      for (int b = a; b < t4::DX; ++b)
+        for (int c = b; c <= 4 * be + 3; ++c) v.push_back((uint32_t)(a | b << 8 | c << 16 | be << 24));
+    // zero-weight padding blocks: flagged 0x80 in the index bytes here, uploaded
+    // as (0, 0, 0, beta) (a valid block whose slots get weight 0)
+    while ((v.size() - v0) % 32) v.push_back((uint32_t)(be << 24) | 0x808080u);
+    if ((int)((v.size() - v0) / 32) != t4::beta_stages(be)) return {};
+  }
   return v;
 }
 int tc4_slots() {
@@ -113,13 +128,16 @@ static const Tc4Tab* tc4_tab() {
   const int ns = (int)blk.size() * 4;
   std::vector<int> idx((size_t)ns * 4);
   std::vector<float> wt(ns);
+  if (blk.empty()) return nullptr;
   for (size_t i = 0; i < blk.size(); ++i) {
-    const int a = blk[i] & 255, b = (blk[i] >> 8) & 255, c = (blk[i] >> 16) & 255, be = blk[i] >> 24;
+    const bool pad = (blk[i] & 0x808080u) != 0;
+    const int a = pad ? 0 : blk[i] & 255, b = pad ? 0 : (blk[i] >> 8) & 255, c = pad ? 0 : (blk[i] >> 16) & 255;
+    const int be = blk[i] >> 24;
     for (int z = 0; z < 4; ++z) {
       const int d = 4 * be + z, f = (int)i * 4 + z;
       const int o[4] = {a, b, c, d};
       for (int y = 0; y < 4; ++y) idx[(size_t)f * 4 + y] = o[y];
-      if (d < c) {
+      if (pad || d < c) {
         wt[f] = 0.f;
         continue;
       }
@@ -132,13 +150,16 @@ static const Tc4Tab* tc4_tab() {
       wt[f] = (float)sqrt(24.0 / den);
     }
   }
+  std::vector<uint32_t> dblk(blk);
+  for (auto& e : dblk)
+    if (e & 0x808080u) e &= 0xff000000u;
   Tc4Tab t;
   if (cudaMalloc(&t.idx, sizeof(int) * idx.size()) != cudaSuccess ||
       cudaMalloc(&t.wt, sizeof(float) * wt.size()) != cudaSuccess ||
       cudaMalloc(&t.blk, sizeof(uint32_t) * blk.size()) != cudaSuccess ||
       cudaMemcpy(t.idx, idx.data(), sizeof(int) * idx.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(t.wt, wt.data(), sizeof(float) * wt.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
-      cudaMemcpy(t.blk, blk.data(), sizeof(uint32_t) * blk.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaMemcpy(t.blk, dblk.data(), sizeof(uint32_t) * dblk.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
     cudaFree(t.idx);
     cudaFree(t.wt);
     cudaFree(t.blk);
@@ -650,7 +671,7 @@ __global__ void __launch_bounds__(t4::TTHREADS) k_tc4_tok(const __grid_constant_
 // kUpd = false (query side): x = sigma q, U = c dz, S = A_{k-1}: dq32 += sigma dx,
 //                            dell += dl
 // kUpd = true  (update side): x = k, U = W [v | 1], S = dS_k:  dk32 += dx,
-//                            dellend[chunk] += sum dl
+//                            dellend[chunk] += sum dl, dell -= dl (dl = W dW)
 template <bool kUpd>
 __global__ void __launch_bounds__(t4::VTHREADS) k_tc4_vjp(const __grid_constant__ CUtensorMap tm_ub,
                                                           const __grid_constant__ CUtensorMap tm_bs, Geo g,
@@ -664,9 +685,8 @@ __global__ void __launch_bounds__(t4::VTHREADS) k_tc4_vjp(const __grid_constant_
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* ub_s = smem;                    // 128 tokens x 64 fp16
   uint8_t* bs_s = ub_s + 16384;            // VS stages of 128 slots x 64 fp16
-  float* xr_s = (float*)(bs_s + VS * 16384);
-  float* dr_s = xr_s + 128 * VR;           // [2 halves][128][VR]
-  uint64_t* bars = (uint64_t*)(dr_s + 2 * 128 * VR);
+  float* xr_s = (float*)(bs_s + VS * 16384);   // x [32][128], dx [2][32][128], gsub 1's dl [128]
+  uint64_t* bars = (uint64_t*)(xr_s + 3 * 128 * VR);
   uint64_t* ufull = bars;            // 1
   uint64_t* full = ufull + 1;        // VS
   uint64_t* empty = full + VS;       // VS
@@ -730,14 +750,22 @@ __global__ void __launch_bounds__(t4::VTHREADS) k_tc4_vjp(const __grid_constant_
       tc_commit_w(&accf[bf]);
     }
   } else {
-    // eight warps: lane quadrant q, half gsub of every stage's 128 slots; each
-    // half keeps its own dx row, summed at the end
+    // eight warps: lane quadrant q, half gsub of every stage's 128 slots (16
+    // blocks).  Stages come in beta groups (beta_stages): inside a group the d
+    // dims 4 beta .. 4 beta + 3 are compile-time, so x_d and dx_d live in
+    // registers; x_a, x_b, x_c and dx_a, dx_b, dx_c are runtime-indexed in
+    // dim-major shared rows (xs[dim][128 tokens], dxs[gsub][dim][128]: one
+    // conflict-free wavefront per access).  Per block (a, b, c, beta) with
+    // cotangents g_z of its four slots and T = sum_z g_z x_{4 beta + z}:
+    //   dx_{4 beta + z} += g_z x_a x_b x_c,  dx_c += T x_a x_b,  U_ab += T x_c,
+    //   dl += T x_a x_b x_c;   at the end of an (a, b) run: dx_a += U x_b, dx_b += U x_a
     const int q = w & 3, gsub = (w - 2) >> 2, row = q * 32 + l, m = m0 + row;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    float* xr = xr_s + row * VR;
-    float* dr = dr_s + (gsub * 128 + row) * VR;
+    float* xs = xr_s;                          // [32][128]
+    float* dxs = xr_s + DX * 128 + gsub * DX * 128;   // [32][128] per gsub
+    float xv[DX], dxv[DX];
     {
-      const float xs = kUpd ? 1.f : g.scale;
+      const float xsc = kUpd ? 1.f : g.scale;
       const uint4* src = (const uint4*)(x + rowid(g, s, m) * DX);
 #pragma unroll
       for (int c8 = 0; c8 < 4; ++c8) {
@@ -746,88 +774,97 @@ __global__ void __launch_bounds__(t4::VTHREADS) k_tc4_vjp(const __grid_constant_
 #pragma unroll
         for (int e2 = 0; e2 < 4; ++e2) {
           const float2 f2 = __bfloat1622float2(*(const __nv_bfloat162*)&pv[e2]);
-          if (!gsub) {
-            xr[c8 * 8 + 2 * e2] = xs * f2.x;
-            xr[c8 * 8 + 2 * e2 + 1] = xs * f2.y;
-          }
-          dr[c8 * 8 + 2 * e2] = 0.f;
-          dr[c8 * 8 + 2 * e2 + 1] = 0.f;
+          xv[c8 * 8 + 2 * e2] = xsc * f2.x;
+          xv[c8 * 8 + 2 * e2 + 1] = xsc * f2.y;
         }
+      }
+#pragma unroll
+      for (int a = 0; a < DX; ++a) {
+        dxv[a] = 0.f;
+        dxs[a * 128 + row] = 0.f;
+        if (!gsub) xs[a * 128 + row] = xv[a];
       }
     }
     named_bar(1, 256);
     uint32_t prev = 0xffffffffu;
-    float xa = 0.f, xb = 0.f, xc = 0.f, P3 = 0.f, T = 0.f, dl = 0.f;
-    int ia = 0, ib = 0, ic = 0;
-    auto flush = [&]() {   // the finished triple's share: d/dx_a, d/dx_b, d/dx_c and dl
-      dr[ia] += T * xb * xc;
-      dr[ib] += T * xa * xc;
-      dr[ic] += T * xa * xb;
-      dl += T * P3;
-      T = 0.f;
+    float xa = 0.f, xb = 0.f, P2 = 0.f, U = 0.f, dl = 0.f;
+    int ia = 0, ib = 0;
+    auto flush = [&]() {
+      dxs[ia * 128 + row] += U * xb;
+      dxs[ib * 128 + row] += U * xa;
+      U = 0.f;
     };
-    for (int j = 0; j < nst; ++j) {
-      const int bf = j & 1;
-      const int bi = j * (SL / 4) + gsub * (SL / 8) + (l & 15);
-      const uint32_t mye = (l < 16 && bi < nblk) ? __ldg(blk + bi) : 0xffffffffu;
-      mbar_wait(&accf[bf], (j >> 1) & 1);
-      tc_fence_after();
-#pragma unroll 1
-      for (int c32 = 0; c32 < 2; ++c32) {
-        uint32_t r[32];
-        tmem_ld32(tm + (uint32_t)(bf * 128 + gsub * 64 + c32 * 32) + lane_off, r);
-        tc_wait_ld();
+    int j = 0;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const uint32_t e = __shfl_sync(0xffffffffu, mye, c32 * 8 + i);
-          if (e == 0xffffffffu) continue;
-          const uint32_t abc = e & 0xffffffu;
-          if (abc != prev) {
-            if (prev != 0xffffffffu) flush();
-            prev = abc;
-            ia = abc & 255;
-            ib = (abc >> 8) & 255;
-            ic = abc >> 16;
-            xa = xr[ia];
-            xb = xr[ib];
-            xc = xr[ic];
-            P3 = xa * xb * xc;
+    for (int be = 0; be < NBETA; ++be) {
+#pragma unroll 1
+      for (int js = 0; js < beta_stages(be); ++js, ++j) {
+        const int bf = j & 1;
+        const int bi = j * (SL / 4) + gsub * (SL / 8) + (l & 15);
+        const uint32_t mye = l < 16 ? __ldg(blk + bi) : 0u;
+        mbar_wait(&accf[bf], (j >> 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c32 = 0; c32 < 2; ++c32) {
+          uint32_t r[32];
+          tmem_ld32(tm + (uint32_t)(bf * 128 + gsub * 64 + c32 * 32) + lane_off, r);
+          tc_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint32_t e = __shfl_sync(0xffffffffu, mye, c32 * 8 + i);
+            const uint32_t ab = e & 0xffffu;
+            if (ab != prev) {
+              if (prev != 0xffffffffu) flush();
+              prev = ab;
+              ia = ab & 255;
+              ib = ab >> 8;
+              xa = xs[ia * 128 + row];
+              xb = xs[ib * 128 + row];
+              P2 = xa * xb;
+            }
+            const int ic = (e >> 16) & 255;
+            const float xc = xs[ic * 128 + row];
+            const float P3 = P2 * xc;
+            const float g0 = __uint_as_float(r[4 * i]), g1 = __uint_as_float(r[4 * i + 1]);
+            const float g2 = __uint_as_float(r[4 * i + 2]), g3 = __uint_as_float(r[4 * i + 3]);
+            const float T = fmaf(g0, xv[4 * be], fmaf(g1, xv[4 * be + 1], fmaf(g2, xv[4 * be + 2], g3 * xv[4 * be + 3])));
+            dxv[4 * be] = fmaf(g0, P3, dxv[4 * be]);
+            dxv[4 * be + 1] = fmaf(g1, P3, dxv[4 * be + 1]);
+            dxv[4 * be + 2] = fmaf(g2, P3, dxv[4 * be + 2]);
+            dxv[4 * be + 3] = fmaf(g3, P3, dxv[4 * be + 3]);
+            dxs[ic * 128 + row] += T * P2;
+            U = fmaf(T, xc, U);
+            dl = fmaf(T, P3, dl);
           }
-          const int d0 = 4 * (e >> 24);
-          const float4 xd = *(const float4*)(xr + d0);
-          const float g0 = __uint_as_float(r[4 * i]), g1 = __uint_as_float(r[4 * i + 1]);
-          const float g2 = __uint_as_float(r[4 * i + 2]), g3 = __uint_as_float(r[4 * i + 3]);
-          T = fmaf(g0, xd.x, fmaf(g1, xd.y, fmaf(g2, xd.z, fmaf(g3, xd.w, T))));
-          float4 dd = *(float4*)(dr + d0);
-          dd.x = fmaf(g0, P3, dd.x);
-          dd.y = fmaf(g1, P3, dd.y);
-          dd.z = fmaf(g2, P3, dd.z);
-          dd.w = fmaf(g3, P3, dd.w);
-          *(float4*)(dr + d0) = dd;
         }
+        tc_fence_before();
+        __syncwarp();
+        if (l == 0) mbar_arrive(&acce[bf]);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (l == 0) mbar_arrive(&acce[bf]);
     }
     if (prev != 0xffffffffu) flush();
-    // combine the two halves: gsub 1 parks dl in its row's padding column
-    if (gsub) dr[DX] = dl;
+    // fold the register dims in, then combine the two halves
+#pragma unroll
+    for (int a = 0; a < DX; ++a) dxs[a * 128 + row] += dxv[a];
+    float* dlx = xr_s + 3 * DX * 128;   // [128] gsub 1's dl
+    if (gsub) dlx[row] = dl;
     named_bar(1, 256);
     if (!gsub) {
-      const float* dr1 = dr_s + (128 + row) * VR;
-      dl += dr1[DX];
+      const float* d1 = xr_s + 2 * DX * 128;
+      dl += dlx[row];
       const float2 sc = scl[s * g.n + k];   // (sx, su) of the U rows of this chunk
       const float inv = 1.f / (sc.y * sb[s * g.n + kst]);
       const size_t it = (size_t)s * g.t + m;
       float* o = dx32 + it * DX;
       const float fx = inv * (kUpd ? 1.f : g.scale);
 #pragma unroll 8
-      for (int a = 0; a < DX; ++a) o[a] += fx * (dr[a] + dr1[a]);
+      for (int a = 0; a < DX; ++a) o[a] += fx * (dxs[a * 128 + row] + d1[a * 128 + row]);
       dl *= inv;
       if (!kUpd) {
         if (g.gated) dell[it] += dl;
       } else {
+        // dl = W_j dW_j with W_j = exp(ell_end - ell_j): +dl to the chunk end, -dl to token j
+        if (g.gated) dell[it] -= dl;
         dl = warp_sum(dl);
         if (l == 0) red[q] = dl;
       }

@@ -281,3 +281,27 @@ def test_fp16_inputs_on_tensor_cores(t, c, normalize):
     nw = {n: float(np.linalg.norm(r[n] - ref) / np.linalg.norm(ref)) for n, ref in pairs}
     print(f"fp16 caller values t={t} c={c} normalize={normalize}: norm-wise {nw}; elementwise {el}")
     assert all(e <= BF16_TOL for e in nw.values()), nw
+
+
+@pytest.mark.parametrize("normalize", [False, True])
+def test_p4_tensor_core_gated(normalize):
+    """The degree-4 tensor-core path (bf16, p=4, d=e=32) with gates (the log-gate
+    cotangent through both state VJPs) over four chunks; gates in [0.99, 1] so
+    the state path carries weight.  Unnormalized p=4 outputs are sums of
+    same-sign-dominated terms at this scale, so the elementwise bar applies."""
+    t, d, c = 1024, 32, 256
+    rng = np.random.default_rng(71 + normalize)
+    q, k, v = (rng.uniform(-1, 1, (1, t, 2, d)) for _ in range(3))
+    q, k, v = _bf16_exact(q, k, v)
+    g = rng.uniform(0.99, 1.0, (1, t, 2))
+    dy, = _bf16_exact(rng.uniform(-1, 1, (1, t, 2, d)))
+    r = _gpu_run(q, k, v, g, 4, c, normalize, dy)
+    if normalize:
+        _compare("p=4 gated normalized", r, q, k, v, g, 4, c, True, dy)
+        return
+    y_ref, _ = O.chunked_forward(q, k, v, g, 4, c)
+    dq, dk, dv, dg = O.chunked_backward(q, k, v, g, 4, c, dy)
+    errs = {n: float(np.linalg.norm(r[n] - ref) / np.linalg.norm(ref))
+            for n, ref in (("y", y_ref), ("dq", dq), ("dk", dk), ("dv", dv), ("dlogg", dg * g))}
+    print(f"p=4 gated: norm-wise {errs}")
+    assert all(e <= BF16_TOL for e in errs.values()), errs
