@@ -536,15 +536,19 @@ __global__ void __launch_bounds__(t4::TTHREADS) k_tc4_tok(const __grid_constant_
     }
     tc_commit_w(fin);
   } else {
-    // eight warps: lane quadrant q, half gsub of every stage's 128 slots
+    // eight warps: lane quadrant q, half gsub of every stage's 128 slots.  The
+    // token's x (fp16, scaled into [1, 2)) sits in registers as packed pairs
+    // (the block's d dims, compile-time per beta group) and in dim-major shared
+    // rows xs[dim][128] for the runtime a, b, c (one conflict-free wavefront per
+    // load); x_a x_b is reused over each run of c.
     const int q = w & 3, gsub = (w - 2) >> 2, row = q * 32 + l;
     const int m = k * g.c + tile * 128 + row;   // token of this lane
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    __half* xr = xr_s + row * XR;
+    __half* xs = xr_s;   // [32][128]
     float sx;
+    uint32_t xh[DX / 2];
     {
       const uint4* src = (const uint4*)(x + rowid(g, s, m) * DX);
-      // (both warps of a quadrant stage the same row; identical values)
       uint4 v4[4];
       float mx = 0.f;
 #pragma unroll
@@ -561,48 +565,54 @@ __global__ void __launch_bounds__(t4::TTHREADS) k_tc4_tok(const __grid_constant_
 #pragma unroll
       for (int c8 = 0; c8 < 4; ++c8) {
         const uint32_t* pv = (const uint32_t*)&v4[c8];
-        uint32_t o[4];
 #pragma unroll
         for (int e2 = 0; e2 < 4; ++e2) {
           const float2 f2 = __bfloat1622float2(*(const __nv_bfloat162*)&pv[e2]);
-          o[e2] = pack_f16(f2.x * sx, f2.y * sx);
+          const uint32_t hp = pack_f16(f2.x * sx, f2.y * sx);
+          xh[c8 * 4 + e2] = hp;
+          if (!gsub) {
+            xs[(c8 * 8 + 2 * e2) * 128 + row] = __ushort_as_half((unsigned short)(hp & 0xffffu));
+            xs[(c8 * 8 + 2 * e2 + 1) * 128 + row] = __ushort_as_half((unsigned short)(hp >> 16));
+          }
         }
-        *(uint2*)(xr + c8 * 8) = make_uint2(o[0], o[1]);
-        *(uint2*)(xr + c8 * 8 + 4) = make_uint2(o[2], o[3]);
       }
     }
-    __syncwarp();
-    uint32_t prev = 0xffffffffu, p3 = 0u;
-    for (int j = 0; j < nst; ++j) {
-      const int bf = j % TNB;
-      const int bi = j * (SL / 4) + gsub * (SL / 8) + (l & 15);
-      const uint32_t mye = (l < 16 && bi < nblk) ? __ldg(blk + bi) : 0xffffffffu;
-      if (j >= TNB) mbar_wait(&aempty[bf], ((j / TNB) + 1) & 1);
-      uint32_t o[32];
+    named_bar(1, 256);
+    uint32_t prev = 0xffffffffu;
+    __half p2 = __float2half(0.f);
+    if (has) {
+      int j = 0;
 #pragma unroll
-      for (int i = 0; i < SL / 8; ++i) {
-        const uint32_t e = __shfl_sync(0xffffffffu, mye, i);
-        if (e == 0xffffffffu) {   // padding slots past the table
-          o[2 * i] = o[2 * i + 1] = 0u;
-          continue;
+      for (int be = 0; be < NBETA; ++be) {
+#pragma unroll 1
+        for (int js = 0; js < beta_stages(be); ++js, ++j) {
+          const int bf = j % TNB;
+          const int bi = j * (SL / 4) + gsub * (SL / 8) + (l & 15);
+          const uint32_t mye = l < 16 ? __ldg(blk + bi) : 0u;
+          if (j >= TNB) mbar_wait(&aempty[bf], ((j / TNB) + 1) & 1);
+          uint32_t o[32];
+#pragma unroll
+          for (int i = 0; i < SL / 8; ++i) {
+            const uint32_t e = __shfl_sync(0xffffffffu, mye, i);
+            const uint32_t ab = e & 0xffffu;
+            if (ab != prev) {
+              prev = ab;
+              p2 = __hmul(xs[(ab & 255) * 128 + row], xs[(ab >> 8) * 128 + row]);
+            }
+            const __half p3 = __hmul(p2, xs[((e >> 16) & 255) * 128 + row]);
+            const __half2 t2 = __half2half2(p3);
+            const uint32_t p3w = *(const uint32_t*)&t2;
+            o[2 * i] = hmul2_f16(p3w, xh[2 * be]);
+            o[2 * i + 1] = hmul2_f16(p3w, xh[2 * be + 1]);
+          }
+          // this warp's half of the stage: 64 slots = 32 TMEM columns
+          tmem_st32(tm + 64u + (uint32_t)(bf * 64 + gsub * 32) + lane_off, o);
+          tc_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (l == 0) mbar_arrive(&afull[bf]);
         }
-        const uint32_t abc = e & 0xffffffu;
-        if (abc != prev) {
-          prev = abc;
-          const __half t = __hmul(__hmul(xr[abc & 255], xr[(abc >> 8) & 255]), xr[abc >> 16]);
-          const __half2 t2 = __half2half2(t);
-          p3 = *(const uint32_t*)&t2;
-        }
-        const uint2 pr = *(const uint2*)(xr + 4 * (e >> 24));
-        o[2 * i] = hmul2_f16(p3, pr.x);
-        o[2 * i + 1] = hmul2_f16(p3, pr.y);
       }
-      // this warp's half of the stage: 64 slots = 32 TMEM columns
-      tmem_st32(tm + 64u + (uint32_t)(bf * 64 + gsub * 32) + lane_off, o);
-      tc_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (l == 0) mbar_arrive(&afull[bf]);
     }
     // epilogue (the gsub 0 warps)
     if (!gsub) {
@@ -953,15 +963,24 @@ int tc4_state(const Geo& g, bool bwd, const void* x, const void* v, const float*
 
 // fp32 states [ns][n][slots][33] -> fp16 MMA operands; which = 0: forward
 // states A (bsa), 1: backward cotangents dS (bsd)
-int tc4_states16(const Geo& g, int which, const float* A, const float* wt, void* scratch, cudaStream_t st) {
+// mx_ready: the per-chunk maxima are already in the scratch (computed by the scan)
+int tc4_states16(const Geo& g, int which, const float* A, const float* wt, void* scratch, cudaStream_t st,
+                 bool mx_ready) {
   size_t nb;
   Tc4Ws w = tc4_carve(g, scratch, &nb);
   const int nsk = g.ns * g.n, Dp = tc4_padded_slots();
-  cudaMemsetAsync(w.mx, 0, sizeof(unsigned) * nsk, st);
-  k_tc4_max<<<dim3(32, nsk), 256, 0, st>>>(g.D, A, wt, w.mx);
+  if (!mx_ready) {
+    cudaMemsetAsync(w.mx, 0, sizeof(unsigned) * nsk, st);
+    k_tc4_max<<<dim3(32, nsk), 256, 0, st>>>(g.D, A, wt, w.mx);
+    count_launch();
+  }
   k_tc4_to16<<<dim3(64, nsk), 256, 0, st>>>(g.D, Dp, A, wt, w.mx, which ? w.bsd : w.bsa, which ? w.sbd : w.sba);
-  count_launch(2);
+  count_launch();
   return cuda_check("tc4 fp16 states");
+}
+unsigned* tc4_mx(const Geo& g, void* scratch) {
+  size_t nb;
+  return tc4_carve(g, scratch, &nb).mx;
 }
 
 // mode 0: y = combine(yat, phi(sigma q) A_{k-1}); mode 1: dv32 += W phi(k) dS_k
