@@ -1148,6 +1148,247 @@ __global__ void k_pub_discumsum(int n, int64_t L, int64_t M, const A* __restrict
 // host launchers
 // ==========================================================================
 
+// --------------------------------------------------------------------------
+// d = e = 32 (configs[2]) variants of the three intra-chunk kernels above with
+// the same math and the same tiling: the thread's own rows live in registers
+// and the shared key / query rows are read as broadcast float4s (the generic
+// kernels re-read every operand as scalars from shared memory: ~160 loads per
+// (query, key) pair against ~100 FMAs).
+// --------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ void load_row32(const T* src, float sc, float* dst) {
+#pragma unroll
+  for (int a = 0; a < 32; ++a) dst[a] = sc * to_f(src[a]);
+}
+template <typename T>
+__global__ void __launch_bounds__(64) k_intra_fwd_r(Geo g, const T* __restrict__ q, const T* __restrict__ k,
+                                                    const T* __restrict__ v, const float* __restrict__ ell,
+                                                    float* yat) {
+  __shared__ float4 Ks[64][8], Vs[64][8];
+  __shared__ float Ls[64];
+  const int tpc = (g.c + 63) / 64;
+  const int kch = blockIdx.x / tpc, tile = blockIdx.x - kch * tpc, s = blockIdx.y;
+  const int s0 = kch * g.c, s1 = min(s0 + g.c, g.t);
+  const int q0 = s0 + tile * 64;
+  if (q0 >= s1) return;
+  const int i = q0 + threadIdx.x;
+  const bool act = i < s1;
+  float qr[32], o[33];
+  if (act) load_row32(q + rowid(g, s, i) * 32, g.scale, qr);
+  else
+#pragma unroll
+    for (int a = 0; a < 32; ++a) qr[a] = 0.f;
+#pragma unroll
+  for (int u = 0; u < 33; ++u) o[u] = 0.f;
+  const float li = act ? ell[(size_t)s * g.t + i] : 0.f;
+  const int jend = min(q0 + 64, s1);
+  for (int j0 = s0; j0 < jend; j0 += 64) {
+    __syncthreads();
+    {
+      const int j = j0 + threadIdx.x;
+      const bool ok = j < jend;
+      float r[32];
+      if (ok) load_row32(k + rowid(g, s, j) * 32, 1.f, r);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) Ks[threadIdx.x][c] = ok ? make_float4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (ok) load_row32(v + rowid(g, s, j) * 32, 1.f, r);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) Vs[threadIdx.x][c] = ok ? make_float4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      Ls[threadIdx.x] = ok ? ell[(size_t)s * g.t + j] : 0.f;
+    }
+    __syncthreads();
+    const int jn = min(64, jend - j0);
+    for (int jj = 0; jj < jn; ++jj) {
+      if (act && j0 + jj <= i) {
+        float sd = 0.f;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 kk = Ks[jj][c];
+          sd = fmaf(qr[4 * c], kk.x, fmaf(qr[4 * c + 1], kk.y, fmaf(qr[4 * c + 2], kk.z, fmaf(qr[4 * c + 3], kk.w, sd))));
+        }
+        const float P = expf(li - Ls[jj]) * ipow(sd, g.p);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 vv = Vs[jj][c];
+          o[4 * c] = fmaf(P, vv.x, o[4 * c]);
+          o[4 * c + 1] = fmaf(P, vv.y, o[4 * c + 1]);
+          o[4 * c + 2] = fmaf(P, vv.z, o[4 * c + 2]);
+          o[4 * c + 3] = fmaf(P, vv.w, o[4 * c + 3]);
+        }
+        o[32] += P;
+      }
+    }
+  }
+  if (!act) return;
+  float4* out = (float4*)(yat + ((size_t)s * g.t + i) * 33);   // 132-byte rows: scalar stores
+  float* of = (float*)out;
+#pragma unroll
+  for (int u = 0; u < 33; ++u) of[u] = o[u];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(64) k_intra_bwd_q_r(Geo g, const T* __restrict__ q, const T* __restrict__ k,
+                                                      const T* __restrict__ v, const float* __restrict__ ell,
+                                                      const float* __restrict__ dz, float* dq32, float* dell) {
+  __shared__ float4 Ks[64][8], Vs[64][8];
+  __shared__ float Ls[64];
+  const int tpc = (g.c + 63) / 64;
+  const int kch = blockIdx.x / tpc, tile = blockIdx.x - kch * tpc, s = blockIdx.y;
+  const int s0 = kch * g.c, s1 = min(s0 + g.c, g.t);
+  const int q0 = s0 + tile * 64;
+  if (q0 >= s1) return;
+  const int i = q0 + threadIdx.x;
+  const bool act = i < s1;
+  float qr[32], zr[33], dqa[32];
+#pragma unroll
+  for (int a = 0; a < 32; ++a) {
+    qr[a] = 0.f;
+    zr[a] = 0.f;
+    dqa[a] = 0.f;
+  }
+  zr[32] = 0.f;
+  if (act) {
+    load_row32(q + rowid(g, s, i) * 32, g.scale, qr);
+    const float* zp = dz + ((size_t)s * g.t + i) * 33;
+#pragma unroll
+    for (int u = 0; u < 33; ++u) zr[u] = zp[u];
+  }
+  float rowD = 0.f;
+  const float li = act ? ell[(size_t)s * g.t + i] : 0.f;
+  const int jend = min(q0 + 64, s1);
+  for (int j0 = s0; j0 < jend; j0 += 64) {
+    __syncthreads();
+    {
+      const int j = j0 + threadIdx.x;
+      const bool ok = j < jend;
+      float r[32];
+      if (ok) load_row32(k + rowid(g, s, j) * 32, 1.f, r);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) Ks[threadIdx.x][c] = ok ? make_float4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (ok) load_row32(v + rowid(g, s, j) * 32, 1.f, r);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) Vs[threadIdx.x][c] = ok ? make_float4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      Ls[threadIdx.x] = ok ? ell[(size_t)s * g.t + j] : 0.f;
+    }
+    __syncthreads();
+    const int jn = min(64, jend - j0);
+    for (int jj = 0; jj < jn; ++jj) {
+      if (act && j0 + jj <= i) {
+        float kr[32];
+        float sd = 0.f, dP = zr[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 kk = Ks[jj][c];
+          kr[4 * c] = kk.x;
+          kr[4 * c + 1] = kk.y;
+          kr[4 * c + 2] = kk.z;
+          kr[4 * c + 3] = kk.w;
+          sd = fmaf(qr[4 * c], kk.x, fmaf(qr[4 * c + 1], kk.y, fmaf(qr[4 * c + 2], kk.z, fmaf(qr[4 * c + 3], kk.w, sd))));
+          const float4 vv = Vs[jj][c];
+          dP = fmaf(zr[4 * c], vv.x, fmaf(zr[4 * c + 1], vv.y, fmaf(zr[4 * c + 2], vv.z, fmaf(zr[4 * c + 3], vv.w, dP))));
+        }
+        const float E = expf(li - Ls[jj]);
+        const float sp1 = ipow(sd, g.p - 1);
+        rowD += dP * E * sp1 * sd;
+        const float ds = dP * E * g.p * sp1;
+#pragma unroll
+        for (int a = 0; a < 32; ++a) dqa[a] = fmaf(ds, kr[a], dqa[a]);
+      }
+    }
+  }
+  if (!act) return;
+  float* o = dq32 + ((size_t)s * g.t + i) * 32;
+#pragma unroll
+  for (int a = 0; a < 32; ++a) o[a] += g.scale * dqa[a];
+  dell[(size_t)s * g.t + i] += rowD;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(64) k_intra_bwd_kv_r(Geo g, const T* __restrict__ q, const T* __restrict__ k,
+                                                       const T* __restrict__ v, const float* __restrict__ ell,
+                                                       const float* __restrict__ dz, float* dk32, float* dv32,
+                                                       float* dell) {
+  __shared__ float4 Qs[64][8], Zs[64][8];
+  __shared__ float Zd[64], Ls[64];
+  const int tpc = (g.c + 63) / 64;
+  const int kch = blockIdx.x / tpc, tile = blockIdx.x - kch * tpc, s = blockIdx.y;
+  const int s0 = kch * g.c, s1 = min(s0 + g.c, g.t);
+  const int k0 = s0 + tile * 64;
+  if (k0 >= s1) return;
+  const int j = k0 + threadIdx.x;
+  const bool act = j < s1;
+  float kr[32], vr[32], dka[32], dva[32];
+#pragma unroll
+  for (int a = 0; a < 32; ++a) {
+    kr[a] = vr[a] = 0.f;
+    dka[a] = dva[a] = 0.f;
+  }
+  if (act) {
+    load_row32(k + rowid(g, s, j) * 32, 1.f, kr);
+    load_row32(v + rowid(g, s, j) * 32, 1.f, vr);
+  }
+  float colD = 0.f;
+  const float lj = act ? ell[(size_t)s * g.t + j] : 0.f;
+  for (int i0 = k0; i0 < s1; i0 += 64) {
+    __syncthreads();
+    {
+      const int i = i0 + threadIdx.x;
+      const bool ok = i < s1;
+      float r[32];
+      if (ok) load_row32(q + rowid(g, s, i) * 32, g.scale, r);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) Qs[threadIdx.x][c] = ok ? make_float4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float* zp = dz + ((size_t)s * g.t + i) * 33;
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        Zs[threadIdx.x][c] = ok ? make_float4(zp[4 * c], zp[4 * c + 1], zp[4 * c + 2], zp[4 * c + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      Zd[threadIdx.x] = ok ? zp[32] : 0.f;
+      Ls[threadIdx.x] = ok ? ell[(size_t)s * g.t + i] : 0.f;
+    }
+    __syncthreads();
+    const int in = min(64, s1 - i0);
+    for (int ii = 0; ii < in; ++ii) {
+      if (act && i0 + ii >= j) {
+        float sd = 0.f, dP = Zd[ii];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 qq = Qs[ii][c];
+          sd = fmaf(qq.x, kr[4 * c], fmaf(qq.y, kr[4 * c + 1], fmaf(qq.z, kr[4 * c + 2], fmaf(qq.w, kr[4 * c + 3], sd))));
+          const float4 zz = Zs[ii][c];
+          dP = fmaf(zz.x, vr[4 * c], fmaf(zz.y, vr[4 * c + 1], fmaf(zz.z, vr[4 * c + 2], fmaf(zz.w, vr[4 * c + 3], dP))));
+        }
+        const float E = expf(Ls[ii] - lj);
+        const float sp1 = ipow(sd, g.p - 1);
+        const float P = E * sp1 * sd;
+        colD += dP * P;
+        const float ds = dP * E * g.p * sp1;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 qq = Qs[ii][c];
+          dka[4 * c] = fmaf(ds, qq.x, dka[4 * c]);
+          dka[4 * c + 1] = fmaf(ds, qq.y, dka[4 * c + 1]);
+          dka[4 * c + 2] = fmaf(ds, qq.z, dka[4 * c + 2]);
+          dka[4 * c + 3] = fmaf(ds, qq.w, dka[4 * c + 3]);
+          const float4 zz = Zs[ii][c];
+          dva[4 * c] = fmaf(P, zz.x, dva[4 * c]);
+          dva[4 * c + 1] = fmaf(P, zz.y, dva[4 * c + 1]);
+          dva[4 * c + 2] = fmaf(P, zz.z, dva[4 * c + 2]);
+          dva[4 * c + 3] = fmaf(P, zz.w, dva[4 * c + 3]);
+        }
+      }
+    }
+  }
+  if (!act) return;
+  float* ok_ = dk32 + ((size_t)s * g.t + j) * 32;
+  float* ov = dv32 + ((size_t)s * g.t + j) * 32;
+#pragma unroll
+  for (int a = 0; a < 32; ++a) {
+    ok_[a] += dka[a];
+    ov[a] += dva[a];
+  }
+  dell[(size_t)s * g.t + j] -= colD;
+}
+
 // dynamic shared memory per block for the kernels above (floats -> bytes)
 template <int DM> constexpr size_t smb_intra_fwd() { return 4 * (2 * 64 * (DM + 1)); }
 template <int DM> constexpr size_t smb_query_combine() { return 4 * (qc_tokens<DM>() * (DM + 1) + 32 * state_row_stride<DM>()); }
@@ -1174,7 +1415,10 @@ static int simt_forward_t(const Geo& g, const T* q, const T* k, const T* v, cons
                           float* rowsum, const SimtWs& w, cudaStream_t st) {
   const int tpc = (g.c + 63) / 64;
   k_gate_prep<<<(g.ns * g.n + 127) / 128, 128, 0, st>>>(g, log_g, w.ell, w.lamlog);
-  k_intra_fwd<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_intra_fwd<T, DM>, smb_intra_fwd<DM>()), st>>>(g, q, k, v, w.ell, w.yat);
+  if (DM == 32 && g.d == 32 && g.e == 32)
+    k_intra_fwd_r<T><<<dim3(g.n * tpc, g.ns), 64, 0, st>>>(g, q, k, v, w.ell, w.yat);
+  else
+    k_intra_fwd<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_intra_fwd<T, DM>, smb_intra_fwd<DM>()), st>>>(g, q, k, v, w.ell, w.yat);
   if (tc4_supported(g, g.dtype)) {
     if (int rc = tc4_state(g, false, k, v, nullptr, w.ell, w.lamlog, w.idx, w.wt, w.tc4, w.A, st)) return rc;
   } else if constexpr (DM <= 64)
@@ -1262,8 +1506,13 @@ static int simt_backward_t(const Geo& g, const T* q, const T* k, const T* v, con
                         dyn_smem(k_update_bwd<T, DM>, smb_update_bwd<DM>()), st>>>(g, k, v, b.dA, w.idx, w.wt, w.ell, w.lamlog, b.dk32, b.dv32, b.dell, b.dellend);
   ++launches;
   }
-  k_intra_bwd_q<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_intra_bwd_q<T, DM>, smb_intra_bwd<DM>()), st>>>(g, q, k, v, w.ell, b.dz, b.dq32, b.dell);
-  k_intra_bwd_kv<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_intra_bwd_kv<T, DM>, smb_intra_bwd<DM>()), st>>>(g, q, k, v, w.ell, b.dz, b.dk32, b.dv32, b.dell);
+  if (DM == 32 && g.d == 32 && g.e == 32) {
+    k_intra_bwd_q_r<T><<<dim3(g.n * tpc, g.ns), 64, 0, st>>>(g, q, k, v, w.ell, b.dz, b.dq32, b.dell);
+    k_intra_bwd_kv_r<T><<<dim3(g.n * tpc, g.ns), 64, 0, st>>>(g, q, k, v, w.ell, b.dz, b.dk32, b.dv32, b.dell);
+  } else {
+    k_intra_bwd_q<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_intra_bwd_q<T, DM>, smb_intra_bwd<DM>()), st>>>(g, q, k, v, w.ell, b.dz, b.dq32, b.dell);
+    k_intra_bwd_kv<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_intra_bwd_kv<T, DM>, smb_intra_bwd<DM>()), st>>>(g, q, k, v, w.ell, b.dz, b.dk32, b.dv32, b.dell);
+  }
   launches += 3;
   if (dlogg) {
     k_gate_finish<<<(g.ns * g.n + 127) / 128, 128, 0, st>>>(g, w.lamlog, b.dell, b.dellend, b.dlam, dlogg);
