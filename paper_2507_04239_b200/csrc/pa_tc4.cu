@@ -88,7 +88,7 @@ __device__ __forceinline__ float pow2_inv(float m) {
 struct Tc4Tab {
   int* idx = nullptr;        // [slots][4]
   float* wt = nullptr;       // [slots]
-  uint32_t* blk = nullptr;   // [slots / 4]: a | b << 8 | c << 16 | beta << 24
+  uint32_t* blk = nullptr;   // [slots / 4]: a | c << 9 | b << 14 | beta << 24 (see tc4_tab)
 };
 namespace t4 {
 constexpr int NBETA = t4::DX / 4;
@@ -150,9 +150,15 @@ static const Tc4Tab* tc4_tab() {
       wt[f] = (float)sqrt(24.0 / den);
     }
   }
-  std::vector<uint32_t> dblk(blk);
-  for (auto& e : dblk)
-    if (e & 0x808080u) e &= 0xff000000u;
+  // device encoding (token-side kernels): a | c << 9 | b << 14 | beta << 24, so the
+  // byte offset of x_c in a dim-major fp32 row block [32][128] is e & 0x3e00 and the
+  // run key (a, b) is e & 0x7c01f; padding blocks are (0, 0, 0, beta)
+  std::vector<uint32_t> dblk(blk.size());
+  for (size_t i = 0; i < blk.size(); ++i) {
+    const uint32_t e = blk[i];
+    const uint32_t a = e & 255, b = (e >> 8) & 255, c = (e >> 16) & 255, be = e >> 24;
+    dblk[i] = (e & 0x808080u) ? (be << 24) : (a | c << 9 | b << 14 | be << 24);
+  }
   Tc4Tab t;
   if (cudaMalloc(&t.idx, sizeof(int) * idx.size()) != cudaSuccess ||
       cudaMalloc(&t.wt, sizeof(float) * wt.size()) != cudaSuccess ||
@@ -580,6 +586,7 @@ __global__ void __launch_bounds__(t4::TTHREADS) k_tc4_tok(const __grid_constant_
     named_bar(1, 256);
     uint32_t prev = 0xffffffffu;
     __half p2 = __float2half(0.f);
+    const __half* xrow = xs + row;
     if (has) {
       int j = 0;
 #pragma unroll
@@ -594,12 +601,12 @@ __global__ void __launch_bounds__(t4::TTHREADS) k_tc4_tok(const __grid_constant_
 #pragma unroll
           for (int i = 0; i < SL / 8; ++i) {
             const uint32_t e = __shfl_sync(0xffffffffu, mye, i);
-            const uint32_t ab = e & 0xffffu;
+            const uint32_t ab = e & 0x7c01fu;
             if (ab != prev) {
               prev = ab;
-              p2 = __hmul(xs[(ab & 255) * 128 + row], xs[(ab >> 8) * 128 + row]);
+              p2 = __hmul(xs[(ab & 31) * 128 + row], xs[(ab >> 14) * 128 + row]);
             }
-            const __half p3 = __hmul(p2, xs[((e >> 16) & 255) * 128 + row]);
+            const __half p3 = __hmul(p2, *(const __half*)((const uint8_t*)xrow + ((e & 0x3e00u) >> 1)));
             const __half2 t2 = __half2half2(p3);
             const uint32_t p3w = *(const uint32_t*)&t2;
             o[2 * i] = hmul2_f16(p3w, xh[2 * be]);
@@ -767,8 +774,8 @@ __global__ void __launch_bounds__(t4::VTHREADS) k_tc4_vjp(const __grid_constant_
     // dim-major shared rows (xs[dim][128 tokens], dxs[gsub][dim][128]: one
     // conflict-free wavefront per access).  Per block (a, b, c, beta) with
     // cotangents g_z of its four slots and T = sum_z g_z x_{4 beta + z}:
-    //   dx_{4 beta + z} += g_z x_a x_b x_c,  dx_c += T x_a x_b,  U_ab += T x_c,
-    //   dl += T x_a x_b x_c;   at the end of an (a, b) run: dx_a += U x_b, dx_b += U x_a
+    //   dx_{4 beta + z} += g_z x_a x_b x_c,  dx_c += T x_a x_b,  U_ab += T x_c;
+    //   at the end of an (a, b) run: dx_a += U x_b, dx_b += U x_a, dl += x_a x_b U
     const int q = w & 3, gsub = (w - 2) >> 2, row = q * 32 + l, m = m0 + row;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     float* xs = xr_s;                          // [32][128]
@@ -802,8 +809,11 @@ __global__ void __launch_bounds__(t4::VTHREADS) k_tc4_vjp(const __grid_constant_
     auto flush = [&]() {
       dxs[ia * 128 + row] += U * xb;
       dxs[ib * 128 + row] += U * xa;
+      dl = fmaf(P2, U, dl);   // sum over the run of T x_a x_b x_c
       U = 0.f;
     };
+    const float* xrow = xs + row;
+    float* dxrow = dxs + row;
     int j = 0;
 #pragma unroll
     for (int be = 0; be < NBETA; ++be) {
@@ -822,18 +832,18 @@ __global__ void __launch_bounds__(t4::VTHREADS) k_tc4_vjp(const __grid_constant_
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const uint32_t e = __shfl_sync(0xffffffffu, mye, c32 * 8 + i);
-            const uint32_t ab = e & 0xffffu;
+            const uint32_t ab = e & 0x7c01fu;
             if (ab != prev) {
               if (prev != 0xffffffffu) flush();
               prev = ab;
-              ia = ab & 255;
-              ib = ab >> 8;
+              ia = ab & 31;
+              ib = ab >> 14;
               xa = xs[ia * 128 + row];
               xb = xs[ib * 128 + row];
               P2 = xa * xb;
             }
-            const int ic = (e >> 16) & 255;
-            const float xc = xs[ic * 128 + row];
+            const uint32_t co = e & 0x3e00u;   // byte offset of dim c in a [32][128] fp32 block
+            const float xc = *(const float*)((const uint8_t*)xrow + co);
             const float P3 = P2 * xc;
             const float g0 = __uint_as_float(r[4 * i]), g1 = __uint_as_float(r[4 * i + 1]);
             const float g2 = __uint_as_float(r[4 * i + 2]), g3 = __uint_as_float(r[4 * i + 3]);
@@ -842,9 +852,9 @@ __global__ void __launch_bounds__(t4::VTHREADS) k_tc4_vjp(const __grid_constant_
             dxv[4 * be + 1] = fmaf(g1, P3, dxv[4 * be + 1]);
             dxv[4 * be + 2] = fmaf(g2, P3, dxv[4 * be + 2]);
             dxv[4 * be + 3] = fmaf(g3, P3, dxv[4 * be + 3]);
-            dxs[ic * 128 + row] += T * P2;
-            U = fmaf(T, xc, U);
-            dl = fmaf(T, P3, dl);
+            float* dc = (float*)((uint8_t*)dxrow + co);
+            *dc = fmaf(T, P2, *dc);
+            U = fmaf(T, xc, U);   // the run's dl share is P2 U (flush)
           }
         }
         tc_fence_before();
