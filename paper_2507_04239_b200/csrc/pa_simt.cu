@@ -384,43 +384,21 @@ __global__ void k_discumsum_states(Geo g, const float* __restrict__ lamlog, floa
 }
 
 // The same scan with 4 consecutive entries per thread and SC_PF chunks of loads
-// in flight (the one-load-per-iteration loop above is latency-bound).  mx != 0:
-// also the per-chunk max |A_k[f][u] wt[f]| (the fp16 operand scale of the
-// degree-4 tensor-core path, pa_tc4.cu), so no separate max pass reads A again.
-// Dynamic shared memory: n x 8 floats.  Needs D * E1 % 4 == 0.
+// in flight (the one-load-per-iteration loop above is latency-bound).  Needs
+// D * E1 % 4 == 0.
 constexpr int SC_PF = 4;
-__device__ __forceinline__ float max4w(float4 v, const float* w) {
-  return fmaxf(fmaxf(fabsf(v.x * w[0]), fabsf(v.y * w[1])), fmaxf(fabsf(v.z * w[2]), fabsf(v.w * w[3])));
-}
-__device__ __forceinline__ float warp_max_f(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-__global__ void __launch_bounds__(256) k_discumsum_states4(Geo g, const float* __restrict__ lamlog, float* A,
-                                                           const float* __restrict__ wt, unsigned* mx) {
-  extern __shared__ float red4[];   // [n][8] chunk maxima per warp
+__global__ void __launch_bounds__(256) k_discumsum_states4(Geo g, const float* __restrict__ lamlog, float* A) {
   const size_t per4 = (size_t)g.D * g.E1 / 4;
-  const int s = blockIdx.y, wq = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = blockIdx.y;
   const size_t m4 = blockIdx.x * (size_t)256 + threadIdx.x;
-  const bool ok = m4 < per4;
+  if (m4 >= per4) return;
   float4* p = (float4*)(A + (size_t)s * g.n * per4 * 4) + m4;
-  float w4[4] = {0.f, 0.f, 0.f, 0.f};
-  if (mx && ok)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) w4[i] = wt[(4 * m4 + i) / g.E1];
-  auto track = [&](int k, float4 v) {
-    if (!mx) return;
-    const float m = warp_max_f(ok ? max4w(v, w4) : 0.f);
-    if (lane == 0) red4[k * 8 + wq] = m;
-  };
-  float4 prev = ok ? p[0] : make_float4(0.f, 0.f, 0.f, 0.f);
-  track(0, prev);
+  float4 prev = p[0];
   for (int k0 = 1; k0 < g.n; k0 += SC_PF) {
     float4 x[SC_PF];
 #pragma unroll
     for (int i = 0; i < SC_PF; ++i)
-      x[i] = (ok && k0 + i < g.n) ? p[(size_t)(k0 + i) * per4] : make_float4(0.f, 0.f, 0.f, 0.f);
+      x[i] = k0 + i < g.n ? p[(size_t)(k0 + i) * per4] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int i = 0; i < SC_PF; ++i) {
       const int k = k0 + i;
@@ -430,17 +408,8 @@ __global__ void __launch_bounds__(256) k_discumsum_states4(Geo g, const float* _
       prev.y = __fadd_rn(__fmul_rn(lam, prev.y), x[i].y);
       prev.z = __fadd_rn(__fmul_rn(lam, prev.z), x[i].z);
       prev.w = __fadd_rn(__fmul_rn(lam, prev.w), x[i].w);
-      if (ok) p[(size_t)k * per4] = prev;
-      track(k, prev);
+      p[(size_t)k * per4] = prev;
     }
-  }
-  if (!mx) return;
-  __syncthreads();
-  for (int k = threadIdx.x; k < g.n; k += 256) {
-    float m = 0.f;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) m = fmaxf(m, red4[k * 8 + i]);
-    atomicMax(mx + s * g.n + k, __float_as_uint(m));
   }
 }
 
@@ -712,76 +681,6 @@ __global__ void __launch_bounds__(256) k_discumsum_bwd(Geo g, const float* __res
     if (ok) {
       acc = dp[(size_t)k * per] + lam * acc;
       dp[(size_t)k * per] = acc;
-    }
-  }
-}
-
-// The same reverse scan with 4 entries per thread, SC_PF chunks of loads in
-// flight and the dlambda partials reduced per warp into shared memory (one block
-// reduction at the end instead of one per chunk); mx != 0: the per-chunk max
-// |dS_k wt| as in k_discumsum_states4.  Dynamic shared memory: 2 x n x 8 floats.
-__global__ void __launch_bounds__(256) k_discumsum_bwd4(Geo g, const float* __restrict__ lamlog,
-                                                        const float* __restrict__ A, float* dA, float* dlam,
-                                                        const float* __restrict__ wt, unsigned* mx) {
-  extern __shared__ float red4[];   // [n][8] dlambda partials, then [n][8] maxima
-  float* redm = red4 + g.n * 8;
-  const size_t per4 = (size_t)g.D * g.E1 / 4;
-  const int s = blockIdx.y, wq = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t m4 = blockIdx.x * (size_t)256 + threadIdx.x;
-  const bool ok = m4 < per4;
-  const float4* ap = (const float4*)(A + (size_t)s * g.n * per4 * 4) + m4;
-  float4* dp = (float4*)(dA + (size_t)s * g.n * per4 * 4) + m4;
-  float w4[4] = {0.f, 0.f, 0.f, 0.f};
-  if (mx && ok)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) w4[i] = wt[(4 * m4 + i) / g.E1];
-  auto track = [&](int k, float4 v) {
-    if (!mx) return;
-    const float m = warp_max_f(ok ? max4w(v, w4) : 0.f);
-    if (lane == 0) redm[k * 8 + wq] = m;
-  };
-  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  float4 acc = ok ? dp[(size_t)(g.n - 1) * per4] : z4;
-  track(g.n - 1, acc);
-  if (threadIdx.x < 8) red4[threadIdx.x] = 0.f;   // dlambda_0 has no term
-  for (int k1 = g.n - 2; k1 >= 0; k1 -= SC_PF) {
-    float4 a[SC_PF], d[SC_PF];
-#pragma unroll
-    for (int i = 0; i < SC_PF; ++i) {
-      const int k = k1 - i;
-      const bool in = ok && k >= 0;
-      a[i] = in ? ap[(size_t)k * per4] : z4;
-      d[i] = in ? dp[(size_t)k * per4] : z4;
-    }
-#pragma unroll
-    for (int i = 0; i < SC_PF; ++i) {
-      const int k = k1 - i;
-      if (k < 0) break;
-      float part = a[i].x * acc.x + a[i].y * acc.y + a[i].z * acc.z + a[i].w * acc.w;
-      part = warp_sum(part);
-      if (lane == 0) red4[(k + 1) * 8 + wq] = part;
-      const float lam = g.gated ? expf(lamlog[s * g.n + k + 1]) : 1.f;
-      acc.x = d[i].x + lam * acc.x;
-      acc.y = d[i].y + lam * acc.y;
-      acc.z = d[i].z + lam * acc.z;
-      acc.w = d[i].w + lam * acc.w;
-      if (ok) dp[(size_t)k * per4] = acc;
-      track(k, acc);
-    }
-  }
-  __syncthreads();
-  for (int k = threadIdx.x; k < g.n; k += 256) {
-    if (k >= 1) {
-      float t = 0.f;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) t += red4[k * 8 + i];
-      atomicAdd(dlam + s * g.n + k, t);
-    }
-    if (mx) {
-      float m = 0.f;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) m = fmaxf(m, redm[k * 8 + i]);
-      atomicMax(mx + s * g.n + k, __float_as_uint(m));
     }
   }
 }
@@ -1427,22 +1326,22 @@ static int simt_forward_t(const Geo& g, const T* q, const T* k, const T* v, cons
   else
     k_state_accum<T, T, DM><<<dim3((g.D + 31) / 32, g.n, g.ns), 256, 0, st>>>(
         g, k, 1.f, g.gated ? 1 : 0, w.ell, w.lamlog, v, 1, g.e, g.e, 1, w.idx, w.wt, 0, 0, w.A);
-  const bool scan4 = ((size_t)g.D * g.E1) % 4 == 0 && (size_t)g.n * 64 <= 48 * 1024;
+  const bool scan4 = ((size_t)g.D * g.E1) % 4 == 0;
   const bool tc4 = tc4_supported(g, g.dtype);
-  unsigned* mx = (tc4 && scan4) ? tc4_mx(g, w.tc4) : nullptr;
-  if (mx) cudaMemsetAsync(mx, 0, sizeof(unsigned) * g.ns * g.n, st);
-  if (scan4 && (g.n > 1 || mx))
-    k_discumsum_states4<<<dim3((unsigned)(((size_t)g.D * g.E1 / 4 + 255) / 256), g.ns), 256, mx ? g.n * 32 : 0, st>>>(
-        g, w.lamlog, w.A, w.wt, mx);
+  if (tc4) {
+    // discumsum + fp16 operands in one pass, then the state query + combine on
+    // the tensor cores (phi(q) generated on chip)
+    if (int rc = tc4_scan_fwd(g, w.lamlog, w.A, w.wt, w.tc4, st)) return rc;
+    if (int rc = tc4_tok(g, 0, q, w.ell, w.lamlog, w.yat, y, rowsum, w.y32, w.zflag, nullptr, w.tc4, st)) return rc;
+  } else {
+  if (scan4 && g.n > 1)
+    k_discumsum_states4<<<dim3((unsigned)(((size_t)g.D * g.E1 / 4 + 255) / 256), g.ns), 256, 0, st>>>(
+        g, w.lamlog, w.A);
   else if (g.n > 1)
     k_discumsum_states<<<dim3((unsigned)std::min<size_t>(((size_t)g.D * g.E1 + 255) / 256, 512), g.ns), 256, 0, st>>>(g, w.lamlog, w.A);
-  if (tc4) {
-    // state query + combine on the tensor cores (phi(q) generated on chip)
-    if (int rc = tc4_states16(g, 0, w.A, w.wt, w.tc4, st, mx != nullptr)) return rc;
-    if (int rc = tc4_tok(g, 0, q, w.ell, w.lamlog, w.yat, y, rowsum, w.y32, w.zflag, nullptr, w.tc4, st)) return rc;
-  } else
   k_query_combine<T, DM><<<dim3(g.n * ((g.c + qc_tokens<DM>() - 1) / qc_tokens<DM>()), g.ns), qc_tokens<DM>(),
                            dyn_smem(k_query_combine<T, DM>, smb_query_combine<DM>()), st>>>(g, q, w.A, w.idx, w.wt, w.ell, w.yat, y, rowsum, w.zflag, w.y32);
+  }
   count_launch(g.n > 1 ? 5 : 4);
   return cuda_check("simt forward");
 }
@@ -1470,19 +1369,9 @@ static int simt_backward_t(const Geo& g, const T* q, const T* k, const T* v, con
       if (int rc = tc4_state(g, true, q, nullptr, b.dz, w.ell, w.lamlog, w.idx, w.wt, w.tc4, b.dA, st)) return rc;
       if (int rc = tc4_vjp(g, false, q, b.dq32, b.dell, nullptr, w.tc4, st)) return rc;
     }
-    // reverse scan (+ the per-chunk max of the fp16 operands when it can fuse it)
-    const bool scan4 = per % 4 == 0 && (size_t)g.n * 64 <= 48 * 1024;
-    unsigned* mx = scan4 ? tc4_mx(g, w.tc4) : nullptr;
-    if (mx) {
-      cudaMemsetAsync(mx, 0, sizeof(unsigned) * g.ns * g.n, st);
-      k_discumsum_bwd4<<<dim3((unsigned)((per / 4 + 255) / 256), g.ns), 256, g.n * 64, st>>>(g, w.lamlog, w.A, b.dA,
-                                                                                           b.dlam, w.wt, mx);
-      ++launches;
-    } else if (g.n > 1) {
-      k_discumsum_bwd<<<dim3((unsigned)((per + 255) / 256), g.ns), 256, 0, st>>>(g, w.lamlog, w.A, b.dA, b.dlam);
-      ++launches;
-    }
-    if (int rc = tc4_states16(g, 1, b.dA, w.wt, w.tc4, st, mx != nullptr)) return rc;
+    // reverse discumsum + fp16 operands of the state cotangents in one pass
+    if (g.n == 1) cudaMemsetAsync(tc4_mxs(g, w.tc4), 0, sizeof(unsigned) * g.ns, st);
+    if (int rc = tc4_scan_bwd(g, w.lamlog, w.A, b.dA, b.dlam, w.wt, w.tc4, st)) return rc;
     if (int rc = tc4_vjp(g, true, k, b.dk32, b.dell, b.dellend, w.tc4, st)) return rc;
     if (int rc = tc4_tok(g, 1, k, w.ell, w.lamlog, nullptr, nullptr, nullptr, nullptr, nullptr, b.dv32, w.tc4, st))
       return rc;

@@ -25,9 +25,11 @@ int tc4_state(const Geo& g, bool bwd, const void* x, const void* v, const float*
 // slot count of the degree-4 block order; copies its (idx, wt) table into a workspace
 int tc4_slots();
 int tc4_copy_tables(int* idx, float* wt, cudaStream_t st);
-int tc4_states16(const Geo& g, int which, const float* A, const float* wt, void* scratch, cudaStream_t st,
-                 bool mx_ready = false);
-unsigned* tc4_mx(const Geo& g, void* scratch);   // per-(stream, chunk) max scratch of tc4_states16
+unsigned* tc4_mxs(const Geo& g, void* scratch);  // per-chunk maxima recorded by tc4_state
+// discumsum fused with the fp16 operand conversion (pa_tc4.cu)
+int tc4_scan_fwd(const Geo& g, const float* lamlog, float* A, const float* wt, void* scratch, cudaStream_t st);
+int tc4_scan_bwd(const Geo& g, const float* lamlog, const float* A, const float* dA, float* dlam, const float* wt,
+                 void* scratch, cudaStream_t st);
 int tc4_vjp(const Geo& g, bool upd, const void* x, float* dx32, float* dell, float* dellend, void* scratch,
             cudaStream_t st);
 int tc4_tok(const Geo& g, int mode, const void* x, const float* ell, const float* lamlog, const float* yat, void* y,

@@ -75,6 +75,12 @@ __device__ __forceinline__ float pow2_inv(float m) {
   return __int_as_float((127 - e) << 23);
 }
 
+__device__ __forceinline__ float warp_max4(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
 // ---------------------------------------------------------------- slot order
 // The tensor-core degree-4 pipeline orders features in blocks of four: block
 // (a, b, c, beta) holds the slots x_a x_b x_c x_d for d = 4 beta .. 4 beta + 3
@@ -281,7 +287,8 @@ template <bool kBwd>
 __global__ void __launch_bounds__(t4::THREADS) k_tc4_state(const __grid_constant__ CUtensorMap tm_xt,
                                                            const __grid_constant__ CUtensorMap tm_ub, Geo g,
                                                            const int* __restrict__ idx, const float* __restrict__ wt,
-                                                           const float2* __restrict__ scl, float xs4, float* out) {
+                                                           const float2* __restrict__ scl, float xs4, float* out,
+                                                           unsigned* mxo) {
   using namespace t4;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -394,7 +401,9 @@ __global__ void __launch_bounds__(t4::THREADS) k_tc4_state(const __grid_constant
     if (ft < nft) {
       float* stg = stg_s + (w - 2) * 32 * (DX + 1);
       const float2 sc = scl[s * g.n + kin];
-      const float fw = live ? wt[f] * xs4 / (sc.x * sc.x * sc.x * sc.x * sc.y) : 0.f;
+      const float wf = live ? wt[f] : 0.f;
+      const float fw = wf * xs4 / (sc.x * sc.x * sc.x * sc.x * sc.y);
+      float mrow = 0.f;
 #pragma unroll
       for (int c0 = 0; c0 < 48; c0 += 16) {
         uint32_t r[16];
@@ -402,8 +411,15 @@ __global__ void __launch_bounds__(t4::THREADS) k_tc4_state(const __grid_constant
         tc_wait_ld();
 #pragma unroll
         for (int c = 0; c < 16; ++c)
-          if (c0 + c <= DX) stg[l * (DX + 1) + c0 + c] = fw * __uint_as_float(r[c]);
+          if (c0 + c <= DX) {
+            const float val = fw * __uint_as_float(r[c]);
+            stg[l * (DX + 1) + c0 + c] = val;
+            mrow = fmaxf(mrow, fabsf(val * wf));
+          }
       }
+      // the chunk's max |S' w| (the fp16 operand scale bound of tc4_scan_fwd / bwd)
+      mrow = warp_max4(mrow);
+      if (l == 0 && live) atomicMax(mxo + s * g.n + kout, __float_as_uint(mrow));
       __syncwarp();
       const int f0 = (grp * FT + ft) * 128 + q * 32;
       const int nf = max(0, min(32, g.D - f0));
@@ -420,43 +436,6 @@ __global__ void __launch_bounds__(t4::THREADS) k_tc4_state(const __grid_constant
 // States (fp32 [sk][slots][33]) as the fp16 B operand of the token-major GEMMs:
 // bs[sk][slot][0..63] = w_slot x state x sB(sk), sB a power of two from the
 // block's max (pass 1), zero in the padding columns and slots.
-__global__ void __launch_bounds__(256) k_tc4_max(int D, const float* __restrict__ A, const float* __restrict__ wt,
-                                                 unsigned* mx) {
-  __shared__ float red[8];
-  const int sk = blockIdx.y;
-  const float* a = A + (size_t)sk * D * 33;
-  float m = 0.f;
-  for (size_t i = blockIdx.x * 256 + threadIdx.x; i < (size_t)D * 33; i += (size_t)gridDim.x * 256)
-    m = fmaxf(m, fabsf(a[i] * wt[i / 33]));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int i = 1; i < 8; ++i) m = fmaxf(m, red[i]);
-    atomicMax(mx + sk, __float_as_uint(m));
-  }
-}
-__global__ void __launch_bounds__(256) k_tc4_to16(int D, int Dp, const float* __restrict__ A,
-                                                  const float* __restrict__ wt, const unsigned* __restrict__ mx,
-                                                  __half* bs, float* sb) {
-  const int sk = blockIdx.y;
-  const float sB = pow2_inv(__uint_as_float(mx[sk]));
-  if (blockIdx.x == 0 && threadIdx.x == 0) sb[sk] = sB;
-  const float* a = A + (size_t)sk * D * 33;
-  uint32_t* o = (uint32_t*)bs + (size_t)sk * Dp * 32;
-  for (size_t i = blockIdx.x * 256 + threadIdx.x; i < (size_t)Dp * 32; i += (size_t)gridDim.x * 256) {
-    const int f = (int)(i >> 5), c2 = (int)(i & 31) * 2;
-    float v0 = 0.f, v1 = 0.f;
-    if (f < D && c2 < 33) {
-      const float w = wt[f] * sB;
-      v0 = a[(size_t)f * 33 + c2] * w;
-      if (c2 + 1 < 33) v1 = a[(size_t)f * 33 + c2 + 1] * w;
-    }
-    o[i] = pack_f16(v0, v1);
-  }
-}
-
 // ---------------------------------------------------------------- token-major GEMM
 // Y[m][u] = sum_slot phi'_slot(x_m) bs[slot][u]: M = 128 tokens on the TMEM
 // lanes, K = slots, N = 48.  A = phi'(x) generated into TMEM by four warps from
@@ -910,7 +889,7 @@ struct Tc4Ws {
   __half* bsd;    // backward state cotangents dS_k, same layout
   float* sba;     // sB per (stream, chunk) of bsa
   float* sbd;     // sB per (stream, chunk) of bsd
-  unsigned* mx;   // max-reduction scratch [ns][n]
+  unsigned* mxs;  // per-chunk max |S'_k w| (forward) / |dA'_k w| (backward) from k_tc4_state
 };
 static Tc4Ws tc4_carve(const Geo& g, void* base, size_t* bytes) {
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
@@ -932,7 +911,7 @@ static Tc4Ws tc4_carve(const Geo& g, void* base, size_t* bytes) {
   w.bsd = (__half*)take(bs);
   w.sba = (float*)take(sk * 4);
   w.sbd = (float*)take(sk * 4);
-  w.mx = (unsigned*)take(sk * 4);
+  w.mxs = (unsigned*)take(sk * 4);
   *bytes = off;
   return w;
 }
@@ -944,6 +923,7 @@ size_t tc4_extra_bytes(const Geo& g) {
 
 int tc4_state(const Geo& g, bool bwd, const void* x, const void* v, const float* dz, const float* ell,
               const float* lamlog, const int* idx, const float* wt, void* scratch, float* out, cudaStream_t st) {
+  // (also records the per-chunk max |out w| for tc4_scan_fwd / tc4_scan_bwd)
   using namespace t4;
   size_t nb;
   Tc4Ws w = tc4_carve(g, scratch, &nb);
@@ -965,32 +945,161 @@ int tc4_state(const Geo& g, bool bwd, const void* x, const void* v, const float*
   const float s2 = bwd ? g.scale * g.scale : 1.f;
   auto fn = bwd ? k_tc4_state<true> : k_tc4_state<false>;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  cudaMemsetAsync(w.mxs, 0, sizeof(unsigned) * g.ns * g.n, st);
   fn<<<dim3(((g.D + 127) / 128 + FT - 1) / FT, nk, g.ns), THREADS, SMEM, st>>>(m_xt, m_ub, g, idx, wt, scl, s2 * s2,
-                                                                                out);
+                                                                                out, w.mxs);
   count_launch();
   return cuda_check("tc4 state GEMM");
 }
 
-// fp32 states [ns][n][slots][33] -> fp16 MMA operands; which = 0: forward
-// states A (bsa), 1: backward cotangents dS (bsd)
-// mx_ready: the per-chunk maxima are already in the scratch (computed by the scan)
-int tc4_states16(const Geo& g, int which, const float* A, const float* wt, void* scratch, cudaStream_t st,
-                 bool mx_ready) {
+unsigned* tc4_mxs(const Geo& g, void* scratch) {
+  size_t nb;
+  return tc4_carve(g, scratch, &nb).mxs;
+}
+
+// ---------------------------------------------------------------- scans
+// The discumsum over the chunk states fused with their conversion to the fp16
+// MMA operands (replaces the separate scan, max and conversion passes).  The
+// per-chunk power-of-two operand scale comes from an upper bound of max |A_k w|
+// built from the per-chunk maxima k_tc4_state records:
+//   forward  B_0 = m_0,           B_k = lambda_k B_{k-1} + m_k  >= max |A_k w|
+//   backward D_{n-1} = m'_{n-1},  D_k = m'_k + lambda_{k+1} D_{k+1} >= max |dS_k w|
+// so stored operands stay below 2 (no overflow) while values near the max keep
+// the full fp16 mantissa.  One thread = 4 operand columns of one slot (16
+// threads per slot, the last ones writing the zero padding columns 33..63 that
+// the state-VJP GEMM contracts over).
+//   forward:  A_k = lambda_k A_{k-1} + S'_k in place (fp32, read by the backward's
+//             dlambda), bsa = A_k w 2^-e (fp16), sba = 2^-e
+//   backward: dS_k = dA'_k + lambda_{k+1} dS_{k+1} (not stored in fp32),
+//             dlambda_{k+1} += <A_k, dS_{k+1}>, bsd = dS_k w 2^-e, sbd = 2^-e
+__global__ void __launch_bounds__(256) k_tc4_scan_fwd16(Geo g, const float* __restrict__ lamlog, float* A,
+                                                        const float* __restrict__ wt,
+                                                        const unsigned* __restrict__ mxs, int Dp, __half* bs,
+                                                        float* sb) {
+  const int s = blockIdx.y;
+  const size_t gid = blockIdx.x * (size_t)256 + threadIdx.x;
+  const int f = (int)(gid >> 4), u0 = (int)(gid & 15) * 4;
+  if (f >= Dp) return;
+  const bool live = f < g.D;
+  const float w = live ? wt[f] : 0.f;
+  const size_t per = (size_t)g.D * 33;
+  float* src = A + (size_t)s * g.n * per + (size_t)f * 33 + u0;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  float B = 0.f;
+  constexpr int PF = 4;   // chunks of loads in flight
+  for (int k0 = 0; k0 < g.n; k0 += PF) {
+    float x[PF][4];
+#pragma unroll
+    for (int j = 0; j < PF; ++j)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        x[j][i] = (live && u0 + i < 33 && k0 + j < g.n) ? src[(size_t)(k0 + j) * per + i] : 0.f;
+#pragma unroll
+    for (int j = 0; j < PF; ++j) {
+      const int k = k0 + j;
+      if (k >= g.n) break;
+      const float lam = (k > 0 && g.gated) ? expf(lamlog[s * g.n + k]) : 1.f;
+      const float m = __uint_as_float(mxs[s * g.n + k]);
+      B = k > 0 ? fmaf(lam, B, m) : m;
+      const float sc = pow2_inv(B);
+      if (gid == 0) sb[s * g.n + k] = sc;
+      float* p = src + (size_t)k * per;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[i] = k > 0 ? __fadd_rn(__fmul_rn(lam, acc[i]), x[j][i]) : x[j][i];
+        if (live && u0 + i < 33) p[i] = acc[i];
+      }
+      const float ws = w * sc;
+      *(uint2*)(bs + ((size_t)(s * g.n + k) * Dp + f) * 64 + u0) =
+          make_uint2(pack_f16(acc[0] * ws, acc[1] * ws), pack_f16(acc[2] * ws, acc[3] * ws));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_tc4_scan_bwd16(Geo g, const float* __restrict__ lamlog,
+                                                        const float* __restrict__ A, const float* __restrict__ dA,
+                                                        float* dlam, const float* __restrict__ wt,
+                                                        const unsigned* __restrict__ mxs, int Dp, __half* bs,
+                                                        float* sb) {
+  extern __shared__ float redk[];   // [n][8] dlambda partials per warp
+  const int s = blockIdx.y, wq = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t gid = blockIdx.x * (size_t)256 + threadIdx.x;
+  const int f = (int)(gid >> 4), u0 = (int)(gid & 15) * 4;
+  const bool live = f < g.D;
+  const float w = live ? wt[f] : 0.f;
+  const size_t per = (size_t)g.D * 33;
+  const float* ap = A + (size_t)s * g.n * per + (size_t)f * 33 + u0;
+  const float* dp = dA + (size_t)s * g.n * per + (size_t)f * 33 + u0;
+  auto ld4 = [&](const float* p, float* o) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[i] = (live && u0 + i < 33) ? p[i] : 0.f;
+  };
+  auto emit = [&](int k, const float* acc, float D) {
+    const float sc = pow2_inv(D);
+    if (gid == 0) sb[s * g.n + k] = sc;
+    if (f < Dp) {
+      const float ws = w * sc;
+      *(uint2*)(bs + ((size_t)(s * g.n + k) * Dp + f) * 64 + u0) =
+          make_uint2(pack_f16(acc[0] * ws, acc[1] * ws), pack_f16(acc[2] * ws, acc[3] * ws));
+    }
+  };
+  float acc[4];
+  ld4(dp + (size_t)(g.n - 1) * per, acc);
+  float D = __uint_as_float(mxs[s * g.n + g.n - 1]);
+  emit(g.n - 1, acc, D);
+  constexpr int PF = 4;   // chunks of loads in flight
+  for (int k1 = g.n - 2; k1 >= 0; k1 -= PF) {
+    float a[PF][4], d[PF][4];
+#pragma unroll
+    for (int j = 0; j < PF; ++j) {
+      if (k1 - j >= 0) {
+        ld4(ap + (size_t)(k1 - j) * per, a[j]);
+        ld4(dp + (size_t)(k1 - j) * per, d[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < PF; ++j) {
+    const int k = k1 - j;
+    if (k < 0) break;
+    float part = a[j][0] * acc[0] + a[j][1] * acc[1] + a[j][2] * acc[2] + a[j][3] * acc[3];
+    part = warp_sum(part);
+    if (lane == 0) redk[(k + 1) * 8 + wq] = part;
+    const float lam = g.gated ? expf(lamlog[s * g.n + k + 1]) : 1.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i] = d[j][i] + lam * acc[i];
+    D = fmaf(lam, D, __uint_as_float(mxs[s * g.n + k]));
+    emit(k, acc, D);
+    }
+  }
+  __syncthreads();
+  for (int k = 1 + threadIdx.x; k < g.n; k += 256) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += redk[k * 8 + i];
+    atomicAdd(dlam + s * g.n + k, t);
+  }
+}
+
+int tc4_scan_fwd(const Geo& g, const float* lamlog, float* A, const float* wt, void* scratch, cudaStream_t st) {
   size_t nb;
   Tc4Ws w = tc4_carve(g, scratch, &nb);
-  const int nsk = g.ns * g.n, Dp = tc4_padded_slots();
-  if (!mx_ready) {
-    cudaMemsetAsync(w.mx, 0, sizeof(unsigned) * nsk, st);
-    k_tc4_max<<<dim3(32, nsk), 256, 0, st>>>(g.D, A, wt, w.mx);
-    count_launch();
-  }
-  k_tc4_to16<<<dim3(64, nsk), 256, 0, st>>>(g.D, Dp, A, wt, w.mx, which ? w.bsd : w.bsa, which ? w.sbd : w.sba);
+  const int Dp = tc4_padded_slots();
+  k_tc4_scan_fwd16<<<dim3((unsigned)(((size_t)Dp * 16 + 255) / 256), g.ns), 256, 0, st>>>(g, lamlog, A, wt, w.mxs, Dp,
+                                                                                          w.bsa, w.sba);
   count_launch();
-  return cuda_check("tc4 fp16 states");
+  return cuda_check("tc4 forward scan");
 }
-unsigned* tc4_mx(const Geo& g, void* scratch) {
+
+int tc4_scan_bwd(const Geo& g, const float* lamlog, const float* A, const float* dA, float* dlam, const float* wt,
+                 void* scratch, cudaStream_t st) {
   size_t nb;
-  return tc4_carve(g, scratch, &nb).mx;
+  Tc4Ws w = tc4_carve(g, scratch, &nb);
+  const int Dp = tc4_padded_slots();
+  if ((size_t)g.n * 32 > 48 * 1024) return 3;
+  k_tc4_scan_bwd16<<<dim3((unsigned)(((size_t)Dp * 16 + 255) / 256), g.ns), 256, g.n * 32, st>>>(
+      g, lamlog, A, dA, dlam, wt, w.mxs, Dp, w.bsd, w.sbd);
+  count_launch();
+  return cuda_check("tc4 backward scan");
 }
 
 // mode 0: y = combine(yat, phi(sigma q) A_{k-1}); mode 1: dv32 += W phi(k) dS_k
