@@ -18,11 +18,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 # bench stage -> kernel-name fragments (pa_tc*.cu)
 STAGES = {
     "fwd_prep": ["k_tc_prep_gates", "k_tc_prep_xt#fwd", "k_tc_prep_rows#fwd"],
-    "fwd_update_state": ["k_tc_featmajor<0"],
+    "fwd_update_state": ["k_tc_featscan<", "k_tc_featmajor<0"],
     "fwd_discumsum": ["k_tc_scan_fwd"],
     "fwd_attn_query": ["k_tc_out"],
     "bwd_prep": ["k_tc_bwd_prep", "k_tc_prep_xt#bwd", "k_tc_prep_rows#bwd"],
-    "bwd_query_state_dA": ["k_tc_featmajor<1"],
+    "bwd_query_state_dA": ["k_tc_featscan_bwd", "k_tc_featmajor<1"],
     "bwd_discumsum": ["k_tc_scan_bwd"],
     "bwd_intra": ["k_tc_intra_bwd", "k_tc_ib"],
     "bwd_query_state_dq": ["k_tc_zvjp<0", "k_tc_dq_chunk0"],
@@ -86,7 +86,7 @@ def main():
     traffic = {}
     phase = "fwd"
     for r in step:
-        if "k_tc_bwd_prep" in r["name"] or ("featmajor<1" in r["name"]):
+        if "k_tc_bwd_prep" in r["name"] or "featmajor<1" in r["name"] or "featscan_bwd" in r["name"]:
             phase = "bwd"
         if r["name"].startswith("k_tc_prep_xt") and phase == "fwd" and any(
                 "k_tc_out" in x["name"] for x in step[: step.index(r)]):
