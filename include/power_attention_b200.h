@@ -51,7 +51,10 @@ enum pa_flags {
   PA_FLAG_DETERMINISTIC = 1,
   /* Refuse (PA_ERR_UNSUPPORTED) instead of running a 16-bit problem on the fp32
    * CUDA-core kernels when the tensor-core kernels do not cover its shape. */
-  PA_FLAG_STRICT_TC = 2
+  PA_FLAG_STRICT_TC = 2,
+  /* Sequence-parallel / streaming states always carry the key-sum column (the
+   * reference ChunkState.key_sum), also when the call does not normalize. */
+  PA_FLAG_KEY_SUM = 4
 };
 
 /* One power_full problem (reference AttentionConfig attention.py:106-171 +

@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PA_B200_LIB") or os.path.join(HERE, "libpa_b200.so")
 
 PA_F32, PA_BF16, PA_F16, PA_F64 = 0, 1, 2, 3
-PA_FLAG_DETERMINISTIC, PA_FLAG_STRICT_TC = 1, 2
+PA_FLAG_DETERMINISTIC, PA_FLAG_STRICT_TC, PA_FLAG_KEY_SUM = 1, 2, 4
 
 _ERRORS = {
     1: InvalidSpec,

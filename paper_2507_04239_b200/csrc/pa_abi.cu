@@ -135,6 +135,7 @@ static int make_geo(const pa_problem* pr, Geo* g) {
   g->ns = pr->b * pr->h;
   g->scale = pr->has_scale ? (float)pr->scale : 1.0f / sqrtf((float)pr->d);
   g->det = (pr->flags & PA_FLAG_DETERMINISTIC) ? 1 : 0;
+  g->keysum = (pr->flags & PA_FLAG_KEY_SUM) ? 1 : 0;
   g->normalize = pr->normalize ? 1 : 0;
   g->gated = pr->gated ? 1 : 0;
   g->bth = 1;

@@ -29,6 +29,7 @@ struct Geo {
   // zero-padded copy (tensor-core path)
   int treal;
   int dtype;   // pa_dtype of q, k, v
+  int keysum;  // PA_FLAG_KEY_SUM: states carry the key-sum column even without normalize
 };
 
 __host__ __device__ __forceinline__ size_t rowid(const Geo& g, int s, int m) {

@@ -1526,7 +1526,7 @@ int tc_forward(const Geo& g, const void* q, const void* k, const void* v, const 
   size_t need;
   TcFwdWs w = carve_fwd(g, ws, &need);
   DeviceGuard dg(q);
-  const int with_den = (g.normalize || rowsum) ? 1 : 0;
+  const int with_den = (g.normalize || rowsum || g.keysum) ? 1 : 0;
   CUtensorMap m_q, m_k, m_v, m_vr, m_wa, m_kt;
   if (!map_bth(&m_q, q, g, 128) || !map_bth(&m_k, k, g, 128) || !map_bth(&m_v, v, g, 128) ||
       !map_2d(&m_vr, w.vr, (size_t)g.ns * g.t, HD, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
