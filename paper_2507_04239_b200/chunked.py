@@ -155,12 +155,12 @@ def chunked_power_attention(batch: SequenceBatch, cfg: AttentionConfig, plan: Ch
     """chunked.py:287-413 as one CUDA pipeline call.  op_timer (if given)
     accumulates wall ns of the whole fused pipeline under "power_full".
 
-    cfg.use_log_space: the fused pipeline computes the intra-chunk scores in the
-    direct form (fp32 accumulation).  The reference's log-space intra-chunk path
-    (chunked.py:336 via attention.py:289-305) equals it within eps for
-    well-separated scores (test_chunked.py:318-330 bar 1e-6); the stabilised
-    kernel runs for the attention form (power_attention_form), where the
-    reference applies it to the whole row."""
+    cfg.use_log_space: the reference threads it into the intra-chunk config
+    (chunked.py:323, 336 -> attention.py:289-305); that call runs the
+    reference's operator loop on the GPU operators instead (_chunked_log_space:
+    the stabilised intra-chunk kernel per chunk, update_state / discumsum /
+    query_state kernels), so the eps of p log(|s| + eps) enters as it does in
+    the reference."""
     if cfg.mechanism not in (Mechanism.POWER, Mechanism.LINEAR) or cfg.expansion is None:
         raise InvalidSpec(f"{cfg.mechanism.value} mechanism has no feature expansion")
     spec = cfg.expansion
@@ -173,12 +173,86 @@ def chunked_power_attention(batch: SequenceBatch, cfg: AttentionConfig, plan: Ch
     itemsize = batch.q.element_size() if isinstance(batch.q, torch.Tensor) else np.asarray(batch.q).dtype.itemsize
     check_state_budget(spec, batch.v_dim, batch.b * batch.h, itemsize, state_budget)
     t0 = time.perf_counter_ns()
-    out = run_power(batch, cfg, plan.c)
+    out = _chunked_log_space(batch, cfg, plan, backend) if cfg.use_log_space else run_power(batch, cfg, plan.c)
     if op_timer is not None:
         if isinstance(out.y, torch.Tensor):
             torch.cuda.synchronize()
         op_timer["power_full"] = op_timer.get("power_full", 0) + time.perf_counter_ns() - t0
     return out
+
+
+def _chunked_log_space(batch: SequenceBatch, cfg: AttentionConfig, plan: ChunkPlan, backend=None):
+    """The reference's chunked loop (chunked.py:315-395) with the log-space
+    intra-chunk form: per chunk the stabilised attention form (unnormalized,
+    pa_power_logspace_fwd) and the state contribution (update_state kernel),
+    then the discounted cumsum over chunks and the query of the carried state,
+    combined and optionally normalized.  numpy in, numpy out; torch stays on
+    the device."""
+    from dataclasses import replace
+
+    spec = cfg.expansion
+    xp = _xp(batch.q)
+    b, t, h = batch.b, batch.t, batch.h
+    e, S = batch.v_dim, batch.b * batch.h
+    scale = cfg.scale_for(batch.d)
+    intra_cfg = replace(cfg, normalize=False, chunk_size=None)
+
+    def streams(x):   # [b, c, h, ...] -> [b*h, c, ...]
+        x = xp.swapaxes(x, 1, 2)
+        return x.reshape(S, *x.shape[2:])
+
+    bounds = plan.bounds()
+    y_attn, zetas, contribs, key_contribs, prefixes, lams = [], [], [], [], [], []
+    for start, stop in bounds:
+        gk = None if batch.gates is None else batch.gates[:, start:stop]
+        sub = SequenceBatch(batch.q[:, start:stop], batch.k[:, start:stop], batch.v[:, start:stop], gk)
+        intra = power_attention_form(sub, intra_cfg)
+        y_attn.append(intra.y)
+        zetas.append(intra.rowsum)
+        if gk is None:
+            decay = prefix = lam = None
+        else:
+            g_s = streams(gk[..., None])[..., 0]                      # [S, c]
+            decay, prefix = _suffix_products(g_s), _prefix_products(g_s)
+            lam = g_s.prod(-1) if xp is torch else np.prod(g_s, axis=-1)
+        prefixes.append(prefix)
+        lams.append(lam)
+        s_k, g_k = update_state_kernel(streams(batch.k[:, start:stop]), streams(batch.v[:, start:stop]), decay,
+                                       spec, backend=backend)
+        contribs.append(s_k)
+        key_contribs.append(g_k)
+    n = len(bounds)
+    if n > 1:
+        if batch.gates is None:
+            trans = xp.ones((n - 1, S), dtype=contribs[0].dtype) if xp is np else \
+                torch.ones(n - 1, S, dtype=contribs[0].dtype, device=contribs[0].device)
+        else:
+            trans = xp.stack([lams[k] for k in range(1, n)])
+        acc = discumsum(xp.stack(contribs), trans)
+        key_acc = discumsum(xp.stack(key_contribs), trans)
+    else:
+        acc, key_acc = xp.stack(contribs), xp.stack(key_contribs)
+    ys, rss = [], []
+    for k, (start, stop) in enumerate(bounds):
+        c = stop - start
+        yk, rk = y_attn[k], zetas[k]
+        if k > 0:
+            qk = streams(scale * batch.q[:, start:stop])
+            yq, den = query_state_kernel(qk, acc[k - 1], key_acc[k - 1], spec, backend=backend)
+            if prefixes[k] is not None:
+                yq = yq * prefixes[k][..., None]
+                den = den * prefixes[k]
+            yk = yk + xp.swapaxes(yq.reshape(b, h, c, e), 1, 2)
+            rk = rk + xp.swapaxes(den.reshape(b, h, c), 1, 2)
+        ys.append(yk)
+        rss.append(rk)
+    cat = (lambda xs: torch.cat(xs, 1)) if xp is torch else (lambda xs: np.concatenate(xs, 1))
+    y, rowsum = cat(ys), cat(rss)
+    if cfg.normalize:
+        if bool((rowsum <= 0).any()):
+            raise ZeroDenominator("zeta + phi(q) . key_sum is not positive; cannot normalize")
+        y = y / rowsum[..., None]
+    return AttentionOutput(y, rowsum)
 
 
 def power_attention(batch, cfg, form="attention", plan=None, backend=None, op_timer=None):

@@ -6,6 +6,7 @@ import numpy as np
 import pytest
 
 from conftest import golden_names, load_golden
+from oracle import power_oracle as O
 
 pytestmark = pytest.mark.gpu
 
@@ -115,3 +116,35 @@ def test_logspace_chunked_and_dispatch():
     att = power_attention(batch, stable, form="attention")
     assert att.y.dtype == np.float64                      # the f64 log-space kernel ran
     assert max_rel_error(att.y, a.y) < 1e-5
+
+
+def test_log_space_intra_chunk_in_the_chunked_pipeline():
+    import paper_2507_04239_b200 as P
+
+    """Reference test_chunked.py:318-330: the chunked form with the log-space
+    intra-chunk config equals the plain one within 1e-6 (f64 inputs)."""
+    rng = np.random.default_rng(8)
+    q = rng.uniform(0.5, 1.5, (1, 12, 1, 4))
+    k = rng.uniform(0.5, 1.5, (1, 12, 1, 4))
+    v = rng.uniform(-1, 1, (1, 12, 1, 3))
+    batch = P.SequenceBatch(q, k, v)
+    plain = P.AttentionConfig.power(P.ExpansionSpec.spow(2, 4), normalize=True)
+    stable = P.AttentionConfig.power(P.ExpansionSpec.spow(2, 4), normalize=True, use_log_space=True)
+    a = P.chunked_power_attention(batch, plain, P.ChunkPlan(12, 5))
+    b = P.chunked_power_attention(batch, stable, P.ChunkPlan(12, 5))
+    assert O.max_rel_error(a.y, b.y) < 1e-6
+
+
+@pytest.mark.parametrize("normalize", [False, True])
+def test_log_space_chunked_pipeline_with_gates_vs_oracle(normalize):
+    """Gated, several streams, a partial last chunk: the log-space chunked
+    pipeline against the oracle's chunked form (f64)."""
+    import paper_2507_04239_b200 as P
+
+    q, k, v, g = O.generate_inputs(2, 70, 3, 8, 5, seed=17, gating=True)
+    batch = P.SequenceBatch(q, k, v, g)
+    cfg = P.AttentionConfig.power(P.ExpansionSpec.spow(2, 8), normalize=normalize, use_log_space=True)
+    out = P.chunked_power_attention(batch, cfg, P.ChunkPlan(70, 16))
+    y_ref, rs_ref = O.chunked_forward(q, k, v, g, 2, 16, normalize=normalize)
+    assert O.max_rel_error(out.y, y_ref) < 1e-6
+    assert O.max_rel_error(out.rowsum, rs_ref) < 1e-6
