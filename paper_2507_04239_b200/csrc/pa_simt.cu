@@ -1099,12 +1099,16 @@ __global__ void __launch_bounds__(64) k_intra_fwd_r(Geo g, const T* __restrict__
     const int jn = min(64, jend - j0);
     for (int jj = 0; jj < jn; ++jj) {
       if (act && j0 + jj <= i) {
-        float sd = 0.f;
+        float sp[4] = {0.f, 0.f, 0.f, 0.f};   // four independent FMA chains
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const float4 kk = Ks[jj][c];
-          sd = fmaf(qr[4 * c], kk.x, fmaf(qr[4 * c + 1], kk.y, fmaf(qr[4 * c + 2], kk.z, fmaf(qr[4 * c + 3], kk.w, sd))));
+          sp[0] = fmaf(qr[4 * c], kk.x, sp[0]);
+          sp[1] = fmaf(qr[4 * c + 1], kk.y, sp[1]);
+          sp[2] = fmaf(qr[4 * c + 2], kk.z, sp[2]);
+          sp[3] = fmaf(qr[4 * c + 3], kk.w, sp[3]);
         }
+        const float sd = (sp[0] + sp[1]) + (sp[2] + sp[3]);
         const float P = expf(li - Ls[jj]) * ipow(sd, g.p);
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
@@ -1174,7 +1178,7 @@ __global__ void __launch_bounds__(64) k_intra_bwd_q_r(Geo g, const T* __restrict
     for (int jj = 0; jj < jn; ++jj) {
       if (act && j0 + jj <= i) {
         float kr[32];
-        float sd = 0.f, dP = zr[32];
+        float sp[4] = {0.f, 0.f, 0.f, 0.f}, dp[4] = {zr[32], 0.f, 0.f, 0.f};   // independent FMA chains
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const float4 kk = Ks[jj][c];
@@ -1182,10 +1186,18 @@ __global__ void __launch_bounds__(64) k_intra_bwd_q_r(Geo g, const T* __restrict
           kr[4 * c + 1] = kk.y;
           kr[4 * c + 2] = kk.z;
           kr[4 * c + 3] = kk.w;
-          sd = fmaf(qr[4 * c], kk.x, fmaf(qr[4 * c + 1], kk.y, fmaf(qr[4 * c + 2], kk.z, fmaf(qr[4 * c + 3], kk.w, sd))));
+          sp[0] = fmaf(qr[4 * c], kk.x, sp[0]);
+          sp[1] = fmaf(qr[4 * c + 1], kk.y, sp[1]);
+          sp[2] = fmaf(qr[4 * c + 2], kk.z, sp[2]);
+          sp[3] = fmaf(qr[4 * c + 3], kk.w, sp[3]);
           const float4 vv = Vs[jj][c];
-          dP = fmaf(zr[4 * c], vv.x, fmaf(zr[4 * c + 1], vv.y, fmaf(zr[4 * c + 2], vv.z, fmaf(zr[4 * c + 3], vv.w, dP))));
+          dp[0] = fmaf(zr[4 * c], vv.x, dp[0]);
+          dp[1] = fmaf(zr[4 * c + 1], vv.y, dp[1]);
+          dp[2] = fmaf(zr[4 * c + 2], vv.z, dp[2]);
+          dp[3] = fmaf(zr[4 * c + 3], vv.w, dp[3]);
         }
+        const float sd = (sp[0] + sp[1]) + (sp[2] + sp[3]);
+        const float dP = (dp[0] + dp[1]) + (dp[2] + dp[3]);
         const float E = expf(li - Ls[jj]);
         const float sp1 = ipow(sd, g.p - 1);
         rowD += dP * E * sp1 * sd;
@@ -1248,14 +1260,22 @@ __global__ void __launch_bounds__(64) k_intra_bwd_kv_r(Geo g, const T* __restric
     const int in = min(64, s1 - i0);
     for (int ii = 0; ii < in; ++ii) {
       if (act && i0 + ii >= j) {
-        float sd = 0.f, dP = Zd[ii];
+        float sp[4] = {0.f, 0.f, 0.f, 0.f}, dp[4] = {Zd[ii], 0.f, 0.f, 0.f};   // independent FMA chains
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const float4 qq = Qs[ii][c];
-          sd = fmaf(qq.x, kr[4 * c], fmaf(qq.y, kr[4 * c + 1], fmaf(qq.z, kr[4 * c + 2], fmaf(qq.w, kr[4 * c + 3], sd))));
+          sp[0] = fmaf(qq.x, kr[4 * c], sp[0]);
+          sp[1] = fmaf(qq.y, kr[4 * c + 1], sp[1]);
+          sp[2] = fmaf(qq.z, kr[4 * c + 2], sp[2]);
+          sp[3] = fmaf(qq.w, kr[4 * c + 3], sp[3]);
           const float4 zz = Zs[ii][c];
-          dP = fmaf(zz.x, vr[4 * c], fmaf(zz.y, vr[4 * c + 1], fmaf(zz.z, vr[4 * c + 2], fmaf(zz.w, vr[4 * c + 3], dP))));
+          dp[0] = fmaf(zz.x, vr[4 * c], dp[0]);
+          dp[1] = fmaf(zz.y, vr[4 * c + 1], dp[1]);
+          dp[2] = fmaf(zz.z, vr[4 * c + 2], dp[2]);
+          dp[3] = fmaf(zz.w, vr[4 * c + 3], dp[3]);
         }
+        const float sd = (sp[0] + sp[1]) + (sp[2] + sp[3]);
+        const float dP = (dp[0] + dp[1]) + (dp[2] + dp[3]);
         const float E = expf(Ls[ii] - lj);
         const float sp1 = ipow(sd, g.p - 1);
         const float P = E * sp1 * sd;
