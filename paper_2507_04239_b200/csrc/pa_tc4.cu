@@ -826,11 +826,19 @@ __global__ void __launch_bounds__(t4::VTHREADS) k_tc4_vjp(const __grid_constant_
             const float P3 = P2 * xc;
             const float g0 = __uint_as_float(r[4 * i]), g1 = __uint_as_float(r[4 * i + 1]);
             const float g2 = __uint_as_float(r[4 * i + 2]), g3 = __uint_as_float(r[4 * i + 3]);
-            const float T = fmaf(g0, xv[4 * be], fmaf(g1, xv[4 * be + 1], fmaf(g2, xv[4 * be + 2], g3 * xv[4 * be + 3])));
-            dxv[4 * be] = fmaf(g0, P3, dxv[4 * be]);
-            dxv[4 * be + 1] = fmaf(g1, P3, dxv[4 * be + 1]);
-            dxv[4 * be + 2] = fmaf(g2, P3, dxv[4 * be + 2]);
-            dxv[4 * be + 3] = fmaf(g3, P3, dxv[4 * be + 3]);
+            // packed fp32 pairs (FMUL2 / FFMA2): T = g . x_d, dx_d += g P3
+            using tc::f2v;
+            using tc::fma2v;
+            using tc::mul2v;
+            const f2v g01{g0, g1}, g23{g2, g3}, p33{P3, P3};
+            const f2v t2 = fma2v(g23, f2v{xv[4 * be + 2], xv[4 * be + 3]}, mul2v(g01, f2v{xv[4 * be], xv[4 * be + 1]}));
+            const float T = t2.x + t2.y;
+            const f2v d01 = fma2v(g01, p33, f2v{dxv[4 * be], dxv[4 * be + 1]});
+            const f2v d23 = fma2v(g23, p33, f2v{dxv[4 * be + 2], dxv[4 * be + 3]});
+            dxv[4 * be] = d01.x;
+            dxv[4 * be + 1] = d01.y;
+            dxv[4 * be + 2] = d23.x;
+            dxv[4 * be + 3] = d23.y;
             float* dc = (float*)((uint8_t*)dxrow + co);
             *dc = fmaf(T, P2, *dc);
             U = fmaf(T, xc, U);   // the run's dl share is P2 U (flush)
