@@ -1049,20 +1049,46 @@ __global__ void k_pub_discumsum(int n, int64_t L, int64_t M, const A* __restrict
 
 // --------------------------------------------------------------------------
 // d = e = 32 (configs[2]) variants of the three intra-chunk kernels above with
-// the same math and the same tiling: the thread's own rows live in registers
-// and the shared key / query rows are read as broadcast float4s (the generic
-// kernels re-read every operand as scalars from shared memory: ~160 loads per
-// (query, key) pair against ~100 FMAs).
+// the same math and tiling: two threads per row (lanes 2r, 2r + 1 each own 16
+// of the 32 dims, each dot product combined with one shuffle), the row's
+// operands in registers and the shared key / query rows read as broadcast
+// float4s (the generic kernels re-read every operand as scalars from shared
+// memory).  128 threads = 64 rows per CTA.
 // --------------------------------------------------------------------------
 template <typename T>
-__device__ __forceinline__ void load_row32(const T* src, float sc, float* dst) {
+__device__ __forceinline__ void load_half16(const T* src, float sc, float* dst) {
 #pragma unroll
-  for (int a = 0; a < 32; ++a) dst[a] = sc * to_f(src[a]);
+  for (int a = 0; a < 16; ++a) dst[a] = sc * to_f(src[a]);
 }
+// 64 rows x 32 values into float4 smem rows, two threads per row
 template <typename T>
-__global__ void __launch_bounds__(64) k_intra_fwd_r(Geo g, const T* __restrict__ q, const T* __restrict__ k,
-                                                    const T* __restrict__ v, const float* __restrict__ ell,
-                                                    float* yat) {
+__device__ __forceinline__ void stage_rows_h(float4 (*dst)[8], const T* base, const Geo& g, int s, int j0, int jend,
+                                             float sc) {
+  const int r = threadIdx.x >> 1, hf = threadIdx.x & 1, j = j0 + r;
+  const bool ok = j < jend;
+  float v[16];
+  if (ok) load_half16(base + rowid(g, s, j) * 32 + 16 * hf, sc, v);
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    dst[r][4 * hf + c] = ok ? make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
+}
+__device__ __forceinline__ float dot16(const float* x, const float4* y) {
+  float p[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const float4 v = y[c];
+    p[0] = fmaf(x[4 * c], v.x, p[0]);
+    p[1] = fmaf(x[4 * c + 1], v.y, p[1]);
+    p[2] = fmaf(x[4 * c + 2], v.z, p[2]);
+    p[3] = fmaf(x[4 * c + 3], v.w, p[3]);
+  }
+  return (p[0] + p[1]) + (p[2] + p[3]);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) k_intra_fwd_h(Geo g, const T* __restrict__ q, const T* __restrict__ k,
+                                                     const T* __restrict__ v, const float* __restrict__ ell,
+                                                     float* yat) {
   __shared__ float4 Ks[64][8], Vs[64][8];
   __shared__ float Ls[64];
   const int tpc = (g.c + 63) / 64;
@@ -1070,69 +1096,49 @@ __global__ void __launch_bounds__(64) k_intra_fwd_r(Geo g, const T* __restrict__
   const int s0 = kch * g.c, s1 = min(s0 + g.c, g.t);
   const int q0 = s0 + tile * 64;
   if (q0 >= s1) return;
-  const int i = q0 + threadIdx.x;
+  const int hf = threadIdx.x & 1, i = q0 + (threadIdx.x >> 1);
   const bool act = i < s1;
-  float qr[32], o[33];
-  if (act) load_row32(q + rowid(g, s, i) * 32, g.scale, qr);
-  else
+  float qr[16], o[16], rs = 0.f;
 #pragma unroll
-    for (int a = 0; a < 32; ++a) qr[a] = 0.f;
-#pragma unroll
-  for (int u = 0; u < 33; ++u) o[u] = 0.f;
+  for (int a = 0; a < 16; ++a) qr[a] = o[a] = 0.f;
+  if (act) load_half16(q + rowid(g, s, i) * 32 + 16 * hf, g.scale, qr);
   const float li = act ? ell[(size_t)s * g.t + i] : 0.f;
   const int jend = min(q0 + 64, s1);
   for (int j0 = s0; j0 < jend; j0 += 64) {
     __syncthreads();
-    {
-      const int j = j0 + threadIdx.x;
-      const bool ok = j < jend;
-      float r[32];
-      if (ok) load_row32(k + rowid(g, s, j) * 32, 1.f, r);
-#pragma unroll
-      for (int c = 0; c < 8; ++c) Ks[threadIdx.x][c] = ok ? make_float4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
-      if (ok) load_row32(v + rowid(g, s, j) * 32, 1.f, r);
-#pragma unroll
-      for (int c = 0; c < 8; ++c) Vs[threadIdx.x][c] = ok ? make_float4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
-      Ls[threadIdx.x] = ok ? ell[(size_t)s * g.t + j] : 0.f;
-    }
+    stage_rows_h(Ks, k, g, s, j0, jend, 1.f);
+    stage_rows_h(Vs, v, g, s, j0, jend, 1.f);
+    if (threadIdx.x < 64) Ls[threadIdx.x] = j0 + threadIdx.x < jend ? ell[(size_t)s * g.t + j0 + threadIdx.x] : 0.f;
     __syncthreads();
     const int jn = min(64, jend - j0);
     for (int jj = 0; jj < jn; ++jj) {
+      float sd = dot16(qr, &Ks[jj][4 * hf]);
+      sd += __shfl_xor_sync(0xffffffffu, sd, 1);
       if (act && j0 + jj <= i) {
-        float sp[4] = {0.f, 0.f, 0.f, 0.f};   // four independent FMA chains
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const float4 kk = Ks[jj][c];
-          sp[0] = fmaf(qr[4 * c], kk.x, sp[0]);
-          sp[1] = fmaf(qr[4 * c + 1], kk.y, sp[1]);
-          sp[2] = fmaf(qr[4 * c + 2], kk.z, sp[2]);
-          sp[3] = fmaf(qr[4 * c + 3], kk.w, sp[3]);
-        }
-        const float sd = (sp[0] + sp[1]) + (sp[2] + sp[3]);
         const float P = expf(li - Ls[jj]) * ipow(sd, g.p);
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const float4 vv = Vs[jj][c];
+        for (int c = 0; c < 4; ++c) {
+          const float4 vv = Vs[jj][4 * hf + c];
           o[4 * c] = fmaf(P, vv.x, o[4 * c]);
           o[4 * c + 1] = fmaf(P, vv.y, o[4 * c + 1]);
           o[4 * c + 2] = fmaf(P, vv.z, o[4 * c + 2]);
           o[4 * c + 3] = fmaf(P, vv.w, o[4 * c + 3]);
         }
-        o[32] += P;
+        rs += P;
       }
     }
   }
   if (!act) return;
-  float4* out = (float4*)(yat + ((size_t)s * g.t + i) * 33);   // 132-byte rows: scalar stores
-  float* of = (float*)out;
+  float* out = yat + ((size_t)s * g.t + i) * 33 + 16 * hf;
 #pragma unroll
-  for (int u = 0; u < 33; ++u) of[u] = o[u];
+  for (int u = 0; u < 16; ++u) out[u] = o[u];
+  if (hf) out[16] = rs;
 }
 
 template <typename T>
-__global__ void __launch_bounds__(64) k_intra_bwd_q_r(Geo g, const T* __restrict__ q, const T* __restrict__ k,
-                                                      const T* __restrict__ v, const float* __restrict__ ell,
-                                                      const float* __restrict__ dz, float* dq32, float* dell) {
+__global__ void __launch_bounds__(128) k_intra_bwd_q_h(Geo g, const T* __restrict__ q, const T* __restrict__ k,
+                                                       const T* __restrict__ v, const float* __restrict__ ell,
+                                                       const float* __restrict__ dz, float* dq32, float* dell) {
   __shared__ float4 Ks[64][8], Vs[64][8];
   __shared__ float Ls[64];
   const int tpc = (g.c + 63) / 64;
@@ -1140,85 +1146,61 @@ __global__ void __launch_bounds__(64) k_intra_bwd_q_r(Geo g, const T* __restrict
   const int s0 = kch * g.c, s1 = min(s0 + g.c, g.t);
   const int q0 = s0 + tile * 64;
   if (q0 >= s1) return;
-  const int i = q0 + threadIdx.x;
+  const int hf = threadIdx.x & 1, i = q0 + (threadIdx.x >> 1);
   const bool act = i < s1;
-  float qr[32], zr[33], dqa[32];
+  float qr[16], zr[16], dqa[16], zd = 0.f;
 #pragma unroll
-  for (int a = 0; a < 32; ++a) {
-    qr[a] = 0.f;
-    zr[a] = 0.f;
-    dqa[a] = 0.f;
-  }
-  zr[32] = 0.f;
+  for (int a = 0; a < 16; ++a) qr[a] = zr[a] = dqa[a] = 0.f;
   if (act) {
-    load_row32(q + rowid(g, s, i) * 32, g.scale, qr);
+    load_half16(q + rowid(g, s, i) * 32 + 16 * hf, g.scale, qr);
     const float* zp = dz + ((size_t)s * g.t + i) * 33;
 #pragma unroll
-    for (int u = 0; u < 33; ++u) zr[u] = zp[u];
+    for (int u = 0; u < 16; ++u) zr[u] = zp[16 * hf + u];
+    if (!hf) zd = zp[32];   // dden, added once per pair
   }
   float rowD = 0.f;
   const float li = act ? ell[(size_t)s * g.t + i] : 0.f;
   const int jend = min(q0 + 64, s1);
   for (int j0 = s0; j0 < jend; j0 += 64) {
     __syncthreads();
-    {
-      const int j = j0 + threadIdx.x;
-      const bool ok = j < jend;
-      float r[32];
-      if (ok) load_row32(k + rowid(g, s, j) * 32, 1.f, r);
-#pragma unroll
-      for (int c = 0; c < 8; ++c) Ks[threadIdx.x][c] = ok ? make_float4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
-      if (ok) load_row32(v + rowid(g, s, j) * 32, 1.f, r);
-#pragma unroll
-      for (int c = 0; c < 8; ++c) Vs[threadIdx.x][c] = ok ? make_float4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
-      Ls[threadIdx.x] = ok ? ell[(size_t)s * g.t + j] : 0.f;
-    }
+    stage_rows_h(Ks, k, g, s, j0, jend, 1.f);
+    stage_rows_h(Vs, v, g, s, j0, jend, 1.f);
+    if (threadIdx.x < 64) Ls[threadIdx.x] = j0 + threadIdx.x < jend ? ell[(size_t)s * g.t + j0 + threadIdx.x] : 0.f;
     __syncthreads();
     const int jn = min(64, jend - j0);
     for (int jj = 0; jj < jn; ++jj) {
+      float sd = dot16(qr, &Ks[jj][4 * hf]);
+      float dP = zd + dot16(zr, &Vs[jj][4 * hf]);
+      sd += __shfl_xor_sync(0xffffffffu, sd, 1);
+      dP += __shfl_xor_sync(0xffffffffu, dP, 1);
       if (act && j0 + jj <= i) {
-        float kr[32];
-        float sp[4] = {0.f, 0.f, 0.f, 0.f}, dp[4] = {zr[32], 0.f, 0.f, 0.f};   // independent FMA chains
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const float4 kk = Ks[jj][c];
-          kr[4 * c] = kk.x;
-          kr[4 * c + 1] = kk.y;
-          kr[4 * c + 2] = kk.z;
-          kr[4 * c + 3] = kk.w;
-          sp[0] = fmaf(qr[4 * c], kk.x, sp[0]);
-          sp[1] = fmaf(qr[4 * c + 1], kk.y, sp[1]);
-          sp[2] = fmaf(qr[4 * c + 2], kk.z, sp[2]);
-          sp[3] = fmaf(qr[4 * c + 3], kk.w, sp[3]);
-          const float4 vv = Vs[jj][c];
-          dp[0] = fmaf(zr[4 * c], vv.x, dp[0]);
-          dp[1] = fmaf(zr[4 * c + 1], vv.y, dp[1]);
-          dp[2] = fmaf(zr[4 * c + 2], vv.z, dp[2]);
-          dp[3] = fmaf(zr[4 * c + 3], vv.w, dp[3]);
-        }
-        const float sd = (sp[0] + sp[1]) + (sp[2] + sp[3]);
-        const float dP = (dp[0] + dp[1]) + (dp[2] + dp[3]);
         const float E = expf(li - Ls[jj]);
         const float sp1 = ipow(sd, g.p - 1);
         rowD += dP * E * sp1 * sd;
         const float ds = dP * E * g.p * sp1;
 #pragma unroll
-        for (int a = 0; a < 32; ++a) dqa[a] = fmaf(ds, kr[a], dqa[a]);
+        for (int c = 0; c < 4; ++c) {
+          const float4 kk = Ks[jj][4 * hf + c];
+          dqa[4 * c] = fmaf(ds, kk.x, dqa[4 * c]);
+          dqa[4 * c + 1] = fmaf(ds, kk.y, dqa[4 * c + 1]);
+          dqa[4 * c + 2] = fmaf(ds, kk.z, dqa[4 * c + 2]);
+          dqa[4 * c + 3] = fmaf(ds, kk.w, dqa[4 * c + 3]);
+        }
       }
     }
   }
   if (!act) return;
-  float* o = dq32 + ((size_t)s * g.t + i) * 32;
+  float* o = dq32 + ((size_t)s * g.t + i) * 32 + 16 * hf;
 #pragma unroll
-  for (int a = 0; a < 32; ++a) o[a] += g.scale * dqa[a];
-  dell[(size_t)s * g.t + i] += rowD;
+  for (int a = 0; a < 16; ++a) o[a] += g.scale * dqa[a];
+  if (!hf) dell[(size_t)s * g.t + i] += rowD;
 }
 
 template <typename T>
-__global__ void __launch_bounds__(64) k_intra_bwd_kv_r(Geo g, const T* __restrict__ q, const T* __restrict__ k,
-                                                       const T* __restrict__ v, const float* __restrict__ ell,
-                                                       const float* __restrict__ dz, float* dk32, float* dv32,
-                                                       float* dell) {
+__global__ void __launch_bounds__(128) k_intra_bwd_kv_h(Geo g, const T* __restrict__ q, const T* __restrict__ k,
+                                                        const T* __restrict__ v, const float* __restrict__ ell,
+                                                        const float* __restrict__ dz, float* dk32, float* dv32,
+                                                        float* dell) {
   __shared__ float4 Qs[64][8], Zs[64][8];
   __shared__ float Zd[64], Ls[64];
   const int tpc = (g.c + 63) / 64;
@@ -1226,69 +1208,51 @@ __global__ void __launch_bounds__(64) k_intra_bwd_kv_r(Geo g, const T* __restric
   const int s0 = kch * g.c, s1 = min(s0 + g.c, g.t);
   const int k0 = s0 + tile * 64;
   if (k0 >= s1) return;
-  const int j = k0 + threadIdx.x;
+  const int hf = threadIdx.x & 1, j = k0 + (threadIdx.x >> 1);
   const bool act = j < s1;
-  float kr[32], vr[32], dka[32], dva[32];
+  float kr[16], vr[16], dka[16], dva[16];
 #pragma unroll
-  for (int a = 0; a < 32; ++a) {
-    kr[a] = vr[a] = 0.f;
-    dka[a] = dva[a] = 0.f;
-  }
+  for (int a = 0; a < 16; ++a) kr[a] = vr[a] = dka[a] = dva[a] = 0.f;
   if (act) {
-    load_row32(k + rowid(g, s, j) * 32, 1.f, kr);
-    load_row32(v + rowid(g, s, j) * 32, 1.f, vr);
+    load_half16(k + rowid(g, s, j) * 32 + 16 * hf, 1.f, kr);
+    load_half16(v + rowid(g, s, j) * 32 + 16 * hf, 1.f, vr);
   }
   float colD = 0.f;
   const float lj = act ? ell[(size_t)s * g.t + j] : 0.f;
   for (int i0 = k0; i0 < s1; i0 += 64) {
     __syncthreads();
+    stage_rows_h(Qs, q, g, s, i0, s1, g.scale);
     {
-      const int i = i0 + threadIdx.x;
+      const int r = threadIdx.x >> 1, i = i0 + r;
       const bool ok = i < s1;
-      float r[32];
-      if (ok) load_row32(q + rowid(g, s, i) * 32, g.scale, r);
+      const float* zp = dz + ((size_t)s * g.t + (ok ? i : 0)) * 33 + 16 * hf;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) Qs[threadIdx.x][c] = ok ? make_float4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
-      const float* zp = dz + ((size_t)s * g.t + i) * 33;
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        Zs[threadIdx.x][c] = ok ? make_float4(zp[4 * c], zp[4 * c + 1], zp[4 * c + 2], zp[4 * c + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
-      Zd[threadIdx.x] = ok ? zp[32] : 0.f;
-      Ls[threadIdx.x] = ok ? ell[(size_t)s * g.t + i] : 0.f;
+      for (int c = 0; c < 4; ++c)
+        Zs[r][4 * hf + c] = ok ? make_float4(zp[4 * c], zp[4 * c + 1], zp[4 * c + 2], zp[4 * c + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (!hf) Zd[r] = ok ? zp[32] : 0.f;
+      if (hf) Ls[r] = ok ? ell[(size_t)s * g.t + i] : 0.f;
     }
     __syncthreads();
     const int in = min(64, s1 - i0);
     for (int ii = 0; ii < in; ++ii) {
+      float sd = dot16(kr, &Qs[ii][4 * hf]);
+      float dP = (hf ? 0.f : Zd[ii]) + dot16(vr, &Zs[ii][4 * hf]);
+      sd += __shfl_xor_sync(0xffffffffu, sd, 1);
+      dP += __shfl_xor_sync(0xffffffffu, dP, 1);
       if (act && i0 + ii >= j) {
-        float sp[4] = {0.f, 0.f, 0.f, 0.f}, dp[4] = {Zd[ii], 0.f, 0.f, 0.f};   // independent FMA chains
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const float4 qq = Qs[ii][c];
-          sp[0] = fmaf(qq.x, kr[4 * c], sp[0]);
-          sp[1] = fmaf(qq.y, kr[4 * c + 1], sp[1]);
-          sp[2] = fmaf(qq.z, kr[4 * c + 2], sp[2]);
-          sp[3] = fmaf(qq.w, kr[4 * c + 3], sp[3]);
-          const float4 zz = Zs[ii][c];
-          dp[0] = fmaf(zz.x, vr[4 * c], dp[0]);
-          dp[1] = fmaf(zz.y, vr[4 * c + 1], dp[1]);
-          dp[2] = fmaf(zz.z, vr[4 * c + 2], dp[2]);
-          dp[3] = fmaf(zz.w, vr[4 * c + 3], dp[3]);
-        }
-        const float sd = (sp[0] + sp[1]) + (sp[2] + sp[3]);
-        const float dP = (dp[0] + dp[1]) + (dp[2] + dp[3]);
         const float E = expf(Ls[ii] - lj);
         const float sp1 = ipow(sd, g.p - 1);
         const float P = E * sp1 * sd;
         colD += dP * P;
         const float ds = dP * E * g.p * sp1;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const float4 qq = Qs[ii][c];
+        for (int c = 0; c < 4; ++c) {
+          const float4 qq = Qs[ii][4 * hf + c];
           dka[4 * c] = fmaf(ds, qq.x, dka[4 * c]);
           dka[4 * c + 1] = fmaf(ds, qq.y, dka[4 * c + 1]);
           dka[4 * c + 2] = fmaf(ds, qq.z, dka[4 * c + 2]);
           dka[4 * c + 3] = fmaf(ds, qq.w, dka[4 * c + 3]);
-          const float4 zz = Zs[ii][c];
+          const float4 zz = Zs[ii][4 * hf + c];
           dva[4 * c] = fmaf(P, zz.x, dva[4 * c]);
           dva[4 * c + 1] = fmaf(P, zz.y, dva[4 * c + 1]);
           dva[4 * c + 2] = fmaf(P, zz.z, dva[4 * c + 2]);
@@ -1298,14 +1262,14 @@ __global__ void __launch_bounds__(64) k_intra_bwd_kv_r(Geo g, const T* __restric
     }
   }
   if (!act) return;
-  float* ok_ = dk32 + ((size_t)s * g.t + j) * 32;
-  float* ov = dv32 + ((size_t)s * g.t + j) * 32;
+  float* ok_ = dk32 + ((size_t)s * g.t + j) * 32 + 16 * hf;
+  float* ov = dv32 + ((size_t)s * g.t + j) * 32 + 16 * hf;
 #pragma unroll
-  for (int a = 0; a < 32; ++a) {
+  for (int a = 0; a < 16; ++a) {
     ok_[a] += dka[a];
     ov[a] += dva[a];
   }
-  dell[(size_t)s * g.t + j] -= colD;
+  if (!hf) dell[(size_t)s * g.t + j] -= colD;
 }
 
 // dynamic shared memory per block for the kernels above (floats -> bytes)
@@ -1335,7 +1299,7 @@ static int simt_forward_t(const Geo& g, const T* q, const T* k, const T* v, cons
   const int tpc = (g.c + 63) / 64;
   k_gate_prep<<<(g.ns * g.n + 127) / 128, 128, 0, st>>>(g, log_g, w.ell, w.lamlog);
   if (DM == 32 && g.d == 32 && g.e == 32)
-    k_intra_fwd_r<T><<<dim3(g.n * tpc, g.ns), 64, 0, st>>>(g, q, k, v, w.ell, w.yat);
+    k_intra_fwd_h<T><<<dim3(g.n * tpc, g.ns), 128, 0, st>>>(g, q, k, v, w.ell, w.yat);
   else
     k_intra_fwd<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_intra_fwd<T, DM>, smb_intra_fwd<DM>()), st>>>(g, q, k, v, w.ell, w.yat);
   if (tc4_supported(g, g.dtype)) {
@@ -1416,8 +1380,8 @@ static int simt_backward_t(const Geo& g, const T* q, const T* k, const T* v, con
   ++launches;
   }
   if (DM == 32 && g.d == 32 && g.e == 32) {
-    k_intra_bwd_q_r<T><<<dim3(g.n * tpc, g.ns), 64, 0, st>>>(g, q, k, v, w.ell, b.dz, b.dq32, b.dell);
-    k_intra_bwd_kv_r<T><<<dim3(g.n * tpc, g.ns), 64, 0, st>>>(g, q, k, v, w.ell, b.dz, b.dk32, b.dv32, b.dell);
+    k_intra_bwd_q_h<T><<<dim3(g.n * tpc, g.ns), 128, 0, st>>>(g, q, k, v, w.ell, b.dz, b.dq32, b.dell);
+    k_intra_bwd_kv_h<T><<<dim3(g.n * tpc, g.ns), 128, 0, st>>>(g, q, k, v, w.ell, b.dz, b.dk32, b.dv32, b.dell);
   } else {
     k_intra_bwd_q<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_intra_bwd_q<T, DM>, smb_intra_bwd<DM>()), st>>>(g, q, k, v, w.ell, b.dz, b.dq32, b.dell);
     k_intra_bwd_kv<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_intra_bwd_kv<T, DM>, smb_intra_bwd<DM>()), st>>>(g, q, k, v, w.ell, b.dz, b.dk32, b.dv32, b.dell);
