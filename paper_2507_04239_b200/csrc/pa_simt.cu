@@ -1049,33 +1049,35 @@ __global__ void k_pub_discumsum(int n, int64_t L, int64_t M, const A* __restrict
 
 // --------------------------------------------------------------------------
 // d = e = 32 (configs[2]) variants of the three intra-chunk kernels above with
-// the same math and tiling: two threads per row (lanes 2r, 2r + 1 each own 16
-// of the 32 dims, each dot product combined with one shuffle), the row's
+// the same math and tiling: TPR threads per row (each owns 32 / TPR of the dims,
+// each dot product combined with log2(TPR) shuffles), the row's
 // operands in registers and the shared key / query rows read as broadcast
 // float4s (the generic kernels re-read every operand as scalars from shared
-// memory).  128 threads = 64 rows per CTA.
+// memory).  64 x TPR threads = 64 rows per CTA.
 // --------------------------------------------------------------------------
-template <typename T>
-__device__ __forceinline__ void load_half16(const T* src, float sc, float* dst) {
+template <int N, typename T>
+__device__ __forceinline__ void load_part(const T* src, float sc, float* dst) {
 #pragma unroll
-  for (int a = 0; a < 16; ++a) dst[a] = sc * to_f(src[a]);
+  for (int a = 0; a < N; ++a) dst[a] = sc * to_f(src[a]);
 }
-// 64 rows x 32 values into float4 smem rows, two threads per row
-template <typename T>
-__device__ __forceinline__ void stage_rows_h(float4 (*dst)[8], const T* base, const Geo& g, int s, int j0, int jend,
+// 64 rows x 32 values into float4 smem rows, TPR threads per row
+template <int TPR, typename T>
+__device__ __forceinline__ void stage_rows_p(float4 (*dst)[8], const T* base, const Geo& g, int s, int j0, int jend,
                                              float sc) {
-  const int r = threadIdx.x >> 1, hf = threadIdx.x & 1, j = j0 + r;
+  constexpr int DP = 32 / TPR;
+  const int r = threadIdx.x / TPR, hf = threadIdx.x % TPR, j = j0 + r;
   const bool ok = j < jend;
-  float v[16];
-  if (ok) load_half16(base + rowid(g, s, j) * 32 + 16 * hf, sc, v);
+  float v[DP];
+  if (ok) load_part<DP>(base + rowid(g, s, j) * 32 + DP * hf, sc, v);
 #pragma unroll
-  for (int c = 0; c < 4; ++c)
-    dst[r][4 * hf + c] = ok ? make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int c = 0; c < DP / 4; ++c)
+    dst[r][(DP / 4) * hf + c] = ok ? make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
 }
-__device__ __forceinline__ float dot16(const float* x, const float4* y) {
+template <int DP>
+__device__ __forceinline__ float dot_part(const float* x, const float4* y) {
   float p[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
+  for (int c = 0; c < DP / 4; ++c) {
     const float4 v = y[c];
     p[0] = fmaf(x[4 * c], v.x, p[0]);
     p[1] = fmaf(x[4 * c + 1], v.y, p[1]);
@@ -1084,11 +1086,29 @@ __device__ __forceinline__ float dot16(const float* x, const float4* y) {
   }
   return (p[0] + p[1]) + (p[2] + p[3]);
 }
+template <int TPR>
+__device__ __forceinline__ float row_sum(float v) {
+#pragma unroll
+  for (int o = 1; o < TPR; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <int DP>
+__device__ __forceinline__ void axpy_part(float a, const float4* y, float* acc) {
+#pragma unroll
+  for (int c = 0; c < DP / 4; ++c) {
+    const float4 v = y[c];
+    acc[4 * c] = fmaf(a, v.x, acc[4 * c]);
+    acc[4 * c + 1] = fmaf(a, v.y, acc[4 * c + 1]);
+    acc[4 * c + 2] = fmaf(a, v.z, acc[4 * c + 2]);
+    acc[4 * c + 3] = fmaf(a, v.w, acc[4 * c + 3]);
+  }
+}
 
-template <typename T>
-__global__ void __launch_bounds__(128) k_intra_fwd_h(Geo g, const T* __restrict__ q, const T* __restrict__ k,
-                                                     const T* __restrict__ v, const float* __restrict__ ell,
-                                                     float* yat) {
+template <typename T, int TPR>
+__global__ void __launch_bounds__(64 * TPR) k_intra_fwd_h(Geo g, const T* __restrict__ q, const T* __restrict__ k,
+                                                          const T* __restrict__ v, const float* __restrict__ ell,
+                                                          float* yat) {
+  constexpr int DP = 32 / TPR;
   __shared__ float4 Ks[64][8], Vs[64][8];
   __shared__ float Ls[64];
   const int tpc = (g.c + 63) / 64;
@@ -1096,49 +1116,42 @@ __global__ void __launch_bounds__(128) k_intra_fwd_h(Geo g, const T* __restrict_
   const int s0 = kch * g.c, s1 = min(s0 + g.c, g.t);
   const int q0 = s0 + tile * 64;
   if (q0 >= s1) return;
-  const int hf = threadIdx.x & 1, i = q0 + (threadIdx.x >> 1);
+  const int hf = threadIdx.x % TPR, i = q0 + threadIdx.x / TPR;
   const bool act = i < s1;
-  float qr[16], o[16], rs = 0.f;
+  float qr[DP], o[DP], rs = 0.f;
 #pragma unroll
-  for (int a = 0; a < 16; ++a) qr[a] = o[a] = 0.f;
-  if (act) load_half16(q + rowid(g, s, i) * 32 + 16 * hf, g.scale, qr);
+  for (int a = 0; a < DP; ++a) qr[a] = o[a] = 0.f;
+  if (act) load_part<DP>(q + rowid(g, s, i) * 32 + DP * hf, g.scale, qr);
   const float li = act ? ell[(size_t)s * g.t + i] : 0.f;
   const int jend = min(q0 + 64, s1);
   for (int j0 = s0; j0 < jend; j0 += 64) {
     __syncthreads();
-    stage_rows_h(Ks, k, g, s, j0, jend, 1.f);
-    stage_rows_h(Vs, v, g, s, j0, jend, 1.f);
+    stage_rows_p<TPR>(Ks, k, g, s, j0, jend, 1.f);
+    stage_rows_p<TPR>(Vs, v, g, s, j0, jend, 1.f);
     if (threadIdx.x < 64) Ls[threadIdx.x] = j0 + threadIdx.x < jend ? ell[(size_t)s * g.t + j0 + threadIdx.x] : 0.f;
     __syncthreads();
     const int jn = min(64, jend - j0);
     for (int jj = 0; jj < jn; ++jj) {
-      float sd = dot16(qr, &Ks[jj][4 * hf]);
-      sd += __shfl_xor_sync(0xffffffffu, sd, 1);
+      const float sd = row_sum<TPR>(dot_part<DP>(qr, &Ks[jj][(DP / 4) * hf]));
       if (act && j0 + jj <= i) {
         const float P = expf(li - Ls[jj]) * ipow(sd, g.p);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const float4 vv = Vs[jj][4 * hf + c];
-          o[4 * c] = fmaf(P, vv.x, o[4 * c]);
-          o[4 * c + 1] = fmaf(P, vv.y, o[4 * c + 1]);
-          o[4 * c + 2] = fmaf(P, vv.z, o[4 * c + 2]);
-          o[4 * c + 3] = fmaf(P, vv.w, o[4 * c + 3]);
-        }
+        axpy_part<DP>(P, &Vs[jj][(DP / 4) * hf], o);
         rs += P;
       }
     }
   }
   if (!act) return;
-  float* out = yat + ((size_t)s * g.t + i) * 33 + 16 * hf;
+  float* out = yat + ((size_t)s * g.t + i) * 33 + DP * hf;
 #pragma unroll
-  for (int u = 0; u < 16; ++u) out[u] = o[u];
-  if (hf) out[16] = rs;
+  for (int u = 0; u < DP; ++u) out[u] = o[u];
+  if (hf == TPR - 1) out[DP] = rs;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(128) k_intra_bwd_q_h(Geo g, const T* __restrict__ q, const T* __restrict__ k,
-                                                       const T* __restrict__ v, const float* __restrict__ ell,
-                                                       const float* __restrict__ dz, float* dq32, float* dell) {
+template <typename T, int TPR>
+__global__ void __launch_bounds__(64 * TPR) k_intra_bwd_q_h(Geo g, const T* __restrict__ q, const T* __restrict__ k,
+                                                            const T* __restrict__ v, const float* __restrict__ ell,
+                                                            const float* __restrict__ dz, float* dq32, float* dell) {
+  constexpr int DP = 32 / TPR;
   __shared__ float4 Ks[64][8], Vs[64][8];
   __shared__ float Ls[64];
   const int tpc = (g.c + 63) / 64;
@@ -1146,16 +1159,16 @@ __global__ void __launch_bounds__(128) k_intra_bwd_q_h(Geo g, const T* __restric
   const int s0 = kch * g.c, s1 = min(s0 + g.c, g.t);
   const int q0 = s0 + tile * 64;
   if (q0 >= s1) return;
-  const int hf = threadIdx.x & 1, i = q0 + (threadIdx.x >> 1);
+  const int hf = threadIdx.x % TPR, i = q0 + threadIdx.x / TPR;
   const bool act = i < s1;
-  float qr[16], zr[16], dqa[16], zd = 0.f;
+  float qr[DP], zr[DP], dqa[DP], zd = 0.f;
 #pragma unroll
-  for (int a = 0; a < 16; ++a) qr[a] = zr[a] = dqa[a] = 0.f;
+  for (int a = 0; a < DP; ++a) qr[a] = zr[a] = dqa[a] = 0.f;
   if (act) {
-    load_half16(q + rowid(g, s, i) * 32 + 16 * hf, g.scale, qr);
+    load_part<DP>(q + rowid(g, s, i) * 32 + DP * hf, g.scale, qr);
     const float* zp = dz + ((size_t)s * g.t + i) * 33;
 #pragma unroll
-    for (int u = 0; u < 16; ++u) zr[u] = zp[16 * hf + u];
+    for (int u = 0; u < DP; ++u) zr[u] = zp[DP * hf + u];
     if (!hf) zd = zp[32];   // dden, added once per pair
   }
   float rowD = 0.f;
@@ -1163,44 +1176,35 @@ __global__ void __launch_bounds__(128) k_intra_bwd_q_h(Geo g, const T* __restric
   const int jend = min(q0 + 64, s1);
   for (int j0 = s0; j0 < jend; j0 += 64) {
     __syncthreads();
-    stage_rows_h(Ks, k, g, s, j0, jend, 1.f);
-    stage_rows_h(Vs, v, g, s, j0, jend, 1.f);
+    stage_rows_p<TPR>(Ks, k, g, s, j0, jend, 1.f);
+    stage_rows_p<TPR>(Vs, v, g, s, j0, jend, 1.f);
     if (threadIdx.x < 64) Ls[threadIdx.x] = j0 + threadIdx.x < jend ? ell[(size_t)s * g.t + j0 + threadIdx.x] : 0.f;
     __syncthreads();
     const int jn = min(64, jend - j0);
     for (int jj = 0; jj < jn; ++jj) {
-      float sd = dot16(qr, &Ks[jj][4 * hf]);
-      float dP = zd + dot16(zr, &Vs[jj][4 * hf]);
-      sd += __shfl_xor_sync(0xffffffffu, sd, 1);
-      dP += __shfl_xor_sync(0xffffffffu, dP, 1);
+      const float sd = row_sum<TPR>(dot_part<DP>(qr, &Ks[jj][(DP / 4) * hf]));
+      const float dP = row_sum<TPR>(zd + dot_part<DP>(zr, &Vs[jj][(DP / 4) * hf]));
       if (act && j0 + jj <= i) {
         const float E = expf(li - Ls[jj]);
         const float sp1 = ipow(sd, g.p - 1);
         rowD += dP * E * sp1 * sd;
-        const float ds = dP * E * g.p * sp1;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const float4 kk = Ks[jj][4 * hf + c];
-          dqa[4 * c] = fmaf(ds, kk.x, dqa[4 * c]);
-          dqa[4 * c + 1] = fmaf(ds, kk.y, dqa[4 * c + 1]);
-          dqa[4 * c + 2] = fmaf(ds, kk.z, dqa[4 * c + 2]);
-          dqa[4 * c + 3] = fmaf(ds, kk.w, dqa[4 * c + 3]);
-        }
+        axpy_part<DP>(dP * E * g.p * sp1, &Ks[jj][(DP / 4) * hf], dqa);
       }
     }
   }
   if (!act) return;
-  float* o = dq32 + ((size_t)s * g.t + i) * 32 + 16 * hf;
+  float* o = dq32 + ((size_t)s * g.t + i) * 32 + DP * hf;
 #pragma unroll
-  for (int a = 0; a < 16; ++a) o[a] += g.scale * dqa[a];
+  for (int a = 0; a < DP; ++a) o[a] += g.scale * dqa[a];
   if (!hf) dell[(size_t)s * g.t + i] += rowD;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(128) k_intra_bwd_kv_h(Geo g, const T* __restrict__ q, const T* __restrict__ k,
-                                                        const T* __restrict__ v, const float* __restrict__ ell,
-                                                        const float* __restrict__ dz, float* dk32, float* dv32,
-                                                        float* dell) {
+template <typename T, int TPR>
+__global__ void __launch_bounds__(64 * TPR) k_intra_bwd_kv_h(Geo g, const T* __restrict__ q, const T* __restrict__ k,
+                                                             const T* __restrict__ v, const float* __restrict__ ell,
+                                                             const float* __restrict__ dz, float* dk32, float* dv32,
+                                                             float* dell) {
+  constexpr int DP = 32 / TPR;
   __shared__ float4 Qs[64][8], Zs[64][8];
   __shared__ float Zd[64], Ls[64];
   const int tpc = (g.c + 63) / 64;
@@ -1208,69 +1212,57 @@ __global__ void __launch_bounds__(128) k_intra_bwd_kv_h(Geo g, const T* __restri
   const int s0 = kch * g.c, s1 = min(s0 + g.c, g.t);
   const int k0 = s0 + tile * 64;
   if (k0 >= s1) return;
-  const int hf = threadIdx.x & 1, j = k0 + (threadIdx.x >> 1);
+  const int hf = threadIdx.x % TPR, j = k0 + threadIdx.x / TPR;
   const bool act = j < s1;
-  float kr[16], vr[16], dka[16], dva[16];
+  float kr[DP], vr[DP], dka[DP], dva[DP];
 #pragma unroll
-  for (int a = 0; a < 16; ++a) kr[a] = vr[a] = dka[a] = dva[a] = 0.f;
+  for (int a = 0; a < DP; ++a) kr[a] = vr[a] = dka[a] = dva[a] = 0.f;
   if (act) {
-    load_half16(k + rowid(g, s, j) * 32 + 16 * hf, 1.f, kr);
-    load_half16(v + rowid(g, s, j) * 32 + 16 * hf, 1.f, vr);
+    load_part<DP>(k + rowid(g, s, j) * 32 + DP * hf, 1.f, kr);
+    load_part<DP>(v + rowid(g, s, j) * 32 + DP * hf, 1.f, vr);
   }
   float colD = 0.f;
   const float lj = act ? ell[(size_t)s * g.t + j] : 0.f;
   for (int i0 = k0; i0 < s1; i0 += 64) {
     __syncthreads();
-    stage_rows_h(Qs, q, g, s, i0, s1, g.scale);
+    stage_rows_p<TPR>(Qs, q, g, s, i0, s1, g.scale);
     {
-      const int r = threadIdx.x >> 1, i = i0 + r;
+      const int r = threadIdx.x / TPR, i = i0 + r;
       const bool ok = i < s1;
-      const float* zp = dz + ((size_t)s * g.t + (ok ? i : 0)) * 33 + 16 * hf;
+      const float* zp = dz + ((size_t)s * g.t + (ok ? i : 0)) * 33 + DP * hf;
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-        Zs[r][4 * hf + c] = ok ? make_float4(zp[4 * c], zp[4 * c + 1], zp[4 * c + 2], zp[4 * c + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
-      if (!hf) Zd[r] = ok ? zp[32] : 0.f;
-      if (hf) Ls[r] = ok ? ell[(size_t)s * g.t + i] : 0.f;
+      for (int c = 0; c < DP / 4; ++c)
+        Zs[r][(DP / 4) * hf + c] = ok ? make_float4(zp[4 * c], zp[4 * c + 1], zp[4 * c + 2], zp[4 * c + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (hf == 0) Zd[r] = ok ? zp[32] : 0.f;
+      if (hf == TPR - 1) Ls[r] = ok ? ell[(size_t)s * g.t + i] : 0.f;
     }
     __syncthreads();
     const int in = min(64, s1 - i0);
     for (int ii = 0; ii < in; ++ii) {
-      float sd = dot16(kr, &Qs[ii][4 * hf]);
-      float dP = (hf ? 0.f : Zd[ii]) + dot16(vr, &Zs[ii][4 * hf]);
-      sd += __shfl_xor_sync(0xffffffffu, sd, 1);
-      dP += __shfl_xor_sync(0xffffffffu, dP, 1);
+      const float sd = row_sum<TPR>(dot_part<DP>(kr, &Qs[ii][(DP / 4) * hf]));
+      const float dP = row_sum<TPR>((hf ? 0.f : Zd[ii]) + dot_part<DP>(vr, &Zs[ii][(DP / 4) * hf]));
       if (act && i0 + ii >= j) {
         const float E = expf(Ls[ii] - lj);
         const float sp1 = ipow(sd, g.p - 1);
         const float P = E * sp1 * sd;
         colD += dP * P;
-        const float ds = dP * E * g.p * sp1;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const float4 qq = Qs[ii][4 * hf + c];
-          dka[4 * c] = fmaf(ds, qq.x, dka[4 * c]);
-          dka[4 * c + 1] = fmaf(ds, qq.y, dka[4 * c + 1]);
-          dka[4 * c + 2] = fmaf(ds, qq.z, dka[4 * c + 2]);
-          dka[4 * c + 3] = fmaf(ds, qq.w, dka[4 * c + 3]);
-          const float4 zz = Zs[ii][4 * hf + c];
-          dva[4 * c] = fmaf(P, zz.x, dva[4 * c]);
-          dva[4 * c + 1] = fmaf(P, zz.y, dva[4 * c + 1]);
-          dva[4 * c + 2] = fmaf(P, zz.z, dva[4 * c + 2]);
-          dva[4 * c + 3] = fmaf(P, zz.w, dva[4 * c + 3]);
-        }
+        axpy_part<DP>(dP * E * g.p * sp1, &Qs[ii][(DP / 4) * hf], dka);
+        axpy_part<DP>(P, &Zs[ii][(DP / 4) * hf], dva);
       }
     }
   }
   if (!act) return;
-  float* ok_ = dk32 + ((size_t)s * g.t + j) * 32 + 16 * hf;
-  float* ov = dv32 + ((size_t)s * g.t + j) * 32 + 16 * hf;
+  float* ok_ = dk32 + ((size_t)s * g.t + j) * 32 + DP * hf;
+  float* ov = dv32 + ((size_t)s * g.t + j) * 32 + DP * hf;
 #pragma unroll
-  for (int a = 0; a < 16; ++a) {
+  for (int a = 0; a < DP; ++a) {
     ok_[a] += dka[a];
     ov[a] += dva[a];
   }
   if (!hf) dell[(size_t)s * g.t + j] -= colD;
 }
+
+constexpr int kIntraTpr = 2;   // threads per row of the d = 32 intra-chunk kernels (4 measured slower)
 
 // dynamic shared memory per block for the kernels above (floats -> bytes)
 template <int DM> constexpr size_t smb_intra_fwd() { return 4 * (2 * 64 * (DM + 1)); }
@@ -1299,7 +1291,7 @@ static int simt_forward_t(const Geo& g, const T* q, const T* k, const T* v, cons
   const int tpc = (g.c + 63) / 64;
   k_gate_prep<<<(g.ns * g.n + 127) / 128, 128, 0, st>>>(g, log_g, w.ell, w.lamlog);
   if (DM == 32 && g.d == 32 && g.e == 32)
-    k_intra_fwd_h<T><<<dim3(g.n * tpc, g.ns), 128, 0, st>>>(g, q, k, v, w.ell, w.yat);
+    k_intra_fwd_h<T, kIntraTpr><<<dim3(g.n * tpc, g.ns), 64 * kIntraTpr, 0, st>>>(g, q, k, v, w.ell, w.yat);
   else
     k_intra_fwd<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_intra_fwd<T, DM>, smb_intra_fwd<DM>()), st>>>(g, q, k, v, w.ell, w.yat);
   if (tc4_supported(g, g.dtype)) {
@@ -1380,8 +1372,10 @@ static int simt_backward_t(const Geo& g, const T* q, const T* k, const T* v, con
   ++launches;
   }
   if (DM == 32 && g.d == 32 && g.e == 32) {
-    k_intra_bwd_q_h<T><<<dim3(g.n * tpc, g.ns), 128, 0, st>>>(g, q, k, v, w.ell, b.dz, b.dq32, b.dell);
-    k_intra_bwd_kv_h<T><<<dim3(g.n * tpc, g.ns), 128, 0, st>>>(g, q, k, v, w.ell, b.dz, b.dk32, b.dv32, b.dell);
+    k_intra_bwd_q_h<T, kIntraTpr><<<dim3(g.n * tpc, g.ns), 64 * kIntraTpr, 0, st>>>(g, q, k, v, w.ell, b.dz, b.dq32,
+                                                                                  b.dell);
+    k_intra_bwd_kv_h<T, kIntraTpr><<<dim3(g.n * tpc, g.ns), 64 * kIntraTpr, 0, st>>>(g, q, k, v, w.ell, b.dz, b.dk32,
+                                                                                   b.dv32, b.dell);
   } else {
     k_intra_bwd_q<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_intra_bwd_q<T, DM>, smb_intra_bwd<DM>()), st>>>(g, q, k, v, w.ell, b.dz, b.dq32, b.dell);
     k_intra_bwd_kv<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_intra_bwd_kv<T, DM>, smb_intra_bwd<DM>()), st>>>(g, q, k, v, w.ell, b.dz, b.dk32, b.dv32, b.dell);
