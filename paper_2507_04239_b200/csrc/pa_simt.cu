@@ -1290,7 +1290,13 @@ static int simt_forward_t(const Geo& g, const T* q, const T* k, const T* v, cons
                           float* rowsum, const SimtWs& w, cudaStream_t st) {
   const int tpc = (g.c + 63) / 64;
   k_gate_prep<<<(g.ns * g.n + 127) / 128, 128, 0, st>>>(g, log_g, w.ell, w.lamlog);
-  if (DM == 32 && g.d == 32 && g.e == 32)
+  int intra_rc = 1;
+  if (tc4_supported(g, g.dtype)) {
+    intra_rc = tc4_intra_fwd(g, q, k, v, w.ell, w.yat, w.tc4, st);
+    if (intra_rc > 1) return intra_rc;
+  }
+  if (intra_rc == 0) {
+  } else if (DM == 32 && g.d == 32 && g.e == 32)
     k_intra_fwd_h<T, kIntraTpr><<<dim3(g.n * tpc, g.ns), 64 * kIntraTpr, 0, st>>>(g, q, k, v, w.ell, w.yat);
   else
     k_intra_fwd<T, DM><<<dim3(g.n * tpc, g.ns), 64, dyn_smem(k_intra_fwd<T, DM>, smb_intra_fwd<DM>()), st>>>(g, q, k, v, w.ell, w.yat);

@@ -26,6 +26,9 @@ int tc4_state(const Geo& g, bool bwd, const void* x, const void* v, const float*
 int tc4_slots();
 int tc4_copy_tables(int* idx, float* wt, cudaStream_t st);
 unsigned* tc4_mxs(const Geo& g, void* scratch);  // per-chunk maxima recorded by tc4_state
+// degree-4 intra-chunk attention on the tensor cores; 1 = shape not covered
+int tc4_intra_fwd(const Geo& g, const void* q, const void* k, const void* v, const float* ell, float* yat,
+                  void* scratch, cudaStream_t st);
 // discumsum fused with the fp16 operand conversion (pa_tc4.cu)
 int tc4_scan_fwd(const Geo& g, const float* lamlog, float* A, const float* wt, void* scratch, cudaStream_t st);
 int tc4_scan_bwd(const Geo& g, const float* lamlog, const float* A, const float* dA, float* dlam, const float* wt,

@@ -898,6 +898,7 @@ struct Tc4Ws {
   float* sba;     // sB per (stream, chunk) of bsa
   float* sbd;     // sB per (stream, chunk) of bsd
   unsigned* mxs;  // per-chunk max |S'_k w| (forward) / |dA'_k w| (backward) from k_tc4_state
+  __nv_bfloat16 *q64, *k64, *v64;   // zero-padded 64-dim copies for the intra-chunk kernel [ns][t][64]
 };
 static Tc4Ws tc4_carve(const Geo& g, void* base, size_t* bytes) {
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
@@ -920,6 +921,10 @@ static Tc4Ws tc4_carve(const Geo& g, void* base, size_t* bytes) {
   w.sba = (float*)take(sk * 4);
   w.sbd = (float*)take(sk * 4);
   w.mxs = (unsigned*)take(sk * 4);
+  const size_t pr = (size_t)g.ns * g.t * 64 * 2;
+  w.q64 = (__nv_bfloat16*)take(pr);
+  w.k64 = (__nv_bfloat16*)take(pr);
+  w.v64 = (__nv_bfloat16*)take(pr);
   *bytes = off;
   return w;
 }
@@ -963,6 +968,211 @@ int tc4_state(const Geo& g, bool bwd, const void* x, const void* v, const float*
 unsigned* tc4_mxs(const Geo& g, void* scratch) {
   size_t nb;
   return tc4_carve(g, scratch, &nb).mxs;
+}
+
+// ---------------------------------------------------------------- intra-chunk
+// Degree-4 intra-chunk attention on the tensor cores (reference attention.py:
+// 273-309 per chunk, unnormalized, chunked.py:336): yat[m] = [sum_j P_mj v_j |
+// sum_j P_mj] with P = exp(ell_m - ell_j) (sigma q.k)^4 under the causal mask,
+// fp32 out for the fp32 pipeline's combine.  d = e = 32 operands run as
+// zero-padded 64-dim bf16 rows (k_tc4_pad64), so the tiles are those of the
+// p = 2 output kernel: one CTA per 128-query tile, S = Q K_J^T (tcgen05, SW128
+// K-major), P computed by eight warps into the S buffer as bf16 pairs, O += P V_J
+// (A from TMEM, V MN-major).  The score sums are added in fp32 by the P warps.
+namespace ti {
+constexpr int TB = 128 * 128;   // one 128-token x 64-dim bf16 tile (SW128 rows)
+constexpr int KV_ST = 2;
+constexpr int NSB = 2;          // S / P buffers
+constexpr int THREADS = 320;    // w0..w7 P (two per lane quadrant), w8 TMA + TMEM, w9 MMA
+constexpr int SMEM = 1024 + TB + KV_ST * 2 * TB + 4096 + 1024 + 2048 + 256;
+}  // namespace ti
+
+// [b][t][h][32] bf16 -> [ns][t][64] bf16 with zero upper half (one thread per row)
+__global__ void __launch_bounds__(256) k_tc4_pad64(Geo g, const __nv_bfloat16* __restrict__ x, __nv_bfloat16* out) {
+  const size_t it = blockIdx.x * (size_t)256 + threadIdx.x;
+  if (it >= (size_t)g.ns * g.t) return;
+  const int s = (int)(it / g.t), m = (int)(it - (size_t)s * g.t);
+  const uint4* src = (const uint4*)(x + rowid(g, s, m) * 32);
+  uint4* dst = (uint4*)(out + it * 64);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) dst[c] = src[c];
+#pragma unroll
+  for (int c = 4; c < 8; ++c) dst[c] = make_uint4(0u, 0u, 0u, 0u);
+}
+
+__global__ void __launch_bounds__(ti::THREADS, 1) k_tc4_intra(const __grid_constant__ CUtensorMap tm_q,
+                                                              const __grid_constant__ CUtensorMap tm_k,
+                                                              const __grid_constant__ CUtensorMap tm_v, Geo g,
+                                                              const float* __restrict__ ell, float* yat) {
+  using namespace ti;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* q_s = smem;
+  uint8_t* k_s = q_s + TB;
+  uint8_t* v_s = k_s + KV_ST * TB;
+  float* ell_s = (float*)(v_s + KV_ST * TB);   // [1024]
+  float* cj = ell_s + 1024;                    // [2][128]
+  float* rs_s = cj + 256;                      // [128] the second half's score sums
+  uint64_t* bars = (uint64_t*)(rs_s + 128 + 128);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = q_full + 1;       // KV_ST
+  uint64_t* kv_empty = kv_full + KV_ST;
+  uint64_t* s_full = kv_empty + KV_ST;  // NSB
+  uint64_t* p_full = s_full + NSB;      // NSB (8 warps)
+  uint64_t* pv_done = p_full + NSB;     // NSB
+  uint64_t* fin = pv_done + NSB;
+  __shared__ uint32_t tmem_base;
+
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  const int I = blockIdx.x, k = blockIdx.y, s = blockIdx.z;
+  const int c0 = k * g.c;
+  constexpr uint32_t TO = NSB * 128;   // O accumulator columns [256, 320)
+  if (w == 8) tmem_alloc<512>(&tmem_base);
+  if (tid == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < KV_ST; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < NSB; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 8);
+      mbar_init(&pv_done[i], 1);
+    }
+    mbar_init(fin, 1);
+    fence_barrier_init();
+  }
+  for (int i = tid; i < (I + 1) * 128; i += THREADS) ell_s[i] = g.gated ? ell[(size_t)s * g.t + c0 + i] : 0.f;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tmem_base;
+  const size_t row0 = (size_t)s * g.t + c0;
+
+  if (w == 8) {
+    if (l == 0) {
+      tma_prefetch(&tm_q);
+      tma_prefetch(&tm_k);
+      tma_prefetch(&tm_v);
+      mbar_expect_tx(q_full, TB);
+      tma_load_2d(q_s, &tm_q, q_full, 0, (int)(row0 + I * 128));
+      for (int J = 0; J <= I; ++J) {
+        const int st = J % KV_ST;
+        if (J >= KV_ST) mbar_wait(&kv_empty[st], ((J / KV_ST) + 1) & 1);
+        mbar_expect_tx(&kv_full[st], 2 * TB);
+        tma_load_2d(k_s + st * TB, &tm_k, &kv_full[st], 0, (int)(row0 + J * 128));
+        tma_load_2d(v_s + st * TB, &tm_v, &kv_full[st], 0, (int)(row0 + J * 128));
+      }
+    }
+  } else if (w == 9) {
+    constexpr uint32_t id128 = idesc_bf16(128, 128, false, false);
+    constexpr uint32_t id64mn = idesc_bf16(128, 64, false, true);
+    const uint64_t qd0 = smem_desc(smem_u32(q_s), 16, 1024, 2);
+    const uint64_t kd0 = smem_desc(smem_u32(k_s), 16, 1024, 2);
+    const uint64_t vd0 = smem_desc(smem_u32(v_s), 8192, 1024, 2);
+    mbar_wait_w(q_full, 0);
+    auto issue_s = [&](int J) {
+      const int st = J % KV_ST, sb = J % NSB;
+      mbar_wait_w(&kv_full[st], (J / KV_ST) & 1);
+      if (J >= NSB) mbar_wait_w(&pv_done[sb], ((J / NSB) + 1) & 1);
+      tc_fence_after();
+      const uint64_t ko = (uint64_t)((st * TB) >> 4);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        mma_ss_w(tm + (uint32_t)(sb * 128), qd0 + (uint64_t)(kk * 2), kd0 + ko + (uint64_t)(kk * 2), id128,
+                 kk > 0 ? 1u : 0u);
+      tc_commit_w(&s_full[sb]);
+    };
+    issue_s(0);
+    for (int J = 0; J <= I; ++J) {
+      if (J + 1 <= I) issue_s(J + 1);
+      const int sb = J % NSB, st = J % KV_ST;
+      mbar_wait_w(&p_full[sb], (J / NSB) & 1);
+      tc_fence_after();
+      const uint64_t vo = (uint64_t)((st * TB) >> 4);
+      const uint32_t pb = tm + (uint32_t)(sb * 128);
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        mma_ts_w(tm + TO, pb + kk * 8, vd0 + vo + (uint64_t)(kk * 128), id64mn, (J > 0 || kk > 0) ? 1u : 0u);
+      tc_commit_w(&pv_done[sb]);
+      tc_commit_w(&kv_empty[st]);
+    }
+    tc_commit_w(fin);
+  } else {
+    // P = exp(ell_i - ell_j) (sigma s)^4, two warps per lane quadrant (columns
+    // [64 ph, 64 ph + 64)), written back into the S buffer as bf16 pairs
+    const int q = w & 3, row = q * 32 + l, ph = w >> 2;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const float li = ell_s[I * 128 + row];
+    const float sig2 = g.scale * g.scale, sig4 = sig2 * sig2;
+    float rs = 0.f;
+    for (int J = 0; J <= I; ++J) {
+      const int sb = J % NSB, cb = J & 1;
+      const bool diag = (J == I);
+      const float lref = ell_s[J * 128 + 127];
+      if (ph == 0) cj[cb * 128 + row] = __expf(lref - ell_s[J * 128 + row]);
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      mbar_wait(&s_full[sb], (J / NSB) & 1);
+      tc_fence_after();
+      const float ri = __expf(li - lref) * sig4;
+      const float* cjs = cj + cb * 128;
+      const uint32_t sp = tm + (uint32_t)(sb * 128) + lane_off;
+      uint32_t rb[2][32];
+      tmem_ld32(sp + ph * 64, rb[0]);
+      tmem_ld32(sp + ph * 64 + 32, rb[1]);
+      tc_wait_ld();
+      // the half-1 warp's P lands on S columns [32, 64), which the half-0 warp of
+      // this quadrant must have read first
+      asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
+#pragma unroll
+      for (int ch = 2 * ph; ch < 2 * ph + 2; ++ch) {
+        uint32_t pk[16];
+        const uint32_t* r = rb[ch & 1];
+#pragma unroll
+        for (int e4 = 0; e4 < 8; ++e4) {
+          const float4 c4 = *(const float4*)(cjs + ch * 32 + e4 * 4);
+          const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
+          float pv[4];
+#pragma unroll
+          for (int z = 0; z < 4; ++z) {
+            const int jj = ch * 32 + e4 * 4 + z;
+            const float sv = __uint_as_float(r[e4 * 4 + z]);
+            const float s2 = sv * sv;
+            float e;
+            if (!diag) e = ri * cc[z] * s2 * s2;
+            else e = (jj <= row) ? __expf(fminf(li - ell_s[J * 128 + jj], 0.f)) * sig4 * s2 * s2 : 0.f;
+            pv[z] = e;
+            rs += e;
+          }
+          pk[e4 * 2] = pack_bf16(pv[0], pv[1]);
+          pk[e4 * 2 + 1] = pack_bf16(pv[2], pv[3]);
+        }
+        tmem_st16(sp + ch * 16, pk);
+      }
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (l == 0) mbar_arrive(&p_full[sb]);
+    }
+    // epilogue: O (32 of 64 columns) and the score sum of both halves
+    if (ph == 1) rs_s[row] = rs;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    if (ph == 0) {
+      mbar_wait(fin, 0);
+      tc_fence_after();
+      uint32_t r[32];
+      tmem_ld32(tm + TO + lane_off, r);
+      tc_wait_ld();
+      const int m = c0 + I * 128 + row;
+      float* dst = yat + ((size_t)s * g.t + m) * 33;
+#pragma unroll
+      for (int u = 0; u < 32; ++u) dst[u] = __uint_as_float(r[u]);
+      dst[32] = rs + rs_s[row];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (w == 8) tmem_dealloc<512>(tm);
 }
 
 // ---------------------------------------------------------------- scans
@@ -1086,6 +1296,29 @@ __global__ void __launch_bounds__(256) k_tc4_scan_bwd16(Geo g, const float* __re
     for (int i = 0; i < 8; ++i) t += redk[k * 8 + i];
     atomicAdd(dlam + s * g.n + k, t);
   }
+}
+
+// intra-chunk part on the tensor cores (chunk a multiple of 128 up to 1024);
+// returns 1 when the shape is not covered (the caller runs the CUDA-core kernel)
+int tc4_intra_fwd(const Geo& g, const void* q, const void* k, const void* v, const float* ell, float* yat,
+                  void* scratch, cudaStream_t st) {
+  using namespace ti;
+  if (g.c % 128 || g.c > 1024 || g.t % g.c) return 1;
+  size_t nb;
+  Tc4Ws w = tc4_carve(g, scratch, &nb);
+  const unsigned pb = (unsigned)(((size_t)g.ns * g.t + 255) / 256);
+  k_tc4_pad64<<<pb, 256, 0, st>>>(g, (const __nv_bfloat16*)q, w.q64);
+  k_tc4_pad64<<<pb, 256, 0, st>>>(g, (const __nv_bfloat16*)k, w.k64);
+  k_tc4_pad64<<<pb, 256, 0, st>>>(g, (const __nv_bfloat16*)v, w.v64);
+  CUtensorMap mq, mk, mv;
+  const size_t rows = (size_t)g.ns * g.t;
+  if (!tc_map_2d(&mq, w.q64, rows, 64, 64, 128, 0) || !tc_map_2d(&mk, w.k64, rows, 64, 64, 128, 0) ||
+      !tc_map_2d(&mv, w.v64, rows, 64, 64, 128, 0))
+    return 3;
+  cudaFuncSetAttribute(k_tc4_intra, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  k_tc4_intra<<<dim3(g.c / 128, g.n, g.ns), THREADS, SMEM, st>>>(mq, mk, mv, g, ell, yat);
+  count_launch(4);
+  return cuda_check("tc4 intra-chunk");
 }
 
 int tc4_scan_fwd(const Geo& g, const float* lamlog, float* A, const float* wt, void* scratch, cudaStream_t st) {
