@@ -977,8 +977,9 @@ unsigned* tc4_mxs(const Geo& g, void* scratch) {
 // fp32 out for the fp32 pipeline's combine.  d = e = 32 operands run as
 // zero-padded 64-dim bf16 rows (k_tc4_pad64), so the tiles are those of the
 // p = 2 output kernel: one CTA per 128-query tile, S = Q K_J^T (tcgen05, SW128
-// K-major), P computed by eight warps into the S buffer as bf16 pairs, O += P V_J
-// (A from TMEM, V MN-major).  The score sums are added in fp32 by the P warps.
+// K-major), P computed by eight warps into the S buffer as bf16 hi + lo pairs,
+// O += P_hi V_J + P_lo V_J (A from TMEM, V MN-major).  The score sums are added
+// in fp32 by the P warps.
 namespace ti {
 constexpr int TB = 128 * 128;   // one 128-token x 64-dim bf16 tile (SW128 rows)
 constexpr int KV_ST = 2;
@@ -1092,8 +1093,10 @@ __global__ void __launch_bounds__(ti::THREADS, 1) k_tc4_intra(const __grid_const
       const uint64_t vo = (uint64_t)((st * TB) >> 4);
       const uint32_t pb = tm + (uint32_t)(sb * 128);
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk)
+      for (int kk = 0; kk < 8; ++kk) {
         mma_ts_w(tm + TO, pb + kk * 8, vd0 + vo + (uint64_t)(kk * 128), id64mn, (J > 0 || kk > 0) ? 1u : 0u);
+        mma_ts_w(tm + TO, pb + 64u + kk * 8, vd0 + vo + (uint64_t)(kk * 128), id64mn, 1u);   // P lo
+      }
       tc_commit_w(&pv_done[sb]);
       tc_commit_w(&kv_empty[st]);
     }
@@ -1126,7 +1129,7 @@ __global__ void __launch_bounds__(ti::THREADS, 1) k_tc4_intra(const __grid_const
       asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
 #pragma unroll
       for (int ch = 2 * ph; ch < 2 * ph + 2; ++ch) {
-        uint32_t pk[16];
+        uint32_t pk[16], pl[16];
         const uint32_t* r = rb[ch & 1];
 #pragma unroll
         for (int e4 = 0; e4 < 8; ++e4) {
@@ -1144,10 +1147,17 @@ __global__ void __launch_bounds__(ti::THREADS, 1) k_tc4_intra(const __grid_const
             pv[z] = e;
             rs += e;
           }
+          // P = hi + lo, two bf16 parts (the degree-4 scores are too skewed for a
+          // single bf16 rounding: one part measured dq 0.016 against 0.004)
           pk[e4 * 2] = pack_bf16(pv[0], pv[1]);
           pk[e4 * 2 + 1] = pack_bf16(pv[2], pv[3]);
+          const float2 h0 = __bfloat1622float2(*(const __nv_bfloat162*)&pk[e4 * 2]);
+          const float2 h1 = __bfloat1622float2(*(const __nv_bfloat162*)&pk[e4 * 2 + 1]);
+          pl[e4 * 2] = pack_bf16(pv[0] - h0.x, pv[1] - h0.y);
+          pl[e4 * 2 + 1] = pack_bf16(pv[2] - h1.x, pv[3] - h1.y);
         }
         tmem_st16(sp + ch * 16, pk);
+        tmem_st16(sp + 64 + ch * 16, pl);
       }
       tc_wait_st();
       tc_fence_before();
