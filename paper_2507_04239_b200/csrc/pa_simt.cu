@@ -1262,6 +1262,10 @@ __global__ void __launch_bounds__(64 * TPR) k_intra_bwd_kv_h(Geo g, const T* __r
   if (!hf) dell[(size_t)s * g.t + j] -= colD;
 }
 
+static bool getenv_flag(const char* name) {
+  const char* e = getenv(name);
+  return e && e[0] == '1';
+}
 constexpr int kIntraTpr = 2;   // threads per row of the d = 32 intra-chunk kernels (4 measured slower)
 
 // dynamic shared memory per block for the kernels above (floats -> bytes)
@@ -1377,7 +1381,13 @@ static int simt_backward_t(const Geo& g, const T* q, const T* k, const T* v, con
                         dyn_smem(k_update_bwd<T, DM>, smb_update_bwd<DM>()), st>>>(g, k, v, b.dA, w.idx, w.wt, w.ell, w.lamlog, b.dk32, b.dv32, b.dell, b.dellend);
   ++launches;
   }
-  if (DM == 32 && g.d == 32 && g.e == 32) {
+  int intra_rc = 1;
+  if (tc4_supported(g, g.dtype) && !getenv_flag("PA_TC4_INTRA_BWD_OFF")) {
+    intra_rc = tc4_intra_bwd(g, w.ell, b.dz, dy, rowsum, b.dq32, b.dk32, b.dv32, b.dell, w.tc4, st);
+    if (intra_rc > 1) return intra_rc;
+  }
+  if (intra_rc == 0) {
+  } else if (DM == 32 && g.d == 32 && g.e == 32) {
     k_intra_bwd_q_h<T, kIntraTpr><<<dim3(g.n * tpc, g.ns), 64 * kIntraTpr, 0, st>>>(g, q, k, v, w.ell, b.dz, b.dq32,
                                                                                   b.dell);
     k_intra_bwd_kv_h<T, kIntraTpr><<<dim3(g.n * tpc, g.ns), 64 * kIntraTpr, 0, st>>>(g, q, k, v, w.ell, b.dz, b.dk32,

@@ -29,6 +29,9 @@ unsigned* tc4_mxs(const Geo& g, void* scratch);  // per-chunk maxima recorded by
 // degree-4 intra-chunk attention on the tensor cores; 1 = shape not covered
 int tc4_intra_fwd(const Geo& g, const void* q, const void* k, const void* v, const float* ell, float* yat,
                   void* scratch, cudaStream_t st);
+// its VJP (needs the padded copies of tc4_intra_fwd in the same scratch); 1 = not covered
+int tc4_intra_bwd(const Geo& g, const float* ell, const float* dz, const void* dy, const float* rowsum, float* dq32,
+                  float* dk32, float* dv32, float* dell, void* scratch, cudaStream_t st);
 // discumsum fused with the fp16 operand conversion (pa_tc4.cu)
 int tc4_scan_fwd(const Geo& g, const float* lamlog, float* A, const float* wt, void* scratch, cudaStream_t st);
 int tc4_scan_bwd(const Geo& g, const float* lamlog, const float* A, const float* dA, float* dlam, const float* wt,

@@ -898,7 +898,8 @@ struct Tc4Ws {
   float* sba;     // sB per (stream, chunk) of bsa
   float* sbd;     // sB per (stream, chunk) of bsd
   unsigned* mxs;  // per-chunk max |S'_k w| (forward) / |dA'_k w| (backward) from k_tc4_state
-  __nv_bfloat16 *q64, *k64, *v64;   // zero-padded 64-dim copies for the intra-chunk kernel [ns][t][64]
+  __nv_bfloat16 *q64, *k64, *v64;   // zero-padded 64-dim copies for the intra-chunk kernels [ns][t][64]
+  __nv_bfloat16* dz64;               // dy rows of the intra-chunk VJP, same layout
 };
 static Tc4Ws tc4_carve(const Geo& g, void* base, size_t* bytes) {
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
@@ -925,6 +926,7 @@ static Tc4Ws tc4_carve(const Geo& g, void* base, size_t* bytes) {
   w.q64 = (__nv_bfloat16*)take(pr);
   w.k64 = (__nv_bfloat16*)take(pr);
   w.v64 = (__nv_bfloat16*)take(pr);
+  w.dz64 = (__nv_bfloat16*)take(pr);
   *bytes = off;
   return w;
 }
@@ -1306,6 +1308,289 @@ __global__ void __launch_bounds__(256) k_tc4_scan_bwd16(Geo g, const float* __re
     for (int i = 0; i < 8; ++i) t += redk[k * 8 + i];
     atomicAdd(dlam + s * g.n + k, t);
   }
+}
+
+// ---------------------------------------------------------------- intra-chunk VJP
+// Degree-4 intra-chunk backward on the tensor cores (reference gradients.py:
+// 98-176 power branch, log-gate rule 79-95): one CTA per (key tile J, chunk,
+// stream), walking the query tiles I >= J of the chunk:
+//   S^T = K_J Q_I^T, dP^T = V_J dy_I^T         (tcgen05, K = 64 zero-padded dims)
+//   P = E s^4, dS = (dP / R_i + dden_i) 4 E s^3,  s = sigma q.k,
+//   E = exp(ell_i - ell_j)  (R_i = 1 without normalization)
+//   dV_J += (P / R)^T dy_I                    (as bf16 in TMEM)
+//   dK_J += dS^T Q_I,  dQ_I = dS K_J          (dS as bf16 hi + lo tiles in shared
+//                                              memory, read K-major for dK and
+//                                              MN-major for dQ); dQ red.add-ed
+//                                              into the fp32 dq rows
+// Log-gate cotangents from fp32 products: dell_j -= sum_i dP' P (per key
+// thread), dell_i += sum_j dP' P (a butterfly reduce-scatter over the key
+// rows, then one atomic per query and CTA).  Four compute warps (key row =
+// TMEM lane, all 128 query columns in groups of 32: each group's S / dP columns
+// are read before the group's P / dS pairs land on the lower half), w4 TMA +
+// TMEM, w5 MMA.
+namespace tb {
+constexpr int TB = 128 * 128;       // 128 tokens x 64 bf16 (SW128)
+constexpr int DS_B = 2 * 128 * 128; // dS: 2 query blocks (64 queries) x 128 keys x 128 B (hi, then lo)
+constexpr int THREADS = 192;   // w0..w3 compute (one per lane quadrant), w4 TMA + TMEM, w5 MMA
+constexpr int SMEM = 1024 + 2 * TB + 2 * 2 * TB + 2 * DS_B + 4096 + 4096 + 256;   // + ell, (ai, ddi, rvi, red), bars
+}  // namespace tb
+
+__global__ void __launch_bounds__(tb::THREADS, 1) k_tc4_intra_bwd(
+    const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_dz, Geo g,
+    const float* __restrict__ ell, const float* __restrict__ dz, const float* __restrict__ rowsum, float* dq32,
+    float* dk32, float* dv32, float* dell) {
+  using namespace tb;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* k_s = smem;                 // K_J
+  uint8_t* v_s = k_s + TB;             // V_J
+  uint8_t* q_s = v_s + TB;             // [2] Q_I
+  uint8_t* z_s = q_s + 2 * TB;         // [2] dnum_I
+  uint8_t* ds_s = z_s + 2 * TB;        // dS tiles: hi, lo
+  float* ell_s = (float*)(ds_s + 2 * DS_B);   // [1024]
+  float* ai = ell_s + 1024;               // [128] query factors of the current I
+  float* ddi = ai + 128;                  // [128] dden of the current I
+  float* rvi = ddi + 128;                 // [128] 1 / R_i (normalize) or 1
+  float* red = rvi + 128;                 // [4 quadrants][128] query row sums
+  uint64_t* bars = (uint64_t*)(red + 512);
+  uint64_t* kv_full = bars;
+  uint64_t* qd_full = bars + 1;   // 2
+  uint64_t* qd_empty = bars + 3;  // 2
+  uint64_t* s_full = bars + 5;
+  uint64_t* p_full = bars + 6;    // 8 warps
+  uint64_t* m_done = bars + 7;
+  uint64_t* dq_empty = bars + 8;  // 8 warps
+  __shared__ uint32_t tmem_base;
+
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  const int J = blockIdx.x, k = blockIdx.y, s = blockIdx.z;
+  const int nq = g.c / 128, c0 = k * g.c;
+  const size_t row0 = (size_t)s * g.t + c0;
+  constexpr uint32_t TS_ = 0, TDP = 128, TDV = 256, TDK = 320, TDQ = 384;
+  if (w == 4) tmem_alloc<512>(&tmem_base);
+  if (tid == 0) {
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&qd_full[i], 1);
+      mbar_init(&qd_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 4);
+    mbar_init(m_done, 1);
+    mbar_init(dq_empty, 4);
+    fence_barrier_init();
+  }
+  for (int i = tid; i < g.c; i += THREADS) ell_s[i] = g.gated ? ell[row0 + i] : 0.f;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tmem_base;
+
+  if (w == 4) {
+    if (l == 0) {
+      tma_prefetch(&tm_q);
+      tma_prefetch(&tm_k);
+      mbar_expect_tx(kv_full, 2 * TB);
+      tma_load_2d(k_s, &tm_k, kv_full, 0, (int)(row0 + J * 128));
+      tma_load_2d(v_s, &tm_v, kv_full, 0, (int)(row0 + J * 128));
+      for (int I = J, n = 0; I < nq; ++I, ++n) {
+        const int st = n & 1;
+        if (n >= 2) mbar_wait(&qd_empty[st], ((n >> 1) + 1) & 1);
+        mbar_expect_tx(&qd_full[st], 2 * TB);
+        tma_load_2d(q_s + st * TB, &tm_q, &qd_full[st], 0, (int)(row0 + I * 128));
+        tma_load_2d(z_s + st * TB, &tm_dz, &qd_full[st], 0, (int)(row0 + I * 128));
+      }
+    }
+  } else if (w == 5) {
+    constexpr uint32_t idSK = idesc_bf16(128, 128, false, false);   // A, B K-major
+    constexpr uint32_t idG = idesc_bf16(128, 64, false, true);      // A TMEM, B MN-major
+    constexpr uint32_t idQ = idesc_bf16(128, 64, true, true);       // A (dS) MN-major smem, B MN-major
+    const uint64_t kd = smem_desc(smem_u32(k_s), 16, 1024, 2), vd = smem_desc(smem_u32(v_s), 16, 1024, 2);
+    const uint64_t km = smem_desc(smem_u32(k_s), 8192, 1024, 2);
+    const uint64_t dsd = smem_desc(smem_u32(ds_s), 16384, 1024, 2);   // dS as MN-major A (M = queries)
+    const uint64_t dsk = smem_desc(smem_u32(ds_s), 16, 1024, 2);      // dS^T as K-major A (M = keys)
+    mbar_wait_w(kv_full, 0);
+    for (int I = J, n = 0; I < nq; ++I, ++n) {
+      const int st = n & 1;
+      mbar_wait_w(&qd_full[st], (n >> 1) & 1);
+      tc_fence_after();
+      const uint64_t qk = smem_desc(smem_u32(q_s + st * TB), 16, 1024, 2);
+      const uint64_t zk = smem_desc(smem_u32(z_s + st * TB), 16, 1024, 2);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        mma_ss_w(tm + TS_, kd + (uint64_t)(kk * 2), qk + (uint64_t)(kk * 2), idSK, kk > 0 ? 1u : 0u);
+        mma_ss_w(tm + TDP, vd + (uint64_t)(kk * 2), zk + (uint64_t)(kk * 2), idSK, kk > 0 ? 1u : 0u);
+      }
+      tc_commit_w(s_full);
+      mbar_wait_w(p_full, n & 1);
+      tc_fence_after();
+      const uint64_t qm = smem_desc(smem_u32(q_s + st * TB), 8192, 1024, 2);
+      const uint64_t zm = smem_desc(smem_u32(z_s + st * TB), 8192, 1024, 2);
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const uint32_t acc = (n > 0 || kk > 0) ? 1u : 0u;
+        mma_ts_w(tm + TDV, tm + TS_ + kk * 8, zm + (uint64_t)(kk * 128), idG, acc);
+        // dK += dS^T Q with dS^T = the dS tile read K-major (rows = keys), hi and lo
+        const uint64_t ako = (uint64_t)((kk >> 2) * (16384 >> 4) + (kk & 3) * 2);
+        mma_ss_w(tm + TDK, dsk + ako, qm + (uint64_t)(kk * 128), idG, acc);
+        mma_ss_w(tm + TDK, dsk + (uint64_t)(DS_B >> 4) + ako, qm + (uint64_t)(kk * 128), idG, 1u);
+      }
+      tc_commit_w(&qd_empty[st]);
+      if (n > 0) mbar_wait_w(dq_empty, (n - 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk)   // dQ = (dS hi + dS lo) K
+        mma_ss_w(tm + TDQ, dsd + (uint64_t)((kk >> 3) * (DS_B >> 4) + (kk & 7) * 128), km + (uint64_t)((kk & 7) * 128),
+                 idQ, kk > 0 ? 1u : 0u);
+      tc_commit_w(m_done);
+    }
+  } else {
+    const int q = w, jr = q * 32 + l;   // key row in the tile (TMEM lane)
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const int jl = J * 128 + jr;        // key index in the chunk
+    const float lref = ell_s[J * 128];
+    const float bj = __expf(lref - ell_s[jl]);   // exp(ell_ref - ell_j) <= e^80
+    const float sig = g.scale;
+    float colD = 0.f;
+    for (int I = J, n = 0; I < nq; ++I, ++n) {
+      // query factors of tile I: exp(ell_i - ell_ref) (and dden_i)
+      {
+        const int il = I * 128 + jr;
+        ai[jr] = __expf(fminf(ell_s[il] - lref, 0.f));
+        ddi[jr] = dz[(row0 + il) * 33 + 32];
+        rvi[jr] = g.normalize ? 1.f / rowsum[rowid(g, s, c0 + il)] : 1.f;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      mbar_wait(s_full, n & 1);
+      tc_fence_after();
+      const bool diag = I == J;
+#pragma unroll 1
+      for (int h = 0; h < 4; ++h) {   // query columns [32 h, 32 h + 32)
+        uint32_t sr[32], dr[32];
+        tmem_ld32(tm + TS_ + lane_off + (uint32_t)(h * 32), sr);
+        tmem_ld32(tm + TDP + lane_off + (uint32_t)(h * 32), dr);
+        tc_wait_ld();
+        float rq[32];
+        uint32_t pk[16], dk[16], dl[16];
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+          float pv[2], dv[2];
+#pragma unroll
+          for (int z = 0; z < 2; ++z) {
+            const int ic = h * 32 + c + z;   // query column in tile I
+            const float sv = sig * __uint_as_float(sr[c + z]);
+            const float s2 = sv * sv;
+            float E = ai[ic] * bj;
+            if (diag) E = (ic >= jr) ? __expf(fminf(ell_s[I * 128 + ic] - ell_s[jl], 0.f)) : 0.f;
+            const float P = E * s2 * s2;
+            // dP' = dy_i . v_j / R_i + dden_i: the GEMM runs on the exact bf16 dy and
+            // 1 / R_i stays fp32 (a rounded dnum = dy / R amplifies at small R)
+            const float dPp = __uint_as_float(dr[c + z]) * rvi[ic] + ddi[ic];
+            pv[z] = P * rvi[ic];   // dV += (P / R)^T dy
+            dv[z] = dPp * 4.f * E * s2 * sv;
+            rq[c + z] = dPp * P;
+            colD += dPp * P;
+          }
+          pk[c / 2] = pack_bf16(pv[0], pv[1]);
+          dk[c / 2] = pack_bf16(dv[0], dv[1]);
+          const float2 dh = __bfloat1622float2(*(const __nv_bfloat162*)&dk[c / 2]);
+          dl[c / 2] = pack_bf16(dv[0] - dh.x, dv[1] - dh.y);
+        }
+        // P^T pairs (query q -> column q / 2); columns [16 h, 16 h + 16) were read in
+        // the group before (or this one)
+        tmem_st16(tm + TS_ + lane_off + (uint32_t)(h * 16), pk);
+        // dS as hi + lo bf16 tiles (the degree-4 dS is too skewed for one bf16
+        // rounding): query block h / 2, row = key jr, 16-byte chunks
+        uint8_t* rowp = ds_s + (h >> 1) * 16384 + jr * 128;
+#pragma unroll
+        for (int c8 = 0; c8 < 4; ++c8) {
+          const int ch = (h & 1) * 4 + c8;
+          *(uint4*)(rowp + ((ch ^ (jr & 7)) << 4)) = make_uint4(dk[4 * c8], dk[4 * c8 + 1], dk[4 * c8 + 2], dk[4 * c8 + 3]);
+          *(uint4*)(rowp + DS_B + ((ch ^ (jr & 7)) << 4)) =
+              make_uint4(dl[4 * c8], dl[4 * c8 + 1], dl[4 * c8 + 2], dl[4 * c8 + 3]);
+        }
+        // query-side sums over this warp's 32 key rows: butterfly reduce-scatter,
+        // lane l ends with column 32 h + l
+#pragma unroll
+        for (int off = 16, n2 = 16; off >= 1; off >>= 1, n2 >>= 1) {
+          const bool up = (l & off) != 0;
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            if (c < n2) {
+              const float send = up ? rq[c] : rq[c + n2];
+              const float keep = up ? rq[c + n2] : rq[c];
+              rq[c] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+            }
+          }
+        }
+        red[q * 128 + h * 32 + l] = rq[0];
+      }
+      tc_wait_st();
+      fence_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (l == 0) mbar_arrive(p_full);
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      {
+        const float t = red[jr] + red[128 + jr] + red[256 + jr] + red[384 + jr];
+        if (g.gated) atomicAdd(dell + row0 + I * 128 + jr, t);
+      }
+      // dQ_I (queries on the TMEM lanes): sigma dS K, 32 columns
+      mbar_wait(m_done, n & 1);
+      tc_fence_after();
+      {
+        uint32_t r[32];
+        tmem_ld32(tm + TDQ + lane_off, r);
+        tc_wait_ld();
+        float* dst = dq32 + (row0 + I * 128 + jr) * 32;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) atomicAdd(dst + c, sig * __uint_as_float(r[c]));
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (l == 0) mbar_arrive(dq_empty);
+      asm volatile("bar.sync 1, 128;" ::: "memory");   // red is rewritten by the next tile
+    }
+    // dK_J (x sigma), dV_J: the last m_done covers every MMA
+    {
+      uint32_t r[32];
+      tmem_ld32(tm + TDK + lane_off, r);
+      tc_wait_ld();
+      float* dst = dk32 + (row0 + jl) * 32;
+#pragma unroll
+      for (int c = 0; c < 32; ++c) dst[c] += sig * __uint_as_float(r[c]);
+      tmem_ld32(tm + TDV + lane_off, r);
+      tc_wait_ld();
+      float* dsv = dv32 + (row0 + jl) * 32;
+#pragma unroll
+      for (int c = 0; c < 32; ++c) dsv[c] += __uint_as_float(r[c]);
+    }
+    if (g.gated) dell[row0 + jl] -= colD;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (w == 4) tmem_dealloc<512>(tm);
+}
+
+int tc4_intra_bwd(const Geo& g, const float* ell, const float* dz, const void* dy, const float* rowsum, float* dq32,
+                  float* dk32, float* dv32, float* dell, void* scratch, cudaStream_t st) {
+  using namespace tb;
+  if (g.c % 128 || g.c > 1024 || g.t % g.c) return 1;
+  size_t nb;
+  Tc4Ws w = tc4_carve(g, scratch, &nb);
+  const unsigned pb = (unsigned)(((size_t)g.ns * g.t + 255) / 256);
+  k_tc4_pad64<<<pb, 256, 0, st>>>(g, (const __nv_bfloat16*)dy, w.dz64);
+  CUtensorMap mq, mk, mv, mz;
+  const size_t rows = (size_t)g.ns * g.t;
+  if (!tc_map_2d(&mq, w.q64, rows, 64, 64, 128, 0) || !tc_map_2d(&mk, w.k64, rows, 64, 64, 128, 0) ||
+      !tc_map_2d(&mv, w.v64, rows, 64, 64, 128, 0) || !tc_map_2d(&mz, w.dz64, rows, 64, 64, 128, 0))
+    return 3;
+  cudaFuncSetAttribute(k_tc4_intra_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  k_tc4_intra_bwd<<<dim3(g.c / 128, g.n, g.ns), THREADS, SMEM, st>>>(mq, mk, mv, mz, g, ell, dz, rowsum, dq32, dk32,
+                                                                    dv32, dell);
+  count_launch(2);
+  return cuda_check("tc4 intra-chunk VJP");
 }
 
 // intra-chunk part on the tensor cores (chunk a multiple of 128 up to 1024);
