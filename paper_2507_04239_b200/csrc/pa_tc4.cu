@@ -1317,7 +1317,7 @@ __global__ void __launch_bounds__(256) k_tc4_scan_bwd16(Geo g, const float* __re
 //   S^T = K_J Q_I^T, dP^T = V_J dy_I^T         (tcgen05, K = 64 zero-padded dims)
 //   P = E s^4, dS = (dP / R_i + dden_i) 4 E s^3,  s = sigma q.k,
 //   E = exp(ell_i - ell_j)  (R_i = 1 without normalization)
-//   dV_J += (P / R)^T dy_I                    (as bf16 in TMEM)
+//   dV_J += (P / R)^T dy_I                    (bf16 hi in TMEM + lo tile in smem)
 //   dK_J += dS^T Q_I,  dQ_I = dS K_J          (dS as bf16 hi + lo tiles in shared
 //                                              memory, read K-major for dK and
 //                                              MN-major for dQ); dQ red.add-ed
@@ -1332,7 +1332,7 @@ namespace tb {
 constexpr int TB = 128 * 128;       // 128 tokens x 64 bf16 (SW128)
 constexpr int DS_B = 2 * 128 * 128; // dS: 2 query blocks (64 queries) x 128 keys x 128 B (hi, then lo)
 constexpr int THREADS = 192;   // w0..w3 compute (one per lane quadrant), w4 TMA + TMEM, w5 MMA
-constexpr int SMEM = 1024 + 2 * TB + 2 * 2 * TB + 2 * DS_B + 4096 + 4096 + 256;   // + ell, (ai, ddi, rvi, red), bars
+constexpr int SMEM = 1024 + 2 * TB + 2 * 2 * TB + 3 * DS_B + 4096 + 4096 + 256;   // + ell, (ai, ddi, rvi, red), bars
 }  // namespace tb
 
 __global__ void __launch_bounds__(tb::THREADS, 1) k_tc4_intra_bwd(
@@ -1347,8 +1347,8 @@ __global__ void __launch_bounds__(tb::THREADS, 1) k_tc4_intra_bwd(
   uint8_t* v_s = k_s + TB;             // V_J
   uint8_t* q_s = v_s + TB;             // [2] Q_I
   uint8_t* z_s = q_s + 2 * TB;         // [2] dnum_I
-  uint8_t* ds_s = z_s + 2 * TB;        // dS tiles: hi, lo
-  float* ell_s = (float*)(ds_s + 2 * DS_B);   // [1024]
+  uint8_t* ds_s = z_s + 2 * TB;        // dS tiles: hi, lo; then the P / R lo tile
+  float* ell_s = (float*)(ds_s + 3 * DS_B);   // [1024]
   float* ai = ell_s + 1024;               // [128] query factors of the current I
   float* ddi = ai + 128;                  // [128] dden of the current I
   float* rvi = ddi + 128;                 // [128] 1 / R_i (normalize) or 1
@@ -1431,6 +1431,8 @@ __global__ void __launch_bounds__(tb::THREADS, 1) k_tc4_intra_bwd(
       for (int kk = 0; kk < 8; ++kk) {
         const uint32_t acc = (n > 0 || kk > 0) ? 1u : 0u;
         mma_ts_w(tm + TDV, tm + TS_ + kk * 8, zm + (uint64_t)(kk * 128), idG, acc);
+        mma_ss_w(tm + TDV, dsk + (uint64_t)(2 * (DS_B >> 4)) + (uint64_t)((kk >> 2) * (16384 >> 4) + (kk & 3) * 2),
+                 zm + (uint64_t)(kk * 128), idG, 1u);   // the P / R lo part
         // dK += dS^T Q with dS^T = the dS tile read K-major (rows = keys), hi and lo
         const uint64_t ako = (uint64_t)((kk >> 2) * (16384 >> 4) + (kk & 3) * 2);
         mma_ss_w(tm + TDK, dsk + ako, qm + (uint64_t)(kk * 128), idG, acc);
@@ -1472,7 +1474,7 @@ __global__ void __launch_bounds__(tb::THREADS, 1) k_tc4_intra_bwd(
         tmem_ld32(tm + TDP + lane_off + (uint32_t)(h * 32), dr);
         tc_wait_ld();
         float rq[32];
-        uint32_t pk[16], dk[16], dl[16];
+        uint32_t pk[16], pl[16], dk[16], dl[16];
 #pragma unroll
         for (int c = 0; c < 32; c += 2) {
           float pv[2], dv[2];
@@ -1493,6 +1495,8 @@ __global__ void __launch_bounds__(tb::THREADS, 1) k_tc4_intra_bwd(
             colD += dPp * P;
           }
           pk[c / 2] = pack_bf16(pv[0], pv[1]);
+          const float2 ph2 = __bfloat1622float2(*(const __nv_bfloat162*)&pk[c / 2]);
+          pl[c / 2] = pack_bf16(pv[0] - ph2.x, pv[1] - ph2.y);
           dk[c / 2] = pack_bf16(dv[0], dv[1]);
           const float2 dh = __bfloat1622float2(*(const __nv_bfloat162*)&dk[c / 2]);
           dl[c / 2] = pack_bf16(dv[0] - dh.x, dv[1] - dh.y);
@@ -1509,6 +1513,8 @@ __global__ void __launch_bounds__(tb::THREADS, 1) k_tc4_intra_bwd(
           *(uint4*)(rowp + ((ch ^ (jr & 7)) << 4)) = make_uint4(dk[4 * c8], dk[4 * c8 + 1], dk[4 * c8 + 2], dk[4 * c8 + 3]);
           *(uint4*)(rowp + DS_B + ((ch ^ (jr & 7)) << 4)) =
               make_uint4(dl[4 * c8], dl[4 * c8 + 1], dl[4 * c8 + 2], dl[4 * c8 + 3]);
+          *(uint4*)(rowp + 2 * DS_B + ((ch ^ (jr & 7)) << 4)) =
+              make_uint4(pl[4 * c8], pl[4 * c8 + 1], pl[4 * c8 + 2], pl[4 * c8 + 3]);
         }
         // query-side sums over this warp's 32 key rows: butterfly reduce-scatter,
         // lane l ends with column 32 h + l
